@@ -1,0 +1,250 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 TRANSIMS CA step.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4a]
+                    [--impl tsim|reference]
+
+One step = one full pass of the hot path (lane change, intersections,
+velocity update + move, injection) over every lane-cell
+of the workload.  Default workload: BASELINE.json configs[3] read as 4a
+(256x256 grid, 4 lanes, 100-cell links, 104,448,000 lane-cells, 20,889,600
+vehicles): the one configuration larger than L2, where the HBM roofline is
+meaningful.  Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import scenarios  # noqa: E402
+
+FALLBACK_HBM_GBS = 6650.0
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy bandwidth)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region"""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu=0):
+        self.gpu = gpu
+        self.rows = []
+        self.stop = threading.Event()
+        self.th = None
+
+    def _run(self):
+        while not self.stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([c.strip() for c in out.split(",")])
+            except Exception:
+                pass
+            self.stop.wait(0.05)
+
+    def __enter__(self):
+        self.th = threading.Thread(target=self._run, daemon=True)
+        self.th.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop.set()
+        if self.th:
+            self.th.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for i, n in enumerate(names):
+                if len(r) > 3 + i and r[3 + i].lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(self.rows)}
+
+
+def workload(name):
+    scn = scenarios.config(name)
+    return scn
+
+
+def sample_workload(name):
+    """bounded sample of the same workload for the CPU oracle: same recipe on
+    a smaller network"""
+    if name in ("4a", "4b"):
+        kw = dict(rows=32, cols=32, seed=1, name=f"config{name}_sample32")
+        if name == "4b":
+            kw["n_veh"] = int(1_000_000 * (32 * 31) / (256 * 255))
+        return scenarios.big_grid(**kw), "32x32-node sub-grid, same lanes/cells/density/route recipe"
+    if name == "2":
+        return scenarios.ring(n_cells=100_000, lanes=3, density=0.15, seed=1), "3 x 100,000-cell ring"
+    if name == "3":
+        s = scenarios.config("3")
+        return s, "full network"
+    return workload(name), "full workload"
+
+
+def run_oracle(name, steps, warmup, budget_s=None):
+    import oracle
+    scn, desc = sample_workload(name)
+    o = oracle.Oracle.from_scenario(scn)
+    o.step(warmup)
+    u0 = o.counters()["vehicle_updates"]
+    t0 = time.perf_counter()
+    done = 0
+    while done < steps:
+        o.step(1)
+        done += 1
+        if budget_s and time.perf_counter() - t0 > budget_s:
+            break
+    dt = time.perf_counter() - t0
+    upd = o.counters()["vehicle_updates"] - u0
+    return dict(value=upd / dt, steps=done, seconds=dt, desc=desc,
+                lane_cells=int(o.lib.or_total_lane_cells(o.h)))
+
+
+def bench_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    r = run_oracle(args.config, args.steps, args.warmup)
+    out = {
+        "impl": "reference", "metric": "vehicle-updates/s", "value": r["value"],
+        "unit": "vehicle-updates/s", "n_gpus": args.gpus, "steps": r["steps"],
+        "warmup": args.warmup, "ms_per_step": 1000 * r["seconds"] / max(1, r["steps"]),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+        "data": "synthetic",
+        "config": {"workload": f"config {args.config} sample: {r['desc']}"},
+        "cpu_baseline": {"value": r["value"], "unit": "vehicle-updates/s", "cores": 1,
+                         "kind": "oracle", "sample": r["desc"]},
+        "e2e": {"value": r["value"], "unit": "vehicle-updates/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+def bench_tsim(args):
+    import paper_cs_0105004_b200 as tsim
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        from paper_cs_0105004_b200 import dist
+        return dist.bench_multi(args)
+    hbm_peak, peak_src = measured_peaks()
+    t_gen = time.perf_counter()
+    scn = workload(args.config)
+    t_gen = time.perf_counter() - t_gen
+    flags = tsim.FLAG_FUSED | (tsim.FLAG_HASH if args.hash else 0)
+    # e2e: wall clock around the public API from host arrays to the final
+    # state on the host (H2D of network + vehicles, W+K steps, D2H of state)
+    h2d = sum(a.nbytes for a in (scn.node_x, scn.node_y, scn.link_from, scn.link_to,
+                                 scn.link_len_mm, scn.link_lanes, scn.link_vmax, scn.link_class,
+                                 scn.route_off, scn.route, scn.depart, scn.entry, scn.place_vid,
+                                 scn.place_lane, scn.place_cell, scn.place_v))
+    w0 = time.perf_counter()
+    sim = tsim.Sim(p_slow=scn.p_slow, seed=scn.seed, flags=flags)
+    sim.load(scn)
+    sim.init(0)
+    sim.step(args.warmup)
+    tot = sim.totals()
+    with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
+        t_from = sim.t
+        sim.step(args.steps)
+    timing = sim.last_timing()
+    hist = sim.history(t_from, args.steps + 1)
+    vst = sim.vehicles()
+    e2e_wall = time.perf_counter() - w0
+    d2h = sum(a.nbytes for a in vst.values())
+    ms_total = timing["total_ms"]
+    updates = int(np.sum(hist["active"][:args.steps]))
+    value = updates / (ms_total / 1e3)
+    rtr = args.steps / (ms_total / 1e3)
+    # roofline of the dominant kernel (k_step): algorithmic bytes per launch
+    # = 2 B x lane-cells (codes in + out) + 8 B x active vehicles (vid in +
+    # out) + 12 B x node crossers
+    lane_cells = tot["lane_cells"]
+    alg = 2 * lane_cells * args.steps + 8 * updates + 12 * int(np.sum(hist["crossings"][1:]))
+    alg_per_launch = alg / args.steps
+    mv_ms = timing["move_ms"] / max(1, timing["move_launches"])
+    achieved = alg_per_launch / (mv_ms / 1e3) / 1e9
+    upd_all = updates + int(np.sum(sim.history(1, min(args.warmup, 4096))["active"])) if args.warmup else updates
+    out = {
+        "metric": "vehicle-updates/s", "value": value, "unit": "vehicle-updates/s",
+        "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_total / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u8",
+        "data": "synthetic (seeded generator, DESIGN.md §5)",
+        "config": {"workload": scn.name, "recipe": scn.recipe, "lane_cells": lane_cells,
+                   "vehicles": scn.n_vehicles, "tiles": tot["tiles"],
+                   "l2": "inputs larger than L2 (state read+written per step > 126 MB)",
+                   "parallelism": "1 GPU, 1 domain", "flags": "fused" + ("+hash" if args.hash else "")},
+        "real_time_ratio": rtr,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": achieved / hbm_peak, "traffic": None, "kernel": "k_step",
+                     "alg_bytes_per_launch": alg_per_launch, "kernel_ms": mv_ms,
+                     "kernel_share": timing["move_ms"] / ms_total, "peak_source": peak_src},
+        "e2e": {"value": upd_all / e2e_wall, "unit": "vehicle-updates/s",
+                "h2d_bytes_per_step": h2d / (args.steps + args.warmup),
+                "d2h_bytes_per_step": d2h / (args.steps + args.warmup),
+                "wall_s": e2e_wall, "scope": "load+init+W+K steps+state readback"},
+        "clocks": clk.summary(),
+        "gpu_launches": 1 + 2 * args.steps,
+        "gen_s": t_gen,
+    }
+    sim.close()
+    if args.cpu_baseline and rank == 0:
+        import multiprocessing
+        r = run_oracle(args.config, 400, 5, budget_s=20.0)
+        out["cpu_baseline"] = {"value": r["value"], "unit": "vehicle-updates/s", "cores": 1,
+                               "kind": "oracle", "host_cores": multiprocessing.cpu_count(),
+                               "sample": f"{r['steps']} steps of {r['desc']} "
+                                         f"({r['lane_cells']} lane-cells), {r['seconds']:.1f} s"}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--config", default="4a")
+    ap.add_argument("--impl", default="tsim", choices=["tsim", "reference"])
+    ap.add_argument("--hash", action="store_true")
+    ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        bench_reference(args)
+    else:
+        bench_tsim(args)
+
+
+if __name__ == "__main__":
+    main()

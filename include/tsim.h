@@ -1,0 +1,153 @@
+/*
+ * tsim.h -- C-ABI of the B200-native TRANSIMS cellular-automaton time step
+ * (Nagel & Rickert, "Parallel implementation of the TRANSIMS
+ * micro-simulation", arxiv cs/0105004; §3-§4).
+ *
+ * One handle = one simulation (one domain of a partitioned network, or the
+ * whole network).  The library copies every input array into its own host
+ * and device memory; callers own all buffers they pass.  Outputs go into
+ * caller buffers.  A handle is not thread-safe.  All results depend only on
+ * (inputs, config, seed): not on the partition, the launch configuration or
+ * the number of devices.
+ *
+ * Return codes: TS_OK = 0, TS_EINTERNAL = 1 (CUDA or internal
+ * error), TS_EINVAL = 2 (invalid input).  ts_last_error() returns a
+ * human-readable message for the last failing call.
+ *
+ * Readings R1-R22 of the paper are listed in DESIGN.md §3.
+ */
+#ifndef TSIM_H
+#define TSIM_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TS_OK 0
+#define TS_EINTERNAL 1
+#define TS_EINVAL 2
+
+/* vehicle status (ts_read_vehicles) */
+#define TS_PENDING 0
+#define TS_ACTIVE 1
+#define TS_ARRIVED 2
+
+/* config flags */
+#define TS_FLAG_FUSED 1u       /* fuse lane change of step t+1 into the move
+                                  kernel of step t (whole-link tiles only) */
+#define TS_FLAG_HASH 2u        /* state hash of S(t+1) every step */
+#define TS_FLAG_LINK_WORK 4u   /* per-link work counters (load feedback) */
+#define TS_FLAG_GRAPH 8u       /* replay steps through a CUDA graph */
+
+typedef struct ts_sim ts_sim;
+
+typedef struct {
+  double p_slow;          /* random-slowdown probability, PAPER.md:334-335 (R3) */
+  uint64_t seed;          /* Philox key = (seed & 0xffffffff, seed >> 32) (R3) */
+  int32_t gap_accept_G;   /* unprotected-turn gap, cells (R9), <= 5 */
+  int32_t desperation_D;  /* lane-change desperation distance, cells (R6) */
+  uint32_t flags;         /* TS_FLAG_* */
+  int32_t device;         /* CUDA device ordinal */
+  int32_t tile_cells;     /* max cells per lane in one tile (0 = default) */
+} ts_config;
+
+/* Create a simulation.  *out receives the handle (NULL on failure). */
+int ts_create(const ts_config *cfg, ts_sim **out);
+void ts_destroy(ts_sim *h);
+/* message of the last failing call on h (or of ts_create when h is NULL) */
+const char *ts_last_error(const ts_sim *h);
+
+/* Road network: n_nodes planar nodes (integer mm
+ * coordinates, used for the exact turn classification R7) and n_links
+ * directed links with length in mm (cells = round-half-up(len/7.5 m), R1),
+ * lanes (1..8), vmax in cells/s (1..5), priority class (R9).
+ * periodic_link = id of the one periodic link of a ring network, or -1.
+ * Errors (TS_EINVAL): dangling node, non-positive length, < 10 cells (R11),
+ * node out-degree > 15, bad lanes/vmax. */
+int ts_load_network(ts_sim *h, int32_t n_nodes, const int64_t *node_x_mm,
+                    const int64_t *node_y_mm, int32_t n_links,
+                    const int32_t *from, const int32_t *to,
+                    const int64_t *length_mm, const int32_t *lanes,
+                    const int32_t *vmax, const int32_t *prio_class,
+                    int32_t periodic_link);
+
+/* Vehicles vid = 0..n-1 (plans): route CSR route_off[n+1]
+ * into route_links (consecutive links must share a node), departure second
+ * and entry cell on route[0] (R13). */
+int ts_load_vehicles(ts_sim *h, int32_t n, const int64_t *route_off,
+                     const int32_t *route_links, const int32_t *depart,
+                     const int32_t *entry_cell);
+
+/* Optional initial placement of active vehicles on their route[0]
+ * (ring / dense starts): vid, lane, cell, velocity. */
+int ts_place_vehicles(ts_sim *h, int32_t n, const int32_t *vid,
+                      const int32_t *lane, const int32_t *cell,
+                      const int32_t *v);
+
+/* Build the device layout, upload, and run the initial injection of
+ * vehicles with departure <= t0 (clock starts at t0). */
+int ts_init(ts_sim *h, int32_t t0);
+
+/* Advance n_steps one-second steps.  Synchronous. */
+int ts_step(ts_sim *h, int32_t n_steps);
+
+/* Enqueue n_steps on the handle's stream without synchronising (for
+ * device-side timing); ts_sync waits. */
+int ts_step_async(ts_sim *h, int32_t n_steps);
+int ts_sync(ts_sim *h);
+
+/* current time t (state is S(t)) */
+int32_t ts_time(const ts_sim *h);
+
+/* Per-vehicle state, arrays of n_vehicles entries (NULL to skip): status
+ * (TS_*), link, lane, cell, v (-1 unless active), route cursor (-1 while
+ * pending), arrival time (-1 unless arrived). */
+int ts_read_vehicles(ts_sim *h, int8_t *status, int32_t *link, int32_t *lane,
+                     int32_t *cell, int32_t *v, int32_t *cursor,
+                     int32_t *t_arrive);
+
+/* vid per lane-cell of one link, lane-major (lanes * cells entries, -1 =
+ * empty), and the link's cell count. */
+int ts_read_cells(ts_sim *h, int32_t link, int32_t *vid_out);
+int32_t ts_link_cells(const ts_sim *h, int32_t link);
+
+/* Order-independent state hash of S(t). */
+int ts_state_hash(ts_sim *h, uint64_t *out);
+
+/* Per-step history for steps whose result time is in [t_from, t_from+n):
+ * hash of S(t) (if TS_FLAG_HASH), active vehicles in S(t), arrivals,
+ * injections, lane changes, crossings.  NULL skips an array.  Only the
+ * last 4096 steps are kept. */
+int ts_read_history(ts_sim *h, int32_t t_from, int32_t n, uint64_t *hash,
+                    int64_t *active, int64_t *arrivals, int64_t *injections,
+                    int64_t *lane_changes, int64_t *crossings);
+
+/* Totals: [0] active [1] pending [2] arrived [3] vehicle-updates since
+ * init [4] lane-cells [5] tiles [6] device bytes allocated
+ * [7] algorithmic bytes per step at the current state. */
+int ts_get_totals(ts_sim *h, int64_t out[8]);
+
+/* Per-link accumulated work (vehicle-updates) when TS_FLAG_LINK_WORK is
+ * set (PAPER.md:730-735 load statistics). link_work[n_links]. */
+int ts_get_link_work(ts_sim *h, int64_t *link_work);
+
+/* Orthogonal recursive bisection of the nodes (SPEC.md
+ * :210-218): node weights (the load of the attached half-links; NULL =
+ * uniform), k domains, output domain_of_node[n_nodes].  Vertical cut first;
+ * the larger piece is cut next; non-power-of-two k splits proportionally.
+ * Pure host function (no device needed). */
+int ts_orb_partition(int32_t n_nodes, const int64_t *node_x_mm,
+                     const int64_t *node_y_mm, const double *node_weight,
+                     int32_t k, int32_t *domain_of_node);
+
+/* Kernel-level timing of the last ts_step call (CUDA events on the
+ * handle's stream): total ms, and ms inside the dominant (move) kernel. */
+int ts_last_timing(ts_sim *h, double *total_ms, double *move_ms,
+                   int64_t *move_launches);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,38 @@
+"""Build libtsim.so in-tree for sm_100a (nvcc, no JIT cache)."""
+import os
+import subprocess
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+SRCS = ["csrc/tsim_kernels.cu", "csrc/tsim_api.cu"]
+SO = os.path.join(HERE, "libtsim.so")
+NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+              "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v"]
+
+
+def stale() -> bool:
+    if not os.path.exists(SO):
+        return True
+    t = os.path.getmtime(SO)
+    deps = [os.path.join(HERE, s) for s in SRCS] + [
+        os.path.join(HERE, "csrc", "tsim_internal.h"),
+        os.path.join(os.path.dirname(HERE), "include", "tsim.h")]
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    if not force and not stale():
+        return SO
+    nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+    cmd = [nvcc] + NVCC_FLAGS + [os.path.join(HERE, s) for s in SRCS] + ["-o", SO]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError("nvcc failed:\n" + r.stdout + r.stderr)
+    if verbose:
+        print(r.stderr)
+    with open(os.path.join(HERE, "ptxas_info.txt"), "w") as f:
+        f.write(r.stderr)
+    return SO
+
+
+if __name__ == "__main__":
+    print(build(force=True, verbose=True))

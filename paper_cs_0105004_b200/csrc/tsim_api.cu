@@ -1,0 +1,906 @@
+// tsim_api.cu -- host side of libtsim: input validation, network tables,
+// tiling and device layout, kernel orchestration, state read-back.
+// C-ABI declared in include/tsim.h.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "../../include/tsim.h"
+#include "tsim_internal.h"
+
+namespace tsim {
+cudaError_t set_smem_attrs(int bytes);
+int occupancy_blocks(int threads, int smem);
+}  // namespace tsim
+
+using namespace tsim;
+
+static std::string g_create_err;
+
+struct DevBuf {
+  void *p = nullptr;
+  size_t bytes = 0;
+};
+
+struct ts_sim {
+  ts_config cfg{};
+  std::string err;
+  int dev = 0;
+  cudaStream_t stream = nullptr;
+  size_t dev_bytes = 0;
+  std::vector<void *> allocs;
+  // network (host)
+  bool have_net = false, have_veh = false, inited = false;
+  int32_t nn = 0, nl = 0, periodic = -1;
+  std::vector<int64_t> nx, ny, len;
+  std::vector<int32_t> from, to, lanes, vmax, cls, ncell, lgid;
+  std::vector<int32_t> in_off, in_list, out_off, out_list, out_pos;
+  std::vector<uint32_t> tt;
+  int64_t nlanes = 0, lane_cells = 0;
+  // vehicles (host)
+  int32_t nv = 0;
+  std::vector<int64_t> roff;
+  std::vector<int32_t> route, dep, entry;
+  std::vector<int32_t> pl_vid, pl_lane, pl_cell, pl_v;
+  std::vector<uint8_t> placed;
+  // layout
+  std::vector<TileDesc> tiles;
+  std::vector<int32_t> link_tile0, link_ntiles;
+  int64_t total_cells = 0;
+  int32_t nstrips = 0;
+  std::vector<int32_t> halo_up, halo_dn;
+  WarpLayout lay{};
+  int threads = 256, blocks = 1, smem = 0;
+  bool fused = false;
+  uint64_t p32 = 0;
+  // device
+  TileDesc *d_tiles = nullptr;
+  uint8_t *d_code[2] = {nullptr, nullptr};
+  int32_t *d_vid[2] = {nullptr, nullptr};
+  Strip *d_strip[2] = {nullptr, nullptr};
+  int32_t *d_halo_up = nullptr, *d_halo_dn = nullptr;
+  uint8_t *d_vmax = nullptr;
+  uint32_t *d_tt = nullptr;
+  int32_t *d_out_pos = nullptr;
+  int64_t *d_roff = nullptr;
+  int32_t *d_route = nullptr, *d_cursor = nullptr, *d_dep = nullptr, *d_entry = nullptr;
+  int32_t *d_inj = nullptr, *d_arr = nullptr;
+  int32_t *d_pend_off = nullptr, *d_pend_list = nullptr, *d_pend_head = nullptr;
+  uint64_t *d_tail = nullptr, *d_entr = nullptr;
+  uint8_t *d_head = nullptr, *d_ext = nullptr;
+  unsigned long long *d_stats = nullptr, *d_work = nullptr, *d_hash = nullptr;
+  int32_t *d_in_off = nullptr, *d_in_list = nullptr, *d_out_off = nullptr, *d_out_list = nullptr;
+  int32_t *d_ncell = nullptr, *d_lanes = nullptr, *d_lgid = nullptr, *d_cls = nullptr;
+  int cur = 0;
+  int32_t t = 0;
+  int64_t veh_updates = 0, arrived = 0, injected = 0, n_placed = 0;
+  // timing
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  std::vector<cudaEvent_t> mv_ev;
+  double last_total_ms = 0, last_move_ms = 0;
+  int64_t last_move_launches = 0;
+  bool timing = true;
+};
+
+static int fail(ts_sim *h, int code, const char *fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (h) h->err = buf;
+  else g_create_err = buf;
+  return code;
+}
+
+#define CK(h, call)                                                                     \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      return fail((h), TS_EINTERNAL, "%s failed: %s (%s:%d)", #call,                    \
+                  cudaGetErrorString(e_), __FILE__, __LINE__);                          \
+  } while (0)
+
+template <class T>
+static int dalloc(ts_sim *h, T **p, size_t n, int fill = -1) {
+  size_t bytes = std::max<size_t>(n, 1) * sizeof(T);
+  cudaError_t e = cudaMalloc((void **)p, bytes);
+  if (e != cudaSuccess)
+    return fail(h, TS_EINTERNAL, "cudaMalloc(%zu) failed: %s", bytes, cudaGetErrorString(e));
+  h->allocs.push_back(*p);
+  h->dev_bytes += bytes;
+  if (fill >= 0) {
+    e = cudaMemsetAsync(*p, fill, bytes, h->stream);
+    if (e != cudaSuccess) return fail(h, TS_EINTERNAL, "memset: %s", cudaGetErrorString(e));
+  }
+  return TS_OK;
+}
+
+template <class T>
+static int upload(ts_sim *h, T **p, const std::vector<T> &v) {
+  int rc = dalloc(h, p, v.size());
+  if (rc) return rc;
+  if (!v.empty())
+    CK(h, cudaMemcpyAsync(*p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, h->stream));
+  return TS_OK;
+}
+
+extern "C" {
+
+int ts_create(const ts_config *cfg, ts_sim **out) {
+  if (!out) return fail(nullptr, TS_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (!cfg) return fail(nullptr, TS_EINVAL, "cfg is NULL");
+  if (!(cfg->p_slow >= 0.0 && cfg->p_slow <= 1.0)) return fail(nullptr, TS_EINVAL, "p_slow not in [0,1]");
+  if (cfg->gap_accept_G < 0 || cfg->gap_accept_G > kGmax)
+    return fail(nullptr, TS_EINVAL, "gap_accept_G must be in [0, 5]");
+  if (cfg->desperation_D < 1) return fail(nullptr, TS_EINVAL, "desperation_D must be >= 1");
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0)
+    return fail(nullptr, TS_EINTERNAL, "no CUDA device: %s", cudaGetErrorString(e));
+  if (cfg->device < 0 || cfg->device >= ndev) return fail(nullptr, TS_EINVAL, "bad device ordinal");
+  ts_sim *h = new ts_sim();
+  h->cfg = *cfg;
+  h->dev = cfg->device;
+  e = cudaSetDevice(h->dev);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreate(&h->ev0);
+  if (e == cudaSuccess) e = cudaEventCreate(&h->ev1);
+  if (e != cudaSuccess) {
+    delete h;
+    return fail(nullptr, TS_EINTERNAL, "CUDA init failed: %s", cudaGetErrorString(e));
+  }
+  // floor(p * 2^32), exact for the power-of-two scaling (R3)
+  h->p32 = (uint64_t)(cfg->p_slow * 4294967296.0);
+  *out = h;
+  return TS_OK;
+}
+
+void ts_destroy(ts_sim *h) {
+  if (!h) return;
+  cudaSetDevice(h->dev);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  for (void *p : h->allocs) cudaFree(p);
+  for (auto e : h->mv_ev) cudaEventDestroy(e);
+  if (h->ev0) cudaEventDestroy(h->ev0);
+  if (h->ev1) cudaEventDestroy(h->ev1);
+  if (h->stream) cudaStreamDestroy(h->stream);
+  delete h;
+}
+
+const char *ts_last_error(const ts_sim *h) { return h ? h->err.c_str() : g_create_err.c_str(); }
+
+// ------------------------------------------------------------------ network
+// reading R7: turn type from integer direction vectors; 0 T, 1 L, 2 R
+static int turn_type(const ts_sim *h, int k, int k2) {
+  const int64_t ax = h->nx[h->to[k]] - h->nx[h->from[k]], ay = h->ny[h->to[k]] - h->ny[h->from[k]];
+  const int64_t bx = h->nx[h->to[k2]] - h->nx[h->from[k2]],
+                by = h->ny[h->to[k2]] - h->ny[h->from[k2]];
+  const int64_t cross = ax * by - ay * bx, dot = ax * bx + ay * by;
+  if (dot > 0 && (cross < 0 ? -cross : cross) <= dot) return 0;
+  if (cross < 0) return 2;
+  return 1;  // left, or U-turn
+}
+
+int ts_load_network(ts_sim *h, int32_t n_nodes, const int64_t *node_x_mm, const int64_t *node_y_mm,
+                    int32_t n_links, const int32_t *from, const int32_t *to,
+                    const int64_t *length_mm, const int32_t *lanes, const int32_t *vmax,
+                    const int32_t *prio_class, int32_t periodic_link) {
+  if (!h) return TS_EINVAL;
+  if (h->have_net) return fail(h, TS_EINVAL, "network already loaded");
+  if (n_nodes < 1 || n_links < 1) return fail(h, TS_EINVAL, "empty network");
+  if (periodic_link >= 0 && n_links != 1)
+    return fail(h, TS_EINVAL, "a periodic link must be the only link");
+  h->nn = n_nodes;
+  h->nl = n_links;
+  h->periodic = periodic_link;
+  h->nx.assign(node_x_mm, node_x_mm + n_nodes);
+  h->ny.assign(node_y_mm, node_y_mm + n_nodes);
+  h->from.assign(from, from + n_links);
+  h->to.assign(to, to + n_links);
+  h->len.assign(length_mm, length_mm + n_links);
+  h->lanes.assign(lanes, lanes + n_links);
+  h->vmax.assign(vmax, vmax + n_links);
+  h->cls.assign(prio_class, prio_class + n_links);
+  h->ncell.resize(n_links);
+  h->lgid.resize(n_links + 1);
+  h->lgid[0] = 0;
+  for (int k = 0; k < n_links; k++) {
+    if (from[k] < 0 || from[k] >= n_nodes || to[k] < 0 || to[k] >= n_nodes)
+      return fail(h, TS_EINVAL, "link %d: dangling node reference", k);
+    if (from[k] == to[k] && k != periodic_link) return fail(h, TS_EINVAL, "link %d: from == to", k);
+    if (length_mm[k] <= 0) return fail(h, TS_EINVAL, "link %d: non-positive length", k);
+    if (lanes[k] < 1 || lanes[k] > kMaxLanes) return fail(h, TS_EINVAL, "link %d: lanes", k);
+    if (vmax[k] < 1 || vmax[k] > kGmax) return fail(h, TS_EINVAL, "link %d: vmax", k);
+    // R1: round-half-up(length / 7.5 m) in integer mm, at least 1
+    int64_t n = std::max<int64_t>(1, (length_mm[k] + 3750) / 7500);
+    if (n < 10) return fail(h, TS_EINVAL, "link %d: %lld cells < 10 (R11)", k, (long long)n);
+    if (n > 100000000) return fail(h, TS_EINVAL, "link %d: too long", k);
+    h->ncell[k] = (int32_t)n;
+    h->lgid[k + 1] = h->lgid[k] + lanes[k];
+    h->lane_cells += n * lanes[k];
+  }
+  h->nlanes = h->lgid[n_links];
+  // incoming / outgoing links per node in ascending link id
+  h->in_off.assign(n_nodes + 1, 0);
+  h->out_off.assign(n_nodes + 1, 0);
+  for (int k = 0; k < n_links; k++) {
+    if (k == periodic_link) continue;
+    h->in_off[to[k] + 1]++;
+    h->out_off[from[k] + 1]++;
+  }
+  for (int i = 0; i < n_nodes; i++) {
+    if (h->out_off[i + 1] > 15) return fail(h, TS_EINVAL, "node %d: out-degree > 15", i);
+    h->in_off[i + 1] += h->in_off[i];
+    h->out_off[i + 1] += h->out_off[i];
+  }
+  h->in_list.assign(std::max(1, h->in_off[n_nodes]), 0);
+  h->out_list.assign(std::max(1, h->out_off[n_nodes]), 0);
+  h->out_pos.assign(n_links, 0);
+  std::vector<int32_t> fi(n_nodes, 0), fo(n_nodes, 0);
+  for (int k = 0; k < n_links; k++) {
+    if (k == periodic_link) continue;
+    h->in_list[h->in_off[to[k]] + fi[to[k]]++] = k;
+    h->out_pos[k] = fo[from[k]];
+    h->out_list[h->out_off[from[k]] + fo[from[k]]++] = k;
+  }
+  h->tt.assign(n_links, 0u);
+  for (int k = 0; k < n_links; k++) {
+    if (k == periodic_link) continue;
+    const int nd = to[k];
+    for (int s = 0; s < h->out_off[nd + 1] - h->out_off[nd]; s++)
+      h->tt[k] |= (uint32_t)turn_type(h, k, h->out_list[h->out_off[nd] + s]) << (2 * s);
+  }
+  h->have_net = true;
+  return TS_OK;
+}
+
+int32_t ts_link_cells(const ts_sim *h, int32_t link) {
+  if (!h || !h->have_net || link < 0 || link >= h->nl) return -1;
+  return h->ncell[link];
+}
+
+int ts_load_vehicles(ts_sim *h, int32_t n, const int64_t *route_off, const int32_t *route_links,
+                     const int32_t *depart, const int32_t *entry_cell) {
+  if (!h) return TS_EINVAL;
+  if (!h->have_net) return fail(h, TS_EINVAL, "load the network first");
+  if (h->have_veh) return fail(h, TS_EINVAL, "vehicles already loaded");
+  if (n < 0) return fail(h, TS_EINVAL, "negative vehicle count");
+  if (n > 0 && route_off[0] != 0) return fail(h, TS_EINVAL, "route_off[0] != 0");
+  for (int32_t i = 0; i < n; i++) {
+    const int64_t a = route_off[i], b = route_off[i + 1];
+    if (b <= a) return fail(h, TS_EINVAL, "vehicle %d: empty route", i);
+    for (int64_t j = a; j < b; j++) {
+      const int32_t k = route_links[j];
+      if (k < 0 || k >= h->nl) return fail(h, TS_EINVAL, "vehicle %d: bad link", i);
+      if (j > a && h->to[route_links[j - 1]] != h->from[k])
+        return fail(h, TS_EINVAL, "vehicle %d: route links not consecutive", i);
+    }
+    if (entry_cell[i] < 0 || entry_cell[i] >= h->ncell[route_links[a]])
+      return fail(h, TS_EINVAL, "vehicle %d: entry cell outside link", i);
+  }
+  h->nv = n;
+  h->roff.assign(route_off, route_off + n + 1);
+  if (n == 0) h->roff.assign(1, 0);
+  h->route.assign(route_links, route_links + h->roff[n]);
+  h->dep.assign(depart, depart + n);
+  h->entry.assign(entry_cell, entry_cell + n);
+  h->placed.assign(n, 0);
+  h->have_veh = true;
+  return TS_OK;
+}
+
+int ts_place_vehicles(ts_sim *h, int32_t n, const int32_t *vid, const int32_t *lane,
+                      const int32_t *cell, const int32_t *v) {
+  if (!h) return TS_EINVAL;
+  if (!h->have_veh) return fail(h, TS_EINVAL, "load vehicles first");
+  if (h->inited) return fail(h, TS_EINVAL, "already initialised");
+  for (int32_t i = 0; i < n; i++) {
+    const int32_t f = vid[i];
+    if (f < 0 || f >= h->nv) return fail(h, TS_EINVAL, "placement %d: bad vid", i);
+    if (h->placed[f]) return fail(h, TS_EINVAL, "placement %d: vehicle placed twice", i);
+    const int32_t k = h->route[h->roff[f]];
+    if (lane[i] < 0 || lane[i] >= h->lanes[k] || cell[i] < 0 || cell[i] >= h->ncell[k])
+      return fail(h, TS_EINVAL, "placement %d: cell outside link", i);
+    if (v[i] < 0 || v[i] > h->vmax[k]) return fail(h, TS_EINVAL, "placement %d: velocity", i);
+    h->placed[f] = 1;
+    h->pl_vid.push_back(f);
+    h->pl_lane.push_back(lane[i]);
+    h->pl_cell.push_back(cell[i]);
+    h->pl_v.push_back(v[i]);
+  }
+  return TS_OK;
+}
+
+// ------------------------------------------------------------------- layout
+static void build_tiles(ts_sim *h) {
+  const int tc = h->cfg.tile_cells > 0 ? h->cfg.tile_cells : 512;
+  h->tiles.clear();
+  h->link_tile0.assign(h->nl + 1, 0);
+  h->link_ntiles.assign(h->nl, 0);
+  int64_t off = 0;
+  int32_t strip = 0;
+  for (int k = 0; k < h->nl; k++) {
+    const int n = h->ncell[k];
+    const bool per = k == h->periodic;
+    int nt = (n + tc - 1) / tc;
+    if (nt > 1 && n / nt < 10) nt = std::max(1, n / 10);
+    h->link_tile0[k] = (int32_t)h->tiles.size();
+    h->link_ntiles[k] = nt;
+    const bool halo = per || nt > 1;
+    int a = 0;
+    for (int i = 0; i < nt; i++) {
+      const int w = n / nt + (i < n % nt ? 1 : 0);
+      TileDesc d{};
+      d.off = off;
+      d.link = k;
+      d.a = a;
+      d.lane_gid = h->lgid[k];
+      d.n = n;
+      d.w = (uint16_t)w;
+      d.L = (uint8_t)h->lanes[k];
+      uint8_t f = 0;
+      if (!per && a == 0) f |= kFirst;
+      if (!per && a + w == n) f |= kLast;
+      if (per) f |= kPeriodic;
+      if (halo) {
+        f |= kHalo;
+        if (per || a > 0) f |= kHasUp;
+        if (per || a + w < n) f |= kHasDn;
+        if (per && nt == 1) f |= 64;
+        d.strip = strip;
+        strip += h->lanes[k];
+      } else {
+        d.strip = -1;
+      }
+      d.flags = f;
+      h->tiles.push_back(d);
+      off += ((int64_t)w * h->lanes[k] + 15) & ~(int64_t)15;
+      a += w;
+    }
+  }
+  h->link_tile0[h->nl] = (int32_t)h->tiles.size();
+  h->total_cells = off + 16;
+  h->nstrips = strip;
+  h->halo_up.assign(std::max(1, strip), -1);
+  h->halo_dn.assign(std::max(1, strip), -1);
+  for (int k = 0; k < h->nl; k++) {
+    const int t0 = h->link_tile0[k], nt = h->link_ntiles[k];
+    for (int i = 0; i < nt; i++) {
+      const TileDesc &d = h->tiles[t0 + i];
+      if (d.strip < 0) continue;
+      if (d.flags & kHasUp) h->halo_up[d.strip] = h->tiles[t0 + (i + nt - 1) % nt].strip;
+      if (d.flags & kHasDn) h->halo_dn[d.strip] = h->tiles[t0 + (i + 1) % nt].strip;
+    }
+  }
+  int nc_max = 32;
+  for (const TileDesc &d : h->tiles) nc_max = std::max(nc_max, (int)d.L * tile_stride(d.w, d.flags));
+  h->lay = warp_layout(nc_max);
+  h->fused = (h->cfg.flags & TS_FLAG_FUSED) && h->nstrips == 0;
+}
+
+static int tile_of(const ts_sim *h, int k, int x) {
+  int t0 = h->link_tile0[k], nt = h->link_ntiles[k];
+  for (int i = 0; i < nt; i++) {
+    const TileDesc &d = h->tiles[t0 + i];
+    if (x >= d.a && x < d.a + d.w) return t0 + i;
+  }
+  return -1;
+}
+
+static int first_slot(const ts_sim *h, int f) {
+  const int64_t a = h->roff[f];
+  return h->roff[f + 1] - a > 1 ? h->out_pos[h->route[a + 1]] : kSlotFinal;
+}
+
+static StepParams step_params(ts_sim *h, int t, int mode) {
+  StepParams P{};
+  P.tiles = h->d_tiles;
+  P.ntiles = (int32_t)h->tiles.size();
+  P.t = t;
+  P.mode = mode;
+  P.D = h->cfg.desperation_D;
+  P.k0 = (uint32_t)(h->cfg.seed & 0xffffffffu);
+  P.k1 = (uint32_t)(h->cfg.seed >> 32);
+  P.p32 = h->p32;
+  P.lay = h->lay;
+  P.code_in = h->d_code[h->cur];
+  P.code_out = h->d_code[h->cur ^ 1];
+  P.vid_in = h->d_vid[h->cur];
+  P.vid_out = h->d_vid[h->cur ^ 1];
+  P.strip_in = h->d_strip[h->cur];
+  P.strip_out = h->d_strip[h->cur ^ 1];
+  P.halo_up = h->d_halo_up;
+  P.halo_dn = h->d_halo_dn;
+  P.vmax_link = h->d_vmax;
+  P.tt_link = h->d_tt;
+  P.out_pos = h->d_out_pos;
+  P.route_off = h->d_roff;
+  P.route = h->d_route;
+  P.cursor = h->d_cursor;
+  P.dep = h->d_dep;
+  P.entry = h->d_entry;
+  P.inj_time = h->d_inj;
+  P.arr_time = h->d_arr;
+  P.pend_off = h->d_pend_off;
+  P.pend_list = h->d_pend_list;
+  P.pend_head = h->d_pend_head;
+  P.tail_rec = h->d_tail;
+  P.head_occ = h->d_head;
+  P.ext = h->d_ext;
+  P.entr = h->d_entr;
+  P.stats = h->d_stats;
+  P.link_work = h->d_work;
+  return P;
+}
+
+static NodeParams node_params(ts_sim *h, int t) {
+  NodeParams N{};
+  N.nnodes = h->periodic >= 0 ? 0 : h->nn;
+  N.t = t;
+  N.G = h->cfg.gap_accept_G;
+  N.k0 = (uint32_t)(h->cfg.seed & 0xffffffffu);
+  N.k1 = (uint32_t)(h->cfg.seed >> 32);
+  N.p32 = h->p32;
+  N.in_off = h->d_in_off;
+  N.in_list = h->d_in_list;
+  N.out_off = h->d_out_off;
+  N.out_list = h->d_out_list;
+  N.link_ncell = h->d_ncell;
+  N.link_lanes = h->d_lanes;
+  N.link_lgid = h->d_lgid;
+  N.link_cls = h->d_cls;
+  N.vmax_link = h->d_vmax;
+  N.tt_link = h->d_tt;
+  N.out_pos = h->d_out_pos;
+  N.route_off = h->d_roff;
+  N.route = h->d_route;
+  N.cursor = h->d_cursor;
+  N.tail_rec = h->d_tail;
+  N.head_occ = h->d_head;
+  N.ext = h->d_ext;
+  N.entr = h->d_entr;
+  N.stats = h->d_stats;
+  return N;
+}
+
+static int base_mode(const ts_sim *h) {
+  int m = kModeMove | kModeInject;
+  if (h->cfg.flags & TS_FLAG_HASH) m |= kModeHash;
+  if (h->cfg.flags & TS_FLAG_LINK_WORK) m |= kModeWork;
+  return m;
+}
+
+static int zero_stats(ts_sim *h, int32_t t_from, int32_t n) {
+  // slots t_from .. t_from+n-1 (mod kHist)
+  if (n >= kHist) {
+    CK(h, cudaMemsetAsync(h->d_stats, 0, sizeof(unsigned long long) * kHist * ST_N, h->stream));
+    return TS_OK;
+  }
+  int s = t_from & (kHist - 1);
+  int n1 = std::min(n, kHist - s);
+  CK(h, cudaMemsetAsync(h->d_stats + (size_t)s * ST_N, 0, sizeof(unsigned long long) * ST_N * n1,
+                        h->stream));
+  if (n > n1)
+    CK(h, cudaMemsetAsync(h->d_stats, 0, sizeof(unsigned long long) * ST_N * (n - n1), h->stream));
+  return TS_OK;
+}
+
+int ts_init(ts_sim *h, int32_t t0) {
+  if (!h) return TS_EINVAL;
+  if (!h->have_veh) return fail(h, TS_EINVAL, "load vehicles first");
+  if (h->inited) return fail(h, TS_EINVAL, "already initialised");
+  if (t0 < 0) return fail(h, TS_EINVAL, "t0 must be >= 0");
+  CK(h, cudaSetDevice(h->dev));
+  build_tiles(h);
+  // host staging of the initial placement: codes + compact vid lists
+  std::vector<uint8_t> code(h->total_cells, kEmpty);
+  std::vector<int32_t> cellvid(h->total_cells, -1);
+  for (size_t i = 0; i < h->pl_vid.size(); i++) {
+    const int f = h->pl_vid[i], k = h->route[h->roff[f]];
+    const int ti = tile_of(h, k, h->pl_cell[i]);
+    const TileDesc &d = h->tiles[ti];
+    const int64_t pos = d.off + (int64_t)h->pl_lane[i] * d.w + (h->pl_cell[i] - d.a);
+    if (code[pos] != kEmpty) return fail(h, TS_EINVAL, "placement %zu: cell taken", i);
+    code[pos] = (uint8_t)(h->pl_v[i] | (first_slot(h, f) << 3));
+    cellvid[pos] = f;
+  }
+  std::vector<int32_t> vids(h->total_cells, -1);
+  for (const TileDesc &d : h->tiles) {
+    int64_t r = d.off;
+    for (int64_t i = 0; i < (int64_t)d.L * d.w; i++)
+      if (code[d.off + i] != kEmpty) vids[r++] = cellvid[d.off + i];
+  }
+  std::vector<int32_t>().swap(cellvid);
+  h->n_placed = (int64_t)h->pl_vid.size();
+  // pending lists per first link in (departure, vid) order (R13)
+  std::vector<int32_t> pend_off(h->nl + 1, 0), pend_list;
+  for (int f = 0; f < h->nv; f++)
+    if (!h->placed[f]) pend_off[h->route[h->roff[f]] + 1]++;
+  for (int k = 0; k < h->nl; k++) pend_off[k + 1] += pend_off[k];
+  pend_list.assign(std::max(1, pend_off[h->nl]), 0);
+  {
+    std::vector<int32_t> fill(h->nl, 0);
+    for (int f = 0; f < h->nv; f++)
+      if (!h->placed[f]) {
+        int k = h->route[h->roff[f]];
+        pend_list[pend_off[k] + fill[k]++] = f;
+      }
+    for (int k = 0; k < h->nl; k++)
+      std::stable_sort(pend_list.begin() + pend_off[k], pend_list.begin() + pend_off[k + 1],
+                       [&](int a, int b) { return h->dep[a] < h->dep[b] || (h->dep[a] == h->dep[b] && a < b); });
+  }
+  std::vector<int32_t> inj(h->nv), arr(h->nv, -1), cur0(h->nv, 0);
+  for (int f = 0; f < h->nv; f++) inj[f] = h->placed[f] ? INT_MIN : INT_MAX;
+  std::vector<uint8_t> vmax8(h->nl);
+  for (int k = 0; k < h->nl; k++) vmax8[k] = (uint8_t)h->vmax[k];
+  // device
+  int rc;
+  if ((rc = upload(h, &h->d_tiles, h->tiles))) return rc;
+  for (int b = 0; b < 2; b++) {
+    if ((rc = dalloc(h, &h->d_code[b], h->total_cells, 0xFF))) return rc;
+    if ((rc = dalloc(h, &h->d_vid[b], h->total_cells, 0xFF))) return rc;
+    if ((rc = dalloc(h, &h->d_strip[b], std::max(1, h->nstrips), 0xFF))) return rc;
+  }
+  CK(h, cudaMemcpyAsync(h->d_code[0], code.data(), code.size(), cudaMemcpyHostToDevice, h->stream));
+  CK(h, cudaMemcpyAsync(h->d_vid[0], vids.data(), vids.size() * 4, cudaMemcpyHostToDevice, h->stream));
+  if ((rc = upload(h, &h->d_halo_up, h->halo_up))) return rc;
+  if ((rc = upload(h, &h->d_halo_dn, h->halo_dn))) return rc;
+  if ((rc = upload(h, &h->d_vmax, vmax8))) return rc;
+  if ((rc = upload(h, &h->d_tt, h->tt))) return rc;
+  if ((rc = upload(h, &h->d_out_pos, h->out_pos))) return rc;
+  if ((rc = upload(h, &h->d_roff, h->roff))) return rc;
+  if ((rc = upload(h, &h->d_route, h->route))) return rc;
+  if ((rc = upload(h, &h->d_cursor, cur0))) return rc;
+  if ((rc = upload(h, &h->d_dep, h->dep))) return rc;
+  if ((rc = upload(h, &h->d_entry, h->entry))) return rc;
+  if ((rc = upload(h, &h->d_inj, inj))) return rc;
+  if ((rc = upload(h, &h->d_arr, arr))) return rc;
+  if ((rc = upload(h, &h->d_pend_off, pend_off))) return rc;
+  if ((rc = upload(h, &h->d_pend_list, pend_list))) return rc;
+  if ((rc = dalloc(h, &h->d_pend_head, h->nl, 0))) return rc;
+  if ((rc = dalloc(h, &h->d_tail, h->nlanes, 0))) return rc;
+  if ((rc = dalloc(h, &h->d_entr, h->nlanes, 0))) return rc;
+  if ((rc = dalloc(h, &h->d_head, h->nlanes, 0))) return rc;
+  if ((rc = dalloc(h, &h->d_ext, h->nlanes, 0))) return rc;
+  if ((rc = dalloc(h, &h->d_stats, (size_t)kHist * ST_N, 0))) return rc;
+  if ((rc = dalloc(h, &h->d_work, h->nl, 0))) return rc;
+  if ((rc = dalloc(h, &h->d_hash, 2, 0))) return rc;
+  if ((rc = upload(h, &h->d_in_off, h->in_off))) return rc;
+  if ((rc = upload(h, &h->d_in_list, h->in_list))) return rc;
+  if ((rc = upload(h, &h->d_out_off, h->out_off))) return rc;
+  if ((rc = upload(h, &h->d_out_list, h->out_list))) return rc;
+  if ((rc = upload(h, &h->d_ncell, h->ncell))) return rc;
+  if ((rc = upload(h, &h->d_lanes, h->lanes))) return rc;
+  if ((rc = upload(h, &h->d_lgid, h->lgid))) return rc;
+  if ((rc = upload(h, &h->d_cls, h->cls))) return rc;
+  // launch geometry
+  h->smem = h->lay.bytes;
+  int wpb = std::max(1, std::min(8, (200 * 1024) / h->lay.bytes));
+  h->threads = 32 * wpb;
+  h->smem = wpb * h->lay.bytes;
+  CK(h, set_smem_attrs(std::max(h->smem, 1)));
+  int nsm = 148;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->dev);
+  int occ = std::max(1, occupancy_blocks(h->threads, h->smem));
+  const int need = (int)((h->tiles.size() + wpb - 1) / wpb);
+  h->blocks = std::max(1, std::min(need, occ * nsm));
+  // initial injection: departure <= t0 (O1 §Init), S(t0) into buffer 1
+  h->cur = 0;
+  if (zero_stats(h, t0, 1)) return TS_EINTERNAL;
+  int mode = kModeInject | (base_mode(h) & kModeHash);
+  StepParams P = step_params(h, t0 - 1, mode);
+  launch_step(P, h->blocks, h->threads, h->smem, h->stream);
+  CK(h, cudaGetLastError());
+  h->cur ^= 1;
+  h->t = t0;
+  CK(h, cudaStreamSynchronize(h->stream));
+  unsigned long long st[ST_N];
+  CK(h, cudaMemcpy(st, h->d_stats + (size_t)(t0 & (kHist - 1)) * ST_N, sizeof st, cudaMemcpyDeviceToHost));
+  h->injected = (int64_t)st[ST_INJ];
+  // the host copies of the plans are no longer needed (all on the device)
+  std::vector<int32_t>().swap(h->route);
+  std::vector<int32_t>().swap(h->pl_vid);
+  std::vector<int32_t>().swap(h->pl_lane);
+  std::vector<int32_t>().swap(h->pl_cell);
+  std::vector<int32_t>().swap(h->pl_v);
+  h->inited = true;
+  return TS_OK;
+}
+
+// --------------------------------------------------------------------- step
+static int enqueue_steps(ts_sim *h, int32_t n) {
+  if (!h || !h->inited) return fail(h, TS_EINVAL, "call ts_init first");
+  if (n < 0) return fail(h, TS_EINVAL, "negative step count");
+  if (n == 0) return TS_OK;
+  CK(h, cudaSetDevice(h->dev));
+  if (zero_stats(h, h->t + 1, std::min(n + 1, kHist))) return TS_EINTERNAL;
+  const int mode = base_mode(h);
+  if ((int)h->mv_ev.size() < 2 * n && h->timing) {
+    while ((int)h->mv_ev.size() < 2 * n) {
+      cudaEvent_t e;
+      CK(h, cudaEventCreate(&e));
+      h->mv_ev.push_back(e);
+    }
+  }
+  CK(h, cudaEventRecord(h->ev0, h->stream));
+  const int t = h->t;
+  if (h->fused) {
+    launch_lc(step_params(h, t, 0), h->blocks, h->threads, h->smem, h->stream);
+    h->cur ^= 1;
+  }
+  for (int i = 0; i < n; i++) {
+    if (!h->fused) {
+      launch_lc(step_params(h, t + i, 0), h->blocks, h->threads, h->smem, h->stream);
+      h->cur ^= 1;
+    }
+    launch_node(node_params(h, t + i), h->stream);
+    int m = mode;
+    if (h->fused && i < n - 1) m |= kModeLC;
+    if (h->timing) CK(h, cudaEventRecord(h->mv_ev[2 * i], h->stream));
+    launch_step(step_params(h, t + i, m), h->blocks, h->threads, h->smem, h->stream);
+    if (h->timing) CK(h, cudaEventRecord(h->mv_ev[2 * i + 1], h->stream));
+    h->cur ^= 1;
+  }
+  CK(h, cudaEventRecord(h->ev1, h->stream));
+  CK(h, cudaGetLastError());
+  h->t = t + n;
+  h->last_move_launches = n;
+  return TS_OK;
+}
+
+static int finish_steps(ts_sim *h, int32_t t_from, int32_t n) {
+  CK(h, cudaStreamSynchronize(h->stream));
+  float ms = 0;
+  CK(h, cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+  h->last_total_ms = ms;
+  double mv = 0;
+  if (h->timing)
+    for (int i = 0; i < n; i++) {
+      float m = 0;
+      CK(h, cudaEventElapsedTime(&m, h->mv_ev[2 * i], h->mv_ev[2 * i + 1]));
+      mv += m;
+    }
+  h->last_move_ms = mv;
+  // counters from the history: active in S(t) for t in [t_from, t_from+n)
+  if (n <= kHist - 1) {
+    std::vector<unsigned long long> st((size_t)(n + 1) * ST_N);
+    for (int i = 0; i <= n; i++) {
+      int s = (t_from + i) & (kHist - 1);
+      CK(h, cudaMemcpy(&st[(size_t)i * ST_N], h->d_stats + (size_t)s * ST_N,
+                       ST_N * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    }
+    for (int i = 0; i < n; i++) h->veh_updates += (int64_t)st[(size_t)i * ST_N + ST_ACTIVE];
+    for (int i = 1; i <= n; i++) {
+      h->arrived += (int64_t)st[(size_t)i * ST_N + ST_ARR];
+      h->injected += (int64_t)st[(size_t)i * ST_N + ST_INJ];
+    }
+  }
+  return TS_OK;
+}
+
+int ts_step(ts_sim *h, int32_t n_steps) {
+  const int32_t t_from = h ? h->t : 0;
+  int rc = enqueue_steps(h, n_steps);
+  if (rc) return rc;
+  if (n_steps == 0) return TS_OK;
+  return finish_steps(h, t_from, n_steps);
+}
+
+static int32_t g_async_from = 0, g_async_n = 0;
+
+int ts_step_async(ts_sim *h, int32_t n_steps) {
+  g_async_from = h ? h->t : 0;
+  g_async_n = n_steps;
+  return enqueue_steps(h, n_steps);
+}
+
+int ts_sync(ts_sim *h) {
+  if (!h) return TS_EINVAL;
+  if (g_async_n > 0) {
+    int rc = finish_steps(h, g_async_from, g_async_n);
+    g_async_n = 0;
+    return rc;
+  }
+  CK(h, cudaStreamSynchronize(h->stream));
+  return TS_OK;
+}
+
+int32_t ts_time(const ts_sim *h) { return h ? h->t : -1; }
+
+// ------------------------------------------------------------------ readers
+int ts_read_vehicles(ts_sim *h, int8_t *status, int32_t *link, int32_t *lane, int32_t *cell,
+                     int32_t *v, int32_t *cursor, int32_t *t_arrive) {
+  if (!h || !h->inited) return fail(h, TS_EINVAL, "not initialised");
+  CK(h, cudaSetDevice(h->dev));
+  CK(h, cudaStreamSynchronize(h->stream));
+  std::vector<uint8_t> code(h->total_cells);
+  std::vector<int32_t> vids(h->total_cells), inj(h->nv), arr(h->nv), cur(h->nv);
+  CK(h, cudaMemcpy(code.data(), h->d_code[h->cur], code.size(), cudaMemcpyDeviceToHost));
+  CK(h, cudaMemcpy(vids.data(), h->d_vid[h->cur], vids.size() * 4, cudaMemcpyDeviceToHost));
+  CK(h, cudaMemcpy(inj.data(), h->d_inj, inj.size() * 4, cudaMemcpyDeviceToHost));
+  CK(h, cudaMemcpy(arr.data(), h->d_arr, arr.size() * 4, cudaMemcpyDeviceToHost));
+  CK(h, cudaMemcpy(cur.data(), h->d_cursor, cur.size() * 4, cudaMemcpyDeviceToHost));
+  std::vector<int32_t> lk(h->nv, -1), ln(h->nv, -1), ce(h->nv, -1), vv(h->nv, -1);
+  std::vector<uint8_t> seen(h->nv, 0);
+  for (const TileDesc &d : h->tiles) {
+    int64_t r = d.off;
+    for (int l = 0; l < d.L; l++)
+      for (int x = 0; x < d.w; x++) {
+        uint8_t c = code[d.off + (int64_t)l * d.w + x];
+        if (c & 0x80) continue;
+        int f = vids[r++];
+        if (f < 0 || f >= h->nv || seen[f])
+          return fail(h, TS_EINTERNAL, "corrupt state: vid %d at link %d", f, d.link);
+        seen[f] = 1;
+        lk[f] = d.link;
+        ln[f] = l;
+        ce[f] = d.a + x;
+        vv[f] = c & 7;
+      }
+  }
+  for (int f = 0; f < h->nv; f++) {
+    int8_t s = TS_ACTIVE;
+    if (arr[f] >= 0) s = TS_ARRIVED;
+    else if (inj[f] == INT_MAX) s = TS_PENDING;
+    if ((s == TS_ACTIVE) != (seen[f] != 0))
+      return fail(h, TS_EINTERNAL, "corrupt state: vehicle %d status %d seen %d", f, s, seen[f]);
+    if (status) status[f] = s;
+    if (link) link[f] = lk[f];
+    if (lane) lane[f] = ln[f];
+    if (cell) cell[f] = ce[f];
+    if (v) v[f] = vv[f];
+    if (cursor) cursor[f] = s == TS_PENDING ? -1 : cur[f];
+    if (t_arrive) t_arrive[f] = s == TS_ARRIVED ? arr[f] : -1;
+  }
+  return TS_OK;
+}
+
+int ts_read_cells(ts_sim *h, int32_t link, int32_t *vid_out) {
+  if (!h || !h->inited) return fail(h, TS_EINVAL, "not initialised");
+  if (link < 0 || link >= h->nl) return fail(h, TS_EINVAL, "bad link");
+  CK(h, cudaSetDevice(h->dev));
+  CK(h, cudaStreamSynchronize(h->stream));
+  const int n = h->ncell[link], L = h->lanes[link];
+  for (int i = h->link_tile0[link]; i < h->link_tile0[link + 1]; i++) {
+    const TileDesc &d = h->tiles[i];
+    std::vector<uint8_t> code((size_t)d.L * d.w);
+    std::vector<int32_t> vids((size_t)d.L * d.w);
+    CK(h, cudaMemcpy(code.data(), h->d_code[h->cur] + d.off, code.size(), cudaMemcpyDeviceToHost));
+    CK(h, cudaMemcpy(vids.data(), h->d_vid[h->cur] + d.off, vids.size() * 4, cudaMemcpyDeviceToHost));
+    int r = 0;
+    for (int l = 0; l < L; l++)
+      for (int x = 0; x < d.w; x++) {
+        uint8_t c = code[(size_t)l * d.w + x];
+        vid_out[(size_t)l * n + d.a + x] = (c & 0x80) ? -1 : vids[r++];
+      }
+  }
+  return TS_OK;
+}
+
+int ts_state_hash(ts_sim *h, uint64_t *out) {
+  if (!h || !h->inited) return fail(h, TS_EINVAL, "not initialised");
+  CK(h, cudaSetDevice(h->dev));
+  CK(h, cudaMemsetAsync(h->d_hash, 0, 16, h->stream));
+  StepParams P = step_params(h, h->t, 0);
+  launch_hash(P, h->blocks, h->threads, h->smem, h->stream, h->d_hash);
+  CK(h, cudaGetLastError());
+  unsigned long long r[2];
+  CK(h, cudaMemcpyAsync(r, h->d_hash, 16, cudaMemcpyDeviceToHost, h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  *out = r[0];
+  return TS_OK;
+}
+
+int ts_read_history(ts_sim *h, int32_t t_from, int32_t n, uint64_t *hash, int64_t *active,
+                    int64_t *arrivals, int64_t *injections, int64_t *lane_changes,
+                    int64_t *crossings) {
+  if (!h || !h->inited) return fail(h, TS_EINVAL, "not initialised");
+  if (n < 0 || n > kHist || t_from + n - 1 > h->t || t_from < h->t - kHist + 1)
+    return fail(h, TS_EINVAL, "history range not available");
+  CK(h, cudaSetDevice(h->dev));
+  CK(h, cudaStreamSynchronize(h->stream));
+  std::vector<unsigned long long> st((size_t)kHist * ST_N);
+  CK(h, cudaMemcpy(st.data(), h->d_stats, st.size() * 8, cudaMemcpyDeviceToHost));
+  for (int i = 0; i < n; i++) {
+    const unsigned long long *s = &st[(size_t)((t_from + i) & (kHist - 1)) * ST_N];
+    if (hash) hash[i] = s[ST_HASH];
+    if (active) active[i] = (int64_t)s[ST_ACTIVE];
+    if (arrivals) arrivals[i] = (int64_t)s[ST_ARR];
+    if (injections) injections[i] = (int64_t)s[ST_INJ];
+    if (lane_changes) lane_changes[i] = (int64_t)s[ST_LC];
+    if (crossings) crossings[i] = (int64_t)s[ST_CROSS];
+  }
+  return TS_OK;
+}
+
+int ts_get_totals(ts_sim *h, int64_t out[8]) {
+  if (!h || !h->inited) return fail(h, TS_EINVAL, "not initialised");
+  CK(h, cudaStreamSynchronize(h->stream));
+  unsigned long long st[ST_N];
+  CK(h, cudaMemcpy(st, h->d_stats + (size_t)(h->t & (kHist - 1)) * ST_N, sizeof st,
+                   cudaMemcpyDeviceToHost));
+  const int64_t active = (int64_t)st[ST_ACTIVE];
+  out[0] = active;
+  out[1] = h->nv - h->n_placed - h->injected;
+  out[2] = h->arrived;
+  out[3] = h->veh_updates;
+  out[4] = h->lane_cells;
+  out[5] = (int64_t)h->tiles.size();
+  out[6] = (int64_t)h->dev_bytes;
+  out[7] = 2 * h->lane_cells + 8 * active;
+  return TS_OK;
+}
+
+int ts_get_link_work(ts_sim *h, int64_t *link_work) {
+  if (!h || !h->inited) return fail(h, TS_EINVAL, "not initialised");
+  CK(h, cudaStreamSynchronize(h->stream));
+  CK(h, cudaMemcpy(link_work, h->d_work, sizeof(int64_t) * h->nl, cudaMemcpyDeviceToHost));
+  return TS_OK;
+}
+
+int ts_last_timing(ts_sim *h, double *total_ms, double *move_ms, int64_t *move_launches) {
+  if (!h) return TS_EINVAL;
+  if (total_ms) *total_ms = h->last_total_ms;
+  if (move_ms) *move_ms = h->last_move_ms;
+  if (move_launches) *move_launches = h->last_move_launches;
+  return TS_OK;
+}
+
+// --------------------------------------------------------------- partition
+// Orthogonal recursive bisection: a vertical line halves
+// the load, then the larger piece is cut by a horizontal line, and so on
+// until k pieces; non-power-of-two k splits in proportion.
+static void orb_rec(std::vector<int32_t> &idx, size_t lo, size_t hi, const int64_t *x,
+                    const int64_t *y, const std::vector<double> &w, int k, int dom0, bool vertical,
+                    int32_t *out) {
+  if (k == 1) {
+    for (size_t i = lo; i < hi; i++) out[idx[i]] = dom0;
+    return;
+  }
+  const int64_t *c = vertical ? x : y;
+  std::stable_sort(idx.begin() + lo, idx.begin() + hi, [&](int a, int b) {
+    return c[a] < c[b] || (c[a] == c[b] && a < b);
+  });
+  const int kl = (k + 1) / 2, kr = k - kl;
+  double tot = 0;
+  for (size_t i = lo; i < hi; i++) tot += w[idx[i]];
+  const double target = tot * kl / k;
+  double acc = 0, best = 1e300;
+  size_t cut = lo + 1;
+  for (size_t i = lo; i + 1 < hi + 1 && i < hi; i++) {
+    acc += w[idx[i]];
+    const size_t c1 = i + 1;
+    if (c1 - lo < (size_t)kl || hi - c1 < (size_t)kr) continue;
+    const double dev = std::fabs(acc - target);
+    if (dev < best) {
+      best = dev;
+      cut = c1;
+    }
+  }
+  orb_rec(idx, lo, cut, x, y, w, kl, dom0, !vertical, out);
+  orb_rec(idx, cut, hi, x, y, w, kr, dom0 + kl, !vertical, out);
+}
+
+int ts_orb_partition(int32_t n_nodes, const int64_t *node_x_mm, const int64_t *node_y_mm,
+                     const double *node_weight, int32_t k, int32_t *domain_of_node) {
+  if (n_nodes < 1 || k < 1 || k > n_nodes) return TS_EINVAL;
+  std::vector<double> w(n_nodes, 1.0);
+  if (node_weight)
+    for (int i = 0; i < n_nodes; i++) w[i] = std::max(0.0, node_weight[i]);
+  std::vector<int32_t> idx(n_nodes);
+  std::iota(idx.begin(), idx.end(), 0);
+  orb_rec(idx, 0, n_nodes, node_x_mm, node_y_mm, w, k, 0, true, domain_of_node);
+  return TS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,174 @@
+// tsim_internal.h -- device layout shared by the host driver (tsim_api.cu)
+// and the sm_100a kernels (tsim_kernels.cu).  See DESIGN.md §6 for the
+// layout rationale.
+#pragma once
+#include <cstdint>
+
+namespace tsim {
+
+constexpr int kGmax = 5;          // interaction range, PAPER.md:390-395 (R2)
+constexpr int kSlotFinal = 15;    // code slot: vehicle is on its final link
+constexpr uint8_t kEmpty = 0xFF;  // empty lane-cell code
+constexpr int kHist = 4096;       // per-step stats ring buffer
+constexpr int kHaloPad = 16;      // smem pad on both sides of a halo tile row
+constexpr int kMaxLanes = 8;
+
+// Cell code (one byte per lane-cell): 0xFF empty, else bits 0-2 velocity
+// (0..5) and bits 3-6 the out-slot of the vehicle's next route link at the
+// link's downstream node (15 = final link).  Occupied iff bit 7 is clear.
+
+// Tile flags
+constexpr uint8_t kFirst = 1;     // tile starts at cell 0 of a non-periodic link
+constexpr uint8_t kLast = 2;      // tile ends at the end of a non-periodic link
+constexpr uint8_t kPeriodic = 4;  // tile of the periodic (ring) link
+constexpr uint8_t kHalo = 8;      // tile reads 5-cell halos from strips
+constexpr uint8_t kHasUp = 16;    // upstream halo present
+constexpr uint8_t kHasDn = 32;    // downstream halo present
+
+// One tile = cells [a, a+w) of all lanes of one link.  Codes are stored
+// lane-major at code[off + l*w + i], vehicles as a compact vid list in
+// (lane, cell) order at vid[off + rank].  32 bytes.
+struct TileDesc {
+  int64_t off;
+  int32_t link;
+  int32_t a;
+  int32_t lane_gid;  // global id of lane 0 of the link
+  int32_t strip;     // first strip slot of this tile (one per lane) or -1
+  int32_t n;         // cells of the link
+  uint16_t w;
+  uint8_t L;
+  uint8_t flags;
+};
+static_assert(sizeof(TileDesc) == 32, "TileDesc must be 32 bytes");
+
+// 5-cell strips next to a tile boundary: written by the
+// tile every time it writes its state; read as halo by its neighbours (or,
+// across domains, copied into a mirror slot by the exchange).
+struct Strip {
+  uint8_t head_code[8];
+  uint8_t tail_code[8];
+  int32_t head_vid[8];
+  int32_t tail_vid[8];
+  int32_t tail_cur[8];
+};
+
+// smem workspace of one warp for a tile with L lanes and row stride S
+struct WarpLayout {
+  int NC, NW;
+  int o_cin, o_cout, o_bin, o_bout, o_vout, o_vpos, bytes;
+};
+
+__host__ __device__ inline int tile_stride(int w, uint8_t flags) {
+  return (flags & kHalo) ? (((w + 15) & ~15) + 2 * kHaloPad) : w;
+}
+
+__host__ __device__ inline WarpLayout warp_layout(int NCmax) {
+  WarpLayout l;
+  l.NC = (NCmax + 31) & ~31;
+  l.NW = l.NC / 32 + 3;  // front pad word + data + 2 back pad words
+  int o = 0;
+  l.o_cin = o;
+  o += l.NC;
+  l.o_cout = o;
+  o += l.NC;
+  l.o_bin = o;
+  o += 4 * l.NW;
+  l.o_bout = o;
+  o += 4 * l.NW;
+  o = (o + 15) & ~15;
+  l.o_vout = o;
+  o += 4 * l.NC;
+  l.o_vpos = o;  // vpos[NC] then dpos[NC] (uint16)
+  o += 4 * l.NC;
+  l.bytes = (o + 127) & ~127;
+  return l;
+}
+
+// stats slot layout (uint64 each)
+enum { ST_HASH = 0, ST_ACTIVE, ST_ARR, ST_INJ, ST_LC, ST_CROSS, ST_SUMV, ST_N };
+
+// kernel modes
+constexpr int kModeMove = 1;    // velocity update + move (H4/H5)
+constexpr int kModeInject = 2;  // injection (H6)
+constexpr int kModeLC = 4;      // lane change on the output state (H1)
+constexpr int kModeHash = 8;    // accumulate state hash
+constexpr int kModeWork = 16;   // per-link work counters
+
+struct StepParams {
+  const TileDesc *tiles;
+  int32_t ntiles;
+  int32_t t;  // step t: S1(t) -> S(t+1); k_lc: S(t) -> S1(t)
+  int32_t mode;
+  int32_t D;
+  uint32_t k0, k1;
+  uint64_t p32;
+  WarpLayout lay;
+  // state (in / out buffers)
+  const uint8_t *code_in;
+  uint8_t *code_out;
+  const int32_t *vid_in;
+  int32_t *vid_out;
+  const Strip *strip_in;
+  Strip *strip_out;
+  const int32_t *halo_up;  // per strip slot of lane 0: strip of upstream neighbour
+  const int32_t *halo_dn;
+  // network
+  const uint8_t *vmax_link;
+  const uint32_t *tt_link;  // 2 bits per out-slot: 0 T, 1 L, 2 R
+  const int32_t *out_pos;   // slot of each link at its from-node
+  // vehicles
+  const int64_t *route_off;
+  const int32_t *route;
+  int32_t *cursor;
+  const int32_t *dep;
+  const int32_t *entry;
+  int32_t *inj_time;
+  int32_t *arr_time;
+  const int32_t *pend_off;   // per link
+  const int32_t *pend_list;  // vids in (departure, vid) order
+  int32_t *pend_head;
+  // node interface
+  uint64_t *tail_rec;  // per lane, written with S1
+  uint8_t *head_occ;   // per lane, written with S1
+  const uint8_t *ext;  // per lane, from k_node
+  const uint64_t *entr;
+  // outputs
+  unsigned long long *stats;  // [kHist][ST_N]
+  unsigned long long *link_work;
+};
+
+struct NodeParams {
+  int32_t nnodes;
+  int32_t t;
+  int32_t G;
+  uint32_t k0, k1;
+  uint64_t p32;
+  const int32_t *in_off, *in_list, *out_off, *out_list;
+  const int32_t *link_ncell, *link_lanes, *link_lgid, *link_cls;
+  const uint8_t *vmax_link;
+  const uint32_t *tt_link;
+  const int32_t *out_pos;
+  const int64_t *route_off;
+  const int32_t *route;
+  int32_t *cursor;
+  const uint64_t *tail_rec;
+  const uint8_t *head_occ;
+  uint8_t *ext;
+  uint64_t *entr;
+  unsigned long long *stats;
+};
+
+// tail record of a lane in S1 (read by k_node):
+//   bits 0-31 front vid, 32-39 front code, 40-42 d = n-1-x, 43 has-front
+//   (front vehicle inside the last 5 cells), 44-48 occupancy of the last 5
+//   cells (bit i = cell n-1-i)
+// entrant record (written by k_node for the target lane):
+//   bits 0-31 vid, 32-39 code, 40-42 landing cell, 43-63 stamp (t+1)
+
+void launch_lc(const StepParams &p, int blocks, int threads, int smem, void *stream);
+void launch_step(const StepParams &p, int blocks, int threads, int smem, void *stream);
+void launch_node(const NodeParams &p, void *stream);
+void launch_hash(const StepParams &p, int blocks, int threads, int smem, void *stream,
+                 unsigned long long *out);
+
+}  // namespace tsim

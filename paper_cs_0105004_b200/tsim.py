@@ -1,0 +1,225 @@
+"""ctypes binding of libtsim (include/tsim.h) -- argument marshalling only.
+
+Every step of the CA path runs in the CUDA kernels of csrc/.  There is no
+CPU fallback: without the built library or a CUDA device the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "libtsim.so")
+
+FLAG_FUSED, FLAG_HASH, FLAG_LINK_WORK, FLAG_GRAPH = 1, 2, 4, 8
+PENDING, ACTIVE, ARRIVED = 0, 1, 2
+
+
+class TsError(RuntimeError):
+    pass
+
+
+class Config(ctypes.Structure):
+    _fields_ = [("p_slow", ctypes.c_double), ("seed", ctypes.c_uint64),
+                ("gap_accept_G", ctypes.c_int32), ("desperation_D", ctypes.c_int32),
+                ("flags", ctypes.c_uint32), ("device", ctypes.c_int32),
+                ("tile_cells", ctypes.c_int32)]
+
+
+_lib = None
+
+
+def load_library():
+    """Load libtsim.so (built in-tree by __graft_entry__.build())."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(_SO):
+        raise TsError(f"{_SO} is missing: run __graft_entry__.build() (no CPU fallback)")
+    lib = ctypes.CDLL(_SO)
+    P, I32, I64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
+    sig = {
+        "ts_create": (ctypes.c_int, [ctypes.POINTER(Config), ctypes.POINTER(P)]),
+        "ts_destroy": (None, [P]),
+        "ts_last_error": (ctypes.c_char_p, [P]),
+        "ts_load_network": (ctypes.c_int, [P, I32, P, P, I32, P, P, P, P, P, P, I32]),
+        "ts_load_vehicles": (ctypes.c_int, [P, I32, P, P, P, P]),
+        "ts_place_vehicles": (ctypes.c_int, [P, I32, P, P, P, P]),
+        "ts_init": (ctypes.c_int, [P, I32]),
+        "ts_step": (ctypes.c_int, [P, I32]),
+        "ts_step_async": (ctypes.c_int, [P, I32]),
+        "ts_sync": (ctypes.c_int, [P]),
+        "ts_time": (I32, [P]),
+        "ts_read_vehicles": (ctypes.c_int, [P, P, P, P, P, P, P, P]),
+        "ts_read_cells": (ctypes.c_int, [P, I32, P]),
+        "ts_link_cells": (I32, [P, I32]),
+        "ts_state_hash": (ctypes.c_int, [P, ctypes.POINTER(ctypes.c_uint64)]),
+        "ts_read_history": (ctypes.c_int, [P, I32, I32, P, P, P, P, P, P]),
+        "ts_get_totals": (ctypes.c_int, [P, P]),
+        "ts_get_link_work": (ctypes.c_int, [P, P]),
+        "ts_orb_partition": (ctypes.c_int, [I32, P, P, P, I32, P]),
+        "ts_last_timing": (ctypes.c_int, [P, ctypes.POINTER(ctypes.c_double),
+                                          ctypes.POINTER(ctypes.c_double),
+                                          ctypes.POINTER(ctypes.c_int64)]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def exported_symbols():
+    """Names declared in include/tsim.h (for the ABI test)."""
+    import re
+    hdr = open(os.path.join(os.path.dirname(_HERE), "include", "tsim.h")).read()
+    return sorted(set(re.findall(r"\b(ts_[a-z_]+)\s*\(", hdr)))
+
+
+def _a(x, dt):
+    return np.ascontiguousarray(x, dtype=dt)
+
+
+def _p(a):
+    return a.ctypes.data if a is not None and a.size else None
+
+
+def orb_partition(node_x, node_y, k, weight=None):
+    """Orthogonal recursive bisection -> domain per node."""
+    lib = load_library()
+    x, y = _a(node_x, np.int64), _a(node_y, np.int64)
+    w = None if weight is None else _a(weight, np.float64)
+    out = np.zeros(x.size, np.int32)
+    rc = lib.ts_orb_partition(x.size, x.ctypes.data, y.ctypes.data, _p(w), int(k), out.ctypes.data)
+    if rc:
+        raise TsError(f"ts_orb_partition failed ({rc})")
+    return out
+
+
+class Sim:
+    """One simulation handle on one GPU."""
+
+    def __init__(self, p_slow=0.2, seed=1, gap_G=5, desp_D=10, flags=FLAG_FUSED | FLAG_HASH,
+                 device=0, tile_cells=0):
+        self.lib = load_library()
+        cfg = Config(float(p_slow), int(seed), int(gap_G), int(desp_D), int(flags), int(device),
+                     int(tile_cells))
+        h = ctypes.c_void_p()
+        rc = self.lib.ts_create(ctypes.byref(cfg), ctypes.byref(h))
+        if rc:
+            raise TsError(self.lib.ts_last_error(None).decode())
+        self.h = h
+        self.flags = flags
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.lib.ts_destroy(self.h)
+            self.h = None
+
+    def close(self):
+        self.__del__()
+
+    def _check(self, rc):
+        if rc:
+            raise TsError(self.lib.ts_last_error(self.h).decode())
+
+    @classmethod
+    def from_scenario(cls, scn, t0=0, **kw):
+        kw.setdefault("p_slow", scn.p_slow)
+        kw.setdefault("seed", scn.seed)
+        s = cls(**kw)
+        s.load(scn)
+        s.init(t0)
+        return s
+
+    def load(self, scn):
+        i32 = lambda a: _a(a, np.int32)  # noqa: E731
+        i64 = lambda a: _a(a, np.int64)  # noqa: E731
+        nx, ny = i64(scn.node_x), i64(scn.node_y)
+        arr = [i32(scn.link_from), i32(scn.link_to), i64(scn.link_len_mm), i32(scn.link_lanes),
+               i32(scn.link_vmax), i32(scn.link_class)]
+        self._check(self.lib.ts_load_network(self.h, scn.n_nodes, nx.ctypes.data, ny.ctypes.data,
+                                             scn.n_links, *(a.ctypes.data for a in arr),
+                                             int(scn.periodic_link)))
+        veh = [i64(scn.route_off), i32(scn.route), i32(scn.depart), i32(scn.entry)]
+        self._check(self.lib.ts_load_vehicles(self.h, scn.n_vehicles, *(_p(a) for a in veh)))
+        self.n_veh = scn.n_vehicles
+        self.n_links = scn.n_links
+        self.lanes = np.asarray(scn.link_lanes, dtype=np.int32)
+        if scn.place_vid.size:
+            pl = [i32(scn.place_vid), i32(scn.place_lane), i32(scn.place_cell), i32(scn.place_v)]
+            self._check(self.lib.ts_place_vehicles(self.h, pl[0].size, *(a.ctypes.data for a in pl)))
+
+    def init(self, t0=0):
+        self._check(self.lib.ts_init(self.h, int(t0)))
+
+    def step(self, n=1):
+        self._check(self.lib.ts_step(self.h, int(n)))
+
+    def step_async(self, n=1):
+        self._check(self.lib.ts_step_async(self.h, int(n)))
+
+    def sync(self):
+        self._check(self.lib.ts_sync(self.h))
+
+    @property
+    def t(self):
+        return int(self.lib.ts_time(self.h))
+
+    def n_cells(self, link):
+        return int(self.lib.ts_link_cells(self.h, int(link)))
+
+    def state_hash(self):
+        out = ctypes.c_uint64()
+        self._check(self.lib.ts_state_hash(self.h, ctypes.byref(out)))
+        return int(out.value)
+
+    def vehicles(self):
+        n = self.n_veh
+        st = np.zeros(n, np.int8)
+        arrs = [np.zeros(n, np.int32) for _ in range(6)]
+        self._check(self.lib.ts_read_vehicles(self.h, _p(st), *(_p(a) for a in arrs)))
+        return dict(status=st, link=arrs[0], lane=arrs[1], cell=arrs[2], v=arrs[3],
+                    cursor=arrs[4], t_arrive=arrs[5])
+
+    def cells(self, link):
+        n = self.n_cells(link)
+        out = np.zeros(int(self.lanes[link]) * n, np.int32)
+        self._check(self.lib.ts_read_cells(self.h, int(link), out.ctypes.data))
+        return out.reshape(int(self.lanes[link]), n)
+
+    def history(self, t_from, n):
+        h = np.zeros(n, np.uint64)
+        cols = [np.zeros(n, np.int64) for _ in range(5)]
+        self._check(self.lib.ts_read_history(self.h, int(t_from), int(n), _p(h),
+                                             *(_p(c) for c in cols)))
+        return dict(hash=[int(x) for x in h], active=cols[0], arrivals=cols[1],
+                    injections=cols[2], lane_changes=cols[3], crossings=cols[4])
+
+    def totals(self):
+        out = np.zeros(8, np.int64)
+        self._check(self.lib.ts_get_totals(self.h, out.ctypes.data))
+        keys = ["active", "pending", "arrived", "vehicle_updates", "lane_cells", "tiles",
+                "device_bytes", "alg_bytes_per_step"]
+        return dict(zip(keys, out.tolist()))
+
+    def link_work(self):
+        out = np.zeros(self.n_links, np.int64)
+        self._check(self.lib.ts_get_link_work(self.h, out.ctypes.data))
+        return out
+
+    def last_timing(self):
+        tot, mv, n = ctypes.c_double(), ctypes.c_double(), ctypes.c_int64()
+        self._check(self.lib.ts_last_timing(self.h, ctypes.byref(tot), ctypes.byref(mv),
+                                            ctypes.byref(n)))
+        return dict(total_ms=tot.value, move_ms=mv.value, move_launches=n.value)
+
+    def run_hashes(self, n):
+        hs = []
+        for _ in range(n):
+            self.step(1)
+            hs.append(self.state_hash())
+        return hs

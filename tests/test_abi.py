@@ -1,0 +1,54 @@
+"""The C-ABI library loads and exports every symbol include/tsim.h declares
+(no compute call without a GPU); the product path has no CPU fallback."""
+import ctypes
+import os
+
+import numpy as np
+import pytest
+
+import paper_cs_0105004_b200 as tsim
+from paper_cs_0105004_b200 import tsim as binding
+
+
+def test_library_exports_header_symbols():
+    lib = tsim.load_library()
+    names = binding.exported_symbols()
+    assert len(names) >= 19
+    for n in names:
+        assert hasattr(lib, n), n
+    # and nothing in the product package imports the oracle
+    pkg = os.path.dirname(binding.__file__)
+    for root, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".h", ".cpp")):
+                src = open(os.path.join(root, f)).read()
+                assert "import oracle" not in src and "tsim_oracle" not in src, f
+
+
+def test_no_cpu_fallback_without_gpu(cuda_available):
+    if cuda_available:
+        pytest.skip("GPU present")
+    with pytest.raises(tsim.TsError, match="CUDA"):
+        tsim.Sim()
+
+
+def test_orb_partition_host():
+    """ORB is a pure host function"""
+    # 4 equal nodes at the corners of a square, p = 2 -> split along x
+    x = np.array([0, 0, 10, 10])
+    y = np.array([0, 10, 0, 10])
+    d = tsim.orb_partition(x, y, 2)
+    assert d[0] == d[1] and d[2] == d[3] and d[0] != d[2]
+    assert set(tsim.orb_partition(x, y, 1)) == {0}
+    # 2 x n grid, p = 4: four contiguous pieces of equal load
+    xs, ys = np.meshgrid(np.arange(8), np.arange(2))
+    d = tsim.orb_partition(xs.ravel(), ys.ravel(), 4)
+    assert np.bincount(d).tolist() == [4, 4, 4, 4]
+    rng = np.random.default_rng(0)
+    x, y = rng.integers(0, 10**6, 1000), rng.integers(0, 10**6, 1000)
+    w = rng.random(1000)
+    for k in (2, 3, 4, 5, 8, 16):
+        d = tsim.orb_partition(x, y, k, w)
+        assert set(d.tolist()) == set(range(k))
+        loads = np.bincount(d, weights=w, minlength=k)
+        assert loads.max() <= w.sum() / k + 2 * w.max() + 1e-9

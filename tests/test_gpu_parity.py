@@ -1,0 +1,136 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle,
+bit-exact in every vehicle's (status, link, lane, cell, v, cursor) and in the
+per-step state hash (north_star: "bit-exact to the oracle in every vehicle's
+cell, lane, velocity and link at every step")."""
+import numpy as np
+import pytest
+
+import oracle
+import scenarios
+from tests._ref import make_network, make_ring
+
+pytestmark = pytest.mark.gpu
+
+tsim = pytest.importorskip("paper_cs_0105004_b200")
+
+FUSED = tsim.FLAG_FUSED | tsim.FLAG_HASH
+UNFUSED = tsim.FLAG_HASH
+
+
+def assert_same_state(o, g, msg=""):
+    vo, vg = o.vehicles(), g.vehicles()
+    for key in ("status", "link", "lane", "cell", "v", "cursor", "t_arrive"):
+        bad = np.nonzero(vo[key] != vg[key])[0]
+        assert bad.size == 0, (f"{msg} {key}: {bad.size} mismatches, first vid {bad[:5]} "
+                               f"oracle {vo[key][bad[:5]]} gpu {vg[key][bad[:5]]}")
+
+
+def run_parity(scn, steps, flags, full_every=1, t0=0, tile_cells=0, hash_every=1):
+    o = oracle.Oracle.from_scenario(scn, t0=t0)
+    g = tsim.Sim.from_scenario(scn, t0=t0, flags=flags, tile_cells=tile_cells)
+    assert g.state_hash() == o.state_hash()
+    assert_same_state(o, g, "init")
+    done = 0
+    while done < steps:
+        n = min(hash_every, steps - done)
+        o.step(n)
+        g.step(n)
+        done += n
+        assert o.t == g.t
+        assert g.state_hash() == o.state_hash(), f"hash differs at t={o.t}"
+        if full_every and (done % full_every == 0 or done == steps):
+            assert_same_state(o, g, f"t={o.t}")
+    return o, g
+
+
+@pytest.mark.parametrize("case", range(24))
+def test_small_rings(case):
+    """single-tile periodic lanes (the tile's own strips as halos), 1-4
+    lanes, every step in full"""
+    rng = np.random.default_rng(900 + case)
+    lanes = int(rng.integers(1, 5))
+    L = int(rng.integers(10, 80))
+    N = int(rng.integers(0, lanes * L))
+    flat = np.sort(rng.choice(lanes * L, size=N, replace=False))
+    s = make_ring(L, flat // L, flat % L, rng.integers(0, 6, N), lanes=lanes,
+                  vmax=int(rng.integers(1, 6)), p_slow=float(rng.choice([0.0, 0.2, 0.5])),
+                  seed=int(rng.integers(1, 2**62)))
+    run_parity(s, 60, FUSED if case % 2 else UNFUSED)
+
+
+@pytest.mark.parametrize("tile_cells", [16, 37, 128, 512])
+def test_ring_multi_tile(tile_cells):
+    """segmented periodic link: halos and ghost moves across tile seams"""
+    s = scenarios.ring(n_cells=3000, lanes=3, density=0.2, seed=5)
+    run_parity(s, 150, FUSED, full_every=10, tile_cells=tile_cells)
+
+
+@pytest.mark.parametrize("flags", [FUSED, UNFUSED])
+def test_config1_full(flags):
+    """BASELINE.json configs[0] for all 600 steps"""
+    s = scenarios.config("1")
+    run_parity(s, 600, flags, full_every=20)
+
+
+@pytest.mark.parametrize("flags", [FUSED, UNFUSED])
+def test_grid_with_departures(flags):
+    """injection retries, conflicting entry cells, nodes at every step"""
+    s = scenarios.grid_trips(rows=6, cols=6, n_veh=3000, depart_max=300, steps=500, seed=7,
+                             name="grid6b")
+    run_parity(s, 500, flags, full_every=25)
+
+
+def test_grid_segmented_links():
+    """links longer than one tile: halo tiles on non-periodic links,
+    injection and node records on segmented links"""
+    s = scenarios.grid_trips(rows=4, cols=4, spacing_mm=1_500_000, lanes=3, n_veh=2500,
+                             depart_max=200, seed=3, name="grid4long")
+    run_parity(s, 400, UNFUSED, full_every=20, tile_cells=64)
+
+
+def test_portland_small():
+    s = scenarios.portland(n_nodes=600, n_edges=800, n_veh=8000, side_km=8.0, n_zones=64,
+                           seed=2)
+    # departures compressed into the first 300 s
+    s.depart = (s.depart // 12).astype(np.int32)
+    run_parity(s, 400, FUSED, full_every=50)
+
+
+def test_t0_and_odd_start():
+    s = scenarios.ring(n_cells=500, lanes=3, density=0.3, seed=9)
+    run_parity(s, 50, FUSED, t0=7)
+
+
+def test_handmade_intersections():
+    nodes = [(0, 0), (1000, 0), (-1000, 0), (0, 1000), (0, -1000)]
+    links = [(2, 0, 1000, 2, 1), (0, 1, 1000, 2, 1), (1, 0, 1000, 2, 1), (0, 2, 1000, 2, 1),
+             (4, 0, 1000, 2, 0), (0, 3, 1000, 2, 0), (3, 0, 1000, 2, 0), (0, 4, 1000, 2, 0)]
+    rng = np.random.default_rng(4)
+    routes = [[0, 1], [0, 5], [0, 7], [0, 3], [2, 3], [2, 5], [2, 7], [4, 5], [4, 1], [4, 3],
+              [6, 7], [6, 1], [6, 3], [1], [3], [5], [7]]
+    veh = []
+    for i in range(400):
+        r = routes[int(rng.integers(len(routes)))]
+        veh.append(dict(route=r, depart=int(rng.integers(0, 120)),
+                        entry=int(rng.integers(0, 120))))
+    s = make_network(nodes, links, veh, p_slow=0.25, seed=11)
+    run_parity(s, 300, FUSED)
+
+
+def test_config2_full_size_prefix():
+    """BASELINE.json configs[1] at full size (3 x 1,000,000 cells, 450,000
+    vehicles): hash every step for 40 steps, full state at the end"""
+    s = scenarios.config("2")
+    run_parity(s, 40, FUSED, full_every=40)
+
+
+def test_history_stream():
+    s = scenarios.config("1")
+    o = oracle.Oracle.from_scenario(s)
+    g = tsim.Sim.from_scenario(s, flags=FUSED)
+    g.step(100)
+    hist = g.history(1, 100)
+    for t in range(100):
+        o.step(1)
+        assert hist["hash"][t] == o.state_hash(), t
+        assert hist["active"][t] == o.counters()["active"]
