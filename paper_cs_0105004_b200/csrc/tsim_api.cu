@@ -567,7 +567,10 @@ int ts_init(ts_sim *h, int32_t t0) {
   if ((rc = upload(h, &h->d_arr, arr))) return rc;
   if ((rc = upload(h, &h->d_pend_off, pend_off))) return rc;
   if ((rc = upload(h, &h->d_pend_list, pend_list))) return rc;
-  if ((rc = dalloc(h, &h->d_pend_head, h->nl, 0))) return rc;
+  {  // absolute head index into pend_list per link
+    std::vector<int32_t> head(pend_off.begin(), pend_off.begin() + h->nl);
+    if ((rc = upload(h, &h->d_pend_head, head))) return rc;
+  }
   if ((rc = dalloc(h, &h->d_tail, h->nlanes, 0))) return rc;
   if ((rc = dalloc(h, &h->d_entr, h->nlanes, 0))) return rc;
   if ((rc = dalloc(h, &h->d_head, h->nlanes, 0))) return rc;

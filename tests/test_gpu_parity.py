@@ -52,8 +52,9 @@ def test_small_rings(case):
     L = int(rng.integers(10, 80))
     N = int(rng.integers(0, lanes * L))
     flat = np.sort(rng.choice(lanes * L, size=N, replace=False))
-    s = make_ring(L, flat // L, flat % L, rng.integers(0, 6, N), lanes=lanes,
-                  vmax=int(rng.integers(1, 6)), p_slow=float(rng.choice([0.0, 0.2, 0.5])),
+    vmax = int(rng.integers(1, 6))
+    s = make_ring(L, flat // L, flat % L, rng.integers(0, vmax + 1, N), lanes=lanes,
+                  vmax=vmax, p_slow=float(rng.choice([0.0, 0.2, 0.5])),
                   seed=int(rng.integers(1, 2**62)))
     run_parity(s, 60, FUSED if case % 2 else UNFUSED)
 
