@@ -40,6 +40,8 @@ extern "C" {
 #define TS_FLAG_HASH 2u        /* state hash of S(t+1) every step */
 #define TS_FLAG_LINK_WORK 4u   /* per-link work counters (load feedback) */
 #define TS_FLAG_GRAPH 8u       /* replay steps through a CUDA graph */
+#define TS_FLAG_GENERAL 16u     /* force the general warp-per-tile kernels (testing) */
+#define TS_FLAG_NODE_GENERAL 32u /* force the thread-per-node kernel (testing) */
 
 typedef struct ts_sim ts_sim;
 
@@ -112,6 +114,14 @@ int ts_read_vehicles(ts_sim *h, int8_t *status, int32_t *link, int32_t *lane,
  * empty), and the link's cell count. */
 int ts_read_cells(ts_sim *h, int32_t link, int32_t *vid_out);
 int32_t ts_link_cells(const ts_sim *h, int32_t link);
+
+/* Diagnostics: raw device state of a link -- for each lane, Wp =
+ * roundup(cells, 4) code bytes and the Wp-entry vid region of the lane
+ * (the first k entries are the vids of its k vehicles, in cell order).
+ * code_out / vid_out hold lanes * Wp entries; *pitch receives Wp.
+ * Single-tile links only. */
+int ts_read_raw(ts_sim *h, int32_t link, uint8_t *code_out, int32_t *vid_out,
+                int32_t *pitch);
 
 /* Order-independent state hash of S(t). */
 int ts_state_hash(ts_sim *h, uint64_t *out);

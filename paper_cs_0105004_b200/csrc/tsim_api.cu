@@ -18,7 +18,9 @@
 
 namespace tsim {
 cudaError_t set_smem_attrs(int bytes);
+cudaError_t set_rows_smem(int bytes);
 int occupancy_blocks(int threads, int smem);
+int occupancy_rows(int threads, int smem);
 }  // namespace tsim
 
 using namespace tsim;
@@ -60,6 +62,16 @@ struct ts_sim {
   WarpLayout lay{};
   int threads = 256, blocks = 1, smem = 0;
   bool fused = false;
+  bool rows_mode = false, node_warp = false;
+  std::vector<GroupDesc> groups;
+  std::vector<uint8_t> rowmap;
+  int rows_cmax = 0, rows_threads = 128, rows_blocks = 1, rows_smem = 0;
+  RowsLayout rlay{};
+  GroupDesc *d_groups = nullptr;
+  uint8_t *d_rowmap = nullptr;
+  NodeLane *d_nlanes = nullptr;
+  int32_t *d_chunk_off = nullptr;
+  int32_t nchunks = 0;
   uint64_t p32 = 0;
   // device
   TileDesc *d_tiles = nullptr;
@@ -364,7 +376,7 @@ static void build_tiles(ts_sim *h) {
       }
       d.flags = f;
       h->tiles.push_back(d);
-      off += ((int64_t)w * h->lanes[k] + 15) & ~(int64_t)15;
+      off += tile_cells_padded(w, h->lanes[k]);
       a += w;
     }
   }
@@ -386,6 +398,86 @@ static void build_tiles(ts_sim *h) {
   for (const TileDesc &d : h->tiles) nc_max = std::max(nc_max, (int)d.L * tile_stride(d.w, d.flags));
   h->lay = warp_layout(nc_max);
   h->fused = (h->cfg.flags & TS_FLAG_FUSED) && h->nstrips == 0;
+  // row groups for k_rows: consecutive whole-link tiles, <= 32 rows and
+  // <= kGroupCells cells per warp
+  h->rows_mode = h->nstrips == 0 && !(h->cfg.flags & TS_FLAG_GENERAL);
+  h->groups.clear();
+  h->rowmap.clear();
+  if (h->rows_mode) {
+    const int kGroupCells = 8192;
+    size_t i = 0;
+    int cmax = 128;
+    while (i < h->tiles.size()) {
+      GroupDesc g{};
+      g.t0 = (int32_t)i;
+      int rows = 0;
+      int64_t cells = 0;
+      while (i < h->tiles.size()) {
+        const TileDesc &d = h->tiles[i];
+        const int64_t c = tile_cells_padded(d.w, d.L);
+        if (g.ntiles > 0 && (rows + d.L > 32 || cells + c > kGroupCells)) break;
+        for (int l = 0; l < d.L; l++) h->rowmap.push_back((uint8_t)((g.ntiles << 3) | l));
+        rows += d.L;
+        cells += c;
+        g.ntiles++;
+        i++;
+      }
+      for (int r = rows; r < 32; r++) h->rowmap.push_back(0);
+      g.nrows = (int16_t)rows;
+      g.bytes = (int32_t)cells;
+      cmax = std::max(cmax, (int)cells);
+      h->groups.push_back(g);
+    }
+    h->rows_cmax = cmax;
+  }
+}
+
+// injection capacity of each row group: at most min(pending, cells) per link
+static int group_inj_caps(ts_sim *h, const std::vector<int32_t> &pend_off) {
+  int cap = 1;
+  for (GroupDesc &g : h->groups) {
+    int64_t c = 0;
+    for (int i = 0; i < g.ntiles; i++) {
+      const TileDesc &d = h->tiles[g.t0 + i];
+      c += std::min<int64_t>(pend_off[d.link + 1] - pend_off[d.link], d.w);
+    }
+    g.inj_cap = (int32_t)c;
+    cap = std::max<int64_t>(cap, c);
+  }
+  return cap;
+}
+
+// incoming lanes of every node in priority order (R9: major class first,
+// then link id, then lane), packed into chunks of <= 32 lanes
+static bool build_node_lanes(ts_sim *h, std::vector<NodeLane> &lanes,
+                             std::vector<int32_t> &chunk_off) {
+  lanes.clear();
+  chunk_off.assign(1, 0);
+  int in_chunk = 0;
+  for (int nd = 0; nd < h->nn; nd++) {
+    const int a = h->in_off[nd], b = h->in_off[nd + 1];
+    if (a == b) continue;
+    int maxcls = h->cls[h->in_list[a]], nl = 0;
+    for (int i = a; i < b; i++) {
+      maxcls = std::max(maxcls, h->cls[h->in_list[i]]);
+      nl += h->lanes[h->in_list[i]];
+    }
+    if (nl > 32) return false;
+    if (in_chunk + nl > 32) {
+      chunk_off.push_back((int32_t)lanes.size());
+      in_chunk = 0;
+    }
+    for (int pass = 0; pass < 2; pass++)
+      for (int i = a; i < b; i++) {
+        const int j = h->in_list[i];
+        if ((h->cls[j] == maxcls) != (pass == 0)) continue;
+        for (int l = 0; l < h->lanes[j]; l++)
+          lanes.push_back(NodeLane{h->lgid[j] + l, j, nd, (int16_t)l, (int16_t)(pass == 0)});
+      }
+    in_chunk += nl;
+  }
+  if (in_chunk > 0) chunk_off.push_back((int32_t)lanes.size());
+  return true;
 }
 
 static int tile_of(const ts_sim *h, int k, int x) {
@@ -509,16 +601,20 @@ int ts_init(ts_sim *h, int32_t t0) {
     const int f = h->pl_vid[i], k = h->route[h->roff[f]];
     const int ti = tile_of(h, k, h->pl_cell[i]);
     const TileDesc &d = h->tiles[ti];
-    const int64_t pos = d.off + (int64_t)h->pl_lane[i] * d.w + (h->pl_cell[i] - d.a);
+    const int64_t pos = d.off + (int64_t)h->pl_lane[i] * row_pitch(d.w) + (h->pl_cell[i] - d.a);
     if (code[pos] != kEmpty) return fail(h, TS_EINVAL, "placement %zu: cell taken", i);
     code[pos] = (uint8_t)(h->pl_v[i] | (first_slot(h, f) << 3));
     cellvid[pos] = f;
   }
   std::vector<int32_t> vids(h->total_cells, -1);
-  for (const TileDesc &d : h->tiles) {
-    int64_t r = d.off;
-    for (int64_t i = 0; i < (int64_t)d.L * d.w; i++)
-      if (code[d.off + i] != kEmpty) vids[r++] = cellvid[d.off + i];
+  for (const TileDesc &d : h->tiles) {  // per-row vid lists in cell order
+    const int Wp = row_pitch(d.w);
+    for (int l = 0; l < d.L; l++) {
+      const int64_t rb = d.off + (int64_t)l * Wp;
+      int64_t r = rb;
+      for (int x = 0; x < d.w; x++)
+        if (code[rb + x] != kEmpty) vids[r++] = cellvid[rb + x];
+    }
   }
   std::vector<int32_t>().swap(cellvid);
   h->n_placed = (int64_t)h->pl_vid.size();
@@ -597,6 +693,29 @@ int ts_init(ts_sim *h, int32_t t0) {
   int occ = std::max(1, occupancy_blocks(h->threads, h->smem));
   const int need = (int)((h->tiles.size() + wpb - 1) / wpb);
   h->blocks = std::max(1, std::min(need, occ * nsm));
+  if (h->rows_mode) {
+    h->rlay = rows_layout(h->rows_cmax, group_inj_caps(h, pend_off));
+    if ((rc = upload(h, &h->d_groups, h->groups))) return rc;
+    if ((rc = upload(h, &h->d_rowmap, h->rowmap))) return rc;
+    const int rw = std::max(1, std::min(4, (200 * 1024) / h->rlay.bytes));
+    h->rows_threads = 32 * rw;
+    h->rows_smem = rw * h->rlay.bytes;
+    CK(h, set_rows_smem(h->rows_smem));
+    const int rocc = std::max(1, occupancy_rows(h->rows_threads, h->rows_smem));
+    const int rneed = (int)((h->groups.size() + rw - 1) / rw);
+    h->rows_blocks = std::max(1, std::min(rneed, rocc * nsm));
+  }
+  {
+    std::vector<NodeLane> nlanes;
+    std::vector<int32_t> chunk_off;
+    h->node_warp = h->periodic < 0 && !(h->cfg.flags & (TS_FLAG_GENERAL | TS_FLAG_NODE_GENERAL)) &&
+                   build_node_lanes(h, nlanes, chunk_off);
+    if (h->node_warp) {
+      h->nchunks = (int32_t)chunk_off.size() - 1;
+      if ((rc = upload(h, &h->d_nlanes, nlanes))) return rc;
+      if ((rc = upload(h, &h->d_chunk_off, chunk_off))) return rc;
+    }
+  }
   // initial injection: departure <= t0 (O1 §Init), S(t0) into buffer 1
   h->cur = 0;
   if (zero_stats(h, t0, 1)) return TS_EINTERNAL;
@@ -646,11 +765,20 @@ static int enqueue_steps(ts_sim *h, int32_t n) {
       launch_lc(step_params(h, t + i, 0), h->blocks, h->threads, h->smem, h->stream);
       h->cur ^= 1;
     }
-    launch_node(node_params(h, t + i), h->stream);
+    if (h->node_warp)
+      launch_node_warp(node_params(h, t + i), NodeWarpParams{h->d_nlanes, h->d_chunk_off, h->nchunks},
+                       h->stream);
+    else
+      launch_node(node_params(h, t + i), h->stream);
     int m = mode;
     if (h->fused && i < n - 1) m |= kModeLC;
     if (h->timing) CK(h, cudaEventRecord(h->mv_ev[2 * i], h->stream));
-    launch_step(step_params(h, t + i, m), h->blocks, h->threads, h->smem, h->stream);
+    if (h->rows_mode)
+      launch_rows(step_params(h, t + i, m),
+                  RowsParams{h->d_groups, h->d_rowmap, (int32_t)h->groups.size(), h->rlay},
+                  h->rows_blocks, h->rows_threads, h->rows_smem, h->stream);
+    else
+      launch_step(step_params(h, t + i, m), h->blocks, h->threads, h->smem, h->stream);
     if (h->timing) CK(h, cudaEventRecord(h->mv_ev[2 * i + 1], h->stream));
     h->cur ^= 1;
   }
@@ -736,10 +864,11 @@ int ts_read_vehicles(ts_sim *h, int8_t *status, int32_t *link, int32_t *lane, in
   std::vector<int32_t> lk(h->nv, -1), ln(h->nv, -1), ce(h->nv, -1), vv(h->nv, -1);
   std::vector<uint8_t> seen(h->nv, 0);
   for (const TileDesc &d : h->tiles) {
-    int64_t r = d.off;
-    for (int l = 0; l < d.L; l++)
+    for (int l = 0; l < d.L; l++) {
+      const int64_t rb = d.off + (int64_t)l * row_pitch(d.w);
+      int64_t r = rb;
       for (int x = 0; x < d.w; x++) {
-        uint8_t c = code[d.off + (int64_t)l * d.w + x];
+        uint8_t c = code[rb + x];
         if (c & 0x80) continue;
         int f = vids[r++];
         if (f < 0 || f >= h->nv || seen[f])
@@ -750,6 +879,7 @@ int ts_read_vehicles(ts_sim *h, int8_t *status, int32_t *link, int32_t *lane, in
         ce[f] = d.a + x;
         vv[f] = c & 7;
       }
+    }
   }
   for (int f = 0; f < h->nv; f++) {
     int8_t s = TS_ACTIVE;
@@ -776,17 +906,33 @@ int ts_read_cells(ts_sim *h, int32_t link, int32_t *vid_out) {
   const int n = h->ncell[link], L = h->lanes[link];
   for (int i = h->link_tile0[link]; i < h->link_tile0[link + 1]; i++) {
     const TileDesc &d = h->tiles[i];
-    std::vector<uint8_t> code((size_t)d.L * d.w);
-    std::vector<int32_t> vids((size_t)d.L * d.w);
+    const int Wp = row_pitch(d.w);
+    std::vector<uint8_t> code((size_t)d.L * Wp);
+    std::vector<int32_t> vids((size_t)d.L * Wp);
     CK(h, cudaMemcpy(code.data(), h->d_code[h->cur] + d.off, code.size(), cudaMemcpyDeviceToHost));
     CK(h, cudaMemcpy(vids.data(), h->d_vid[h->cur] + d.off, vids.size() * 4, cudaMemcpyDeviceToHost));
-    int r = 0;
-    for (int l = 0; l < L; l++)
+    for (int l = 0; l < L; l++) {
+      int r = l * Wp;
       for (int x = 0; x < d.w; x++) {
-        uint8_t c = code[(size_t)l * d.w + x];
+        uint8_t c = code[(size_t)l * Wp + x];
         vid_out[(size_t)l * n + d.a + x] = (c & 0x80) ? -1 : vids[r++];
       }
+    }
   }
+  return TS_OK;
+}
+
+int ts_read_raw(ts_sim *h, int32_t link, uint8_t *code_out, int32_t *vid_out, int32_t *pitch) {
+  if (!h || !h->inited) return fail(h, TS_EINVAL, "not initialised");
+  if (link < 0 || link >= h->nl) return fail(h, TS_EINVAL, "bad link");
+  if (h->link_ntiles[link] != 1) return fail(h, TS_EINVAL, "link spans several tiles");
+  CK(h, cudaSetDevice(h->dev));
+  CK(h, cudaStreamSynchronize(h->stream));
+  const TileDesc &d = h->tiles[h->link_tile0[link]];
+  const int Wp = row_pitch(d.w);
+  *pitch = Wp;
+  CK(h, cudaMemcpy(code_out, h->d_code[h->cur] + d.off, (size_t)d.L * Wp, cudaMemcpyDeviceToHost));
+  CK(h, cudaMemcpy(vid_out, h->d_vid[h->cur] + d.off, (size_t)d.L * Wp * 4, cudaMemcpyDeviceToHost));
   return TS_OK;
 }
 

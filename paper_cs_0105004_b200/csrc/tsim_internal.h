@@ -25,9 +25,10 @@ constexpr uint8_t kHalo = 8;      // tile reads 5-cell halos from strips
 constexpr uint8_t kHasUp = 16;    // upstream halo present
 constexpr uint8_t kHasDn = 32;    // downstream halo present
 
-// One tile = cells [a, a+w) of all lanes of one link.  Codes are stored
-// lane-major at code[off + l*w + i], vehicles as a compact vid list in
-// (lane, cell) order at vid[off + rank].  32 bytes.
+// One tile = cells [a, a+w) of all lanes of one link.  Lane l of the tile
+// is a "row" of Wp = roundup(w, 4) cells: codes at code[off + l*Wp + i],
+// and the vids of the row's vehicles, in cell order, at vid[off + l*Wp + j]
+// (j < number of vehicles in the row).  32 bytes.
 struct TileDesc {
   int64_t off;
   int32_t link;
@@ -55,12 +56,77 @@ struct Strip {
 // smem workspace of one warp for a tile with L lanes and row stride S
 struct WarpLayout {
   int NC, NW;
-  int o_cin, o_cout, o_bin, o_bout, o_vout, o_vpos, bytes;
+  int o_cin, o_cout, o_bin, o_bout, o_vout, o_vpos, o_lf, bytes;
 };
 
+__host__ __device__ inline int row_pitch(int w) { return (w + 3) & ~3; }
+
+// smem row stride of a tile in the general (warp-per-tile) kernels
 __host__ __device__ inline int tile_stride(int w, uint8_t flags) {
-  return (flags & kHalo) ? (((w + 15) & ~15) + 2 * kHaloPad) : w;
+  return (flags & kHalo) ? (((w + 15) & ~15) + 2 * kHaloPad) : row_pitch(w);
 }
+
+// global cells occupied by a tile (16-cell aligned)
+__host__ __device__ inline int64_t tile_cells_padded(int w, int L) {
+  return ((int64_t)row_pitch(w) * L + 15) & ~(int64_t)15;
+}
+
+// Row kernel (k_rows): one warp per group of consecutive whole-link tiles
+// with at most 32 rows; thread i owns row i.  rowmap[g*32+i] =
+// (tile index within the group << 3) | lane.
+struct GroupDesc {
+  int32_t t0;
+  int16_t ntiles;
+  int16_t nrows;
+  int32_t bytes;    // cells spanned by the group's tiles (16-aligned)
+  int32_t inj_cap;  // bound on vehicles the group can inject in one step
+};
+
+struct RowsLayout {
+  int CMAX, NW, injcap;
+  int o_cin, o_cout, o_bin, o_bmid, o_bspec, o_bleave, o_ent, o_injx, o_injv, o_misc, bytes;
+};
+
+__host__ __device__ inline RowsLayout rows_layout(int cmax, int injcap) {
+  RowsLayout l;
+  l.CMAX = (cmax + 127) & ~127;
+  l.NW = l.CMAX / 32 + 3;
+  l.injcap = injcap;
+  int o = 0;
+  l.o_cin = o;
+  o += l.CMAX;
+  l.o_cout = o;
+  o += l.CMAX;
+  l.o_bin = o;
+  o += 4 * l.NW;
+  l.o_bmid = o;
+  o += 4 * l.NW;
+  l.o_bspec = o;
+  o += 4 * l.NW;
+  l.o_bleave = o;
+  o += 4 * l.NW;
+  l.o_ent = o;  // entrant vid per row, then entrant cell per row
+  o += 4 * 64;
+  l.o_injx = o;  // injected: (row << 16) | cell
+  o += 4 * injcap;
+  l.o_injv = o;  // injected vid
+  o += 4 * injcap;
+  l.o_misc = o;  // injection counter
+  o += 16;
+  l.bytes = (o + 127) & ~127;
+  return l;
+}
+
+// Warp-cooperative node kernel: the incoming lanes of every node, in the
+// priority order (major class first, then link id, then lane; R9), packed
+// into chunks of <= 32 that never split a node.
+struct NodeLane {
+  int32_t lane_gid;
+  int32_t link;
+  int32_t node;
+  int16_t lane;
+  int16_t major;
+};
 
 __host__ __device__ inline WarpLayout warp_layout(int NCmax) {
   WarpLayout l;
@@ -78,8 +144,11 @@ __host__ __device__ inline WarpLayout warp_layout(int NCmax) {
   o = (o + 15) & ~15;
   l.o_vout = o;
   o += 4 * l.NC;
-  l.o_vpos = o;  // vpos[NC] then dpos[NC] (uint16)
-  o += 4 * l.NC;
+  l.o_vpos = o;  // vpos[NC], dpos[NC], vrow[NC] (uint16)
+  o += 6 * l.NC;
+  o = (o + 15) & ~15;
+  l.o_lf = o;  // first rank of each lane
+  o += 4 * 8;
   l.bytes = (o + 127) & ~127;
   return l;
 }
@@ -165,7 +234,23 @@ struct NodeParams {
 // entrant record (written by k_node for the target lane):
 //   bits 0-31 vid, 32-39 code, 40-42 landing cell, 43-63 stamp (t+1)
 
+struct RowsParams {
+  const GroupDesc *groups;
+  const uint8_t *rowmap;
+  int32_t ngroups;
+  RowsLayout lay;
+};
+
+struct NodeWarpParams {
+  const NodeLane *lanes;
+  const int32_t *chunk_off;  // [nchunks + 1]
+  int32_t nchunks;
+};
+
 void launch_lc(const StepParams &p, int blocks, int threads, int smem, void *stream);
+void launch_rows(const StepParams &p, const RowsParams &r, int blocks, int threads, int smem,
+                 void *stream);
+void launch_node_warp(const NodeParams &p, const NodeWarpParams &w, void *stream);
 void launch_step(const StepParams &p, int blocks, int threads, int smem, void *stream);
 void launch_node(const NodeParams &p, void *stream);
 void launch_hash(const StepParams &p, int blocks, int threads, int smem, void *stream,

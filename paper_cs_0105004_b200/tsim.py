@@ -13,7 +13,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_HERE, "libtsim.so")
 
-FLAG_FUSED, FLAG_HASH, FLAG_LINK_WORK, FLAG_GRAPH = 1, 2, 4, 8
+FLAG_FUSED, FLAG_HASH, FLAG_LINK_WORK, FLAG_GRAPH, FLAG_GENERAL = 1, 2, 4, 8, 16
 PENDING, ACTIVE, ARRIVED = 0, 1, 2
 
 
@@ -55,6 +55,7 @@ def load_library():
         "ts_read_vehicles": (ctypes.c_int, [P, P, P, P, P, P, P, P]),
         "ts_read_cells": (ctypes.c_int, [P, I32, P]),
         "ts_link_cells": (I32, [P, I32]),
+        "ts_read_raw": (ctypes.c_int, [P, I32, P, P, P]),
         "ts_state_hash": (ctypes.c_int, [P, ctypes.POINTER(ctypes.c_uint64)]),
         "ts_read_history": (ctypes.c_int, [P, I32, I32, P, P, P, P, P, P]),
         "ts_get_totals": (ctypes.c_int, [P, P]),
@@ -190,6 +191,17 @@ class Sim:
         out = np.zeros(int(self.lanes[link]) * n, np.int32)
         self._check(self.lib.ts_read_cells(self.h, int(link), out.ctypes.data))
         return out.reshape(int(self.lanes[link]), n)
+
+    def raw(self, link):
+        """raw per-lane codes and vid regions of a single-tile link"""
+        L = int(self.lanes[link])
+        wp = (self.n_cells(link) + 3) & ~3
+        code = np.zeros(L * wp, np.uint8)
+        vid = np.zeros(L * wp, np.int32)
+        pitch = ctypes.c_int32()
+        self._check(self.lib.ts_read_raw(self.h, int(link), code.ctypes.data, vid.ctypes.data,
+                                         ctypes.byref(pitch)))
+        return code.reshape(L, wp), vid.reshape(L, wp)
 
     def history(self, t_from, n):
         h = np.zeros(n, np.uint64)

@@ -15,6 +15,7 @@ tsim = pytest.importorskip("paper_cs_0105004_b200")
 
 FUSED = tsim.FLAG_FUSED | tsim.FLAG_HASH
 UNFUSED = tsim.FLAG_HASH
+GENERAL = tsim.FLAG_FUSED | tsim.FLAG_HASH | tsim.FLAG_GENERAL  # warp-per-tile kernels
 
 
 def assert_same_state(o, g, msg=""):
@@ -33,10 +34,15 @@ def run_parity(scn, steps, flags, full_every=1, t0=0, tile_cells=0, hash_every=1
     done = 0
     while done < steps:
         n = min(hash_every, steps - done)
-        o.step(n)
-        g.step(n)
+        t_from = o.t + 1
+        ohash = o.run_hashes(n)  # oracle: one step at a time
+        g.step(n)  # GPU: n steps in one call (fused lane change inside)
         done += n
         assert o.t == g.t
+        if flags & tsim.FLAG_HASH:
+            gh = g.history(t_from, n)["hash"]
+            bad = [t_from + i for i in range(n) if gh[i] != ohash[i]]
+            assert not bad, f"per-step hash differs at t={bad[:5]}"
         assert g.state_hash() == o.state_hash(), f"hash differs at t={o.t}"
         if full_every and (done % full_every == 0 or done == steps):
             assert_same_state(o, g, f"t={o.t}")
@@ -64,16 +70,28 @@ def test_ring_multi_tile(tile_cells):
     """segmented periodic link: halos and ghost moves across tile seams"""
     s = scenarios.ring(n_cells=3000, lanes=3, density=0.2, seed=5)
     run_parity(s, 150, FUSED, full_every=10, tile_cells=tile_cells)
+    run_parity(s, 150, FUSED, full_every=0, tile_cells=tile_cells, hash_every=30)
 
 
-@pytest.mark.parametrize("flags", [FUSED, UNFUSED])
+@pytest.mark.parametrize("flags", [FUSED, UNFUSED, GENERAL])
 def test_config1_full(flags):
-    """BASELINE.json configs[0] for all 600 steps"""
+    """BASELINE.json configs[0] for all 600 steps, one step per call"""
     s = scenarios.config("1")
     run_parity(s, 600, flags, full_every=20)
 
 
-@pytest.mark.parametrize("flags", [FUSED, UNFUSED])
+@pytest.mark.parametrize("flags", [FUSED, GENERAL])
+@pytest.mark.parametrize("chunk", [7, 50])
+def test_multistep_calls(flags, chunk):
+    """several steps per ts_step call: the lane change of step t+1 runs
+    inside the move kernel of step t; every per-step hash is checked"""
+    s = scenarios.grid_trips(rows=6, cols=6, n_veh=3000, depart_max=300, seed=8, name="grid6c")
+    run_parity(s, 400, flags, full_every=0, hash_every=chunk)
+    s = scenarios.big_grid(rows=20, cols=20, seed=4, name="grid20dense")
+    run_parity(s, 150, flags, full_every=0, hash_every=chunk)
+
+
+@pytest.mark.parametrize("flags", [FUSED, UNFUSED, GENERAL])
 def test_grid_with_departures(flags):
     """injection retries, conflicting entry cells, nodes at every step"""
     s = scenarios.grid_trips(rows=6, cols=6, n_veh=3000, depart_max=300, steps=500, seed=7,
@@ -89,12 +107,21 @@ def test_grid_segmented_links():
     run_parity(s, 400, UNFUSED, full_every=20, tile_cells=64)
 
 
-def test_portland_small():
+@pytest.mark.parametrize("flags", [FUSED, GENERAL])
+def test_portland_small(flags):
     s = scenarios.portland(n_nodes=600, n_edges=800, n_veh=8000, side_km=8.0, n_zones=64,
                            seed=2)
     # departures compressed into the first 300 s
     s.depart = (s.depart // 12).astype(np.int32)
-    run_parity(s, 400, FUSED, full_every=50)
+    run_parity(s, 400, flags, full_every=50)
+    run_parity(s, 400, flags, full_every=0, hash_every=40)
+
+
+def test_big_grid_dense():
+    """config-4a recipe (density 0.2, 4 lanes, 100-cell links, Manhattan
+    routes) on a 24x24 lattice: heavy lane changing and node traffic"""
+    s = scenarios.big_grid(rows=24, cols=24, seed=3, name="grid24dense")
+    run_parity(s, 200, FUSED, full_every=20)
 
 
 def test_t0_and_odd_start():
