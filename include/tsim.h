@@ -53,6 +53,7 @@ typedef struct {
   uint32_t flags;         /* TS_FLAG_* */
   int32_t device;         /* CUDA device ordinal */
   int32_t tile_cells;     /* max cells per lane in one tile (0 = default) */
+  int32_t group_cells;    /* max cells per warp in the row kernel (0 = default) */
 } ts_config;
 
 /* Create a simulation.  *out receives the handle (NULL on failure). */

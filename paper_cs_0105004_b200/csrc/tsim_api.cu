@@ -404,7 +404,7 @@ static void build_tiles(ts_sim *h) {
   h->groups.clear();
   h->rowmap.clear();
   if (h->rows_mode) {
-    const int kGroupCells = 8192;
+    const int kGroupCells = h->cfg.group_cells > 0 ? std::min(8192, h->cfg.group_cells) : 2048;
     size_t i = 0;
     int cmax = 128;
     while (i < h->tiles.size()) {

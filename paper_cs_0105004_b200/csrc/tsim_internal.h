@@ -84,7 +84,8 @@ struct GroupDesc {
 
 struct RowsLayout {
   int CMAX, NW, injcap;
-  int o_cin, o_cout, o_bin, o_bmid, o_bspec, o_bleave, o_ent, o_injx, o_injv, o_misc, bytes;
+  int o_cin, o_cout, o_bin, o_bmid, o_bspec, o_bleave, o_ent, o_injx, o_injv, o_misc, o_rows,
+      o_q, o_rowof, o_bfin, o_vpos, o_wp, bytes;
 };
 
 __host__ __device__ inline RowsLayout rows_layout(int cmax, int injcap) {
@@ -113,6 +114,19 @@ __host__ __device__ inline RowsLayout rows_layout(int cmax, int injcap) {
   o += 4 * injcap;
   l.o_misc = o;  // injection counter
   o += 16;
+  l.o_rows = o;  // per row: flat start, cells, link, lane|vmax<<8, lane gid, front vid
+  o += 4 * 12 * 32;
+  l.o_q = o;  // work queue: 64 entries + 64 vids
+  o += 4 * 128;
+  l.o_rowof = o;  // row index of every cell
+  o += l.CMAX;
+  l.o_bfin = o;  // final occupancy
+  o += 4 * l.NW;
+  l.o_vpos = o;  // rank -> position
+  o += 2 * l.CMAX;
+  l.o_wp = o;  // per-word exclusive popcount prefixes of three bitmaps
+  o += 3 * 2 * l.NW;
+  o = (o + 15) & ~15;
   l.bytes = (o + 127) & ~127;
   return l;
 }

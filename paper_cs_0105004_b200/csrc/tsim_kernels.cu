@@ -1,183 +1,28 @@
-// tsim_kernels.cu -- sm_100a kernels of the TRANSIMS CA time step
-// (Nagel & Rickert, §3-§4; readings R1-R22 in DESIGN.md §3).
+// tsim_kernels.cu -- general-path and node kernels of the TRANSIMS CA step
+// on sm_100a (Nagel & Rickert, §3-§4; readings R1-R22 in
+// DESIGN.md §3).  The fast row kernel lives in tsim_rows.cu.
 //
 // State: one int8 code per lane-cell (0xFF empty, else velocity | out-slot
-// << 3) and, per lane-row, the vids of its vehicles in cell order.  Gap
-// queries use an occupancy bitmap (one bit per lane-cell): the 5-cell
-// look-ahead / look-behind of PAPER.md:390-395 is a funnel-shifted 32-bit
-// window and a ctz.
+// << 3) and, per lane-row, the vids of its vehicles in cell order.
 //
-// Fast path (whole-link tiles, the HBM-bound configs):
-//   k_rows       one warp per group of <= 32 lane-rows, one thread per row:
-//                velocity update + move (H4/H5), node entrants, injection
-//                (H6), and -- fused -- the lane change of step t+1 (H1)
-//   k_node_warp  intersections (H3), one thread per incoming lane,
-//                __match_any_sync picks one winner per target lane
-// General path (tiles with 5-cell halos: long / periodic / split links):
-//   k_lc, k_step one warp per tile, vehicles enumerated by rank
-//   k_node       one thread per node
-//   k_hash       state hash
-#include <cuda_runtime.h>
-
-#include "tsim_internal.h"
+// General path (any tile, incl. tiles with 5-cell halos: long, periodic or
+// split links): one warp per tile; the tile's codes are staged in shared
+// memory, vehicles are enumerated by rank (prefix popcount).
+//   k_lc    S(t)  -> S1(t)   lane change (H1), node records + strips
+//   k_step  S1(t) -> S(t+1)  velocity update + move (H4/H5), entrants,
+//                            injection (H6), ghost moves across tile seams,
+//                            optionally the lane change of step t+1
+//   k_hash  state hash of S(t)
+// Intersections (H3):
+//   k_node_warp  one thread per incoming lane; __match_any_sync picks the
+//                winner of every target lane
+//   k_node       one thread per node (fallback for > 32 incoming lanes)
+#include "tsim_device.cuh"
 
 namespace tsim {
 
-#define FULL 0xffffffffu
-
-// ------------------------------------------------------------- Philox
-// Philox4x32-10 (Salmon et al., SC'11) with the curand round and Weyl
-// constants, counter (t, vid, 0, 0), key (k0, k1); only output word 0 is
-// used (reading R3).  The zero counter words fold away in round 1.
-__device__ __forceinline__ uint32_t philox_w0(uint32_t t, uint32_t vid, uint32_t k0,
-                                              uint32_t k1) {
-  uint32_t c0 = t, c1 = vid, c2 = 0u, c3 = 0u;
-#pragma unroll
-  for (int r = 0; r < 10; r++) {
-    if (r) {
-      k0 += 0x9E3779B9u;
-      k1 += 0xBB67AE85u;
-    }
-    const uint32_t lo0 = 0xD2511F53u * c0, hi0 = __umulhi(0xD2511F53u, c0);
-    const uint32_t lo1 = 0xCD9E8D57u * c2, hi1 = __umulhi(0xCD9E8D57u, c2);
-    const uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
-    c0 = n0;
-    c1 = lo1;
-    c2 = n2;
-    c3 = lo0;
-  }
-  return c0;
-}
-
-// NaSch velocity update (PAPER.md:330-335 rules (i)-(iii); R15):
-// accelerate, clamp to the gap, random slowdown (draw skipped when v2 = 0,
-// which cannot change the result).
-__device__ __forceinline__ int nasch_v3(int v, int Vk, int g, uint32_t t, uint32_t vid,
-                                        uint32_t k0, uint32_t k1, uint64_t p32) {
-  int v2 = min(min(v + 1, Vk), g);
-  if (v2 > 0 && (uint64_t)philox_w0(t, vid, k0, k1) < p32) v2 -= 1;
-  return v2;
-}
-
-// ---------------------------------------------------------- state hash
-__device__ __forceinline__ uint64_t fmix64(uint64_t z) {
-  z ^= z >> 33;
-  z *= 0xff51afd7ed558ccdULL;
-  z ^= z >> 33;
-  z *= 0xc4ceb9fe1a85ec53ULL;
-  z ^= z >> 33;
-  return z;
-}
-__device__ __forceinline__ uint64_t vmix(int vid, int link, int lane, int cell, int v) {
-  uint64_t a = (uint64_t)(uint32_t)vid | ((uint64_t)(uint32_t)link << 32);
-  uint64_t b = (uint64_t)(uint32_t)cell | ((uint64_t)(uint32_t)lane << 32) |
-               ((uint64_t)(uint32_t)v << 40);
-  return fmix64(fmix64(a) + b * 0x9E3779B97F4A7C15ULL);
-}
-
-// ------------------------------------------------------------ bit helpers
-// 4 code bytes -> 4 occupancy bits (occupied iff bit 7 clear)
-__device__ __forceinline__ uint32_t occ4(uint32_t w) {
-  return ((((~w) & 0x80808080u) >> 7) * 0x01020408u) >> 24;
-}
-
-// bits[0] and bits[nwords+1..] are zero pads so that windows never branch
-__device__ __forceinline__ void build_bits(const uint8_t *c, uint32_t *bits, int nwords,
-                                           int lane) {
-  for (int j = lane; j < nwords; j += 32) {
-    const uint4 *p = reinterpret_cast<const uint4 *>(c + 32 * j);
-    uint4 a = p[0], b = p[1];
-    bits[j + 1] = occ4(a.x) | occ4(a.y) << 4 | occ4(a.z) << 8 | occ4(a.w) << 12 |
-                  occ4(b.x) << 16 | occ4(b.y) << 20 | occ4(b.z) << 24 | occ4(b.w) << 28;
-  }
-  if (lane == 0) {
-    bits[0] = 0u;
-    bits[nwords + 1] = 0u;
-    bits[nwords + 2] = 0u;
-  }
-}
-
-__device__ __forceinline__ int occupied(const uint32_t *bits, int q) {
-  return (bits[(q >> 5) + 1] >> (q & 31)) & 1u;
-}
-__device__ __forceinline__ void set_bit(uint32_t *bits, int q) {
-  atomicOr(bits + (q >> 5) + 1, 1u << (q & 31));
-}
-// bit i = position s+i
-__device__ __forceinline__ uint32_t win_at(const uint32_t *bits, int s) {
-  return __funnelshift_r(bits[(s >> 5) + 1], bits[(s >> 5) + 2], s & 31);
-}
-// bit i = position q+1+i
-__device__ __forceinline__ uint32_t win_ahead(const uint32_t *bits, int q) {
-  return win_at(bits, q + 1);
-}
-// bit i = position q-1-i
-__device__ __forceinline__ uint32_t win_behind(const uint32_t *bits, int q) {
-  return __brev(win_at(bits, q - 32));
-}
-
-__device__ __forceinline__ int ctz32(uint32_t m) { return m ? __ffs(m) - 1 : 32; }
-__device__ __forceinline__ uint32_t low_mask(int n) {  // bits [0, n), n in [0, 32]
-  return n >= 32 ? FULL : ((1u << n) - 1u);
-}
-
-__device__ __forceinline__ uint32_t range_mask(int lo, int hi) {
-  lo = max(lo, 0);
-  hi = min(hi, 32);
-  if (lo >= hi) return 0u;
-  return low_mask(hi) & ~low_mask(lo);
-}
-
-// ------------------------------------------------------------- tile ctx
-struct Acc {
-  uint64_t hash, sumv;
-  uint32_t active, arr, inj, lc, work;
-};
-
-__device__ __forceinline__ void acc_place(Acc &a, bool hash, int vid, int link, int l, int x,
-                                          int v) {
-  a.active++;
-  a.sumv += v;
-  if (hash) a.hash += vmix(vid, link, l, x, v);
-}
-
-__device__ void flush_acc(const StepParams &P, Acc &a, int slot_t, unsigned long long *smem_red) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint64_t h = a.hash, sv = a.sumv;
-  uint32_t act = a.active, arr = a.arr, inj = a.inj, lc = a.lc;
-#pragma unroll
-  for (int o = 16; o; o >>= 1) {
-    h += __shfl_down_sync(FULL, h, o);
-    sv += __shfl_down_sync(FULL, sv, o);
-    act += __shfl_down_sync(FULL, act, o);
-    arr += __shfl_down_sync(FULL, arr, o);
-    inj += __shfl_down_sync(FULL, inj, o);
-    lc += __shfl_down_sync(FULL, lc, o);
-  }
-  if (lane == 0) {
-    unsigned long long *r = smem_red + warp * 8;
-    r[0] = h;
-    r[1] = act;
-    r[2] = arr;
-    r[3] = inj;
-    r[4] = lc;
-    r[5] = sv;
-  }
-  __syncthreads();
-  if (threadIdx.x < 6) {
-    unsigned long long s = 0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); w++) s += smem_red[w * 8 + threadIdx.x];
-    const int idx = threadIdx.x == 0 ? ST_HASH : threadIdx.x == 1 ? ST_ACTIVE
-                  : threadIdx.x == 2 ? ST_ARR : threadIdx.x == 3 ? ST_INJ
-                  : threadIdx.x == 4 ? ST_LC : ST_SUMV;
-    unsigned long long *st = P.stats + (size_t)(slot_t & (kHist - 1)) * ST_N;
-    if (s) atomicAdd(st + idx, s);
-  }
-  __syncthreads();
-}
-
 // ====================================================================
-// General path: one warp per tile (halo tiles, split links, any layout)
+// General path
 // ====================================================================
 struct TileCtx {
   TileDesc d;
@@ -218,9 +63,9 @@ __device__ __forceinline__ int lane_of(const TileCtx &T, int p) {
   return l;
 }
 
-// owned positions of word j
+// owned positions of word j; a word spans every row it intersects (rows can
+// be as short as 12 cells)
 __device__ __forceinline__ uint32_t owned_mask(const TileCtx &T, int j) {
-  // a word spans every row it intersects (rows can be as short as 12 cells)
   const int p0 = 32 * j;
   const int k1 = min(T.L - 1, (p0 + 31) / T.S);
   uint32_t m = 0u;
@@ -266,7 +111,7 @@ __device__ __forceinline__ int64_t vid_index(const TileCtx &T, int q, int r) {
   return T.d.off + (int64_t)lane_of(T, q) * T.Wp + T.vrow[r];
 }
 
-// stage S codes of the tile (+ 5-cell halos from strips) into smem
+// stage the codes of the tile (+ 5-cell halos from strips) into smem
 __device__ void load_codes(const TileCtx &T, const uint8_t *gcode, const Strip *strips,
                            const int32_t *halo_up, const int32_t *halo_dn, int lane) {
   const int nb = T.nwords * 32;
@@ -299,56 +144,12 @@ __device__ __forceinline__ void clear_codes(const TileCtx &T, uint8_t *c, int la
   for (int i = lane; i < T.nwords * 2; i += 32) c16[i] = e;
 }
 
-// cells ahead / behind inside the lane's valid range (R2)
+// valid range of lane l in the smem rows (R2)
 __device__ __forceinline__ int row_hi(const TileCtx &T, int l) {
   return l * T.S + T.HP + T.w + (T.has_dn ? kGmax : 0);
 }
 __device__ __forceinline__ int row_lo(const TileCtx &T, int l) {
   return l * T.S + T.HP - (T.has_up ? kGmax : 0);
-}
-
-// lane-change geometry shared by both paths: [lo, hi) is the valid range of
-// the lane-row in the flat bitmap (positions below lo are before the link
-// start and count as empty; the row ends at hi).
-__device__ __forceinline__ int ahead_in(const uint32_t *bits, int q, int hi) {
-  return min(min(ctz32(win_ahead(bits, q)), kGmax), hi - q - 1);
-}
-__device__ __forceinline__ int behind_in(const uint32_t *bits, int q, int lo) {
-  uint32_t r = win_behind(bits, q);
-  int nvalid = q - lo;
-  if (nvalid < 32) r &= low_mask(nvalid);
-  return min(ctz32(r), kGmax);
-}
-
-// O1 §LC decision (R4-R7).  q: position of the vehicle,
-// q2 = q + dir*stride the target cell; lanes l (own) and l2 (target) with
-// valid ranges [lo, hi) / [lo2, hi2); d = cells to the link end.
-__device__ __forceinline__ bool lc_rule(const uint32_t *bits, int q, int q2, int lo, int hi,
-                                        int lo2, int hi2, int code, int l, int l2, int L,
-                                        int dir, int d, uint32_t tt, bool periodic, int Vk,
-                                        int D) {
-  if (occupied(bits, q2)) return false;
-  const int v = code & 7, slot = code >> 3;
-  int set = 0;  // 0 all lanes, 1 {0} (right turn), 2 {L-1} (left turn)
-  if (slot != kSlotFinal && !periodic) {
-    int tty = (tt >> (2 * slot)) & 3;
-    set = tty == 0 ? 0 : (tty == 2 ? 1 : 2);
-  }
-  const bool own_ok = set == 0 || (set == 1 ? l == 0 : l == L - 1);
-  if (!own_ok) {  // turn-motivated, only towards the allowed lane
-    const bool toward = (set == 1 && dir < 0) || (set == 2 && dir > 0);
-    if (!toward) return false;
-    int rf = min(v + 1, Vk), rb = Vk;
-    if (d < D) {  // R6: desperation over the last D cells
-      rf = (rf * d) / D;
-      rb = (rb * d) / D;
-    }
-    return ahead_in(bits, q2, hi2) >= rf && behind_in(bits, q2, lo2) >= rb;
-  }
-  const bool tgt_ok = set == 0 || (set == 1 ? l2 == 0 : l2 == L - 1);
-  if (!tgt_ok) return false;
-  const int g = ahead_in(bits, q, hi);  // R5: the other lane is faster
-  return g < v + 1 && ahead_in(bits, q2, hi2) > g && behind_in(bits, q2, lo2) >= Vk;
 }
 
 __device__ int lc_decide(const StepParams &P, const TileCtx &T, const uint8_t *c,
@@ -481,36 +282,9 @@ __device__ __forceinline__ void move_one(const StepParams &P, TileCtx &T, Acc &a
       P.arr_time[vid] = P.t + 1;
       acc.arr++;
     }
-    // else: node crossing; k_node placed it on the next link
+    // else: node crossing; the node kernel placed it on the next link
   }
   if (!ghost) acc.work++;
-}
-
-// injection from parking (R13) by one thread: walks the
-// link's pending list in (departure, vid) order; cell_free / place_fn act
-// on lane 0 of the tile.
-template <class FreeFn, class PlaceFn>
-__device__ __forceinline__ void inject_link(const StepParams &P, int k, int a, int w, bool first,
-                                            FreeFn cell_free, PlaceFn place_fn) {
-  const int e = P.pend_off[k + 1];
-  int h = P.pend_head[k];
-  const int tn = P.t + 1;
-  for (int i = h; i < e; i++) {
-    const int vid = P.pend_list[i];
-    if (P.dep[vid] > tn) break;
-    if (P.inj_time[vid] <= P.t) continue;
-    const int ec = P.entry[vid];
-    if (ec < a || ec >= a + w) continue;
-    if (!cell_free(ec - a)) continue;  // retry next step
-    const int64_t ro = P.route_off[vid];
-    const int slot0 = (P.route_off[vid + 1] - ro > 1) ? P.out_pos[P.route[ro + 1]] : kSlotFinal;
-    P.inj_time[vid] = tn;
-    place_fn(ec - a, (uint8_t)(slot0 << 3), vid);
-  }
-  if (first) {
-    while (h < e && P.inj_time[P.pend_list[h]] <= tn) h++;
-    P.pend_head[k] = h;
-  }
 }
 
 // ------------------------------------------------------------- k_lc
@@ -595,7 +369,7 @@ __global__ void __launch_bounds__(256) k_step(const StepParams P) {
             move_one(P, T, acc, q, P.strip_in[P.halo_up[T.d.strip] + l].tail_vid[j], true, Vk);
         }
       }
-      // entrants granted by k_node (H3/H5): at most one per lane
+      // entrants granted by the node kernel (H3/H5): at most one per lane
       if ((T.d.flags & kFirst) && lane < T.L) {
         uint64_t rec = P.entr[T.d.lane_gid + lane];
         if ((uint32_t)(rec >> 43) == ((uint32_t)(P.t + 1) & 0x1FFFFFu)) {
@@ -642,289 +416,6 @@ __global__ void __launch_bounds__(256) k_step(const StepParams P) {
   if (P.mode & kModeLC) flush_acc(P, acc_next, P.t + 2, red);
 }
 
-// ====================================================================
-// Fast path: k_rows -- one warp per group of whole-link tiles, one thread
-// per lane-row.  All vehicles of a row are processed by its thread in cell
-// order; the in-lane order is preserved by the move, so the row's vid list
-// is streamed in and out with 128-bit accesses.
-// ====================================================================
-struct VidReader {  // sequential 128-bit reader of a row's vid list
-  const int32_t *p;
-  int i;
-  uint4 buf;
-  __device__ __forceinline__ int next() {
-    if ((i & 3) == 0) buf = __ldg(reinterpret_cast<const uint4 *>(p + i));
-    const int k = i & 3;
-    i++;
-    return k == 0 ? (int)buf.x : k == 1 ? (int)buf.y : k == 2 ? (int)buf.z : (int)buf.w;
-  }
-};
-
-struct VidWriter {  // sequential 128-bit writer of a row's vid list
-  int32_t *p;
-  int j;
-  uint4 buf;
-  __device__ __forceinline__ void put(int v) {
-    const int k = j & 3;
-    if (k == 0) buf.x = v;
-    else if (k == 1) buf.y = v;
-    else if (k == 2) buf.z = v;
-    else buf.w = v;
-    j++;
-    if (k == 3) __stcs(reinterpret_cast<uint4 *>(p + j - 4), buf);
-  }
-  __device__ __forceinline__ void flush() {
-    const int k = j & 3, b = j & ~3;
-    if (k > 0) p[b] = (int)buf.x;
-    if (k > 1) p[b + 1] = (int)buf.y;
-    if (k > 2) p[b + 2] = (int)buf.z;
-  }
-};
-
-// bits of row cells [32*wj, 32*wj+32) (row starting at flat position s,
-// w cells)
-__device__ __forceinline__ uint32_t row_word(const uint32_t *bits, int s, int w, int wj) {
-  return win_at(bits, s + 32 * wj) & low_mask(w - 32 * wj);
-}
-
-// vid of an entrant / injected vehicle of row `row` at cell x
-__device__ __forceinline__ int special_vid(const int32_t *ent, const int32_t *injx,
-                                           const int32_t *injv, int ninj, int row, int x) {
-  if (ent[32 + row] == x) return ent[row];
-  const int key = (row << 16) | x;
-  for (int k = 0; k < ninj; k++)
-    if (injx[k] == key) return injv[k];
-  return -1;
-}
-
-__global__ void __launch_bounds__(128) k_rows(const StepParams P, const RowsParams R) {
-  extern __shared__ __align__(16) uint8_t smem[];
-  __shared__ unsigned long long red[4 * 8];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int nwarps_total = gridDim.x * (blockDim.x >> 5);
-  const RowsLayout &Y = R.lay;
-  uint8_t *base = smem + warp * Y.bytes;
-  uint8_t *cin = base + Y.o_cin, *cout = base + Y.o_cout;
-  uint32_t *bin = reinterpret_cast<uint32_t *>(base + Y.o_bin);
-  uint32_t *bmid = reinterpret_cast<uint32_t *>(base + Y.o_bmid);
-  uint32_t *bspec = reinterpret_cast<uint32_t *>(base + Y.o_bspec);
-  uint32_t *blv = reinterpret_cast<uint32_t *>(base + Y.o_bleave);
-  int32_t *ent = reinterpret_cast<int32_t *>(base + Y.o_ent);
-  int32_t *injx = reinterpret_cast<int32_t *>(base + Y.o_injx);
-  int32_t *injv = reinterpret_cast<int32_t *>(base + Y.o_injv);
-  int32_t *misc = reinterpret_cast<int32_t *>(base + Y.o_misc);
-  const bool hash = (P.mode & kModeHash) != 0;
-  const bool lc_next = (P.mode & kModeLC) != 0;
-  const int dir = ((P.t + 1) & 1) ? -1 : +1;  // R4, lane change of step t+1
-  Acc acc = {};
-  Acc acc_next = {};
-  for (int g = blockIdx.x * (blockDim.x >> 5) + warp; g < R.ngroups; g += nwarps_total) {
-    const GroupDesc G = R.groups[g];
-    const int64_t off0 = P.tiles[G.t0].off;
-    const int nw = (G.bytes + 31) >> 5;
-    // ---- stage the group's codes, clear the work bitmaps
-    {
-      const uint4 *src = reinterpret_cast<const uint4 *>(P.code_in + off0);
-      uint4 *dst = reinterpret_cast<uint4 *>(cin);
-      uint4 *dco = reinterpret_cast<uint4 *>(cout);
-      const uint4 e = make_uint4(FULL, FULL, FULL, FULL);
-      const int n16 = G.bytes >> 4;
-      for (int i = lane; i < 2 * nw; i += 32) {
-        dst[i] = i < n16 ? __ldcs(src + i) : e;
-        dco[i] = e;
-      }
-      for (int i = lane; i < nw + 3; i += 32) {
-        bmid[i] = 0u;
-        bspec[i] = 0u;
-        blv[i] = 0u;
-      }
-      if (lane == 0) misc[0] = 0;
-      ent[32 + lane] = -1;  // entrant cell per row
-    }
-    __syncwarp();
-    build_bits(cin, bin, nw, lane);
-    __syncwarp();
-    // ---- this thread's row
-    const bool active = lane < G.nrows;
-    TileDesc d;
-    int l = 0, s = 0, Wp = 4, Vk = 1, nrw = 0;
-    if (active) {
-      const int rm = R.rowmap[(size_t)g * 32 + lane];
-      l = rm & 7;
-      d = P.tiles[G.t0 + (rm >> 3)];
-      Wp = row_pitch(d.w);
-      s = (int)(d.off - off0) + l * Wp;
-      Vk = P.vmax_link[d.link];
-      nrw = (d.w + 31) >> 5;
-    }
-    const int64_t rbase = active ? d.off + (int64_t)l * Wp : 0;
-    const uint32_t work0 = acc.work;
-    // ---- velocity update + move (H4/H5)
-    if (active && (P.mode & kModeMove)) {
-      VidReader rd{P.vid_in + rbase, 0, make_uint4(0, 0, 0, 0)};
-      for (int wj = 0; wj < nrw; wj++) {
-        uint32_t m = row_word(bin, s, d.w, wj);
-        while (m) {
-          const int x = 32 * wj + __ffs(m) - 1;
-          m &= m - 1u;
-          const int q = s + x;
-          const int code = cin[q];
-          const int v = code & 7, slot = code >> 3;
-          const int vid = rd.next();
-          const int lim = min(kGmax, d.w - 1 - x);
-          const uint32_t ma = win_ahead(bin, q) & low_mask(lim);
-          int gp;
-          if (ma) gp = __ffs(ma) - 1;
-          else if (lim == kGmax || slot == kSlotFinal) gp = kGmax;  // R12 open end
-          else gp = min(kGmax, lim + (int)P.ext[d.lane_gid + l]);   // node grant
-          const int v3 = nasch_v3(v, Vk, gp, (uint32_t)P.t, (uint32_t)vid, P.k0, P.k1, P.p32);
-          const int y = x + v3;
-          if (y < d.w) {
-            cout[s + y] = (uint8_t)(v3 | (slot << 3));
-            set_bit(bmid, s + y);
-            acc_place(acc, hash, vid, d.link, l, y, v3);
-          } else if (slot == kSlotFinal) {  // exit to parking
-            P.arr_time[vid] = P.t + 1;
-            acc.arr++;
-          }  // else: crossed the node; k_node_warp placed it
-          acc.work++;
-        }
-      }
-      // entrant granted by the node kernel
-      if (d.flags & kFirst) {
-        const uint64_t rec = P.entr[d.lane_gid + l];
-        if ((uint32_t)(rec >> 43) == ((uint32_t)(P.t + 1) & 0x1FFFFFu)) {
-          const int vid = (int)(uint32_t)rec;
-          const uint8_t code = (uint8_t)(rec >> 32);
-          const int y = (int)((rec >> 40) & 7);
-          cout[s + y] = code;
-          set_bit(bmid, s + y);
-          set_bit(bspec, s + y);
-          ent[lane] = vid;
-          ent[32 + lane] = y;
-          acc_place(acc, hash, vid, d.link, l, y, code & 7);
-        }
-      }
-      if ((P.mode & kModeInject) && l == 0 && P.pend_off[d.link + 1] > P.pend_head[d.link]) {
-        const int row = lane;
-        inject_link(
-            P, d.link, 0, d.w, true, [&](int x) { return cout[s + x] == kEmpty; },
-            [&](int x, uint8_t code, int vid) {
-              cout[s + x] = code;
-              set_bit(bmid, s + x);
-              set_bit(bspec, s + x);
-              const int k = atomicAdd(misc, 1);
-              injx[k] = (row << 16) | x;
-              injv[k] = vid;
-              acc.inj++;
-              acc_place(acc, hash, vid, d.link, 0, x, 0);
-            });
-      }
-    }
-    __syncwarp();
-    // ---- lane change of step t+1 on the post-move state (H1, fused)
-    const int l2 = l + dir;
-    if (active && lc_next && l2 >= 0 && l2 < d.L) {
-      const uint32_t tt = P.tt_link[d.link];
-      const int s2 = s + dir * Wp;
-      int nch = 0;
-      for (int wj = 0; wj < nrw; wj++) {
-        uint32_t m = row_word(bmid, s, d.w, wj);
-        while (m) {
-          const int x = 32 * wj + __ffs(m) - 1;
-          m &= m - 1u;
-          if (lc_rule(bmid, s + x, s2 + x, s, s + d.w, s2, s2 + d.w, cout[s + x], l, l2, d.L, dir,
-                      d.w - 1 - x, tt, false, Vk, P.D)) {
-            set_bit(blv, s + x);
-            nch++;
-          }
-        }
-      }
-      acc_next.lc += nch;
-    }
-    // final codes are assembled in cin
-    for (int i = lane; i < 2 * nw; i += 32)
-      reinterpret_cast<uint4 *>(cin)[i] = make_uint4(FULL, FULL, FULL, FULL);
-    __syncwarp();
-    // ---- final state of the row: own post-move vehicles that stay, plus
-    // arrivals from the row l - dir; vid list streamed out in cell order
-    if (active) {
-      const int ls = l - dir;  // source row of arrivals (thread lane - dir)
-      const bool has_src = lc_next && ls >= 0 && ls < d.L;
-      const int ss = s - dir * Wp;
-      VidReader rd{P.vid_in + rbase, 0, make_uint4(0, 0, 0, 0)};
-      VidWriter wr{P.vid_out + rbase, 0, make_uint4(0, 0, 0, 0)};
-      uint32_t tocc = 0, hocc = 0;
-      int fx = -1, fvid = 0, fcode = 0;
-      for (int wj = 0; wj < nrw; wj++) {
-        const uint32_t mid = row_word(bmid, s, d.w, wj);
-        const uint32_t lv = lc_next ? row_word(blv, s, d.w, wj) : 0u;
-        const uint32_t arr = has_src ? row_word(blv, ss, d.w, wj) : 0u;
-        const uint32_t sp = row_word(bspec, s, d.w, wj);
-        uint32_t u = mid | arr;
-        while (u) {
-          const int b = __ffs(u) - 1;
-          u &= u - 1u;
-          const uint32_t bit = 1u << b;
-          const int x = 32 * wj + b;
-          int vid, code;
-          if (mid & bit) {
-            vid = (sp & bit) ? special_vid(ent, injx, injv, misc[0], lane, x) : rd.next();
-            if (lv & bit) continue;  // changed to row l + dir
-            code = cout[s + x];
-          } else {  // arrived from row ls at the same cell
-            code = cout[ss + x];
-            if (occupied(bspec, ss + x)) {
-              vid = special_vid(ent, injx, injv, misc[0], lane - dir, x);
-            } else {  // rank among the source row's input-derived vehicles
-              int idx = 0;
-              for (int wk = 0; wk <= (x >> 5); wk++) {
-                uint32_t mm = row_word(bmid, ss, d.w, wk) & ~row_word(bspec, ss, d.w, wk);
-                if (wk == (x >> 5)) mm &= low_mask(x & 31);
-                idx += __popc(mm);
-              }
-              vid = P.vid_in[d.off + (int64_t)ls * Wp + idx];
-            }
-          }
-          wr.put(vid);
-          cin[s + x] = (uint8_t)code;
-          if (x >= d.w - kGmax) {
-            tocc |= 1u << (d.w - 1 - x);
-            fx = x;
-            fvid = vid;
-            fcode = code;
-          }
-          if (x < kGmax) hocc |= 1u << x;
-        }
-      }
-      wr.flush();
-      if (lc_next) {  // the output is S1(t+1): node records for k_node_warp
-        if (d.flags & kLast) {
-          uint64_t rec = (uint64_t)tocc << 44;
-          if (fx >= 0)
-            rec |= (uint64_t)(uint32_t)fvid | ((uint64_t)fcode << 32) |
-                   ((uint64_t)(d.w - 1 - fx) << 40) | (1ull << 43);
-          P.tail_rec[d.lane_gid + l] = rec;
-        }
-        if (d.flags & kFirst) P.head_occ[d.lane_gid + l] = (uint8_t)hocc;
-      }
-    }
-    __syncwarp();
-    {
-      uint4 *dst = reinterpret_cast<uint4 *>(P.code_out + off0);
-      const uint4 *src = reinterpret_cast<const uint4 *>(cin);
-      for (int i = lane; i < (G.bytes >> 4); i += 32) __stcs(dst + i, src[i]);
-    }
-    __syncwarp();
-    if ((P.mode & kModeWork) && P.link_work && active) {  // load statistics
-      const uint32_t wk = acc.work - work0;
-      if (wk) atomicAdd(P.link_work + d.link, (unsigned long long)wk);
-    }
-  }
-  flush_acc(P, acc, P.t + 1, red);
-  if (lc_next) flush_acc(P, acc_next, P.t + 2, red);
-}
-
 // ------------------------------------------------------------- k_hash
 __global__ void __launch_bounds__(256) k_hash(const StepParams P, unsigned long long *out) {
   extern __shared__ __align__(16) uint8_t smem[];
@@ -959,13 +450,14 @@ __global__ void __launch_bounds__(256) k_hash(const StepParams P, unsigned long 
   }
 }
 
-// ------------------------------------------------------------- nodes
-// O1 §Node (R8-R10).  Candidates are the front vehicles
-// of the incoming lanes that want to pass the stop line (d < min(v+1, V));
-// majors first, minors only if the last G cells of every major lane are
-// empty; one winner per target lane in (class, link, lane) order; the
-// winner is granted the entry space E and, if its velocity takes it past
-// the stop line, is written as the entrant of the target lane.
+// ====================================================================
+// Intersections: O1 §Node (R8-R10).  Candidates are the
+// front vehicles of the incoming lanes that want to pass the stop line
+// (d < min(v+1, V)); majors first, minors only if the last G cells of every
+// major lane are empty; one winner per target lane in (class, link, lane)
+// order; the winner is granted the entry space E and, if its velocity takes
+// it past the stop line, is written as the entrant of the target lane.
+// ====================================================================
 struct Cand {
   bool cand;
   int tgt, k2, l2, d, v, vid;
@@ -1026,7 +518,7 @@ __device__ __forceinline__ void node_flush(const NodeParams &P, uint32_t crossin
 
 // one thread per incoming lane; the lanes of a node are consecutive threads
 // in priority order, so the winner of a target lane is the lowest eligible
-// thread with that target (__match_any_sync)
+// thread with that target
 __global__ void __launch_bounds__(256) k_node_warp(const NodeParams P, const NodeWarpParams W) {
   __shared__ unsigned long long red[8];
   const int lane = threadIdx.x & 31;
@@ -1108,10 +600,6 @@ void launch_lc(const StepParams &p, int blocks, int threads, int smem, void *str
 void launch_step(const StepParams &p, int blocks, int threads, int smem, void *stream) {
   k_step<<<blocks, threads, smem, (cudaStream_t)stream>>>(p);
 }
-void launch_rows(const StepParams &p, const RowsParams &r, int blocks, int threads, int smem,
-                 void *stream) {
-  k_rows<<<blocks, threads, smem, (cudaStream_t)stream>>>(p, r);
-}
 void launch_node(const NodeParams &p, void *stream) {
   if (p.nnodes <= 0) return;
   k_node<<<(p.nnodes + 127) / 128, 128, 0, (cudaStream_t)stream>>>(p);
@@ -1133,18 +621,10 @@ cudaError_t set_smem_attrs(int bytes) {
   if (e != cudaSuccess) return e;
   return cudaFuncSetAttribute(k_hash, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
 }
-cudaError_t set_rows_smem(int bytes) {
-  return cudaFuncSetAttribute(k_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-}
 
 int occupancy_blocks(int threads, int smem) {
   int nb = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_step, threads, smem);
-  return nb;
-}
-int occupancy_rows(int threads, int smem) {
-  int nb = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_rows, threads, smem);
   return nb;
 }
 

@@ -25,7 +25,7 @@ class Config(ctypes.Structure):
     _fields_ = [("p_slow", ctypes.c_double), ("seed", ctypes.c_uint64),
                 ("gap_accept_G", ctypes.c_int32), ("desperation_D", ctypes.c_int32),
                 ("flags", ctypes.c_uint32), ("device", ctypes.c_int32),
-                ("tile_cells", ctypes.c_int32)]
+                ("tile_cells", ctypes.c_int32), ("group_cells", ctypes.c_int32)]
 
 
 _lib = None
@@ -104,10 +104,10 @@ class Sim:
     """One simulation handle on one GPU."""
 
     def __init__(self, p_slow=0.2, seed=1, gap_G=5, desp_D=10, flags=FLAG_FUSED | FLAG_HASH,
-                 device=0, tile_cells=0):
+                 device=0, tile_cells=0, group_cells=0):
         self.lib = load_library()
         cfg = Config(float(p_slow), int(seed), int(gap_G), int(desp_D), int(flags), int(device),
-                     int(tile_cells))
+                     int(tile_cells), int(group_cells))
         h = ctypes.c_void_p()
         rc = self.lib.ts_create(ctypes.byref(cfg), ctypes.byref(h))
         if rc:
