@@ -63,6 +63,10 @@ struct ts_sim {
   int threads = 256, blocks = 1, smem = 0;
   bool fused = false;
   bool rows_mode = false, node_warp = false;
+  std::vector<int32_t> pw;  // row mode: plane word offset per tile
+  int64_t plane_words = 0;
+  uint32_t *d_planes[2] = {nullptr, nullptr};
+  int32_t *d_pw = nullptr;
   std::vector<GroupDesc> groups;
   std::vector<uint8_t> rowmap;
   int rows_cmax = 0, rows_threads = 128, rows_blocks = 1, rows_smem = 0;
@@ -398,38 +402,51 @@ static void build_tiles(ts_sim *h) {
   for (const TileDesc &d : h->tiles) nc_max = std::max(nc_max, (int)d.L * tile_stride(d.w, d.flags));
   h->lay = warp_layout(nc_max);
   h->fused = (h->cfg.flags & TS_FLAG_FUSED) && h->nstrips == 0;
+  h->rows_mode = h->nstrips == 0 && !(h->cfg.flags & TS_FLAG_GENERAL);
   // row groups for k_rows: consecutive whole-link tiles, <= 32 rows and
   // <= kGroupCells cells per warp
   h->rows_mode = h->nstrips == 0 && !(h->cfg.flags & TS_FLAG_GENERAL);
   h->groups.clear();
   h->rowmap.clear();
+  h->pw.clear();
   if (h->rows_mode) {
-    const int kGroupCells = h->cfg.group_cells > 0 ? std::min(8192, h->cfg.group_cells) : 2048;
+    // bit-plane offsets of every tile (4 planes, 16-byte aligned)
+    int64_t pwo = 0;
+    for (const TileDesc &d : h->tiles) {
+      h->pw.push_back((int32_t)pwo);
+      pwo += tile_pwords(d.w, d.L);
+    }
+    h->plane_words = pwo + 4;
+    const int kGroupWords = (h->cfg.group_cells > 0 ? std::min(16384, h->cfg.group_cells) : 2048) / 32;
     size_t i = 0;
-    int cmax = 128;
+    int ngmax = 4;
     while (i < h->tiles.size()) {
       GroupDesc g{};
       g.t0 = (int32_t)i;
-      int rows = 0;
-      int64_t cells = 0;
+      int rows = 0, words = 0;
       while (i < h->tiles.size()) {
         const TileDesc &d = h->tiles[i];
-        const int64_t c = tile_cells_padded(d.w, d.L);
-        if (g.ntiles > 0 && (rows + d.L > 32 || cells + c > kGroupCells)) break;
+        const int c = tile_words(d.w, d.L);
+        if (g.ntiles > 0 && (rows + d.L > 32 || words + c > kGroupWords)) break;
         for (int l = 0; l < d.L; l++) h->rowmap.push_back((uint8_t)((g.ntiles << 3) | l));
         rows += d.L;
-        cells += c;
+        words += c;
         g.ntiles++;
         i++;
       }
       for (int r = rows; r < 32; r++) h->rowmap.push_back(0);
       g.nrows = (int16_t)rows;
-      g.bytes = (int32_t)cells;
-      cmax = std::max(cmax, (int)cells);
+      g.nwg = words;
+      ngmax = std::max(ngmax, words);
       h->groups.push_back(g);
     }
-    h->rows_cmax = cmax;
+    h->rows_cmax = ngmax;  // max words per plane in a group
   }
+}
+
+// ----- row-mode state <-> host (codes are velocity | out-slot << 3)
+static int64_t vid_row(const ts_sim *h, const TileDesc &d, int l) {
+  return d.off + (int64_t)l * row_pitch(d.w);
 }
 
 // injection capacity of each row group: at most min(pending, cells) per link
@@ -565,6 +582,18 @@ static NodeParams node_params(ts_sim *h, int t) {
   return N;
 }
 
+static RowsParams rows_params(ts_sim *h) {
+  RowsParams r{};
+  r.groups = h->d_groups;
+  r.rowmap = h->d_rowmap;
+  r.pw = h->d_pw;
+  r.planes_in = h->d_planes[h->cur];
+  r.planes_out = h->d_planes[h->cur ^ 1];
+  r.ngroups = (int32_t)h->groups.size();
+  r.lay = h->rlay;
+  return r;
+}
+
 static int base_mode(const ts_sim *h) {
   int m = kModeMove | kModeInject;
   if (h->cfg.flags & TS_FLAG_HASH) m |= kModeHash;
@@ -618,6 +647,39 @@ int ts_init(ts_sim *h, int32_t t0) {
   }
   std::vector<int32_t>().swap(cellvid);
   h->n_placed = (int64_t)h->pl_vid.size();
+  std::vector<uint32_t> planes;
+  if (h->rows_mode) {
+    // row mode: bit-planes O, V0, V1, V2 per tile; list entries vid | slot << 27
+    if (h->nv > (int32_t)kVidMask) return fail(h, TS_EINVAL, "too many vehicles for row mode");
+    planes.assign(h->plane_words, 0u);
+    for (size_t ti = 0; ti < h->tiles.size(); ti++) {
+      const TileDesc &d = h->tiles[ti];
+      const int Wp = row_pitch(d.w), nwt = tile_words(d.w, d.L);
+      uint32_t *pl = planes.data() + h->pw[ti];
+      for (int l = 0; l < d.L; l++) {
+        int64_t r = d.off + (int64_t)l * Wp;
+        for (int x = 0; x < d.w; x++) {
+          const uint8_t c = code[d.off + (int64_t)l * Wp + x];
+          if (c == kEmpty) continue;
+          const int b = l * d.w + x;
+          pl[b >> 5] |= 1u << (b & 31);
+          for (int k = 0; k < 3; k++)
+            if ((c >> k) & 1) pl[(k + 1) * nwt + (b >> 5)] |= 1u << (b & 31);
+          // allowed-lane class (R7): 0 all, 1 curb (right turn), 2 median (left)
+          const int slot = c >> 3;
+          int cls = 0;
+          if (slot != kSlotFinal) {
+            const int tty = (h->tt[d.link] >> (2 * slot)) & 3;
+            cls = tty == 0 ? 0 : (tty == 2 ? 1 : 2);
+          }
+          for (int k = 0; k < 2; k++)
+            if ((cls >> k) & 1) pl[(k + 4) * nwt + (b >> 5)] |= 1u << (b & 31);
+          vids[r] = (int32_t)((uint32_t)vids[r] | ((uint32_t)(c >> 3) << kSlotShift));
+          r++;
+        }
+      }
+    }
+  }
   // pending lists per first link in (departure, vid) order (R13)
   std::vector<int32_t> pend_off(h->nl + 1, 0), pend_list;
   for (int f = 0; f < h->nv; f++)
@@ -643,11 +705,18 @@ int ts_init(ts_sim *h, int32_t t0) {
   int rc;
   if ((rc = upload(h, &h->d_tiles, h->tiles))) return rc;
   for (int b = 0; b < 2; b++) {
-    if ((rc = dalloc(h, &h->d_code[b], h->total_cells, 0xFF))) return rc;
+    if ((rc = dalloc(h, &h->d_code[b], h->rows_mode ? 16 : h->total_cells, 0xFF))) return rc;
     if ((rc = dalloc(h, &h->d_vid[b], h->total_cells, 0xFF))) return rc;
     if ((rc = dalloc(h, &h->d_strip[b], std::max(1, h->nstrips), 0xFF))) return rc;
+    if (h->rows_mode && (rc = dalloc(h, &h->d_planes[b], h->plane_words, 0))) return rc;
   }
-  CK(h, cudaMemcpyAsync(h->d_code[0], code.data(), code.size(), cudaMemcpyHostToDevice, h->stream));
+  if (h->rows_mode) {
+    if ((rc = upload(h, &h->d_pw, h->pw))) return rc;
+    CK(h, cudaMemcpyAsync(h->d_planes[0], planes.data(), planes.size() * 4, cudaMemcpyHostToDevice,
+                          h->stream));
+  } else {
+    CK(h, cudaMemcpyAsync(h->d_code[0], code.data(), code.size(), cudaMemcpyHostToDevice, h->stream));
+  }
   CK(h, cudaMemcpyAsync(h->d_vid[0], vids.data(), vids.size() * 4, cudaMemcpyHostToDevice, h->stream));
   if ((rc = upload(h, &h->d_halo_up, h->halo_up))) return rc;
   if ((rc = upload(h, &h->d_halo_dn, h->halo_dn))) return rc;
@@ -721,7 +790,10 @@ int ts_init(ts_sim *h, int32_t t0) {
   if (zero_stats(h, t0, 1)) return TS_EINTERNAL;
   int mode = kModeInject | (base_mode(h) & kModeHash);
   StepParams P = step_params(h, t0 - 1, mode);
-  launch_step(P, h->blocks, h->threads, h->smem, h->stream);
+  if (h->rows_mode)
+    launch_rows(P, rows_params(h), h->rows_blocks, h->rows_threads, h->rows_smem, h->stream);
+  else
+    launch_step(P, h->blocks, h->threads, h->smem, h->stream);
   CK(h, cudaGetLastError());
   h->cur ^= 1;
   h->t = t0;
@@ -756,15 +828,19 @@ static int enqueue_steps(ts_sim *h, int32_t n) {
   }
   CK(h, cudaEventRecord(h->ev0, h->stream));
   const int t = h->t;
-  if (h->fused) {
-    launch_lc(step_params(h, t, 0), h->blocks, h->threads, h->smem, h->stream);
+  // lane change of step t on S(t) (general: k_lc; row mode: k_rows in
+  // lane-change-only mode)
+  auto lane_change = [&](int ts) {
+    if (h->rows_mode)
+      launch_rows(step_params(h, ts, kModeLC), rows_params(h), h->rows_blocks, h->rows_threads,
+                  h->rows_smem, h->stream);
+    else
+      launch_lc(step_params(h, ts, 0), h->blocks, h->threads, h->smem, h->stream);
     h->cur ^= 1;
-  }
+  };
+  if (h->fused) lane_change(t);
   for (int i = 0; i < n; i++) {
-    if (!h->fused) {
-      launch_lc(step_params(h, t + i, 0), h->blocks, h->threads, h->smem, h->stream);
-      h->cur ^= 1;
-    }
+    if (!h->fused) lane_change(t + i);
     if (h->node_warp)
       launch_node_warp(node_params(h, t + i), NodeWarpParams{h->d_nlanes, h->d_chunk_off, h->nchunks},
                        h->stream);
@@ -774,9 +850,8 @@ static int enqueue_steps(ts_sim *h, int32_t n) {
     if (h->fused && i < n - 1) m |= kModeLC;
     if (h->timing) CK(h, cudaEventRecord(h->mv_ev[2 * i], h->stream));
     if (h->rows_mode)
-      launch_rows(step_params(h, t + i, m),
-                  RowsParams{h->d_groups, h->d_rowmap, (int32_t)h->groups.size(), h->rlay},
-                  h->rows_blocks, h->rows_threads, h->rows_smem, h->stream);
+      launch_rows(step_params(h, t + i, m), rows_params(h), h->rows_blocks, h->rows_threads,
+                  h->rows_smem, h->stream);
     else
       launch_step(step_params(h, t + i, m), h->blocks, h->threads, h->smem, h->stream);
     if (h->timing) CK(h, cudaEventRecord(h->mv_ev[2 * i + 1], h->stream));
@@ -849,15 +924,53 @@ int ts_sync(ts_sim *h) {
 int32_t ts_time(const ts_sim *h) { return h ? h->t : -1; }
 
 // ------------------------------------------------------------------ readers
+// State of tiles [t0, t1) in the byte-code layout (codes at off + l*Wp + x,
+// per-row vid lists) starting at element 0 = cell off(t0).  Row mode:
+// decoded from the bit-planes and the vid | slot << 27 list entries.
+static int download_tiles(ts_sim *h, int t0, int t1, std::vector<uint8_t> &code,
+                          std::vector<int32_t> &vids) {
+  const int64_t c0 = h->tiles[t0].off;
+  const int64_t c1 = t1 < (int)h->tiles.size() ? h->tiles[t1].off : h->total_cells;
+  code.assign(c1 - c0, kEmpty);
+  vids.assign(c1 - c0, -1);
+  CK(h, cudaMemcpy(vids.data(), h->d_vid[h->cur] + c0, (c1 - c0) * 4, cudaMemcpyDeviceToHost));
+  if (!h->rows_mode) {
+    CK(h, cudaMemcpy(code.data(), h->d_code[h->cur] + c0, c1 - c0, cudaMemcpyDeviceToHost));
+    return TS_OK;
+  }
+  const int64_t p0 = h->pw[t0];
+  const int64_t p1 = t1 < (int)h->tiles.size() ? h->pw[t1] : h->plane_words;
+  std::vector<uint32_t> pl(p1 - p0);
+  CK(h, cudaMemcpy(pl.data(), h->d_planes[h->cur] + p0, (p1 - p0) * 4, cudaMemcpyDeviceToHost));
+  for (int ti = t0; ti < t1; ti++) {
+    const TileDesc &d = h->tiles[ti];
+    const int nwt = tile_words(d.w, d.L), Wp = row_pitch(d.w);
+    const uint32_t *P = pl.data() + (h->pw[ti] - p0);
+    for (int l = 0; l < d.L; l++) {
+      const int64_t rb = d.off - c0 + (int64_t)l * Wp;
+      int64_t r = rb;
+      for (int x = 0; x < d.w; x++) {
+        const int b = l * d.w + x, wd = b >> 5, bt = b & 31;
+        if (!((P[wd] >> bt) & 1u)) continue;
+        const int v = (int)((P[nwt + wd] >> bt) & 1u) | (int)(((P[2 * nwt + wd] >> bt) & 1u) << 1) |
+                      (int)(((P[3 * nwt + wd] >> bt) & 1u) << 2);
+        const uint32_t e = (uint32_t)vids[r];
+        code[rb + x] = (uint8_t)(v | ((e >> kSlotShift) << 3));
+        vids[r++] = (int32_t)(e & kVidMask);
+      }
+    }
+  }
+  return TS_OK;
+}
+
 int ts_read_vehicles(ts_sim *h, int8_t *status, int32_t *link, int32_t *lane, int32_t *cell,
                      int32_t *v, int32_t *cursor, int32_t *t_arrive) {
   if (!h || !h->inited) return fail(h, TS_EINVAL, "not initialised");
   CK(h, cudaSetDevice(h->dev));
   CK(h, cudaStreamSynchronize(h->stream));
-  std::vector<uint8_t> code(h->total_cells);
-  std::vector<int32_t> vids(h->total_cells), inj(h->nv), arr(h->nv), cur(h->nv);
-  CK(h, cudaMemcpy(code.data(), h->d_code[h->cur], code.size(), cudaMemcpyDeviceToHost));
-  CK(h, cudaMemcpy(vids.data(), h->d_vid[h->cur], vids.size() * 4, cudaMemcpyDeviceToHost));
+  std::vector<uint8_t> code;
+  std::vector<int32_t> vids, inj(h->nv), arr(h->nv), cur(h->nv);
+  if (int rc = download_tiles(h, 0, (int)h->tiles.size(), code, vids)) return rc;
   CK(h, cudaMemcpy(inj.data(), h->d_inj, inj.size() * 4, cudaMemcpyDeviceToHost));
   CK(h, cudaMemcpy(arr.data(), h->d_arr, arr.size() * 4, cudaMemcpyDeviceToHost));
   CK(h, cudaMemcpy(cur.data(), h->d_cursor, cur.size() * 4, cudaMemcpyDeviceToHost));
@@ -907,10 +1020,9 @@ int ts_read_cells(ts_sim *h, int32_t link, int32_t *vid_out) {
   for (int i = h->link_tile0[link]; i < h->link_tile0[link + 1]; i++) {
     const TileDesc &d = h->tiles[i];
     const int Wp = row_pitch(d.w);
-    std::vector<uint8_t> code((size_t)d.L * Wp);
-    std::vector<int32_t> vids((size_t)d.L * Wp);
-    CK(h, cudaMemcpy(code.data(), h->d_code[h->cur] + d.off, code.size(), cudaMemcpyDeviceToHost));
-    CK(h, cudaMemcpy(vids.data(), h->d_vid[h->cur] + d.off, vids.size() * 4, cudaMemcpyDeviceToHost));
+    std::vector<uint8_t> code;
+    std::vector<int32_t> vids;
+    if (int rc = download_tiles(h, i, i + 1, code, vids)) return rc;
     for (int l = 0; l < L; l++) {
       int r = l * Wp;
       for (int x = 0; x < d.w; x++) {
@@ -928,11 +1040,15 @@ int ts_read_raw(ts_sim *h, int32_t link, uint8_t *code_out, int32_t *vid_out, in
   if (h->link_ntiles[link] != 1) return fail(h, TS_EINVAL, "link spans several tiles");
   CK(h, cudaSetDevice(h->dev));
   CK(h, cudaStreamSynchronize(h->stream));
-  const TileDesc &d = h->tiles[h->link_tile0[link]];
+  const int ti = h->link_tile0[link];
+  const TileDesc &d = h->tiles[ti];
   const int Wp = row_pitch(d.w);
   *pitch = Wp;
-  CK(h, cudaMemcpy(code_out, h->d_code[h->cur] + d.off, (size_t)d.L * Wp, cudaMemcpyDeviceToHost));
-  CK(h, cudaMemcpy(vid_out, h->d_vid[h->cur] + d.off, (size_t)d.L * Wp * 4, cudaMemcpyDeviceToHost));
+  std::vector<uint8_t> code;
+  std::vector<int32_t> vids;
+  if (int rc = download_tiles(h, ti, ti + 1, code, vids)) return rc;
+  memcpy(code_out, code.data(), (size_t)d.L * Wp);
+  memcpy(vid_out, vids.data(), (size_t)d.L * Wp * 4);
   return TS_OK;
 }
 
@@ -941,7 +1057,8 @@ int ts_state_hash(ts_sim *h, uint64_t *out) {
   CK(h, cudaSetDevice(h->dev));
   CK(h, cudaMemsetAsync(h->d_hash, 0, 16, h->stream));
   StepParams P = step_params(h, h->t, 0);
-  launch_hash(P, h->blocks, h->threads, h->smem, h->stream, h->d_hash);
+  if (h->rows_mode) launch_rows_hash(P, rows_params(h), h->stream, h->d_hash);
+  else launch_hash(P, h->blocks, h->threads, h->smem, h->stream, h->d_hash);
   CK(h, cudaGetLastError());
   unsigned long long r[2];
   CK(h, cudaMemcpyAsync(r, h->d_hash, 16, cudaMemcpyDeviceToHost, h->stream));

@@ -133,17 +133,31 @@ static __device__ __forceinline__ int behind_in(const uint32_t *bits, int q, int
 // q2 = its cell in the target lane; lanes l (own) and l2 (target) with valid
 // ranges [lo, hi) / [lo2, hi2); d = cells to the link end.  Cheap rejections
 // first: target occupied, then (speed-motivated) own gap >= v+1.
+// allowed-lane class of a vehicle (R7): 0 all lanes (straight on or final
+// link), 1 {0} (right turn), 2 {L-1} (left turn); tt = turn types of the
+// link's out-slots (2 bits each: 0 T, 1 L, 2 R)
+static __device__ __forceinline__ int lane_class(int slot, uint32_t tt) {
+  if (slot == kSlotFinal) return 0;
+  const int tty = (tt >> (2 * slot)) & 3;
+  return tty == 0 ? 0 : (tty == 2 ? 1 : 2);
+}
+
+static __device__ __forceinline__ bool lc_rule_set(const uint32_t *bits, int q, int q2, int lo,
+                                                   int hi, int lo2, int hi2, int v, int set, int l,
+                                                   int l2, int L, int dir, int d, int Vk, int D);
+
 static __device__ __forceinline__ bool lc_rule(const uint32_t *bits, int q, int q2, int lo,
                                                int hi, int lo2, int hi2, int code, int l, int l2,
                                                int L, int dir, int d, uint32_t tt, bool periodic,
                                                int Vk, int D) {
+  const int set = periodic ? 0 : lane_class(code >> 3, tt);
+  return lc_rule_set(bits, q, q2, lo, hi, lo2, hi2, code & 7, set, l, l2, L, dir, d, Vk, D);
+}
+
+static __device__ __forceinline__ bool lc_rule_set(const uint32_t *bits, int q, int q2, int lo,
+                                                   int hi, int lo2, int hi2, int v, int set, int l,
+                                                   int l2, int L, int dir, int d, int Vk, int D) {
   if (occupied(bits, q2)) return false;
-  const int v = code & 7, slot = code >> 3;
-  int set = 0;  // 0 all lanes, 1 {0} (right turn), 2 {L-1} (left turn)
-  if (slot != kSlotFinal && !periodic) {
-    const int tty = (tt >> (2 * slot)) & 3;
-    set = tty == 0 ? 0 : (tty == 2 ? 1 : 2);
-  }
   const bool own_ok = set == 0 || (set == 1 ? l == 0 : l == L - 1);
   if (own_ok) {
     // speed-motivated (R5): own gap < v+1, target gap larger, back gap >= V

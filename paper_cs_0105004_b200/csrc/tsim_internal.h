@@ -71,62 +71,85 @@ __host__ __device__ inline int64_t tile_cells_padded(int w, int L) {
   return ((int64_t)row_pitch(w) * L + 15) & ~(int64_t)15;
 }
 
-// Row kernel (k_rows): one warp per group of consecutive whole-link tiles
-// with at most 32 rows; thread i owns row i.  rowmap[g*32+i] =
-// (tile index within the group << 3) | lane.
+// ---------------------------------------------------------------- row mode
+// Fast path for networks whose tiles are all whole links.
+// The lane-cells of a tile are bits: cell (l, x) is bit l*w + x of the
+// tile's nwt = ceil(L*w/32) words, in six planes stored plane-major at
+// planes[pw + p*nwt + j]: occupancy O, the velocity bits V0, V1, V2 and the
+// vehicle's allowed-lane class A0, A1 (0 all lanes, 1 curb lane, 2 median
+// lane; reading R7) for its current link.
+// The vehicles of each lane-row are listed in cell order at
+// vid[off + l*Wp + k] as entries vid | slot << 27 (the out-slot travels
+// with the vehicle in its list entry; list order is preserved by the move).
+constexpr int kSlotShift = 27;
+constexpr uint32_t kVidMask = (1u << kSlotShift) - 1u;
+
+__host__ __device__ inline int tile_words(int w, int L) { return (L * w + 31) >> 5; }
+constexpr int kStatePlanes = 6;
+__host__ __device__ inline int tile_pwords(int w, int L) {
+  return (kStatePlanes * tile_words(w, L) + 3) & ~3;
+}
+
+// k_rows: one warp per group of consecutive tiles with <= 32 rows; the
+// group's words are numbered consecutively (tile after tile).
 struct GroupDesc {
   int32_t t0;
   int16_t ntiles;
   int16_t nrows;
-  int32_t bytes;    // cells spanned by the group's tiles (16-aligned)
+  int32_t nwg;      // words per plane in the group
   int32_t inj_cap;  // bound on vehicles the group can inject in one step
 };
 
-struct RowsLayout {
-  int CMAX, NW, injcap;
-  int o_cin, o_cout, o_bin, o_bmid, o_bspec, o_bleave, o_ent, o_injx, o_injv, o_misc, o_rows,
-      o_q, o_rowof, o_bfin, o_vpos, o_wp, bytes;
+// smem planes of one group, NG words each (+ pad words).  The last four
+// reuse the storage of U1..U4, dead after the hop.
+enum {
+  PL_O = 0,                   // input occupancy
+  PL_V0, PL_V1, PL_V2,        // input velocity bits
+  PL_A0, PL_A1,               // input allowed-lane class
+  PL_U1, PL_U2, PL_U3, PL_U4, PL_U5,  // v2 >= k (thermometer)
+  PL_B,                       // random slowdown
+  PL_RE,                      // last cell of a row
+  PL_OO, PL_OV0, PL_OV1, PL_OV2, PL_OA0, PL_OA1,  // S(t+1) (lane-changed in place)
+  PL_LR,                      // left the row (exit / node crossing)
+  PL_NUM,
+  PL_SP = PL_U1,              // entrant or injected vehicle
+  PL_LV = PL_U2,              // lane change: leaves this cell
+  PL_FIN = PL_U3,             // final occupancy
+  PL_WORK = PL_U4             // scratch
 };
 
-__host__ __device__ inline RowsLayout rows_layout(int cmax, int injcap) {
+struct RowsLayout {
+  int NG, PS, CMAX, injcap;
+  int o_planes, o_wp, o_wdesc, o_tiles, o_rows, o_ent, o_injx, o_injv, o_misc, bytes;
+};
+
+__host__ __device__ inline RowsLayout rows_layout(int ng, int injcap) {
   RowsLayout l;
-  l.CMAX = (cmax + 127) & ~127;
-  l.NW = l.CMAX / 32 + 3;
+  l.NG = (ng + 3) & ~3;
+  l.PS = l.NG + 4;  // pad word before, three after
+  l.CMAX = 32 * l.NG;
   l.injcap = injcap;
   int o = 0;
-  l.o_cin = o;
-  o += l.CMAX;
-  l.o_cout = o;
-  o += l.CMAX;
-  l.o_bin = o;
-  o += 4 * l.NW;
-  l.o_bmid = o;
-  o += 4 * l.NW;
-  l.o_bspec = o;
-  o += 4 * l.NW;
-  l.o_bleave = o;
-  o += 4 * l.NW;
-  l.o_ent = o;  // entrant vid per row, then entrant cell per row
+  l.o_planes = o;
+  o += 4 * PL_NUM * l.PS;
+  l.o_wp = o;  // per-word exclusive popcount prefixes of three bitmaps
+  o += 3 * 2 * (l.NG + 4);
+  o = (o + 15) & ~15;
+  l.o_wdesc = o;  // word -> (tile << 8) | word in tile
+  o += 2 * l.NG;
+  o = (o + 15) & ~15;
+  l.o_tiles = o;  // 8 arrays of 32
+  o += 4 * 8 * 32;
+  l.o_rows = o;  // 12 arrays of 32
+  o += 4 * 12 * 32;
+  l.o_ent = o;  // entrant entry per row, entrant cell per row
   o += 4 * 64;
   l.o_injx = o;  // injected: (row << 16) | cell
   o += 4 * injcap;
-  l.o_injv = o;  // injected vid
+  l.o_injv = o;  // injected entry
   o += 4 * injcap;
-  l.o_misc = o;  // injection counter
+  l.o_misc = o;
   o += 16;
-  l.o_rows = o;  // per row: flat start, cells, link, lane|vmax<<8, lane gid, front vid
-  o += 4 * 12 * 32;
-  l.o_q = o;  // work queue: 64 entries + 64 vids
-  o += 4 * 128;
-  l.o_rowof = o;  // row index of every cell
-  o += l.CMAX;
-  l.o_bfin = o;  // final occupancy
-  o += 4 * l.NW;
-  l.o_vpos = o;  // rank -> position
-  o += 2 * l.CMAX;
-  l.o_wp = o;  // per-word exclusive popcount prefixes of three bitmaps
-  o += 3 * 2 * l.NW;
-  o = (o + 15) & ~15;
   l.bytes = (o + 127) & ~127;
   return l;
 }
@@ -251,6 +274,9 @@ struct NodeParams {
 struct RowsParams {
   const GroupDesc *groups;
   const uint8_t *rowmap;
+  const int32_t *pw;  // plane word offset of every tile
+  const uint32_t *planes_in;
+  uint32_t *planes_out;
   int32_t ngroups;
   RowsLayout lay;
 };
@@ -269,5 +295,7 @@ void launch_step(const StepParams &p, int blocks, int threads, int smem, void *s
 void launch_node(const NodeParams &p, void *stream);
 void launch_hash(const StepParams &p, int blocks, int threads, int smem, void *stream,
                  unsigned long long *out);
+void launch_rows_hash(const StepParams &p, const RowsParams &r, void *stream,
+                      unsigned long long *out);
 
 }  // namespace tsim

@@ -1,42 +1,57 @@
-// tsim_rows.cu -- fast path of the TRANSIMS CA step on sm_100a: k_rows.
+// tsim_rows.cu -- bit-sliced fast path of the TRANSIMS CA step on sm_100a.
 //
-// One warp per group of consecutive whole-link tiles (<= 32 lane-rows,
-// ~2K cells).  The group's int8 codes are staged in shared memory with
-// 128-bit coalesced loads and an occupancy bitmap (one bit per lane-cell)
-// is built; a warp scan enumerates the vehicles in (row, cell) order and
-// keeps per-word popcount prefixes, so the rank of any cell is two loads
-// and a popc.  All per-vehicle work is vehicle-parallel (32 vehicles per
-// warp step), never row-serial:
-//   1. move (H4/H5): gap from the bitmap, NaSch velocity
-//      with the Philox slowdown, placement; the vid of a vehicle is read at
-//      its rank within its row.  Node entrants, injection (H6)  -> S(t+1)
-//   2. (fused) lane change of step t+1 (H1): bit-parallel
-//      prefilter per 32-cell word (target cell, the cell ahead of it and
-//      the V cells behind it free, or desperation zone), exact rule on the
-//      candidates only, applied in place                     -> S1(t+1)
-//   3. vid lists: a row that gained or lost no vehicle except exits at its
-//      front keeps a prefix of its list (128-bit copy); in the other rows
-//      every vehicle's output slot is its rank in the final bitmap and its
-//      vid is found by rank in the input list (order is preserved).
+// k_rows: one warp per group of consecutive whole-link tiles (<= 32
+// lane-rows).  The state of a tile is four bit-planes over its lane-cells
+// (occupancy O, velocity bits V0..V2) plus, per lane-row, the list of its
+// vehicles in cell order (entries vid | out-slot << 27).  One lane handles
+// one 32-cell word at a time, so the car-following rules of PAPER.md:330-335
+// become boolean algebra on 32 cells at once:
+//   F_k  = cells x+1..x+k empty and inside the row          (gap >= k)
+//   T_k  = min(v+1, V) >= k                                 (acceleration)
+//   U_k  = T_k & F_k                      (v2 >= k; thermometer code, R15)
+//   B    = Philox slowdown draw of every vehicle with v2 >= 1  (R3)
+//   W_k  = (U_k & ~B) | (U_{k+1} & B)                      (v3 >= k)
+//   D_k  = W_k & ~W_{k+1}                 (vehicles that move exactly k)
+//   O'   = OR_k D_k << k,  V' = bits of k placed the same way   (hop)
+// The Philox draws (which need the vid) are enumerated across the warp, 32
+// vehicles per step.  Row fronts near the stop line (open end R12, node
+// grant H3), entrants, injection (H6) and the fused lane change of step
+// t+1 (H1, bit-parallel prefilter + exact rule on candidates) are the only
+// per-vehicle paths.  Vid lists: rows without entrants, injections or lane
+// changes keep a prefix of their list (128-bit copy); the others are
+// rebuilt by rank arithmetic (in-lane order is preserved).
 #include "tsim_device.cuh"
 
 namespace tsim {
 
-// rank of position q in a flat bitmap with per-word exclusive prefixes wp
+// rank of group-flat bit position q in a plane with per-word prefixes wp
 static __device__ __forceinline__ int flat_rank(const uint32_t *bits, const uint16_t *wp, int q) {
   return wp[q >> 5] + __popc(bits[(q >> 5) + 1] & low_mask(q & 31));
 }
-// same for the bitmap (b1 & ~b2)
+// same for (b1 & ~b2)
 static __device__ __forceinline__ int flat_rank2(const uint32_t *b1, const uint32_t *b2,
                                                  const uint16_t *wp, int q) {
   const int j = (q >> 5) + 1;
   return wp[q >> 5] + __popc(b1[j] & ~b2[j] & low_mask(q & 31));
 }
 
+// position of the set bit of rank r (wp: per-word exclusive prefixes,
+// wp[nw] = total): binary search for the word, __fns for the bit
+static __device__ __forceinline__ int select_pos(const uint32_t *bits, const uint16_t *wp, int nw,
+                                                 int r) {
+  int lo = 0, hi = nw - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (wp[mid] <= r) lo = mid;
+    else hi = mid - 1;
+  }
+  return 32 * lo + (int)__fns(bits[lo + 1], 0, r - wp[lo] + 1);
+}
+
 // warp scan over the words of (b1 & ~b2) (b2 may be null): wp[j] = bits
-// before word j; optionally vpos[rank] = position.  Returns the total.
+// before word j, wp[nw] = total.  Returns the total.
 static __device__ __forceinline__ int scan_words(const uint32_t *b1, const uint32_t *b2, int nw,
-                                                 uint16_t *wp, uint16_t *vpos, int lane) {
+                                                 uint16_t *wp, int lane) {
   int total = 0;
   for (int j0 = 0; j0 < nw; j0 += 32) {
     const int j = j0 + lane;
@@ -49,13 +64,7 @@ static __device__ __forceinline__ int scan_words(const uint32_t *b1, const uint3
       const int y = __shfl_up_sync(FULL, sc, o);
       if (lane >= o) sc += y;
     }
-    int r = total + sc - c;
-    if (j < nw) wp[j] = (uint16_t)r;
-    if (vpos)
-      while (m) {
-        vpos[r++] = (uint16_t)(32 * j + __ffs(m) - 1);
-        m &= m - 1u;
-      }
+    if (j < nw) wp[j] = (uint16_t)(total + sc - c);
     total += __shfl_sync(FULL, sc, 31);
   }
   if (lane == 0) wp[nw] = (uint16_t)total;
@@ -63,317 +72,593 @@ static __device__ __forceinline__ int scan_words(const uint32_t *b1, const uint3
   return total;
 }
 
-// any bit of a row set?
 static __device__ __forceinline__ bool row_any(const uint32_t *bits, int s, int w) {
   uint32_t a = 0u;
-  for (int wj = 0; wj * 32 < w; wj++) a |= win_at(bits, s + 32 * wj) & low_mask(w - 32 * wj);
+  for (int x0 = 0; x0 < w; x0 += 32) a |= win_at(bits, s + x0) & low_mask(w - x0);
   return a != 0u;
 }
 
-// vid of an entrant / injected vehicle of row `row` at cell x
-static __device__ __forceinline__ int special_vid(const int32_t *ent, const int32_t *injx,
-                                                  const int32_t *injv, int ninj, int row, int x) {
-  if (ent[32 + row] == x) return ent[row];
-  const int key = (row << 16) | x;
-  for (int k = 0; k < ninj; k++)
-    if (injx[k] == key) return injv[k];
-  return -1;
+static __device__ __forceinline__ int get3(const uint32_t *v0, const uint32_t *v1,
+                                           const uint32_t *v2, int q) {
+  return occupied(v0, q) | (occupied(v1, q) << 1) | (occupied(v2, q) << 2);
 }
 
-__global__ void __launch_bounds__(128, 8) k_rows(const StepParams P, const RowsParams R) {
+// list entry of an entrant / injected vehicle of row `row` at cell x
+static __device__ __forceinline__ uint32_t special_entry(const int32_t *ent, const int32_t *injx,
+                                                         const int32_t *injv, int ninj, int row,
+                                                         int x) {
+  if (ent[32 + row] == x) return (uint32_t)ent[row];
+  const int key = (row << 16) | x;
+  for (int k = 0; k < ninj; k++)
+    if (injx[k] == key) return (uint32_t)injv[k];
+  return 0xFFFFFFFFu;
+}
+
+struct RowsSmem {
+  uint32_t *pl;  // planes, stride PS; plane p = pl + p*PS (pad word first)
+  int PS;
+  uint16_t *wp_in, *wp_mid, *wp_fin, *wdesc;
+  int32_t *t_wbase, *t_w, *t_lv, *t_lg, *t_link, *t_vrel, *t_row0, *t_pw;
+  int32_t *r_tile, *r_l, *r_gs, *r_w, *r_lg, *r_vrel, *r_r0, *r_m0, *r_f0, *r_nin, *r_nfin,
+      *r_front;
+  int32_t *ent, *injx, *injv, *misc;
+  __device__ __forceinline__ uint32_t *P(int p) const { return pl + p * PS; }
+};
+
+// D_k (vehicles of word j moving exactly k cells, k = 0..5) and the
+// vehicles that leave their row (row fronts passing the stop line)
+static __device__ __forceinline__ void move_masks(const RowsSmem &S, int j, uint32_t D[6],
+                                                  uint32_t &lr) {
+  const int q = j + 1;
+  const uint32_t O = S.P(PL_O)[q], B = S.P(PL_B)[q];
+  uint32_t U[6];
+  U[0] = S.P(PL_U1)[q];
+  U[1] = S.P(PL_U2)[q];
+  U[2] = S.P(PL_U3)[q];
+  U[3] = S.P(PL_U4)[q];
+  U[4] = S.P(PL_U5)[q];
+  U[5] = 0u;
+  uint32_t W[6];
+#pragma unroll
+  for (int k = 0; k < 5; k++) W[k] = (U[k] & ~B) | (U[k + 1] & B);  // v3 >= k+1
+  W[5] = 0u;
+  D[0] = O & ~W[0];
+#pragma unroll
+  for (int k = 1; k < 6; k++) D[k] = W[k - 1] & ~W[k];
+  // a move of k cells that passes a row end leaves the row
+  const uint32_t RE = S.P(PL_RE)[q], REn = S.P(PL_RE)[q + 1];
+  uint32_t cr = 0u;
+  lr = 0u;
+#pragma unroll
+  for (int k = 1; k < 6; k++) {
+    cr |= __funnelshift_r(RE, REn, k - 1);
+    lr |= D[k] & cr;
+    D[k] &= ~cr;
+  }
+}
+
+__global__ void __launch_bounds__(128) k_rows(const StepParams P, const RowsParams R) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ unsigned long long red[4 * 8];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nwarps_total = gridDim.x * (blockDim.x >> 5);
   const RowsLayout &Y = R.lay;
   uint8_t *base = smem + warp * Y.bytes;
-  uint8_t *cin = base + Y.o_cin, *cout = base + Y.o_cout, *rowof = base + Y.o_rowof;
-  uint32_t *bin = reinterpret_cast<uint32_t *>(base + Y.o_bin);
-  uint32_t *bmid = reinterpret_cast<uint32_t *>(base + Y.o_bmid);
-  uint32_t *bspec = reinterpret_cast<uint32_t *>(base + Y.o_bspec);
-  uint32_t *blv = reinterpret_cast<uint32_t *>(base + Y.o_bleave);
-  uint32_t *bfin = reinterpret_cast<uint32_t *>(base + Y.o_bfin);
-  uint16_t *vpos = reinterpret_cast<uint16_t *>(base + Y.o_vpos);
-  uint16_t *wp_in = reinterpret_cast<uint16_t *>(base + Y.o_wp);
-  uint16_t *wp_fin = wp_in + Y.NW;
-  uint16_t *wp_mid = wp_in + 2 * Y.NW;
-  int32_t *ent = reinterpret_cast<int32_t *>(base + Y.o_ent);
-  int32_t *injx = reinterpret_cast<int32_t *>(base + Y.o_injx);
-  int32_t *injv = reinterpret_cast<int32_t *>(base + Y.o_injv);
-  int32_t *misc = reinterpret_cast<int32_t *>(base + Y.o_misc);
-  int32_t *row_s = reinterpret_cast<int32_t *>(base + Y.o_rows);
-  int32_t *row_w = row_s + 32;       // cells
-  int32_t *row_link = row_s + 64;    // link
-  int32_t *row_lv = row_s + 96;      // lane | vmax << 8
-  int32_t *row_lg = row_s + 128;     // global lane id
-  int32_t *row_nfin = row_s + 160;   // vehicles in the final state
-  int32_t *row_front = row_s + 192;  // vid of the front vehicle (final state)
-  int32_t *row_r0 = row_s + 224;     // rank of the row start in bin
-  int32_t *row_f0 = row_s + 256;     // ... in bfin
-  int32_t *row_m0 = row_s + 288;     // ... in (bmid & ~bspec)
+  RowsSmem S;
+  S.pl = reinterpret_cast<uint32_t *>(base + Y.o_planes);
+  S.PS = Y.PS;
+  S.wp_in = reinterpret_cast<uint16_t *>(base + Y.o_wp);
+  S.wp_mid = S.wp_in + (Y.NG + 4);
+  S.wp_fin = S.wp_in + 2 * (Y.NG + 4);
+  S.wdesc = reinterpret_cast<uint16_t *>(base + Y.o_wdesc);
+  int32_t *tt = reinterpret_cast<int32_t *>(base + Y.o_tiles);
+  S.t_wbase = tt;
+  S.t_w = tt + 32;
+  S.t_lv = tt + 64;  // L | Vk << 4 | nwt << 8
+  S.t_lg = tt + 96;
+  S.t_link = tt + 128;
+  S.t_vrel = tt + 160;
+  S.t_row0 = tt + 192;
+  S.t_pw = tt + 224;
+  int32_t *rt = reinterpret_cast<int32_t *>(base + Y.o_rows);
+  S.r_tile = rt;
+  S.r_l = rt + 32;
+  S.r_gs = rt + 64;  // group-flat bit of the row start
+  S.r_w = rt + 96;
+  S.r_lg = rt + 128;
+  S.r_vrel = rt + 160;  // vid list of the row, relative to the group's first tile
+  S.r_r0 = rt + 192;
+  S.r_m0 = rt + 224;
+  S.r_f0 = rt + 256;
+  S.r_nin = rt + 288;
+  S.r_nfin = rt + 320;
+  S.r_front = rt + 352;
+  S.ent = reinterpret_cast<int32_t *>(base + Y.o_ent);
+  S.injx = reinterpret_cast<int32_t *>(base + Y.o_injx);
+  S.injv = reinterpret_cast<int32_t *>(base + Y.o_injv);
+  S.misc = reinterpret_cast<int32_t *>(base + Y.o_misc);
+  const bool do_move = (P.mode & kModeMove) != 0;
   const bool hash = (P.mode & kModeHash) != 0;
-  const bool lc_next = (P.mode & kModeLC) != 0;
-  const bool work = (P.mode & kModeWork) && P.link_work;
-  const int dir = ((P.t + 1) & 1) ? -1 : +1;  // R4, lane change of step t+1
+  const bool lc = (P.mode & kModeLC) != 0;
+  const int lct = do_move ? P.t + 1 : P.t;  // time of the lane-change sub-step
+  const int dir = (lct & 1) ? -1 : +1;      // R4
   Acc acc = {};
   Acc acc_next = {};
 
   for (int g = blockIdx.x * (blockDim.x >> 5) + warp; g < R.ngroups; g += nwarps_total) {
     const GroupDesc G = R.groups[g];
     const int64_t off0 = P.tiles[G.t0].off;
-    const int nw = (G.bytes + 31) >> 5;
-    // ---- rows of the group (thread i describes row i)
+    const int nw = G.nwg;
+    // ---- tile table (lane = tile) and row table (lane = row)
+    {
+      int nwt = 0, L = 0;
+      if (lane < G.ntiles) {
+        const TileDesc d = P.tiles[G.t0 + lane];
+        nwt = tile_words(d.w, d.L);
+        L = d.L;
+        S.t_w[lane] = d.w;
+        S.t_lv[lane] = d.L | (P.vmax_link[d.link] << 4) | (nwt << 8);
+        S.t_lg[lane] = d.lane_gid;
+        S.t_link[lane] = d.link;
+        S.t_vrel[lane] = (int)(d.off - off0);
+        S.t_pw[lane] = R.pw[G.t0 + lane];
+      }
+      int sw = nwt, sl = L;  // inclusive scans of words and rows
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int a = __shfl_up_sync(FULL, sw, o), b = __shfl_up_sync(FULL, sl, o);
+        if (lane >= o) {
+          sw += a;
+          sl += b;
+        }
+      }
+      if (lane < G.ntiles) {
+        S.t_wbase[lane] = sw - nwt;
+        S.t_row0[lane] = sl - L;
+        for (int jj = 0; jj < nwt; jj++) S.wdesc[sw - nwt + jj] = (uint16_t)((lane << 8) | jj);
+      }
+    }
+    __syncwarp();
     const bool active = lane < G.nrows;
-    TileDesc d;
-    d.w = 0;
-    d.L = 1;
-    d.link = 0;
-    d.lane_gid = 0;
-    int l = 0, s = 0, Wp = 4, Vk = 1;
+    int tl = 0, l = 0, gs = 0, w = 0, Wp = 4, Vk = 1, L = 1;
     if (active) {
       const int rm = R.rowmap[(size_t)g * 32 + lane];
+      tl = rm >> 3;
       l = rm & 7;
-      d = P.tiles[G.t0 + (rm >> 3)];
-      Wp = row_pitch(d.w);
-      s = (int)(d.off - off0) + l * Wp;
-      Vk = P.vmax_link[d.link];
+      w = S.t_w[tl];
+      Wp = row_pitch(w);
+      L = S.t_lv[tl] & 15;
+      Vk = (S.t_lv[tl] >> 4) & 15;
+      gs = 32 * S.t_wbase[tl] + l * w;
+      S.r_tile[lane] = tl;
+      S.r_l[lane] = l;
+      S.r_gs[lane] = gs;
+      S.r_w[lane] = w;
+      S.r_lg[lane] = S.t_lg[tl] + l;
+      S.r_vrel[lane] = S.t_vrel[tl] + l * Wp;
     }
-    // ---- stage the group's codes, clear the work bitmaps, row table
-    {
-      const uint4 *src = reinterpret_cast<const uint4 *>(P.code_in + off0);
-      uint4 *dst = reinterpret_cast<uint4 *>(cin);
-      uint4 *dco = reinterpret_cast<uint4 *>(cout);
-      const uint4 e = make_uint4(FULL, FULL, FULL, FULL);
-      const int n16 = G.bytes >> 4;
-      for (int i = lane; i < 2 * nw; i += 32) {
-        dst[i] = i < n16 ? __ldcs(src + i) : e;
-        dco[i] = e;
+    const int lg = active ? S.t_lg[tl] + l : 0;
+    const int link = active ? S.t_link[tl] : 0;
+    const int32_t *vin_row = P.vid_in + off0 + (active ? S.t_vrel[tl] + l * Wp : 0);
+    // ---- stage the input planes, clear the work planes
+    for (int j = lane; j < nw + 3; j += 32) {
+      const int q = j + 1;
+      uint32_t in[kStatePlanes] = {0u, 0u, 0u, 0u, 0u, 0u};
+      if (j < nw) {
+        const int wd = S.wdesc[j], t = wd >> 8, jj = wd & 255;
+        const int nwt = S.t_lv[t] >> 8;
+        const uint32_t *src = R.planes_in + S.t_pw[t] + jj;
+#pragma unroll
+        for (int p = 0; p < kStatePlanes; p++) in[p] = __ldcs(src + p * nwt);
       }
-      for (int i = lane; i < nw + 3; i += 32) {
-        bmid[i] = 0u;
-        bspec[i] = 0u;
-        blv[i] = 0u;
-      }
-      if (lane == 0) misc[0] = 0;
-      ent[32 + lane] = -1;
-      row_s[lane] = s;
-      row_w[lane] = d.w;
-      row_link[lane] = d.link;
-      row_lv[lane] = l | (Vk << 8);
-      row_lg[lane] = d.lane_gid + l;
-      if (active) {  // row id of every cell of the row
-        uint32_t *ro = reinterpret_cast<uint32_t *>(rowof + s);
-        const uint32_t id4 = (uint32_t)lane * 0x01010101u;
-        for (int i = 0; i < (Wp >> 2); i++) ro[i] = id4;
-      }
+#pragma unroll
+      for (int p = 0; p < kStatePlanes; p++) S.P(p)[q] = in[p];
+      for (int p = kStatePlanes; p < PL_NUM; p++) S.P(p)[q] = 0u;
+    }
+    if (lane < PL_NUM) S.P(lane)[0] = 0u;
+    if (lane == 0) S.misc[0] = 0;
+    S.ent[32 + lane] = -1;
+    __syncwarp();
+    if (active) set_bit(S.P(PL_RE), gs + w - 1);  // row ends
+    scan_words(S.P(PL_O), nullptr, nw, S.wp_in, lane);
+    if (active) {
+      S.r_r0[lane] = flat_rank(S.P(PL_O), S.wp_in, gs);
+      int nin = 0;
+      for (int x0 = 0; x0 < w; x0 += 32) nin += __popc(win_at(S.P(PL_O), gs + x0) & low_mask(w - x0));
+      S.r_nin[lane] = nin;
+      if ((P.mode & kModeWork) && P.link_work && nin)
+        atomicAdd(P.link_work + link, (unsigned long long)nin);
+      acc.work += nin;
     }
     __syncwarp();
-    build_bits(cin, bin, nw, lane);
-    __syncwarp();
-    const int nveh = scan_words(bin, nullptr, nw, wp_in, vpos, lane);
-    row_r0[lane] = active ? flat_rank(bin, wp_in, s) : 0;
-    __syncwarp();
-    // ---- 1. velocity update + move (H4/H5), 32 vehicles per warp step
-    if (P.mode & kModeMove) {
-      for (int r = lane; r < nveh; r += 32) {
-        const int p = vpos[r];
-        const int row = rowof[p];
-        const int rs = row_s[row], w = row_w[row], lv = row_lv[row];
-        const int x = p - rs;
-        const int code = cin[p];
-        const int v = code & 7, slot = code >> 3;
-        const int vid = P.vid_in[off0 + rs + (r - row_r0[row])];  // rank within the row
-        const int lim = min(kGmax, w - 1 - x);
-        const uint32_t ma = win_ahead(bin, p) & low_mask(lim);
-        int gp;
-        if (ma) gp = __ffs(ma) - 1;
-        else if (lim == kGmax || slot == kSlotFinal) gp = kGmax;  // R12 open end
-        else gp = min(kGmax, lim + (int)P.ext[row_lg[row]]);      // node grant (H3)
-        const int v3 = nasch_v3(v, lv >> 8, gp, (uint32_t)P.t, (uint32_t)vid, P.k0, P.k1, P.p32);
-        const int y = x + v3;
-        if (y < w) {
-          cout[rs + y] = (uint8_t)(v3 | (slot << 3));
-          set_bit(bmid, rs + y);
-          acc_place(acc, hash, vid, row_link[row], lv & 255, y, v3);
-        } else if (slot == kSlotFinal) {  // exit to parking
-          P.arr_time[vid] = P.t + 1;
-          acc.arr++;
-        }  // else: crossed the node; the node kernel placed it on the next link
-        acc.work++;
-        if (work) atomicAdd(P.link_work + row_link[row], 1ull);
+    if (do_move) {
+      // ---- 1a. thermometer codes, one 32-cell word per lane
+      for (int j = lane; j < nw; j += 32) {
+        const int q = j + 1;
+        const uint32_t O = S.P(PL_O)[q], On = S.P(PL_O)[q + 1];
+        const uint32_t RE = S.P(PL_RE)[q], REn = S.P(PL_RE)[q + 1];
+        const uint32_t V0 = S.P(PL_V0)[q], V1 = S.P(PL_V1)[q], V2 = S.P(PL_V2)[q];
+        const int vk = (S.t_lv[S.wdesc[j] >> 8] >> 4) & 15;
+        // gap >= k: cells x+1..x+k empty, none past the row end
+        uint32_t F = ~__funnelshift_r(O, On, 1) & ~RE;
+        uint32_t T = O;  // min(v+1, V) >= 1
+        S.P(PL_U1)[q] = T & F;
+        F &= ~__funnelshift_r(O, On, 2) & ~__funnelshift_r(RE, REn, 1);
+        T = vk >= 2 ? (O & (V0 | V1 | V2)) : 0u;  // v >= 1
+        S.P(PL_U2)[q] = T & F;
+        F &= ~__funnelshift_r(O, On, 3) & ~__funnelshift_r(RE, REn, 2);
+        T = vk >= 3 ? (V1 | V2) : 0u;  // v >= 2
+        S.P(PL_U3)[q] = T & F;
+        F &= ~__funnelshift_r(O, On, 4) & ~__funnelshift_r(RE, REn, 3);
+        T = vk >= 4 ? (V2 | (V1 & V0)) : 0u;  // v >= 3
+        S.P(PL_U4)[q] = T & F;
+        F &= ~__funnelshift_r(O, On, 5) & ~__funnelshift_r(RE, REn, 4);
+        T = vk >= 5 ? V2 : 0u;  // v >= 4
+        S.P(PL_U5)[q] = T & F;
       }
       __syncwarp();
+      // ---- 1b. the row front near the stop line: open end of the final
+      //          link (R12) or entry space granted by the node (H3)
       if (active) {
-        // entrant granted by the node kernel (lands in front of every vehicle)
-        const uint64_t rec = P.entr[d.lane_gid + l];
-        if ((uint32_t)(rec >> 43) == ((uint32_t)(P.t + 1) & 0x1FFFFFu)) {
-          const int evid = (int)(uint32_t)rec;
-          const uint8_t code = (uint8_t)(rec >> 32);
-          const int y = (int)((rec >> 40) & 7);
-          cout[s + y] = code;
-          set_bit(bmid, s + y);
-          set_bit(bspec, s + y);
-          ent[lane] = evid;
-          ent[32 + lane] = y;
-          acc_place(acc, hash, evid, d.link, l, y, code & 7);
+        int xf = -1;
+        for (int x0 = ((w - 1) >> 5) << 5; x0 >= 0 && xf < 0; x0 -= 32) {
+          const uint32_t m = win_at(S.P(PL_O), gs + x0) & low_mask(w - x0);
+          if (m) xf = x0 + 31 - __clz(m);
         }
-        if ((P.mode & kModeInject) && l == 0 && P.pend_off[d.link + 1] > P.pend_head[d.link]) {
-          const int row = lane;
-          inject_link(
-              P, d.link, 0, d.w, true, [&](int xx) { return cout[s + xx] == kEmpty; },
-              [&](int xx, uint8_t code, int ivid) {
-                cout[s + xx] = code;
-                set_bit(bmid, s + xx);
-                set_bit(bspec, s + xx);
-                const int k = atomicAdd(misc, 1);
-                injx[k] = (row << 16) | xx;
-                injv[k] = ivid;
-                acc.inj++;
-                acc_place(acc, hash, ivid, d.link, 0, xx, 0);
-              });
+        const int d = w - 1 - xf;
+        if (xf >= 0 && d < kGmax) {
+          const uint32_t e = (uint32_t)__ldg(vin_row + S.r_nin[lane] - 1);
+          const int slot = (int)(e >> kSlotShift);
+          const int gp = slot == kSlotFinal ? kGmax : min(kGmax, d + (int)P.ext[lg]);
+          if (gp > d) {
+            const int q = gs + xf;
+            const int v = get3(S.P(PL_V0), S.P(PL_V1), S.P(PL_V2), q);
+            const int v2 = min(min(v + 1, Vk), gp);
+            for (int k = d + 1; k <= v2; k++) set_bit(S.P(PL_U1 + k - 1), q);
+          }
         }
+      }
+      __syncwarp();
+      // ---- 1c. Philox slowdown draws (R3), 32 vehicles per warp step
+      const int nd = scan_words(S.P(PL_U1), nullptr, nw, S.wp_mid, lane);
+      for (int r = lane; r < nd; r += 32) {
+        const int q = select_pos(S.P(PL_U1), S.wp_mid, nw, r);
+        const int t = S.wdesc[q >> 5] >> 8;
+        const int tb = q - 32 * S.t_wbase[t];
+        const int tw = S.t_w[t], tL = S.t_lv[t] & 15;
+        int rl = 0;
+        while (rl + 1 < tL && tb >= (rl + 1) * tw) rl++;
+        const int row = S.t_row0[t] + rl;
+        const int rank = flat_rank(S.P(PL_O), S.wp_in, q) - S.r_r0[row];
+        const uint32_t e = (uint32_t)P.vid_in[off0 + S.r_vrel[row] + rank];
+        if ((uint64_t)philox_w0((uint32_t)P.t, e & kVidMask, P.k0, P.k1) < P.p32)
+          set_bit(S.P(PL_B), q);
+      }
+      __syncwarp();
+      // ---- 1d. hop: O' = OR_k D_k << k, velocity bits likewise
+      for (int j = lane; j < nw; j += 32) {
+        uint32_t Dj[6], Dp[6], lrj, lrp;
+        move_masks(S, j, Dj, lrj);
+        if (j > 0) move_masks(S, j - 1, Dp, lrp);
+        else {
+#pragma unroll
+          for (int k = 0; k < 6; k++) Dp[k] = 0u;
+        }
+        uint32_t sh[6];
+        sh[0] = Dj[0];
+#pragma unroll
+        for (int k = 1; k < 6; k++) sh[k] = __funnelshift_l(Dp[k], Dj[k], k);
+        const int q = j + 1;
+        const uint32_t OO = sh[0] | sh[1] | sh[2] | sh[3] | sh[4] | sh[5];
+        S.P(PL_OO)[q] = OO;
+        S.P(PL_OV0)[q] = sh[1] | sh[3] | sh[5];
+        S.P(PL_OV1)[q] = sh[2] | sh[3];
+        S.P(PL_OV2)[q] = sh[4] | sh[5];
+        // the allowed-lane class hops with its vehicle
+        const uint32_t A0 = S.P(PL_A0)[q], A1 = S.P(PL_A1)[q];
+        const uint32_t A0p = j > 0 ? S.P(PL_A0)[q - 1] : 0u, A1p = j > 0 ? S.P(PL_A1)[q - 1] : 0u;
+        uint32_t oa0 = Dj[0] & A0, oa1 = Dj[0] & A1;
+#pragma unroll
+        for (int k = 1; k < 6; k++) {
+          oa0 |= __funnelshift_l(Dp[k] & A0p, Dj[k] & A0, k);
+          oa1 |= __funnelshift_l(Dp[k] & A1p, Dj[k] & A1, k);
+        }
+        S.P(PL_OA0)[q] = oa0;
+        S.P(PL_OA1)[q] = oa1;
+        S.P(PL_LR)[q] = lrj;
+        acc.active += __popc(OO);
+        acc.sumv += __popc(sh[1]) + 2 * __popc(sh[2]) + 3 * __popc(sh[3]) + 4 * __popc(sh[4]) +
+                    5 * __popc(sh[5]);
+      }
+    } else {  // no move (initial injection / lane change only)
+      for (int j = lane; j < nw; j += 32) {
+        const int q = j + 1;
+        S.P(PL_OO)[q] = S.P(PL_O)[q];
+        S.P(PL_OV0)[q] = S.P(PL_V0)[q];
+        S.P(PL_OV1)[q] = S.P(PL_V1)[q];
+        S.P(PL_OV2)[q] = S.P(PL_V2)[q];
+        S.P(PL_OA0)[q] = S.P(PL_A0)[q];
+        S.P(PL_OA1)[q] = S.P(PL_A1)[q];
+        if (P.mode & kModeInject) acc.active += __popc(S.P(PL_O)[q]);
       }
     }
     __syncwarp();
-    // ---- 2. lane change of step t+1 on S(t+1) (H1, fused)
+    for (int j = lane; j < nw + 3; j += 32) {  // U1, U2 storage becomes SP, LV
+      S.P(PL_SP)[j + 1] = 0u;
+      S.P(PL_LV)[j + 1] = 0u;
+    }
+    __syncwarp();
+    // ---- 1e. row events: exits, entrant, injection
+    if (active && do_move) {
+      for (int x0 = 0; x0 < w; x0 += 32) {  // the front left the row
+        const uint32_t m = win_at(S.P(PL_LR), gs + x0) & low_mask(w - x0);
+        if (m) {
+          const uint32_t e = (uint32_t)__ldg(vin_row + S.r_nin[lane] - 1);
+          if ((int)(e >> kSlotShift) == kSlotFinal) {  // exit to parking
+            P.arr_time[e & kVidMask] = P.t + 1;
+            acc.arr++;
+          }  // else: crossed the node; k_node_warp placed it on the next link
+        }
+      }
+      const uint64_t rec = P.entr[lg];  // entrant granted by the node kernel
+      if ((uint32_t)(rec >> 43) == ((uint32_t)(P.t + 1) & 0x1FFFFFu)) {
+        const int evid = (int)(uint32_t)rec;
+        const int code = (int)((rec >> 32) & 0xFF);
+        const int y = (int)((rec >> 40) & 7);
+        const int q = gs + y;
+        set_bit(S.P(PL_OO), q);
+        if (code & 1) set_bit(S.P(PL_OV0), q);
+        if (code & 2) set_bit(S.P(PL_OV1), q);
+        if (code & 4) set_bit(S.P(PL_OV2), q);
+        set_bit(S.P(PL_SP), q);
+        const int cls = lane_class(code >> 3, P.tt_link[link]);
+        if (cls & 1) set_bit(S.P(PL_OA0), q);
+        if (cls & 2) set_bit(S.P(PL_OA1), q);
+        S.ent[lane] = evid | ((code >> 3) << kSlotShift);
+        S.ent[32 + lane] = y;
+        acc.active++;
+        acc.sumv += code & 7;
+      }
+    }
+    if (active && (P.mode & kModeInject) && l == 0 && P.pend_off[link + 1] > P.pend_head[link]) {
+      const int row = lane;
+      inject_link(
+          P, link, 0, w, true, [&](int x) { return !occupied(S.P(PL_OO), gs + x); },
+          [&](int x, uint8_t code, int ivid) {
+            const int q = gs + x;
+            set_bit(S.P(PL_OO), q);
+            set_bit(S.P(PL_SP), q);
+            const int cls = lane_class(code >> 3, P.tt_link[link]);
+            if (cls & 1) set_bit(S.P(PL_OA0), q);
+            if (cls & 2) set_bit(S.P(PL_OA1), q);
+            const int k = atomicAdd(S.misc, 1);
+            S.injx[k] = (row << 16) | x;
+            S.injv[k] = ivid | ((code >> 3) << kSlotShift);
+            acc.inj++;
+            acc.active++;
+          });
+    }
+    __syncwarp();
+    // rank of input-derived vehicles (for vid lookups of S(t+1))
+    scan_words(S.P(PL_OO), S.P(PL_SP), nw, S.wp_mid, lane);
+    if (active) S.r_m0[lane] = flat_rank2(S.P(PL_OO), S.P(PL_SP), S.wp_mid, gs);
+    __syncwarp();
+    // entry (vid | slot) of the vehicle of S(t+1) at group-flat position q
+    auto entry_at = [&](int row, int q) -> uint32_t {
+      const int x = q - S.r_gs[row];
+      if (occupied(S.P(PL_SP), q)) return special_entry(S.ent, S.injx, S.injv, S.misc[0], row, x);
+      return (uint32_t)P.vid_in[off0 + S.r_vrel[row] + flat_rank2(S.P(PL_OO), S.P(PL_SP),
+                                                                   S.wp_mid, q) - S.r_m0[row]];
+    };
+    if (hash) {  // state hash of S(t+1) (tests)
+      const int n = scan_words(S.P(PL_OO), nullptr, nw, S.wp_fin, lane);
+      for (int r = lane; r < n; r += 32) {
+        const int q = select_pos(S.P(PL_OO), S.wp_fin, nw, r);
+        const int t = S.wdesc[q >> 5] >> 8;
+        const int tb = q - 32 * S.t_wbase[t];
+        const int tw = S.t_w[t], tL = S.t_lv[t] & 15;
+        int rl = 0;
+        while (rl + 1 < tL && tb >= (rl + 1) * tw) rl++;
+        const int row = S.t_row0[t] + rl;
+        const uint32_t e = entry_at(row, q);
+        acc.hash += vmix((int)(e & kVidMask), S.t_link[t], rl, tb - rl * tw,
+                         get3(S.P(PL_OV0), S.P(PL_OV1), S.P(PL_OV2), q));
+      }
+      __syncwarp();
+    }
+    // ---- 2. lane change on S(t+1) (fused) or S(t) (lane change only)
     const int l2 = l + dir;
-    const bool can_lc = active && lc_next && l2 >= 0 && l2 < d.L;
-    const int s2 = s + dir * Wp;
+    const bool can_lc = active && lc && l2 >= 0 && l2 < L;
+    const int gs2 = gs + dir * w;
+    const uint32_t *OO = S.P(PL_OO);
     if (can_lc) {
-      const uint32_t tt = P.tt_link[d.link];
-      for (int x0 = 0; x0 < d.w; x0 += 32) {
-        const uint32_t own = win_at(bmid, s + x0) & low_mask(d.w - x0);
+      for (int x0 = 0; x0 < w; x0 += 32) {
+        const uint32_t own = win_at(OO, gs + x0) & low_mask(w - x0);
         if (!own) continue;
         // target lane cells x0-5 .. x0+58 as one 64-bit window
-        uint64_t W = (uint64_t)win_at(bmid, s2 + x0 - kGmax) |
-                     ((uint64_t)win_at(bmid, s2 + x0 + 27) << 32);
-        if (x0 == 0) W &= ~(uint64_t)31u;  // before the link start: empty (R2)
-        const int endb = d.w - x0 + kGmax;  // first bit at or beyond the link end
-        const uint64_t Wend = endb < 64 ? (W | (~0ull << endb)) : W;
-        const uint32_t T = (uint32_t)(W >> kGmax);            // target cell
+        uint64_t Wt = (uint64_t)win_at(OO, gs2 + x0 - kGmax) |
+                      ((uint64_t)win_at(OO, gs2 + x0 + 27) << 32);
+        if (x0 == 0) Wt &= ~(uint64_t)31u;  // before the link start: empty (R2)
+        const int endb = w - x0 + kGmax;     // first bit at or beyond the link end
+        const uint64_t Wend = endb < 64 ? (Wt | (~0ull << endb)) : Wt;
+        const uint32_t T = (uint32_t)(Wt >> kGmax);            // target cell
         const uint32_t Tn = (uint32_t)(Wend >> (kGmax + 1));  // cell ahead of it
-        uint32_t B = 0u;                                      // Vk cells behind it
-        for (int k = 1; k <= Vk; k++) B |= (uint32_t)(W >> (kGmax - k));
-        const uint32_t DZ = range_mask(d.w - P.D - x0, 32);  // desperation zone
-        uint32_t cand = own & ~T & ((~Tn & ~B) | DZ);
+        uint32_t Bk = 0u;                                     // Vk cells behind it
+        for (int k = 1; k <= Vk; k++) Bk |= (uint32_t)(Wt >> (kGmax - k));
+        const uint32_t DZ = range_mask(w - P.D - x0, 32);  // desperation zone
+        uint32_t cand = own & ~T & ((~Tn & ~Bk) | DZ);
         while (cand) {
           const int x = x0 + __ffs(cand) - 1;
           cand &= cand - 1u;
-          if (lc_rule(bmid, s + x, s2 + x, s, s + d.w, s2, s2 + d.w, cout[s + x], l, l2, d.L,
-                      dir, d.w - 1 - x, tt, false, Vk, P.D)) {
-            set_bit(blv, s + x);
+          const int q = gs + x;
+          const int v = get3(S.P(PL_OV0), S.P(PL_OV1), S.P(PL_OV2), q);
+          const int cls = occupied(S.P(PL_OA0), q) | (occupied(S.P(PL_OA1), q) << 1);
+          if (lc_rule_set(OO, q, gs2 + x, gs, gs + w, gs2, gs2 + w, v, cls, l, l2, L, dir,
+                          w - 1 - x, Vk, P.D)) {
+            set_bit(S.P(PL_LV), q);
             acc_next.lc++;
           }
         }
       }
     }
     __syncwarp();
-    for (int i = lane; i < nw + 3; i += 32) bfin[i] = bmid[i] & ~blv[i];
+    for (int j = lane; j < nw; j += 32) S.P(PL_FIN)[j + 1] = OO[j + 1] & ~S.P(PL_LV)[j + 1];
     __syncwarp();
     if (can_lc) {  // apply: sideways moves into cells that were empty
-      for (int x0 = 0; x0 < d.w; x0 += 32) {
-        uint32_t m = win_at(blv, s + x0) & low_mask(d.w - x0);
+      for (int x0 = 0; x0 < w; x0 += 32) {
+        uint32_t m = win_at(S.P(PL_LV), gs + x0) & low_mask(w - x0);
         while (m) {
           const int x = x0 + __ffs(m) - 1;
           m &= m - 1u;
-          cout[s2 + x] = cout[s + x];
-          cout[s + x] = kEmpty;
-          set_bit(bfin, s2 + x);
+          const int q = gs + x, q2 = gs2 + x;
+          set_bit(S.P(PL_FIN), q2);
+#pragma unroll
+          for (int p = PL_OV0; p <= PL_OA1; p++)
+            if (occupied(S.P(p), q)) {
+              set_bit(S.P(p), q2);
+              atomicAnd(S.P(p) + (q >> 5) + 1, ~(1u << (q & 31)));
+            }
         }
       }
     }
+    __syncwarp();
     // ---- 3. vid lists of the final state
-    for (int i = lane; i < nw + 3; i += 32) bin[i] = 0u;  // becomes: changed rows' cells
+    for (int j = lane; j < nw + 3; j += 32) S.P(PL_WORK)[j + 1] = 0u;  // changed rows' cells
     __syncwarp();
     bool changed = false;
     if (active) {
-      changed = row_any(bspec, s, d.w) || (lc_next && row_any(blv, s, d.w));
+      changed = row_any(S.P(PL_SP), gs, w) || (lc && row_any(S.P(PL_LV), gs, w));
       int nfin = 0;
       uint32_t diff = 0u;
-      for (int x0 = 0; x0 < d.w; x0 += 32) {
-        const uint32_t f = win_at(bfin, s + x0) & low_mask(d.w - x0);
+      for (int x0 = 0; x0 < w; x0 += 32) {
+        const uint32_t f = win_at(S.P(PL_FIN), gs + x0) & low_mask(w - x0);
         nfin += __popc(f);
-        diff |= f ^ (win_at(bmid, s + x0) & low_mask(d.w - x0));
+        diff |= f ^ (win_at(OO, gs + x0) & low_mask(w - x0));
       }
       changed |= diff != 0u;  // arrivals
-      row_nfin[lane] = nfin;
+      S.r_nfin[lane] = nfin;
       if (!changed) {
         // input vehicles minus exits at the front: a prefix of the input list
-        const uint4 *src = reinterpret_cast<const uint4 *>(P.vid_in + off0 + s);
-        uint4 *dst = reinterpret_cast<uint4 *>(P.vid_out + off0 + s);
+        const uint4 *src = reinterpret_cast<const uint4 *>(vin_row);
+        uint4 *dst = reinterpret_cast<uint4 *>(P.vid_out + off0 + S.r_vrel[lane]);
         uint4 bufv = make_uint4(0, 0, 0, 0);
         for (int i = 0; i < nfin; i += 4) {
           bufv = __ldg(src + (i >> 2));
           __stcs(dst + (i >> 2), bufv);
         }
         const int k = (nfin - 1) & 3;
-        row_front[lane] = (int)(k == 0 ? bufv.x : k == 1 ? bufv.y : k == 2 ? bufv.z : bufv.w);
+        S.r_front[lane] = (int)(k == 0 ? bufv.x : k == 1 ? bufv.y : k == 2 ? bufv.z : bufv.w);
       } else {
-        for (int x0 = 0; x0 < d.w; x0 += 32) {  // mark the row's cells
-          const uint32_t m = low_mask(d.w - x0);
-          const int q = s + x0, sh = q & 31;
-          atomicOr(bin + (q >> 5) + 1, m << sh);
-          if (sh) atomicOr(bin + (q >> 5) + 2, m >> (32 - sh));
+        for (int x0 = 0; x0 < w; x0 += 32) {  // mark the row's cells
+          const uint32_t m = low_mask(w - x0);
+          const int q = gs + x0, sh = q & 31;
+          atomicOr(S.P(PL_WORK) + (q >> 5) + 1, m << sh);
+          if (sh) atomicOr(S.P(PL_WORK) + (q >> 5) + 2, m >> (32 - sh));
         }
       }
     }
     if (__ballot_sync(FULL, changed)) {
       __syncwarp();
-      for (int i = lane; i < nw; i += 32) bin[i + 1] &= bfin[i + 1];
-      scan_words(bfin, nullptr, nw, wp_fin, nullptr, lane);
-      scan_words(bmid, bspec, nw, wp_mid, nullptr, lane);
-      const int nch = scan_words(bin, nullptr, nw, wp_in, vpos, lane);
-      row_f0[lane] = active ? flat_rank(bfin, wp_fin, s) : 0;
-      row_m0[lane] = active ? flat_rank2(bmid, bspec, wp_mid, s) : 0;
+      for (int j = lane; j < nw; j += 32) S.P(PL_WORK)[j + 1] &= S.P(PL_FIN)[j + 1];
+      scan_words(S.P(PL_FIN), nullptr, nw, S.wp_fin, lane);
+      const int nch = scan_words(S.P(PL_WORK), nullptr, nw, S.wp_in, lane);
+      if (active) S.r_f0[lane] = flat_rank(S.P(PL_FIN), S.wp_fin, gs);
       __syncwarp();
       for (int r = lane; r < nch; r += 32) {
-        const int p = vpos[r];
-        const int row = rowof[p];
-        const int rs = row_s[row];
-        const int x = p - rs;
-        const int j = flat_rank(bfin, wp_fin, p) - row_f0[row];  // output slot
-        int vid;
-        if (occupied(bmid, p)) {  // own post-move vehicle
-          if (occupied(bspec, p)) vid = special_vid(ent, injx, injv, misc[0], row, x);
-          else vid = P.vid_in[off0 + rs + flat_rank2(bmid, bspec, wp_mid, p) - row_m0[row]];
-        } else {  // arrived from the row l - dir of the same link
-          const int wpr = row_pitch(row_w[row]);
-          const int ps = p - dir * wpr, srow = row - dir;
-          if (occupied(bspec, ps)) vid = special_vid(ent, injx, injv, misc[0], srow, x);
-          else
-            vid = P.vid_in[off0 + (rs - dir * wpr) + flat_rank2(bmid, bspec, wp_mid, ps) -
-                           row_m0[srow]];
-        }
-        P.vid_out[off0 + rs + j] = vid;
-        if (j == row_nfin[row] - 1) row_front[row] = vid;  // front vehicle
+        const int q = select_pos(S.P(PL_WORK), S.wp_in, nw, r);
+        const int t = S.wdesc[q >> 5] >> 8;
+        const int tb = q - 32 * S.t_wbase[t];
+        const int tw = S.t_w[t], tL = S.t_lv[t] & 15;
+        int rl = 0;
+        while (rl + 1 < tL && tb >= (rl + 1) * tw) rl++;
+        const int row = S.t_row0[t] + rl;
+        const int j = flat_rank(S.P(PL_FIN), S.wp_fin, q) - S.r_f0[row];  // output slot
+        const uint32_t e = occupied(OO, q) ? entry_at(row, q)  // own vehicle
+                                           : entry_at(row - dir, q - dir * tw);  // arrived
+        P.vid_out[off0 + S.r_vrel[row] + j] = (int)e;
+        if (j == S.r_nfin[row] - 1) S.r_front[row] = (int)e;  // front vehicle
       }
     }
     __syncwarp();
-    if (active && lc_next) {  // the output is S1(t+1): node records for k_node_warp
-      const uint32_t fin = win_at(bfin, s + d.w - kGmax) & 31u;  // bit i = cell w-5+i
-      uint64_t rec = (uint64_t)(__brev(fin) >> 27) << 44;          // bit i = cell n-1-i
+    if (active && lc) {  // the output is S1: node records for k_node_warp
+      const int st = gs + w - kGmax;
+      const uint32_t fin = win_at(S.P(PL_FIN), st) & 31u;  // bit i = cell w-5+i
+      uint64_t rec = (uint64_t)(__brev(fin) >> 27) << 44;    // bit i = cell n-1-i
       if (fin) {
-        const int xf = d.w - kGmax + 31 - __clz(fin);
-        rec |= (uint64_t)(uint32_t)row_front[lane] | ((uint64_t)cout[s + xf] << 32) |
-               ((uint64_t)(d.w - 1 - xf) << 40) | (1ull << 43);
+        const int xf = w - kGmax + 31 - __clz(fin);
+        const uint32_t e = (uint32_t)S.r_front[lane];
+        const int code = get3(S.P(PL_OV0), S.P(PL_OV1), S.P(PL_OV2), gs + xf) |
+                         ((int)(e >> kSlotShift) << 3);
+        rec |= (uint64_t)(e & kVidMask) | ((uint64_t)code << 32) |
+               ((uint64_t)(w - 1 - xf) << 40) | (1ull << 43);
       }
-      P.tail_rec[d.lane_gid + l] = rec;
-      P.head_occ[d.lane_gid + l] = (uint8_t)(win_at(bfin, s) & 31u);
+      P.tail_rec[lg] = rec;
+      P.head_occ[lg] = (uint8_t)(win_at(S.P(PL_FIN), gs) & 31u);
     }
-    {
-      uint4 *dst = reinterpret_cast<uint4 *>(P.code_out + off0);
-      const uint4 *src = reinterpret_cast<const uint4 *>(cout);
-      for (int i = lane; i < (G.bytes >> 4); i += 32) __stcs(dst + i, src[i]);
+    // ---- write the final planes
+    for (int j = lane; j < nw; j += 32) {
+      const int wd = S.wdesc[j], t = wd >> 8, jj = wd & 255;
+      const int nwt = S.t_lv[t] >> 8;
+      uint32_t *dst = R.planes_out + S.t_pw[t] + jj;
+      const int q = j + 1;
+      __stcs(dst, S.P(PL_FIN)[q]);
+      __stcs(dst + nwt, S.P(PL_OV0)[q]);
+      __stcs(dst + 2 * nwt, S.P(PL_OV1)[q]);
+      __stcs(dst + 3 * nwt, S.P(PL_OV2)[q]);
+      __stcs(dst + 4 * nwt, S.P(PL_OA0)[q]);
+      __stcs(dst + 5 * nwt, S.P(PL_OA1)[q]);
     }
     __syncwarp();
   }
   flush_acc(P, acc, P.t + 1, red);
-  if (lc_next) flush_acc(P, acc_next, P.t + 2, red);
+  if (lc) flush_acc(P, acc_next, lct + 1, red);
+}
+
+// state hash of the row-mode state S(t) (one thread per lane-row)
+__global__ void __launch_bounds__(128) k_rows_hash(const StepParams P, const RowsParams R,
+                                                   unsigned long long *out) {
+  const int gid = blockIdx.x * blockDim.x + threadIdx.x;
+  uint64_t h = 0, cnt = 0;
+  // rows are enumerated through the tiles: gid = tile * 8 + lane of tile
+  const int ti = gid >> 3, l = gid & 7;
+  if (ti < P.ntiles) {
+    const TileDesc d = P.tiles[ti];
+    if (l < d.L) {
+      const int nwt = tile_words(d.w, d.L);
+      const uint32_t *pl = R.planes_in + R.pw[ti];
+      const int32_t *vl = P.vid_in + d.off + (int64_t)l * row_pitch(d.w);
+      int k = 0;
+      for (int x = 0; x < d.w; x++) {
+        const int b = l * d.w + x;
+        if (!((pl[b >> 5] >> (b & 31)) & 1u)) continue;
+        const int v = (int)((pl[nwt + (b >> 5)] >> (b & 31)) & 1u) |
+                      (int)(((pl[2 * nwt + (b >> 5)] >> (b & 31)) & 1u) << 1) |
+                      (int)(((pl[3 * nwt + (b >> 5)] >> (b & 31)) & 1u) << 2);
+        const uint32_t e = (uint32_t)vl[k++];
+        h += vmix((int)(e & kVidMask), d.link, l, d.a + x, v);
+        cnt++;
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    h += __shfl_down_sync(FULL, h, o);
+    cnt += __shfl_down_sync(FULL, cnt, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(out, (unsigned long long)h);
+    atomicAdd(out + 1, (unsigned long long)cnt);
+  }
 }
 
 void launch_rows(const StepParams &p, const RowsParams &r, int blocks, int threads, int smem,
                  void *stream) {
   k_rows<<<blocks, threads, smem, (cudaStream_t)stream>>>(p, r);
+}
+void launch_rows_hash(const StepParams &p, const RowsParams &r, void *stream,
+                      unsigned long long *out) {
+  const int n = p.ntiles * 8;
+  k_rows_hash<<<(n + 127) / 128, 128, 0, (cudaStream_t)stream>>>(p, r, out);
 }
 cudaError_t set_rows_smem(int bytes) {
   return cudaFuncSetAttribute(k_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
