@@ -100,27 +100,30 @@ struct GroupDesc {
   int32_t inj_cap;  // bound on vehicles the group can inject in one step
 };
 
-// smem planes of one group, NG words each (+ pad words).  The last four
-// reuse the storage of U1..U4, dead after the hop.
+// smem planes of one group, NG words each (+ pad words).  The overlays
+// reuse storage that is dead by the time they are written: U1..U5 after
+// the hop, the input velocity bits after the row-front fix-up.
 enum {
   PL_O = 0,                   // input occupancy
   PL_V0, PL_V1, PL_V2,        // input velocity bits
   PL_A0, PL_A1,               // input allowed-lane class
   PL_U1, PL_U2, PL_U3, PL_U4, PL_U5,  // v2 >= k (thermometer)
   PL_B,                       // random slowdown
-  PL_RE,                      // last cell of a row
-  PL_OO, PL_OV0, PL_OV1, PL_OV2, PL_OA0, PL_OA1,  // S(t+1) (lane-changed in place)
+  PL_RE, PL_RS, PL_ZN,        // static: last cell / first cell of a row, last D cells
+  PL_OO, PL_OV0, PL_OV1, PL_OV2, PL_OA0, PL_OA1,  // S(t+1) before its lane change
   PL_LR,                      // left the row (exit / node crossing)
   PL_NUM,
   PL_SP = PL_U1,              // entrant or injected vehicle
   PL_LV = PL_U2,              // lane change: leaves this cell
   PL_FIN = PL_U3,             // final occupancy
-  PL_WORK = PL_U4             // scratch
+  PL_WORK = PL_U4,            // scratch (rows whose vid list is rebuilt)
+  PL_CH = PL_U5,              // cells touched by a lane change (left or arrived)
+  PL_FV0 = PL_V0, PL_FV1 = PL_V1, PL_FV2 = PL_V2  // final velocity bits
 };
 
 struct RowsLayout {
   int NG, PS, CMAX, injcap;
-  int o_planes, o_wp, o_wdesc, o_tiles, o_rows, o_ent, o_injx, o_injv, o_misc, bytes;
+  int o_planes, o_wp, o_wdesc, o_wrow, o_own, o_tiles, o_rows, o_ent, o_injx, o_injv, o_misc, bytes;
 };
 
 __host__ __device__ inline RowsLayout rows_layout(int ng, int injcap) {
@@ -137,6 +140,10 @@ __host__ __device__ inline RowsLayout rows_layout(int ng, int injcap) {
   o = (o + 15) & ~15;
   l.o_wdesc = o;  // word -> (tile << 8) | word in tile
   o += 2 * l.NG;
+  l.o_wrow = o;  // word -> row holding its first cell
+  o += l.NG;
+  l.o_own = o;  // bit enumeration: lane owning each slot of a 32-slot window
+  o += 32;
   o = (o + 15) & ~15;
   l.o_tiles = o;  // 8 arrays of 32
   o += 4 * 8 * 32;
