@@ -1,5 +1,5 @@
 import sys, numpy as np
-sys.path.insert(0, '.')
+import os; sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import oracle, scenarios, paper_cs_0105004_b200 as tsim
 
 KEYS = ("status", "link", "lane", "cell", "v", "cursor")

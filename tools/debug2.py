@@ -1,5 +1,5 @@
 import sys, numpy as np
-sys.path.insert(0, '.')
+import os; sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import oracle, scenarios, paper_cs_0105004_b200 as tsim
 s2 = scenarios.portland(n_nodes=600, n_edges=800, n_veh=3000, side_km=8.0, n_zones=64, seed=2)
 s2.depart[:] = 0

@@ -1,5 +1,5 @@
 import sys
-sys.path.insert(0, '.')
+import os; sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import scenarios, paper_cs_0105004_b200 as tsim
 gc = int(sys.argv[1]) if len(sys.argv) > 1 else 0
 scn = scenarios.config('4a')

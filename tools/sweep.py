@@ -1,5 +1,5 @@
 import sys, time, json
-sys.path.insert(0, '.')
+import os; sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, scenarios, paper_cs_0105004_b200 as tsim
 scn = scenarios.config('4a')
 for gc in [int(a) for a in sys.argv[1:]]:
