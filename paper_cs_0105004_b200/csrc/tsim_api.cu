@@ -61,18 +61,22 @@ struct ts_sim {
   std::vector<int32_t> halo_up, halo_dn;
   WarpLayout lay{};
   int threads = 256, blocks = 1, smem = 0;
-  bool fused = false;
-  bool rows_mode = false, node_warp = false;
-  std::vector<int32_t> pw;  // row mode: plane word offset per tile
-  int64_t plane_words = 0;
+  bool gfused = false, rfused = false, node_warp = false;
+  // general tiles (halo / long / periodic links): byte codes at device
+  // offsets of their own; uploaded as d_tiles
+  std::vector<TileDesc> gtiles;
+  std::vector<int32_t> tile_g;  // tile -> index in gtiles, or -1
+  int64_t gcells = 0;
+  // row tiles (whole links of <= kRowMaxCells cells): k_rows
+  std::vector<int32_t> tile_row;  // tile -> global row slot of its lane 0, or -1
+  std::vector<RowDesc> rows;      // ngroups * 32 slots
+  int32_t ngroups = 0;
+  int64_t rvid_entries = 0;
   uint32_t *d_planes[2] = {nullptr, nullptr};
-  int32_t *d_pw = nullptr;
-  std::vector<GroupDesc> groups;
-  std::vector<uint8_t> rowmap;
-  int rows_cmax = 0, rows_threads = 128, rows_blocks = 1, rows_smem = 0;
-  RowsLayout rlay{};
-  GroupDesc *d_groups = nullptr;
-  uint8_t *d_rowmap = nullptr;
+  int32_t *d_rvid[2] = {nullptr, nullptr};
+  int32_t *d_inj_scratch = nullptr;
+  RowDesc *d_rows = nullptr;
+  int rows_threads = 128, rows_blocks = 1;
   NodeLane *d_nlanes = nullptr;
   int32_t *d_chunk_off = nullptr;
   int32_t nchunks = 0;
@@ -95,7 +99,7 @@ struct ts_sim {
   unsigned long long *d_stats = nullptr, *d_work = nullptr, *d_hash = nullptr;
   int32_t *d_in_off = nullptr, *d_in_list = nullptr, *d_out_off = nullptr, *d_out_list = nullptr;
   int32_t *d_ncell = nullptr, *d_lanes = nullptr, *d_lgid = nullptr, *d_cls = nullptr;
-  int cur = 0;
+  int gcur = 0, rcur = 0;  // current buffer of the general / row state
   int32_t t = 0;
   int64_t veh_updates = 0, arrived = 0, injected = 0, n_placed = 0;
   // timing
@@ -398,70 +402,55 @@ static void build_tiles(ts_sim *h) {
       if (d.flags & kHasDn) h->halo_dn[d.strip] = h->tiles[t0 + (i + 1) % nt].strip;
     }
   }
+  // classify: whole non-periodic links of <= kRowMaxCells cells and <= 32
+  // lanes run in k_rows (row tiles, lanes of a link on consecutive slots of
+  // one 32-slot group); everything else runs in the general kernels
+  const bool allow_rows = !(h->cfg.flags & TS_FLAG_GENERAL);
+  h->tile_g.assign(h->tiles.size(), -1);
+  h->tile_row.assign(h->tiles.size(), -1);
+  h->gtiles.clear();
+  h->rows.clear();
+  int64_t goff = 0, voff = 0;
+  int slot = 32;
+  for (size_t i = 0; i < h->tiles.size(); i++) {
+    const TileDesc &d = h->tiles[i];
+    const bool row = allow_rows && !(d.flags & kHalo) && (d.flags & kFirst) && (d.flags & kLast) &&
+                     d.w <= kRowMaxCells && d.L <= 32;
+    if (!row) {
+      TileDesc gd = d;
+      gd.off = goff;
+      goff += tile_cells_padded(d.w, d.L);
+      h->tile_g[i] = (int32_t)h->gtiles.size();
+      h->gtiles.push_back(gd);
+      continue;
+    }
+    if (slot + d.L > 32) {
+      h->rows.resize(h->rows.size() + 32, RowDesc{0, 0, 0, 0, 0, 0, 1});
+      slot = 0;
+    }
+    const size_t base = h->rows.size() - 32;
+    h->tile_row[i] = (int32_t)(base + slot);
+    for (int l = 0; l < d.L; l++) {
+      RowDesc &r = h->rows[base + slot + l];
+      r.voff = (int32_t)voff;
+      r.link = d.link;
+      r.lg = d.lane_gid + l;
+      r.w = (uint8_t)d.w;
+      r.l = (uint8_t)l;
+      r.L = (uint8_t)d.L;
+      r.vk = (uint8_t)h->vmax[d.link];
+      voff += row_pitch(d.w);
+    }
+    slot += d.L;
+  }
+  h->ngroups = (int32_t)(h->rows.size() / 32);
+  h->gcells = goff + 16;
+  h->rvid_entries = voff + 16;
   int nc_max = 32;
-  for (const TileDesc &d : h->tiles) nc_max = std::max(nc_max, (int)d.L * tile_stride(d.w, d.flags));
+  for (const TileDesc &d : h->gtiles) nc_max = std::max(nc_max, (int)d.L * tile_stride(d.w, d.flags));
   h->lay = warp_layout(nc_max);
-  h->fused = (h->cfg.flags & TS_FLAG_FUSED) && h->nstrips == 0;
-  h->rows_mode = h->nstrips == 0 && !(h->cfg.flags & TS_FLAG_GENERAL);
-  // row groups for k_rows: consecutive whole-link tiles, <= 32 rows and
-  // <= kGroupCells cells per warp
-  h->rows_mode = h->nstrips == 0 && !(h->cfg.flags & TS_FLAG_GENERAL);
-  h->groups.clear();
-  h->rowmap.clear();
-  h->pw.clear();
-  if (h->rows_mode) {
-    // bit-plane offsets of every tile (4 planes, 16-byte aligned)
-    int64_t pwo = 0;
-    for (const TileDesc &d : h->tiles) {
-      h->pw.push_back((int32_t)pwo);
-      pwo += tile_pwords(d.w, d.L);
-    }
-    h->plane_words = pwo + 4;
-    const int kGroupWords = (h->cfg.group_cells > 0 ? std::min(16384, h->cfg.group_cells) : 2048) / 32;
-    size_t i = 0;
-    int ngmax = 4;
-    while (i < h->tiles.size()) {
-      GroupDesc g{};
-      g.t0 = (int32_t)i;
-      int rows = 0, words = 0;
-      while (i < h->tiles.size()) {
-        const TileDesc &d = h->tiles[i];
-        const int c = tile_words(d.w, d.L);
-        if (g.ntiles > 0 && (rows + d.L > 32 || words + c > kGroupWords)) break;
-        for (int l = 0; l < d.L; l++) h->rowmap.push_back((uint8_t)((g.ntiles << 3) | l));
-        rows += d.L;
-        words += c;
-        g.ntiles++;
-        i++;
-      }
-      for (int r = rows; r < 32; r++) h->rowmap.push_back(0);
-      g.nrows = (int16_t)rows;
-      g.nwg = words;
-      ngmax = std::max(ngmax, words);
-      h->groups.push_back(g);
-    }
-    h->rows_cmax = ngmax;  // max words per plane in a group
-  }
-}
-
-// ----- row-mode state <-> host (codes are velocity | out-slot << 3)
-static int64_t vid_row(const ts_sim *h, const TileDesc &d, int l) {
-  return d.off + (int64_t)l * row_pitch(d.w);
-}
-
-// injection capacity of each row group: at most min(pending, cells) per link
-static int group_inj_caps(ts_sim *h, const std::vector<int32_t> &pend_off) {
-  int cap = 1;
-  for (GroupDesc &g : h->groups) {
-    int64_t c = 0;
-    for (int i = 0; i < g.ntiles; i++) {
-      const TileDesc &d = h->tiles[g.t0 + i];
-      c += std::min<int64_t>(pend_off[d.link + 1] - pend_off[d.link], d.w);
-    }
-    g.inj_cap = (int32_t)c;
-    cap = std::max<int64_t>(cap, c);
-  }
-  return cap;
+  h->gfused = (h->cfg.flags & TS_FLAG_FUSED) && h->nstrips == 0;
+  h->rfused = (h->cfg.flags & TS_FLAG_FUSED) != 0;
 }
 
 // incoming lanes of every node in priority order (R9: major class first,
@@ -514,7 +503,7 @@ static int first_slot(const ts_sim *h, int f) {
 static StepParams step_params(ts_sim *h, int t, int mode) {
   StepParams P{};
   P.tiles = h->d_tiles;
-  P.ntiles = (int32_t)h->tiles.size();
+  P.ntiles = (int32_t)h->gtiles.size();
   P.t = t;
   P.mode = mode;
   P.D = h->cfg.desperation_D;
@@ -522,12 +511,12 @@ static StepParams step_params(ts_sim *h, int t, int mode) {
   P.k1 = (uint32_t)(h->cfg.seed >> 32);
   P.p32 = h->p32;
   P.lay = h->lay;
-  P.code_in = h->d_code[h->cur];
-  P.code_out = h->d_code[h->cur ^ 1];
-  P.vid_in = h->d_vid[h->cur];
-  P.vid_out = h->d_vid[h->cur ^ 1];
-  P.strip_in = h->d_strip[h->cur];
-  P.strip_out = h->d_strip[h->cur ^ 1];
+  P.code_in = h->d_code[h->gcur];
+  P.code_out = h->d_code[h->gcur ^ 1];
+  P.vid_in = h->d_vid[h->gcur];
+  P.vid_out = h->d_vid[h->gcur ^ 1];
+  P.strip_in = h->d_strip[h->gcur];
+  P.strip_out = h->d_strip[h->gcur ^ 1];
   P.halo_up = h->d_halo_up;
   P.halo_dn = h->d_halo_dn;
   P.vmax_link = h->d_vmax;
@@ -584,13 +573,13 @@ static NodeParams node_params(ts_sim *h, int t) {
 
 static RowsParams rows_params(ts_sim *h) {
   RowsParams r{};
-  r.groups = h->d_groups;
-  r.rowmap = h->d_rowmap;
-  r.pw = h->d_pw;
-  r.planes_in = h->d_planes[h->cur];
-  r.planes_out = h->d_planes[h->cur ^ 1];
-  r.ngroups = (int32_t)h->groups.size();
-  r.lay = h->rlay;
+  r.rows = h->d_rows;
+  r.planes_in = h->d_planes[h->rcur];
+  r.planes_out = h->d_planes[h->rcur ^ 1];
+  r.vid_in = h->d_rvid[h->rcur];
+  r.vid_out = h->d_rvid[h->rcur ^ 1];
+  r.inj_scratch = h->d_inj_scratch;
+  r.ngroups = h->ngroups;
   return r;
 }
 
@@ -647,39 +636,55 @@ int ts_init(ts_sim *h, int32_t t0) {
   }
   std::vector<int32_t>().swap(cellvid);
   h->n_placed = (int64_t)h->pl_vid.size();
-  std::vector<uint32_t> planes;
-  if (h->rows_mode) {
-    // row mode: bit-planes O, V0, V1, V2 per tile; list entries vid | slot << 27
-    if (h->nv > (int32_t)kVidMask) return fail(h, TS_EINVAL, "too many vehicles for row mode");
-    planes.assign(h->plane_words, 0u);
-    for (size_t ti = 0; ti < h->tiles.size(); ti++) {
-      const TileDesc &d = h->tiles[ti];
-      const int Wp = row_pitch(d.w), nwt = tile_words(d.w, d.L);
-      uint32_t *pl = planes.data() + h->pw[ti];
-      for (int l = 0; l < d.L; l++) {
-        int64_t r = d.off + (int64_t)l * Wp;
-        for (int x = 0; x < d.w; x++) {
-          const uint8_t c = code[d.off + (int64_t)l * Wp + x];
-          if (c == kEmpty) continue;
-          const int b = l * d.w + x;
-          pl[b >> 5] |= 1u << (b & 31);
-          for (int k = 0; k < 3; k++)
-            if ((c >> k) & 1) pl[(k + 1) * nwt + (b >> 5)] |= 1u << (b & 31);
-          // allowed-lane class (R7): 0 all, 1 curb (right turn), 2 median (left)
-          const int slot = c >> 3;
-          int cls = 0;
-          if (slot != kSlotFinal) {
-            const int tty = (h->tt[d.link] >> (2 * slot)) & 3;
-            cls = tty == 0 ? 0 : (tty == 2 ? 1 : 2);
-          }
-          for (int k = 0; k < 2; k++)
-            if ((cls >> k) & 1) pl[(k + 4) * nwt + (b >> 5)] |= 1u << (b & 31);
-          vids[r] = (int32_t)((uint32_t)vids[r] | ((uint32_t)(c >> 3) << kSlotShift));
-          r++;
+  // general tiles: the byte layout at their own device offsets
+  std::vector<uint8_t> gcode(h->gcells, kEmpty);
+  std::vector<int32_t> gvid(h->gcells, -1);
+  for (size_t ti = 0; ti < h->tiles.size(); ti++) {
+    if (h->tile_g[ti] < 0) continue;
+    const TileDesc &d = h->tiles[ti], &gd = h->gtiles[h->tile_g[ti]];
+    const int64_t n = (int64_t)d.L * row_pitch(d.w);
+    std::copy(code.begin() + d.off, code.begin() + d.off + n, gcode.begin() + gd.off);
+    std::copy(vids.begin() + d.off, vids.begin() + d.off + n, gvid.begin() + gd.off);
+  }
+  // row tiles: bit-planes O, V0..V2, A0, A1 per row (group-interleaved);
+  // list entries vid | slot << 27
+  if (h->ngroups > 0 && h->nv > (int32_t)kVidMask)
+    return fail(h, TS_EINVAL, "too many vehicles for the row kernel");
+  if (h->rvid_entries > INT32_MAX) return fail(h, TS_EINVAL, "network too large for one device");
+  std::vector<uint32_t> planes(group_plane_base(h->ngroups), 0u);
+  std::vector<int32_t> rvid(h->rvid_entries, -1);
+  for (size_t ti = 0; ti < h->tiles.size(); ti++) {
+    if (h->tile_row[ti] < 0) continue;
+    const TileDesc &d = h->tiles[ti];
+    const int Wp = row_pitch(d.w);
+    for (int l = 0; l < d.L; l++) {
+      const int s = h->tile_row[ti] + l;
+      uint32_t *pl = planes.data() + group_plane_base(s >> 5) + (s & 31);
+      const RowDesc &rd = h->rows[s];
+      int64_t r = d.off + (int64_t)l * Wp, k = 0;
+      for (int x = 0; x < d.w; x++) {
+        const uint8_t c = code[d.off + (int64_t)l * Wp + x];
+        if (c == kEmpty) continue;
+        const uint32_t bit = 1u << (x & 31);
+        const int wd = x >> 5;
+        pl[(0 * kRowWords + wd) * 32] |= bit;
+        for (int b = 0; b < 3; b++)
+          if ((c >> b) & 1) pl[((1 + b) * kRowWords + wd) * 32] |= bit;
+        // allowed-lane class (R7): 0 all, 1 curb (right turn), 2 median (left)
+        const int slot = c >> 3;
+        int cls = 0;
+        if (slot != kSlotFinal) {
+          const int tty = (h->tt[d.link] >> (2 * slot)) & 3;
+          cls = tty == 0 ? 0 : (tty == 2 ? 1 : 2);
         }
+        for (int b = 0; b < 2; b++)
+          if ((cls >> b) & 1) pl[((4 + b) * kRowWords + wd) * 32] |= bit;
+        rvid[rd.voff + k++] = (int32_t)((uint32_t)vids[r++] | ((uint32_t)slot << kSlotShift));
       }
     }
   }
+  std::vector<uint8_t>().swap(code);
+  std::vector<int32_t>().swap(vids);
   // pending lists per first link in (departure, vid) order (R13)
   std::vector<int32_t> pend_off(h->nl + 1, 0), pend_list;
   for (int f = 0; f < h->nv; f++)
@@ -703,21 +708,32 @@ int ts_init(ts_sim *h, int32_t t0) {
   for (int k = 0; k < h->nl; k++) vmax8[k] = (uint8_t)h->vmax[k];
   // device
   int rc;
-  if ((rc = upload(h, &h->d_tiles, h->tiles))) return rc;
+  if ((rc = upload(h, &h->d_tiles, h->gtiles))) return rc;
   for (int b = 0; b < 2; b++) {
-    if ((rc = dalloc(h, &h->d_code[b], h->rows_mode ? 16 : h->total_cells, 0xFF))) return rc;
-    if ((rc = dalloc(h, &h->d_vid[b], h->total_cells, 0xFF))) return rc;
+    if ((rc = dalloc(h, &h->d_code[b], h->gtiles.empty() ? 16 : h->gcells, 0xFF))) return rc;
+    if ((rc = dalloc(h, &h->d_vid[b], h->gtiles.empty() ? 16 : h->gcells, 0xFF))) return rc;
     if ((rc = dalloc(h, &h->d_strip[b], std::max(1, h->nstrips), 0xFF))) return rc;
-    if (h->rows_mode && (rc = dalloc(h, &h->d_planes[b], h->plane_words, 0))) return rc;
+    if ((rc = dalloc(h, &h->d_planes[b], std::max<size_t>(16, planes.size()), 0))) return rc;
+    if ((rc = dalloc(h, &h->d_rvid[b], h->rvid_entries, 0xFF))) return rc;
   }
-  if (h->rows_mode) {
-    if ((rc = upload(h, &h->d_pw, h->pw))) return rc;
+  if (!h->gtiles.empty()) {
+    CK(h, cudaMemcpyAsync(h->d_code[0], gcode.data(), gcode.size(), cudaMemcpyHostToDevice, h->stream));
+    CK(h, cudaMemcpyAsync(h->d_vid[0], gvid.data(), gvid.size() * 4, cudaMemcpyHostToDevice, h->stream));
+  }
+  if (h->ngroups > 0) {
+    if ((rc = upload(h, &h->d_rows, h->rows))) return rc;
     CK(h, cudaMemcpyAsync(h->d_planes[0], planes.data(), planes.size() * 4, cudaMemcpyHostToDevice,
                           h->stream));
-  } else {
-    CK(h, cudaMemcpyAsync(h->d_code[0], code.data(), code.size(), cudaMemcpyHostToDevice, h->stream));
+    CK(h, cudaMemcpyAsync(h->d_rvid[0], rvid.data(), rvid.size() * 4, cudaMemcpyHostToDevice,
+                          h->stream));
   }
-  CK(h, cudaMemcpyAsync(h->d_vid[0], vids.data(), vids.size() * 4, cudaMemcpyHostToDevice, h->stream));
+  {  // injection scratch of the row kernel: needed only if a row link has pending trips
+    bool need = false;
+    for (size_t ti = 0; ti < h->tiles.size() && !need; ti++)
+      if (h->tile_row[ti] >= 0 && pend_off[h->tiles[ti].link + 1] > pend_off[h->tiles[ti].link])
+        need = true;
+    if ((rc = dalloc(h, &h->d_inj_scratch, need ? h->rvid_entries : 16, 0xFF))) return rc;
+  }
   if ((rc = upload(h, &h->d_halo_up, h->halo_up))) return rc;
   if ((rc = upload(h, &h->d_halo_dn, h->halo_dn))) return rc;
   if ((rc = upload(h, &h->d_vmax, vmax8))) return rc;
@@ -760,20 +776,11 @@ int ts_init(ts_sim *h, int32_t t0) {
   int nsm = 148;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->dev);
   int occ = std::max(1, occupancy_blocks(h->threads, h->smem));
-  const int need = (int)((h->tiles.size() + wpb - 1) / wpb);
+  const int need = (int)((h->gtiles.size() + wpb - 1) / wpb);
   h->blocks = std::max(1, std::min(need, occ * nsm));
-  if (h->rows_mode) {
-    h->rlay = rows_layout(h->rows_cmax, group_inj_caps(h, pend_off));
-    if ((rc = upload(h, &h->d_groups, h->groups))) return rc;
-    if ((rc = upload(h, &h->d_rowmap, h->rowmap))) return rc;
-    const int rw = std::max(1, std::min(4, (200 * 1024) / h->rlay.bytes));
-    h->rows_threads = 32 * rw;
-    h->rows_smem = rw * h->rlay.bytes;
-    CK(h, set_rows_smem(h->rows_smem));
-    const int rocc = std::max(1, occupancy_rows(h->rows_threads, h->rows_smem));
-    const int rneed = (int)((h->groups.size() + rw - 1) / rw);
-    h->rows_blocks = std::max(1, std::min(rneed, rocc * nsm));
-  }
+  // row kernel: one warp per 32-row group, 4 warps per block
+  h->rows_threads = 128;
+  h->rows_blocks = std::max(1, (h->ngroups + 3) / 4);
   {
     std::vector<NodeLane> nlanes;
     std::vector<int32_t> chunk_off;
@@ -786,16 +793,20 @@ int ts_init(ts_sim *h, int32_t t0) {
     }
   }
   // initial injection: departure <= t0 (O1 §Init), S(t0) into buffer 1
-  h->cur = 0;
+  h->gcur = 0;
+  h->rcur = 0;
   if (zero_stats(h, t0, 1)) return TS_EINTERNAL;
   int mode = kModeInject | (base_mode(h) & kModeHash);
   StepParams P = step_params(h, t0 - 1, mode);
-  if (h->rows_mode)
-    launch_rows(P, rows_params(h), h->rows_blocks, h->rows_threads, h->rows_smem, h->stream);
-  else
+  if (h->ngroups > 0) {
+    launch_rows(P, rows_params(h), h->rows_blocks, h->rows_threads, 0, h->stream);
+    h->rcur ^= 1;
+  }
+  if (!h->gtiles.empty()) {
     launch_step(P, h->blocks, h->threads, h->smem, h->stream);
+    h->gcur ^= 1;
+  }
   CK(h, cudaGetLastError());
-  h->cur ^= 1;
   h->t = t0;
   CK(h, cudaStreamSynchronize(h->stream));
   unsigned long long st[ST_N];
@@ -828,34 +839,41 @@ static int enqueue_steps(ts_sim *h, int32_t n) {
   }
   CK(h, cudaEventRecord(h->ev0, h->stream));
   const int t = h->t;
-  // lane change of step t on S(t) (general: k_lc; row mode: k_rows in
-  // lane-change-only mode)
-  auto lane_change = [&](int ts) {
-    if (h->rows_mode)
-      launch_rows(step_params(h, ts, kModeLC), rows_params(h), h->rows_blocks, h->rows_threads,
-                  h->rows_smem, h->stream);
-    else
-      launch_lc(step_params(h, ts, 0), h->blocks, h->threads, h->smem, h->stream);
-    h->cur ^= 1;
+  const bool gen = !h->gtiles.empty(), rows = h->ngroups > 0;
+  // lane change of step t on S(t): general tiles (k_lc) and row tiles
+  // (k_rows in lane-change-only mode)
+  auto lc_gen = [&](int ts) {
+    launch_lc(step_params(h, ts, 0), h->blocks, h->threads, h->smem, h->stream);
+    h->gcur ^= 1;
   };
-  if (h->fused) lane_change(t);
+  auto lc_rows = [&](int ts) {
+    launch_rows(step_params(h, ts, kModeLC), rows_params(h), h->rows_blocks, h->rows_threads, 0,
+                h->stream);
+    h->rcur ^= 1;
+  };
+  if (gen && h->gfused) lc_gen(t);
+  if (rows && h->rfused) lc_rows(t);
   for (int i = 0; i < n; i++) {
-    if (!h->fused) lane_change(t + i);
+    if (gen && !h->gfused) lc_gen(t + i);
+    if (rows && !h->rfused) lc_rows(t + i);
     if (h->node_warp)
       launch_node_warp(node_params(h, t + i), NodeWarpParams{h->d_nlanes, h->d_chunk_off, h->nchunks},
                        h->stream);
     else
       launch_node(node_params(h, t + i), h->stream);
-    int m = mode;
-    if (h->fused && i < n - 1) m |= kModeLC;
     if (h->timing) CK(h, cudaEventRecord(h->mv_ev[2 * i], h->stream));
-    if (h->rows_mode)
-      launch_rows(step_params(h, t + i, m), rows_params(h), h->rows_blocks, h->rows_threads,
-                  h->rows_smem, h->stream);
-    else
+    if (rows) {
+      const int m = mode | (h->rfused && i < n - 1 ? kModeLC : 0);
+      launch_rows(step_params(h, t + i, m), rows_params(h), h->rows_blocks, h->rows_threads, 0,
+                  h->stream);
+      h->rcur ^= 1;
+    }
+    if (gen) {
+      const int m = mode | (h->gfused && i < n - 1 ? kModeLC : 0);
       launch_step(step_params(h, t + i, m), h->blocks, h->threads, h->smem, h->stream);
+      h->gcur ^= 1;
+    }
     if (h->timing) CK(h, cudaEventRecord(h->mv_ev[2 * i + 1], h->stream));
-    h->cur ^= 1;
   }
   CK(h, cudaEventRecord(h->ev1, h->stream));
   CK(h, cudaGetLastError());
@@ -933,30 +951,66 @@ static int download_tiles(ts_sim *h, int t0, int t1, std::vector<uint8_t> &code,
   const int64_t c1 = t1 < (int)h->tiles.size() ? h->tiles[t1].off : h->total_cells;
   code.assign(c1 - c0, kEmpty);
   vids.assign(c1 - c0, -1);
-  CK(h, cudaMemcpy(vids.data(), h->d_vid[h->cur] + c0, (c1 - c0) * 4, cudaMemcpyDeviceToHost));
-  if (!h->rows_mode) {
-    CK(h, cudaMemcpy(code.data(), h->d_code[h->cur] + c0, c1 - c0, cudaMemcpyDeviceToHost));
-    return TS_OK;
-  }
-  const int64_t p0 = h->pw[t0];
-  const int64_t p1 = t1 < (int)h->tiles.size() ? h->pw[t1] : h->plane_words;
-  std::vector<uint32_t> pl(p1 - p0);
-  CK(h, cudaMemcpy(pl.data(), h->d_planes[h->cur] + p0, (p1 - p0) * 4, cudaMemcpyDeviceToHost));
+  // general tiles of the range: one contiguous device range
+  int g0 = -1, g1 = -1, s0 = -1, s1 = -1;
   for (int ti = t0; ti < t1; ti++) {
-    const TileDesc &d = h->tiles[ti];
-    const int nwt = tile_words(d.w, d.L), Wp = row_pitch(d.w);
-    const uint32_t *P = pl.data() + (h->pw[ti] - p0);
-    for (int l = 0; l < d.L; l++) {
-      const int64_t rb = d.off - c0 + (int64_t)l * Wp;
-      int64_t r = rb;
-      for (int x = 0; x < d.w; x++) {
-        const int b = l * d.w + x, wd = b >> 5, bt = b & 31;
-        if (!((P[wd] >> bt) & 1u)) continue;
-        const int v = (int)((P[nwt + wd] >> bt) & 1u) | (int)(((P[2 * nwt + wd] >> bt) & 1u) << 1) |
-                      (int)(((P[3 * nwt + wd] >> bt) & 1u) << 2);
-        const uint32_t e = (uint32_t)vids[r];
-        code[rb + x] = (uint8_t)(v | ((e >> kSlotShift) << 3));
-        vids[r++] = (int32_t)(e & kVidMask);
+    if (h->tile_g[ti] >= 0) {
+      if (g0 < 0) g0 = h->tile_g[ti];
+      g1 = h->tile_g[ti] + 1;
+    }
+    if (h->tile_row[ti] >= 0) {
+      if (s0 < 0) s0 = h->tile_row[ti];
+      s1 = h->tile_row[ti] + h->tiles[ti].L;
+    }
+  }
+  if (g0 >= 0) {
+    const TileDesc &la = h->gtiles[g1 - 1];
+    const int64_t a = h->gtiles[g0].off, b = la.off + tile_cells_padded(la.w, la.L);
+    std::vector<uint8_t> gc(b - a);
+    std::vector<int32_t> gv(b - a);
+    CK(h, cudaMemcpy(gc.data(), h->d_code[h->gcur] + a, b - a, cudaMemcpyDeviceToHost));
+    CK(h, cudaMemcpy(gv.data(), h->d_vid[h->gcur] + a, (b - a) * 4, cudaMemcpyDeviceToHost));
+    for (int ti = t0; ti < t1; ti++) {
+      if (h->tile_g[ti] < 0) continue;
+      const TileDesc &d = h->tiles[ti];
+      const int64_t n = (int64_t)d.L * row_pitch(d.w), src = h->gtiles[h->tile_g[ti]].off - a;
+      std::copy(gc.begin() + src, gc.begin() + src + n, code.begin() + (d.off - c0));
+      std::copy(gv.begin() + src, gv.begin() + src + n, vids.begin() + (d.off - c0));
+    }
+  }
+  if (s0 >= 0) {
+    // row tiles: planes of the covering groups and the span of their vid lists
+    const int gr0 = s0 >> 5, gr1 = ((s1 - 1) >> 5) + 1;
+    int64_t va = INT64_MAX, vb = 0;
+    for (int s = s0; s < s1; s++) {
+      va = std::min<int64_t>(va, h->rows[s].voff);
+      vb = std::max<int64_t>(vb, h->rows[s].voff + row_pitch(h->rows[s].w));
+    }
+    std::vector<uint32_t> pl(group_plane_base(gr1) - group_plane_base(gr0));
+    std::vector<int32_t> rv(vb - va);
+    CK(h, cudaMemcpy(pl.data(), h->d_planes[h->rcur] + group_plane_base(gr0), pl.size() * 4,
+                     cudaMemcpyDeviceToHost));
+    CK(h, cudaMemcpy(rv.data(), h->d_rvid[h->rcur] + va, rv.size() * 4, cudaMemcpyDeviceToHost));
+    for (int ti = t0; ti < t1; ti++) {
+      if (h->tile_row[ti] < 0) continue;
+      const TileDesc &d = h->tiles[ti];
+      const int Wp = row_pitch(d.w);
+      for (int l = 0; l < d.L; l++) {
+        const int s = h->tile_row[ti] + l;
+        const uint32_t *P = pl.data() + (group_plane_base(s >> 5) - group_plane_base(gr0)) + (s & 31);
+        const int32_t *lst = rv.data() + (h->rows[s].voff - va);
+        const int64_t rb = d.off - c0 + (int64_t)l * Wp;
+        int64_t r = rb, k = 0;
+        for (int x = 0; x < d.w; x++) {
+          const int wd = x >> 5, bt = x & 31;
+          if (!((P[wd * 32] >> bt) & 1u)) continue;
+          const int v = (int)((P[(kRowWords + wd) * 32] >> bt) & 1u) |
+                        (int)(((P[(2 * kRowWords + wd) * 32] >> bt) & 1u) << 1) |
+                        (int)(((P[(3 * kRowWords + wd) * 32] >> bt) & 1u) << 2);
+          const uint32_t e = (uint32_t)lst[k++];
+          code[rb + x] = (uint8_t)(v | ((e >> kSlotShift) << 3));
+          vids[r++] = (int32_t)(e & kVidMask);
+        }
       }
     }
   }
@@ -1057,8 +1111,8 @@ int ts_state_hash(ts_sim *h, uint64_t *out) {
   CK(h, cudaSetDevice(h->dev));
   CK(h, cudaMemsetAsync(h->d_hash, 0, 16, h->stream));
   StepParams P = step_params(h, h->t, 0);
-  if (h->rows_mode) launch_rows_hash(P, rows_params(h), h->stream, h->d_hash);
-  else launch_hash(P, h->blocks, h->threads, h->smem, h->stream, h->d_hash);
+  if (h->ngroups > 0) launch_rows_hash(P, rows_params(h), h->stream, h->d_hash);
+  if (!h->gtiles.empty()) launch_hash(P, h->blocks, h->threads, h->smem, h->stream, h->d_hash);
   CK(h, cudaGetLastError());
   unsigned long long r[2];
   CK(h, cudaMemcpyAsync(r, h->d_hash, 16, cudaMemcpyDeviceToHost, h->stream));

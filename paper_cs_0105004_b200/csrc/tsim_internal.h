@@ -72,94 +72,37 @@ __host__ __device__ inline int64_t tile_cells_padded(int w, int L) {
 }
 
 // ---------------------------------------------------------------- row mode
-// Fast path for networks whose tiles are all whole links.
-// The lane-cells of a tile are bits: cell (l, x) is bit l*w + x of the
-// tile's nwt = ceil(L*w/32) words, in six planes stored plane-major at
-// planes[pw + p*nwt + j]: occupancy O, the velocity bits V0, V1, V2 and the
-// vehicle's allowed-lane class A0, A1 (0 all lanes, 1 curb lane, 2 median
-// lane; reading R7) for its current link.
-// The vehicles of each lane-row are listed in cell order at
-// vid[off + l*Wp + k] as entries vid | slot << 27 (the out-slot travels
-// with the vehicle in its list entry; list order is preserved by the move).
+// Fast path for whole links of <= kRowMaxCells cells: one
+// thread per lane-row ("row"), the lanes of a link on consecutive threads
+// of one warp, 32 row slots per group (one warp).  A row's state is six
+// bit-planes of kRowWords 32-bit words each -- occupancy O, velocity bits
+// V0..V2 and the vehicle's allowed-lane class A0/A1 (0 all lanes, 1 curb
+// lane, 2 median lane; reading R7) for its current link -- bit x of word
+// x >> 5 being cell x.  Planes are stored group-interleaved so that every
+// warp access is one contiguous 128-byte line:
+//   planes[group_plane_base(g) + (p * kRowWords + i) * 32 + slot].
+// The vehicles of a row are listed in cell order at vid[voff + k] as
+// entries vid | slot << 27 (the out-slot travels with the vehicle in its
+// list entry; list order is preserved by the move).
 constexpr int kSlotShift = 27;
 constexpr uint32_t kVidMask = (1u << kSlotShift) - 1u;
-
-__host__ __device__ inline int tile_words(int w, int L) { return (L * w + 31) >> 5; }
+constexpr int kRowWords = 4;
+constexpr int kRowMaxCells = 32 * kRowWords;
 constexpr int kStatePlanes = 6;
-__host__ __device__ inline int tile_pwords(int w, int L) {
-  return (kStatePlanes * tile_words(w, L) + 3) & ~3;
+
+__host__ __device__ inline size_t group_plane_base(int64_t g) {
+  return (size_t)g * kStatePlanes * kRowWords * 32;
 }
 
-// k_rows: one warp per group of consecutive tiles with <= 32 rows; the
-// group's words are numbered consecutively (tile after tile).
-struct GroupDesc {
-  int32_t t0;
-  int16_t ntiles;
-  int16_t nrows;
-  int32_t nwg;      // words per plane in the group
-  int32_t inj_cap;  // bound on vehicles the group can inject in one step
+struct RowDesc {
+  int32_t voff;  // first entry of the row's vid list (multiple of 4)
+  int32_t link;
+  int32_t lg;    // global lane id
+  uint8_t w;     // cells (0 = empty slot)
+  uint8_t l, L;  // lane, lanes of the link
+  uint8_t vk;    // vmax of the link
 };
-
-// smem planes of one group, NG words each (+ pad words).  The overlays
-// reuse storage that is dead by the time they are written: U1..U5 after
-// the hop, the input velocity bits after the row-front fix-up.
-enum {
-  PL_O = 0,                   // input occupancy
-  PL_V0, PL_V1, PL_V2,        // input velocity bits
-  PL_A0, PL_A1,               // input allowed-lane class
-  PL_U1, PL_U2, PL_U3, PL_U4, PL_U5,  // v2 >= k (thermometer)
-  PL_B,                       // random slowdown
-  PL_RE, PL_RS, PL_ZN,        // static: last cell / first cell of a row, last D cells
-  PL_OO, PL_OV0, PL_OV1, PL_OV2, PL_OA0, PL_OA1,  // S(t+1) before its lane change
-  PL_LR,                      // left the row (exit / node crossing)
-  PL_NUM,
-  PL_SP = PL_U1,              // entrant or injected vehicle
-  PL_LV = PL_U2,              // lane change: leaves this cell
-  PL_FIN = PL_U3,             // final occupancy
-  PL_WORK = PL_U4,            // scratch (rows whose vid list is rebuilt)
-  PL_CH = PL_U5,              // cells touched by a lane change (left or arrived)
-  PL_FV0 = PL_V0, PL_FV1 = PL_V1, PL_FV2 = PL_V2  // final velocity bits
-};
-
-struct RowsLayout {
-  int NG, PS, CMAX, injcap;
-  int o_planes, o_wp, o_wdesc, o_wrow, o_own, o_tiles, o_rows, o_ent, o_injx, o_injv, o_misc, bytes;
-};
-
-__host__ __device__ inline RowsLayout rows_layout(int ng, int injcap) {
-  RowsLayout l;
-  l.NG = (ng + 3) & ~3;
-  l.PS = l.NG + 4;  // pad word before, three after
-  l.CMAX = 32 * l.NG;
-  l.injcap = injcap;
-  int o = 0;
-  l.o_planes = o;
-  o += 4 * PL_NUM * l.PS;
-  l.o_wp = o;  // per-word exclusive popcount prefixes of three bitmaps
-  o += 3 * 2 * (l.NG + 4);
-  o = (o + 15) & ~15;
-  l.o_wdesc = o;  // word -> (tile << 8) | word in tile
-  o += 2 * l.NG;
-  l.o_wrow = o;  // word -> row holding its first cell
-  o += l.NG;
-  l.o_own = o;  // bit enumeration: lane owning each slot of a 32-slot window
-  o += 32;
-  o = (o + 15) & ~15;
-  l.o_tiles = o;  // 8 arrays of 32
-  o += 4 * 8 * 32;
-  l.o_rows = o;  // 12 arrays of 32
-  o += 4 * 12 * 32;
-  l.o_ent = o;  // entrant entry per row, entrant cell per row
-  o += 4 * 64;
-  l.o_injx = o;  // injected: (row << 16) | cell
-  o += 4 * injcap;
-  l.o_injv = o;  // injected entry
-  o += 4 * injcap;
-  l.o_misc = o;
-  o += 16;
-  l.bytes = (o + 127) & ~127;
-  return l;
-}
+static_assert(sizeof(RowDesc) == 16, "RowDesc must be 16 bytes");
 
 // Warp-cooperative node kernel: the incoming lanes of every node, in the
 // priority order (major class first, then link id, then lane; R9), packed
@@ -279,13 +222,13 @@ struct NodeParams {
 //   bits 0-31 vid, 32-39 code, 40-42 landing cell, 43-63 stamp (t+1)
 
 struct RowsParams {
-  const GroupDesc *groups;
-  const uint8_t *rowmap;
-  const int32_t *pw;  // plane word offset of every tile
-  const uint32_t *planes_in;
+  const RowDesc *rows;        // [ngroups * 32]
+  const uint32_t *planes_in;  // S1(t) (fused) or S(t)
   uint32_t *planes_out;
+  const int32_t *vid_in;      // row vid lists
+  int32_t *vid_out;
+  int32_t *inj_scratch;       // per lane-0 row cell: entry of a vehicle injected there
   int32_t ngroups;
-  RowsLayout lay;
 };
 
 struct NodeWarpParams {
