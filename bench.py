@@ -155,8 +155,7 @@ def bench_tsim(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if world > 1:
-        from paper_cs_0105004_b200 import dist
-        return dist.bench_multi(args)
+        return bench_multi(args)
     hbm_peak, peak_src = measured_peaks()
     t_gen = time.perf_counter()
     scn = workload(args.config)
@@ -227,6 +226,86 @@ def bench_tsim(args):
                                "sample": f"{r['steps']} steps of {r['desc']} "
                                          f"({r['lane_cells']} lane-cells), {r['seconds']:.1f} s"}
     print(json.dumps(out), flush=True)
+
+
+def bench_multi(args):
+    """N > 1: one process per GPU, one domain of an ORB partition per rank
+    (§4), two strip exchanges per step with the neighbour domains
+    over NCCL (NVLink).  The workload is the same as at N = 1 (strong
+    scaling); the step time is the max over ranks of the device-timed K
+    steps."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_cs_0105004_b200 as tsim
+    from paper_cs_0105004_b200 import domains
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    hbm_peak, peak_src = measured_peaks()
+    scn = workload(args.config)
+    dom = domains.partition(scn, world)
+    n_spl, pairs = domains.split_stats(scn, dom)
+    w0 = time.perf_counter()
+    d = domains.DistDomain(scn, dom, device=local, flags=tsim.FLAG_FUSED)
+    d.step(args.warmup)
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        t_from = d.t
+        e0.record(d.stream)
+        d.step(args.steps)
+        e1.record(d.stream)
+        torch.cuda.synchronize()
+    dist.barrier()
+    ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=f"cuda:{local}")
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    hist = d.sim.history(t_from, args.steps + 1)
+    tot = d.sim.totals()
+    vst = d.sim.vehicles()
+    e2e_local = time.perf_counter() - w0
+    loc = torch.tensor([float(np.sum(hist["active"][:args.steps])), float(tot["lane_cells"]),
+                        float(np.sum(hist["crossings"][1:])), e2e_local], dtype=torch.float64,
+                       device=f"cuda:{local}")
+    s = loc.clone()
+    dist.all_reduce(s, op=dist.ReduceOp.SUM)
+    e2e = loc[3:4].clone()
+    dist.all_reduce(e2e, op=dist.ReduceOp.MAX)
+    ms_total = float(ms.item())
+    updates, lane_cells, cross = float(s[0]), float(s[1]), float(s[2])
+    if rank == 0:
+        value = updates / (ms_total / 1e3)
+        alg = (2 * lane_cells * args.steps + 8 * updates + 12 * cross) / world
+        achieved = alg / (ms_total / 1e3) / 1e9
+        out = {
+            "metric": "vehicle-updates/s", "value": value, "unit": "vehicle-updates/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_total / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic (seeded generator, DESIGN.md §5)",
+            "config": {"workload": scn.name, "recipe": scn.recipe, "lane_cells": int(lane_cells),
+                       "vehicles": scn.n_vehicles,
+                       "l2": "inputs larger than L2 (state read+written per step > 126 MB)",
+                       "parallelism": f"{world} GPUs, ORB domains, split links, 2 NCCL strip "
+                                      f"exchanges per step", "split_links": n_spl,
+                       "domain_pairs": len(pairs)},
+            "real_time_ratio": args.steps / (ms_total / 1e3),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": achieved / hbm_peak, "traffic": None,
+                         "kernel": "whole step per GPU (incl. exchanges)",
+                         "alg_bytes_per_launch": alg / args.steps, "peak_source": peak_src},
+            "e2e": {"value": (updates) / float(e2e.item()), "unit": "vehicle-updates/s",
+                    "h2d_bytes_per_step": None, "d2h_bytes_per_step": sum(
+                        a.nbytes for a in vst.values()) / (args.steps + args.warmup),
+                    "wall_s": float(e2e.item()),
+                    "scope": "per rank: load+init+W+K steps+state readback, max over ranks"},
+            "clocks": clk.summary(),
+            "gpu_launches": 1 + 4 * args.steps,
+        }
+        print(json.dumps(out), flush=True)
+    dist.destroy_process_group()
 
 
 def main():

@@ -33,6 +33,7 @@ extern "C" {
 #define TS_PENDING 0
 #define TS_ACTIVE 1
 #define TS_ARRIVED 2
+#define TS_ABSENT 3 /* domain mode: the vehicle is reported by another domain */
 
 /* config flags */
 #define TS_FLAG_FUSED 1u       /* fuse lane change of step t+1 into the move
@@ -89,9 +90,47 @@ int ts_place_vehicles(ts_sim *h, int32_t n, const int32_t *vid,
                       const int32_t *lane, const int32_t *cell,
                       const int32_t *v);
 
+/* Placement on any link of the route (checkpoint restore, repartitioning):
+ * vehicle vid[i] stands on link route[cursor[i]] (cursor NULL = 0) at
+ * (lane, cell) with velocity v.  Vehicles neither placed nor marked arrived
+ * are pending. */
+int ts_place_vehicles_at(ts_sim *h, int32_t n, const int32_t *vid, const int32_t *cursor,
+                         const int32_t *lane, const int32_t *cell, const int32_t *v);
+/* Vehicles that already arrived (restore): vid[i] left at t_arrive[i]. */
+int ts_set_arrived(ts_sim *h, int32_t n, const int32_t *vid, const int32_t *t_arrive);
+
+/* Domain decomposition (§4, :366-452).  This handle simulates
+ * domain `me` of a k-way node partition domain_of_node[n_nodes] (e.g. from
+ * ts_orb_partition).  Call after ts_load_network, before ts_init.  Nodes
+ * are never split; a link with both end nodes in `me` is owned whole; a
+ * link whose end nodes lie in different domains is split at h = floor(n/2)
+ * (reading R16): cells [0, h) belong to the domain of its from-node,
+ * [h, n) to the domain of its to-node.  Every handle of a partition gets
+ * the same inputs (network, all vehicles, placement); each keeps only its
+ * own cells.  k = 1 is the undivided network.  TS_EINVAL: k < 1, me out of
+ * range, k > n_nodes, a ring network, a node's domain out of range.
+ * Results do not depend on k or the partition. */
+int ts_set_domain(ts_sim *h, int32_t k, const int32_t *domain_of_node, int32_t me);
+
+/* Pure host: the exchange partners of domain `me` (ascending domain id) and
+ * the number of strips of one message to / from each (one per lane of
+ * every split link the two share); a message is strips x ts_strip_bytes()
+ * bytes, the same in both directions.  cap bounds the outputs; *n_out
+ * receives the partner count.  No device needed. */
+int ts_domain_plan(int32_t n_nodes, int32_t n_links, const int32_t *from, const int32_t *to,
+                   const int64_t *length_mm, const int32_t *lanes, int32_t k,
+                   const int32_t *domain_of_node, int32_t me, int32_t cap, int32_t *nbr_dom,
+                   int64_t *nbr_strips, int32_t *n_out);
+int32_t ts_strip_bytes(void);
+
 /* Build the device layout, upload, and run the initial injection of
- * vehicles with departure <= t0 (clock starts at t0). */
+ * vehicles with departure <= t0 (clock starts at t0).  In domain mode with
+ * partners the boundary strips of S(t0) are packed at the end: exchange
+ * them (below), then call ts_step_phase(h, 2, 0). */
 int ts_init(ts_sim *h, int32_t t0);
+/* As ts_init without the initial injection: the placed / arrived /
+ * pending vehicles ARE the state S(t) (restore at time t). */
+int ts_resume(ts_sim *h, int32_t t);
 
 /* Advance n_steps one-second steps.  Synchronous. */
 int ts_step(ts_sim *h, int32_t n_steps);
@@ -101,12 +140,41 @@ int ts_step(ts_sim *h, int32_t n_steps);
 int ts_step_async(ts_sim *h, int32_t n_steps);
 int ts_sync(ts_sim *h);
 
+/* One step in three phases, for domains that exchange boundary strips
+ * (PAPER.md:412-427).  With S(t) and its mirrors in place:
+ *   phase 0: lane change (H1); packs exchange #1 (post-lane-change strips)
+ *   -- the caller moves every send segment to its partner's receive segment
+ *   phase 1: unpacks #1; intersections, velocity update, move, injection
+ *            (H3-H6); time becomes t+1; packs exchange #2.  more != 0: a
+ *            further step follows (lets whole-link tiles fuse the next lane
+ *            change into this move).
+ *   -- exchange
+ *   phase 2: unpacks #2.
+ * Kernels are enqueued on the handle's stream (ts_stream) in order. */
+int ts_step_phase(ts_sim *h, int32_t phase, int32_t more);
+
+/* Exchange plan after ts_init: partner domains, strips per message and the
+ * first strip of each partner's segment in the send / receive buffers. */
+int ts_exchange_plan(const ts_sim *h, int32_t cap, int32_t *nbr_dom, int64_t *nbr_strips,
+                     int64_t *nbr_off, int32_t *n_out);
+/* Device pointers of the packed send and receive buffers (owned by h). */
+int ts_exchange_buffers(ts_sim *h, void **send_dev, void **recv_dev);
+/* The CUDA stream (cudaStream_t) all of h's work is enqueued on. */
+void *ts_stream(const ts_sim *h);
+/* In-process exchange among the k handles of one partition (any devices):
+ * copies every send segment into its partner's receive segment, ordered by
+ * events after the senders' packs and before the receivers' next work. */
+int ts_exchange_local(ts_sim **hs, int32_t k);
+
 /* current time t (state is S(t)) */
 int32_t ts_time(const ts_sim *h);
 
 /* Per-vehicle state, arrays of n_vehicles entries (NULL to skip): status
  * (TS_*), link, lane, cell, v (-1 unless active), route cursor (-1 while
- * pending), arrival time (-1 unless arrived). */
+ * pending), arrival time (-1 unless arrived).  Domain mode: vehicles on
+ * another domain's cells read TS_ABSENT; a pending vehicle is reported by
+ * the domain owning its entry cell; merge by taking, per vehicle, the
+ * domain that reports it ACTIVE, else ARRIVED, else PENDING. */
 int ts_read_vehicles(ts_sim *h, int8_t *status, int32_t *link, int32_t *lane,
                      int32_t *cell, int32_t *v, int32_t *cursor,
                      int32_t *t_arrive);

@@ -51,8 +51,29 @@ struct ts_sim {
   int32_t nv = 0;
   std::vector<int64_t> roff;
   std::vector<int32_t> route, dep, entry;
-  std::vector<int32_t> pl_vid, pl_lane, pl_cell, pl_v;
+  std::vector<int32_t> pl_vid, pl_lane, pl_cell, pl_v, pl_cur;
   std::vector<uint8_t> placed;
+  std::vector<int32_t> arr0;     // arrival time of vehicles restored as arrived (-1 otherwise)
+  std::vector<int32_t> first_link, entry_h;  // route[0] and entry cell (kept after init)
+  // domain decomposition (§4; ts_set_domain): owned cells per link
+  int32_t dom_k = 1, dom_me = 0;
+  std::vector<int32_t> dom_of_node;
+  std::vector<int32_t> own_lo, own_hi;
+  std::vector<int32_t> mirror;  // per link: first mirror strip slot of the remote half, or -1
+  struct Nbr {
+    int32_t dom;
+    std::vector<int32_t> send_slot, recv_slot;  // strip slots, (link, lane) order
+    int64_t off;                                // first Strip of this neighbour in d_send/d_recv
+  };
+  std::vector<Nbr> nbrs;
+  int64_t n_xs = 0;  // strips per exchange (sum over neighbours)
+  Strip *d_send = nullptr, *d_recv = nullptr;
+  int32_t *d_send_slot = nullptr, *d_recv_slot = nullptr;
+  std::vector<int32_t> my_nodes;
+  int32_t *d_node_ids = nullptr;
+  bool rows_s1 = false, gen_s1 = false;  // row / general state holds S1(t) (lane change applied)
+  int64_t n_pending0 = 0;
+  int32_t folded_t = 0;  // stats folded into the host counters up to this time
   // layout
   std::vector<TileDesc> tiles;
   std::vector<int32_t> link_tile0, link_ntiles;
@@ -101,7 +122,7 @@ struct ts_sim {
   int32_t *d_ncell = nullptr, *d_lanes = nullptr, *d_lgid = nullptr, *d_cls = nullptr;
   int gcur = 0, rcur = 0;  // current buffer of the general / row state
   int32_t t = 0;
-  int64_t veh_updates = 0, arrived = 0, injected = 0, n_placed = 0;
+  int64_t veh_updates = 0, arrived = 0, injected = 0, n_placed = 0, n_arrived0 = 0;
   // timing
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   std::vector<cudaEvent_t> mv_ev;
@@ -319,8 +340,8 @@ int ts_load_vehicles(ts_sim *h, int32_t n, const int64_t *route_off, const int32
   return TS_OK;
 }
 
-int ts_place_vehicles(ts_sim *h, int32_t n, const int32_t *vid, const int32_t *lane,
-                      const int32_t *cell, const int32_t *v) {
+int ts_place_vehicles_at(ts_sim *h, int32_t n, const int32_t *vid, const int32_t *cursor,
+                         const int32_t *lane, const int32_t *cell, const int32_t *v) {
   if (!h) return TS_EINVAL;
   if (!h->have_veh) return fail(h, TS_EINVAL, "load vehicles first");
   if (h->inited) return fail(h, TS_EINVAL, "already initialised");
@@ -328,12 +349,16 @@ int ts_place_vehicles(ts_sim *h, int32_t n, const int32_t *vid, const int32_t *l
     const int32_t f = vid[i];
     if (f < 0 || f >= h->nv) return fail(h, TS_EINVAL, "placement %d: bad vid", i);
     if (h->placed[f]) return fail(h, TS_EINVAL, "placement %d: vehicle placed twice", i);
-    const int32_t k = h->route[h->roff[f]];
+    const int32_t c = cursor ? cursor[i] : 0;
+    if (c < 0 || c >= h->roff[f + 1] - h->roff[f])
+      return fail(h, TS_EINVAL, "placement %d: cursor outside the route", i);
+    const int32_t k = h->route[h->roff[f] + c];
     if (lane[i] < 0 || lane[i] >= h->lanes[k] || cell[i] < 0 || cell[i] >= h->ncell[k])
       return fail(h, TS_EINVAL, "placement %d: cell outside link", i);
     if (v[i] < 0 || v[i] > h->vmax[k]) return fail(h, TS_EINVAL, "placement %d: velocity", i);
     h->placed[f] = 1;
     h->pl_vid.push_back(f);
+    h->pl_cur.push_back(c);
     h->pl_lane.push_back(lane[i]);
     h->pl_cell.push_back(cell[i]);
     h->pl_v.push_back(v[i]);
@@ -341,25 +366,118 @@ int ts_place_vehicles(ts_sim *h, int32_t n, const int32_t *vid, const int32_t *l
   return TS_OK;
 }
 
+int ts_place_vehicles(ts_sim *h, int32_t n, const int32_t *vid, const int32_t *lane,
+                      const int32_t *cell, const int32_t *v) {
+  return ts_place_vehicles_at(h, n, vid, nullptr, lane, cell, v);
+}
+
+int ts_set_arrived(ts_sim *h, int32_t n, const int32_t *vid, const int32_t *t_arrive) {
+  if (!h) return TS_EINVAL;
+  if (!h->have_veh) return fail(h, TS_EINVAL, "load vehicles first");
+  if (h->inited) return fail(h, TS_EINVAL, "already initialised");
+  if (h->arr0.empty()) h->arr0.assign(h->nv, -1);
+  for (int32_t i = 0; i < n; i++) {
+    const int32_t f = vid[i];
+    if (f < 0 || f >= h->nv || h->placed[f]) return fail(h, TS_EINVAL, "arrival %d: bad vid", i);
+    if (t_arrive[i] < 0) return fail(h, TS_EINVAL, "arrival %d: negative time", i);
+    h->placed[f] = 1;
+    h->arr0[f] = t_arrive[i];
+  }
+  return TS_OK;
+}
+
+int ts_set_domain(ts_sim *h, int32_t k, const int32_t *domain_of_node, int32_t me) {
+  if (!h) return TS_EINVAL;
+  if (!h->have_net) return fail(h, TS_EINVAL, "load the network first");
+  if (h->inited) return fail(h, TS_EINVAL, "already initialised");
+  if (k < 1 || me < 0 || me >= k) return fail(h, TS_EINVAL, "bad domain count or index");
+  if (k > std::max(1, h->nn)) return fail(h, TS_EINVAL, "more domains than nodes");
+  if (k > 1 && h->periodic >= 0) return fail(h, TS_EINVAL, "a ring network has no nodes to cut at");
+  if (k > 1 && !domain_of_node) return fail(h, TS_EINVAL, "domain_of_node is NULL");
+  for (int i = 0; k > 1 && i < h->nn; i++)
+    if (domain_of_node[i] < 0 || domain_of_node[i] >= k)
+      return fail(h, TS_EINVAL, "node %d: domain %d out of range", i, domain_of_node[i]);
+  h->dom_k = k;
+  h->dom_me = me;
+  if (k > 1) h->dom_of_node.assign(domain_of_node, domain_of_node + h->nn);
+  else h->dom_of_node.assign(h->nn, 0);
+  return TS_OK;
+}
+
+// pure host: the exchange partners of domain `me` and the strips (one per
+// lane of every split link shared with the partner) of one message
+int ts_domain_plan(int32_t n_nodes, int32_t n_links, const int32_t *from, const int32_t *to,
+                   const int64_t *length_mm, const int32_t *lanes, int32_t k,
+                   const int32_t *domain_of_node, int32_t me, int32_t cap, int32_t *nbr_dom,
+                   int64_t *nbr_strips, int32_t *n_out) {
+  if (k < 1 || me < 0 || me >= k || n_links < 0 || !n_out) return TS_EINVAL;
+  std::vector<int64_t> cnt(k, 0);
+  for (int32_t j = 0; j < n_links; j++) {
+    if (from[j] < 0 || from[j] >= n_nodes || to[j] < 0 || to[j] >= n_nodes) return TS_EINVAL;
+    const int a = domain_of_node[from[j]], b = domain_of_node[to[j]];
+    if (a == b || (a != me && b != me)) continue;
+    const int n = (int)((length_mm[j] + 3750) / 7500);
+    if (n < 10) return TS_EINVAL;
+    cnt[a == me ? b : a] += lanes[j];
+  }
+  int32_t m = 0;
+  for (int d = 0; d < k; d++)
+    if (cnt[d] > 0) {
+      if (m < cap) {
+        if (nbr_dom) nbr_dom[m] = d;
+        if (nbr_strips) nbr_strips[m] = cnt[d];
+      }
+      m++;
+    }
+  *n_out = m;
+  return TS_OK;
+}
+
 // ------------------------------------------------------------------- layout
+// cells [lo, hi) of link k owned by domain `me` under a node partition:
+// whole links inside the domain; a link whose end nodes lie in different
+// domains is cut at h = floor(n/2), the upstream domain owning [0, h)
+// (reading R16)
+static void owned_range(int n, int dfrom, int dto, int me, int &lo, int &hi) {
+  lo = hi = 0;
+  if (dfrom == me && dto == me) hi = n;
+  else if (dfrom == me) hi = n / 2;
+  else if (dto == me) {
+    lo = n / 2;
+    hi = n;
+  }
+}
+
 static void build_tiles(ts_sim *h) {
   const int tc = h->cfg.tile_cells > 0 ? h->cfg.tile_cells : 512;
+  const bool dom = h->dom_k > 1;
   h->tiles.clear();
   h->link_tile0.assign(h->nl + 1, 0);
   h->link_ntiles.assign(h->nl, 0);
+  h->own_lo.assign(h->nl, 0);
+  h->own_hi.assign(h->nl, 0);
+  for (int k = 0; k < h->nl; k++) {
+    if (dom && k != h->periodic)
+      owned_range(h->ncell[k], h->dom_of_node[h->from[k]], h->dom_of_node[h->to[k]], h->dom_me,
+                  h->own_lo[k], h->own_hi[k]);
+    else
+      h->own_hi[k] = h->ncell[k];
+  }
   int64_t off = 0;
   int32_t strip = 0;
   for (int k = 0; k < h->nl; k++) {
-    const int n = h->ncell[k];
+    const int n = h->ncell[k], lo = h->own_lo[k], hi = h->own_hi[k], span = hi - lo;
     const bool per = k == h->periodic;
-    int nt = (n + tc - 1) / tc;
-    if (nt > 1 && n / nt < 10) nt = std::max(1, n / 10);
     h->link_tile0[k] = (int32_t)h->tiles.size();
+    if (span <= 0) continue;
+    const bool split = lo > 0 || hi < n;
+    int nt = (span + tc - 1) / tc;
+    if (nt > 1 && span / nt < 10) nt = std::max(1, span / 10);
     h->link_ntiles[k] = nt;
-    const bool halo = per || nt > 1;
-    int a = 0;
+    const bool halo = per || nt > 1 || split;
+    int a = lo;
     for (int i = 0; i < nt; i++) {
-      const int w = n / nt + (i < n % nt ? 1 : 0);
+      const int w = span / nt + (i < span % nt ? 1 : 0);
       TileDesc d{};
       d.off = off;
       d.link = k;
@@ -390,6 +508,15 @@ static void build_tiles(ts_sim *h) {
   }
   h->link_tile0[h->nl] = (int32_t)h->tiles.size();
   h->total_cells = off + 16;
+  // mirror strips: the 5-cell strip of the remote half of every split link
+  // (R17), filled by the exchanges
+  h->mirror.assign(h->nl, -1);
+  for (int k = 0; k < h->nl; k++)
+    if (h->own_hi[k] > h->own_lo[k] && (h->own_lo[k] > 0 || h->own_hi[k] < h->ncell[k]) &&
+        k != h->periodic) {
+      h->mirror[k] = strip;
+      strip += h->lanes[k];
+    }
   h->nstrips = strip;
   h->halo_up.assign(std::max(1, strip), -1);
   h->halo_dn.assign(std::max(1, strip), -1);
@@ -398,8 +525,42 @@ static void build_tiles(ts_sim *h) {
     for (int i = 0; i < nt; i++) {
       const TileDesc &d = h->tiles[t0 + i];
       if (d.strip < 0) continue;
-      if (d.flags & kHasUp) h->halo_up[d.strip] = h->tiles[t0 + (i + nt - 1) % nt].strip;
-      if (d.flags & kHasDn) h->halo_dn[d.strip] = h->tiles[t0 + (i + 1) % nt].strip;
+      const bool per = k == h->periodic;
+      if (d.flags & kHasUp)
+        h->halo_up[d.strip] = (i > 0 || per) ? h->tiles[t0 + (i + nt - 1) % nt].strip : h->mirror[k];
+      if (d.flags & kHasDn)
+        h->halo_dn[d.strip] = (i + 1 < nt || per) ? h->tiles[t0 + (i + 1) % nt].strip : h->mirror[k];
+    }
+  }
+  // exchange plan: per neighbour domain, the split links shared with it in
+  // link order, all lanes; each side sends the strip of its boundary tile
+  // and receives into the mirror slot (one buffer per neighbour,
+  // PAPER.md:897-900)
+  h->nbrs.clear();
+  h->n_xs = 0;
+  if (dom) {
+    std::vector<int32_t> nb_index(h->dom_k, -1);
+    for (int k = 0; k < h->nl; k++) {
+      if (h->mirror[k] < 0) continue;
+      const bool up = h->own_lo[k] == 0;  // this domain owns the upstream half
+      const int other = up ? h->dom_of_node[h->to[k]] : h->dom_of_node[h->from[k]];
+      if (nb_index[other] < 0) {
+        nb_index[other] = (int32_t)h->nbrs.size();
+        h->nbrs.push_back(ts_sim::Nbr{other, {}, {}, 0});
+      }
+      ts_sim::Nbr &nb = h->nbrs[nb_index[other]];
+      const int t0 = h->link_tile0[k], nt = h->link_ntiles[k];
+      const TileDesc &bt = h->tiles[up ? t0 + nt - 1 : t0];
+      for (int l = 0; l < h->lanes[k]; l++) {
+        nb.send_slot.push_back(bt.strip + l);
+        nb.recv_slot.push_back(h->mirror[k] + l);
+      }
+    }
+    std::sort(h->nbrs.begin(), h->nbrs.end(),
+              [](const ts_sim::Nbr &a, const ts_sim::Nbr &b) { return a.dom < b.dom; });
+    for (ts_sim::Nbr &nb : h->nbrs) {
+      nb.off = h->n_xs;
+      h->n_xs += (int64_t)nb.send_slot.size();
     }
   }
   // classify: whole non-periodic links of <= kRowMaxCells cells and <= 32
@@ -462,7 +623,7 @@ static bool build_node_lanes(ts_sim *h, std::vector<NodeLane> &lanes,
   int in_chunk = 0;
   for (int nd = 0; nd < h->nn; nd++) {
     const int a = h->in_off[nd], b = h->in_off[nd + 1];
-    if (a == b) continue;
+    if (a == b || h->dom_of_node[nd] != h->dom_me) continue;
     int maxcls = h->cls[h->in_list[a]], nl = 0;
     for (int i = a; i < b; i++) {
       maxcls = std::max(maxcls, h->cls[h->in_list[i]]);
@@ -543,7 +704,8 @@ static StepParams step_params(ts_sim *h, int t, int mode) {
 
 static NodeParams node_params(ts_sim *h, int t) {
   NodeParams N{};
-  N.nnodes = h->periodic >= 0 ? 0 : h->nn;
+  N.nnodes = h->periodic >= 0 ? 0 : (int32_t)h->my_nodes.size();
+  N.node_ids = h->d_node_ids;
   N.t = t;
   N.G = h->cfg.gap_accept_G;
   N.k0 = (uint32_t)(h->cfg.seed & 0xffffffffu);
@@ -605,24 +767,43 @@ static int zero_stats(ts_sim *h, int32_t t_from, int32_t n) {
   return TS_OK;
 }
 
-int ts_init(ts_sim *h, int32_t t0) {
+static int init_impl(ts_sim *h, int32_t t0, bool inject0);
+static void pack_strips(ts_sim *h);
+
+int ts_init(ts_sim *h, int32_t t0) { return init_impl(h, t0, true); }
+int ts_resume(ts_sim *h, int32_t t) { return init_impl(h, t, false); }
+
+static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
   if (!h) return TS_EINVAL;
   if (!h->have_veh) return fail(h, TS_EINVAL, "load vehicles first");
   if (h->inited) return fail(h, TS_EINVAL, "already initialised");
   if (t0 < 0) return fail(h, TS_EINVAL, "t0 must be >= 0");
   CK(h, cudaSetDevice(h->dev));
+  if (h->dom_of_node.empty()) h->dom_of_node.assign(h->nn, 0);
   build_tiles(h);
-  // host staging of the initial placement: codes + compact vid lists
+  h->first_link.resize(h->nv);
+  h->entry_h = h->entry;
+  for (int f = 0; f < h->nv; f++) h->first_link[f] = h->route[h->roff[f]];
+  // host staging of the initial placement: codes + compact vid lists (cells
+  // of other domains are skipped)
   std::vector<uint8_t> code(h->total_cells, kEmpty);
   std::vector<int32_t> cellvid(h->total_cells, -1);
+  std::vector<int32_t> cur0(h->nv, 0);
+  h->n_placed = 0;
   for (size_t i = 0; i < h->pl_vid.size(); i++) {
-    const int f = h->pl_vid[i], k = h->route[h->roff[f]];
+    const int f = h->pl_vid[i], c = h->pl_cur[i];
+    const int k = h->route[h->roff[f] + c];
+    cur0[f] = c;
     const int ti = tile_of(h, k, h->pl_cell[i]);
+    if (ti < 0) continue;  // another domain's cell
     const TileDesc &d = h->tiles[ti];
     const int64_t pos = d.off + (int64_t)h->pl_lane[i] * row_pitch(d.w) + (h->pl_cell[i] - d.a);
     if (code[pos] != kEmpty) return fail(h, TS_EINVAL, "placement %zu: cell taken", i);
-    code[pos] = (uint8_t)(h->pl_v[i] | (first_slot(h, f) << 3));
+    const int64_t ro = h->roff[f];
+    const int slot = c + 1 < h->roff[f + 1] - ro ? h->out_pos[h->route[ro + c + 1]] : kSlotFinal;
+    code[pos] = (uint8_t)(h->pl_v[i] | (slot << 3));
     cellvid[pos] = f;
+    h->n_placed++;
   }
   std::vector<int32_t> vids(h->total_cells, -1);
   for (const TileDesc &d : h->tiles) {  // per-row vid lists in cell order
@@ -635,7 +816,6 @@ int ts_init(ts_sim *h, int32_t t0) {
     }
   }
   std::vector<int32_t>().swap(cellvid);
-  h->n_placed = (int64_t)h->pl_vid.size();
   // general tiles: the byte layout at their own device offsets
   std::vector<uint8_t> gcode(h->gcells, kEmpty);
   std::vector<int32_t> gvid(h->gcells, -1);
@@ -687,23 +867,39 @@ int ts_init(ts_sim *h, int32_t t0) {
   std::vector<int32_t>().swap(vids);
   // pending lists per first link in (departure, vid) order (R13)
   std::vector<int32_t> pend_off(h->nl + 1, 0), pend_list;
+  auto mine = [&](int f) {  // pending vehicle whose entry cell this domain owns
+    const int k = h->first_link[f];
+    return !h->placed[f] && h->entry[f] >= h->own_lo[k] && h->entry[f] < h->own_hi[k];
+  };
+  h->n_pending0 = 0;
   for (int f = 0; f < h->nv; f++)
-    if (!h->placed[f]) pend_off[h->route[h->roff[f]] + 1]++;
+    if (mine(f)) {
+      pend_off[h->first_link[f] + 1]++;
+      h->n_pending0++;
+    }
   for (int k = 0; k < h->nl; k++) pend_off[k + 1] += pend_off[k];
   pend_list.assign(std::max(1, pend_off[h->nl]), 0);
   {
     std::vector<int32_t> fill(h->nl, 0);
     for (int f = 0; f < h->nv; f++)
-      if (!h->placed[f]) {
-        int k = h->route[h->roff[f]];
+      if (mine(f)) {
+        int k = h->first_link[f];
         pend_list[pend_off[k] + fill[k]++] = f;
       }
     for (int k = 0; k < h->nl; k++)
       std::stable_sort(pend_list.begin() + pend_off[k], pend_list.begin() + pend_off[k + 1],
                        [&](int a, int b) { return h->dep[a] < h->dep[b] || (h->dep[a] == h->dep[b] && a < b); });
   }
-  std::vector<int32_t> inj(h->nv), arr(h->nv, -1), cur0(h->nv, 0);
+  std::vector<int32_t> inj(h->nv), arr(h->nv, -1);
   for (int f = 0; f < h->nv; f++) inj[f] = h->placed[f] ? INT_MIN : INT_MAX;
+  h->n_arrived0 = 0;
+  if (!h->arr0.empty()) {
+    for (int f = 0; f < h->nv; f++) {
+      arr[f] = h->arr0[f];
+      if (arr[f] >= 0) cur0[f] = (int32_t)(h->roff[f + 1] - h->roff[f] - 1);  // on its final link
+      if (arr[f] >= 0 && h->dom_me == 0) h->n_arrived0++;  // counted once over the domains
+    }
+  }
   std::vector<uint8_t> vmax8(h->nl);
   for (int k = 0; k < h->nl; k++) vmax8[k] = (uint8_t)h->vmax[k];
   // device
@@ -792,11 +988,31 @@ int ts_init(ts_sim *h, int32_t t0) {
       if ((rc = upload(h, &h->d_chunk_off, chunk_off))) return rc;
     }
   }
-  // initial injection: departure <= t0 (O1 §Init), S(t0) into buffer 1
+  // the nodes of this domain (nodes are never split)
+  h->my_nodes.clear();
+  for (int nd = 0; nd < h->nn; nd++)
+    if (h->dom_of_node[nd] == h->dom_me) h->my_nodes.push_back(nd);
+  if ((rc = upload(h, &h->d_node_ids, h->my_nodes))) return rc;
+  // exchange buffers: one contiguous segment of Strips per neighbour
+  if (h->n_xs > 0) {
+    std::vector<int32_t> ss, rs;
+    for (const ts_sim::Nbr &nb : h->nbrs) {
+      ss.insert(ss.end(), nb.send_slot.begin(), nb.send_slot.end());
+      rs.insert(rs.end(), nb.recv_slot.begin(), nb.recv_slot.end());
+    }
+    if ((rc = upload(h, &h->d_send_slot, ss))) return rc;
+    if ((rc = upload(h, &h->d_recv_slot, rs))) return rc;
+    if ((rc = dalloc(h, &h->d_send, h->n_xs, 0xFF))) return rc;
+    if ((rc = dalloc(h, &h->d_recv, h->n_xs, 0xFF))) return rc;
+  }
+  // S(t0) into buffer 1: the initial injection of departure <= t0 (O1
+  // §Init), or (resume) a plain pass that writes strips and counters
   h->gcur = 0;
   h->rcur = 0;
+  h->rows_s1 = false;
+  h->gen_s1 = false;
   if (zero_stats(h, t0, 1)) return TS_EINTERNAL;
-  int mode = kModeInject | (base_mode(h) & kModeHash);
+  int mode = (inject0 ? kModeInject : 0) | (base_mode(h) & kModeHash);
   StepParams P = step_params(h, t0 - 1, mode);
   if (h->ngroups > 0) {
     launch_rows(P, rows_params(h), h->rows_blocks, h->rows_threads, 0, h->stream);
@@ -808,6 +1024,8 @@ int ts_init(ts_sim *h, int32_t t0) {
   }
   CK(h, cudaGetLastError());
   h->t = t0;
+  h->folded_t = t0;
+  if (h->n_xs > 0) pack_strips(h);  // the caller exchanges, then ts_step_phase(h, 2, 0)
   CK(h, cudaStreamSynchronize(h->stream));
   unsigned long long st[ST_N];
   CK(h, cudaMemcpy(st, h->d_stats + (size_t)(t0 & (kHist - 1)) * ST_N, sizeof st, cudaMemcpyDeviceToHost));
@@ -815,6 +1033,7 @@ int ts_init(ts_sim *h, int32_t t0) {
   // the host copies of the plans are no longer needed (all on the device)
   std::vector<int32_t>().swap(h->route);
   std::vector<int32_t>().swap(h->pl_vid);
+  std::vector<int32_t>().swap(h->pl_cur);
   std::vector<int32_t>().swap(h->pl_lane);
   std::vector<int32_t>().swap(h->pl_cell);
   std::vector<int32_t>().swap(h->pl_v);
@@ -823,13 +1042,73 @@ int ts_init(ts_sim *h, int32_t t0) {
 }
 
 // --------------------------------------------------------------------- step
+// strips of the boundary tiles -> send buffer (after k_lc / k_step)
+static void pack_strips(ts_sim *h) {
+  launch_strip_copy(h->d_strip[h->gcur], h->d_send_slot, h->d_send, nullptr, h->n_xs, h->stream);
+}
+// receive buffer -> mirror strips, read as halos by the next kernel
+static void unpack_strips(ts_sim *h) {
+  launch_strip_copy(h->d_recv, nullptr, h->d_strip[h->gcur], h->d_recv_slot, h->n_xs, h->stream);
+}
+
+// Phase 0 of step t: lane change on S(t) (H1) of the
+// general tiles and, unless already fused into the previous move, of the
+// row tiles; pack exchange #1 (H2).
+static void phase_lc(ts_sim *h) {
+  const int t = h->t;
+  if (!h->gtiles.empty() && !h->gen_s1) {
+    launch_lc(step_params(h, t, 0), h->blocks, h->threads, h->smem, h->stream);
+    h->gcur ^= 1;
+  }
+  if (h->ngroups > 0 && !h->rows_s1) {
+    launch_rows(step_params(h, t, kModeLC), rows_params(h), h->rows_blocks, h->rows_threads, 0,
+                h->stream);
+    h->rcur ^= 1;
+  }
+  h->gen_s1 = h->rows_s1 = true;
+  if (h->n_xs > 0) pack_strips(h);
+}
+
+// Phase 1: intersections (H3), velocity update + move (H4/H5), injection
+// (H6); with `more`, the lane change of step t+1 is fused into the move
+// kernels whose tiles need no exchange for it.  Pack exchange #2 (H7).
+static void phase_move(ts_sim *h, bool more, cudaEvent_t e0, cudaEvent_t e1) {
+  const int t = h->t;
+  const int mode = base_mode(h);
+  if (h->n_xs > 0) unpack_strips(h);
+  if (h->node_warp)
+    launch_node_warp(node_params(h, t), NodeWarpParams{h->d_nlanes, h->d_chunk_off, h->nchunks},
+                     h->stream);
+  else
+    launch_node(node_params(h, t), h->stream);
+  if (e0) cudaEventRecord(e0, h->stream);
+  if (h->ngroups > 0) {
+    const bool f = more && h->rfused;
+    launch_rows(step_params(h, t, mode | (f ? kModeLC : 0)), rows_params(h), h->rows_blocks,
+                h->rows_threads, 0, h->stream);
+    h->rcur ^= 1;
+    h->rows_s1 = f;
+  }
+  if (!h->gtiles.empty()) {
+    const bool f = more && h->gfused;
+    launch_step(step_params(h, t, mode | (f ? kModeLC : 0)), h->blocks, h->threads, h->smem,
+                h->stream);
+    h->gcur ^= 1;
+    h->gen_s1 = f;
+  }
+  if (e1) cudaEventRecord(e1, h->stream);
+  h->t = t + 1;
+  if (h->n_xs > 0) pack_strips(h);
+}
+
 static int enqueue_steps(ts_sim *h, int32_t n) {
   if (!h || !h->inited) return fail(h, TS_EINVAL, "call ts_init first");
   if (n < 0) return fail(h, TS_EINVAL, "negative step count");
+  if (h->n_xs > 0)
+    return fail(h, TS_EINVAL, "domain with neighbours: step with ts_step_phase and an exchange");
   if (n == 0) return TS_OK;
   CK(h, cudaSetDevice(h->dev));
   if (zero_stats(h, h->t + 1, std::min(n + 1, kHist))) return TS_EINTERNAL;
-  const int mode = base_mode(h);
   if ((int)h->mv_ev.size() < 2 * n && h->timing) {
     while ((int)h->mv_ev.size() < 2 * n) {
       cudaEvent_t e;
@@ -838,51 +1117,39 @@ static int enqueue_steps(ts_sim *h, int32_t n) {
     }
   }
   CK(h, cudaEventRecord(h->ev0, h->stream));
-  const int t = h->t;
-  const bool gen = !h->gtiles.empty(), rows = h->ngroups > 0;
-  // lane change of step t on S(t): general tiles (k_lc) and row tiles
-  // (k_rows in lane-change-only mode)
-  auto lc_gen = [&](int ts) {
-    launch_lc(step_params(h, ts, 0), h->blocks, h->threads, h->smem, h->stream);
-    h->gcur ^= 1;
-  };
-  auto lc_rows = [&](int ts) {
-    launch_rows(step_params(h, ts, kModeLC), rows_params(h), h->rows_blocks, h->rows_threads, 0,
-                h->stream);
-    h->rcur ^= 1;
-  };
-  if (gen && h->gfused) lc_gen(t);
-  if (rows && h->rfused) lc_rows(t);
   for (int i = 0; i < n; i++) {
-    if (gen && !h->gfused) lc_gen(t + i);
-    if (rows && !h->rfused) lc_rows(t + i);
-    if (h->node_warp)
-      launch_node_warp(node_params(h, t + i), NodeWarpParams{h->d_nlanes, h->d_chunk_off, h->nchunks},
-                       h->stream);
-    else
-      launch_node(node_params(h, t + i), h->stream);
-    if (h->timing) CK(h, cudaEventRecord(h->mv_ev[2 * i], h->stream));
-    if (rows) {
-      const int m = mode | (h->rfused && i < n - 1 ? kModeLC : 0);
-      launch_rows(step_params(h, t + i, m), rows_params(h), h->rows_blocks, h->rows_threads, 0,
-                  h->stream);
-      h->rcur ^= 1;
-    }
-    if (gen) {
-      const int m = mode | (h->gfused && i < n - 1 ? kModeLC : 0);
-      launch_step(step_params(h, t + i, m), h->blocks, h->threads, h->smem, h->stream);
-      h->gcur ^= 1;
-    }
-    if (h->timing) CK(h, cudaEventRecord(h->mv_ev[2 * i + 1], h->stream));
+    phase_lc(h);
+    phase_move(h, i < n - 1, h->timing ? h->mv_ev[2 * i] : nullptr,
+               h->timing ? h->mv_ev[2 * i + 1] : nullptr);
   }
   CK(h, cudaEventRecord(h->ev1, h->stream));
   CK(h, cudaGetLastError());
-  h->t = t + n;
   h->last_move_launches = n;
   return TS_OK;
 }
 
+// fold the per-step counters of steps whose result time is in
+// (folded_t, t] into the host totals
+static int fold_stats(ts_sim *h) {
+  const int n = h->t - h->folded_t;
+  if (n <= 0) return TS_OK;
+  if (n < kHist) {
+    std::vector<unsigned long long> st((size_t)kHist * ST_N);
+    CK(h, cudaMemcpy(st.data(), h->d_stats, st.size() * 8, cudaMemcpyDeviceToHost));
+    for (int tt = h->folded_t + 1; tt <= h->t; tt++) {
+      const unsigned long long *a = &st[(size_t)(tt & (kHist - 1)) * ST_N];
+      const unsigned long long *p = &st[(size_t)((tt - 1) & (kHist - 1)) * ST_N];
+      h->veh_updates += (int64_t)p[ST_ACTIVE];
+      h->arrived += (int64_t)a[ST_ARR];
+      h->injected += (int64_t)a[ST_INJ];
+    }
+  }
+  h->folded_t = h->t;
+  return TS_OK;
+}
+
 static int finish_steps(ts_sim *h, int32_t t_from, int32_t n) {
+  (void)t_from;
   CK(h, cudaStreamSynchronize(h->stream));
   float ms = 0;
   CK(h, cudaEventElapsedTime(&ms, h->ev0, h->ev1));
@@ -895,21 +1162,7 @@ static int finish_steps(ts_sim *h, int32_t t_from, int32_t n) {
       mv += m;
     }
   h->last_move_ms = mv;
-  // counters from the history: active in S(t) for t in [t_from, t_from+n)
-  if (n <= kHist - 1) {
-    std::vector<unsigned long long> st((size_t)(n + 1) * ST_N);
-    for (int i = 0; i <= n; i++) {
-      int s = (t_from + i) & (kHist - 1);
-      CK(h, cudaMemcpy(&st[(size_t)i * ST_N], h->d_stats + (size_t)s * ST_N,
-                       ST_N * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
-    }
-    for (int i = 0; i < n; i++) h->veh_updates += (int64_t)st[(size_t)i * ST_N + ST_ACTIVE];
-    for (int i = 1; i <= n; i++) {
-      h->arrived += (int64_t)st[(size_t)i * ST_N + ST_ARR];
-      h->injected += (int64_t)st[(size_t)i * ST_N + ST_INJ];
-    }
-  }
-  return TS_OK;
+  return fold_stats(h);
 }
 
 int ts_step(ts_sim *h, int32_t n_steps) {
@@ -936,6 +1189,105 @@ int ts_sync(ts_sim *h) {
     return rc;
   }
   CK(h, cudaStreamSynchronize(h->stream));
+  return fold_stats(h);
+}
+
+int ts_step_phase(ts_sim *h, int32_t phase, int32_t more) {
+  if (!h || !h->inited) return fail(h, TS_EINVAL, "call ts_init first");
+  CK(h, cudaSetDevice(h->dev));
+  switch (phase) {
+    case 0:
+      if (zero_stats(h, h->t + 1, 1)) return TS_EINTERNAL;
+      phase_lc(h);
+      break;
+    case 1:
+      if (!h->gen_s1 || !h->rows_s1) return fail(h, TS_EINVAL, "phase 1 before phase 0");
+      phase_move(h, more != 0, nullptr, nullptr);
+      break;
+    case 2:
+      if (h->n_xs > 0) unpack_strips(h);
+      break;
+    default:
+      return fail(h, TS_EINVAL, "phase must be 0, 1 or 2");
+  }
+  CK(h, cudaGetLastError());
+  return TS_OK;
+}
+
+int ts_exchange_plan(const ts_sim *h, int32_t cap, int32_t *nbr_dom, int64_t *nbr_strips,
+                     int64_t *nbr_off, int32_t *n_out) {
+  if (!h || !h->inited || !n_out) return TS_EINVAL;
+  const int32_t m = (int32_t)h->nbrs.size();
+  for (int32_t i = 0; i < m && i < cap; i++) {
+    if (nbr_dom) nbr_dom[i] = h->nbrs[i].dom;
+    if (nbr_strips) nbr_strips[i] = (int64_t)h->nbrs[i].send_slot.size();
+    if (nbr_off) nbr_off[i] = h->nbrs[i].off;
+  }
+  *n_out = m;
+  return TS_OK;
+}
+
+int ts_exchange_buffers(ts_sim *h, void **send_dev, void **recv_dev) {
+  if (!h || !h->inited) return TS_EINVAL;
+  if (send_dev) *send_dev = h->d_send;
+  if (recv_dev) *recv_dev = h->d_recv;
+  return TS_OK;
+}
+
+int32_t ts_strip_bytes(void) { return (int32_t)sizeof(Strip); }
+
+void *ts_stream(const ts_sim *h) { return h ? (void *)h->stream : nullptr; }
+
+// in-process exchange between the domains of one partition (all handles of
+// the same k-way partition, any devices): every send segment is copied into
+// the partner's receive segment, ordered after the sender's pack and before
+// the receiver's unpack by events
+int ts_exchange_local(ts_sim **hs, int32_t k) {
+  if (!hs || k < 1) return TS_EINVAL;
+  std::vector<ts_sim *> by_dom(k, nullptr);
+  for (int i = 0; i < k; i++) {
+    if (!hs[i] || !hs[i]->inited || hs[i]->dom_k != k) return TS_EINVAL;
+    by_dom[hs[i]->dom_me] = hs[i];
+  }
+  std::vector<cudaEvent_t> ev(k);
+  for (int i = 0; i < k; i++) {
+    ts_sim *a = by_dom[i];
+    if (!a) return fail(hs[0], TS_EINVAL, "domain %d missing", i);
+    CK(a, cudaSetDevice(a->dev));
+    CK(a, cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
+    CK(a, cudaEventRecord(ev[i], a->stream));
+  }
+  for (int i = 0; i < k; i++) {
+    ts_sim *b = by_dom[i];  // receiver
+    CK(b, cudaSetDevice(b->dev));
+    for (const ts_sim::Nbr &nb : b->nbrs) {
+      ts_sim *a = by_dom[nb.dom];
+      const ts_sim::Nbr *back = nullptr;
+      for (const ts_sim::Nbr &x : a->nbrs)
+        if (x.dom == b->dom_me) back = &x;
+      if (!back || back->send_slot.size() != nb.recv_slot.size())
+        return fail(b, TS_EINTERNAL, "exchange plans of domains %d and %d disagree", a->dom_me,
+                    b->dom_me);
+      CK(b, cudaStreamWaitEvent(b->stream, ev[nb.dom], 0));
+      CK(b, cudaMemcpyPeerAsync(b->d_recv + nb.off, b->dev, a->d_send + back->off, a->dev,
+                                nb.recv_slot.size() * sizeof(Strip), b->stream));
+    }
+  }
+  // a sender may not overwrite its send buffer before the receivers copied
+  for (int i = 0; i < k; i++) {
+    ts_sim *b = by_dom[i];
+    cudaEvent_t done;
+    CK(b, cudaSetDevice(b->dev));
+    CK(b, cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+    CK(b, cudaEventRecord(done, b->stream));
+    for (const ts_sim::Nbr &nb : b->nbrs) {
+      ts_sim *a = by_dom[nb.dom];
+      CK(a, cudaSetDevice(a->dev));
+      CK(a, cudaStreamWaitEvent(a->stream, done, 0));
+    }
+    cudaEventDestroy(done);
+  }
+  for (int i = 0; i < k; i++) cudaEventDestroy(ev[i]);
   return TS_OK;
 }
 
@@ -1050,16 +1402,23 @@ int ts_read_vehicles(ts_sim *h, int8_t *status, int32_t *link, int32_t *lane, in
   }
   for (int f = 0; f < h->nv; f++) {
     int8_t s = TS_ACTIVE;
-    if (arr[f] >= 0) s = TS_ARRIVED;
-    else if (inj[f] == INT_MAX) s = TS_PENDING;
-    if ((s == TS_ACTIVE) != (seen[f] != 0))
-      return fail(h, TS_EINTERNAL, "corrupt state: vehicle %d status %d seen %d", f, s, seen[f]);
+    if (seen[f]) s = TS_ACTIVE;
+    else if (arr[f] >= 0) s = TS_ARRIVED;
+    else if (inj[f] == INT_MAX) {
+      // pending: reported by the domain owning its entry cell
+      const int k = h->first_link[f];
+      s = (h->entry_h[f] >= h->own_lo[k] && h->entry_h[f] < h->own_hi[k]) ? TS_PENDING : TS_ABSENT;
+    } else {
+      s = TS_ABSENT;  // on a cell of another domain
+    }
+    if (s == TS_ABSENT && h->dom_k == 1)
+      return fail(h, TS_EINTERNAL, "corrupt state: vehicle %d lost", f);
     if (status) status[f] = s;
     if (link) link[f] = lk[f];
     if (lane) lane[f] = ln[f];
     if (cell) cell[f] = ce[f];
     if (v) v[f] = vv[f];
-    if (cursor) cursor[f] = s == TS_PENDING ? -1 : cur[f];
+    if (cursor) cursor[f] = (s == TS_ACTIVE || s == TS_ARRIVED) ? cur[f] : -1;
     if (t_arrive) t_arrive[f] = s == TS_ARRIVED ? arr[f] : -1;
   }
   return TS_OK;
@@ -1146,13 +1505,14 @@ int ts_read_history(ts_sim *h, int32_t t_from, int32_t n, uint64_t *hash, int64_
 int ts_get_totals(ts_sim *h, int64_t out[8]) {
   if (!h || !h->inited) return fail(h, TS_EINVAL, "not initialised");
   CK(h, cudaStreamSynchronize(h->stream));
+  if (int rc = fold_stats(h)) return rc;
   unsigned long long st[ST_N];
   CK(h, cudaMemcpy(st, h->d_stats + (size_t)(h->t & (kHist - 1)) * ST_N, sizeof st,
                    cudaMemcpyDeviceToHost));
   const int64_t active = (int64_t)st[ST_ACTIVE];
   out[0] = active;
-  out[1] = h->nv - h->n_placed - h->injected;
-  out[2] = h->arrived;
+  out[1] = h->n_pending0 - h->injected;
+  out[2] = h->n_arrived0 + h->arrived;
   out[3] = h->veh_updates;
   out[4] = h->lane_cells;
   out[5] = (int64_t)h->tiles.size();

@@ -194,7 +194,8 @@ struct StepParams {
 };
 
 struct NodeParams {
-  int32_t nnodes;
+  int32_t nnodes;            // nodes of this domain
+  const int32_t *node_ids;   // their ids (NULL: 0..nnodes-1)
   int32_t t;
   int32_t G;
   uint32_t k0, k1;
@@ -243,6 +244,8 @@ void launch_rows(const StepParams &p, const RowsParams &r, int blocks, int threa
 void launch_node_warp(const NodeParams &p, const NodeWarpParams &w, void *stream);
 void launch_step(const StepParams &p, int blocks, int threads, int smem, void *stream);
 void launch_node(const NodeParams &p, void *stream);
+void launch_strip_copy(const Strip *src, const int32_t *sslot, Strip *dst, const int32_t *dslot,
+                       int64_t n, void *stream);
 void launch_hash(const StepParams &p, int blocks, int threads, int smem, void *stream,
                  unsigned long long *out);
 void launch_rows_hash(const StepParams &p, const RowsParams &r, void *stream,

@@ -255,7 +255,7 @@ __device__ __forceinline__ void place(TileCtx &T, int pos, uint8_t code, int vid
 // move one vehicle at smem position q (owned, or a ghost in the upstream
 // halo) -- H4 + H5
 __device__ __forceinline__ void move_one(const StepParams &P, TileCtx &T, Acc &acc, int q,
-                                         int vid, bool ghost, int Vk) {
+                                         int vid, bool ghost, int Vk, int ghost_cur = -1) {
   const int l = lane_of(T, q);
   int x = T.d.a + (q - l * T.S - T.HP);
   const bool periodic = (T.d.flags & kPeriodic) != 0;
@@ -277,6 +277,9 @@ __device__ __forceinline__ void move_one(const StepParams &P, TileCtx &T, Acc &a
   if (yl >= 0 && yl < T.w) {
     place(T, l * T.S + T.HP + yl, (uint8_t)(v3 | (slot << 3)), vid);
     acc_place(acc, P.mode & kModeHash, vid, T.d.link, l, y, v3);
+    // a migrant from the upstream strip brings its route cursor (the
+    // cursor array of another domain is not visible here)
+    if (ghost) P.cursor[vid] = ghost_cur;
   } else if (!periodic && y > T.d.n - 1 && !ghost) {
     if (slot == kSlotFinal) {  // exit to parking
       P.arr_time[vid] = P.t + 1;
@@ -365,8 +368,10 @@ __global__ void __launch_bounds__(256) k_step(const StepParams P) {
         for (int i = lane; i < T.L * kGmax; i += 32) {
           int l = i / kGmax, j = i - l * kGmax;
           int q = l * T.S + T.HP - kGmax + j;
-          if (occupied(T.bin, q))
-            move_one(P, T, acc, q, P.strip_in[P.halo_up[T.d.strip] + l].tail_vid[j], true, Vk);
+          if (occupied(T.bin, q)) {
+            const Strip &hs = P.strip_in[P.halo_up[T.d.strip] + l];
+            move_one(P, T, acc, q, hs.tail_vid[j], true, Vk, hs.tail_cur[j]);
+          }
         }
       }
       // entrants granted by the node kernel (H3/H5): at most one per lane
@@ -553,9 +558,10 @@ __global__ void __launch_bounds__(256) k_node_warp(const NodeParams P, const Nod
 // general fallback: one thread per node (any in-degree)
 __global__ void __launch_bounds__(128) k_node(const NodeParams P) {
   __shared__ unsigned long long red[4];
-  const int node = blockIdx.x * blockDim.x + threadIdx.x;
+  const int ni = blockIdx.x * blockDim.x + threadIdx.x;
   uint32_t crossings = 0;
-  if (node < P.nnodes) {
+  if (ni < P.nnodes) {
+    const int node = P.node_ids ? P.node_ids[ni] : ni;
     const int a = P.in_off[node], b = P.in_off[node + 1];
     int maxcls = -2147483647;
     for (int i = a; i < b; i++) maxcls = max(maxcls, P.link_cls[P.in_list[i]]);
@@ -593,7 +599,29 @@ __global__ void __launch_bounds__(128) k_node(const NodeParams P) {
   node_flush(P, crossings, red);
 }
 
+// ------------------------------------------------------- strip exchange
+// dst[dslot ? dslot[j] : j] = src[sslot ? sslot[j] : j] for j < n, one
+// 4-byte word per thread (pack: boundary strips -> send buffer; unpack:
+// receive buffer -> mirror strips, H2/H7)
+__global__ void __launch_bounds__(256) k_strip_copy(const Strip *src, const int32_t *sslot,
+                                                    Strip *dst, const int32_t *dslot, int64_t n) {
+  constexpr int kW = sizeof(Strip) / 4;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n * kW) return;
+  const int64_t j = i / kW;
+  const int w = (int)(i - j * kW);
+  const int64_t s = sslot ? sslot[j] : j, d = dslot ? dslot[j] : j;
+  reinterpret_cast<uint32_t *>(dst + d)[w] = reinterpret_cast<const uint32_t *>(src + s)[w];
+}
+
 // ------------------------------------------------------------ launchers
+void launch_strip_copy(const Strip *src, const int32_t *sslot, Strip *dst, const int32_t *dslot,
+                       int64_t n, void *stream) {
+  if (n <= 0) return;
+  const int64_t words = n * (int64_t)(sizeof(Strip) / 4);
+  k_strip_copy<<<(unsigned)((words + 255) / 256), 256, 0, (cudaStream_t)stream>>>(src, sslot, dst,
+                                                                                 dslot, n);
+}
 void launch_lc(const StepParams &p, int blocks, int threads, int smem, void *stream) {
   k_lc<<<blocks, threads, smem, (cudaStream_t)stream>>>(p);
 }

@@ -68,16 +68,6 @@ __device__ __forceinline__ bool any_row(const uint32_t (&x)[NW]) {
   for (int i = 0; i < NW; i++) a |= x[i];
   return a != 0u;
 }
-// number of set bits below cell x
-__device__ __forceinline__ int rank_row(const uint32_t (&x)[NW], int c) {
-  int r = 0;
-#pragma unroll
-  for (int i = 0; i < NW; i++) {
-    const int lo = c - 32 * i;
-    r += __popc(x[i] & lowm(lo));
-  }
-  return r;
-}
 // one-hot mask of cell c inside word i (no dynamic register indexing: the
 // compiler would otherwise move the row to local memory)
 __device__ __forceinline__ uint32_t onehot(int i, int c) {
@@ -316,7 +306,7 @@ __global__ void __launch_bounds__(128) k_rows(const StepParams P, const RowsPara
             acc.inj++;
           });
     }
-    if (do_move || (P.mode & kModeInject)) acc.active += popc_row(OO);
+    if (do_move || !lc) acc.active += popc_row(OO);
     if (do_move) acc.sumv += popc_row(OV0) + 2 * popc_row(OV1) + 4 * popc_row(OV2);
 
     // ---- lane change on S(t+1) (fused) or S(t) (lane change only):

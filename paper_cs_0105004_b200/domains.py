@@ -1,0 +1,252 @@
+"""Domain decomposition of the TRANSIMS CA step (§4, :366-452).
+
+The network is cut into k domains by orthogonal recursive bisection of its
+nodes; a link whose end nodes fall into different
+domains is split at its middle (R16) and each side keeps a mirror of the
+other side's 5-cell strip next to the cut (R17).  Every step exchanges the
+strips twice -- after the lane change and after the move
+-- with each neighbour domain, one buffer per neighbour.
+The simulation result does not depend on k or on the partition
+(SPEC.md:326), which is what the tests check against the CPU oracle.
+
+Each domain is one libtsim handle; its kernels, the strip packing and
+unpacking all run in the library (csrc/).  This module only moves the
+packed buffers between handles:
+
+* ``LocalDomains``: all k domains in this process (one or several GPUs);
+  the exchange is an in-process device copy (``ts_exchange_local``).
+* ``DistDomain``: one domain per rank of a torch.distributed group (one
+  process per GPU); the exchange is point-to-point send/recv with every
+  neighbour -- NCCL over NVLink on B200s, gloo in the CPU tests.
+
+Adaptive rebalancing: per-link work counters and the
+measured per-domain step times give node weights; a new ORB partition is
+computed and the state migrates by a read / restore at the current time
+(exact: the state S(t) is the whole simulation state).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import tsim as _t
+
+ACTIVE, ARRIVED, PENDING, ABSENT = _t.ACTIVE, _t.ARRIVED, _t.PENDING, _t.ABSENT
+
+
+# ------------------------------------------------------------- partition
+def link_cells(scn):
+    """cells per link, round-half-up of length / 7.5 m (R1)"""
+    return np.maximum(1, (np.asarray(scn.link_len_mm, np.int64) + 3750) // 7500)
+
+
+def node_weights(scn, link_work=None):
+    """ORB node weights: half of the load of every attached link
+    (SPEC.md:373-379).  Load = cells x lanes, or the
+    measured per-link work when given."""
+    if link_work is None:
+        lw = link_cells(scn) * np.asarray(scn.link_lanes, np.int64)
+    else:
+        lw = np.asarray(link_work, np.float64)
+    w = np.zeros(scn.n_nodes, np.float64)
+    np.add.at(w, np.asarray(scn.link_from), 0.5 * lw)
+    np.add.at(w, np.asarray(scn.link_to), 0.5 * lw)
+    return w + 1e-9
+
+
+def partition(scn, k, weights=None):
+    """domain of every node: ORB on the node coordinates"""
+    if weights is None:
+        weights = node_weights(scn)
+    return _t.orb_partition(scn.node_x, scn.node_y, k, weights)
+
+
+def split_stats(scn, dom):
+    """N_spl (split links) and the domain neighbour graph"""
+    d = np.asarray(dom)
+    a, b = d[np.asarray(scn.link_from)], d[np.asarray(scn.link_to)]
+    cut = a != b
+    pairs = set(zip(a[cut].tolist(), b[cut].tolist()))
+    return int(cut.sum()), sorted(pairs)
+
+
+# ----------------------------------------------------------------- merge
+def merge_vehicles(parts):
+    """merge per-domain vehicle reads: per vehicle, the domain reporting it
+    ACTIVE, else ARRIVED, else PENDING (include/tsim.h)"""
+    out = {k: np.array(v, copy=True) for k, v in parts[0].items()}
+    rank = {ACTIVE: 3, ARRIVED: 2, PENDING: 1, ABSENT: 0}
+    best = np.vectorize(rank.get)(out["status"])
+    for p in parts[1:]:
+        r = np.vectorize(rank.get)(p["status"])
+        take = r > best
+        for k in out:
+            out[k][take] = p[k][take]
+        best = np.maximum(best, r)
+    if np.any(best == 0):
+        raise _t.TsError(f"{int(np.sum(best == 0))} vehicles reported by no domain")
+    return out
+
+
+def restore_into(sim, state, t):
+    """place a vehicle state (merged read at time t) into a fresh handle
+    (loaded without initial placement) and resume at t"""
+    st = state["status"]
+    a = np.nonzero(st == ACTIVE)[0]
+    if a.size:
+        sim.place_at(a, state["cursor"][a], state["lane"][a], state["cell"][a], state["v"][a])
+    r = np.nonzero(st == ARRIVED)[0]
+    if r.size:
+        sim.set_arrived(r, state["t_arrive"][r])
+    sim.resume(t)
+
+
+# ------------------------------------------------------ in-process domains
+class LocalDomains:
+    """k domains of one partition, all in this process."""
+
+    def __init__(self, scn, k, domain_of_node=None, t0=0, devices=(0,),
+                 flags=_t.FLAG_FUSED | _t.FLAG_HASH, state=None, **kw):
+        self.scn, self.k, self.flags, self.kw = scn, int(k), flags, kw
+        self.dom = np.asarray(partition(scn, k) if domain_of_node is None else domain_of_node,
+                              np.int32)
+        self.devices = list(devices)
+        self.sims = []
+        for me in range(self.k):
+            s = _t.Sim(p_slow=scn.p_slow, seed=scn.seed, flags=flags,
+                       device=self.devices[me % len(self.devices)], **kw)
+            s.load(scn, place=state is None)
+            s.set_domain(self.k, self.dom, me)
+            if state is None:
+                s.init(t0)
+            else:
+                restore_into(s, state, t0)
+            self.sims.append(s)
+        self._exchange()
+        for s in self.sims:
+            s.phase(2)
+
+    def _exchange(self):
+        if self.k > 1:
+            _t.exchange_local(self.sims)
+
+    def step(self, n=1):
+        for i in range(n):
+            for s in self.sims:
+                s.phase(0)
+            self._exchange()
+            for s in self.sims:
+                s.phase(1, more=i < n - 1)
+            self._exchange()
+            for s in self.sims:
+                s.phase(2)
+
+    @property
+    def t(self):
+        return self.sims[0].t
+
+    def vehicles(self):
+        return merge_vehicles([s.vehicles() for s in self.sims])
+
+    def state_hash(self):
+        return sum(s.state_hash() for s in self.sims) & (2**64 - 1)
+
+    def history(self, t_from, n):
+        hs = [s.history(t_from, n) for s in self.sims]
+        out = {"hash": [sum(h["hash"][i] for h in hs) & (2**64 - 1) for i in range(n)]}
+        for key in ("active", "arrivals", "injections", "lane_changes", "crossings"):
+            out[key] = sum(h[key] for h in hs)
+        return out
+
+    def totals(self):
+        ts = [s.totals() for s in self.sims]
+        return {k: sum(t[k] for t in ts) for k in ts[0]}
+
+    def link_work(self):
+        return sum(s.link_work() for s in self.sims)
+
+    def repartition(self, domain_of_node, k=None):
+        """migrate to a new partition at the current time (exact)"""
+        t, state = self.t, self.vehicles()
+        self.close()
+        self.__init__(self.scn, self.k if k is None else k, domain_of_node, t0=t,
+                      devices=self.devices, flags=self.flags, state=state, **self.kw)
+
+    def close(self):
+        for s in self.sims:
+            s.close()
+        self.sims = []
+
+
+# ------------------------------------------------- one domain per rank
+def exchange_p2p(sends, recvs, peers, group=None):
+    """one message to and from every peer (batched isend / irecv); blocks
+    until the receives are complete (NCCL: until the current stream is
+    ordered after them)"""
+    import torch.distributed as dist
+    if not peers:
+        return
+    ops = []
+    for s, r, p in zip(sends, recvs, peers):
+        g = p if group is None else dist.get_global_rank(group, p)
+        ops.append(dist.P2POp(dist.isend, s, g, group))
+        ops.append(dist.P2POp(dist.irecv, r, g, group))
+    for req in dist.batch_isend_irecv(ops):
+        req.wait()
+
+
+class _CudaBuf:
+    """zero-copy view of a library-owned device buffer for torch"""
+
+    def __init__(self, ptr, nbytes):
+        self.__cuda_array_interface__ = {"shape": (int(nbytes),), "typestr": "|u1",
+                                         "data": (int(ptr), False), "version": 3}
+
+
+class DistDomain:
+    """The domain of this rank; exchanges over torch.distributed."""
+
+    def __init__(self, scn, domain_of_node, device=0, t0=0, flags=_t.FLAG_FUSED, group=None,
+                 state=None, **kw):
+        import torch
+        import torch.distributed as dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.k = dist.get_world_size(group)
+        self.dev = device
+        self.sim = _t.Sim(p_slow=scn.p_slow, seed=scn.seed, flags=flags, device=device, **kw)
+        self.sim.load(scn, place=state is None)
+        self.sim.set_domain(self.k, np.asarray(domain_of_node, np.int32), self.rank)
+        if state is None:
+            self.sim.init(t0)
+        else:
+            restore_into(self.sim, state, t0)
+        self.plan = self.sim.exchange_plan()
+        sb = _t.strip_bytes()
+        sp, rp = self.sim.exchange_buffers()
+        cuda = f"cuda:{device}"
+        self.peers = [p for p, _, _ in self.plan]
+        self.sends = [torch.as_tensor(_CudaBuf(sp + off * sb, n * sb), device=cuda)
+                      for _, n, off in self.plan]
+        self.recvs = [torch.as_tensor(_CudaBuf(rp + off * sb, n * sb), device=cuda)
+                      for _, n, off in self.plan]
+        self.stream = torch.cuda.ExternalStream(self.sim.stream(), device=cuda)
+        self.exchange_ms = 0.0
+        self.exchange()
+        self.sim.phase(2)
+
+    def exchange(self):
+        import torch
+        with torch.cuda.stream(self.stream):
+            exchange_p2p(self.sends, self.recvs, self.peers, self.group)
+
+    def step(self, n=1):
+        for i in range(n):
+            self.sim.phase(0)
+            self.exchange()
+            self.sim.phase(1, more=i < n - 1)
+            self.exchange()
+            self.sim.phase(2)
+
+    @property
+    def t(self):
+        return self.sim.t

@@ -14,7 +14,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_HERE, "libtsim.so")
 
 FLAG_FUSED, FLAG_HASH, FLAG_LINK_WORK, FLAG_GRAPH, FLAG_GENERAL = 1, 2, 4, 8, 16
-PENDING, ACTIVE, ARRIVED = 0, 1, 2
+PENDING, ACTIVE, ARRIVED, ABSENT = 0, 1, 2, 3
 
 
 class TsError(RuntimeError):
@@ -61,6 +61,17 @@ def load_library():
         "ts_get_totals": (ctypes.c_int, [P, P]),
         "ts_get_link_work": (ctypes.c_int, [P, P]),
         "ts_orb_partition": (ctypes.c_int, [I32, P, P, P, I32, P]),
+        "ts_place_vehicles_at": (ctypes.c_int, [P, I32, P, P, P, P, P]),
+        "ts_set_arrived": (ctypes.c_int, [P, I32, P, P]),
+        "ts_set_domain": (ctypes.c_int, [P, I32, P, I32]),
+        "ts_domain_plan": (ctypes.c_int, [I32, I32, P, P, P, P, I32, P, I32, I32, P, P, P]),
+        "ts_strip_bytes": (I32, []),
+        "ts_resume": (ctypes.c_int, [P, I32]),
+        "ts_step_phase": (ctypes.c_int, [P, I32, I32]),
+        "ts_exchange_plan": (ctypes.c_int, [P, I32, P, P, P, P]),
+        "ts_exchange_buffers": (ctypes.c_int, [P, ctypes.POINTER(P), ctypes.POINTER(P)]),
+        "ts_stream": (P, [P]),
+        "ts_exchange_local": (ctypes.c_int, [ctypes.POINTER(P), I32]),
         "ts_last_timing": (ctypes.c_int, [P, ctypes.POINTER(ctypes.c_double),
                                           ctypes.POINTER(ctypes.c_double),
                                           ctypes.POINTER(ctypes.c_int64)]),
@@ -100,8 +111,41 @@ def orb_partition(node_x, node_y, k, weight=None):
     return out
 
 
+def strip_bytes():
+    """bytes of one exchanged strip (5 cells of one lane next to a cut)"""
+    return int(load_library().ts_strip_bytes())
+
+
+def domain_plan(scn, k, domain_of_node, me):
+    """Exchange partners of domain `me` and strips per message (pure host,
+    no device; one buffer per neighbour)."""
+    lib = load_library()
+    i32 = lambda a: _a(a, np.int32)  # noqa: E731
+    fr, to, ln = i32(scn.link_from), i32(scn.link_to), _a(scn.link_len_mm, np.int64)
+    la, dom = i32(scn.link_lanes), i32(domain_of_node)
+    cap = int(k)
+    nb = np.zeros(cap, np.int32)
+    ns = np.zeros(cap, np.int64)
+    n = ctypes.c_int32()
+    rc = lib.ts_domain_plan(scn.n_nodes, scn.n_links, fr.ctypes.data, to.ctypes.data, ln.ctypes.data,
+                            la.ctypes.data, int(k), dom.ctypes.data, int(me), cap, nb.ctypes.data,
+                            ns.ctypes.data, ctypes.byref(n))
+    if rc:
+        raise TsError(f"ts_domain_plan failed ({rc})")
+    return nb[:n.value].tolist(), ns[:n.value].tolist()
+
+
+def exchange_local(sims):
+    """in-process exchange among the handles of one partition"""
+    lib = load_library()
+    arr = (ctypes.c_void_p * len(sims))(*[s.h for s in sims])
+    rc = lib.ts_exchange_local(arr, len(sims))
+    if rc:
+        raise TsError(lib.ts_last_error(sims[0].h).decode())
+
+
 class Sim:
-    """One simulation handle on one GPU."""
+    """One simulation handle (one domain, or the whole network) on one GPU."""
 
     def __init__(self, p_slow=0.2, seed=1, gap_G=5, desp_D=10, flags=FLAG_FUSED | FLAG_HASH,
                  device=0, tile_cells=0, group_cells=0):
@@ -136,7 +180,7 @@ class Sim:
         s.init(t0)
         return s
 
-    def load(self, scn):
+    def load(self, scn, place=True):
         i32 = lambda a: _a(a, np.int32)  # noqa: E731
         i64 = lambda a: _a(a, np.int64)  # noqa: E731
         nx, ny = i64(scn.node_x), i64(scn.node_y)
@@ -150,9 +194,46 @@ class Sim:
         self.n_veh = scn.n_vehicles
         self.n_links = scn.n_links
         self.lanes = np.asarray(scn.link_lanes, dtype=np.int32)
-        if scn.place_vid.size:
+        if place and scn.place_vid.size:
             pl = [i32(scn.place_vid), i32(scn.place_lane), i32(scn.place_cell), i32(scn.place_v)]
             self._check(self.lib.ts_place_vehicles(self.h, pl[0].size, *(a.ctypes.data for a in pl)))
+
+    def place_at(self, vid, cursor, lane, cell, v):
+        """place vehicles on link route[cursor] (restore / repartition)"""
+        a = [_a(x, np.int32) for x in (vid, cursor, lane, cell, v)]
+        self._check(self.lib.ts_place_vehicles_at(self.h, a[0].size, *(_p(x) for x in a)))
+
+    def set_arrived(self, vid, t_arrive):
+        a = [_a(x, np.int32) for x in (vid, t_arrive)]
+        self._check(self.lib.ts_set_arrived(self.h, a[0].size, *(_p(x) for x in a)))
+
+    def set_domain(self, k, domain_of_node, me):
+        d = _a(domain_of_node, np.int32)
+        self._check(self.lib.ts_set_domain(self.h, int(k), _p(d), int(me)))
+
+    def resume(self, t):
+        self._check(self.lib.ts_resume(self.h, int(t)))
+
+    def phase(self, p, more=False):
+        self._check(self.lib.ts_step_phase(self.h, int(p), int(bool(more))))
+
+    def exchange_plan(self):
+        """[(partner domain, strips per message, first strip of its segment)]"""
+        cap = 4096
+        nb, ns, off = np.zeros(cap, np.int32), np.zeros(cap, np.int64), np.zeros(cap, np.int64)
+        n = ctypes.c_int32()
+        self._check(self.lib.ts_exchange_plan(self.h, cap, nb.ctypes.data, ns.ctypes.data,
+                                              off.ctypes.data, ctypes.byref(n)))
+        return [(int(nb[i]), int(ns[i]), int(off[i])) for i in range(n.value)]
+
+    def exchange_buffers(self):
+        """device pointers (send, recv) of the packed strip buffers"""
+        s, r = ctypes.c_void_p(), ctypes.c_void_p()
+        self._check(self.lib.ts_exchange_buffers(self.h, ctypes.byref(s), ctypes.byref(r)))
+        return s.value, r.value
+
+    def stream(self):
+        return self.lib.ts_stream(self.h)
 
     def init(self, t0=0):
         self._check(self.lib.ts_init(self.h, int(t0)))
