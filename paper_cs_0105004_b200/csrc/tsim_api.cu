@@ -97,7 +97,7 @@ struct ts_sim {
   int32_t *d_rvid[2] = {nullptr, nullptr};
   int32_t *d_inj_scratch = nullptr;
   RowDesc *d_rows = nullptr;
-  int rows_threads = 128, rows_blocks = 1;
+  int rows_threads = 128, rows_blocks = 1, rows_cap = 0, rows_smem = 0;
   NodeLane *d_nlanes = nullptr;
   int32_t *d_chunk_off = nullptr;
   int32_t nchunks = 0;
@@ -112,7 +112,9 @@ struct ts_sim {
   uint32_t *d_tt = nullptr;
   int32_t *d_out_pos = nullptr;
   int64_t *d_roff = nullptr;
-  int32_t *d_route = nullptr, *d_cursor = nullptr, *d_dep = nullptr, *d_entry = nullptr;
+  uint8_t *d_rslot = nullptr;
+  NodeOut *d_nodeout = nullptr;
+  int32_t *d_cursor = nullptr, *d_dep = nullptr, *d_entry = nullptr;
   int32_t *d_inj = nullptr, *d_arr = nullptr;
   int32_t *d_pend_off = nullptr, *d_pend_list = nullptr, *d_pend_head = nullptr;
   uint64_t *d_tail = nullptr, *d_entr = nullptr;
@@ -571,7 +573,7 @@ static void build_tiles(ts_sim *h) {
   h->tile_row.assign(h->tiles.size(), -1);
   h->gtiles.clear();
   h->rows.clear();
-  int64_t goff = 0, voff = 0;
+  int64_t goff = 0, voff = 0, gbase = 0;
   int slot = 32;
   for (size_t i = 0; i < h->tiles.size(); i++) {
     const TileDesc &d = h->tiles[i];
@@ -585,22 +587,24 @@ static void build_tiles(ts_sim *h) {
       h->gtiles.push_back(gd);
       continue;
     }
-    if (slot + d.L > 32) {
-      h->rows.resize(h->rows.size() + 32, RowDesc{0, 0, 0, 0, 0, 0, 1});
+    if (slot + d.L > 32) {  // new group: its vid block starts after the last one
+      voff = (voff + 3) & ~(int64_t)3;
+      gbase = voff;
+      h->rows.resize(h->rows.size() + 32, RowDesc{(int32_t)gbase, 0, 0, 0, 0, 0, 1});
       slot = 0;
     }
     const size_t base = h->rows.size() - 32;
     h->tile_row[i] = (int32_t)(base + slot);
     for (int l = 0; l < d.L; l++) {
       RowDesc &r = h->rows[base + slot + l];
-      r.voff = (int32_t)voff;
+      r.voff = (int32_t)gbase;
       r.link = d.link;
       r.lg = d.lane_gid + l;
       r.w = (uint8_t)d.w;
       r.l = (uint8_t)l;
       r.L = (uint8_t)d.L;
       r.vk = (uint8_t)h->vmax[d.link];
-      voff += row_pitch(d.w);
+      voff += d.w;
     }
     slot += d.L;
   }
@@ -639,7 +643,8 @@ static bool build_node_lanes(ts_sim *h, std::vector<NodeLane> &lanes,
         const int j = h->in_list[i];
         if ((h->cls[j] == maxcls) != (pass == 0)) continue;
         for (int l = 0; l < h->lanes[j]; l++)
-          lanes.push_back(NodeLane{h->lgid[j] + l, j, nd, (int16_t)l, (int16_t)(pass == 0)});
+          lanes.push_back(NodeLane{h->lgid[j] + l, nd, h->out_off[nd], h->tt[j], (uint8_t)l,
+                                   (uint8_t)(pass == 0), (uint8_t)h->vmax[j], 0});
       }
     in_chunk += nl;
   }
@@ -684,7 +689,7 @@ static StepParams step_params(ts_sim *h, int t, int mode) {
   P.tt_link = h->d_tt;
   P.out_pos = h->d_out_pos;
   P.route_off = h->d_roff;
-  P.route = h->d_route;
+  P.rslot = h->d_rslot;
   P.cursor = h->d_cursor;
   P.dep = h->d_dep;
   P.entry = h->d_entry;
@@ -723,7 +728,8 @@ static NodeParams node_params(ts_sim *h, int t) {
   N.tt_link = h->d_tt;
   N.out_pos = h->d_out_pos;
   N.route_off = h->d_roff;
-  N.route = h->d_route;
+  N.rslot = h->d_rslot;
+  N.nodeout = h->d_nodeout;
   N.cursor = h->d_cursor;
   N.tail_rec = h->d_tail;
   N.head_occ = h->d_head;
@@ -742,6 +748,7 @@ static RowsParams rows_params(ts_sim *h) {
   r.vid_out = h->d_rvid[h->rcur ^ 1];
   r.inj_scratch = h->d_inj_scratch;
   r.ngroups = h->ngroups;
+  r.cap = h->rows_cap;
   return r;
 }
 
@@ -833,15 +840,19 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
   if (h->rvid_entries > INT32_MAX) return fail(h, TS_EINVAL, "network too large for one device");
   std::vector<uint32_t> planes(group_plane_base(h->ngroups), 0u);
   std::vector<int32_t> rvid(h->rvid_entries, -1);
-  for (size_t ti = 0; ti < h->tiles.size(); ti++) {
-    if (h->tile_row[ti] < 0) continue;
-    const TileDesc &d = h->tiles[ti];
-    const int Wp = row_pitch(d.w);
-    for (int l = 0; l < d.L; l++) {
-      const int s = h->tile_row[ti] + l;
-      uint32_t *pl = planes.data() + group_plane_base(s >> 5) + (s & 31);
-      const RowDesc &rd = h->rows[s];
-      int64_t r = d.off + (int64_t)l * Wp, k = 0;
+  std::vector<int32_t> row_tile(h->rows.size(), -1);  // row slot -> tile
+  for (size_t ti = 0; ti < h->tiles.size(); ti++)
+    if (h->tile_row[ti] >= 0)
+      for (int l = 0; l < h->tiles[ti].L; l++) row_tile[h->tile_row[ti] + l] = (int32_t)ti;
+  for (int g = 0; g < h->ngroups; g++) {
+    int64_t k = h->rows[(size_t)g * 32].voff;  // the group's block: rows in slot order
+    for (int sl = 0; sl < 32; sl++) {
+      const int s = g * 32 + sl;
+      if (row_tile[s] < 0) continue;
+      const TileDesc &d = h->tiles[row_tile[s]];
+      const int l = h->rows[s].l, Wp = row_pitch(d.w);
+      uint32_t *pl = planes.data() + group_plane_base(g) + sl;
+      int64_t r = d.off + (int64_t)l * Wp;
       for (int x = 0; x < d.w; x++) {
         const uint8_t c = code[d.off + (int64_t)l * Wp + x];
         if (c == kEmpty) continue;
@@ -859,7 +870,7 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
         }
         for (int b = 0; b < 2; b++)
           if ((cls >> b) & 1) pl[((4 + b) * kRowWords + wd) * 32] |= bit;
-        rvid[rd.voff + k++] = (int32_t)((uint32_t)vids[r++] | ((uint32_t)slot << kSlotShift));
+        rvid[k++] = (int32_t)((uint32_t)vids[r++] | ((uint32_t)slot << kSlotShift));
       }
     }
   }
@@ -928,7 +939,8 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
     for (size_t ti = 0; ti < h->tiles.size() && !need; ti++)
       if (h->tile_row[ti] >= 0 && pend_off[h->tiles[ti].link + 1] > pend_off[h->tiles[ti].link])
         need = true;
-    if ((rc = dalloc(h, &h->d_inj_scratch, need ? h->rvid_entries : 16, 0xFF))) return rc;
+    if ((rc = dalloc(h, &h->d_inj_scratch, need ? h->rows.size() * kRowMaxCells : 16, 0xFF)))
+      return rc;
   }
   if ((rc = upload(h, &h->d_halo_up, h->halo_up))) return rc;
   if ((rc = upload(h, &h->d_halo_dn, h->halo_dn))) return rc;
@@ -936,7 +948,19 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
   if ((rc = upload(h, &h->d_tt, h->tt))) return rc;
   if ((rc = upload(h, &h->d_out_pos, h->out_pos))) return rc;
   if ((rc = upload(h, &h->d_roff, h->roff))) return rc;
-  if ((rc = upload(h, &h->d_route, h->route))) return rc;
+  {  // routes as out-slot sequences: rslot[j] = slot of R[j] at its from-node
+    std::vector<uint8_t> rslot(h->route.size(), 0xFF);
+    for (int f = 0; f < h->nv; f++)
+      for (int64_t j = h->roff[f] + 1; j < h->roff[f + 1]; j++)
+        rslot[j] = (uint8_t)h->out_pos[h->route[j]];
+    if ((rc = upload(h, &h->d_rslot, rslot))) return rc;
+    std::vector<NodeOut> nodeout(h->out_list.size());
+    for (size_t i = 0; i < h->out_list.size(); i++) {
+      const int k = h->out_list[i];
+      nodeout[i] = NodeOut{h->lgid[k], (int16_t)h->lanes[k], (int16_t)std::min(h->ncell[k], 32767)};
+    }
+    if ((rc = upload(h, &h->d_nodeout, nodeout))) return rc;
+  }
   if ((rc = upload(h, &h->d_cursor, cur0))) return rc;
   if ((rc = upload(h, &h->d_dep, h->dep))) return rc;
   if ((rc = upload(h, &h->d_entry, h->entry))) return rc;
@@ -974,9 +998,13 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
   int occ = std::max(1, occupancy_blocks(h->threads, h->smem));
   const int need = (int)((h->gtiles.size() + wpb - 1) / wpb);
   h->blocks = std::max(1, std::min(need, occ * nsm));
-  // row kernel: one warp per 32-row group, 4 warps per block
+  // row kernel: one warp per 32-row group, 4 warps per block; each warp
+  // stages its group's vid blocks (in + out) in shared memory
   h->rows_threads = 128;
   h->rows_blocks = std::max(1, (h->ngroups + 3) / 4);
+  h->rows_cap = 1664;
+  h->rows_smem = 4 * 2 * h->rows_cap * 4;
+  CK(h, set_rows_smem(h->rows_smem));
   {
     std::vector<NodeLane> nlanes;
     std::vector<int32_t> chunk_off;
@@ -1015,7 +1043,7 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
   int mode = (inject0 ? kModeInject : 0) | (base_mode(h) & kModeHash);
   StepParams P = step_params(h, t0 - 1, mode);
   if (h->ngroups > 0) {
-    launch_rows(P, rows_params(h), h->rows_blocks, h->rows_threads, 0, h->stream);
+    launch_rows(P, rows_params(h), h->rows_blocks, h->rows_threads, h->rows_smem, h->stream);
     h->rcur ^= 1;
   }
   if (!h->gtiles.empty()) {
@@ -1061,7 +1089,7 @@ static void phase_lc(ts_sim *h) {
     h->gcur ^= 1;
   }
   if (h->ngroups > 0 && !h->rows_s1) {
-    launch_rows(step_params(h, t, kModeLC), rows_params(h), h->rows_blocks, h->rows_threads, 0,
+    launch_rows(step_params(h, t, kModeLC), rows_params(h), h->rows_blocks, h->rows_threads, h->rows_smem,
                 h->stream);
     h->rcur ^= 1;
   }
@@ -1085,7 +1113,7 @@ static void phase_move(ts_sim *h, bool more, cudaEvent_t e0, cudaEvent_t e1) {
   if (h->ngroups > 0) {
     const bool f = more && h->rfused;
     launch_rows(step_params(h, t, mode | (f ? kModeLC : 0)), rows_params(h), h->rows_blocks,
-                h->rows_threads, 0, h->stream);
+                h->rows_threads, h->rows_smem, h->stream);
     h->rcur ^= 1;
     h->rows_s1 = f;
   }
@@ -1331,18 +1359,25 @@ static int download_tiles(ts_sim *h, int t0, int t1, std::vector<uint8_t> &code,
     }
   }
   if (s0 >= 0) {
-    // row tiles: planes of the covering groups and the span of their vid lists
+    // row tiles: planes and vid blocks of the covering groups; a row's list
+    // starts at the prefix of the vehicle counts of the rows before it
     const int gr0 = s0 >> 5, gr1 = ((s1 - 1) >> 5) + 1;
-    int64_t va = INT64_MAX, vb = 0;
-    for (int s = s0; s < s1; s++) {
-      va = std::min<int64_t>(va, h->rows[s].voff);
-      vb = std::max<int64_t>(vb, h->rows[s].voff + row_pitch(h->rows[s].w));
-    }
+    const int64_t va = h->rows[(size_t)gr0 * 32].voff;
+    const int64_t vb = gr1 < h->ngroups ? h->rows[(size_t)gr1 * 32].voff : h->rvid_entries;
     std::vector<uint32_t> pl(group_plane_base(gr1) - group_plane_base(gr0));
     std::vector<int32_t> rv(vb - va);
     CK(h, cudaMemcpy(pl.data(), h->d_planes[h->rcur] + group_plane_base(gr0), pl.size() * 4,
                      cudaMemcpyDeviceToHost));
     CK(h, cudaMemcpy(rv.data(), h->d_rvid[h->rcur] + va, rv.size() * 4, cudaMemcpyDeviceToHost));
+    std::vector<int64_t> roff((size_t)(gr1 - gr0) * 32);
+    for (int g = gr0; g < gr1; g++) {
+      int64_t k = h->rows[(size_t)g * 32].voff - va;
+      for (int sl = 0; sl < 32; sl++) {
+        roff[(size_t)(g - gr0) * 32 + sl] = k;
+        const uint32_t *P = pl.data() + (group_plane_base(g) - group_plane_base(gr0)) + sl;
+        for (int wd = 0; wd < kRowWords; wd++) k += __builtin_popcount(P[wd * 32]);
+      }
+    }
     for (int ti = t0; ti < t1; ti++) {
       if (h->tile_row[ti] < 0) continue;
       const TileDesc &d = h->tiles[ti];
@@ -1350,7 +1385,7 @@ static int download_tiles(ts_sim *h, int t0, int t1, std::vector<uint8_t> &code,
       for (int l = 0; l < d.L; l++) {
         const int s = h->tile_row[ti] + l;
         const uint32_t *P = pl.data() + (group_plane_base(s >> 5) - group_plane_base(gr0)) + (s & 31);
-        const int32_t *lst = rv.data() + (h->rows[s].voff - va);
+        const int32_t *lst = rv.data() + roff[(size_t)(s - gr0 * 32)];
         const int64_t rb = d.off - c0 + (int64_t)l * Wp;
         int64_t r = rb, k = 0;
         for (int x = 0; x < d.w; x++) {

@@ -81,9 +81,13 @@ __host__ __device__ inline int64_t tile_cells_padded(int w, int L) {
 // x >> 5 being cell x.  Planes are stored group-interleaved so that every
 // warp access is one contiguous 128-byte line:
 //   planes[group_plane_base(g) + (p * kRowWords + i) * 32 + slot].
-// The vehicles of a row are listed in cell order at vid[voff + k] as
-// entries vid | slot << 27 (the out-slot travels with the vehicle in its
-// list entry; list order is preserved by the move).
+// The vehicles of a group are listed in one contiguous block at vid[voff]
+// (capacity: the group's cells): row after row in slot order, each row's
+// vehicles in cell order, as entries vid | slot << 27 (the out-slot travels
+// with the vehicle in its list entry; list order is preserved by the
+// move).  A row's list starts at the prefix sum of the vehicle counts of
+// the rows before it (popcounts of their occupancy planes), so the block
+// is read and written with dense, coalesced warp accesses.
 constexpr int kSlotShift = 27;
 constexpr uint32_t kVidMask = (1u << kSlotShift) - 1u;
 constexpr int kRowWords = 4;
@@ -95,7 +99,7 @@ __host__ __device__ inline size_t group_plane_base(int64_t g) {
 }
 
 struct RowDesc {
-  int32_t voff;  // first entry of the row's vid list (multiple of 4)
+  int32_t voff;  // first entry of the group's vid block (multiple of 4)
   int32_t link;
   int32_t lg;    // global lane id
   uint8_t w;     // cells (0 = empty slot)
@@ -109,10 +113,18 @@ static_assert(sizeof(RowDesc) == 16, "RowDesc must be 16 bytes");
 // into chunks of <= 32 that never split a node.
 struct NodeLane {
   int32_t lane_gid;
-  int32_t link;
   int32_t node;
-  int16_t lane;
-  int16_t major;
+  int32_t out_base;  // first NodeOut entry of the node (its out-slots)
+  uint32_t tt;       // turn types of the link's out-slots (2 bits each)
+  uint8_t lane, major, vk, pad;
+};
+static_assert(sizeof(NodeLane) == 20, "NodeLane must be 20 bytes");
+
+// an outgoing link of a node, by out-slot: what a winner needs to enter it
+struct NodeOut {
+  int32_t lgid;  // global id of its lane 0
+  int16_t L;     // lanes
+  int16_t n;     // cells
 };
 
 __host__ __device__ inline WarpLayout warp_layout(int NCmax) {
@@ -174,7 +186,7 @@ struct StepParams {
   const int32_t *out_pos;   // slot of each link at its from-node
   // vehicles
   const int64_t *route_off;
-  const int32_t *route;
+  const uint8_t *rslot;  // per route entry j >= 1: out-slot of link R[j] at its from-node
   int32_t *cursor;
   const int32_t *dep;
   const int32_t *entry;
@@ -206,8 +218,9 @@ struct NodeParams {
   const uint32_t *tt_link;
   const int32_t *out_pos;
   const int64_t *route_off;
-  const int32_t *route;
+  const uint8_t *rslot;
   int32_t *cursor;
+  const NodeOut *nodeout;  // [out_off[node] + slot]
   const uint64_t *tail_rec;
   const uint8_t *head_occ;
   uint8_t *ext;
@@ -228,8 +241,9 @@ struct RowsParams {
   uint32_t *planes_out;
   const int32_t *vid_in;      // row vid lists
   int32_t *vid_out;
-  int32_t *inj_scratch;       // per lane-0 row cell: entry of a vehicle injected there
+  int32_t *inj_scratch;       // [row slot * kRowMaxCells + cell]: entry of a vehicle injected there
   int32_t ngroups;
+  int32_t cap;                // smem staging capacity (entries) of a group's vid block
 };
 
 struct NodeWarpParams {

@@ -465,42 +465,44 @@ __global__ void __launch_bounds__(256) k_hash(const StepParams P, unsigned long 
 // ====================================================================
 struct Cand {
   bool cand;
-  int tgt, k2, l2, d, v, vid;
+  int tgt, n2, d, v, vid;
 };
 
-__device__ __forceinline__ Cand node_candidate(const NodeParams &P, uint64_t rec, int link,
-                                               int lane, int node) {
-  Cand c{false, -1, 0, 0, 0, 0, 0};
+// the front vehicle of an incoming lane: candidate to cross (d < min(v+1,
+// V)) unless it is on its final link; its target lane (R8)
+__device__ __forceinline__ Cand node_candidate(const NodeParams &P, uint64_t rec, int lane,
+                                               int out_base, uint32_t tt, int vk) {
+  Cand c{false, -1, 0, 0, 0, 0};
   if (!((rec >> 43) & 1)) return c;
   const int code = (int)((rec >> 32) & 0xFF);
   c.d = (int)((rec >> 40) & 7);
   c.v = code & 7;
   const int slot = code >> 3;
-  if (slot == kSlotFinal || !(c.d < min(c.v + 1, (int)P.vmax_link[link]))) return c;
-  c.k2 = P.out_list[P.out_off[node] + slot];
-  const int tty = (P.tt_link[link] >> (2 * slot)) & 3;
-  const int L2 = P.link_lanes[c.k2];
-  c.l2 = tty == 0 ? min(lane, L2 - 1) : (tty == 2 ? 0 : L2 - 1);  // R8
-  c.tgt = P.link_lgid[c.k2] + c.l2;
+  if (slot == kSlotFinal || !(c.d < min(c.v + 1, vk))) return c;
+  const NodeOut o = P.nodeout[out_base + slot];
+  const int tty = (tt >> (2 * slot)) & 3;
+  const int l2 = tty == 0 ? min(lane, o.L - 1) : (tty == 2 ? 0 : o.L - 1);  // R8
+  c.tgt = o.lgid + l2;
+  c.n2 = o.n;
   c.vid = (int)(uint32_t)rec;
   c.cand = true;
   return c;
 }
 
 // the winner's grant: returns ext; writes the entrant record if it crosses
-__device__ __forceinline__ int node_grant(const NodeParams &P, const Cand &c, int link,
+__device__ __forceinline__ int node_grant(const NodeParams &P, const Cand &c, int vk,
                                           uint32_t &crossings) {
-  const int E = min(ctz32((uint32_t)P.head_occ[c.tgt] | 0x20u), min(kGmax, P.link_ncell[c.k2]));
+  const int E = min(ctz32((uint32_t)P.head_occ[c.tgt] | 0x20u), min(kGmax, c.n2));
   if (E == 0) return 0;
-  const int v3 = nasch_v3(c.v, P.vmax_link[link], min(kGmax, c.d + E), (uint32_t)P.t,
-                          (uint32_t)c.vid, P.k0, P.k1, P.p32);
+  const int v3 = nasch_v3(c.v, vk, min(kGmax, c.d + E), (uint32_t)P.t, (uint32_t)c.vid, P.k0,
+                          P.k1, P.p32);
   if (v3 > c.d) {
-    const int y2 = v3 - c.d - 1;
+    // independent loads first (the cursor store must not serialise them)
     const int r = P.cursor[c.vid];
+    const int64_t ro = P.route_off[c.vid], re = P.route_off[c.vid + 1];
+    const int nslot = (ro + r + 2 < re) ? (int)P.rslot[ro + r + 2] : kSlotFinal;
     P.cursor[c.vid] = r + 1;
-    const int64_t ro = P.route_off[c.vid];
-    const int m = (int)(P.route_off[c.vid + 1] - ro);
-    const int nslot = (r + 2 < m) ? P.out_pos[P.route[ro + r + 2]] : kSlotFinal;
+    const int y2 = v3 - c.d - 1;
     P.entr[c.tgt] = (uint64_t)(uint32_t)c.vid | ((uint64_t)(v3 | (nslot << 3)) << 32) |
                     ((uint64_t)y2 << 40) | ((uint64_t)((P.t + 1) & 0x1FFFFF) << 43);
     crossings++;
@@ -534,7 +536,7 @@ __global__ void __launch_bounds__(256) k_node_warp(const NodeParams P, const Nod
        c += nwarps_total) {
     const int a = W.chunk_off[c], n = W.chunk_off[c + 1] - a;
     const bool act = lane < n;
-    NodeLane e{0, 0, -1 - lane, 0, 0};
+    NodeLane e{0, -1 - lane, 0, 0u, 0, 0, 1, 0};
     uint64_t rec = 0;
     if (act) {
       e = W.lanes[a + lane];
@@ -543,13 +545,13 @@ __global__ void __launch_bounds__(256) k_node_warp(const NodeParams P, const Nod
     const uint32_t nodemask = __match_any_sync(FULL, e.node);
     const bool busy = (__ballot_sync(FULL, act && e.major && (((uint32_t)(rec >> 44)) & gmask)) &
                        nodemask) != 0u;
-    Cand cd{false, -1, 0, 0, 0, 0, 0};
-    if (act) cd = node_candidate(P, rec, e.link, e.lane, e.node);
+    Cand cd{false, -1, 0, 0, 0, 0};
+    if (act) cd = node_candidate(P, rec, e.lane, e.out_base, e.tt, e.vk);
     const bool eligible = cd.cand && (e.major || !busy);
     const int key = eligible ? cd.tgt : -1 - lane;
     const uint32_t grp = __match_any_sync(FULL, key);
     int ext = 0;
-    if (eligible && (__ffs(grp) - 1) == lane) ext = node_grant(P, cd, e.link, crossings);
+    if (eligible && (__ffs(grp) - 1) == lane) ext = node_grant(P, cd, e.vk, crossings);
     if (act) P.ext[e.lane_gid] = (uint8_t)ext;
   }
   node_flush(P, crossings, red);
@@ -576,7 +578,9 @@ __global__ void __launch_bounds__(128) k_node(const NodeParams P) {
           majorfree = false;
       }
     }
-    uint32_t claimed[4] = {0u, 0u, 0u, 0u};  // (slot, lane) targets taken
+    constexpr int kMaxClaim = 128;  // target lanes taken (<= out-links x lanes)
+    int claimed[kMaxClaim];
+    int nclaimed = 0;
     for (int pass = 0; pass < 2; pass++) {
       if (pass == 1 && !majorfree) break;
       for (int i = a; i < b; i++) {
@@ -585,13 +589,14 @@ __global__ void __launch_bounds__(128) k_node(const NodeParams P) {
         const int lg = P.link_lgid[j];
         for (int l = 0; l < P.link_lanes[j]; l++) {
           const uint64_t rec = P.tail_rec[lg + l];
-          const Cand cd = node_candidate(P, rec, j, l, node);
+          const Cand cd = node_candidate(P, rec, l, P.out_off[node], P.tt_link[j], P.vmax_link[j]);
           if (!cd.cand) continue;
-          const int slot = (int)((rec >> 35) & 15);
-          const int bit = slot * 8 + cd.l2;
-          if (claimed[bit >> 5] & (1u << (bit & 31))) continue;
-          claimed[bit >> 5] |= 1u << (bit & 31);
-          P.ext[lg + l] = (uint8_t)node_grant(P, cd, j, crossings);
+          const int bit = cd.tgt;  // target lanes of a node are distinct global lanes
+          bool taken = false;
+          for (int q = 0; q < nclaimed; q++) taken |= claimed[q] == bit;
+          if (taken) continue;
+          if (nclaimed < kMaxClaim) claimed[nclaimed++] = bit;
+          P.ext[lg + l] = (uint8_t)node_grant(P, cd, P.vmax_link[j], crossings);
         }
       }
     }

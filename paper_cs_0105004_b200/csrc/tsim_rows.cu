@@ -97,11 +97,39 @@ __device__ __forceinline__ uint32_t range_w(int i, int a, int b) {
   return lowm(b - 32 * i) & ~lowm(a - 32 * i);
 }
 __device__ __forceinline__ uint32_t shfl_w(uint32_t v, int src) { return __shfl_sync(FULL, v, src); }
+
+// exclusive warp prefix sum; *total = warp sum
+__device__ __forceinline__ int warp_scan(int v, int lane, int *total) {
+  int s = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(FULL, s, o);
+    if (lane >= o) s += y;
+  }
+  *total = __shfl_sync(FULL, s, 31);
+  return s - v;
+}
+// coalesced warp copies of n entries between 16-byte aligned buffers
+__device__ __forceinline__ void warp_load(int32_t *dst, const int32_t *gsrc, int n, int lane) {
+  const int n4 = n >> 2;
+  for (int i = lane; i < n4; i += 32)
+    reinterpret_cast<int4 *>(dst)[i] = __ldcs(reinterpret_cast<const int4 *>(gsrc) + i);
+  for (int i = 4 * n4 + lane; i < n; i += 32) dst[i] = __ldcs(gsrc + i);
+}
+__device__ __forceinline__ void warp_store(int32_t *gdst, const int32_t *src, int n, int lane) {
+  const int n4 = n >> 2;
+  for (int i = lane; i < n4; i += 32)
+    __stcs(reinterpret_cast<int4 *>(gdst) + i, reinterpret_cast<const int4 *>(src)[i]);
+  for (int i = 4 * n4 + lane; i < n; i += 32) __stcs(gdst + i, src[i]);
+}
 }  // namespace
 
 __global__ void __launch_bounds__(128) k_rows(const StepParams P, const RowsParams R) {
   __shared__ unsigned long long red[4 * 8];
+  extern __shared__ __align__(16) int32_t stage[];  // per warp: vid block in, vid block out
   const int lane = threadIdx.x & 31;
+  int32_t *s_in = stage + (threadIdx.x >> 5) * 2 * R.cap;
+  int32_t *s_out = s_in + R.cap;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   const bool do_move = (P.mode & kModeMove) != 0;
   const bool hash = (P.mode & kModeHash) != 0;
@@ -112,6 +140,7 @@ __global__ void __launch_bounds__(128) k_rows(const StepParams P, const RowsPara
   Acc acc_next = {};
 
   for (int g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; g < R.ngroups; g += nwarps) {
+    __syncwarp();  // the previous group's staged blocks are no longer in use
     const RowDesc rd = R.rows[(size_t)g * 32 + lane];
     const int w = rd.w, l = rd.l, L = rd.L, link = rd.link, lg = rd.lg, vk = rd.vk;
     const uint32_t *pin = R.planes_in + group_plane_base(g) + lane;
@@ -125,11 +154,19 @@ __global__ void __launch_bounds__(128) k_rows(const StepParams P, const RowsPara
       A0[i] = __ldcs(pin + (4 * NW + i) * 32);
       A1[i] = __ldcs(pin + (5 * NW + i) * 32);
     }
-    const int32_t *vin = R.vid_in + rd.voff;
     uint32_t VAL[NW];
 #pragma unroll
     for (int i = 0; i < NW; i++) VAL[i] = lowm(w - 32 * i);
     const int nin = popc_row(O);
+    // the group's vid block: staged in shared memory when it fits
+    int tot_in;
+    const int in_off = warp_scan(nin, lane, &tot_in);
+    const bool staged = tot_in <= R.cap;
+    if (staged) {
+      warp_load(s_in, R.vid_in + rd.voff, tot_in, lane);
+      __syncwarp();
+    }
+    const int32_t *vin = (staged ? (const int32_t *)s_in : R.vid_in + rd.voff) + in_off;
     acc.work += nin;
     if ((P.mode & kModeWork) && P.link_work && nin)
       atomicAdd(P.link_work + link, (unsigned long long)nin);
@@ -145,7 +182,7 @@ __global__ void __launch_bounds__(128) k_rows(const StepParams P, const RowsPara
       const int xf = top_row(O);
       const int nb = min(w, kGmax);
       const bool front_zone = xf >= w - nb && xf >= 0;
-      if (front_zone) efront = (uint32_t)__ldg(vin + nin - 1);
+      if (front_zone) efront = (uint32_t)vin[nin - 1];
       // ---- thermometer codes U_k (v2 >= k), cells past the row end occupied
       uint32_t Oext[NW], F[NW], S[NW];
 #pragma unroll
@@ -192,7 +229,7 @@ __global__ void __launch_bounds__(128) k_rows(const StepParams P, const RowsPara
           while (m) {
             const int x = __ffs(m) - 1;
             m &= m - 1u;
-            const uint32_t e = (uint32_t)__ldg(vin + rb + __popc(O[i] & lowm(x)));
+            const uint32_t e = (uint32_t)vin[rb + __popc(O[i] & lowm(x))];
             if ((uint64_t)philox_w0((uint32_t)P.t, e & kVidMask, P.k0, P.k1) < P.p32)
               b |= 1u << x;
           }
@@ -292,7 +329,7 @@ __global__ void __launch_bounds__(128) k_rows(const StepParams P, const RowsPara
     for (int i = 0; i < NW; i++) INJ[i] = 0u;
     bool injected = false;
     if ((P.mode & kModeInject) && w > 0 && l == 0 && P.pend_off[link + 1] > P.pend_head[link]) {
-      int32_t *scratch = R.inj_scratch + rd.voff;
+      int32_t *scratch = R.inj_scratch + ((size_t)g * 32 + lane) * kRowMaxCells;
       inject_link(
           P, link, 0, w, true, [&](int x) { return !bit_row(OO, x); },
           [&](int x, uint8_t code, int ivid) {
@@ -460,53 +497,33 @@ __global__ void __launch_bounds__(128) k_rows(const StepParams P, const RowsPara
       }
     }
 
-    // ---- vid lists of the final state
+    // ---- vid lists of the final state: the group's output block, staged
+    //      in shared memory when it fits, written back with coalesced stores
     const int nfin = popc_row(FO);
-    int32_t *vout = R.vid_out + rd.voff;
+    int tot_out;
+    const int out_off = warp_scan(nfin, lane, &tot_out);
+    const bool ostaged = tot_out <= R.cap;
+    int32_t *obase = ostaged ? s_out : R.vid_out + rd.voff;
+    int32_t *vout = obase + out_off;
     const bool moved_lc = any_row(LV) || any_row(AR);
     const bool general = moved_lc || injected || hash;
-    const bool gany = __any_sync(FULL, general);
-    uint32_t efin = 0u;  // list entry of the final front vehicle
     if (!general && nfin > 0) {
-      const uint4 *src = reinterpret_cast<const uint4 *>(vin);
-      uint4 *dst = reinterpret_cast<uint4 *>(vout);
       if (!has_ent) {
         // input vehicles minus an exit at the front: a prefix of the input list
-        uint4 a = make_uint4(0, 0, 0, 0);
-        int i = 0;
-        for (; i + 8 <= nfin; i += 8) {
-          const uint4 a0 = __ldcs(src + (i >> 2)), a1 = __ldcs(src + (i >> 2) + 1);
-          __stcs(dst + (i >> 2), a0);
-          __stcs(dst + (i >> 2) + 1, a1);
-          a = a1;
-        }
-        for (; i < nfin; i += 4) {
-          a = __ldcs(src + (i >> 2));
-          __stcs(dst + (i >> 2), a);
-        }
-        const int k = (nfin - 1) & 3;
-        efin = k == 0 ? a.x : k == 1 ? a.y : k == 2 ? a.z : a.w;
+        for (int i = 0; i < nfin; i++) vout[i] = vin[i];
       } else {
         // the entrant lands behind every vehicle: the list shifts by one
-        uint32_t prev = ent_e;
-        uint4 o = make_uint4(prev, 0, 0, 0);
-        for (int i = 0; i < nfin; i += 4) {
-          const uint4 a = __ldcs(src + (i >> 2));
-          o = make_uint4(prev, a.x, a.y, a.z);
-          prev = a.w;
-          __stcs(dst + (i >> 2), o);
-        }
-        const int k = (nfin - 1) & 3;
-        efin = k == 0 ? o.x : k == 1 ? o.y : k == 2 ? o.z : o.w;
+        vout[0] = (int32_t)ent_e;
+        for (int i = 1; i < nfin; i++) vout[i] = vin[i - 1];
       }
     }
-    if (gany) {
+    if (__any_sync(FULL, general)) {
       // every vehicle of S(t+1) before the lane change, in cell order, goes
       // to its rank in the final occupancy of its row (own, or l + dir)
       uint32_t FT[NW];
 #pragma unroll
       for (int i = 0; i < NW; i++) FT[i] = shfl_w(FO[i], lane + dir);
-      const int toff = __shfl_sync(FULL, rd.voff, lane + dir);
+      int32_t *tout = obase + __shfl_sync(FULL, out_off, lane + dir);
       if (general) {
         int k = 0, rown = 0, rtgt = 0;
 #pragma unroll
@@ -518,15 +535,16 @@ __global__ void __launch_bounds__(128) k_rows(const StepParams P, const RowsPara
             const int c = 32 * i + x;
             uint32_t e;
             if (c == ent_y) e = ent_e;
-            else if ((INJ[i] >> x) & 1u) e = (uint32_t)R.inj_scratch[rd.voff + c];
-            else e = (uint32_t)__ldg(vin + k++);
+            else if ((INJ[i] >> x) & 1u)
+              e = (uint32_t)R.inj_scratch[((size_t)g * 32 + lane) * kRowMaxCells + c];
+            else e = (uint32_t)vin[k++];
             if (hash) {  // state hash of S(t+1), before its lane change (tests)
               const int v = (int)((OV0[i] >> x) & 1u) | (int)(((OV1[i] >> x) & 1u) << 1) |
                             (int)(((OV2[i] >> x) & 1u) << 2);
               acc.hash += vmix((int)(e & kVidMask), link, l, c, v);
             }
             if ((LV[i] >> x) & 1u)
-              R.vid_out[toff + rtgt + __popc(FT[i] & lowm(x))] = (int32_t)e;
+              tout[rtgt + __popc(FT[i] & lowm(x))] = (int32_t)e;
             else
               vout[rown + __popc(FO[i] & lowm(x))] = (int32_t)e;
           }
@@ -534,9 +552,10 @@ __global__ void __launch_bounds__(128) k_rows(const StepParams P, const RowsPara
           rtgt += __popc(FT[i]);
         }
       }
-      __syncwarp();
-      if (general && nfin > 0) efin = (uint32_t)vout[nfin - 1];
     }
+    __syncwarp();
+    const uint32_t efin = nfin > 0 ? (uint32_t)vout[nfin - 1] : 0u;  // final front vehicle
+    if (ostaged) warp_store(R.vid_out + rd.voff, s_out, tot_out, lane);
     // ---- node records of the output S1 (read by k_node_warp, H3)
     if (lc && w > 0) {
       const int nb = min(w, kGmax);
@@ -563,12 +582,18 @@ __global__ void __launch_bounds__(128) k_rows(const StepParams P, const RowsPara
 // state hash of the row-mode state S(t) (one thread per lane-row)
 __global__ void __launch_bounds__(128) k_rows_hash(const RowsParams R, unsigned long long *out) {
   const int gid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int g = gid >> 5, lane = gid & 31;
   uint64_t h = 0, cnt = 0;
-  if (gid < R.ngroups * 32) {
+  const bool act = g < R.ngroups;
+  const uint32_t *pl = R.planes_in + group_plane_base(act ? g : 0) + lane;
+  int n = 0;
+  if (act)
+    for (int i = 0; i < NW; i++) n += __popc(pl[i * 32]);
+  int tot;
+  const int off = warp_scan(n, lane, &tot);
+  if (act) {
     const RowDesc rd = R.rows[gid];
-    const int g = gid >> 5, lane = gid & 31;
-    const uint32_t *pl = R.planes_in + group_plane_base(g) + lane;
-    const int32_t *vl = R.vid_in + rd.voff;
+    const int32_t *vl = R.vid_in + rd.voff + off;
     int k = 0;
     for (int i = 0; i < NW; i++) {
       uint32_t m = pl[i * 32];
