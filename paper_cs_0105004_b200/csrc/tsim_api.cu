@@ -95,6 +95,7 @@ struct ts_sim {
   int64_t rvid_entries = 0;
   uint32_t *d_planes[2] = {nullptr, nullptr};
   int32_t *d_rvid[2] = {nullptr, nullptr};
+  int32_t *d_gcnt[2] = {nullptr, nullptr};  // vehicles per group
   int32_t *d_inj_scratch = nullptr;
   RowDesc *d_rows = nullptr;
   int rows_threads = 128, rows_blocks = 1, rows_cap = 0, rows_smem = 0;
@@ -114,7 +115,8 @@ struct ts_sim {
   int64_t *d_roff = nullptr;
   uint8_t *d_rslot = nullptr;
   NodeOut *d_nodeout = nullptr;
-  int32_t *d_cursor = nullptr, *d_dep = nullptr, *d_entry = nullptr;
+  VehPos *d_vpos = nullptr;
+  int32_t *d_dep = nullptr, *d_entry = nullptr;
   int32_t *d_inj = nullptr, *d_arr = nullptr;
   int32_t *d_pend_off = nullptr, *d_pend_list = nullptr, *d_pend_head = nullptr;
   uint64_t *d_tail = nullptr, *d_entr = nullptr;
@@ -638,13 +640,15 @@ static bool build_node_lanes(ts_sim *h, std::vector<NodeLane> &lanes,
       chunk_off.push_back((int32_t)lanes.size());
       in_chunk = 0;
     }
+    const int node_first = in_chunk;  // the node's first lane in its chunk (match key)
     for (int pass = 0; pass < 2; pass++)
       for (int i = a; i < b; i++) {
         const int j = h->in_list[i];
         if ((h->cls[j] == maxcls) != (pass == 0)) continue;
         for (int l = 0; l < h->lanes[j]; l++)
-          lanes.push_back(NodeLane{h->lgid[j] + l, nd, h->out_off[nd], h->tt[j], (uint8_t)l,
-                                   (uint8_t)(pass == 0), (uint8_t)h->vmax[j], 0});
+          lanes.push_back(NodeLane{h->lgid[j] + l, h->out_off[nd], h->tt[j], (uint8_t)l,
+                                   (uint8_t)(pass == 0), (uint8_t)h->vmax[j],
+                                   (uint8_t)node_first});
       }
     in_chunk += nl;
   }
@@ -688,9 +692,8 @@ static StepParams step_params(ts_sim *h, int t, int mode) {
   P.vmax_link = h->d_vmax;
   P.tt_link = h->d_tt;
   P.out_pos = h->d_out_pos;
-  P.route_off = h->d_roff;
   P.rslot = h->d_rslot;
-  P.cursor = h->d_cursor;
+  P.vpos = h->d_vpos;
   P.dep = h->d_dep;
   P.entry = h->d_entry;
   P.inj_time = h->d_inj;
@@ -727,10 +730,9 @@ static NodeParams node_params(ts_sim *h, int t) {
   N.vmax_link = h->d_vmax;
   N.tt_link = h->d_tt;
   N.out_pos = h->d_out_pos;
-  N.route_off = h->d_roff;
   N.rslot = h->d_rslot;
   N.nodeout = h->d_nodeout;
-  N.cursor = h->d_cursor;
+  N.vpos = h->d_vpos;
   N.tail_rec = h->d_tail;
   N.head_occ = h->d_head;
   N.ext = h->d_ext;
@@ -747,6 +749,8 @@ static RowsParams rows_params(ts_sim *h) {
   r.vid_in = h->d_rvid[h->rcur];
   r.vid_out = h->d_rvid[h->rcur ^ 1];
   r.inj_scratch = h->d_inj_scratch;
+  r.gcnt_in = h->d_gcnt[h->rcur];
+  r.gcnt_out = h->d_gcnt[h->rcur ^ 1];
   r.ngroups = h->ngroups;
   r.cap = h->rows_cap;
   return r;
@@ -844,8 +848,10 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
   for (size_t ti = 0; ti < h->tiles.size(); ti++)
     if (h->tile_row[ti] >= 0)
       for (int l = 0; l < h->tiles[ti].L; l++) row_tile[h->tile_row[ti] + l] = (int32_t)ti;
+  std::vector<int32_t> gcnt(std::max(1, h->ngroups), 0);
   for (int g = 0; g < h->ngroups; g++) {
-    int64_t k = h->rows[(size_t)g * 32].voff;  // the group's block: rows in slot order
+    const int64_t k0 = h->rows[(size_t)g * 32].voff;
+    int64_t k = k0;  // the group's block: rows in slot order
     for (int sl = 0; sl < 32; sl++) {
       const int s = g * 32 + sl;
       if (row_tile[s] < 0) continue;
@@ -873,6 +879,7 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
         rvid[k++] = (int32_t)((uint32_t)vids[r++] | ((uint32_t)slot << kSlotShift));
       }
     }
+    gcnt[g] = (int32_t)(k - k0);
   }
   std::vector<uint8_t>().swap(code);
   std::vector<int32_t>().swap(vids);
@@ -922,6 +929,7 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
     if ((rc = dalloc(h, &h->d_strip[b], std::max(1, h->nstrips), 0xFF))) return rc;
     if ((rc = dalloc(h, &h->d_planes[b], std::max<size_t>(16, planes.size()), 0))) return rc;
     if ((rc = dalloc(h, &h->d_rvid[b], h->rvid_entries, 0xFF))) return rc;
+    if ((rc = dalloc(h, &h->d_gcnt[b], std::max(1, h->ngroups), 0))) return rc;
   }
   if (!h->gtiles.empty()) {
     CK(h, cudaMemcpyAsync(h->d_code[0], gcode.data(), gcode.size(), cudaMemcpyHostToDevice, h->stream));
@@ -932,6 +940,8 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
     CK(h, cudaMemcpyAsync(h->d_planes[0], planes.data(), planes.size() * 4, cudaMemcpyHostToDevice,
                           h->stream));
     CK(h, cudaMemcpyAsync(h->d_rvid[0], rvid.data(), rvid.size() * 4, cudaMemcpyHostToDevice,
+                          h->stream));
+    CK(h, cudaMemcpyAsync(h->d_gcnt[0], gcnt.data(), gcnt.size() * 4, cudaMemcpyHostToDevice,
                           h->stream));
   }
   {  // injection scratch of the row kernel: needed only if a row link has pending trips
@@ -947,7 +957,6 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
   if ((rc = upload(h, &h->d_vmax, vmax8))) return rc;
   if ((rc = upload(h, &h->d_tt, h->tt))) return rc;
   if ((rc = upload(h, &h->d_out_pos, h->out_pos))) return rc;
-  if ((rc = upload(h, &h->d_roff, h->roff))) return rc;
   {  // routes as out-slot sequences: rslot[j] = slot of R[j] at its from-node
     std::vector<uint8_t> rslot(h->route.size(), 0xFF);
     for (int f = 0; f < h->nv; f++)
@@ -961,7 +970,11 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
     }
     if ((rc = upload(h, &h->d_nodeout, nodeout))) return rc;
   }
-  if ((rc = upload(h, &h->d_cursor, cur0))) return rc;
+  {
+    std::vector<VehPos> vp(h->nv);
+    for (int f = 0; f < h->nv; f++) vp[f] = VehPos{h->roff[f] + cur0[f], h->roff[f + 1]};
+    if ((rc = upload(h, &h->d_vpos, vp))) return rc;
+  }
   if ((rc = upload(h, &h->d_dep, h->dep))) return rc;
   if ((rc = upload(h, &h->d_entry, h->entry))) return rc;
   if ((rc = upload(h, &h->d_inj, inj))) return rc;
@@ -1001,10 +1014,15 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
   // row kernel: one warp per 32-row group, 4 warps per block; each warp
   // stages its group's vid blocks (in + out) in shared memory
   h->rows_threads = 128;
-  h->rows_blocks = std::max(1, (h->ngroups + 3) / 4);
-  h->rows_cap = 1664;
-  h->rows_smem = 4 * 2 * h->rows_cap * 4;
+  // staging capacity per warp: 5 blocks of 4 warps per SM (96 registers)
+  // leave ~44 KB of shared memory per block; group_cells overrides (tuning)
+  h->rows_cap = h->cfg.group_cells > 0 ? (h->cfg.group_cells + 3) & ~3 : 1312;
+  h->rows_smem = 4 * rows_stage_words(h->rows_cap) * 4;
   CK(h, set_rows_smem(h->rows_smem));
+  {  // persistent grid: every resident warp loops over groups
+    const int rocc = std::max(1, occupancy_rows(h->rows_threads, h->rows_smem));
+    h->rows_blocks = std::max(1, std::min((h->ngroups + 3) / 4, rocc * nsm));
+  }
   {
     std::vector<NodeLane> nlanes;
     std::vector<int32_t> chunk_off;
@@ -1411,10 +1429,12 @@ int ts_read_vehicles(ts_sim *h, int8_t *status, int32_t *link, int32_t *lane, in
   CK(h, cudaStreamSynchronize(h->stream));
   std::vector<uint8_t> code;
   std::vector<int32_t> vids, inj(h->nv), arr(h->nv), cur(h->nv);
+  std::vector<VehPos> vp(h->nv);
   if (int rc = download_tiles(h, 0, (int)h->tiles.size(), code, vids)) return rc;
   CK(h, cudaMemcpy(inj.data(), h->d_inj, inj.size() * 4, cudaMemcpyDeviceToHost));
   CK(h, cudaMemcpy(arr.data(), h->d_arr, arr.size() * 4, cudaMemcpyDeviceToHost));
-  CK(h, cudaMemcpy(cur.data(), h->d_cursor, cur.size() * 4, cudaMemcpyDeviceToHost));
+  CK(h, cudaMemcpy(vp.data(), h->d_vpos, vp.size() * sizeof(VehPos), cudaMemcpyDeviceToHost));
+  for (int f = 0; f < h->nv; f++) cur[f] = (int32_t)(vp[f].p - h->roff[f]);
   std::vector<int32_t> lk(h->nv, -1), ln(h->nv, -1), ce(h->nv, -1), vv(h->nv, -1);
   std::vector<uint8_t> seen(h->nv, 0);
   for (const TileDesc &d : h->tiles) {

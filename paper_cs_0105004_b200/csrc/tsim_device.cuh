@@ -246,8 +246,8 @@ static __device__ __forceinline__ void inject_link(const StepParams &P, int k, i
     const int ec = P.entry[vid];
     if (ec < a || ec >= a + w) continue;
     if (!cell_free(ec - a)) continue;  // retry next step
-    const int64_t ro = P.route_off[vid];
-    const int slot0 = (P.route_off[vid + 1] - ro > 1) ? (int)P.rslot[ro + 1] : kSlotFinal;
+    const VehPos q = P.vpos[vid];
+    const int slot0 = (q.e - q.p > 1) ? (int)P.rslot[q.p + 1] : kSlotFinal;
     P.inj_time[vid] = tn;
     place_fn(ec - a, (uint8_t)(slot0 << 3), vid);
   }

@@ -50,7 +50,13 @@ struct Strip {
   uint8_t tail_code[8];
   int32_t head_vid[8];
   int32_t tail_vid[8];
-  int32_t tail_cur[8];
+  int64_t tail_pos[8];  // route position (VehPos::p) of the tail vehicles
+};
+
+// where a vehicle is on its route: p = absolute index of its current link
+// in the route arrays (route_off[vid] + cursor), e = route_off[vid + 1]
+struct VehPos {
+  int64_t p, e;
 };
 
 // smem workspace of one warp for a tile with L lanes and row stride S
@@ -108,17 +114,24 @@ struct RowDesc {
 };
 static_assert(sizeof(RowDesc) == 16, "RowDesc must be 16 bytes");
 
+// shared memory of one k_rows warp (4-byte words): the group's vid block in
+// and out (cap entries each; the out area first serves as the list of the
+// vehicles that draw), then the brake bits of the 32 rows (4 words each)
+__host__ __device__ inline int rows_stage_words(int cap) {
+  return 2 * cap + 32 * kRowWords;  // cap is a multiple of 4: 16-byte aligned
+}
+
 // Warp-cooperative node kernel: the incoming lanes of every node, in the
 // priority order (major class first, then link id, then lane; R9), packed
 // into chunks of <= 32 that never split a node.
-struct NodeLane {
+struct __align__(16) NodeLane {
   int32_t lane_gid;
-  int32_t node;
   int32_t out_base;  // first NodeOut entry of the node (its out-slots)
   uint32_t tt;       // turn types of the link's out-slots (2 bits each)
-  uint8_t lane, major, vk, pad;
+  uint8_t lane, major, vk;
+  uint8_t first;     // the node's first lane within its chunk (node key)
 };
-static_assert(sizeof(NodeLane) == 20, "NodeLane must be 20 bytes");
+static_assert(sizeof(NodeLane) == 16, "NodeLane must be 16 bytes");
 
 // an outgoing link of a node, by out-slot: what a winner needs to enter it
 struct NodeOut {
@@ -185,9 +198,8 @@ struct StepParams {
   const uint32_t *tt_link;  // 2 bits per out-slot: 0 T, 1 L, 2 R
   const int32_t *out_pos;   // slot of each link at its from-node
   // vehicles
-  const int64_t *route_off;
   const uint8_t *rslot;  // per route entry j >= 1: out-slot of link R[j] at its from-node
-  int32_t *cursor;
+  VehPos *vpos;
   const int32_t *dep;
   const int32_t *entry;
   int32_t *inj_time;
@@ -217,9 +229,8 @@ struct NodeParams {
   const uint8_t *vmax_link;
   const uint32_t *tt_link;
   const int32_t *out_pos;
-  const int64_t *route_off;
   const uint8_t *rslot;
-  int32_t *cursor;
+  VehPos *vpos;
   const NodeOut *nodeout;  // [out_off[node] + slot]
   const uint64_t *tail_rec;
   const uint8_t *head_occ;
@@ -242,6 +253,8 @@ struct RowsParams {
   const int32_t *vid_in;      // row vid lists
   int32_t *vid_out;
   int32_t *inj_scratch;       // [row slot * kRowMaxCells + cell]: entry of a vehicle injected there
+  const int32_t *gcnt_in;     // vehicles of each group (input state)
+  int32_t *gcnt_out;
   int32_t ngroups;
   int32_t cap;                // smem staging capacity (entries) of a group's vid block
 };

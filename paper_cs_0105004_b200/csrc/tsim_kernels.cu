@@ -223,7 +223,7 @@ __device__ void write_back(const StepParams &P, TileCtx &T, bool node_recs, int 
       s->tail_code[j] = ct;
       s->head_vid[j] = vh;
       s->tail_vid[j] = vt;
-      s->tail_cur[j] = vt >= 0 ? P.cursor[vt] : -1;
+      s->tail_pos[j] = vt >= 0 ? P.vpos[vt].p : -1;
     }
   }
   if (node_recs && !(T.d.flags & kPeriodic)) {
@@ -255,7 +255,7 @@ __device__ __forceinline__ void place(TileCtx &T, int pos, uint8_t code, int vid
 // move one vehicle at smem position q (owned, or a ghost in the upstream
 // halo) -- H4 + H5
 __device__ __forceinline__ void move_one(const StepParams &P, TileCtx &T, Acc &acc, int q,
-                                         int vid, bool ghost, int Vk, int ghost_cur = -1) {
+                                         int vid, bool ghost, int Vk, int64_t ghost_pos = -1) {
   const int l = lane_of(T, q);
   int x = T.d.a + (q - l * T.S - T.HP);
   const bool periodic = (T.d.flags & kPeriodic) != 0;
@@ -277,9 +277,9 @@ __device__ __forceinline__ void move_one(const StepParams &P, TileCtx &T, Acc &a
   if (yl >= 0 && yl < T.w) {
     place(T, l * T.S + T.HP + yl, (uint8_t)(v3 | (slot << 3)), vid);
     acc_place(acc, P.mode & kModeHash, vid, T.d.link, l, y, v3);
-    // a migrant from the upstream strip brings its route cursor (the
-    // cursor array of another domain is not visible here)
-    if (ghost) P.cursor[vid] = ghost_cur;
+    // a migrant from the upstream strip brings its route position (the
+    // vehicle state of another domain is not visible here)
+    if (ghost) P.vpos[vid].p = ghost_pos;
   } else if (!periodic && y > T.d.n - 1 && !ghost) {
     if (slot == kSlotFinal) {  // exit to parking
       P.arr_time[vid] = P.t + 1;
@@ -370,7 +370,7 @@ __global__ void __launch_bounds__(256) k_step(const StepParams P) {
           int q = l * T.S + T.HP - kGmax + j;
           if (occupied(T.bin, q)) {
             const Strip &hs = P.strip_in[P.halo_up[T.d.strip] + l];
-            move_one(P, T, acc, q, hs.tail_vid[j], true, Vk, hs.tail_cur[j]);
+            move_one(P, T, acc, q, hs.tail_vid[j], true, Vk, hs.tail_pos[j]);
           }
         }
       }
@@ -497,11 +497,10 @@ __device__ __forceinline__ int node_grant(const NodeParams &P, const Cand &c, in
   const int v3 = nasch_v3(c.v, vk, min(kGmax, c.d + E), (uint32_t)P.t, (uint32_t)c.vid, P.k0,
                           P.k1, P.p32);
   if (v3 > c.d) {
-    // independent loads first (the cursor store must not serialise them)
-    const int r = P.cursor[c.vid];
-    const int64_t ro = P.route_off[c.vid], re = P.route_off[c.vid + 1];
-    const int nslot = (ro + r + 2 < re) ? (int)P.rslot[ro + r + 2] : kSlotFinal;
-    P.cursor[c.vid] = r + 1;
+    // one 16-byte record per vehicle: its route position and end
+    const VehPos q = P.vpos[c.vid];
+    const int nslot = (q.p + 2 < q.e) ? (int)P.rslot[q.p + 2] : kSlotFinal;
+    P.vpos[c.vid].p = q.p + 1;
     const int y2 = v3 - c.d - 1;
     P.entr[c.tgt] = (uint64_t)(uint32_t)c.vid | ((uint64_t)(v3 | (nslot << 3)) << 32) |
                     ((uint64_t)y2 << 40) | ((uint64_t)((P.t + 1) & 0x1FFFFF) << 43);
@@ -536,13 +535,13 @@ __global__ void __launch_bounds__(256) k_node_warp(const NodeParams P, const Nod
        c += nwarps_total) {
     const int a = W.chunk_off[c], n = W.chunk_off[c + 1] - a;
     const bool act = lane < n;
-    NodeLane e{0, -1 - lane, 0, 0u, 0, 0, 1, 0};
+    NodeLane e{0, 0, 0u, 0, 0, 1, (uint8_t)(64 + lane)};
     uint64_t rec = 0;
     if (act) {
       e = W.lanes[a + lane];
       rec = P.tail_rec[e.lane_gid];
     }
-    const uint32_t nodemask = __match_any_sync(FULL, e.node);
+    const uint32_t nodemask = __match_any_sync(FULL, (int)e.first);
     const bool busy = (__ballot_sync(FULL, act && e.major && (((uint32_t)(rec >> 44)) & gmask)) &
                        nodemask) != 0u;
     Cand cd{false, -1, 0, 0, 0, 0};

@@ -124,11 +124,11 @@ __device__ __forceinline__ void warp_store(int32_t *gdst, const int32_t *src, in
 }
 }  // namespace
 
-__global__ void __launch_bounds__(128) k_rows(const StepParams P, const RowsParams R) {
+__global__ void __launch_bounds__(128, 5) k_rows(const StepParams P, const RowsParams R) {
   __shared__ unsigned long long red[4 * 8];
   extern __shared__ __align__(16) int32_t stage[];  // per warp: vid block in, vid block out
   const int lane = threadIdx.x & 31;
-  int32_t *s_in = stage + (threadIdx.x >> 5) * 2 * R.cap;
+  int32_t *s_in = stage + (threadIdx.x >> 5) * rows_stage_words(R.cap);
   int32_t *s_out = s_in + R.cap;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   const bool do_move = (P.mode & kModeMove) != 0;
@@ -143,6 +143,18 @@ __global__ void __launch_bounds__(128) k_rows(const StepParams P, const RowsPara
     __syncwarp();  // the previous group's staged blocks are no longer in use
     const RowDesc rd = R.rows[(size_t)g * 32 + lane];
     const int w = rd.w, l = rd.l, L = rd.L, link = rd.link, lg = rd.lg, vk = rd.vk;
+    // the group's vid block (its vehicle count was written with it) is
+    // staged in shared memory when it fits, loaded together with the planes
+    const int tot_in = R.gcnt_in[g];
+    const bool staged = tot_in <= R.cap;
+    if (staged) warp_load(s_in, R.vid_in + rd.voff, tot_in, lane);
+    // per-row gathers of this step, issued early: node grant, entrant,
+    // pending trips
+    const bool do_move0 = (P.mode & kModeMove) != 0 && w > 0;
+    const int ext_lg = do_move0 ? (int)P.ext[lg] : 0;
+    const uint64_t ent_rec = do_move0 ? P.entr[lg] : 0ull;
+    const bool may_inject = (P.mode & kModeInject) && w > 0 && l == 0 &&
+                            P.pend_off[link + 1] > P.pend_head[link];
     const uint32_t *pin = R.planes_in + group_plane_base(g) + lane;
     uint32_t O[NW], V0[NW], V1[NW], V2[NW], A0[NW], A1[NW];
 #pragma unroll
@@ -158,14 +170,9 @@ __global__ void __launch_bounds__(128) k_rows(const StepParams P, const RowsPara
 #pragma unroll
     for (int i = 0; i < NW; i++) VAL[i] = lowm(w - 32 * i);
     const int nin = popc_row(O);
-    // the group's vid block: staged in shared memory when it fits
-    int tot_in;
-    const int in_off = warp_scan(nin, lane, &tot_in);
-    const bool staged = tot_in <= R.cap;
-    if (staged) {
-      warp_load(s_in, R.vid_in + rd.voff, tot_in, lane);
-      __syncwarp();
-    }
+    int tot_chk;
+    const int in_off = warp_scan(nin, lane, &tot_chk);
+    if (staged) __syncwarp();
     const int32_t *vin = (staged ? (const int32_t *)s_in : R.vid_in + rd.voff) + in_off;
     acc.work += nin;
     if ((P.mode & kModeWork) && P.link_work && nin)
@@ -183,109 +190,146 @@ __global__ void __launch_bounds__(128) k_rows(const StepParams P, const RowsPara
       const int nb = min(w, kGmax);
       const bool front_zone = xf >= w - nb && xf >= 0;
       if (front_zone) efront = (uint32_t)vin[nin - 1];
-      // ---- thermometer codes U_k (v2 >= k), cells past the row end occupied
-      uint32_t Oext[NW], F[NW], S[NW];
+      // ---- thermometer codes U_k = (v2 >= k), word by word; cells past the
+      //      row end count as occupied.  The row front near the stop line
+      //      takes its gap from the node grant (H3) or the open end of its
+      //      final link (R12): fv2 = its v2 when that lets it go past d.
+      uint32_t Oext[NW];
 #pragma unroll
       for (int i = 0; i < NW; i++) Oext[i] = O[i] | ~VAL[i];
-      uint32_t U[6][NW];
+      int fd = 99, fv2 = 0;
+      if (front_zone) {
+        const int d = w - 1 - xf;
+        const int slot = (int)(efront >> kSlotShift);
+        const int gp = slot == kSlotFinal ? kGmax : min(kGmax, d + ext_lg);
+        if (gp > d) {
+          const int v = bit_row(V0, xf) | (bit_row(V1, xf) << 1) | (bit_row(V2, xf) << 2);
+          fd = d;
+          fv2 = min(min(v + 1, vk), gp);
+        }
+      }
+      // U_k of word i (k = 1..5)
+      auto thermo = [&](int i, uint32_t (&u)[5]) {
+        const uint32_t o0 = Oext[i], o1 = i + 1 < NW ? Oext[i + 1] : FULL;
+        uint32_t f = FULL;
 #pragma unroll
-      for (int k = 1; k <= 5; k++) {
-        shr(S, Oext, k, FULL);
-#pragma unroll
-        for (int i = 0; i < NW; i++) {
-          F[i] = (k == 1 ? ~S[i] : F[i] & ~S[i]);
+        for (int k = 1; k <= 5; k++) {
+          f &= ~__funnelshift_r(o0, o1, k);
           uint32_t T;
           if (k == 1) T = O[i];
           else if (k == 2) T = vk >= 2 ? (V0[i] | V1[i] | V2[i]) : 0u;  // v >= 1
           else if (k == 3) T = vk >= 3 ? (V1[i] | V2[i]) : 0u;          // v >= 2
           else if (k == 4) T = vk >= 4 ? (V2[i] | (V1[i] & V0[i])) : 0u;  // v >= 3
           else T = vk >= 5 ? V2[i] : 0u;                                  // v >= 4
-          U[k - 1][i] = T & F[i];
+          u[k - 1] = T & f;
+          if (k > fd && k <= fv2) u[k - 1] |= onehot(i, xf);
         }
-      }
-#pragma unroll
-      for (int i = 0; i < NW; i++) U[5][i] = 0u;
-      // ---- the row front near the stop line: open end of the final link
-      //      (R12) or entry space granted by the node (H3)
-      if (front_zone) {
-        const int d = w - 1 - xf;
-        const int slot = (int)(efront >> kSlotShift);
-        const int gp = slot == kSlotFinal ? kGmax : min(kGmax, d + (int)P.ext[lg]);
-        if (gp > d) {
-          const int v = bit_row(V0, xf) | (bit_row(V1, xf) << 1) | (bit_row(V2, xf) << 2);
-          const int v2 = min(min(v + 1, vk), gp);
-#pragma unroll
-          for (int k = 1; k <= 5; k++)
-            if (k > d && k <= v2) set_row(U[k - 1], xf);
-        }
-      }
-      // ---- Philox slowdown draws (R3) of the vehicles with v2 >= 1
-      uint32_t Bm[NW];
-      {
-        int rb = 0;
-#pragma unroll
-        for (int i = 0; i < NW; i++) {
-          uint32_t m = U[0][i], b = 0u;
-          while (m) {
-            const int x = __ffs(m) - 1;
-            m &= m - 1u;
-            const uint32_t e = (uint32_t)vin[rb + __popc(O[i] & lowm(x))];
-            if ((uint64_t)philox_w0((uint32_t)P.t, e & kVidMask, P.k0, P.k1) < P.p32)
-              b |= 1u << x;
-          }
-          Bm[i] = b;
-          rb += __popc(O[i]);
-        }
-      }
-      // ---- hop: D_k vehicles move exactly k; those passing the row end leave
-      uint32_t D[6][NW], Wn[NW], Wc[NW], LR = 0u;
-#pragma unroll
-      for (int i = 0; i < NW; i++) Wc[i] = (U[0][i] & ~Bm[i]) | (U[1][i] & Bm[i]);  // v3 >= 1
-#pragma unroll
-      for (int i = 0; i < NW; i++) D[0][i] = O[i] & ~Wc[i];
-#pragma unroll
-      for (int k = 1; k <= 5; k++) {
-#pragma unroll
-        for (int i = 0; i < NW; i++) Wn[i] = k < 5 ? ((U[k][i] & ~Bm[i]) | (U[k + 1][i] & Bm[i])) : 0u;
-        shr(S, VAL, k, 0u);  // cells with x + k inside the row
-#pragma unroll
-        for (int i = 0; i < NW; i++) {
-          const uint32_t dk = Wc[i] & ~Wn[i];
-          LR |= dk & ~S[i];
-          D[k][i] = dk & S[i];
-          Wc[i] = Wn[i];
-        }
-      }
+      };
+      uint32_t U1[NW];  // movers: v2 >= 1
 #pragma unroll
       for (int i = 0; i < NW; i++) {
-        OO[i] = D[0][i];
-        OV0[i] = 0u;
-        OV1[i] = 0u;
-        OV2[i] = 0u;
-        OA0[i] = D[0][i] & A0[i];
-        OA1[i] = D[0][i] & A1[i];
+        const uint32_t o1 = i + 1 < NW ? Oext[i + 1] : FULL;
+        U1[i] = O[i] & ~__funnelshift_r(Oext[i], o1, 1);
+        if (fd == 0 && fv2 >= 1) U1[i] |= onehot(i, xf);
       }
-      uint32_t Dk[NW], Sh[NW];
+      // ---- Philox slowdown draws (R3) of the vehicles with v2 >= 1, 32 at a
+      //      time across the warp: each row lists the block offsets of its
+      //      movers, the warp draws for the whole list (full lanes), each row
+      //      takes its brake bits back in order
+      uint32_t Bm[NW];
+      {
+        int mtot;
+        const int mc = popc_row(U1);
+        const int moff = warp_scan(mc, lane, &mtot);
+        const int32_t *vbase = staged ? (const int32_t *)s_in : R.vid_in + rd.voff;
+        if (mtot <= R.cap) {
+          // mover list entries: block offset << 12 | row slot << 7 | cell
+          int32_t *mlist = s_out;  // free until the output phase
+          uint32_t *bw = reinterpret_cast<uint32_t *>(s_out + R.cap) + lane * NW;
 #pragma unroll
-      for (int k = 1; k <= 5; k++) {
-        shl(Sh, D[k], k);
+          for (int i = 0; i < NW; i++) bw[i] = 0u;  // this row's brake bits
+          int j = moff, rb = in_off;
 #pragma unroll
-        for (int i = 0; i < NW; i++) {
-          OO[i] |= Sh[i];
-          if (k & 1) OV0[i] |= Sh[i];
-          if (k & 2) OV1[i] |= Sh[i];
-          if (k & 4) OV2[i] |= Sh[i];
+          for (int i = 0; i < NW; i++) {
+            uint32_t m = U1[i];
+            while (m) {
+              const int x = __ffs(m) - 1;
+              m &= m - 1u;
+              mlist[j++] = ((rb + __popc(O[i] & lowm(x))) << 12) | (lane << 7) | (32 * i + x);
+            }
+            rb += __popc(O[i]);
+          }
+          __syncwarp();
+          uint32_t *bw0 = reinterpret_cast<uint32_t *>(s_out + R.cap);
+          for (int jj = lane; jj < mtot; jj += 32) {
+            const int me = mlist[jj];
+            const uint32_t e = (uint32_t)vbase[me >> 12];
+            if ((uint64_t)philox_w0((uint32_t)P.t, e & kVidMask, P.k0, P.k1) < P.p32)
+              atomicOr(bw0 + ((me >> 7) & 31) * NW + ((me >> 5) & 3), 1u << (me & 31));
+          }
+          __syncwarp();
+#pragma unroll
+          for (int i = 0; i < NW; i++) Bm[i] = bw[i];
+          __syncwarp();
+        } else {  // more movers than staging room: each row draws its own
+          int rb = 0;
+#pragma unroll
+          for (int i = 0; i < NW; i++) {
+            uint32_t m = U1[i], b = 0u;
+            while (m) {
+              const int x = __ffs(m) - 1;
+              m &= m - 1u;
+              const uint32_t e = (uint32_t)vin[rb + __popc(O[i] & lowm(x))];
+              if ((uint64_t)philox_w0((uint32_t)P.t, e & kVidMask, P.k0, P.k1) < P.p32)
+                b |= 1u << x;
+            }
+            Bm[i] = b;
+            rb += __popc(O[i]);
+          }
         }
+      }
+      // ---- hop, word by word: D_k = vehicles moving exactly k (v3 = k);
+      //      those passing the row end leave it (LR); O' = OR_k D_k << k with
+      //      the velocity and class bits carried along
+      uint32_t LR = 0u, Dp[6], DpA0[6], DpA1[6];
 #pragma unroll
-        for (int i = 0; i < NW; i++) Dk[i] = D[k][i] & A0[i];
-        shl(Sh, Dk, k);
+      for (int k = 0; k < 6; k++) Dp[k] = DpA0[k] = DpA1[k] = 0u;
 #pragma unroll
-        for (int i = 0; i < NW; i++) OA0[i] |= Sh[i];
+      for (int i = 0; i < NW; i++) {
+        uint32_t u[5];
+        thermo(i, u);
+        const uint32_t b = Bm[i];
+        uint32_t W[6];
 #pragma unroll
-        for (int i = 0; i < NW; i++) Dk[i] = D[k][i] & A1[i];
-        shl(Sh, Dk, k);
+        for (int k = 1; k <= 5; k++)
+          W[k - 1] = (u[k - 1] & ~b) | ((k < 5 ? u[k] : 0u) & b);  // v3 >= k
+        W[5] = 0u;
+        const uint32_t D0 = O[i] & ~W[0];
+        uint32_t oo = D0, ov0 = 0u, ov1 = 0u, ov2 = 0u, oa0 = D0 & A0[i], oa1 = D0 & A1[i];
+        const uint32_t val1 = i + 1 < NW ? VAL[i + 1] : 0u;
 #pragma unroll
-        for (int i = 0; i < NW; i++) OA1[i] |= Sh[i];
+        for (int k = 1; k <= 5; k++) {
+          const uint32_t stay = __funnelshift_r(VAL[i], val1, k);  // x + k inside the row
+          const uint32_t dk0 = W[k - 1] & ~W[k];
+          LR |= dk0 & ~stay;
+          const uint32_t dk = dk0 & stay, da0 = dk & A0[i], da1 = dk & A1[i];
+          const uint32_t sh = __funnelshift_l(Dp[k], dk, k);
+          oo |= sh;
+          if (k & 1) ov0 |= sh;
+          if (k & 2) ov1 |= sh;
+          if (k & 4) ov2 |= sh;
+          oa0 |= __funnelshift_l(DpA0[k], da0, k);
+          oa1 |= __funnelshift_l(DpA1[k], da1, k);
+          Dp[k] = dk;
+          DpA0[k] = da0;
+          DpA1[k] = da1;
+        }
+        OO[i] = oo;
+        OV0[i] = ov0;
+        OV1[i] = ov1;
+        OV2[i] = ov2;
+        OA0[i] = oa0;
+        OA1[i] = oa1;
       }
       // ---- the front left the row: exit to parking or
       //      node crossing (the node kernel placed it on the next link)
@@ -297,7 +341,7 @@ __global__ void __launch_bounds__(128) k_rows(const StepParams P, const RowsPara
       }
       // ---- entrant granted by the node kernel (H3/H5), behind every vehicle
       if (w > 0) {
-        const uint64_t rec = P.entr[lg];
+        const uint64_t rec = ent_rec;
         if ((uint32_t)(rec >> 43) == ((uint32_t)(P.t + 1) & 0x1FFFFFu)) {
           const int code = (int)((rec >> 32) & 0xFF);
           ent_y = (int)((rec >> 40) & 7);
@@ -328,7 +372,7 @@ __global__ void __launch_bounds__(128) k_rows(const StepParams P, const RowsPara
 #pragma unroll
     for (int i = 0; i < NW; i++) INJ[i] = 0u;
     bool injected = false;
-    if ((P.mode & kModeInject) && w > 0 && l == 0 && P.pend_off[link + 1] > P.pend_head[link]) {
+    if (may_inject) {
       int32_t *scratch = R.inj_scratch + ((size_t)g * 32 + lane) * kRowMaxCells;
       inject_link(
           P, link, 0, w, true, [&](int x) { return !bit_row(OO, x); },
@@ -368,62 +412,46 @@ __global__ void __launch_bounds__(128) k_rows(const StepParams P, const RowsPara
         anyc |= cand[i] != 0u;
       }
       if (anyc) {
-        uint32_t OOx[NW], T0x[NW], S[NW];
-#pragma unroll
-        for (int i = 0; i < NW; i++) {
-          OOx[i] = OO[i] | ~VAL[i];
-          T0x[i] = T0[i] | ~VAL[i];
-        }
-        // gaps ahead in the own and target lanes (stop at the row end, R2);
-        // gap behind in the target lane (before the row start = empty)
-        uint32_t G[6][NW], TG[6][NW], BK[NW], BKv[NW];
-#pragma unroll
-        for (int i = 0; i < NW; i++) {
-          G[0][i] = FULL;
-          TG[0][i] = FULL;
-          BK[i] = FULL;
-          BKv[i] = FULL;
-        }
-#pragma unroll
-        for (int k = 1; k <= 5; k++) {
-          shr(S, OOx, k, FULL);
-#pragma unroll
-          for (int i = 0; i < NW; i++) G[k][i] = G[k - 1][i] & ~S[i];
-          shr(S, T0x, k, FULL);
-#pragma unroll
-          for (int i = 0; i < NW; i++) TG[k][i] = TG[k - 1][i] & ~S[i];
-          shl(S, T0, k);
-#pragma unroll
-          for (int i = 0; i < NW; i++) {
-            BK[i] &= ~S[i];
-            if (k == vk) BKv[i] = BK[i];
-          }
-        }
         const int zs = P.D >= w ? 0 : w - P.D;  // desperation zone: last D cells (R6)
 #pragma unroll
         for (int i = 0; i < NW; i++) {
+          // word i: gaps ahead in the own and target lanes (stop at the row
+          // end, R2); gap behind in the target lane (before the row start =
+          // empty).  G_k / TG_k / BK_k = gap >= k.
+          const uint32_t o0 = OO[i] | ~VAL[i], o1 = i + 1 < NW ? (OO[i + 1] | ~VAL[i + 1]) : FULL;
+          const uint32_t t0 = T0[i] | ~VAL[i], t1 = i + 1 < NW ? (T0[i + 1] | ~VAL[i + 1]) : FULL;
+          const uint32_t tp = i > 0 ? T0[i - 1] : 0u;
+          uint32_t G[6], TG[6], BK = FULL, BKv = FULL;
+          G[0] = TG[0] = FULL;
+#pragma unroll
+          for (int k = 1; k <= 5; k++) {
+            G[k] = G[k - 1] & ~__funnelshift_r(o0, o1, k);
+            TG[k] = TG[k - 1] & ~__funnelshift_r(t0, t1, k);
+            BK &= ~__funnelshift_l(tp, T0[i], k);
+            if (k == vk) BKv = BK;
+          }
           // E_k = (v + 1 >= k)
           const uint32_t E2 = OV0[i] | OV1[i] | OV2[i], E3 = OV1[i] | OV2[i],
                          E4 = OV2[i] | (OV1[i] & OV0[i]), E5 = OV2[i], E6 = OV2[i] & OV0[i];
           // speed-motivated (R5): own gap < v+1, target gap ahead > own gap,
           // target gap behind >= V; only for vehicles free to use any lane
-          const uint32_t geq = G[1][i] & (~E2 | G[2][i]) & (~E3 | G[3][i]) & (~E4 | G[4][i]) &
-                               (~E5 | G[5][i]) & ~E6;
-          const uint32_t tgt = TG[1][i] & (~G[1][i] | TG[2][i]) & (~G[2][i] | TG[3][i]) &
-                               (~G[3][i] | TG[4][i]) & (~G[4][i] | TG[5][i]) & ~G[5][i];
-          uint32_t lv = cand[i] & ~OA0[i] & ~OA1[i] & ~geq & tgt & BKv[i];
+          const uint32_t geq =
+              G[1] & (~E2 | G[2]) & (~E3 | G[3]) & (~E4 | G[4]) & (~E5 | G[5]) & ~E6;
+          const uint32_t tgt = TG[1] & (~G[1] | TG[2]) & (~G[2] | TG[3]) & (~G[3] | TG[4]) &
+                               (~G[4] | TG[5]) & ~G[5];
+          uint32_t lv = cand[i] & ~OA0[i] & ~OA1[i] & ~geq & tgt & BKv;
           // turn-motivated (R6, R7): towards the allowed lane
           const uint32_t turn =
               cand[i] & (dir < 0 ? (OA0[i] & ~OA1[i]) : (OA1[i] & ~OA0[i]));
           if (turn) {
             const uint32_t ZN = range_w(i, zs, w);
             // ahead >= min(v+1, V), behind >= V outside the last D cells
-            uint32_t req = TG[1][i];
-            if (vk >= 2) req &= ~E2 | TG[2][i];
-            if (vk >= 3) req &= ~E3 | TG[3][i];
-            if (vk >= 4) req &= ~E4 | TG[4][i];
-            if (vk >= 5) req &= ~E5 | TG[5][i];
-            lv |= turn & ~ZN & req & BKv[i];
+            uint32_t req = TG[1];
+            if (vk >= 2) req &= ~E2 | TG[2];
+            if (vk >= 3) req &= ~E3 | TG[3];
+            if (vk >= 4) req &= ~E4 | TG[4];
+            if (vk >= 5) req &= ~E5 | TG[5];
+            lv |= turn & ~ZN & req & BKv;
             uint32_t zc = turn & ZN;  // scaled thresholds (R6): per candidate
             while (zc) {
               const int x = __ffs(zc) - 1;
@@ -436,7 +464,7 @@ __global__ void __launch_bounds__(128) k_rows(const StepParams P, const RowsPara
               bool ok = true;
 #pragma unroll
               for (int k = 1; k <= 5; k++) {
-                if (k <= rf && !((TG[k][i] >> x) & 1u)) ok = false;
+                if (k <= rf && !((TG[k] >> x) & 1u)) ok = false;
               }
               if (rb > 0) {
                 // behind >= rb: target cells x-1..x-rb empty (before 0 = empty)
@@ -459,41 +487,31 @@ __global__ void __launch_bounds__(128) k_rows(const StepParams P, const RowsPara
       }
       acc_next.lc += popc_row(LV);
     }
-    // ---- apply the lane changes; final planes
-    uint32_t FO[NW], FV0[NW], FV1[NW], FV2[NW], FA0[NW], FA1[NW];
-    {
-      uint32_t s0[NW], s1[NW], s2[NW], s3[NW], s4[NW];
-      if (lc) {
-#pragma unroll
-        for (int i = 0; i < NW; i++) {
-          s0[i] = shfl_w(OV0[i], lane - dir);
-          s1[i] = shfl_w(OV1[i], lane - dir);
-          s2[i] = shfl_w(OV2[i], lane - dir);
-          s3[i] = shfl_w(OA0[i], lane - dir);
-          s4[i] = shfl_w(OA1[i], lane - dir);
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < NW; i++) {
-        const uint32_t keep = ~LV[i];
-        FO[i] = (OO[i] & keep) | AR[i];
-        FV0[i] = (OV0[i] & keep) | (lc ? (s0[i] & AR[i]) : 0u);
-        FV1[i] = (OV1[i] & keep) | (lc ? (s1[i] & AR[i]) : 0u);
-        FV2[i] = (OV2[i] & keep) | (lc ? (s2[i] & AR[i]) : 0u);
-        FA0[i] = (OA0[i] & keep) | (lc ? (s3[i] & AR[i]) : 0u);
-        FA1[i] = (OA1[i] & keep) | (lc ? (s4[i] & AR[i]) : 0u);
-      }
-    }
+    // ---- apply the lane changes word by word; final planes to HBM
+    uint32_t FO[NW], FV0[NW], FV1[NW], FV2[NW];
     {
       uint32_t *pout = R.planes_out + group_plane_base(g) + lane;
 #pragma unroll
       for (int i = 0; i < NW; i++) {
+        const uint32_t keep = ~LV[i], ar = AR[i];
+        uint32_t fa0 = OA0[i], fa1 = OA1[i];
+        FO[i] = (OO[i] & keep) | ar;
+        FV0[i] = OV0[i];
+        FV1[i] = OV1[i];
+        FV2[i] = OV2[i];
+        if (lc) {  // arrivals carry their velocity and class bits from lane l - dir
+          FV0[i] = (FV0[i] & keep) | (shfl_w(OV0[i], lane - dir) & ar);
+          FV1[i] = (FV1[i] & keep) | (shfl_w(OV1[i], lane - dir) & ar);
+          FV2[i] = (FV2[i] & keep) | (shfl_w(OV2[i], lane - dir) & ar);
+          fa0 = (fa0 & keep) | (shfl_w(OA0[i], lane - dir) & ar);
+          fa1 = (fa1 & keep) | (shfl_w(OA1[i], lane - dir) & ar);
+        }
         __stcs(pout + (0 * NW + i) * 32, FO[i]);
         __stcs(pout + (1 * NW + i) * 32, FV0[i]);
         __stcs(pout + (2 * NW + i) * 32, FV1[i]);
         __stcs(pout + (3 * NW + i) * 32, FV2[i]);
-        __stcs(pout + (4 * NW + i) * 32, FA0[i]);
-        __stcs(pout + (5 * NW + i) * 32, FA1[i]);
+        __stcs(pout + (4 * NW + i) * 32, fa0);
+        __stcs(pout + (5 * NW + i) * 32, fa1);
       }
     }
 
@@ -508,14 +526,20 @@ __global__ void __launch_bounds__(128) k_rows(const StepParams P, const RowsPara
     const bool moved_lc = any_row(LV) || any_row(AR);
     const bool general = moved_lc || injected || hash;
     if (!general && nfin > 0) {
-      if (!has_ent) {
-        // input vehicles minus an exit at the front: a prefix of the input list
-        for (int i = 0; i < nfin; i++) vout[i] = vin[i];
-      } else {
-        // the entrant lands behind every vehicle: the list shifts by one
-        vout[0] = (int32_t)ent_e;
-        for (int i = 1; i < nfin; i++) vout[i] = vin[i - 1];
+      // input vehicles minus an exit at the front (a prefix of the input
+      // list), shifted by one when the entrant lands behind every vehicle
+      const int sh = has_ent ? 1 : 0;
+      if (has_ent) vout[0] = (int32_t)ent_e;
+      int i = sh;
+      for (; i + 4 <= nfin; i += 4) {
+        const int32_t a0 = vin[i - sh], a1 = vin[i + 1 - sh], a2 = vin[i + 2 - sh],
+                      a3 = vin[i + 3 - sh];
+        vout[i] = a0;
+        vout[i + 1] = a1;
+        vout[i + 2] = a2;
+        vout[i + 3] = a3;
       }
+      for (; i < nfin; i++) vout[i] = vin[i - sh];
     }
     if (__any_sync(FULL, general)) {
       // every vehicle of S(t+1) before the lane change, in cell order, goes
@@ -556,6 +580,7 @@ __global__ void __launch_bounds__(128) k_rows(const StepParams P, const RowsPara
     __syncwarp();
     const uint32_t efin = nfin > 0 ? (uint32_t)vout[nfin - 1] : 0u;  // final front vehicle
     if (ostaged) warp_store(R.vid_out + rd.voff, s_out, tot_out, lane);
+    if (lane == 0) R.gcnt_out[g] = tot_out;
     // ---- node records of the output S1 (read by k_node_warp, H3)
     if (lc && w > 0) {
       const int nb = min(w, kGmax);
