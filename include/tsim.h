@@ -123,6 +123,17 @@ int ts_domain_plan(int32_t n_nodes, int32_t n_links, const int32_t *from, const 
                    int64_t *nbr_strips, int32_t *n_out);
 int32_t ts_strip_bytes(void);
 
+/* Fixed-time two-phase signals (reading R23) at the given
+ * nodes: phase 0 = the incoming links of the node's maximal priority class,
+ * green for the first green0 seconds of every (green0 + green1)-second
+ * cycle shifted by offset (tau = (t + offset) mod cycle < green0); phase 1
+ * green for the rest.  A red approach has the paper's virtual vehicle of
+ * maximum velocity zero beyond its last cell (no crossing); green
+ * approaches need no gap acceptance.  green0 + green1 in [1, 1023],
+ * offset >= 0.  Before ts_init.  TS_EINVAL: bad node or plan. */
+int ts_set_signals(ts_sim *h, int32_t n, const int32_t *node, const int32_t *green0,
+                   const int32_t *green1, const int32_t *offset);
+
 /* Build the device layout, upload, and run the initial injection of
  * vehicles with departure <= t0 (clock starts at t0).  In domain mode with
  * partners the boundary strips of S(t0) are packed at the end: exchange
@@ -203,6 +214,12 @@ int ts_read_history(ts_sim *h, int32_t t_from, int32_t n, uint64_t *hash,
                     int64_t *active, int64_t *arrivals, int64_t *injections,
                     int64_t *lane_changes, int64_t *crossings);
 
+/* Sum of the velocities of S(t) (cells moved in the step that produced
+ * it) for t in [t_from, t_from + n): the flow q(t) = sumv(t) / lane-cells
+ * of the fundamental diagram.  Same range rules as
+ * ts_read_history. */
+int ts_read_flow(ts_sim *h, int32_t t_from, int32_t n, int64_t *sumv);
+
 /* Totals: [0] active [1] pending [2] arrived [3] vehicle-updates since
  * init [4] lane-cells [5] tiles [6] device bytes allocated
  * [7] algorithmic bytes per step at the current state. */
@@ -220,6 +237,18 @@ int ts_get_link_work(ts_sim *h, int64_t *link_work);
 int ts_orb_partition(int32_t n_nodes, const int64_t *node_x_mm,
                      const int64_t *node_y_mm, const double *node_weight,
                      int32_t k, int32_t *domain_of_node);
+
+/* Multilevel k-way partition of the node graph (the
+ * METIS-style alternative to ORB): heavy-edge matching
+ * coarsening (seeded), ORB of the coarsest graph, greedy boundary
+ * refinement at every level keeping each domain's load <= (1 + imbalance)
+ * x average.  Vertex weight = node_weight (NULL = 1), edge weight = lanes
+ * of the links joining two nodes (the strips a cut there costs per
+ * exchange).  Pure host function; deterministic for a seed. */
+int ts_multilevel_partition(int32_t n_nodes, const int64_t *node_x_mm, const int64_t *node_y_mm,
+                            int32_t n_links, const int32_t *from, const int32_t *to,
+                            const int32_t *lanes, const double *node_weight, int32_t k,
+                            double imbalance, uint64_t seed, int32_t *domain_of_node);
 
 /* Kernel-level timing of the last ts_step call (CUDA events on the
  * handle's stream): total ms, and ms inside the dominant (move) kernel. */

@@ -68,6 +68,7 @@ def _load():
     lib.or_set_partition.argtypes = [P, I32, P]
     lib.or_domain_stats.argtypes = [P, P, I32]
     lib.or_set_brake_override.argtypes = [P, P]
+    lib.or_set_signals.argtypes = [P, I32, P, P, P, P]
     _lib = lib
     return lib
 
@@ -138,6 +139,10 @@ class Oracle:
             pl = [i32(scn.place_vid), i32(scn.place_lane), i32(scn.place_cell),
                   i32(scn.place_v)]
             self._check(self.lib.or_place_vehicles(self.h, pl[0].size, *(a.ctypes.data for a in pl)))
+        sig = getattr(scn, "sig_node", None)
+        if sig is not None and len(sig):
+            a = [i32(scn.sig_node), i32(scn.sig_g0), i32(scn.sig_g1), i32(scn.sig_off)]
+            self._check(self.lib.or_set_signals(self.h, a[0].size, *(x.ctypes.data for x in a)))
 
     def init(self, t0=0):
         self._check(self.lib.or_init(self.h, int(t0)))

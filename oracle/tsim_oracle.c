@@ -60,6 +60,7 @@ struct orc {
   int64_t *lbase; /* global lane id of (k, 0) */
   int64_t ncells, nlanes;
   int32_t *in_off, *in_list; /* incoming links per node, ascending id */
+  int32_t *sig_g0, *sig_g1, *sig_off; /* fixed-time signal per node (g0 = 0: none) */
   /* vehicles */
   int32_t nv;
   int64_t *roff;
@@ -229,6 +230,9 @@ void or_destroy(orc *o) {
   free(o->lbase);
   free(o->in_off);
   free(o->in_list);
+  free(o->sig_g0);
+  free(o->sig_g1);
+  free(o->sig_off);
   free(o->roff);
   free(o->route);
   free(o->dep);
@@ -638,9 +642,23 @@ static int cand_less(const cand_t *a, const cand_t *b) {
 
 /* O1 §Node for one node (readings R8-R10): sets o->ext
  * for the lanes of every incoming link of the node. */
-static void node_resolve(orc *o, const view *V, const int32_t *S, int32_t node) {
+/* Signalized node (reading R23): a fixed-time two-phase
+ * plan; phase 0 = the incoming links of the node's maximal priority class,
+ * phase 1 = the others.  With cycle c = g0 + g1 and tau = (t + offset) mod
+ * c, phase 0 is green for tau < g0, phase 1 for tau >= g0.  A red approach
+ * has the paper's "virtual vehicle of maximum velocity zero at the end of
+ * the lane": its front vehicle gets no entry space (ext = 0); green
+ * approaches need no gap acceptance. */
+static int signal_green(const orc *o, int32_t node, int phase, int32_t t) {
+  const int32_t g0 = o->sig_g0[node], c = g0 + o->sig_g1[node];
+  const int32_t tau = (int32_t)((((int64_t)t + o->sig_off[node]) % c + c) % c);
+  return phase == 0 ? tau < g0 : tau >= g0;
+}
+
+static void node_resolve(orc *o, const view *V, const int32_t *S, int32_t node, int32_t t) {
   int32_t a = o->in_off[node], b = o->in_off[node + 1];
   if (a == b) return;
+  const int signalized = o->sig_g0 && o->sig_g0[node] + o->sig_g1[node] > 0;
   int32_t maxcls = o->cls[o->in_list[a]];
   for (int32_t i = a; i < b; i++) maxcls = imax(maxcls, o->cls[o->in_list[i]]);
   int32_t ncand = 0, cap = 0;
@@ -662,6 +680,8 @@ static void node_resolve(orc *o, const view *V, const int32_t *S, int32_t node) 
       if (is_final(o, V, f)) continue;
       int32_t d = n - 1 - x;
       if (!(d < imin(V->vel[f] + 1, o->vmax[k]))) continue;
+      /* red: the virtual blocker beyond the last cell */
+      if (signalized && !signal_green(o, node, o->cls[k] == maxcls ? 0 : 1, t)) continue;
       cand_t c;
       c.rank = o->cls[k] == maxcls ? 0 : 1;
       c.k = k;
@@ -675,7 +695,7 @@ static void node_resolve(orc *o, const view *V, const int32_t *S, int32_t node) 
   /* gap acceptance: the last G cells of every lane of every major
    * incoming link are empty */
   int majorfree = 1;
-  for (int32_t i = a; i < b && majorfree; i++) {
+  for (int32_t i = a; i < b && majorfree && !signalized; i++) {
     int32_t j = o->in_list[i];
     if (o->cls[j] != maxcls) continue;
     for (int32_t l = 0; l < o->lanes[j] && majorfree; l++)
@@ -834,7 +854,7 @@ static void step_single(orc *o) {
       }
   /* --- §Node on S1 --- */
   for (int64_t i = 0; i < o->nlanes; i++) o->ext[i] = 0;
-  for (int32_t node = 0; node < o->nn; node++) node_resolve(o, V, V->occ, node);
+  for (int32_t node = 0; node < o->nn; node++) node_resolve(o, V, V->occ, node, t);
   /* --- §Move S1 -> S2 --- */
   int32_t *S1 = V->occ;
   int32_t *S2 = o->S0;
@@ -1081,7 +1101,7 @@ static void step_domains(orc *o) {
   for (int64_t i = 0; i < o->nlanes; i++) o->ext[i] = 0;
   for (int32_t node = 0; node < o->nn; node++)
     node_resolve(o, &o->dom[o->dom_of_node[node]],
-                 o->dom[o->dom_of_node[node]].occ, node);
+                 o->dom[o->dom_of_node[node]].occ, node, t);
   /* 4. compute speed and move: own vehicles plus the up-side strips
    *    received in exchange 1 ("ghosts") */
   int32_t *S2 = (int32_t *)xcalloc(o->ncells, 4);
@@ -1158,6 +1178,28 @@ int or_set_brake_override(orc *o, const uint8_t *mask) {
 }
 
 /* --------------------------------------------------------------- readers */
+/* fixed-time signals (reading R23): node ids and their plans */
+int or_set_signals(orc *o, int32_t n, const int32_t *node, const int32_t *green0,
+                   const int32_t *green1, const int32_t *offset) {
+  if (!o->have_net) return fail(o, 2, "load the network first");
+  if (o->inited) return fail(o, 2, "already initialised");
+  if (!o->sig_g0) {
+    o->sig_g0 = (int32_t *)xcalloc(o->nn, 4);
+    o->sig_g1 = (int32_t *)xcalloc(o->nn, 4);
+    o->sig_off = (int32_t *)xcalloc(o->nn, 4);
+  }
+  for (int32_t i = 0; i < n; i++) {
+    if (node[i] < 0 || node[i] >= o->nn) return fail(o, 2, "signal %d: bad node", i);
+    if (green0[i] < 0 || green1[i] < 0 || green0[i] + green1[i] < 1 ||
+        green0[i] + green1[i] > 1023 || offset[i] < 0)
+      return fail(o, 2, "signal %d: bad plan", i);
+    o->sig_g0[node[i]] = green0[i];
+    o->sig_g1[node[i]] = green1[i];
+    o->sig_off[node[i]] = offset[i];
+  }
+  return 0;
+}
+
 int32_t or_time(const orc *o) { return o->t; }
 
 uint64_t or_state_hash(const orc *o) {

@@ -57,6 +57,13 @@ int or_place_vehicles(orc *o, int32_t n, const int32_t *vid,
 
 /* finish initialisation: injection for departure <= t0 (O1 §Init step 3),
  * time starts at t0 (normally 0). */
+/* fixed-time two-phase signals at the given nodes (reading R23): phase 0 =
+ * incoming links of the node's maximal class, green for the first green0
+ * seconds of each (green0 + green1)-second cycle shifted by offset; phase
+ * 1 green for the rest.  green0 + green1 in [1, 1023].  Before or_init. */
+int or_set_signals(orc *o, int32_t n, const int32_t *node, const int32_t *green0,
+                   const int32_t *green1, const int32_t *offset);
+
 int or_init(orc *o, int32_t t0);
 
 /* advance n steps (single domain or k-domain emulation, see below). */

@@ -3,7 +3,7 @@ import os
 import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SRCS = ["csrc/tsim_kernels.cu", "csrc/tsim_rows.cu", "csrc/tsim_api.cu"]
+SRCS = ["csrc/tsim_kernels.cu", "csrc/tsim_rows.cu", "csrc/tsim_api.cu", "csrc/tsim_partition.cpp"]
 SO = os.path.join(HERE, "libtsim.so")
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v"]

@@ -71,6 +71,8 @@ struct ts_sim {
   int32_t *d_send_slot = nullptr, *d_recv_slot = nullptr;
   std::vector<int32_t> my_nodes;
   int32_t *d_node_ids = nullptr;
+  std::vector<uint32_t> node_sig;  // per node: phase-0 signal word (R23), 0 = none
+  uint32_t *d_node_sig = nullptr, *d_lane_sig = nullptr;
   bool rows_s1 = false, gen_s1 = false;  // row / general state holds S1(t) (lane change applied)
   int64_t n_pending0 = 0;
   int32_t folded_t = 0;  // stats folded into the host counters up to this time
@@ -96,6 +98,8 @@ struct ts_sim {
   uint32_t *d_planes[2] = {nullptr, nullptr};
   int32_t *d_rvid[2] = {nullptr, nullptr};
   int32_t *d_gcnt[2] = {nullptr, nullptr};  // vehicles per group
+  unsigned long long *d_gctr = nullptr;      // k_rows work counter
+  unsigned long long gctr_base = 0;
   int32_t *d_inj_scratch = nullptr;
   RowDesc *d_rows = nullptr;
   int rows_threads = 128, rows_blocks = 1, rows_cap = 0, rows_smem = 0;
@@ -390,6 +394,26 @@ int ts_set_arrived(ts_sim *h, int32_t n, const int32_t *vid, const int32_t *t_ar
   return TS_OK;
 }
 
+static uint32_t sig_word(int cycle, int shift, int len) {
+  return (1u << 31) | (uint32_t)cycle | ((uint32_t)shift << 10) | ((uint32_t)len << 20);
+}
+
+int ts_set_signals(ts_sim *h, int32_t n, const int32_t *node, const int32_t *green0,
+                   const int32_t *green1, const int32_t *offset) {
+  if (!h) return TS_EINVAL;
+  if (!h->have_net) return fail(h, TS_EINVAL, "load the network first");
+  if (h->inited) return fail(h, TS_EINVAL, "already initialised");
+  if (h->node_sig.empty()) h->node_sig.assign(h->nn, 0u);
+  for (int32_t i = 0; i < n; i++) {
+    if (node[i] < 0 || node[i] >= h->nn) return fail(h, TS_EINVAL, "signal %d: bad node", i);
+    const int g0 = green0[i], g1 = green1[i], c = g0 + g1;
+    if (g0 < 0 || g1 < 0 || c < 1 || c > 1023 || offset[i] < 0)
+      return fail(h, TS_EINVAL, "signal %d: bad plan", i);
+    h->node_sig[node[i]] = sig_word(c, offset[i] % c, g0);
+  }
+  return TS_OK;
+}
+
 int ts_set_domain(ts_sim *h, int32_t k, const int32_t *domain_of_node, int32_t me) {
   if (!h) return TS_EINVAL;
   if (!h->have_net) return fail(h, TS_EINVAL, "load the network first");
@@ -623,8 +647,9 @@ static void build_tiles(ts_sim *h) {
 // incoming lanes of every node in priority order (R9: major class first,
 // then link id, then lane), packed into chunks of <= 32 lanes
 static bool build_node_lanes(ts_sim *h, std::vector<NodeLane> &lanes,
-                             std::vector<int32_t> &chunk_off) {
+                             std::vector<int32_t> &chunk_off, std::vector<uint32_t> &sig) {
   lanes.clear();
+  sig.clear();
   chunk_off.assign(1, 0);
   int in_chunk = 0;
   for (int nd = 0; nd < h->nn; nd++) {
@@ -649,6 +674,14 @@ static bool build_node_lanes(ts_sim *h, std::vector<NodeLane> &lanes,
           lanes.push_back(NodeLane{h->lgid[j] + l, h->out_off[nd], h->tt[j], (uint8_t)l,
                                    (uint8_t)(pass == 0), (uint8_t)h->vmax[j],
                                    (uint8_t)node_first});
+          uint32_t sw = 0u;  // the lane's phase (R23): 0 = maximal class, 1 = the rest
+          const uint32_t s0 = h->node_sig.empty() ? 0u : h->node_sig[nd];
+          if (s0 >> 31) {
+            const int c = (int)(s0 & 1023u), sh = (int)((s0 >> 10) & 1023u),
+                      g0 = (int)((s0 >> 20) & 1023u);
+            sw = pass == 0 ? s0 : sig_word(c, ((sh - g0) % c + c) % c, c - g0);
+          }
+          sig.push_back(sw);
       }
     in_chunk += nl;
   }
@@ -732,6 +765,7 @@ static NodeParams node_params(ts_sim *h, int t) {
   N.out_pos = h->d_out_pos;
   N.rslot = h->d_rslot;
   N.nodeout = h->d_nodeout;
+  N.node_sig = h->d_node_sig;
   N.vpos = h->d_vpos;
   N.tail_rec = h->d_tail;
   N.head_occ = h->d_head;
@@ -753,7 +787,17 @@ static RowsParams rows_params(ts_sim *h) {
   r.gcnt_out = h->d_gcnt[h->rcur ^ 1];
   r.ngroups = h->ngroups;
   r.cap = h->rows_cap;
+  r.gctr = h->d_gctr;
+  r.gbase = h->gctr_base;
   return r;
+}
+
+// k_rows launch; the work counter advances by the groups plus one failed
+// fetch per warp
+static void rows_launch(ts_sim *h, const StepParams &p) {
+  launch_rows(p, rows_params(h), h->rows_blocks, h->rows_threads, h->rows_smem, h->stream);
+  h->gctr_base += (unsigned long long)h->ngroups + (unsigned long long)h->rows_blocks *
+                                                        (h->rows_threads / 32);
 }
 
 static int base_mode(const ts_sim *h) {
@@ -930,6 +974,7 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
     if ((rc = dalloc(h, &h->d_planes[b], std::max<size_t>(16, planes.size()), 0))) return rc;
     if ((rc = dalloc(h, &h->d_rvid[b], h->rvid_entries, 0xFF))) return rc;
     if ((rc = dalloc(h, &h->d_gcnt[b], std::max(1, h->ngroups), 0))) return rc;
+    if (b == 0 && (rc = dalloc(h, &h->d_gctr, 1, 0))) return rc;
   }
   if (!h->gtiles.empty()) {
     CK(h, cudaMemcpyAsync(h->d_code[0], gcode.data(), gcode.size(), cudaMemcpyHostToDevice, h->stream));
@@ -1013,26 +1058,30 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
   h->blocks = std::max(1, std::min(need, occ * nsm));
   // row kernel: one warp per 32-row group, 4 warps per block; each warp
   // stages its group's vid blocks (in + out) in shared memory
-  h->rows_threads = 128;
   // staging capacity per warp: 5 blocks of 4 warps per SM (96 registers)
   // leave ~44 KB of shared memory per block; group_cells overrides (tuning)
-  h->rows_cap = h->cfg.group_cells > 0 ? (h->cfg.group_cells + 3) & ~3 : 1312;
-  h->rows_smem = 4 * rows_stage_words(h->rows_cap) * 4;
+  h->rows_cap = h->cfg.group_cells > 0 ? (h->cfg.group_cells + 3) & ~3 : 1024;
+  h->rows_threads = 128;
+  h->rows_smem = (h->rows_threads / 32) * rows_stage_words(h->rows_cap) * 4;
   CK(h, set_rows_smem(h->rows_smem));
   {  // persistent grid: every resident warp loops over groups
+    const int wpb = h->rows_threads / 32;
     const int rocc = std::max(1, occupancy_rows(h->rows_threads, h->rows_smem));
-    h->rows_blocks = std::max(1, std::min((h->ngroups + 3) / 4, rocc * nsm));
+    h->rows_blocks = std::max(1, std::min((h->ngroups + wpb - 1) / wpb, rocc * nsm));
   }
   {
     std::vector<NodeLane> nlanes;
     std::vector<int32_t> chunk_off;
+    std::vector<uint32_t> lsig;
     h->node_warp = h->periodic < 0 && !(h->cfg.flags & (TS_FLAG_GENERAL | TS_FLAG_NODE_GENERAL)) &&
-                   build_node_lanes(h, nlanes, chunk_off);
+                   build_node_lanes(h, nlanes, chunk_off, lsig);
     if (h->node_warp) {
       h->nchunks = (int32_t)chunk_off.size() - 1;
       if ((rc = upload(h, &h->d_nlanes, nlanes))) return rc;
       if ((rc = upload(h, &h->d_chunk_off, chunk_off))) return rc;
+      if ((rc = upload(h, &h->d_lane_sig, lsig))) return rc;
     }
+    if (!h->node_sig.empty() && (rc = upload(h, &h->d_node_sig, h->node_sig))) return rc;
   }
   // the nodes of this domain (nodes are never split)
   h->my_nodes.clear();
@@ -1061,7 +1110,7 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
   int mode = (inject0 ? kModeInject : 0) | (base_mode(h) & kModeHash);
   StepParams P = step_params(h, t0 - 1, mode);
   if (h->ngroups > 0) {
-    launch_rows(P, rows_params(h), h->rows_blocks, h->rows_threads, h->rows_smem, h->stream);
+    rows_launch(h, P);
     h->rcur ^= 1;
   }
   if (!h->gtiles.empty()) {
@@ -1107,8 +1156,7 @@ static void phase_lc(ts_sim *h) {
     h->gcur ^= 1;
   }
   if (h->ngroups > 0 && !h->rows_s1) {
-    launch_rows(step_params(h, t, kModeLC), rows_params(h), h->rows_blocks, h->rows_threads, h->rows_smem,
-                h->stream);
+    rows_launch(h, step_params(h, t, kModeLC));
     h->rcur ^= 1;
   }
   h->gen_s1 = h->rows_s1 = true;
@@ -1123,15 +1171,14 @@ static void phase_move(ts_sim *h, bool more, cudaEvent_t e0, cudaEvent_t e1) {
   const int mode = base_mode(h);
   if (h->n_xs > 0) unpack_strips(h);
   if (h->node_warp)
-    launch_node_warp(node_params(h, t), NodeWarpParams{h->d_nlanes, h->d_chunk_off, h->nchunks},
+    launch_node_warp(node_params(h, t), NodeWarpParams{h->d_lane_sig, h->d_nlanes, h->d_chunk_off, h->nchunks},
                      h->stream);
   else
     launch_node(node_params(h, t), h->stream);
   if (e0) cudaEventRecord(e0, h->stream);
   if (h->ngroups > 0) {
     const bool f = more && h->rfused;
-    launch_rows(step_params(h, t, mode | (f ? kModeLC : 0)), rows_params(h), h->rows_blocks,
-                h->rows_threads, h->rows_smem, h->stream);
+    rows_launch(h, step_params(h, t, mode | (f ? kModeLC : 0)));
     h->rcur ^= 1;
     h->rows_s1 = f;
   }
@@ -1554,6 +1601,19 @@ int ts_read_history(ts_sim *h, int32_t t_from, int32_t n, uint64_t *hash, int64_
     if (lane_changes) lane_changes[i] = (int64_t)s[ST_LC];
     if (crossings) crossings[i] = (int64_t)s[ST_CROSS];
   }
+  return TS_OK;
+}
+
+int ts_read_flow(ts_sim *h, int32_t t_from, int32_t n, int64_t *sumv) {
+  if (!h || !h->inited) return fail(h, TS_EINVAL, "not initialised");
+  if (n < 0 || n > kHist || t_from + n - 1 > h->t || t_from < h->t - kHist + 1)
+    return fail(h, TS_EINVAL, "history range not available");
+  CK(h, cudaSetDevice(h->dev));
+  CK(h, cudaStreamSynchronize(h->stream));
+  std::vector<unsigned long long> st((size_t)kHist * ST_N);
+  CK(h, cudaMemcpy(st.data(), h->d_stats, st.size() * 8, cudaMemcpyDeviceToHost));
+  for (int i = 0; i < n; i++)
+    sumv[i] = (int64_t)st[(size_t)((t_from + i) & (kHist - 1)) * ST_N + ST_SUMV];
   return TS_OK;
 }
 

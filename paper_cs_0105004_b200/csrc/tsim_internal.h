@@ -116,9 +116,12 @@ static_assert(sizeof(RowDesc) == 16, "RowDesc must be 16 bytes");
 
 // shared memory of one k_rows warp (4-byte words): the group's vid block in
 // and out (cap entries each; the out area first serves as the list of the
-// vehicles that draw), then the brake bits of the 32 rows (4 words each)
+// vehicles that draw), then an aux area: the brake bits of the 32 rows
+// during the draws, the masks and list offsets of the rows the lane change
+// touched during the list rebuild
+constexpr int kRowsAuxWords = 4 * 32 * kRowWords + 5 * 32 + 4;
 __host__ __device__ inline int rows_stage_words(int cap) {
-  return 2 * cap + 32 * kRowWords;  // cap is a multiple of 4: 16-byte aligned
+  return 2 * cap + kRowsAuxWords;  // cap is a multiple of 4: 16-byte aligned
 }
 
 // Warp-cooperative node kernel: the incoming lanes of every node, in the
@@ -232,6 +235,7 @@ struct NodeParams {
   const uint8_t *rslot;
   VehPos *vpos;
   const NodeOut *nodeout;  // [out_off[node] + slot]
+  const uint32_t *node_sig;  // per node, phase-0 signal word (phase 1 derived); NULL = none
   const uint64_t *tail_rec;
   const uint8_t *head_occ;
   uint8_t *ext;
@@ -257,9 +261,20 @@ struct RowsParams {
   int32_t *gcnt_out;
   int32_t ngroups;
   int32_t cap;                // smem staging capacity (entries) of a group's vid block
+  unsigned long long *gctr;   // work counter, monotonic across launches
+  unsigned long long gbase;   // its value at the start of this launch
 };
 
+// signal word of an incoming lane (reading R23): 0 = unsignalized, else
+// bit 31 | cycle (bits 0-9) | shift (10-19) | green length (20-29); the lane
+// is green at time t iff (t + shift) mod cycle < green length
+__host__ __device__ inline bool sig_green(uint32_t s, int t) {
+  const int c = (int)(s & 1023u), sh = (int)((s >> 10) & 1023u), len = (int)((s >> 20) & 1023u);
+  return (t + sh) % c < len;
+}
+
 struct NodeWarpParams {
+  const uint32_t *sig;  // per lane (same order as lanes)
   const NodeLane *lanes;
   const int32_t *chunk_off;  // [nchunks + 1]
   int32_t nchunks;

@@ -546,7 +546,10 @@ __global__ void __launch_bounds__(256) k_node_warp(const NodeParams P, const Nod
                        nodemask) != 0u;
     Cand cd{false, -1, 0, 0, 0, 0};
     if (act) cd = node_candidate(P, rec, e.lane, e.out_base, e.tt, e.vk);
-    const bool eligible = cd.cand && (e.major || !busy);
+    // signalized node (R23): red approaches have the virtual blocker, green
+    // ones need no gap acceptance; otherwise priority + gap acceptance (R9)
+    const uint32_t sg = act ? W.sig[a + lane] : 0u;
+    const bool eligible = cd.cand && ((sg >> 31) ? sig_green(sg, P.t) : (e.major || !busy));
     const int key = eligible ? cd.tgt : -1 - lane;
     const uint32_t grp = __match_any_sync(FULL, key);
     int ext = 0;
@@ -563,6 +566,7 @@ __global__ void __launch_bounds__(128) k_node(const NodeParams P) {
   uint32_t crossings = 0;
   if (ni < P.nnodes) {
     const int node = P.node_ids ? P.node_ids[ni] : ni;
+    const uint32_t sg0 = P.node_sig ? P.node_sig[node] : 0u;  // phase-0 word (R23)
     const int a = P.in_off[node], b = P.in_off[node + 1];
     int maxcls = -2147483647;
     for (int i = a; i < b; i++) maxcls = max(maxcls, P.link_cls[P.in_list[i]]);
@@ -573,7 +577,8 @@ __global__ void __launch_bounds__(128) k_node(const NodeParams P) {
       const int lg = P.link_lgid[j];
       for (int l = 0; l < P.link_lanes[j]; l++) {
         P.ext[lg + l] = 0;
-        if (P.link_cls[j] == maxcls && ((uint32_t)(P.tail_rec[lg + l] >> 44) & gmask))
+        if (!(sg0 >> 31) && P.link_cls[j] == maxcls &&
+            ((uint32_t)(P.tail_rec[lg + l] >> 44) & gmask))
           majorfree = false;
       }
     }
@@ -590,6 +595,15 @@ __global__ void __launch_bounds__(128) k_node(const NodeParams P) {
           const uint64_t rec = P.tail_rec[lg + l];
           const Cand cd = node_candidate(P, rec, l, P.out_off[node], P.tt_link[j], P.vmax_link[j]);
           if (!cd.cand) continue;
+          if (sg0 >> 31) {  // signalized: phase 0 = maximal class, phase 1 = the rest
+            const int c = (int)(sg0 & 1023u), g0 = (int)((sg0 >> 20) & 1023u);
+            const int off = (int)((sg0 >> 10) & 1023u);
+            const bool ph0 = P.link_cls[j] == maxcls;
+            const uint32_t s1 = (1u << 31) | (uint32_t)c |
+                                ((uint32_t)(((off - g0) % c + c) % c) << 10) |
+                                ((uint32_t)(c - g0) << 20);
+            if (!sig_green(ph0 ? sg0 : s1, P.t)) continue;
+          }
           const int bit = cd.tgt;  // target lanes of a node are distinct global lanes
           bool taken = false;
           for (int q = 0; q < nclaimed; q++) taken |= claimed[q] == bit;
@@ -646,7 +660,15 @@ void launch_hash(const StepParams &p, int blocks, int threads, int smem, void *s
   k_hash<<<blocks, threads, smem, (cudaStream_t)stream>>>(p, out);
 }
 
+// The attribute is per function (process-wide), while every handle asks for
+// its own size: only ever raise it, so no handle's launch falls below it.
 cudaError_t set_smem_attrs(int bytes) {
+  static int current[64] = {0};  // per device
+  int dev = 0;
+  cudaGetDevice(&dev);
+  dev &= 63;
+  if (bytes <= current[dev]) return cudaSuccess;
+  current[dev] = bytes;
   cudaError_t e = cudaFuncSetAttribute(k_lc, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(k_step, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);

@@ -74,6 +74,17 @@ __device__ __forceinline__ uint32_t onehot(int i, int c) {
   const unsigned d = (unsigned)(c - 32 * i);
   return d < 32u ? (1u << d) : 0u;
 }
+// word i of the row (arithmetic select: no dynamic register indexing)
+__device__ __forceinline__ uint32_t pick(const uint32_t (&x)[NW], int i) {
+  uint32_t r = 0u;
+#pragma unroll
+  for (int k = 0; k < NW; k++) r |= x[k] & (0u - (uint32_t)(k == i));
+  return r;
+}
+// bits [s, s + 32) of the row, s >= 0
+__device__ __forceinline__ uint32_t win_row(const uint32_t (&x)[NW], int s) {
+  return __funnelshift_r(pick(x, s >> 5), pick(x, (s >> 5) + 1), s & 31);
+}
 __device__ __forceinline__ int bit_row(const uint32_t (&x)[NW], int c) {
   uint32_t b = 0u;
 #pragma unroll
@@ -124,6 +135,66 @@ __device__ __forceinline__ void warp_store(int32_t *gdst, const int32_t *src, in
 }
 }  // namespace
 
+struct RowWords {
+  uint32_t w[kRowWords];
+};
+
+// state hash contribution of one row of S(t+1) before its lane change
+// (test instrument; kept out of line)
+static __device__ __noinline__ uint64_t hash_row(RowWords oo, RowWords v0, RowWords v1,
+                                                 RowWords v2, RowWords inj, int ent_y,
+                                                 uint32_t ent_e, const int32_t *vin,
+                                                 const int32_t *scratch, int link, int l) {
+  uint64_t h = 0;
+  int k = 0;
+  for (int c = 0; c < kRowMaxCells; c++) {
+    const int i = c >> 5, x = c & 31;
+    if (!((oo.w[i] >> x) & 1u)) continue;
+    uint32_t e;
+    if (c == ent_y) e = ent_e;
+    else if ((inj.w[i] >> x) & 1u) e = (uint32_t)scratch[c];
+    else e = (uint32_t)vin[k++];
+    const int v = (int)((v0.w[i] >> x) & 1u) | (int)(((v1.w[i] >> x) & 1u) << 1) |
+                  (int)(((v2.w[i] >> x) & 1u) << 2);
+    h += vmix((int)(e & kVidMask), link, l, c, v);
+  }
+  return h;
+}
+
+// Turn-motivated lane change inside the last D cells (R6): the accepted
+// gaps shrink with the distance d to the link end, (floor(min(v+1,V) d/D),
+// floor(V d/D)); evaluated per candidate (rare, kept out of line).  zc:
+// candidates of the word starting at cell c0; tg1..tg5: target-lane gap
+// ahead >= k; tp, t0: target-lane occupancy of the previous / this word.
+static __device__ __noinline__ uint32_t zone_lc(uint32_t zc, int c0, int w, int vk, int D,
+                                                uint32_t v0, uint32_t v1, uint32_t v2,
+                                                uint32_t tg1, uint32_t tg2, uint32_t tg3,
+                                                uint32_t tg4, uint32_t tg5, uint32_t tp,
+                                                uint32_t t0) {
+  uint32_t lv = 0u;
+  while (zc) {
+    const int x = __ffs(zc) - 1;
+    zc &= zc - 1u;
+    const int d = w - 1 - (c0 + x);
+    const int v = (int)((v0 >> x) & 1u) | (int)(((v1 >> x) & 1u) << 1) | (int)(((v2 >> x) & 1u) << 2);
+    const int rf = (min(v + 1, vk) * d) / D, rb = (vk * d) / D;
+    // ahead >= rf: tg_rf at x; behind >= rb: target cells x-1..x-rb empty,
+    // cells before the row start count as empty
+    const uint32_t tg = rf <= 0 ? FULL : rf == 1 ? tg1 : rf == 2 ? tg2 : rf == 3 ? tg3
+                      : rf == 4 ? tg4 : tg5;
+    bool ok = (tg >> x) & 1u;
+    if (rb > 0) {
+      const uint32_t behind = __funnelshift_lc(tp, t0, 32 - x);  // bit j: cell c0+x-32+j
+      const uint32_t need = ((1u << rb) - 1u) << (32 - rb);       // cells x-rb..x-1
+      const int c = c0 + x;
+      const uint32_t valid = c >= 32 ? FULL : (c == 0 ? 0u : ~((1u << (32 - c)) - 1u));
+      if (behind & need & valid) ok = false;
+    }
+    if (ok) lv |= 1u << x;
+  }
+  return lv;
+}
+
 __global__ void __launch_bounds__(128, 5) k_rows(const StepParams P, const RowsParams R) {
   __shared__ unsigned long long red[4 * 8];
   extern __shared__ __align__(16) int32_t stage[];  // per warp: vid block in, vid block out
@@ -139,7 +210,14 @@ __global__ void __launch_bounds__(128, 5) k_rows(const StepParams P, const RowsP
   Acc acc = {};
   Acc acc_next = {};
 
-  for (int g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; g < R.ngroups; g += nwarps) {
+  // groups are handed out dynamically (one atomic per warp and group): no
+  // warp idles while another still has a queue of groups
+  (void)nwarps;
+  for (;;) {
+    int g = 0;
+    if (lane == 0) g = (int)(atomicAdd(R.gctr, 1ull) - R.gbase);
+    g = __shfl_sync(FULL, g, 0);
+    if (g >= R.ngroups) break;
     __syncwarp();  // the previous group's staged blocks are no longer in use
     const RowDesc rd = R.rows[(size_t)g * 32 + lane];
     const int w = rd.w, l = rd.l, L = rd.L, link = rd.link, lg = rd.lg, vk = rd.vk;
@@ -208,6 +286,8 @@ __global__ void __launch_bounds__(128, 5) k_rows(const StepParams P, const RowsP
           fv2 = min(min(v + 1, vk), gp);
         }
       }
+      const int xw = xf >> 5;  // the front's word and bit
+      const uint32_t xbit = 1u << (xf & 31);
       // U_k of word i (k = 1..5)
       auto thermo = [&](int i, uint32_t (&u)[5]) {
         const uint32_t o0 = Oext[i], o1 = i + 1 < NW ? Oext[i + 1] : FULL;
@@ -222,7 +302,7 @@ __global__ void __launch_bounds__(128, 5) k_rows(const StepParams P, const RowsP
           else if (k == 4) T = vk >= 4 ? (V2[i] | (V1[i] & V0[i])) : 0u;  // v >= 3
           else T = vk >= 5 ? V2[i] : 0u;                                  // v >= 4
           u[k - 1] = T & f;
-          if (k > fd && k <= fv2) u[k - 1] |= onehot(i, xf);
+          if (i == xw && k > fd && k <= fv2) u[k - 1] |= xbit;
         }
       };
       uint32_t U1[NW];  // movers: v2 >= 1
@@ -230,7 +310,7 @@ __global__ void __launch_bounds__(128, 5) k_rows(const StepParams P, const RowsP
       for (int i = 0; i < NW; i++) {
         const uint32_t o1 = i + 1 < NW ? Oext[i + 1] : FULL;
         U1[i] = O[i] & ~__funnelshift_r(Oext[i], o1, 1);
-        if (fd == 0 && fv2 >= 1) U1[i] |= onehot(i, xf);
+        if (i == xw && fd == 0 && fv2 >= 1) U1[i] |= xbit;
       }
       // ---- Philox slowdown draws (R3) of the vehicles with v2 >= 1, 32 at a
       //      time across the warp: each row lists the block offsets of its
@@ -242,51 +322,40 @@ __global__ void __launch_bounds__(128, 5) k_rows(const StepParams P, const RowsP
         const int mc = popc_row(U1);
         const int moff = warp_scan(mc, lane, &mtot);
         const int32_t *vbase = staged ? (const int32_t *)s_in : R.vid_in + rd.voff;
-        if (mtot <= R.cap) {
-          // mover list entries: block offset << 12 | row slot << 7 | cell
-          int32_t *mlist = s_out;  // free until the output phase
-          uint32_t *bw = reinterpret_cast<uint32_t *>(s_out + R.cap) + lane * NW;
+        // mover list entries: block offset << 12 | row slot << 7 | cell, in
+        // chunks of the staging capacity (one chunk unless the group is huge)
+        int32_t *mlist = s_out;  // free until the output phase
+        uint32_t *bw = reinterpret_cast<uint32_t *>(s_out + R.cap);
 #pragma unroll
-          for (int i = 0; i < NW; i++) bw[i] = 0u;  // this row's brake bits
-          int j = moff, rb = in_off;
-#pragma unroll
+        for (int i = 0; i < NW; i++) bw[lane * NW + i] = 0u;  // this row's brake bits
+        for (int base = 0; base < mtot; base += R.cap) {
+          int j = moff - base, rb = in_off;
+#pragma unroll 1
           for (int i = 0; i < NW; i++) {
-            uint32_t m = U1[i];
+            uint32_t m = pick(U1, i);
+            const uint32_t o = pick(O, i);
             while (m) {
               const int x = __ffs(m) - 1;
               m &= m - 1u;
-              mlist[j++] = ((rb + __popc(O[i] & lowm(x))) << 12) | (lane << 7) | (32 * i + x);
+              if (j >= 0 && j < R.cap)
+                mlist[j] = ((rb + __popc(o & ((1u << x) - 1u))) << 12) | (lane << 7) | (32 * i + x);
+              j++;
             }
-            rb += __popc(O[i]);
+            rb += __popc(o);
           }
           __syncwarp();
-          uint32_t *bw0 = reinterpret_cast<uint32_t *>(s_out + R.cap);
-          for (int jj = lane; jj < mtot; jj += 32) {
+          const int n = min(mtot - base, R.cap);
+          for (int jj = lane; jj < n; jj += 32) {
             const int me = mlist[jj];
             const uint32_t e = (uint32_t)vbase[me >> 12];
             if ((uint64_t)philox_w0((uint32_t)P.t, e & kVidMask, P.k0, P.k1) < P.p32)
-              atomicOr(bw0 + ((me >> 7) & 31) * NW + ((me >> 5) & 3), 1u << (me & 31));
+              atomicOr(bw + ((me >> 7) & 31) * NW + ((me >> 5) & 3), 1u << (me & 31));
           }
           __syncwarp();
-#pragma unroll
-          for (int i = 0; i < NW; i++) Bm[i] = bw[i];
-          __syncwarp();
-        } else {  // more movers than staging room: each row draws its own
-          int rb = 0;
-#pragma unroll
-          for (int i = 0; i < NW; i++) {
-            uint32_t m = U1[i], b = 0u;
-            while (m) {
-              const int x = __ffs(m) - 1;
-              m &= m - 1u;
-              const uint32_t e = (uint32_t)vin[rb + __popc(O[i] & lowm(x))];
-              if ((uint64_t)philox_w0((uint32_t)P.t, e & kVidMask, P.k0, P.k1) < P.p32)
-                b |= 1u << x;
-            }
-            Bm[i] = b;
-            rb += __popc(O[i]);
-          }
         }
+#pragma unroll
+        for (int i = 0; i < NW; i++) Bm[i] = bw[lane * NW + i];
+        __syncwarp();
       }
       // ---- hop, word by word: D_k = vehicles moving exactly k (v3 = k);
       //      those passing the row end leave it (LR); O' = OR_k D_k << k with
@@ -452,29 +521,10 @@ __global__ void __launch_bounds__(128, 5) k_rows(const StepParams P, const RowsP
             if (vk >= 4) req &= ~E4 | TG[4];
             if (vk >= 5) req &= ~E5 | TG[5];
             lv |= turn & ~ZN & req & BKv;
-            uint32_t zc = turn & ZN;  // scaled thresholds (R6): per candidate
-            while (zc) {
-              const int x = __ffs(zc) - 1;
-              zc &= zc - 1u;
-              const int d = w - 1 - (32 * i + x);
-              const int v = (int)((OV0[i] >> x) & 1u) | (int)(((OV1[i] >> x) & 1u) << 1) |
-                            (int)(((OV2[i] >> x) & 1u) << 2);
-              const int rf = (min(v + 1, vk) * d) / P.D, rb = (vk * d) / P.D;
-              // ahead >= rf and behind >= rb in the target lane
-              bool ok = true;
-#pragma unroll
-              for (int k = 1; k <= 5; k++) {
-                if (k <= rf && !((TG[k] >> x) & 1u)) ok = false;
-              }
-              if (rb > 0) {
-                // behind >= rb: target cells x-1..x-rb empty (before 0 = empty)
-                const int c = 32 * i + x;
-#pragma unroll
-                for (int k = 1; k <= 5; k++)
-                  if (k <= rb && c - k >= 0 && bit_row(T0, c - k)) ok = false;
-              }
-              if (ok) lv |= 1u << x;
-            }
+            const uint32_t zc = turn & ZN;  // scaled thresholds (R6): per candidate
+            if (zc)
+              lv |= zone_lc(zc, 32 * i, w, vk, P.D, OV0[i], OV1[i], OV2[i], TG[1], TG[2], TG[3],
+                            TG[4], TG[5], tp, T0[i]);
           }
           LV[i] = lv;
         }
@@ -541,41 +591,104 @@ __global__ void __launch_bounds__(128, 5) k_rows(const StepParams P, const RowsP
       }
       for (; i < nfin; i++) vout[i] = vin[i - sh];
     }
-    if (__any_sync(FULL, general)) {
-      // every vehicle of S(t+1) before the lane change, in cell order, goes
-      // to its rank in the final occupancy of its row (own, or l + dir)
-      uint32_t FT[NW];
+    if (const uint32_t gmask = __ballot_sync(FULL, general)) {
+      // rows whose vehicle set changed inside (lane changes, injections):
+      // every vehicle of S(t+1) before the lane change goes to its rank in
+      // the final occupancy of its row (own, or l + dir).  The vehicles of
+      // all such rows are processed 32 at a time across the warp from the
+      // rows' masks published in shared memory.
+      int32_t *aux = s_out + R.cap;  // brake bits are dead by now
+      uint32_t *rOO = reinterpret_cast<uint32_t *>(aux), *rFO = rOO + 32 * NW,
+               *rLV = rFO + 32 * NW, *rIN = rLV + 32 * NW;
+      int32_t *mInOff = aux + 4 * 32 * NW, *mOutOff = mInOff + 32, *mEnt = mOutOff + 32,
+              *mEntE = mEnt + 32, *mItem = mEntE + 32;  // mItem: 33 entries
 #pragma unroll
-      for (int i = 0; i < NW; i++) FT[i] = shfl_w(FO[i], lane + dir);
-      int32_t *tout = obase + __shfl_sync(FULL, out_off, lane + dir);
-      if (general) {
-        int k = 0, rown = 0, rtgt = 0;
+      for (int i = 0; i < NW; i++) {
+        rOO[lane * NW + i] = OO[i];
+        rFO[lane * NW + i] = FO[i];
+        rLV[lane * NW + i] = LV[i];
+        rIN[lane * NW + i] = INJ[i];
+      }
+      mInOff[lane] = in_off;
+      mOutOff[lane] = out_off;
+      mEnt[lane] = ent_y;
+      mEntE[lane] = (int32_t)ent_e;
+      int itot;
+      const int ioff = warp_scan(general ? popc_row(OO) : 0, lane, &itot);
+      mItem[lane] = ioff;
+      if (lane == 0) mItem[32] = itot;
+      __syncwarp();
+      const int32_t *ibase = staged ? (const int32_t *)s_in : R.vid_in + rd.voff;
+      for (int J = lane; J < itot; J += 32) {
+        // the row of item J: the last row whose first item is <= J
+        int r0 = 0;
+#pragma unroll
+        for (int st = 16; st; st >>= 1)
+          if (mItem[r0 + st] <= J) r0 += st;
+        const int rr = J - mItem[r0];  // rank of the vehicle in the row's OO
+        // the word holding set bit number rr, and the rank inside it
+        uint32_t wsel = 0u;
+        int c = 0, k2 = rr;
+        bool found = false;
 #pragma unroll
         for (int i = 0; i < NW; i++) {
-          uint32_t m = OO[i];
-          while (m) {
-            const int x = __ffs(m) - 1;
-            m &= m - 1u;
-            const int c = 32 * i + x;
-            uint32_t e;
-            if (c == ent_y) e = ent_e;
-            else if ((INJ[i] >> x) & 1u)
-              e = (uint32_t)R.inj_scratch[((size_t)g * 32 + lane) * kRowMaxCells + c];
-            else e = (uint32_t)vin[k++];
-            if (hash) {  // state hash of S(t+1), before its lane change (tests)
-              const int v = (int)((OV0[i] >> x) & 1u) | (int)(((OV1[i] >> x) & 1u) << 1) |
-                            (int)(((OV2[i] >> x) & 1u) << 2);
-              acc.hash += vmix((int)(e & kVidMask), link, l, c, v);
+          const uint32_t wv = rOO[r0 * NW + i];
+          const int pc = __popc(wv);
+          if (!found) {
+            if (k2 < pc) {
+              wsel = wv;
+              c = 32 * i;
+              found = true;
+            } else {
+              k2 -= pc;
             }
-            if ((LV[i] >> x) & 1u)
-              tout[rtgt + __popc(FT[i] & lowm(x))] = (int32_t)e;
-            else
-              vout[rown + __popc(FO[i] & lowm(x))] = (int32_t)e;
           }
-          rown += __popc(FO[i]);
-          rtgt += __popc(FT[i]);
         }
+        {  // select bit k2 of wsel by popcount halving
+          uint32_t m = wsel;
+          int pos = 0, cnt = __popc(m & 0xFFFFu);
+          if (k2 >= cnt) { k2 -= cnt; pos = 16; m >>= 16; }
+          cnt = __popc(m & 0xFFu);
+          if (k2 >= cnt) { k2 -= cnt; pos += 8; m >>= 8; }
+          cnt = __popc(m & 0xFu);
+          if (k2 >= cnt) { k2 -= cnt; pos += 4; m >>= 4; }
+          cnt = __popc(m & 0x3u);
+          if (k2 >= cnt) { k2 -= cnt; pos += 2; m >>= 2; }
+          c += pos + (k2 >= (int)(m & 1u) ? 1 : 0);
+        }
+        const int ci = c >> 5;
+        const uint32_t bit = 1u << (c & 31), lowb = bit - 1u;
+        const uint32_t inj_w = rIN[r0 * NW + ci];
+        uint32_t e;
+        if (c == mEnt[r0]) {
+          e = (uint32_t)mEntE[r0];
+        } else if (inj_w & bit) {
+          e = (uint32_t)R.inj_scratch[((size_t)g * 32 + r0) * kRowMaxCells + c];
+        } else {
+          int ninj = __popc(inj_w & lowb);
+          for (int i = 0; i < ci; i++) ninj += __popc(rIN[r0 * NW + i]);
+          const int me = (mEnt[r0] >= 0 && mEnt[r0] < c) ? 1 : 0;
+          e = (uint32_t)ibase[mInOff[r0] + rr - me - ninj];
+        }
+        const int dst = (rLV[r0 * NW + ci] & bit) ? r0 + dir : r0;
+        int rank = __popc(rFO[dst * NW + ci] & lowb);
+        for (int i = 0; i < ci; i++) rank += __popc(rFO[dst * NW + i]);
+        obase[mOutOff[dst] + rank] = (int32_t)e;
       }
+      if (hash && general) {  // state hash of S(t+1), before its lane change (tests)
+        RowWords oo, v0, v1, v2, inj;
+#pragma unroll
+        for (int i = 0; i < NW; i++) {
+          oo.w[i] = OO[i];
+          v0.w[i] = OV0[i];
+          v1.w[i] = OV1[i];
+          v2.w[i] = OV2[i];
+          inj.w[i] = INJ[i];
+        }
+        acc.hash += hash_row(oo, v0, v1, v2, inj, ent_y, ent_e, vin,
+                             R.inj_scratch + ((size_t)g * 32 + lane) * kRowMaxCells, link, l);
+      }
+      (void)gmask;
     }
     __syncwarp();
     const uint32_t efin = nfin > 0 ? (uint32_t)vout[nfin - 1] : 0u;  // final front vehicle
@@ -585,14 +698,13 @@ __global__ void __launch_bounds__(128, 5) k_rows(const StepParams P, const RowsP
     if (lc && w > 0) {
       const int nb = min(w, kGmax);
       const int xf = top_row(FO);
-      uint32_t occ = 0u;  // bit i = cell n-1-i
-#pragma unroll
-      for (int j = 0; j < kGmax; j++)
-        if (j < nb && bit_row(FO, w - 1 - j)) occ |= 1u << j;
+      // bit j = cell n-1-j of the last nb cells
+      const uint32_t occ = __brev(win_row(FO, w - nb) & lowm(nb)) >> (32 - nb);
       uint64_t rec = (uint64_t)occ << 44;
       if (occ) {
-        const int code = (bit_row(FV0, xf) | (bit_row(FV1, xf) << 1) | (bit_row(FV2, xf) << 2)) |
-                         ((int)(efin >> kSlotShift) << 3);
+        const int xi = xf >> 5, xb = xf & 31;
+        const int code = (int)((pick(FV0, xi) >> xb) & 1u) | (int)(((pick(FV1, xi) >> xb) & 1u) << 1) |
+                         (int)(((pick(FV2, xi) >> xb) & 1u) << 2) | ((int)(efin >> kSlotShift) << 3);
         rec |= (uint64_t)(efin & kVidMask) | ((uint64_t)code << 32) |
                ((uint64_t)(w - 1 - xf) << 40) | (1ull << 43);
       }
@@ -655,7 +767,13 @@ void launch_rows_hash(const StepParams &p, const RowsParams &r, void *stream,
   const int n = r.ngroups * 32;
   k_rows_hash<<<(n + 127) / 128, 128, 0, (cudaStream_t)stream>>>(r, out);
 }
-cudaError_t set_rows_smem(int bytes) {
+cudaError_t set_rows_smem(int bytes) {  // only ever raised (see set_smem_attrs)
+  static int current[64] = {0};  // per device
+  int dev = 0;
+  cudaGetDevice(&dev);
+  dev &= 63;
+  if (bytes <= current[dev]) return cudaSuccess;
+  current[dev] = bytes;
   return cudaFuncSetAttribute(k_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
 }
 int occupancy_rows(int threads, int smem) {

@@ -53,10 +53,13 @@ def node_weights(scn, link_work=None):
     return w + 1e-9
 
 
-def partition(scn, k, weights=None):
-    """domain of every node: ORB on the node coordinates"""
+def partition(scn, k, weights=None, method="orb"):
+    """domain of every node: ORB on the node coordinates
+    or the multilevel graph partitioner"""
     if weights is None:
         weights = node_weights(scn)
+    if method == "multilevel":
+        return _t.multilevel_partition(scn, k, weights)
     return _t.orb_partition(scn.node_x, scn.node_y, k, weights)
 
 

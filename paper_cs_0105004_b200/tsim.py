@@ -59,11 +59,15 @@ def load_library():
         "ts_state_hash": (ctypes.c_int, [P, ctypes.POINTER(ctypes.c_uint64)]),
         "ts_read_history": (ctypes.c_int, [P, I32, I32, P, P, P, P, P, P]),
         "ts_get_totals": (ctypes.c_int, [P, P]),
+        "ts_read_flow": (ctypes.c_int, [P, I32, I32, P]),
         "ts_get_link_work": (ctypes.c_int, [P, P]),
         "ts_orb_partition": (ctypes.c_int, [I32, P, P, P, I32, P]),
+        "ts_multilevel_partition": (ctypes.c_int, [I32, P, P, I32, P, P, P, P, I32,
+                                                   ctypes.c_double, ctypes.c_uint64, P]),
         "ts_place_vehicles_at": (ctypes.c_int, [P, I32, P, P, P, P, P]),
         "ts_set_arrived": (ctypes.c_int, [P, I32, P, P]),
         "ts_set_domain": (ctypes.c_int, [P, I32, P, I32]),
+        "ts_set_signals": (ctypes.c_int, [P, I32, P, P, P, P]),
         "ts_domain_plan": (ctypes.c_int, [I32, I32, P, P, P, P, I32, P, I32, I32, P, P, P]),
         "ts_strip_bytes": (I32, []),
         "ts_resume": (ctypes.c_int, [P, I32]),
@@ -108,6 +112,22 @@ def orb_partition(node_x, node_y, k, weight=None):
     rc = lib.ts_orb_partition(x.size, x.ctypes.data, y.ctypes.data, _p(w), int(k), out.ctypes.data)
     if rc:
         raise TsError(f"ts_orb_partition failed ({rc})")
+    return out
+
+
+def multilevel_partition(scn, k, weight=None, imbalance=0.05, seed=1):
+    """multilevel k-way partition (METIS-style) -> domain
+    per node; edges weighted by lanes (strips per exchange)"""
+    lib = load_library()
+    x, y = _a(scn.node_x, np.int64), _a(scn.node_y, np.int64)
+    fr, to, la = _a(scn.link_from, np.int32), _a(scn.link_to, np.int32), _a(scn.link_lanes, np.int32)
+    w = None if weight is None else _a(weight, np.float64)
+    out = np.zeros(x.size, np.int32)
+    rc = lib.ts_multilevel_partition(x.size, x.ctypes.data, y.ctypes.data, fr.size, fr.ctypes.data,
+                                     to.ctypes.data, la.ctypes.data, _p(w), int(k),
+                                     float(imbalance), int(seed), out.ctypes.data)
+    if rc:
+        raise TsError(f"ts_multilevel_partition failed ({rc})")
     return out
 
 
@@ -194,6 +214,10 @@ class Sim:
         self.n_veh = scn.n_vehicles
         self.n_links = scn.n_links
         self.lanes = np.asarray(scn.link_lanes, dtype=np.int32)
+        sig = getattr(scn, "sig_node", None)
+        if sig is not None and len(sig):
+            a = [i32(scn.sig_node), i32(scn.sig_g0), i32(scn.sig_g1), i32(scn.sig_off)]
+            self._check(self.lib.ts_set_signals(self.h, a[0].size, *(x.ctypes.data for x in a)))
         if place and scn.place_vid.size:
             pl = [i32(scn.place_vid), i32(scn.place_lane), i32(scn.place_cell), i32(scn.place_v)]
             self._check(self.lib.ts_place_vehicles(self.h, pl[0].size, *(a.ctypes.data for a in pl)))
@@ -291,6 +315,12 @@ class Sim:
                                              *(_p(c) for c in cols)))
         return dict(hash=[int(x) for x in h], active=cols[0], arrivals=cols[1],
                     injections=cols[2], lane_changes=cols[3], crossings=cols[4])
+
+    def flow(self, t_from, n):
+        """sum of velocities of S(t), t in [t_from, t_from + n)"""
+        out = np.zeros(n, np.int64)
+        self._check(self.lib.ts_read_flow(self.h, int(t_from), int(n), _p(out)))
+        return out
 
     def totals(self):
         out = np.zeros(8, np.int64)

@@ -51,6 +51,11 @@ class Scenario:
     p_slow: float = 0.2
     seed: int = 1
     recipe: str = ""
+    # fixed-time signals (reading R23): node ids, green of phase 0 / 1, offset
+    sig_node: np.ndarray = dataclasses.field(default_factory=lambda: np.zeros(0, np.int32))
+    sig_g0: np.ndarray = dataclasses.field(default_factory=lambda: np.zeros(0, np.int32))
+    sig_g1: np.ndarray = dataclasses.field(default_factory=lambda: np.zeros(0, np.int32))
+    sig_off: np.ndarray = dataclasses.field(default_factory=lambda: np.zeros(0, np.int32))
 
     @property
     def n_nodes(self) -> int:
@@ -63,6 +68,28 @@ class Scenario:
     @property
     def n_vehicles(self) -> int:
         return int(self.depart.shape[0])
+
+
+def with_signals(scn, nodes=None, green0=30, green1=30, offset=None, seed=0):
+    """the same scenario with fixed-time two-phase signals (reading R23) at
+    `nodes` (default: every node with >= 2 incoming links); offsets seeded
+    uniform in [0, cycle) unless given"""
+    import copy
+    s = copy.copy(scn)
+    if nodes is None:
+        indeg = np.bincount(np.asarray(scn.link_to), minlength=scn.n_nodes)
+        nodes = np.nonzero(indeg >= 2)[0]
+    nodes = _i32(nodes)
+    n = nodes.size
+    if offset is None:
+        offset = np.random.default_rng(seed).integers(0, green0 + green1, n)
+    s.sig_node = nodes
+    s.sig_g0 = _i32(np.broadcast_to(green0, n))
+    s.sig_g1 = _i32(np.broadcast_to(green1, n))
+    s.sig_off = _i32(np.broadcast_to(offset, n))
+    s.name = scn.name + "_signals"
+    s.recipe = scn.recipe + f"; fixed-time signals {green0}/{green1} s at {n} nodes"
+    return s
 
 
 def _i32(a):

@@ -76,6 +76,14 @@ def test_portland_mixed_tiles():
     run_domains(s, 4, 200, chunk=50, tile_cells=64)
 
 
+@pytest.mark.parametrize("k", [3, 6])
+def test_multilevel_partition(k):
+    """the multilevel partitioner's domains (irregular, few split links)"""
+    s = scenarios.portland(n_nodes=600, n_edges=800, n_veh=8000, side_km=8.0, n_zones=64, seed=5)
+    s.depart = (s.depart // 12).astype(np.int32)
+    run_domains(s, k, 200, chunk=40, dom=domains.partition(s, k, method="multilevel"))
+
+
 def test_restore_is_exact():
     """read S(t), restore into a fresh handle, continue: identical to the
     uninterrupted run (checkpoint / migration primitive)"""

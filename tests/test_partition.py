@@ -1,0 +1,66 @@
+"""Partitioners: ORB (the paper's method for its runs)
+and the multilevel graph partitioner (the METIS-style
+alternative the paper compares with).  Host code: CPU tests."""
+import numpy as np
+import pytest
+
+import scenarios
+import paper_cs_0105004_b200 as tsim
+from paper_cs_0105004_b200 import domains
+
+
+@pytest.fixture(scope="module")
+def portland():
+    return scenarios.portland(n_nodes=2000, n_edges=2500, n_veh=100, side_km=20.0, n_zones=16,
+                              seed=2)
+
+
+def loads(scn, dom, k):
+    w = domains.node_weights(scn)
+    out = np.zeros(k)
+    np.add.at(out, dom, w)
+    return out
+
+
+@pytest.mark.parametrize("k", [2, 3, 4, 8, 16])
+def test_multilevel_valid_balanced(portland, k):
+    dom = domains.partition(portland, k, method="multilevel")
+    assert dom.shape == (portland.n_nodes,)
+    assert set(np.unique(dom)) == set(range(k))
+    ld = loads(portland, dom, k)
+    assert ld.max() / ld.mean() <= 1.05 + 1e-9, ld
+
+
+@pytest.mark.parametrize("k", [2, 4, 8])
+def test_multilevel_cuts_fewer_links_than_orb(portland, k):
+    """the paper's observation: the graph partitioner yields far fewer split
+    links than ORB"""
+    n_orb, _ = domains.split_stats(portland, domains.partition(portland, k))
+    n_ml, _ = domains.split_stats(portland, domains.partition(portland, k, method="multilevel"))
+    assert n_ml < n_orb, (n_ml, n_orb)
+
+
+def test_multilevel_deterministic_and_seeded(portland):
+    a = tsim.multilevel_partition(portland, 4, seed=3)
+    b = tsim.multilevel_partition(portland, 4, seed=3)
+    assert np.array_equal(a, b)
+
+
+def test_orb_on_grid_is_blocks():
+    """ORB of a regular lattice with uniform weights: contiguous blocks"""
+    s = scenarios.config("1")
+    dom = domains.partition(s, 4)
+    g = dom.reshape(4, 4)
+    assert len(np.unique(g[:2, :2])) == 1 and len(np.unique(g[2:, 2:])) == 1
+    n_spl, pairs = domains.split_stats(s, dom)
+    assert n_spl == 16 and len(pairs) == 8
+
+
+def test_partition_input_errors():
+    s = scenarios.config("1")
+    with pytest.raises(tsim.TsError):
+        tsim.multilevel_partition(s, 0)
+    with pytest.raises(tsim.TsError):
+        tsim.multilevel_partition(s, s.n_nodes + 1)
+    with pytest.raises(tsim.TsError):
+        tsim.orb_partition(s.node_x, s.node_y, s.n_nodes + 1)
