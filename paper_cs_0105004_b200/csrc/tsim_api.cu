@@ -103,9 +103,13 @@ struct ts_sim {
   int32_t *d_inj_scratch = nullptr;
   RowDesc *d_rows = nullptr;
   int rows_threads = 128, rows_blocks = 1, rows_cap = 0, rows_smem = 0;
+  std::vector<int32_t> gvoff;                // first vid-block entry of each group
+  int32_t *d_gvoff = nullptr;
   NodeLane *d_nlanes = nullptr;
-  int32_t *d_chunk_off = nullptr;
   int32_t nchunks = 0;
+  std::vector<int32_t> nli;   // node-lane index of every global lane id
+  int64_t n_nli = 0;          // size of the node-lane indexed arrays
+  int32_t *d_nli = nullptr;
   uint64_t p32 = 0;
   // device
   TileDesc *d_tiles = nullptr;
@@ -599,6 +603,7 @@ static void build_tiles(ts_sim *h) {
   h->tile_row.assign(h->tiles.size(), -1);
   h->gtiles.clear();
   h->rows.clear();
+  h->gvoff.clear();
   int64_t goff = 0, voff = 0, gbase = 0;
   int slot = 32;
   for (size_t i = 0; i < h->tiles.size(); i++) {
@@ -616,14 +621,14 @@ static void build_tiles(ts_sim *h) {
     if (slot + d.L > 32) {  // new group: its vid block starts after the last one
       voff = (voff + 3) & ~(int64_t)3;
       gbase = voff;
-      h->rows.resize(h->rows.size() + 32, RowDesc{(int32_t)gbase, 0, 0, 0, 0, 0, 1});
+      h->rows.resize(h->rows.size() + 32, RowDesc{0, 0, 0, 0, 0, 0, 1});
+      h->gvoff.push_back((int32_t)gbase);
       slot = 0;
     }
     const size_t base = h->rows.size() - 32;
     h->tile_row[i] = (int32_t)(base + slot);
     for (int l = 0; l < d.L; l++) {
       RowDesc &r = h->rows[base + slot + l];
-      r.voff = (int32_t)gbase;
       r.link = d.link;
       r.lg = d.lane_gid + l;
       r.w = (uint8_t)d.w;
@@ -647,11 +652,17 @@ static void build_tiles(ts_sim *h) {
 // incoming lanes of every node in priority order (R9: major class first,
 // then link id, then lane), packed into chunks of <= 32 lanes
 static bool build_node_lanes(ts_sim *h, std::vector<NodeLane> &lanes,
-                             std::vector<int32_t> &chunk_off, std::vector<uint32_t> &sig) {
+                             std::vector<uint32_t> &sig) {
   lanes.clear();
   sig.clear();
-  chunk_off.assign(1, 0);
   int in_chunk = 0;
+  auto close_chunk = [&]() {  // pad the chunk to 32 entries
+    while (lanes.size() % 32) {
+      lanes.push_back(NodeLane{-1, 0, 0u, 0, 0, 1, 0});
+      sig.push_back(0u);
+    }
+    in_chunk = 0;
+  };
   for (int nd = 0; nd < h->nn; nd++) {
     const int a = h->in_off[nd], b = h->in_off[nd + 1];
     if (a == b || h->dom_of_node[nd] != h->dom_me) continue;
@@ -661,10 +672,7 @@ static bool build_node_lanes(ts_sim *h, std::vector<NodeLane> &lanes,
       nl += h->lanes[h->in_list[i]];
     }
     if (nl > 32) return false;
-    if (in_chunk + nl > 32) {
-      chunk_off.push_back((int32_t)lanes.size());
-      in_chunk = 0;
-    }
+    if (in_chunk + nl > 32) close_chunk();
     const int node_first = in_chunk;  // the node's first lane in its chunk (match key)
     for (int pass = 0; pass < 2; pass++)
       for (int i = a; i < b; i++) {
@@ -685,8 +693,36 @@ static bool build_node_lanes(ts_sim *h, std::vector<NodeLane> &lanes,
       }
     in_chunk += nl;
   }
-  if (in_chunk > 0) chunk_off.push_back((int32_t)lanes.size());
+  close_chunk();
   return true;
+}
+
+// node-lane indices (tail records, node grants): the lane's position in the
+// node kernel's lane array, or the identity for the thread-per-node kernel;
+// lanes without a node of this domain share a dummy slot at the end
+static int setup_node_lanes(ts_sim *h) {
+  std::vector<NodeLane> nlanes;
+  std::vector<uint32_t> lsig;
+  h->node_warp = h->periodic < 0 && !(h->cfg.flags & (TS_FLAG_GENERAL | TS_FLAG_NODE_GENERAL)) &&
+                 build_node_lanes(h, nlanes, lsig);
+  h->nli.assign(h->nlanes, 0);
+  if (h->node_warp) {
+    h->nchunks = (int32_t)(nlanes.size() / 32);
+    h->n_nli = std::max<int64_t>((int64_t)nlanes.size(), 1) + 1;
+    for (int32_t &x : h->nli) x = (int32_t)(h->n_nli - 1);
+    for (size_t i = 0; i < nlanes.size(); i++)
+      if (nlanes[i].lane_gid >= 0) h->nli[nlanes[i].lane_gid] = (int32_t)i;
+    int rc;
+    if ((rc = upload(h, &h->d_nlanes, nlanes))) return rc;
+    if (h->node_sig.empty()) h->d_lane_sig = nullptr;
+    else if ((rc = upload(h, &h->d_lane_sig, lsig))) return rc;
+  } else {
+    h->n_nli = std::max<int64_t>(h->nlanes, 1);
+    for (int i = 0; i < h->nlanes; i++) h->nli[i] = i;
+  }
+  for (RowDesc &r : h->rows)
+    if (r.w > 0) r.nli = h->nli[r.lg];
+  return 0;
 }
 
 static int tile_of(const ts_sim *h, int k, int x) {
@@ -734,6 +770,7 @@ static StepParams step_params(ts_sim *h, int t, int mode) {
   P.pend_off = h->d_pend_off;
   P.pend_list = h->d_pend_list;
   P.pend_head = h->d_pend_head;
+  P.nli = h->d_nli;
   P.tail_rec = h->d_tail;
   P.head_occ = h->d_head;
   P.ext = h->d_ext;
@@ -778,6 +815,7 @@ static NodeParams node_params(ts_sim *h, int t) {
 static RowsParams rows_params(ts_sim *h) {
   RowsParams r{};
   r.rows = h->d_rows;
+  r.gvoff = h->d_gvoff;
   r.planes_in = h->d_planes[h->rcur];
   r.planes_out = h->d_planes[h->rcur ^ 1];
   r.vid_in = h->d_rvid[h->rcur];
@@ -894,7 +932,7 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
       for (int l = 0; l < h->tiles[ti].L; l++) row_tile[h->tile_row[ti] + l] = (int32_t)ti;
   std::vector<int32_t> gcnt(std::max(1, h->ngroups), 0);
   for (int g = 0; g < h->ngroups; g++) {
-    const int64_t k0 = h->rows[(size_t)g * 32].voff;
+    const int64_t k0 = h->gvoff[g];
     int64_t k = k0;  // the group's block: rows in slot order
     for (int sl = 0; sl < 32; sl++) {
       const int s = g * 32 + sl;
@@ -966,6 +1004,8 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
   for (int k = 0; k < h->nl; k++) vmax8[k] = (uint8_t)h->vmax[k];
   // device
   int rc;
+  if ((rc = setup_node_lanes(h))) return rc;
+  if ((rc = upload(h, &h->d_nli, h->nli))) return rc;
   if ((rc = upload(h, &h->d_tiles, h->gtiles))) return rc;
   for (int b = 0; b < 2; b++) {
     if ((rc = dalloc(h, &h->d_code[b], h->gtiles.empty() ? 16 : h->gcells, 0xFF))) return rc;
@@ -982,6 +1022,7 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
   }
   if (h->ngroups > 0) {
     if ((rc = upload(h, &h->d_rows, h->rows))) return rc;
+    if ((rc = upload(h, &h->d_gvoff, h->gvoff))) return rc;
     CK(h, cudaMemcpyAsync(h->d_planes[0], planes.data(), planes.size() * 4, cudaMemcpyHostToDevice,
                           h->stream));
     CK(h, cudaMemcpyAsync(h->d_rvid[0], rvid.data(), rvid.size() * 4, cudaMemcpyHostToDevice,
@@ -1030,10 +1071,10 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
     std::vector<int32_t> head(pend_off.begin(), pend_off.begin() + h->nl);
     if ((rc = upload(h, &h->d_pend_head, head))) return rc;
   }
-  if ((rc = dalloc(h, &h->d_tail, h->nlanes, 0))) return rc;
+  if ((rc = dalloc(h, &h->d_tail, h->n_nli, 0))) return rc;
   if ((rc = dalloc(h, &h->d_entr, h->nlanes, 0))) return rc;
   if ((rc = dalloc(h, &h->d_head, h->nlanes, 0))) return rc;
-  if ((rc = dalloc(h, &h->d_ext, h->nlanes, 0))) return rc;
+  if ((rc = dalloc(h, &h->d_ext, h->n_nli, 0))) return rc;
   if ((rc = dalloc(h, &h->d_stats, (size_t)kHist * ST_N, 0))) return rc;
   if ((rc = dalloc(h, &h->d_work, h->nl, 0))) return rc;
   if ((rc = dalloc(h, &h->d_hash, 2, 0))) return rc;
@@ -1069,20 +1110,7 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
     const int rocc = std::max(1, occupancy_rows(h->rows_threads, h->rows_smem));
     h->rows_blocks = std::max(1, std::min((h->ngroups + wpb - 1) / wpb, rocc * nsm));
   }
-  {
-    std::vector<NodeLane> nlanes;
-    std::vector<int32_t> chunk_off;
-    std::vector<uint32_t> lsig;
-    h->node_warp = h->periodic < 0 && !(h->cfg.flags & (TS_FLAG_GENERAL | TS_FLAG_NODE_GENERAL)) &&
-                   build_node_lanes(h, nlanes, chunk_off, lsig);
-    if (h->node_warp) {
-      h->nchunks = (int32_t)chunk_off.size() - 1;
-      if ((rc = upload(h, &h->d_nlanes, nlanes))) return rc;
-      if ((rc = upload(h, &h->d_chunk_off, chunk_off))) return rc;
-      if ((rc = upload(h, &h->d_lane_sig, lsig))) return rc;
-    }
-    if (!h->node_sig.empty() && (rc = upload(h, &h->d_node_sig, h->node_sig))) return rc;
-  }
+  if (!h->node_sig.empty() && (rc = upload(h, &h->d_node_sig, h->node_sig))) return rc;
   // the nodes of this domain (nodes are never split)
   h->my_nodes.clear();
   for (int nd = 0; nd < h->nn; nd++)
@@ -1171,7 +1199,7 @@ static void phase_move(ts_sim *h, bool more, cudaEvent_t e0, cudaEvent_t e1) {
   const int mode = base_mode(h);
   if (h->n_xs > 0) unpack_strips(h);
   if (h->node_warp)
-    launch_node_warp(node_params(h, t), NodeWarpParams{h->d_lane_sig, h->d_nlanes, h->d_chunk_off, h->nchunks},
+    launch_node_warp(node_params(h, t), NodeWarpParams{h->d_lane_sig, h->d_nlanes, h->nchunks},
                      h->stream);
   else
     launch_node(node_params(h, t), h->stream);
@@ -1427,8 +1455,8 @@ static int download_tiles(ts_sim *h, int t0, int t1, std::vector<uint8_t> &code,
     // row tiles: planes and vid blocks of the covering groups; a row's list
     // starts at the prefix of the vehicle counts of the rows before it
     const int gr0 = s0 >> 5, gr1 = ((s1 - 1) >> 5) + 1;
-    const int64_t va = h->rows[(size_t)gr0 * 32].voff;
-    const int64_t vb = gr1 < h->ngroups ? h->rows[(size_t)gr1 * 32].voff : h->rvid_entries;
+    const int64_t va = h->gvoff[gr0];
+    const int64_t vb = gr1 < h->ngroups ? h->gvoff[gr1] : h->rvid_entries;
     std::vector<uint32_t> pl(group_plane_base(gr1) - group_plane_base(gr0));
     std::vector<int32_t> rv(vb - va);
     CK(h, cudaMemcpy(pl.data(), h->d_planes[h->rcur] + group_plane_base(gr0), pl.size() * 4,
@@ -1436,7 +1464,7 @@ static int download_tiles(ts_sim *h, int t0, int t1, std::vector<uint8_t> &code,
     CK(h, cudaMemcpy(rv.data(), h->d_rvid[h->rcur] + va, rv.size() * 4, cudaMemcpyDeviceToHost));
     std::vector<int64_t> roff((size_t)(gr1 - gr0) * 32);
     for (int g = gr0; g < gr1; g++) {
-      int64_t k = h->rows[(size_t)g * 32].voff - va;
+      int64_t k = h->gvoff[g] - va;
       for (int sl = 0; sl < 32; sl++) {
         roff[(size_t)(g - gr0) * 32 + sl] = k;
         const uint32_t *P = pl.data() + (group_plane_base(g) - group_plane_base(gr0)) + sl;

@@ -105,9 +105,9 @@ __host__ __device__ inline size_t group_plane_base(int64_t g) {
 }
 
 struct RowDesc {
-  int32_t voff;  // first entry of the group's vid block (multiple of 4)
+  int32_t nli;   // node-lane index of the row (tail record and node grant)
   int32_t link;
-  int32_t lg;    // global lane id
+  int32_t lg;    // global lane id (head occupancy and entrant record)
   uint8_t w;     // cells (0 = empty slot)
   uint8_t l, L;  // lane, lanes of the link
   uint8_t vk;    // vmax of the link
@@ -126,7 +126,11 @@ __host__ __device__ inline int rows_stage_words(int cap) {
 
 // Warp-cooperative node kernel: the incoming lanes of every node, in the
 // priority order (major class first, then link id, then lane; R9), packed
-// into chunks of <= 32 that never split a node.
+// into chunks of 32 entries that never split a node (unused entries have
+// lane_gid = -1).  The position of a lane in this array is its node-lane
+// index (nli): the tail record (written with S1) and the node grant `ext`
+// of the lane are stored at that index, so the node kernel reads and
+// writes them coalesced.
 struct __align__(16) NodeLane {
   int32_t lane_gid;
   int32_t out_base;  // first NodeOut entry of the node (its out-slots)
@@ -211,10 +215,11 @@ struct StepParams {
   const int32_t *pend_list;  // vids in (departure, vid) order
   int32_t *pend_head;
   // node interface
-  uint64_t *tail_rec;  // per lane, written with S1
+  const int32_t *nli;  // node-lane index of every global lane id
+  uint64_t *tail_rec;  // per node-lane index, written with S1
   uint8_t *head_occ;   // per lane, written with S1
-  const uint8_t *ext;  // per lane, from k_node
-  const uint64_t *entr;
+  const uint8_t *ext;  // per node-lane index, from k_node
+  const uint64_t *entr;  // per global lane id
   // outputs
   unsigned long long *stats;  // [kHist][ST_N]
   unsigned long long *link_work;
@@ -236,9 +241,9 @@ struct NodeParams {
   VehPos *vpos;
   const NodeOut *nodeout;  // [out_off[node] + slot]
   const uint32_t *node_sig;  // per node, phase-0 signal word (phase 1 derived); NULL = none
-  const uint64_t *tail_rec;
+  const uint64_t *tail_rec;  // by node-lane index (k_node: identity)
   const uint8_t *head_occ;
-  uint8_t *ext;
+  uint8_t *ext;              // by node-lane index (k_node: identity)
   uint64_t *entr;
   unsigned long long *stats;
 };
@@ -252,6 +257,7 @@ struct NodeParams {
 
 struct RowsParams {
   const RowDesc *rows;        // [ngroups * 32]
+  const int32_t *gvoff;       // first entry of each group's vid block (multiple of 4)
   const uint32_t *planes_in;  // S1(t) (fused) or S(t)
   uint32_t *planes_out;
   const int32_t *vid_in;      // row vid lists
@@ -274,9 +280,8 @@ __host__ __device__ inline bool sig_green(uint32_t s, int t) {
 }
 
 struct NodeWarpParams {
-  const uint32_t *sig;  // per lane (same order as lanes)
-  const NodeLane *lanes;
-  const int32_t *chunk_off;  // [nchunks + 1]
+  const uint32_t *sig;  // per lane (same order as lanes); NULL = no signals
+  const NodeLane *lanes;  // [32 * nchunks]
   int32_t nchunks;
 };
 

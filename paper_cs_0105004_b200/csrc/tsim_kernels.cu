@@ -238,7 +238,7 @@ __device__ void write_back(const StepParams &P, TileCtx &T, bool node_recs, int 
           rec |= (uint64_t)(uint32_t)T.vout[pf] | ((uint64_t)T.cout[pf] << 32) |
                  ((uint64_t)i << 40) | (1ull << 43);
         }
-        P.tail_rec[T.d.lane_gid + l] = rec;
+        P.tail_rec[P.nli[T.d.lane_gid + l]] = rec;
       }
       if (T.d.flags & kFirst)
         P.head_occ[T.d.lane_gid + l] = (uint8_t)(win_at(T.bout, l * T.S + T.HP) & 31u);
@@ -269,7 +269,7 @@ __device__ __forceinline__ void move_one(const StepParams &P, TileCtx &T, Acc &a
   if (m) g = __ffs(m) - 1;
   else if (lim == kGmax) g = kGmax;
   else if (slot == kSlotFinal) g = kGmax;  // R12: open end of the final link
-  else g = min(kGmax, lim + (int)P.ext[T.d.lane_gid + l]);  // node grant (H3)
+  else g = min(kGmax, lim + (int)P.ext[P.nli[T.d.lane_gid + l]]);  // node grant (H3)
   const int v3 = nasch_v3(v, Vk, g, (uint32_t)P.t, (uint32_t)vid, P.k0, P.k1, P.p32);
   int y = x + v3;
   if (periodic && y >= T.d.n) y -= T.d.n;
@@ -489,16 +489,16 @@ __device__ __forceinline__ Cand node_candidate(const NodeParams &P, uint64_t rec
   return c;
 }
 
-// the winner's grant: returns ext; writes the entrant record if it crosses
-__device__ __forceinline__ int node_grant(const NodeParams &P, const Cand &c, int vk,
-                                          uint32_t &crossings) {
-  const int E = min(ctz32((uint32_t)P.head_occ[c.tgt] | 0x20u), min(kGmax, c.n2));
+// the winner's grant: returns ext; writes the entrant record if it crosses.
+// head: occupancy of the first cells of the target lane; q: the winner's
+// route position record (one 16-byte record per vehicle)
+__device__ __forceinline__ int node_grant(const NodeParams &P, const Cand &c, int vk, uint8_t head,
+                                          const VehPos &q, uint32_t &crossings) {
+  const int E = min(ctz32((uint32_t)head | 0x20u), min(kGmax, c.n2));
   if (E == 0) return 0;
   const int v3 = nasch_v3(c.v, vk, min(kGmax, c.d + E), (uint32_t)P.t, (uint32_t)c.vid, P.k0,
                           P.k1, P.p32);
   if (v3 > c.d) {
-    // one 16-byte record per vehicle: its route position and end
-    const VehPos q = P.vpos[c.vid];
     const int nslot = (q.p + 2 < q.e) ? (int)P.rslot[q.p + 2] : kSlotFinal;
     P.vpos[c.vid].p = q.p + 1;
     const int y2 = v3 - c.d - 1;
@@ -524,37 +524,62 @@ __device__ __forceinline__ void node_flush(const NodeParams &P, uint32_t crossin
 
 // one thread per incoming lane; the lanes of a node are consecutive threads
 // in priority order, so the winner of a target lane is the lowest eligible
-// thread with that target
+// thread with that target.  Every warp resolves kNodeILP chunks at once
+// stage by stage (records, out-slot table, head occupancy and route
+// position, grant), so their dependent loads overlap instead of running
+// as one latency chain per chunk.
+#ifndef TS_NODE_ILP
+#define TS_NODE_ILP 1  // measured on 4a: 1 -> 31.5 us, 2 -> 35, 4 -> 39.6, 8 -> 49.6
+#endif
+constexpr int kNodeILP = TS_NODE_ILP;
 __global__ void __launch_bounds__(256) k_node_warp(const NodeParams P, const NodeWarpParams W) {
   __shared__ unsigned long long red[8];
   const int lane = threadIdx.x & 31;
-  const int nwarps_total = gridDim.x * (blockDim.x >> 5);
   const uint32_t gmask = (1u << P.G) - 1u;
   uint32_t crossings = 0;
-  for (int c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); c < W.nchunks;
-       c += nwarps_total) {
-    const int a = W.chunk_off[c], n = W.chunk_off[c + 1] - a;
-    const bool act = lane < n;
-    NodeLane e{0, 0, 0u, 0, 0, 1, (uint8_t)(64 + lane)};
-    uint64_t rec = 0;
-    if (act) {
-      e = W.lanes[a + lane];
-      rec = P.tail_rec[e.lane_gid];
-    }
-    const uint32_t nodemask = __match_any_sync(FULL, (int)e.first);
-    const bool busy = (__ballot_sync(FULL, act && e.major && (((uint32_t)(rec >> 44)) & gmask)) &
-                       nodemask) != 0u;
-    Cand cd{false, -1, 0, 0, 0, 0};
-    if (act) cd = node_candidate(P, rec, e.lane, e.out_base, e.tt, e.vk);
+  const int c0 = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * kNodeILP;
+  NodeLane e[kNodeILP];
+  uint64_t rec[kNodeILP];
+  uint32_t sg[kNodeILP];
+  bool act[kNodeILP];
+#pragma unroll
+  for (int k = 0; k < kNodeILP; k++) {  // stage 1: lane records of S1
+    const int c = min(c0 + k, W.nchunks - 1), i = 32 * c + lane;  // node-lane index
+    act[k] = c0 + k < W.nchunks;
+    e[k] = W.lanes[i];
+    rec[k] = P.tail_rec[i];
+    sg[k] = W.sig ? W.sig[i] : 0u;
+  }
+  Cand cd[kNodeILP];
+  bool win[kNodeILP];
+#pragma unroll
+  for (int k = 0; k < kNodeILP; k++) {  // stage 2: candidates and winners
+    const bool a = act[k] && e[k].lane_gid >= 0;
+    if (!a) rec[k] = 0;
+    const uint32_t nodemask = __match_any_sync(FULL, a ? (int)e[k].first : 64 + lane);
+    const bool busy =
+        (__ballot_sync(FULL, a && e[k].major && (((uint32_t)(rec[k] >> 44)) & gmask)) & nodemask) != 0u;
+    cd[k] = Cand{false, -1, 0, 0, 0, 0};
+    if (a) cd[k] = node_candidate(P, rec[k], e[k].lane, e[k].out_base, e[k].tt, e[k].vk);
     // signalized node (R23): red approaches have the virtual blocker, green
     // ones need no gap acceptance; otherwise priority + gap acceptance (R9)
-    const uint32_t sg = act ? W.sig[a + lane] : 0u;
-    const bool eligible = cd.cand && ((sg >> 31) ? sig_green(sg, P.t) : (e.major || !busy));
-    const int key = eligible ? cd.tgt : -1 - lane;
-    const uint32_t grp = __match_any_sync(FULL, key);
+    const bool eligible =
+        cd[k].cand && ((sg[k] >> 31) ? sig_green(sg[k], P.t) : (e[k].major || !busy));
+    const uint32_t grp = __match_any_sync(FULL, eligible ? cd[k].tgt : -1 - lane);
+    win[k] = eligible && (__ffs(grp) - 1) == lane;
+  }
+  uint8_t head[kNodeILP];
+  VehPos q[kNodeILP];
+#pragma unroll
+  for (int k = 0; k < kNodeILP; k++) {  // stage 3: target head and route position
+    head[k] = win[k] ? P.head_occ[cd[k].tgt] : (uint8_t)0;
+    q[k] = win[k] ? P.vpos[cd[k].vid] : VehPos{0, 0};
+  }
+#pragma unroll
+  for (int k = 0; k < kNodeILP; k++) {  // stage 4: grants
     int ext = 0;
-    if (eligible && (__ffs(grp) - 1) == lane) ext = node_grant(P, cd, e.vk, crossings);
-    if (act) P.ext[e.lane_gid] = (uint8_t)ext;
+    if (win[k]) ext = node_grant(P, cd[k], e[k].vk, head[k], q[k], crossings);
+    if (act[k]) P.ext[32 * (c0 + k) + lane] = (uint8_t)ext;
   }
   node_flush(P, crossings, red);
 }
@@ -609,7 +634,8 @@ __global__ void __launch_bounds__(128) k_node(const NodeParams P) {
           for (int q = 0; q < nclaimed; q++) taken |= claimed[q] == bit;
           if (taken) continue;
           if (nclaimed < kMaxClaim) claimed[nclaimed++] = bit;
-          P.ext[lg + l] = (uint8_t)node_grant(P, cd, P.vmax_link[j], crossings);
+          P.ext[lg + l] = (uint8_t)node_grant(P, cd, P.vmax_link[j], P.head_occ[cd.tgt],
+                                              P.vpos[cd.vid], crossings);
         }
       }
     }
@@ -652,7 +678,7 @@ void launch_node(const NodeParams &p, void *stream) {
 }
 void launch_node_warp(const NodeParams &p, const NodeWarpParams &w, void *stream) {
   if (w.nchunks <= 0) return;
-  const int blocks = (w.nchunks + 7) / 8;
+  const int blocks = (w.nchunks + 8 * kNodeILP - 1) / (8 * kNodeILP);
   k_node_warp<<<blocks, 256, 0, (cudaStream_t)stream>>>(p, w);
 }
 void launch_hash(const StepParams &p, int blocks, int threads, int smem, void *stream,

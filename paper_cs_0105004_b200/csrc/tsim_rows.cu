@@ -195,7 +195,19 @@ static __device__ __noinline__ uint32_t zone_lc(uint32_t zc, int c0, int w, int 
   return lv;
 }
 
-__global__ void __launch_bounds__(128, 5) k_rows(const StepParams P, const RowsParams R) {
+#ifndef TS_ROWS_MINB
+#define TS_ROWS_MINB 5  // resident 128-thread blocks per SM (register budget)
+#endif
+#ifndef TS_ROWS_PF
+#define TS_ROWS_PF 0  // prefetch the next group's state into L2 (measured: no gain)
+#endif
+
+// bulk prefetch of [p, p + bytes) into L2 (p 16-byte aligned, bytes % 16 == 0)
+__device__ __forceinline__ void prefetch_l2(const void *p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+__global__ void __launch_bounds__(128, TS_ROWS_MINB) k_rows(const StepParams P, const RowsParams R) {
   __shared__ unsigned long long red[4 * 8];
   extern __shared__ __align__(16) int32_t stage[];  // per warp: vid block in, vid block out
   const int lane = threadIdx.x & 31;
@@ -212,24 +224,41 @@ __global__ void __launch_bounds__(128, 5) k_rows(const StepParams P, const RowsP
 
   // groups are handed out dynamically (one atomic per warp and group): no
   // warp idles while another still has a queue of groups
+  // The next group is fetched one iteration ahead and its planes, row
+  // descriptors and vid block are prefetched into L2 while this one runs.
   (void)nwarps;
-  for (;;) {
+  auto grab = [&]() {
     int g = 0;
     if (lane == 0) g = (int)(atomicAdd(R.gctr, 1ull) - R.gbase);
-    g = __shfl_sync(FULL, g, 0);
+    return __shfl_sync(FULL, g, 0);
+  };
+  int g_next = grab();
+  for (;;) {
+    const int g = g_next;
     if (g >= R.ngroups) break;
+    g_next = grab();
+    int pf_voff = 0, pf_cnt = 0;  // the next group's vid block (prefetched later)
+    if (TS_ROWS_PF && g_next < R.ngroups) {
+      if (lane == 0) prefetch_l2(R.planes_in + group_plane_base(g_next), kStatePlanes * kRowWords * 128);
+      if (lane == 1) prefetch_l2(R.rows + (size_t)g_next * 32, 32 * sizeof(RowDesc));
+      if (lane == 2) {
+        pf_voff = __ldg(&R.gvoff[g_next]);
+        pf_cnt = __ldg(&R.gcnt_in[g_next]);
+      }
+    }
     __syncwarp();  // the previous group's staged blocks are no longer in use
     const RowDesc rd = R.rows[(size_t)g * 32 + lane];
     const int w = rd.w, l = rd.l, L = rd.L, link = rd.link, lg = rd.lg, vk = rd.vk;
+    const int voff = R.gvoff[g];
     // the group's vid block (its vehicle count was written with it) is
     // staged in shared memory when it fits, loaded together with the planes
     const int tot_in = R.gcnt_in[g];
     const bool staged = tot_in <= R.cap;
-    if (staged) warp_load(s_in, R.vid_in + rd.voff, tot_in, lane);
+    if (staged) warp_load(s_in, R.vid_in + voff, tot_in, lane);
     // per-row gathers of this step, issued early: node grant, entrant,
     // pending trips
     const bool do_move0 = (P.mode & kModeMove) != 0 && w > 0;
-    const int ext_lg = do_move0 ? (int)P.ext[lg] : 0;
+    const int ext_lg = do_move0 ? (int)P.ext[rd.nli] : 0;
     const uint64_t ent_rec = do_move0 ? P.entr[lg] : 0ull;
     const bool may_inject = (P.mode & kModeInject) && w > 0 && l == 0 &&
                             P.pend_off[link + 1] > P.pend_head[link];
@@ -251,7 +280,7 @@ __global__ void __launch_bounds__(128, 5) k_rows(const StepParams P, const RowsP
     int tot_chk;
     const int in_off = warp_scan(nin, lane, &tot_chk);
     if (staged) __syncwarp();
-    const int32_t *vin = (staged ? (const int32_t *)s_in : R.vid_in + rd.voff) + in_off;
+    const int32_t *vin = (staged ? (const int32_t *)s_in : R.vid_in + voff) + in_off;
     acc.work += nin;
     if ((P.mode & kModeWork) && P.link_work && nin)
       atomicAdd(P.link_work + link, (unsigned long long)nin);
@@ -321,7 +350,7 @@ __global__ void __launch_bounds__(128, 5) k_rows(const StepParams P, const RowsP
         int mtot;
         const int mc = popc_row(U1);
         const int moff = warp_scan(mc, lane, &mtot);
-        const int32_t *vbase = staged ? (const int32_t *)s_in : R.vid_in + rd.voff;
+        const int32_t *vbase = staged ? (const int32_t *)s_in : R.vid_in + voff;
         // mover list entries: block offset << 12 | row slot << 7 | cell, in
         // chunks of the staging capacity (one chunk unless the group is huge)
         int32_t *mlist = s_out;  // free until the output phase
@@ -357,6 +386,8 @@ __global__ void __launch_bounds__(128, 5) k_rows(const StepParams P, const RowsP
         for (int i = 0; i < NW; i++) Bm[i] = bw[lane * NW + i];
         __syncwarp();
       }
+      if (TS_ROWS_PF && lane == 2 && pf_cnt > 0)
+        prefetch_l2(R.vid_in + pf_voff, (uint32_t)((pf_cnt + 3) & ~3) * 4u);
       // ---- hop, word by word: D_k = vehicles moving exactly k (v3 = k);
       //      those passing the row end leave it (LR); O' = OR_k D_k << k with
       //      the velocity and class bits carried along
@@ -571,7 +602,7 @@ __global__ void __launch_bounds__(128, 5) k_rows(const StepParams P, const RowsP
     int tot_out;
     const int out_off = warp_scan(nfin, lane, &tot_out);
     const bool ostaged = tot_out <= R.cap;
-    int32_t *obase = ostaged ? s_out : R.vid_out + rd.voff;
+    int32_t *obase = ostaged ? s_out : R.vid_out + voff;
     int32_t *vout = obase + out_off;
     const bool moved_lc = any_row(LV) || any_row(AR);
     const bool general = moved_lc || injected || hash;
@@ -618,7 +649,7 @@ __global__ void __launch_bounds__(128, 5) k_rows(const StepParams P, const RowsP
       mItem[lane] = ioff;
       if (lane == 0) mItem[32] = itot;
       __syncwarp();
-      const int32_t *ibase = staged ? (const int32_t *)s_in : R.vid_in + rd.voff;
+      const int32_t *ibase = staged ? (const int32_t *)s_in : R.vid_in + voff;
       for (int J = lane; J < itot; J += 32) {
         // the row of item J: the last row whose first item is <= J
         int r0 = 0;
@@ -692,7 +723,7 @@ __global__ void __launch_bounds__(128, 5) k_rows(const StepParams P, const RowsP
     }
     __syncwarp();
     const uint32_t efin = nfin > 0 ? (uint32_t)vout[nfin - 1] : 0u;  // final front vehicle
-    if (ostaged) warp_store(R.vid_out + rd.voff, s_out, tot_out, lane);
+    if (ostaged) warp_store(R.vid_out + voff, s_out, tot_out, lane);
     if (lane == 0) R.gcnt_out[g] = tot_out;
     // ---- node records of the output S1 (read by k_node_warp, H3)
     if (lc && w > 0) {
@@ -708,7 +739,7 @@ __global__ void __launch_bounds__(128, 5) k_rows(const StepParams P, const RowsP
         rec |= (uint64_t)(efin & kVidMask) | ((uint64_t)code << 32) |
                ((uint64_t)(w - 1 - xf) << 40) | (1ull << 43);
       }
-      P.tail_rec[lg] = rec;
+      P.tail_rec[rd.nli] = rec;
       P.head_occ[lg] = (uint8_t)(FO[0] & lowm(nb));
     }
   }
@@ -730,7 +761,7 @@ __global__ void __launch_bounds__(128) k_rows_hash(const RowsParams R, unsigned 
   const int off = warp_scan(n, lane, &tot);
   if (act) {
     const RowDesc rd = R.rows[gid];
-    const int32_t *vl = R.vid_in + rd.voff + off;
+    const int32_t *vl = R.vid_in + R.gvoff[g] + off;
     int k = 0;
     for (int i = 0; i < NW; i++) {
       uint32_t m = pl[i * 32];

@@ -11,7 +11,9 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_SO = os.path.join(_HERE, "libtsim.so")
+# TSIM_LIB selects another in-tree build of the same sources (tuning
+# variants built by tools/variants.py); the default is the in-tree library
+_SO = os.environ.get("TSIM_LIB") or os.path.join(_HERE, "libtsim.so")
 
 FLAG_FUSED, FLAG_HASH, FLAG_LINK_WORK, FLAG_GRAPH, FLAG_GENERAL = 1, 2, 4, 8, 16
 PENDING, ACTIVE, ARRIVED, ABSENT = 0, 1, 2, 3
