@@ -207,6 +207,9 @@ __device__ __forceinline__ void prefetch_l2(const void *p, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
+// MODE = the uniform mode bits kModeMove | kModeLC | kModeHash of the launch
+// (specialised so the hot fused instantiation carries no dead paths)
+template <int MODE>
 __global__ void __launch_bounds__(128, TS_ROWS_MINB) k_rows(const StepParams P, const RowsParams R) {
   __shared__ unsigned long long red[4 * 8];
   extern __shared__ __align__(16) int32_t stage[];  // per warp: vid block in, vid block out
@@ -214,9 +217,9 @@ __global__ void __launch_bounds__(128, TS_ROWS_MINB) k_rows(const StepParams P, 
   int32_t *s_in = stage + (threadIdx.x >> 5) * rows_stage_words(R.cap);
   int32_t *s_out = s_in + R.cap;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
-  const bool do_move = (P.mode & kModeMove) != 0;
-  const bool hash = (P.mode & kModeHash) != 0;
-  const bool lc = (P.mode & kModeLC) != 0;
+  constexpr bool do_move = (MODE & kModeMove) != 0;
+  constexpr bool hash = (MODE & kModeHash) != 0;
+  constexpr bool lc = (MODE & kModeLC) != 0;
   const int lct = do_move ? P.t + 1 : P.t;  // time of the lane-change sub-step
   const int dir = (lct & 1) ? -1 : +1;      // R4
   Acc acc = {};
@@ -257,7 +260,7 @@ __global__ void __launch_bounds__(128, TS_ROWS_MINB) k_rows(const StepParams P, 
     if (staged) warp_load(s_in, R.vid_in + voff, tot_in, lane);
     // per-row gathers of this step, issued early: node grant, entrant,
     // pending trips
-    const bool do_move0 = (P.mode & kModeMove) != 0 && w > 0;
+    const bool do_move0 = do_move && w > 0;
     const int ext_lg = do_move0 ? (int)P.ext[rd.nli] : 0;
     const uint64_t ent_rec = do_move0 ? P.entr[lg] : 0ull;
     const bool may_inject = (P.mode & kModeInject) && w > 0 && l == 0 &&
@@ -790,7 +793,14 @@ __global__ void __launch_bounds__(128) k_rows_hash(const RowsParams R, unsigned 
 
 void launch_rows(const StepParams &p, const RowsParams &r, int blocks, int threads, int smem,
                  void *stream) {
-  k_rows<<<blocks, threads, smem, (cudaStream_t)stream>>>(p, r);
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (p.mode & (kModeMove | kModeLC | kModeHash)) {
+#define TS_ROWS_CASE(m) \
+  case m: k_rows<m><<<blocks, threads, smem, st>>>(p, r); break;
+    TS_ROWS_CASE(0) TS_ROWS_CASE(1) TS_ROWS_CASE(4) TS_ROWS_CASE(5)
+    TS_ROWS_CASE(8) TS_ROWS_CASE(9) TS_ROWS_CASE(12) TS_ROWS_CASE(13)
+#undef TS_ROWS_CASE
+  }
 }
 void launch_rows_hash(const StepParams &p, const RowsParams &r, void *stream,
                       unsigned long long *out) {
@@ -805,11 +815,21 @@ cudaError_t set_rows_smem(int bytes) {  // only ever raised (see set_smem_attrs)
   dev &= 63;
   if (bytes <= current[dev]) return cudaSuccess;
   current[dev] = bytes;
-  return cudaFuncSetAttribute(k_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cudaError_t e = cudaSuccess;
+  for (cudaError_t x : {cudaFuncSetAttribute(k_rows<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
+                        cudaFuncSetAttribute(k_rows<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
+                        cudaFuncSetAttribute(k_rows<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
+                        cudaFuncSetAttribute(k_rows<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
+                        cudaFuncSetAttribute(k_rows<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
+                        cudaFuncSetAttribute(k_rows<9>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
+                        cudaFuncSetAttribute(k_rows<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
+                        cudaFuncSetAttribute(k_rows<13>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes)})
+    if (x != cudaSuccess) e = x;
+  return e;
 }
 int occupancy_rows(int threads, int smem) {
   int nb = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_rows, threads, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_rows<kModeMove | kModeLC>, threads, smem);
   return nb;
 }
 
