@@ -90,6 +90,19 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
+def ncu_traffic():
+    """DRAM bytes per launch of k_rows from the committed ncu --set full
+    capture (profiles/traffic_k_rows.json, written by tools/ncu_traffic.py)."""
+    p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "traffic_k_rows.json")
+    try:
+        with open(p) as f:
+            t = json.load(f)
+        return {"bytes": t["traffic_bytes_per_launch"],
+                "source": f"ncu --set full, {t['report']}: {t['note']}"}
+    except (OSError, KeyError, ValueError):
+        return {"bytes": None, "source": None}
+
+
 def workload(name):
     scn = scenarios.config(name)
     return scn
@@ -157,6 +170,7 @@ def bench_tsim(args):
     if world > 1:
         return bench_multi(args)
     hbm_peak, peak_src = measured_peaks()
+    traffic = ncu_traffic()
     t_gen = time.perf_counter()
     scn = workload(args.config)
     t_gen = time.perf_counter() - t_gen
@@ -185,7 +199,7 @@ def bench_tsim(args):
     updates = int(np.sum(hist["active"][:args.steps]))
     value = updates / (ms_total / 1e3)
     rtr = args.steps / (ms_total / 1e3)
-    # roofline of the dominant kernel (k_step): algorithmic bytes per launch
+    # roofline of the dominant kernel (k_rows): algorithmic bytes per launch
     # = 2 B x lane-cells (codes in + out) + 8 B x active vehicles (vid in +
     # out) + 12 B x node crossers
     lane_cells = tot["lane_cells"]
@@ -206,7 +220,8 @@ def bench_tsim(args):
                    "parallelism": "1 GPU, 1 domain", "flags": "fused" + ("+hash" if args.hash else "")},
         "real_time_ratio": rtr,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": achieved / hbm_peak, "traffic": None, "kernel": "k_step",
+                     "frac": achieved / hbm_peak, "traffic": traffic["bytes"],
+                     "traffic_source": traffic["source"], "kernel": "k_rows",
                      "alg_bytes_per_launch": alg_per_launch, "kernel_ms": mv_ms,
                      "kernel_share": timing["move_ms"] / ms_total, "peak_source": peak_src},
         "e2e": {"value": upd_all / e2e_wall, "unit": "vehicle-updates/s",
