@@ -119,7 +119,7 @@ static_assert(sizeof(RowDesc) == 16, "RowDesc must be 16 bytes");
 // vehicles that draw), then an aux area: the brake bits of the 32 rows
 // during the draws, the masks and list offsets of the rows the lane change
 // touched during the list rebuild
-constexpr int kRowsAuxWords = 4 * 32 * kRowWords + 5 * 32 + 4;
+constexpr int kRowsAuxWords = 4 * 32 * kRowWords + 5 * 32 + 4 + 64;
 __host__ __device__ inline int rows_stage_words(int cap) {
   return 2 * cap + kRowsAuxWords;  // cap is a multiple of 4: 16-byte aligned
 }

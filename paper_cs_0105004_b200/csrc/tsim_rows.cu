@@ -127,6 +127,36 @@ __device__ __forceinline__ void warp_load(int32_t *dst, const int32_t *gsrc, int
     reinterpret_cast<int4 *>(dst)[i] = __ldcs(reinterpret_cast<const int4 *>(gsrc) + i);
   for (int i = 4 * n4 + lane; i < n; i += 32) dst[i] = __ldcs(gsrc + i);
 }
+// asynchronous variant of warp_load (cp.async, no register round trip):
+// 16-byte copies of the first n & ~3 entries, the tail entry by entry;
+// completes at cp_async_wait()
+__device__ __forceinline__ void warp_load_async(int32_t *dst, const int32_t *gsrc, int n, int lane) {
+  const int n4 = n >> 2;
+  for (int i = lane; i < n4; i += 32) {
+    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst + 4 * i);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gsrc + 4 * i) : "memory");
+  }
+  for (int i = 4 * n4 + lane; i < n; i += 32) {
+    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst + i);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(gsrc + i) : "memory");
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+// one-lane bulk (TMA) store of n entries of shared memory to global memory;
+// both 16-byte aligned, the byte count rounded up to 16 (the destination
+// block has room: group capacities are multiples of 4 entries)
+__device__ __forceinline__ void bulk_store(int32_t *gdst, const int32_t *src, int n) {
+  const uint32_t sa = (uint32_t)__cvta_generic_to_shared(src);
+  const uint32_t bytes = (uint32_t)((n + 3) & ~3) * 4u;
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(sa),
+               "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+// the bulk stores of this thread have finished reading shared memory
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
 __device__ __forceinline__ void warp_store(int32_t *gdst, const int32_t *src, int n, int lane) {
   const int n4 = n >> 2;
   for (int i = lane; i < n4; i += 32)
@@ -198,6 +228,9 @@ static __device__ __noinline__ uint32_t zone_lc(uint32_t zc, int c0, int w, int 
 #ifndef TS_ROWS_MINB
 #define TS_ROWS_MINB 5  // resident 128-thread blocks per SM (register budget)
 #endif
+#ifndef TS_ROWS_ASYNC
+#define TS_ROWS_ASYNC 1  // vid blocks: cp.async in, bulk (TMA) store out
+#endif
 #ifndef TS_ROWS_PF
 #define TS_ROWS_PF 0  // prefetch the next group's state into L2 (measured: no gain)
 #endif
@@ -249,6 +282,7 @@ __global__ void __launch_bounds__(128, TS_ROWS_MINB) k_rows(const StepParams P, 
         pf_cnt = __ldg(&R.gcnt_in[g_next]);
       }
     }
+    if (TS_ROWS_ASYNC && lane == 0) bulk_wait_read();  // the previous group's output block
     __syncwarp();  // the previous group's staged blocks are no longer in use
     const RowDesc rd = R.rows[(size_t)g * 32 + lane];
     const int w = rd.w, l = rd.l, L = rd.L, link = rd.link, lg = rd.lg, vk = rd.vk;
@@ -257,7 +291,10 @@ __global__ void __launch_bounds__(128, TS_ROWS_MINB) k_rows(const StepParams P, 
     // staged in shared memory when it fits, loaded together with the planes
     const int tot_in = R.gcnt_in[g];
     const bool staged = tot_in <= R.cap;
-    if (staged) warp_load(s_in, R.vid_in + voff, tot_in, lane);
+    if (staged) {
+      if (TS_ROWS_ASYNC) warp_load_async(s_in, R.vid_in + voff, tot_in, lane);
+      else warp_load(s_in, R.vid_in + voff, tot_in, lane);
+    }
     // per-row gathers of this step, issued early: node grant, entrant,
     // pending trips
     const bool do_move0 = do_move && w > 0;
@@ -282,7 +319,10 @@ __global__ void __launch_bounds__(128, TS_ROWS_MINB) k_rows(const StepParams P, 
     const int nin = popc_row(O);
     int tot_chk;
     const int in_off = warp_scan(nin, lane, &tot_chk);
-    if (staged) __syncwarp();
+    if (staged) {
+      if (TS_ROWS_ASYNC) cp_async_wait();
+      __syncwarp();
+    }
     const int32_t *vin = (staged ? (const int32_t *)s_in : R.vid_in + voff) + in_off;
     acc.work += nin;
     if ((P.mode & kModeWork) && P.link_work && nin)
@@ -636,12 +676,28 @@ __global__ void __launch_bounds__(128, TS_ROWS_MINB) k_rows(const StepParams P, 
                *rLV = rFO + 32 * NW, *rIN = rLV + 32 * NW;
       int32_t *mInOff = aux + 4 * 32 * NW, *mOutOff = mInOff + 32, *mEnt = mOutOff + 32,
               *mEntE = mEnt + 32, *mItem = mEntE + 32;  // mItem: 33 entries
+      // per row: popcount prefixes of the OO / FO words (bytes 1..3: words 0,
+      // 0-1, 0-2), so an item finds its word and its rank without loops
+      uint32_t *pOO = reinterpret_cast<uint32_t *>(mItem + 36), *pFO = pOO + 32;
+      const bool ginj = __any_sync(FULL, injected);
+      {
+        uint32_t po = 0u, pf = 0u;
+        int so = 0, sf = 0;
 #pragma unroll
-      for (int i = 0; i < NW; i++) {
-        rOO[lane * NW + i] = OO[i];
-        rFO[lane * NW + i] = FO[i];
-        rLV[lane * NW + i] = LV[i];
-        rIN[lane * NW + i] = INJ[i];
+        for (int i = 0; i < NW; i++) {
+          rOO[lane * NW + i] = OO[i];
+          rFO[lane * NW + i] = FO[i];
+          rLV[lane * NW + i] = LV[i];
+          if (ginj) rIN[lane * NW + i] = INJ[i];
+          if (i > 0) {
+            po |= (uint32_t)so << (8 * i);
+            pf |= (uint32_t)sf << (8 * i);
+          }
+          so += __popc(OO[i]);
+          sf += __popc(FO[i]);
+        }
+        pOO[lane] = po;
+        pFO[lane] = pf;
       }
       mInOff[lane] = in_off;
       mOutOff[lane] = out_off;
@@ -661,23 +717,11 @@ __global__ void __launch_bounds__(128, TS_ROWS_MINB) k_rows(const StepParams P, 
           if (mItem[r0 + st] <= J) r0 += st;
         const int rr = J - mItem[r0];  // rank of the vehicle in the row's OO
         // the word holding set bit number rr, and the rank inside it
-        uint32_t wsel = 0u;
-        int c = 0, k2 = rr;
-        bool found = false;
-#pragma unroll
-        for (int i = 0; i < NW; i++) {
-          const uint32_t wv = rOO[r0 * NW + i];
-          const int pc = __popc(wv);
-          if (!found) {
-            if (k2 < pc) {
-              wsel = wv;
-              c = 32 * i;
-              found = true;
-            } else {
-              k2 -= pc;
-            }
-          }
-        }
+        const uint32_t po = pOO[r0];
+        const int p1 = (int)((po >> 8) & 0xFF), p2 = (int)((po >> 16) & 0xFF), p3 = (int)(po >> 24);
+        const int wi = (rr >= p1) + (rr >= p2) + (rr >= p3);
+        uint32_t wsel = rOO[r0 * NW + wi];
+        int c = 32 * wi, k2 = rr - (int)((po >> (8 * wi)) & 0xFF);
         {  // select bit k2 of wsel by popcount halving
           uint32_t m = wsel;
           int pos = 0, cnt = __popc(m & 0xFFFFu);
@@ -692,21 +736,23 @@ __global__ void __launch_bounds__(128, TS_ROWS_MINB) k_rows(const StepParams P, 
         }
         const int ci = c >> 5;
         const uint32_t bit = 1u << (c & 31), lowb = bit - 1u;
-        const uint32_t inj_w = rIN[r0 * NW + ci];
+        const uint32_t inj_w = ginj ? rIN[r0 * NW + ci] : 0u;
         uint32_t e;
         if (c == mEnt[r0]) {
           e = (uint32_t)mEntE[r0];
         } else if (inj_w & bit) {
           e = (uint32_t)R.inj_scratch[((size_t)g * 32 + r0) * kRowMaxCells + c];
         } else {
-          int ninj = __popc(inj_w & lowb);
-          for (int i = 0; i < ci; i++) ninj += __popc(rIN[r0 * NW + i]);
+          int ninj = 0;
+          if (ginj) {
+            ninj = __popc(inj_w & lowb);
+            for (int i = 0; i < ci; i++) ninj += __popc(rIN[r0 * NW + i]);
+          }
           const int me = (mEnt[r0] >= 0 && mEnt[r0] < c) ? 1 : 0;
           e = (uint32_t)ibase[mInOff[r0] + rr - me - ninj];
         }
         const int dst = (rLV[r0 * NW + ci] & bit) ? r0 + dir : r0;
-        int rank = __popc(rFO[dst * NW + ci] & lowb);
-        for (int i = 0; i < ci; i++) rank += __popc(rFO[dst * NW + i]);
+        const int rank = __popc(rFO[dst * NW + ci] & lowb) + (int)((pFO[dst] >> (8 * ci)) & 0xFF);
         obase[mOutOff[dst] + rank] = (int32_t)e;
       }
       if (hash && general) {  // state hash of S(t+1), before its lane change (tests)
@@ -724,9 +770,17 @@ __global__ void __launch_bounds__(128, TS_ROWS_MINB) k_rows(const StepParams P, 
       }
       (void)gmask;
     }
+    // the output block's shared-memory writes become visible to the bulk copy
+    if (TS_ROWS_ASYNC) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncwarp();
     const uint32_t efin = nfin > 0 ? (uint32_t)vout[nfin - 1] : 0u;  // final front vehicle
-    if (ostaged) warp_store(R.vid_out + voff, s_out, tot_out, lane);
+    if (ostaged) {
+      if (TS_ROWS_ASYNC) {
+        if (lane == 0 && tot_out > 0) bulk_store(R.vid_out + voff, s_out, tot_out);
+      } else {
+        warp_store(R.vid_out + voff, s_out, tot_out, lane);
+      }
+    }
     if (lane == 0) R.gcnt_out[g] = tot_out;
     // ---- node records of the output S1 (read by k_node_warp, H3)
     if (lc && w > 0) {
@@ -746,6 +800,7 @@ __global__ void __launch_bounds__(128, TS_ROWS_MINB) k_rows(const StepParams P, 
       P.head_occ[lg] = (uint8_t)(FO[0] & lowm(nb));
     }
   }
+  if (TS_ROWS_ASYNC && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   flush_acc(P, acc, P.t + 1, red);
   if (lc) flush_acc(P, acc_next, lct + 1, red);
 }

@@ -23,7 +23,7 @@ for ln in dis:
     if m and m.group(1).endswith('tsim_rows.cu'):
         last = int(m.group(2))
     m = re.search(r'/\*([0-9a-f]{4,})\*/', ln)
-    if m and fn and 'k_rowsENS' in fn:
+    if m and fn and 'k_rowsILi5E' in fn:
         amap[int(m.group(1), 16)] = last
 src = open(f'{sdir}/tsim_rows.cu').read().split('\n')
 k0 = next(i for i, l in enumerate(src) if 'k_rows(const StepParams' in l) + 1
