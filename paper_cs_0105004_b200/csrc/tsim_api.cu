@@ -110,6 +110,9 @@ struct ts_sim {
   std::vector<int32_t> nli;   // node-lane index of every global lane id
   int64_t n_nli = 0;          // size of the node-lane indexed arrays
   int32_t *d_nli = nullptr;
+  std::vector<int32_t> nlo;   // node-out-lane index of every global lane id
+  int64_t n_nlo = 0;          // size of the node-out-lane indexed arrays
+  int32_t *d_nlo = nullptr;
   uint64_t p32 = 0;
   // device
   TileDesc *d_tiles = nullptr;
@@ -720,8 +723,31 @@ static int setup_node_lanes(ts_sim *h) {
     h->n_nli = std::max<int64_t>(h->nlanes, 1);
     for (int i = 0; i < h->nlanes; i++) h->nli[i] = i;
   }
+  // node-out-lane indices (head occupancy, entrant records): the outgoing
+  // lanes of every node of this domain contiguous, in node order, so the
+  // node kernel's target lookups stay within a few sectors per node
+  h->nlo.assign(h->nlanes, 0);
+  if (h->node_warp) {
+    int32_t cnt = 0;
+    std::vector<int32_t> map(h->nlanes, -1);
+    for (int nd = 0; nd < h->nn; nd++) {
+      if (h->dom_of_node[nd] != h->dom_me) continue;
+      for (int i = h->out_off[nd]; i < h->out_off[nd + 1]; i++) {
+        const int k = h->out_list[i];
+        for (int l = 0; l < h->lanes[k]; l++) map[h->lgid[k] + l] = cnt++;
+      }
+    }
+    h->n_nlo = (int64_t)cnt + 1;
+    for (int i = 0; i < h->nlanes; i++) h->nlo[i] = map[i] >= 0 ? map[i] : cnt;
+  } else {
+    h->n_nlo = std::max<int64_t>(h->nlanes, 1);
+    for (int i = 0; i < h->nlanes; i++) h->nlo[i] = i;
+  }
   for (RowDesc &r : h->rows)
-    if (r.w > 0) r.nli = h->nli[r.lg];
+    if (r.w > 0) {
+      r.nli = h->nli[r.lg];
+      r.lg = h->nlo[r.lg];
+    }
   return 0;
 }
 
@@ -771,6 +797,7 @@ static StepParams step_params(ts_sim *h, int t, int mode) {
   P.pend_list = h->d_pend_list;
   P.pend_head = h->d_pend_head;
   P.nli = h->d_nli;
+  P.nlo = h->d_nlo;
   P.tail_rec = h->d_tail;
   P.head_occ = h->d_head;
   P.ext = h->d_ext;
@@ -1006,6 +1033,7 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
   int rc;
   if ((rc = setup_node_lanes(h))) return rc;
   if ((rc = upload(h, &h->d_nli, h->nli))) return rc;
+  if ((rc = upload(h, &h->d_nlo, h->nlo))) return rc;
   if ((rc = upload(h, &h->d_tiles, h->gtiles))) return rc;
   for (int b = 0; b < 2; b++) {
     if ((rc = dalloc(h, &h->d_code[b], h->gtiles.empty() ? 16 : h->gcells, 0xFF))) return rc;
@@ -1052,7 +1080,8 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
     std::vector<NodeOut> nodeout(h->out_list.size());
     for (size_t i = 0; i < h->out_list.size(); i++) {
       const int k = h->out_list[i];
-      nodeout[i] = NodeOut{h->lgid[k], (int16_t)h->lanes[k], (int16_t)std::min(h->ncell[k], 32767)};
+      nodeout[i] = NodeOut{h->nlo[h->lgid[k]], (int16_t)h->lanes[k],
+                           (int16_t)std::min(h->ncell[k], 32767)};
     }
     if ((rc = upload(h, &h->d_nodeout, nodeout))) return rc;
   }
@@ -1072,8 +1101,8 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
     if ((rc = upload(h, &h->d_pend_head, head))) return rc;
   }
   if ((rc = dalloc(h, &h->d_tail, h->n_nli, 0))) return rc;
-  if ((rc = dalloc(h, &h->d_entr, h->nlanes, 0))) return rc;
-  if ((rc = dalloc(h, &h->d_head, h->nlanes, 0))) return rc;
+  if ((rc = dalloc(h, &h->d_entr, h->n_nlo, 0))) return rc;
+  if ((rc = dalloc(h, &h->d_head, h->n_nlo, 0))) return rc;
   if ((rc = dalloc(h, &h->d_ext, h->n_nli, 0))) return rc;
   if ((rc = dalloc(h, &h->d_stats, (size_t)kHist * ST_N, 0))) return rc;
   if ((rc = dalloc(h, &h->d_work, h->nl, 0))) return rc;

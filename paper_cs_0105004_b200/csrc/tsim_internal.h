@@ -107,7 +107,7 @@ __host__ __device__ inline size_t group_plane_base(int64_t g) {
 struct RowDesc {
   int32_t nli;   // node-lane index of the row (tail record and node grant)
   int32_t link;
-  int32_t lg;    // global lane id (head occupancy and entrant record)
+  int32_t lg;    // node-out-lane index (head occupancy and entrant record)
   uint8_t w;     // cells (0 = empty slot)
   uint8_t l, L;  // lane, lanes of the link
   uint8_t vk;    // vmax of the link
@@ -142,7 +142,7 @@ static_assert(sizeof(NodeLane) == 16, "NodeLane must be 16 bytes");
 
 // an outgoing link of a node, by out-slot: what a winner needs to enter it
 struct NodeOut {
-  int32_t lgid;  // global id of its lane 0
+  int32_t lgid;  // node-out-lane index of its lane 0 (head occupancy, entrant record)
   int16_t L;     // lanes
   int16_t n;     // cells
 };
@@ -216,10 +216,11 @@ struct StepParams {
   int32_t *pend_head;
   // node interface
   const int32_t *nli;  // node-lane index of every global lane id
+  const int32_t *nlo;  // node-out-lane index of every global lane id
   uint64_t *tail_rec;  // per node-lane index, written with S1
-  uint8_t *head_occ;   // per lane, written with S1
+  uint8_t *head_occ;   // per node-out-lane index, written with S1
   const uint8_t *ext;  // per node-lane index, from k_node
-  const uint64_t *entr;  // per global lane id
+  const uint64_t *entr;  // per node-out-lane index
   // outputs
   unsigned long long *stats;  // [kHist][ST_N]
   unsigned long long *link_work;

@@ -241,7 +241,7 @@ __device__ void write_back(const StepParams &P, TileCtx &T, bool node_recs, int 
         P.tail_rec[P.nli[T.d.lane_gid + l]] = rec;
       }
       if (T.d.flags & kFirst)
-        P.head_occ[T.d.lane_gid + l] = (uint8_t)(win_at(T.bout, l * T.S + T.HP) & 31u);
+        P.head_occ[P.nlo[T.d.lane_gid + l]] = (uint8_t)(win_at(T.bout, l * T.S + T.HP) & 31u);
     }
   }
   __syncwarp();
@@ -376,7 +376,7 @@ __global__ void __launch_bounds__(256) k_step(const StepParams P) {
       }
       // entrants granted by the node kernel (H3/H5): at most one per lane
       if ((T.d.flags & kFirst) && lane < T.L) {
-        uint64_t rec = P.entr[T.d.lane_gid + lane];
+        uint64_t rec = P.entr[P.nlo[T.d.lane_gid + lane]];
         if ((uint32_t)(rec >> 43) == ((uint32_t)(P.t + 1) & 0x1FFFFFu)) {
           int vid = (int)(uint32_t)rec;
           uint8_t code = (uint8_t)(rec >> 32);
@@ -490,15 +490,16 @@ __device__ __forceinline__ Cand node_candidate(const NodeParams &P, uint64_t rec
 }
 
 // the winner's grant: returns ext; writes the entrant record if it crosses.
-// head: occupancy of the first cells of the target lane; q: the winner's
-// route position record (one 16-byte record per vehicle)
+// head: occupancy of the first cells of the target lane.  The route
+// position record (16 bytes per vehicle) is read only for a crossing.
 __device__ __forceinline__ int node_grant(const NodeParams &P, const Cand &c, int vk, uint8_t head,
-                                          const VehPos &q, uint32_t &crossings) {
+                                          uint32_t &crossings) {
   const int E = min(ctz32((uint32_t)head | 0x20u), min(kGmax, c.n2));
   if (E == 0) return 0;
   const int v3 = nasch_v3(c.v, vk, min(kGmax, c.d + E), (uint32_t)P.t, (uint32_t)c.vid, P.k0,
                           P.k1, P.p32);
   if (v3 > c.d) {
+    const VehPos q = P.vpos[c.vid];
     const int nslot = (q.p + 2 < q.e) ? (int)P.rslot[q.p + 2] : kSlotFinal;
     P.vpos[c.vid].p = q.p + 1;
     const int y2 = v3 - c.d - 1;
@@ -525,9 +526,9 @@ __device__ __forceinline__ void node_flush(const NodeParams &P, uint32_t crossin
 // one thread per incoming lane; the lanes of a node are consecutive threads
 // in priority order, so the winner of a target lane is the lowest eligible
 // thread with that target.  Every warp resolves kNodeILP chunks at once
-// stage by stage (records, out-slot table, head occupancy and route
-// position, grant), so their dependent loads overlap instead of running
-// as one latency chain per chunk.
+// stage by stage (records, out-slot table, target heads, grant), so their
+// dependent loads overlap instead of running as one latency chain per
+// chunk.
 #ifndef TS_NODE_ILP
 #define TS_NODE_ILP 1  // measured on 4a: 1 -> 31.5 us, 2 -> 35, 4 -> 39.6, 8 -> 49.6
 #endif
@@ -569,16 +570,13 @@ __global__ void __launch_bounds__(256) k_node_warp(const NodeParams P, const Nod
     win[k] = eligible && (__ffs(grp) - 1) == lane;
   }
   uint8_t head[kNodeILP];
-  VehPos q[kNodeILP];
 #pragma unroll
-  for (int k = 0; k < kNodeILP; k++) {  // stage 3: target head and route position
+  for (int k = 0; k < kNodeILP; k++)  // stage 3: target heads
     head[k] = win[k] ? P.head_occ[cd[k].tgt] : (uint8_t)0;
-    q[k] = win[k] ? P.vpos[cd[k].vid] : VehPos{0, 0};
-  }
 #pragma unroll
   for (int k = 0; k < kNodeILP; k++) {  // stage 4: grants
     int ext = 0;
-    if (win[k]) ext = node_grant(P, cd[k], e[k].vk, head[k], q[k], crossings);
+    if (win[k]) ext = node_grant(P, cd[k], e[k].vk, head[k], crossings);
     if (act[k]) P.ext[32 * (c0 + k) + lane] = (uint8_t)ext;
   }
   node_flush(P, crossings, red);
@@ -635,7 +633,7 @@ __global__ void __launch_bounds__(128) k_node(const NodeParams P) {
           if (taken) continue;
           if (nclaimed < kMaxClaim) claimed[nclaimed++] = bit;
           P.ext[lg + l] = (uint8_t)node_grant(P, cd, P.vmax_link[j], P.head_occ[cd.tgt],
-                                              P.vpos[cd.vid], crossings);
+                                              crossings);
         }
       }
     }

@@ -231,6 +231,9 @@ static __device__ __noinline__ uint32_t zone_lc(uint32_t zc, int c0, int w, int 
 #ifndef TS_ROWS_ASYNC
 #define TS_ROWS_ASYNC 1  // vid blocks: cp.async in, bulk (TMA) store out
 #endif
+#ifndef TS_ROWS_PIPE
+#define TS_ROWS_PIPE 0  // (measured: no gain) 1: next group's vid block copied in during this one; 2: + its planes
+#endif
 #ifndef TS_ROWS_PF
 #define TS_ROWS_PF 0  // prefetch the next group's state into L2 (measured: no gain)
 #endif
@@ -269,10 +272,38 @@ __global__ void __launch_bounds__(128, TS_ROWS_MINB) k_rows(const StepParams P, 
     return __shfl_sync(FULL, g, 0);
   };
   int g_next = grab();
+  // pipelined staging: the vid block of the group to process next is copied
+  // into s_in (cp.async) while the current one finishes; (cur_voff,
+  // cur_cnt) describe the block in flight
+  int cur_voff = 0, cur_cnt = 0;
+  uint32_t O[NW], V0[NW], V1[NW], V2[NW], A0[NW], A1[NW];
+  auto load_planes = [&](int gg) {
+    const uint32_t *pin = R.planes_in + group_plane_base(gg) + lane;
+#pragma unroll
+    for (int i = 0; i < NW; i++) {
+      O[i] = __ldcs(pin + (0 * NW + i) * 32);
+      V0[i] = __ldcs(pin + (1 * NW + i) * 32);
+      V1[i] = __ldcs(pin + (2 * NW + i) * 32);
+      V2[i] = __ldcs(pin + (3 * NW + i) * 32);
+      A0[i] = __ldcs(pin + (4 * NW + i) * 32);
+      A1[i] = __ldcs(pin + (5 * NW + i) * 32);
+    }
+  };
+  if (TS_ROWS_PIPE && g_next < R.ngroups) {
+    cur_voff = R.gvoff[g_next];
+    cur_cnt = R.gcnt_in[g_next];
+    if (cur_cnt <= R.cap) warp_load_async(s_in, R.vid_in + cur_voff, cur_cnt, lane);
+    if (TS_ROWS_PIPE >= 2) load_planes(g_next);
+  }
   for (;;) {
     const int g = g_next;
     if (g >= R.ngroups) break;
     g_next = grab();
+    int nx_voff = 0, nx_cnt = 0;  // the next group's block, issued at the end of this one
+    if (TS_ROWS_PIPE && g_next < R.ngroups) {
+      nx_voff = __ldg(&R.gvoff[g_next]);
+      nx_cnt = __ldg(&R.gcnt_in[g_next]);
+    }
     int pf_voff = 0, pf_cnt = 0;  // the next group's vid block (prefetched later)
     if (TS_ROWS_PF && g_next < R.ngroups) {
       if (lane == 0) prefetch_l2(R.planes_in + group_plane_base(g_next), kStatePlanes * kRowWords * 128);
@@ -286,12 +317,12 @@ __global__ void __launch_bounds__(128, TS_ROWS_MINB) k_rows(const StepParams P, 
     __syncwarp();  // the previous group's staged blocks are no longer in use
     const RowDesc rd = R.rows[(size_t)g * 32 + lane];
     const int w = rd.w, l = rd.l, L = rd.L, link = rd.link, lg = rd.lg, vk = rd.vk;
-    const int voff = R.gvoff[g];
+    const int voff = TS_ROWS_PIPE ? cur_voff : R.gvoff[g];
     // the group's vid block (its vehicle count was written with it) is
     // staged in shared memory when it fits, loaded together with the planes
-    const int tot_in = R.gcnt_in[g];
+    const int tot_in = TS_ROWS_PIPE ? cur_cnt : R.gcnt_in[g];
     const bool staged = tot_in <= R.cap;
-    if (staged) {
+    if (staged && !TS_ROWS_PIPE) {
       if (TS_ROWS_ASYNC) warp_load_async(s_in, R.vid_in + voff, tot_in, lane);
       else warp_load(s_in, R.vid_in + voff, tot_in, lane);
     }
@@ -302,17 +333,7 @@ __global__ void __launch_bounds__(128, TS_ROWS_MINB) k_rows(const StepParams P, 
     const uint64_t ent_rec = do_move0 ? P.entr[lg] : 0ull;
     const bool may_inject = (P.mode & kModeInject) && w > 0 && l == 0 &&
                             P.pend_off[link + 1] > P.pend_head[link];
-    const uint32_t *pin = R.planes_in + group_plane_base(g) + lane;
-    uint32_t O[NW], V0[NW], V1[NW], V2[NW], A0[NW], A1[NW];
-#pragma unroll
-    for (int i = 0; i < NW; i++) {
-      O[i] = __ldcs(pin + (0 * NW + i) * 32);
-      V0[i] = __ldcs(pin + (1 * NW + i) * 32);
-      V1[i] = __ldcs(pin + (2 * NW + i) * 32);
-      V2[i] = __ldcs(pin + (3 * NW + i) * 32);
-      A0[i] = __ldcs(pin + (4 * NW + i) * 32);
-      A1[i] = __ldcs(pin + (5 * NW + i) * 32);
-    }
+    if (TS_ROWS_PIPE < 2) load_planes(g);
     uint32_t VAL[NW];
 #pragma unroll
     for (int i = 0; i < NW; i++) VAL[i] = lowm(w - 32 * i);
@@ -773,6 +794,11 @@ __global__ void __launch_bounds__(128, TS_ROWS_MINB) k_rows(const StepParams P, 
     // the output block's shared-memory writes become visible to the bulk copy
     if (TS_ROWS_ASYNC) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncwarp();
+    if (TS_ROWS_PIPE && g_next < R.ngroups) {  // s_in is free: stage the next group's block
+      if (nx_cnt <= R.cap) warp_load_async(s_in, R.vid_in + nx_voff, nx_cnt, lane);
+      cur_voff = nx_voff;
+      cur_cnt = nx_cnt;
+    }
     const uint32_t efin = nfin > 0 ? (uint32_t)vout[nfin - 1] : 0u;  // final front vehicle
     if (ostaged) {
       if (TS_ROWS_ASYNC) {
@@ -799,6 +825,7 @@ __global__ void __launch_bounds__(128, TS_ROWS_MINB) k_rows(const StepParams P, 
       P.tail_rec[rd.nli] = rec;
       P.head_occ[lg] = (uint8_t)(FO[0] & lowm(nb));
     }
+    if (TS_ROWS_PIPE >= 2 && g_next < R.ngroups) load_planes(g_next);
   }
   if (TS_ROWS_ASYNC && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   flush_acc(P, acc, P.t + 1, red);
