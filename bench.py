@@ -223,7 +223,8 @@ def bench_tsim(args):
                      "frac": achieved / hbm_peak, "traffic": traffic["bytes"],
                      "traffic_source": traffic["source"], "kernel": "k_rows",
                      "alg_bytes_per_launch": alg_per_launch, "kernel_ms": mv_ms,
-                     "kernel_share": timing["move_ms"] / ms_total, "peak_source": peak_src},
+                     "kernel_share": mv_ms * args.steps / ms_total,
+                     "kernel_launches_timed": timing["move_launches"], "peak_source": peak_src},
         "e2e": {"value": upd_all / e2e_wall, "unit": "vehicle-updates/s",
                 "h2d_bytes_per_step": h2d / (args.steps + args.warmup),
                 "d2h_bytes_per_step": d2h / (args.steps + args.warmup),

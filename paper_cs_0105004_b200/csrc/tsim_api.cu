@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -103,6 +104,9 @@ struct ts_sim {
   int32_t *d_inj_scratch = nullptr;
   RowDesc *d_rows = nullptr;
   int rows_threads = 128, rows_blocks = 1, rows_cap = 0, rows_smem = 0;
+  // programmatic dependent launch of the node and move kernels (TSIM_NO_PDL
+  // turns it off for comparisons)
+  bool pdl = true;
   std::vector<int32_t> gvoff;                // first vid-block entry of each group
   int32_t *d_gvoff = nullptr;
   NodeLane *d_nlanes = nullptr;
@@ -859,8 +863,8 @@ static RowsParams rows_params(ts_sim *h) {
 
 // k_rows launch; the work counter advances by the groups plus one failed
 // fetch per warp
-static void rows_launch(ts_sim *h, const StepParams &p) {
-  launch_rows(p, rows_params(h), h->rows_blocks, h->rows_threads, h->rows_smem, h->stream);
+static void rows_launch(ts_sim *h, const StepParams &p, bool pdl = false) {
+  launch_rows(p, rows_params(h), h->rows_blocks, h->rows_threads, h->rows_smem, h->stream, pdl);
   h->gctr_base += (unsigned long long)h->ngroups + (unsigned long long)h->rows_blocks *
                                                         (h->rows_threads / 32);
 }
@@ -1128,9 +1132,10 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
   h->blocks = std::max(1, std::min(need, occ * nsm));
   // row kernel: one warp per 32-row group, 4 warps per block; each warp
   // stages its group's vid blocks (in + out) in shared memory
-  // staging capacity per warp: 5 blocks of 4 warps per SM (96 registers)
-  // leave ~44 KB of shared memory per block; group_cells overrides (tuning)
-  h->rows_cap = h->cfg.group_cells > 0 ? (h->cfg.group_cells + 3) & ~3 : 1024;
+  // staging capacity per warp: 4 blocks of 4 warps per SM (128 registers)
+  // leave ~55 KB of shared memory per block; group_cells overrides (tuning)
+  h->rows_cap = h->cfg.group_cells > 0 ? (h->cfg.group_cells + 3) & ~3 : 1344;
+  h->pdl = getenv("TSIM_NO_PDL") == nullptr;
   h->rows_threads = 128;
   h->rows_smem = (h->rows_threads / 32) * rows_stage_words(h->rows_cap) * 4;
   CK(h, set_rows_smem(h->rows_smem));
@@ -1229,13 +1234,13 @@ static void phase_move(ts_sim *h, bool more, cudaEvent_t e0, cudaEvent_t e1) {
   if (h->n_xs > 0) unpack_strips(h);
   if (h->node_warp)
     launch_node_warp(node_params(h, t), NodeWarpParams{h->d_lane_sig, h->d_nlanes, h->nchunks},
-                     h->stream);
+                     h->stream, h->pdl);
   else
     launch_node(node_params(h, t), h->stream);
   if (e0) cudaEventRecord(e0, h->stream);
   if (h->ngroups > 0) {
     const bool f = more && h->rfused;
-    rows_launch(h, step_params(h, t, mode | (f ? kModeLC : 0)));
+    rows_launch(h, step_params(h, t, mode | (f ? kModeLC : 0)), h->pdl && h->node_warp);
     h->rcur ^= 1;
     h->rows_s1 = f;
   }
@@ -1250,6 +1255,8 @@ static void phase_move(ts_sim *h, bool more, cudaEvent_t e0, cudaEvent_t e1) {
   h->t = t + 1;
   if (h->n_xs > 0) pack_strips(h);
 }
+
+constexpr int kTimingStride = 8;
 
 static int enqueue_steps(ts_sim *h, int32_t n) {
   if (!h || !h->inited) return fail(h, TS_EINVAL, "call ts_init first");
@@ -1267,14 +1274,18 @@ static int enqueue_steps(ts_sim *h, int32_t n) {
     }
   }
   CK(h, cudaEventRecord(h->ev0, h->stream));
+  // the move kernel is timed on every kTimingStride-th step only: events
+  // between two kernels would serialise their programmatic overlap
+  int ns = 0;
   for (int i = 0; i < n; i++) {
     phase_lc(h);
-    phase_move(h, i < n - 1, h->timing ? h->mv_ev[2 * i] : nullptr,
-               h->timing ? h->mv_ev[2 * i + 1] : nullptr);
+    const bool tm = h->timing && i % kTimingStride == 0;
+    phase_move(h, i < n - 1, tm ? h->mv_ev[2 * ns] : nullptr, tm ? h->mv_ev[2 * ns + 1] : nullptr);
+    ns += tm;
   }
   CK(h, cudaEventRecord(h->ev1, h->stream));
   CK(h, cudaGetLastError());
-  h->last_move_launches = n;
+  h->last_move_launches = ns;
   return TS_OK;
 }
 
@@ -1306,7 +1317,7 @@ static int finish_steps(ts_sim *h, int32_t t_from, int32_t n) {
   h->last_total_ms = ms;
   double mv = 0;
   if (h->timing)
-    for (int i = 0; i < n; i++) {
+    for (int i = 0; i < h->last_move_launches; i++) {
       float m = 0;
       CK(h, cudaEventElapsedTime(&m, h->mv_ev[2 * i], h->mv_ev[2 * i + 1]));
       mv += m;

@@ -11,6 +11,33 @@ namespace tsim {
 
 #define FULL 0xffffffffu
 
+// ------------------------------------------- programmatic dependent launch
+// griddepcontrol (sm_90+): a kernel launched with programmatic stream
+// serialisation may start while its predecessor finishes; it must wait
+// before reading the predecessor's output.  Both are no-ops otherwise.
+static __device__ __forceinline__ void grid_dep_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+static __device__ __forceinline__ void grid_dep_launch() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+// launch with the programmatic-serialisation attribute when pdl is set
+template <typename... KArgs, typename... Args>
+static inline cudaError_t launch_pdl(void (*kern)(KArgs...), int blocks, int threads, int smem,
+                                     void *stream, bool pdl, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(blocks);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = (cudaStream_t)stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 // ------------------------------------------------------------- Philox
 // Philox4x32-10 (Salmon et al., SC'11) with the curand round and Weyl
 // constants, counter (t, vid, 0, 0), key (k0, k1); only output word 0 is

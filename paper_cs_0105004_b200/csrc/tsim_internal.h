@@ -288,8 +288,8 @@ struct NodeWarpParams {
 
 void launch_lc(const StepParams &p, int blocks, int threads, int smem, void *stream);
 void launch_rows(const StepParams &p, const RowsParams &r, int blocks, int threads, int smem,
-                 void *stream);
-void launch_node_warp(const NodeParams &p, const NodeWarpParams &w, void *stream);
+                 void *stream, bool pdl = false);
+void launch_node_warp(const NodeParams &p, const NodeWarpParams &w, void *stream, bool pdl = false);
 void launch_step(const StepParams &p, int blocks, int threads, int smem, void *stream);
 void launch_node(const NodeParams &p, void *stream);
 void launch_strip_copy(const Strip *src, const int32_t *sslot, Strip *dst, const int32_t *dslot,

@@ -544,13 +544,20 @@ __global__ void __launch_bounds__(256) k_node_warp(const NodeParams P, const Nod
   uint32_t sg[kNodeILP];
   bool act[kNodeILP];
 #pragma unroll
-  for (int k = 0; k < kNodeILP; k++) {  // stage 1: lane records of S1
+  for (int k = 0; k < kNodeILP; k++) {  // stage 1: static lane data (before the wait)
     const int c = min(c0 + k, W.nchunks - 1), i = 32 * c + lane;  // node-lane index
     act[k] = c0 + k < W.nchunks;
     e[k] = W.lanes[i];
-    rec[k] = P.tail_rec[i];
     sg[k] = W.sig ? W.sig[i] : 0u;
   }
+  // programmatic dependent launch: the records of S1 are the previous
+  // kernel's output; once it is complete the next move kernel may start
+  // its own prologue
+  grid_dep_wait();
+  grid_dep_launch();
+#pragma unroll
+  for (int k = 0; k < kNodeILP; k++)  // lane records of S1
+    rec[k] = P.tail_rec[32 * min(c0 + k, W.nchunks - 1) + lane];
   Cand cd[kNodeILP];
   bool win[kNodeILP];
 #pragma unroll
@@ -674,10 +681,10 @@ void launch_node(const NodeParams &p, void *stream) {
   if (p.nnodes <= 0) return;
   k_node<<<(p.nnodes + 127) / 128, 128, 0, (cudaStream_t)stream>>>(p);
 }
-void launch_node_warp(const NodeParams &p, const NodeWarpParams &w, void *stream) {
+void launch_node_warp(const NodeParams &p, const NodeWarpParams &w, void *stream, bool pdl) {
   if (w.nchunks <= 0) return;
   const int blocks = (w.nchunks + 8 * kNodeILP - 1) / (8 * kNodeILP);
-  k_node_warp<<<blocks, 256, 0, (cudaStream_t)stream>>>(p, w);
+  launch_pdl(k_node_warp, blocks, 256, 0, stream, pdl, p, w);
 }
 void launch_hash(const StepParams &p, int blocks, int threads, int smem, void *stream,
                  unsigned long long *out) {

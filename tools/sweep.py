@@ -15,6 +15,6 @@ for gc in [int(a) for a in sys.argv[1:]]:
     sim.step(200)
     sim.step(100)
     tm = sim.last_timing()
-    print(json.dumps(dict(cap=gc, ms_step=tm['total_ms'] / 100, ms_move=tm['move_ms'] / 100)),
+    print(json.dumps(dict(cap=gc, ms_step=tm['total_ms'] / 100, ms_move=tm['move_ms'] / max(1, tm['move_launches']))),
           flush=True)
     sim.close()

@@ -40,7 +40,7 @@ sim.init(0)
 sim.step(200)
 sim.step({steps})
 tm = sim.last_timing()
-print(json.dumps(dict(ms_step=tm['total_ms'] / {steps}, ms_move=tm['move_ms'] / {steps})))
+print(json.dumps(dict(ms_step=tm['total_ms'] / {steps}, ms_move=tm['move_ms'] / max(1, tm['move_launches']))))
 '''
 
 
@@ -48,6 +48,9 @@ def time(steps, specs):
     for spec in specs:
         name, _, gc = spec.partition(':')
         env = dict(os.environ)
+        if name.endswith('+nopdl'):
+            name = name[:-len('+nopdl')]
+            env['TSIM_NO_PDL'] = '1'
         if name != 'base':
             env['TSIM_LIB'] = os.path.join(ROOT, 'build', f'var_{name}', 'libtsim.so')
         code = CHILD.format(root=ROOT, gc=int(gc or 0), steps=steps)
