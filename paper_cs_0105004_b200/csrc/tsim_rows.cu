@@ -427,30 +427,52 @@ __global__ void __launch_bounds__(128, TS_ROWS_MINB) k_rows(const StepParams P, 
         uint32_t *bw = reinterpret_cast<uint32_t *>(s_out + R.cap);
 #pragma unroll
         for (int i = 0; i < NW; i++) bw[lane * NW + i] = 0u;  // this row's brake bits
-        for (int base = 0; base < mtot; base += R.cap) {
-          int j = moff - base, rb = in_off;
-#pragma unroll 1
-          for (int i = 0; i < NW; i++) {
-            uint32_t m = pick(U1, i);
-            const uint32_t o = pick(O, i);
-            while (m) {
-              const int x = __ffs(m) - 1;
-              m &= m - 1u;
-              if (j >= 0 && j < R.cap)
-                mlist[j] = ((rb + __popc(o & ((1u << x) - 1u))) << 12) | (lane << 7) | (32 * i + x);
-              j++;
-            }
-            rb += __popc(o);
-          }
-          __syncwarp();
-          const int n = min(mtot - base, R.cap);
+        auto draw = [&](int n) {  // the draws of list entries [0, n)
           for (int jj = lane; jj < n; jj += 32) {
             const int me = mlist[jj];
             const uint32_t e = (uint32_t)vbase[me >> 12];
             if ((uint64_t)philox_w0((uint32_t)P.t, e & kVidMask, P.k0, P.k1) < P.p32)
               atomicOr(bw + ((me >> 7) & 31) * NW + ((me >> 5) & 3), 1u << (me & 31));
           }
+        };
+        if (mtot <= R.cap) {  // one chunk (the common case): no bounds checks
+          int j = moff, rb = in_off;
+#pragma unroll
+          for (int i = 0; i < NW; i++) {
+            uint32_t m = U1[i];
+            const uint32_t o = O[i];
+            const int b = (rb << 12) | (lane << 7) | (32 * i);
+            while (m) {
+              const uint32_t lsb = m & (0u - m), below = lsb - 1u;
+              m ^= lsb;
+              mlist[j++] = b + (__popc(o & below) << 12) + __popc(below);
+            }
+            rb += __popc(o);
+          }
           __syncwarp();
+          draw(mtot);
+          __syncwarp();
+        } else {
+          for (int base = 0; base < mtot; base += R.cap) {
+            int j = moff - base, rb = in_off;
+#pragma unroll 1
+            for (int i = 0; i < NW; i++) {
+              uint32_t m = pick(U1, i);
+              const uint32_t o = pick(O, i);
+              while (m) {
+                const int x = __ffs(m) - 1;
+                m &= m - 1u;
+                if (j >= 0 && j < R.cap)
+                  mlist[j] = ((rb + __popc(o & ((1u << x) - 1u))) << 12) | (lane << 7) | (32 * i + x);
+                j++;
+              }
+              rb += __popc(o);
+            }
+            __syncwarp();
+            const int n = min(mtot - base, R.cap);
+            draw(n);
+            __syncwarp();
+          }
         }
 #pragma unroll
         for (int i = 0; i < NW; i++) Bm[i] = bw[lane * NW + i];
