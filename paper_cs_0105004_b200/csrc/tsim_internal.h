@@ -120,8 +120,12 @@ static_assert(sizeof(RowDesc) == 16, "RowDesc must be 16 bytes");
 // during the draws, the masks and list offsets of the rows the lane change
 // touched during the list rebuild
 constexpr int kRowsAuxWords = 4 * 32 * kRowWords + 5 * 32 + 4 + 64;
+#ifndef TS_ROWS_PPF
+#define TS_ROWS_PPF 0  // prefetch the next group's planes into shared memory
+#endif
+constexpr int kRowsPlaneWords = TS_ROWS_PPF ? kStatePlanes * kRowWords * 32 : 0;
 __host__ __device__ inline int rows_stage_words(int cap) {
-  return 2 * cap + kRowsAuxWords;  // cap is a multiple of 4: 16-byte aligned
+  return 2 * cap + kRowsAuxWords + kRowsPlaneWords;  // cap % 4 == 0: 16-byte aligned
 }
 
 // Warp-cooperative node kernel: the incoming lanes of every node, in the

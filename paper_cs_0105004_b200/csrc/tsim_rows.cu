@@ -231,18 +231,6 @@ static __device__ __noinline__ uint32_t zone_lc(uint32_t zc, int c0, int w, int 
 #ifndef TS_ROWS_ASYNC
 #define TS_ROWS_ASYNC 1  // vid blocks: cp.async in, bulk (TMA) store out
 #endif
-#ifndef TS_ROWS_PIPE
-#define TS_ROWS_PIPE 0  // (measured: no gain) 1: next group's vid block copied in during this one; 2: + its planes
-#endif
-#ifndef TS_ROWS_PF
-#define TS_ROWS_PF 0  // prefetch the next group's state into L2 (measured: no gain)
-#endif
-
-// bulk prefetch of [p, p + bytes) into L2 (p 16-byte aligned, bytes % 16 == 0)
-__device__ __forceinline__ void prefetch_l2(const void *p, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-}
-
 // MODE = the uniform mode bits kModeMove | kModeLC | kModeHash of the launch
 // (specialised so the hot fused instantiation carries no dead paths)
 template <int MODE>
@@ -265,69 +253,58 @@ __global__ void __launch_bounds__(128, TS_ROWS_MINB) k_rows(const StepParams P, 
 
   // groups are handed out dynamically (one atomic per warp and group): no
   // warp idles while another still has a queue of groups
-  // The next group is fetched one iteration ahead and its planes, row
-  // descriptors and vid block are prefetched into L2 while this one runs.
+  // The next group is fetched one iteration ahead; with TS_ROWS_PPF its
+  // planes are copied into shared memory (cp.async) while this one runs.
   (void)nwarps;
   auto grab = [&]() {
     int g = 0;
     if (lane == 0) g = (int)(atomicAdd(R.gctr, 1ull) - R.gbase);
     return __shfl_sync(FULL, g, 0);
   };
-  int g_next = grab();
-  // pipelined staging: the vid block of the group to process next is copied
-  // into s_in (cp.async) while the current one finishes; (cur_voff,
-  // cur_cnt) describe the block in flight
-  int cur_voff = 0, cur_cnt = 0;
-  uint32_t O[NW], V0[NW], V1[NW], V2[NW], A0[NW], A1[NW];
-  auto load_planes = [&](int gg) {
-    const uint32_t *pin = R.planes_in + group_plane_base(gg) + lane;
-#pragma unroll
-    for (int i = 0; i < NW; i++) {
-      O[i] = __ldcs(pin + (0 * NW + i) * 32);
-      V0[i] = __ldcs(pin + (1 * NW + i) * 32);
-      V1[i] = __ldcs(pin + (2 * NW + i) * 32);
-      V2[i] = __ldcs(pin + (3 * NW + i) * 32);
-      A0[i] = __ldcs(pin + (4 * NW + i) * 32);
-      A1[i] = __ldcs(pin + (5 * NW + i) * 32);
+  uint32_t *s_pl = reinterpret_cast<uint32_t *>(s_out + R.cap + kRowsAuxWords);  // PPF buffer
+  auto issue_planes = [&](int gg) {  // cp.async of the group's 3 KB of planes
+    const uint32_t *src = R.planes_in + group_plane_base(gg);
+    for (int c = lane; c < kStatePlanes * kRowWords * 8; c += 32) {
+      const uint32_t sa = (uint32_t)__cvta_generic_to_shared(s_pl + 4 * c);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(src + 4 * c) : "memory");
     }
+    asm volatile("cp.async.commit_group;" ::: "memory");
   };
-  if (TS_ROWS_PIPE && g_next < R.ngroups) {
-    cur_voff = R.gvoff[g_next];
-    cur_cnt = R.gcnt_in[g_next];
-    if (cur_cnt <= R.cap) warp_load_async(s_in, R.vid_in + cur_voff, cur_cnt, lane);
-    if (TS_ROWS_PIPE >= 2) load_planes(g_next);
-  }
+  int g_next = grab();
+  if (TS_ROWS_PPF && g_next < R.ngroups) issue_planes(g_next);
   for (;;) {
     const int g = g_next;
     if (g >= R.ngroups) break;
     g_next = grab();
-    int nx_voff = 0, nx_cnt = 0;  // the next group's block, issued at the end of this one
-    if (TS_ROWS_PIPE && g_next < R.ngroups) {
-      nx_voff = __ldg(&R.gvoff[g_next]);
-      nx_cnt = __ldg(&R.gcnt_in[g_next]);
-    }
-    int pf_voff = 0, pf_cnt = 0;  // the next group's vid block (prefetched later)
-    if (TS_ROWS_PF && g_next < R.ngroups) {
-      if (lane == 0) prefetch_l2(R.planes_in + group_plane_base(g_next), kStatePlanes * kRowWords * 128);
-      if (lane == 1) prefetch_l2(R.rows + (size_t)g_next * 32, 32 * sizeof(RowDesc));
-      if (lane == 2) {
-        pf_voff = __ldg(&R.gvoff[g_next]);
-        pf_cnt = __ldg(&R.gcnt_in[g_next]);
+    if (TS_ROWS_ASYNC && lane == 0) bulk_wait_read();  // the previous group's output block
+    uint32_t O[NW], V0[NW], V1[NW], V2[NW], A0[NW], A1[NW];
+    if (TS_ROWS_PPF) {  // this group's planes, prefetched during the previous one
+      asm volatile("cp.async.wait_all;" ::: "memory");
+      __syncwarp();
+#pragma unroll
+      for (int i = 0; i < NW; i++) {
+        O[i] = s_pl[(0 * NW + i) * 32 + lane];
+        V0[i] = s_pl[(1 * NW + i) * 32 + lane];
+        V1[i] = s_pl[(2 * NW + i) * 32 + lane];
+        V2[i] = s_pl[(3 * NW + i) * 32 + lane];
+        A0[i] = s_pl[(4 * NW + i) * 32 + lane];
+        A1[i] = s_pl[(5 * NW + i) * 32 + lane];
       }
     }
-    if (TS_ROWS_ASYNC && lane == 0) bulk_wait_read();  // the previous group's output block
-    __syncwarp();  // the previous group's staged blocks are no longer in use
+    __syncwarp();  // the previous group's staged blocks (and the plane buffer) are free
     const RowDesc rd = R.rows[(size_t)g * 32 + lane];
     const int w = rd.w, l = rd.l, L = rd.L, link = rd.link, lg = rd.lg, vk = rd.vk;
-    const int voff = TS_ROWS_PIPE ? cur_voff : R.gvoff[g];
+    const int voff = R.gvoff[g];
     // the group's vid block (its vehicle count was written with it) is
     // staged in shared memory when it fits, loaded together with the planes
-    const int tot_in = TS_ROWS_PIPE ? cur_cnt : R.gcnt_in[g];
+    const int tot_in = R.gcnt_in[g];
     const bool staged = tot_in <= R.cap;
-    if (staged && !TS_ROWS_PIPE) {
+    if (staged) {
       if (TS_ROWS_ASYNC) warp_load_async(s_in, R.vid_in + voff, tot_in, lane);
       else warp_load(s_in, R.vid_in + voff, tot_in, lane);
     }
+    const bool pl_next = TS_ROWS_PPF && g_next < R.ngroups;
+    if (pl_next) issue_planes(g_next);  // committed after the vid block
     // per-row gathers of this step, issued early: node grant, entrant,
     // pending trips
     const bool do_move0 = do_move && w > 0;
@@ -339,7 +316,18 @@ __global__ void __launch_bounds__(128, TS_ROWS_MINB) k_rows(const StepParams P, 
     const uint64_t ent_rec = do_move0 ? P.entr[lg] : 0ull;
     const bool may_inject = (P.mode & kModeInject) && w > 0 && l == 0 &&
                             P.pend_off[link + 1] > P.pend_head[link];
-    if (TS_ROWS_PIPE < 2) load_planes(g);
+    if (!TS_ROWS_PPF) {
+      const uint32_t *pin = R.planes_in + group_plane_base(g) + lane;
+#pragma unroll
+      for (int i = 0; i < NW; i++) {
+        O[i] = __ldcs(pin + (0 * NW + i) * 32);
+        V0[i] = __ldcs(pin + (1 * NW + i) * 32);
+        V1[i] = __ldcs(pin + (2 * NW + i) * 32);
+        V2[i] = __ldcs(pin + (3 * NW + i) * 32);
+        A0[i] = __ldcs(pin + (4 * NW + i) * 32);
+        A1[i] = __ldcs(pin + (5 * NW + i) * 32);
+      }
+    }
     uint32_t VAL[NW];
 #pragma unroll
     for (int i = 0; i < NW; i++) VAL[i] = lowm(w - 32 * i);
@@ -347,7 +335,10 @@ __global__ void __launch_bounds__(128, TS_ROWS_MINB) k_rows(const StepParams P, 
     int tot_chk;
     const int in_off = warp_scan(nin, lane, &tot_chk);
     if (staged) {
-      if (TS_ROWS_ASYNC) cp_async_wait();
+      if (TS_ROWS_ASYNC) {
+        if (pl_next) asm volatile("cp.async.wait_group 1;" ::: "memory");  // planes may pend
+        else cp_async_wait();
+      }
       __syncwarp();
     }
     const int32_t *vin = (staged ? (const int32_t *)s_in : R.vid_in + voff) + in_off;
@@ -478,8 +469,6 @@ __global__ void __launch_bounds__(128, TS_ROWS_MINB) k_rows(const StepParams P, 
         for (int i = 0; i < NW; i++) Bm[i] = bw[lane * NW + i];
         __syncwarp();
       }
-      if (TS_ROWS_PF && lane == 2 && pf_cnt > 0)
-        prefetch_l2(R.vid_in + pf_voff, (uint32_t)((pf_cnt + 3) & ~3) * 4u);
       // ---- hop, word by word: D_k = vehicles moving exactly k (v3 = k);
       //      those passing the row end leave it (LR); O' = OR_k D_k << k with
       //      the velocity and class bits carried along
@@ -822,11 +811,6 @@ __global__ void __launch_bounds__(128, TS_ROWS_MINB) k_rows(const StepParams P, 
     // the output block's shared-memory writes become visible to the bulk copy
     if (TS_ROWS_ASYNC) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncwarp();
-    if (TS_ROWS_PIPE && g_next < R.ngroups) {  // s_in is free: stage the next group's block
-      if (nx_cnt <= R.cap) warp_load_async(s_in, R.vid_in + nx_voff, nx_cnt, lane);
-      cur_voff = nx_voff;
-      cur_cnt = nx_cnt;
-    }
     const uint32_t efin = nfin > 0 ? (uint32_t)vout[nfin - 1] : 0u;  // final front vehicle
     if (ostaged) {
       if (TS_ROWS_ASYNC) {
@@ -853,7 +837,6 @@ __global__ void __launch_bounds__(128, TS_ROWS_MINB) k_rows(const StepParams P, 
       P.tail_rec[rd.nli] = rec;
       P.head_occ[lg] = (uint8_t)(FO[0] & lowm(nb));
     }
-    if (TS_ROWS_PIPE >= 2 && g_next < R.ngroups) load_planes(g_next);
   }
   if (TS_ROWS_ASYNC && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   flush_acc(P, acc, P.t + 1, red);
