@@ -685,7 +685,7 @@ static bool build_node_lanes(ts_sim *h, std::vector<NodeLane> &lanes,
       for (int i = a; i < b; i++) {
         const int j = h->in_list[i];
         if ((h->cls[j] == maxcls) != (pass == 0)) continue;
-        for (int l = 0; l < h->lanes[j]; l++)
+        for (int l = 0; l < h->lanes[j]; l++) {  // one NodeLane and one signal word per lane
           lanes.push_back(NodeLane{h->lgid[j] + l, h->out_off[nd], h->tt[j], (uint8_t)l,
                                    (uint8_t)(pass == 0), (uint8_t)h->vmax[j],
                                    (uint8_t)node_first});
@@ -697,6 +697,7 @@ static bool build_node_lanes(ts_sim *h, std::vector<NodeLane> &lanes,
             sw = pass == 0 ? s0 : sig_word(c, ((sh - g0) % c + c) % c, c - g0);
           }
           sig.push_back(sw);
+        }
       }
     in_chunk += nl;
   }

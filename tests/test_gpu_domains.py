@@ -138,3 +138,11 @@ def test_bad_domain_inputs():
     g2.load(r)
     with pytest.raises(tsim.TsError):
         g2.set_domain(2, np.zeros(r.n_nodes, np.int32), 0)
+
+
+@pytest.mark.parametrize("k", [2, 4])
+def test_signalized_grid_domains(k):
+    """signals at every node of config 1, k ORB domains: identical to the
+    undivided oracle (signal state is a function of t and the node only)"""
+    s = scenarios.with_signals(scenarios.config("1"), seed=5)
+    run_domains(s, k, 200, chunk=50)

@@ -162,3 +162,26 @@ def test_history_stream():
         o.step(1)
         assert hist["hash"][t] == o.state_hash(), t
         assert hist["active"][t] == o.counters()["active"]
+
+
+# ---------------------------------------------------- signals
+NODE_GENERAL = tsim.FLAG_FUSED | tsim.FLAG_HASH | 32  # TS_FLAG_NODE_GENERAL: thread-per-node kernel
+
+
+@pytest.mark.parametrize("flags", [FUSED, UNFUSED, GENERAL, NODE_GENERAL])
+def test_signalized_grid(flags):
+    """config 1 with fixed-time 30 s / 30 s signals at every node (reading
+    R23): red approaches see the virtual blocker, green
+    ones cross without gap acceptance; bit-exact against the oracle"""
+    s = scenarios.with_signals(scenarios.config("1"), seed=3)
+    run_parity(s, 300, flags, full_every=25, hash_every=25)
+
+
+@pytest.mark.parametrize("g0,g1", [(1, 1), (7, 23), (45, 5)])
+def test_signalized_portland(g0, g1):
+    """unequal phases and short cycles on the Portland-shaped network (mixed
+    row and general tiles, nodes of in-degree up to the network's maximum)"""
+    s = scenarios.portland(n_nodes=400, n_edges=560, n_veh=5000, side_km=6.0, n_zones=48, seed=5)
+    s.depart = (s.depart // 20).astype(np.int32)
+    s = scenarios.with_signals(s, green0=g0, green1=g1, seed=g0)
+    run_parity(s, 250, FUSED, full_every=50, hash_every=50)
