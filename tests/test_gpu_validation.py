@@ -56,3 +56,48 @@ def test_three_lanes_vs_one():
     act = veh["status"] == tsim.ACTIVE
     per_lane = np.array([np.sum(veh["v"][act & (veh["lane"] == k)]) for k in range(3)], float)
     assert per_lane.max() / per_lane.mean() < 1.10, per_lane
+
+
+def discharge_network(m, green0, green1, p, queue=400, seed=11):
+    """m independent approaches: a 3 km link (400 cells) filled with a
+    standing queue, a signal at its downstream node (offsets spread over the
+    cycle), a 750 m exit link; returns the scenario"""
+    import scenarios
+    from tests._ref import make_network
+    nodes, links, veh = [], [], []
+    for i in range(m):
+        y = 2000.0 * i
+        nodes += [(0.0, y), (3000.0, y), (3750.0, y)]
+        links += [(3 * i, 3 * i + 1, 3000, 1, 1), (3 * i + 1, 3 * i + 2, 750, 1, 1)]
+        veh += [dict(route=[2 * i, 2 * i + 1], place=(0, c, 0)) for c in range(queue)]
+    s = make_network(nodes, links, veh, p_slow=p, seed=seed)
+    cyc = green0 + green1
+    off = (np.arange(m) * 7) % max(1, cyc)
+    return scenarios.with_signals(s, nodes=np.arange(m) * 3 + 1, green0=green0, green1=green1,
+                                  offset=off)
+
+
+def passed_per_step(s, window):
+    g = tsim.Sim.from_scenario(s, flags=tsim.FLAG_FUSED)
+    g.step(window)
+    v = g.vehicles()
+    link = v["link"]
+    through = (v["status"] == tsim.ARRIVED) | ((v["status"] == tsim.ACTIVE) & (link % 2 == 1))
+    queued = (v["status"] == tsim.ACTIVE) & (link % 2 == 0)
+    m = s.n_links // 2
+    per = np.bincount(np.asarray(link)[queued] // 2, minlength=m)
+    assert per.min() > 0  # every queue outlasts the window
+    return through.sum() / (m * window)
+
+
+@pytest.mark.parametrize("p", [0.0, 0.2])
+def test_signal_half_green_half_saturation(p):
+    """Fig. 4d (SPEC acceptance #4): a 30 s / 30 s
+    fixed-time signal passes 0.5 x the saturation flow of the same approach
+    always green, within the +-10 % of SPEC acceptance #4; averaged over 256
+    approaches with spread offsets (measured at p = 0.2: 0.478, the start-up
+    of the queue at every green costing time each cycle)."""
+    sat = passed_per_step(discharge_network(256, 60, 0, p), 480)
+    half = passed_per_step(discharge_network(256, 30, 30, p), 960)
+    assert sat > 0.25
+    assert 0.45 <= half / sat <= 0.55, (half, sat)
