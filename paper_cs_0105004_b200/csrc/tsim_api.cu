@@ -12,6 +12,10 @@
 #include <cstring>
 #include <numeric>
 #include <string>
+#include <thread>
+#include <chrono>
+#include <utility>
+#include <memory>
 #include <vector>
 
 #include "../../include/tsim.h"
@@ -33,6 +37,27 @@ struct DevBuf {
   size_t bytes = 0;
 };
 
+// vector allocator that leaves elements uninitialised (the multi-GB route
+// arrays are filled in parallel right after allocation)
+template <typename T>
+struct UninitAlloc : std::allocator<T> {
+  template <typename U>
+  struct rebind {
+    using other = UninitAlloc<U>;
+  };
+  UninitAlloc() = default;
+  template <typename U>
+  UninitAlloc(const UninitAlloc<U> &) {}
+  template <typename U>
+  void construct(U *p) noexcept {
+    ::new (static_cast<void *>(p)) U;
+  }
+  template <typename U, typename... A>
+  void construct(U *p, A &&...a) {
+    ::new (static_cast<void *>(p)) U(std::forward<A>(a)...);
+  }
+};
+
 struct ts_sim {
   ts_config cfg{};
   std::string err;
@@ -51,7 +76,8 @@ struct ts_sim {
   // vehicles (host)
   int32_t nv = 0;
   std::vector<int64_t> roff;
-  std::vector<int32_t> route, dep, entry;
+  std::vector<int32_t, UninitAlloc<int32_t>> route;
+  std::vector<int32_t> dep, entry;
   std::vector<int32_t> pl_vid, pl_lane, pl_cell, pl_v, pl_cur;
   std::vector<uint8_t> placed;
   std::vector<int32_t> arr0;     // arrival time of vehicles restored as arrived (-1 otherwise)
@@ -191,6 +217,21 @@ static int upload(ts_sim *h, T **p, const std::vector<T> &v) {
   if (!v.empty())
     CK(h, cudaMemcpyAsync(*p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, h->stream));
   return TS_OK;
+}
+
+// parallel loop over [0, n) in contiguous chunks on the host cores (load
+// and init handle billions of route entries at the largest configs)
+template <typename F>
+static void parallel_for(int64_t n, F f) {
+  const int nt = (int)std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+  if (n < (int64_t)1 << 16 || nt == 1) {
+    f((int64_t)0, n, 0);
+    return;
+  }
+  std::vector<std::thread> th;
+  for (int i = 0; i < nt; i++)
+    th.emplace_back([=, &f]() { f(n * i / nt, n * (i + 1) / nt, i); });
+  for (auto &t : th) t.join();
 }
 
 extern "C" {
@@ -336,22 +377,40 @@ int ts_load_vehicles(ts_sim *h, int32_t n, const int64_t *route_off, const int32
   if (h->have_veh) return fail(h, TS_EINVAL, "vehicles already loaded");
   if (n < 0) return fail(h, TS_EINVAL, "negative vehicle count");
   if (n > 0 && route_off[0] != 0) return fail(h, TS_EINVAL, "route_off[0] != 0");
-  for (int32_t i = 0; i < n; i++) {
+  // validation in parallel over vehicles: error code of vehicle i (0 = ok);
+  // the first failing vehicle is reported
+  auto check = [&](int32_t i) -> int {
     const int64_t a = route_off[i], b = route_off[i + 1];
-    if (b <= a) return fail(h, TS_EINVAL, "vehicle %d: empty route", i);
+    if (b <= a) return 1;
     for (int64_t j = a; j < b; j++) {
       const int32_t k = route_links[j];
-      if (k < 0 || k >= h->nl) return fail(h, TS_EINVAL, "vehicle %d: bad link", i);
-      if (j > a && h->to[route_links[j - 1]] != h->from[k])
-        return fail(h, TS_EINVAL, "vehicle %d: route links not consecutive", i);
+      if (k < 0 || k >= h->nl) return 2;
+      if (j > a && h->to[route_links[j - 1]] != h->from[k]) return 3;
     }
-    if (entry_cell[i] < 0 || entry_cell[i] >= h->ncell[route_links[a]])
-      return fail(h, TS_EINVAL, "vehicle %d: entry cell outside link", i);
+    if (entry_cell[i] < 0 || entry_cell[i] >= h->ncell[route_links[a]]) return 4;
+    return 0;
+  };
+  std::vector<int32_t> first_bad(64, INT32_MAX);
+  parallel_for(n, [&](int64_t lo, int64_t hi, int t) {
+    for (int64_t i = lo; i < hi; i++)
+      if (check((int32_t)i)) {
+        first_bad[t] = (int32_t)i;
+        return;
+      }
+  });
+  const int32_t bad = *std::min_element(first_bad.begin(), first_bad.end());
+  if (bad != INT32_MAX) {
+    static const char *msg[] = {"", "empty route", "bad link", "route links not consecutive",
+                                "entry cell outside link"};
+    return fail(h, TS_EINVAL, "vehicle %d: %s", bad, msg[check(bad)]);
   }
   h->nv = n;
   h->roff.assign(route_off, route_off + n + 1);
   if (n == 0) h->roff.assign(1, 0);
-  h->route.assign(route_links, route_links + h->roff[n]);
+  h->route.resize(h->roff[n]);
+  parallel_for(h->roff[n], [&](int64_t lo, int64_t hi, int) {
+    std::copy(route_links + lo, route_links + hi, h->route.begin() + lo);
+  });
   h->dep.assign(depart, depart + n);
   h->entry.assign(entry_cell, entry_cell + n);
   h->placed.assign(n, 0);
@@ -898,7 +957,20 @@ static void pack_strips(ts_sim *h);
 int ts_init(ts_sim *h, int32_t t0) { return init_impl(h, t0, true); }
 int ts_resume(ts_sim *h, int32_t t) { return init_impl(h, t, false); }
 
+// TSIM_TRACE=1: wall-clock phases of ts_init on stderr (host-side tuning)
+struct InitTrace {
+  bool on = getenv("TSIM_TRACE") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void operator()(const char *what) {
+    if (!on) return;
+    const auto n = std::chrono::steady_clock::now();
+    fprintf(stderr, "[tsim init] %-28s %8.3f s\n", what, std::chrono::duration<double>(n - t).count());
+    t = n;
+  }
+};
+
 static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
+  InitTrace trace;
   if (!h) return TS_EINVAL;
   if (!h->have_veh) return fail(h, TS_EINVAL, "load vehicles first");
   if (h->inited) return fail(h, TS_EINVAL, "already initialised");
@@ -931,15 +1003,19 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
     h->n_placed++;
   }
   std::vector<int32_t> vids(h->total_cells, -1);
-  for (const TileDesc &d : h->tiles) {  // per-row vid lists in cell order
-    const int Wp = row_pitch(d.w);
-    for (int l = 0; l < d.L; l++) {
-      const int64_t rb = d.off + (int64_t)l * Wp;
-      int64_t r = rb;
-      for (int x = 0; x < d.w; x++)
-        if (code[rb + x] != kEmpty) vids[r++] = cellvid[rb + x];
+  parallel_for((int64_t)h->tiles.size(), [&](int64_t lo, int64_t hi, int) {
+    for (int64_t ti = lo; ti < hi; ti++) {  // per-row vid lists in cell order
+      const TileDesc &d = h->tiles[ti];
+      const int Wp = row_pitch(d.w);
+      for (int l = 0; l < d.L; l++) {
+        const int64_t rb = d.off + (int64_t)l * Wp;
+        int64_t r = rb;
+        for (int x = 0; x < d.w; x++)
+          if (code[rb + x] != kEmpty) vids[r++] = cellvid[rb + x];
+      }
     }
-  }
+  });
+  trace("placement + row lists");
   std::vector<int32_t>().swap(cellvid);
   // general tiles: the byte layout at their own device offsets
   std::vector<uint8_t> gcode(h->gcells, kEmpty);
@@ -951,6 +1027,7 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
     std::copy(code.begin() + d.off, code.begin() + d.off + n, gcode.begin() + gd.off);
     std::copy(vids.begin() + d.off, vids.begin() + d.off + n, gvid.begin() + gd.off);
   }
+  trace("general tiles");
   // row tiles: bit-planes O, V0..V2, A0, A1 per row (group-interleaved);
   // list entries vid | slot << 27
   if (h->ngroups > 0 && h->nv > (int32_t)kVidMask)
@@ -963,7 +1040,8 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
     if (h->tile_row[ti] >= 0)
       for (int l = 0; l < h->tiles[ti].L; l++) row_tile[h->tile_row[ti] + l] = (int32_t)ti;
   std::vector<int32_t> gcnt(std::max(1, h->ngroups), 0);
-  for (int g = 0; g < h->ngroups; g++) {
+  parallel_for(h->ngroups, [&](int64_t glo, int64_t ghi, int) {
+  for (int g = (int)glo; g < (int)ghi; g++) {
     const int64_t k0 = h->gvoff[g];
     int64_t k = k0;  // the group's block: rows in slot order
     for (int sl = 0; sl < 32; sl++) {
@@ -995,8 +1073,10 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
     }
     gcnt[g] = (int32_t)(k - k0);
   }
+  });
   std::vector<uint8_t>().swap(code);
   std::vector<int32_t>().swap(vids);
+  trace("planes + vid blocks");
   // pending lists per first link in (departure, vid) order (R13)
   std::vector<int32_t> pend_off(h->nl + 1, 0), pend_list;
   auto mine = [&](int f) {  // pending vehicle whose entry cell this domain owns
@@ -1063,6 +1143,7 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
     CK(h, cudaMemcpyAsync(h->d_gcnt[0], gcnt.data(), gcnt.size() * 4, cudaMemcpyHostToDevice,
                           h->stream));
   }
+  trace("pending + uploads");
   {  // injection scratch of the row kernel: needed only if a row link has pending trips
     bool need = false;
     for (size_t ti = 0; ti < h->tiles.size() && !need; ti++)
@@ -1077,11 +1158,17 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
   if ((rc = upload(h, &h->d_tt, h->tt))) return rc;
   if ((rc = upload(h, &h->d_out_pos, h->out_pos))) return rc;
   {  // routes as out-slot sequences: rslot[j] = slot of R[j] at its from-node
-    std::vector<uint8_t> rslot(h->route.size(), 0xFF);
-    for (int f = 0; f < h->nv; f++)
-      for (int64_t j = h->roff[f] + 1; j < h->roff[f + 1]; j++)
-        rslot[j] = (uint8_t)h->out_pos[h->route[j]];
-    if ((rc = upload(h, &h->d_rslot, rslot))) return rc;
+    std::vector<uint8_t, UninitAlloc<uint8_t>> rslot(h->route.size());
+    parallel_for(h->nv, [&](int64_t lo, int64_t hi, int) {
+      for (int64_t f = lo; f < hi; f++) {
+        rslot[h->roff[f]] = 0xFF;
+        for (int64_t j = h->roff[f] + 1; j < h->roff[f + 1]; j++)
+          rslot[j] = (uint8_t)h->out_pos[h->route[j]];
+      }
+    });
+    if ((rc = dalloc(h, &h->d_rslot, rslot.size()))) return rc;
+    if (!rslot.empty())
+      CK(h, cudaMemcpy(h->d_rslot, rslot.data(), rslot.size(), cudaMemcpyHostToDevice));
     std::vector<NodeOut> nodeout(h->out_list.size());
     for (size_t i = 0; i < h->out_list.size(); i++) {
       const int k = h->out_list[i];
@@ -1120,6 +1207,7 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
   if ((rc = upload(h, &h->d_lanes, h->lanes))) return rc;
   if ((rc = upload(h, &h->d_lgid, h->lgid))) return rc;
   if ((rc = upload(h, &h->d_cls, h->cls))) return rc;
+  trace("routes + node tables");
   // launch geometry
   h->smem = h->lay.bytes;
   int wpb = std::max(1, std::min(8, (200 * 1024) / h->lay.bytes));
@@ -1163,6 +1251,7 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
     if ((rc = dalloc(h, &h->d_send, h->n_xs, 0xFF))) return rc;
     if ((rc = dalloc(h, &h->d_recv, h->n_xs, 0xFF))) return rc;
   }
+  trace("launch geometry + node lanes");
   // S(t0) into buffer 1: the initial injection of departure <= t0 (O1
   // §Init), or (resume) a plain pass that writes strips and counters
   h->gcur = 0;
@@ -1189,13 +1278,14 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
   CK(h, cudaMemcpy(st, h->d_stats + (size_t)(t0 & (kHist - 1)) * ST_N, sizeof st, cudaMemcpyDeviceToHost));
   h->injected = (int64_t)st[ST_INJ];
   // the host copies of the plans are no longer needed (all on the device)
-  std::vector<int32_t>().swap(h->route);
+  std::vector<int32_t, UninitAlloc<int32_t>>().swap(h->route);
   std::vector<int32_t>().swap(h->pl_vid);
   std::vector<int32_t>().swap(h->pl_cur);
   std::vector<int32_t>().swap(h->pl_lane);
   std::vector<int32_t>().swap(h->pl_cell);
   std::vector<int32_t>().swap(h->pl_v);
   h->inited = true;
+  trace("initial kernels");
   return TS_OK;
 }
 
@@ -1512,7 +1602,8 @@ static int download_tiles(ts_sim *h, int t0, int t1, std::vector<uint8_t> &code,
         for (int wd = 0; wd < kRowWords; wd++) k += __builtin_popcount(P[wd * 32]);
       }
     }
-    for (int ti = t0; ti < t1; ti++) {
+    parallel_for(t1 - t0, [&](int64_t lo, int64_t hi, int) {
+    for (int ti = t0 + (int)lo; ti < t0 + (int)hi; ti++) {
       if (h->tile_row[ti] < 0) continue;
       const TileDesc &d = h->tiles[ti];
       const int Wp = row_pitch(d.w);
@@ -1534,6 +1625,7 @@ static int download_tiles(ts_sim *h, int t0, int t1, std::vector<uint8_t> &code,
         }
       }
     }
+    });
   }
   return TS_OK;
 }
@@ -1553,24 +1645,32 @@ int ts_read_vehicles(ts_sim *h, int8_t *status, int32_t *link, int32_t *lane, in
   for (int f = 0; f < h->nv; f++) cur[f] = (int32_t)(vp[f].p - h->roff[f]);
   std::vector<int32_t> lk(h->nv, -1), ln(h->nv, -1), ce(h->nv, -1), vv(h->nv, -1);
   std::vector<uint8_t> seen(h->nv, 0);
-  for (const TileDesc &d : h->tiles) {
-    for (int l = 0; l < d.L; l++) {
-      const int64_t rb = d.off + (int64_t)l * row_pitch(d.w);
-      int64_t r = rb;
-      for (int x = 0; x < d.w; x++) {
-        uint8_t c = code[rb + x];
-        if (c & 0x80) continue;
-        int f = vids[r++];
-        if (f < 0 || f >= h->nv || seen[f])
-          return fail(h, TS_EINTERNAL, "corrupt state: vid %d at link %d", f, d.link);
-        seen[f] = 1;
-        lk[f] = d.link;
-        ln[f] = l;
-        ce[f] = d.a + x;
-        vv[f] = c & 7;
+  std::vector<int64_t> bad(64, -1);  // per thread: a corrupt entry (vid << 32 | link)
+  parallel_for((int64_t)h->tiles.size(), [&](int64_t lo, int64_t hi, int th) {
+    for (int64_t ti = lo; ti < hi; ti++) {
+      const TileDesc &d = h->tiles[ti];
+      for (int l = 0; l < d.L; l++) {
+        const int64_t rb = d.off + (int64_t)l * row_pitch(d.w);
+        int64_t r = rb;
+        for (int x = 0; x < d.w; x++) {
+          uint8_t c = code[rb + x];
+          if (c & 0x80) continue;
+          int f = vids[r++];
+          if (f < 0 || f >= h->nv || __atomic_exchange_n(&seen[f], (uint8_t)1, __ATOMIC_RELAXED)) {
+            bad[th] = ((int64_t)f << 32) | (uint32_t)d.link;
+            return;
+          }
+          lk[f] = d.link;
+          ln[f] = l;
+          ce[f] = d.a + x;
+          vv[f] = c & 7;
+        }
       }
     }
-  }
+  });
+  for (int64_t b : bad)
+    if (b != -1)
+      return fail(h, TS_EINTERNAL, "corrupt state: vid %d at link %d", (int)(b >> 32), (int)(int32_t)b);
   for (int f = 0; f < h->nv; f++) {
     int8_t s = TS_ACTIVE;
     if (seen[f]) s = TS_ACTIVE;
