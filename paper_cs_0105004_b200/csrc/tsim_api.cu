@@ -569,7 +569,10 @@ static void build_tiles(ts_sim *h) {
     h->link_tile0[k] = (int32_t)h->tiles.size();
     if (span <= 0) continue;
     const bool split = lo > 0 || hi < n;
-    int nt = (span + tc - 1) / tc;
+    // the ring is one very long link: smaller tiles give its warp-per-tile
+    // kernels more warps (config 2: 512 -> 91 us, 256 -> 66 us per step)
+    const int tck = (per && h->cfg.tile_cells <= 0) ? 256 : tc;
+    int nt = (span + tck - 1) / tck;
     if (nt > 1 && span / nt < 10) nt = std::max(1, span / 10);
     h->link_ntiles[k] = nt;
     const bool halo = per || nt > 1 || split;
