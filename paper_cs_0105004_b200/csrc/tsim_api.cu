@@ -170,6 +170,15 @@ struct ts_sim {
   int64_t veh_updates = 0, arrived = 0, injected = 0, n_placed = 0, n_arrived0 = 0;
   // timing
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // CUDA-graph replay of kGraphSteps steps (TS_FLAG_GRAPH): the kernels read
+  // the step time from the device clock d_clock; while capturing, step and
+  // node parameters carry t - graph_t0 and tdev = d_clock
+  int32_t *d_clock = nullptr;
+  // one graph per parity of the double buffers (rcur, gcur) at its start
+  cudaGraphExec_t graph_exec[4] = {nullptr, nullptr, nullptr, nullptr};
+  unsigned long long graph_gctr_end[4] = {0, 0, 0, 0};
+  bool graph_off = false, capturing = false;
+  int32_t graph_t0 = 0;
   std::vector<cudaEvent_t> mv_ev;
   double last_total_ms = 0, last_move_ms = 0;
   int64_t last_move_launches = 0;
@@ -272,6 +281,8 @@ void ts_destroy(ts_sim *h) {
   if (h->stream) cudaStreamSynchronize(h->stream);
   for (void *p : h->allocs) cudaFree(p);
   for (auto e : h->mv_ev) cudaEventDestroy(e);
+  for (auto g : h->graph_exec)
+    if (g) cudaGraphExecDestroy(g);
   if (h->ev0) cudaEventDestroy(h->ev0);
   if (h->ev1) cudaEventDestroy(h->ev1);
   if (h->stream) cudaStreamDestroy(h->stream);
@@ -834,6 +845,10 @@ static int first_slot(const ts_sim *h, int f) {
 
 static StepParams step_params(ts_sim *h, int t, int mode) {
   StepParams P{};
+  if (h->capturing) {
+    P.tdev = h->d_clock;
+    t -= h->graph_t0;
+  }
   P.tiles = h->d_tiles;
   P.ntiles = (int32_t)h->gtiles.size();
   P.t = t;
@@ -876,6 +891,10 @@ static StepParams step_params(ts_sim *h, int t, int mode) {
 
 static NodeParams node_params(ts_sim *h, int t) {
   NodeParams N{};
+  if (h->capturing) {
+    N.tdev = h->d_clock;
+    t -= h->graph_t0;
+  }
   N.nnodes = h->periodic >= 0 ? 0 : (int32_t)h->my_nodes.size();
   N.node_ids = h->d_node_ids;
   N.t = t;
@@ -1351,6 +1370,73 @@ static void phase_move(ts_sim *h, bool more, cudaEvent_t e0, cudaEvent_t e1) {
 }
 
 constexpr int kTimingStride = 8;
+// steps per CUDA graph: odd, so that the row buffers return to their parity
+// (one lane-change-only launch + kGraphSteps move launches flip them)
+constexpr int kGraphSteps = 15;
+
+// both tile kinds hold S(t) with its lane change pending (bits 1: rows, 2:
+// general tiles; a kind without tiles counts as pending)
+static int pending_lc(const ts_sim *h) {
+  return ((h->ngroups == 0 || !h->rows_s1) ? 1 : 0) | ((h->gtiles.empty() || !h->gen_s1) ? 2 : 0);
+}
+
+// capture kGraphSteps steps from the current state (lane change of S(t)
+// pending) into h->graph_exec; false if the capture is not possible
+static int graph_key(const ts_sim *h) { return (h->rcur & 1) | ((h->gcur & 1) << 1); }
+
+static bool capture_graph(ts_sim *h) {
+  if (!h->d_clock && dalloc(h, &h->d_clock, 1, 0)) return false;
+  const int key = graph_key(h);
+  const int t0 = h->t, rc0 = h->rcur, gc0 = h->gcur;
+  const bool rs0 = h->rows_s1, gs0 = h->gen_s1;
+  const unsigned long long gb0 = h->gctr_base;
+  h->capturing = true;
+  h->graph_t0 = t0;
+  h->gctr_base = 0;
+  cudaGraph_t graph = nullptr;
+  bool ok = cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+  if (ok) {
+    cudaMemsetAsync(h->d_gctr, 0, sizeof(unsigned long long), h->stream);
+    launch_clock(h->d_clock, h->d_stats, kGraphSteps + 1, false, h->stream);
+    for (int i = 0; i < kGraphSteps; i++) {
+      phase_lc(h);
+      phase_move(h, i < kGraphSteps - 1, nullptr, nullptr);
+    }
+    launch_clock(h->d_clock, h->d_stats, kGraphSteps, true, h->stream);
+    const cudaError_t e = cudaStreamEndCapture(h->stream, &graph);
+    ok = e == cudaSuccess && graph;
+    if (!ok && getenv("TSIM_TRACE")) fprintf(stderr, "[tsim] end capture: %s\n", cudaGetErrorString(e));
+  }
+  const bool parity = h->rcur == rc0 && h->gcur == gc0 && pending_lc(h) == 3;
+  if (!parity && getenv("TSIM_TRACE"))
+    fprintf(stderr, "[tsim] graph parity: rcur %d->%d gcur %d->%d rows_s1 %d->%d gen_s1 %d->%d\n", rc0,
+            h->rcur, gc0, h->gcur, rs0, h->rows_s1, gs0, h->gen_s1);
+  ok = ok && parity;
+  if (ok) {
+    const cudaError_t e = cudaGraphInstantiate(&h->graph_exec[key], graph, 0);
+    ok = e == cudaSuccess;
+    if (!ok && getenv("TSIM_TRACE")) fprintf(stderr, "[tsim] instantiate: %s\n", cudaGetErrorString(e));
+  }
+  if (graph) cudaGraphDestroy(graph);
+  h->graph_gctr_end[key] = h->gctr_base;
+  h->capturing = false;
+  h->t = t0;
+  h->rcur = rc0;
+  h->gcur = gc0;
+  h->rows_s1 = rs0;
+  h->gen_s1 = gs0;
+  h->gctr_base = gb0;
+  cudaGetLastError();  // a failed capture leaves no sticky error
+  if (getenv("TSIM_TRACE"))
+    fprintf(stderr, "[tsim] graph capture of %d steps at t=%d: %s\n", kGraphSteps, t0,
+            ok ? "ok" : "failed (steps launched one by one)");
+  if (!ok) {
+    if (h->graph_exec[key]) cudaGraphExecDestroy(h->graph_exec[key]);
+    h->graph_exec[key] = nullptr;
+    h->graph_off = true;
+  }
+  return ok;
+}
 
 static int enqueue_steps(ts_sim *h, int32_t n) {
   if (!h || !h->inited) return fail(h, TS_EINVAL, "call ts_init first");
@@ -1359,7 +1445,21 @@ static int enqueue_steps(ts_sim *h, int32_t n) {
     return fail(h, TS_EINVAL, "domain with neighbours: step with ts_step_phase and an exchange");
   if (n == 0) return TS_OK;
   CK(h, cudaSetDevice(h->dev));
-  if (zero_stats(h, h->t + 1, std::min(n + 1, kHist))) return TS_EINTERNAL;
+  // TS_FLAG_GRAPH: whole kGraphSteps blocks of steps replay one CUDA graph
+  int reps = 0;
+  if ((h->cfg.flags & TS_FLAG_GRAPH) && !h->graph_off && n >= kGraphSteps && pending_lc(h) == 3 &&
+      (h->graph_exec[graph_key(h)] || capture_graph(h)))
+    reps = n / kGraphSteps;
+  CK(h, cudaEventRecord(h->ev0, h->stream));
+  if (reps) {
+    CK(h, cudaMemcpyAsync(h->d_clock, &h->t, sizeof(int32_t), cudaMemcpyHostToDevice, h->stream));
+    const int key = graph_key(h);  // the buffer parity is the same after every replay
+    for (int r = 0; r < reps; r++) CK(h, cudaGraphLaunch(h->graph_exec[key], h->stream));
+    h->t += reps * kGraphSteps;
+    h->gctr_base = h->graph_gctr_end[key];
+    n -= reps * kGraphSteps;
+  }
+  if (n > 0 && zero_stats(h, h->t + 1, std::min(n + 1, kHist))) return TS_EINTERNAL;
   if ((int)h->mv_ev.size() < 2 * n && h->timing) {
     while ((int)h->mv_ev.size() < 2 * n) {
       cudaEvent_t e;
@@ -1367,7 +1467,6 @@ static int enqueue_steps(ts_sim *h, int32_t n) {
       h->mv_ev.push_back(e);
     }
   }
-  CK(h, cudaEventRecord(h->ev0, h->stream));
   // the move kernel is timed on every kTimingStride-th step only: events
   // between two kernels would serialise their programmatic overlap
   int ns = 0;

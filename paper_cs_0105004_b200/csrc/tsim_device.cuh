@@ -38,6 +38,16 @@ static inline cudaError_t launch_pdl(void (*kern)(KArgs...), int blocks, int thr
   return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
+// ------------------------------------------------------ step time
+// Kernels replayed from a CUDA graph read the step time from the device
+// clock (tdev); the captured t is the offset within the graph.
+template <typename Params>
+static __device__ __forceinline__ Params with_time(const Params &p) {
+  Params q = p;
+  if (p.tdev) q.t += *p.tdev;
+  return q;
+}
+
 // ------------------------------------------------------------- Philox
 // Philox4x32-10 (Salmon et al., SC'11) with the curand round and Weyl
 // constants, counter (t, vid, 0, 0), key (k0, k1); only output word 0 is

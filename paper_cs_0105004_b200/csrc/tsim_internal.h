@@ -190,6 +190,7 @@ struct StepParams {
   const TileDesc *tiles;
   int32_t ntiles;
   int32_t t;  // step t: S1(t) -> S(t+1); k_lc: S(t) -> S1(t)
+  const int32_t *tdev;  // CUDA-graph replay: t = *tdev + t (NULL: t as is)
   int32_t mode;
   int32_t D;
   uint32_t k0, k1;
@@ -234,6 +235,7 @@ struct NodeParams {
   int32_t nnodes;            // nodes of this domain
   const int32_t *node_ids;   // their ids (NULL: 0..nnodes-1)
   int32_t t;
+  const int32_t *tdev;       // CUDA-graph replay: t = *tdev + t (NULL: t as is)
   int32_t G;
   uint32_t k0, k1;
   uint64_t p32;
@@ -291,6 +293,9 @@ struct NodeWarpParams {
 };
 
 void launch_lc(const StepParams &p, int blocks, int threads, int smem, void *stream);
+// CUDA-graph clock: zero the stats slots of steps *clock + 1 .. *clock + n
+// (before the replayed steps), or advance *clock by n (after them)
+void launch_clock(int32_t *clock, unsigned long long *stats, int n, bool advance, void *stream);
 void launch_rows(const StepParams &p, const RowsParams &r, int blocks, int threads, int smem,
                  void *stream, bool pdl = false);
 void launch_node_warp(const NodeParams &p, const NodeWarpParams &w, void *stream, bool pdl = false);

@@ -291,7 +291,8 @@ __device__ __forceinline__ void move_one(const StepParams &P, TileCtx &T, Acc &a
 }
 
 // ------------------------------------------------------------- k_lc
-__global__ void __launch_bounds__(256) k_lc(const StepParams P) {
+__global__ void __launch_bounds__(256) k_lc(const StepParams P_) {
+  const StepParams P = with_time(P_);
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ unsigned long long red[8 * 8];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -340,7 +341,8 @@ __global__ void __launch_bounds__(256) k_lc(const StepParams P) {
 }
 
 // ------------------------------------------------------------- k_step
-__global__ void __launch_bounds__(256) k_step(const StepParams P) {
+__global__ void __launch_bounds__(256) k_step(const StepParams P_) {
+  const StepParams P = with_time(P_);
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ unsigned long long red[8 * 8];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -533,7 +535,8 @@ __device__ __forceinline__ void node_flush(const NodeParams &P, uint32_t crossin
 #define TS_NODE_ILP 1  // measured on 4a: 1 -> 31.5 us, 2 -> 35, 4 -> 39.6, 8 -> 49.6
 #endif
 constexpr int kNodeILP = TS_NODE_ILP;
-__global__ void __launch_bounds__(256) k_node_warp(const NodeParams P, const NodeWarpParams W) {
+__global__ void __launch_bounds__(256) k_node_warp(const NodeParams P_, const NodeWarpParams W) {
+  const NodeParams P = with_time(P_);
   __shared__ unsigned long long red[8];
   const int lane = threadIdx.x & 31;
   const uint32_t gmask = (1u << P.G) - 1u;
@@ -590,7 +593,8 @@ __global__ void __launch_bounds__(256) k_node_warp(const NodeParams P, const Nod
 }
 
 // general fallback: one thread per node (any in-degree)
-__global__ void __launch_bounds__(128) k_node(const NodeParams P) {
+__global__ void __launch_bounds__(128) k_node(const NodeParams P_) {
+  const NodeParams P = with_time(P_);
   __shared__ unsigned long long red[4];
   const int ni = blockIdx.x * blockDim.x + threadIdx.x;
   uint32_t crossings = 0;
@@ -681,6 +685,19 @@ void launch_node(const NodeParams &p, void *stream) {
   if (p.nnodes <= 0) return;
   k_node<<<(p.nnodes + 127) / 128, 128, 0, (cudaStream_t)stream>>>(p);
 }
+__global__ void k_clock(int32_t *clock, unsigned long long *stats, int n, int advance) {
+  if (advance) {
+    if (threadIdx.x == 0) *clock += n;
+    return;
+  }
+  const int t0 = *clock;
+  for (int i = threadIdx.x; i < n * ST_N; i += blockDim.x)
+    stats[(size_t)((t0 + 1 + i / ST_N) & (kHist - 1)) * ST_N + i % ST_N] = 0ull;
+}
+void launch_clock(int32_t *clock, unsigned long long *stats, int n, bool advance, void *stream) {
+  k_clock<<<1, 256, 0, (cudaStream_t)stream>>>(clock, stats, n, advance ? 1 : 0);
+}
+
 void launch_node_warp(const NodeParams &p, const NodeWarpParams &w, void *stream, bool pdl) {
   if (w.nchunks <= 0) return;
   const int blocks = (w.nchunks + 8 * kNodeILP - 1) / (8 * kNodeILP);

@@ -234,7 +234,8 @@ static __device__ __noinline__ uint32_t zone_lc(uint32_t zc, int c0, int w, int 
 // MODE = the uniform mode bits kModeMove | kModeLC | kModeHash of the launch
 // (specialised so the hot fused instantiation carries no dead paths)
 template <int MODE>
-__global__ void __launch_bounds__(128, TS_ROWS_MINB) k_rows(const StepParams P, const RowsParams R) {
+__global__ void __launch_bounds__(128, TS_ROWS_MINB) k_rows(const StepParams P_, const RowsParams R) {
+  const StepParams P = with_time(P_);
   __shared__ unsigned long long red[4 * 8];
   extern __shared__ __align__(16) int32_t stage[];  // per warp: vid block in, vid block out
   const int lane = threadIdx.x & 31;

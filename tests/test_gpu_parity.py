@@ -185,3 +185,35 @@ def test_signalized_portland(g0, g1):
     s.depart = (s.depart // 20).astype(np.int32)
     s = scenarios.with_signals(s, green0=g0, green1=g1, seed=g0)
     run_parity(s, 250, FUSED, full_every=50, hash_every=50)
+
+
+# ------------------------------------------- CUDA-graph replay (TS_FLAG_GRAPH)
+GRAPH = FUSED | tsim.FLAG_GRAPH
+GRAPH_GENERAL = GENERAL | tsim.FLAG_GRAPH
+
+
+@pytest.mark.parametrize("chunk", [15, 47, 100])
+def test_graph_replay_grid(chunk):
+    """steps replayed from one captured graph of 15 steps (the step time read
+    from the device clock) plus normally launched remainders: every
+    per-step hash equals the oracle's"""
+    s = scenarios.grid_trips(rows=6, cols=6, n_veh=3000, depart_max=300, seed=8, name="grid6g")
+    run_parity(s, 400, GRAPH, full_every=0, hash_every=chunk)
+    s = scenarios.big_grid(rows=20, cols=20, seed=4, name="grid20g")
+    run_parity(s, 150, GRAPH, full_every=0, hash_every=chunk)
+
+
+@pytest.mark.parametrize("flags", [GRAPH, GRAPH_GENERAL])
+def test_graph_replay_mixed(flags):
+    """row and general tiles, signals, long links, injection: graph replays
+    across 400 steps, full state checked after every call"""
+    s = scenarios.portland(n_nodes=600, n_edges=800, n_veh=8000, side_km=8.0, n_zones=64, seed=2)
+    s.depart = (s.depart // 12).astype(np.int32)
+    s = scenarios.with_signals(s, green0=20, green1=25, seed=4)
+    run_parity(s, 400, flags, full_every=1, hash_every=45)
+
+
+def test_graph_replay_ring():
+    """the periodic ring (general tiles only, lane change not fusable)"""
+    s = scenarios.ring(n_cells=3000, lanes=3, density=0.2, seed=5)
+    run_parity(s, 150, GRAPH, full_every=1, hash_every=30)
