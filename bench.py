@@ -143,6 +143,12 @@ def run_oracle(name, steps, warmup, budget_s=None):
                 lane_cells=int(o.lib.or_total_lane_cells(o.h)))
 
 
+# names of the scenarios (scenarios.config(name).name) without generating them
+WORKLOAD_NAMES = {"1": "config1_grid4x4", "2": "config2_ring", "3": "config3_portland",
+                  "4a": "config4a_grid256", "4b": "config4b_grid256_1M",
+                  "5": "config5_portland_x8"}
+
+
 def bench_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -154,7 +160,9 @@ def bench_reference(args):
         "warmup": args.warmup, "ms_per_step": 1000 * r["seconds"] / max(1, r["steps"]),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
         "data": "synthetic",
-        "config": {"workload": f"config {args.config} sample: {r['desc']}"},
+        "config": {"workload": WORKLOAD_NAMES.get(args.config, f"config{args.config}"),
+                   "sample": r["desc"], "l2": "sample runs on the host (CPU oracle)",
+                   "parallelism": "1 host thread"},
         "cpu_baseline": {"value": r["value"], "unit": "vehicle-updates/s", "cores": 1,
                          "kind": "oracle", "sample": r["desc"]},
         "e2e": {"value": r["value"], "unit": "vehicle-updates/s", "h2d_bytes_per_step": 0,
