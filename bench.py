@@ -272,7 +272,12 @@ def bench_multi(args):
     dom = domains.partition(scn, world)
     n_spl, pairs = domains.split_stats(scn, dom)
     w0 = time.perf_counter()
-    d = domains.DistDomain(scn, dom, device=local, flags=tsim.FLAG_FUSED)
+    # native exchanges (the library's own NCCL communicator, whole steps per
+    # ts_step call); torch.distributed send/recv between the phases otherwise
+    try:
+        d = domains.DistDomain(scn, dom, device=local, flags=tsim.FLAG_FUSED, native=True)
+    except tsim.TsError:
+        d = domains.DistDomain(scn, dom, device=local, flags=tsim.FLAG_FUSED)
     d.step(args.warmup)
     torch.cuda.synchronize()
     dist.barrier()
@@ -313,7 +318,8 @@ def bench_multi(args):
                        "vehicles": scn.n_vehicles,
                        "l2": "inputs larger than L2 (state read+written per step > 126 MB)",
                        "parallelism": f"{world} GPUs, ORB domains, split links, 2 NCCL strip "
-                                      f"exchanges per step", "split_links": n_spl,
+                                      f"exchanges per step ({'native' if d.native else 'torch'})",
+                       "split_links": n_spl,
                        "domain_pairs": len(pairs)},
             "real_time_ratio": args.steps / (ms_total / 1e3),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",

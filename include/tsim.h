@@ -250,6 +250,21 @@ int ts_multilevel_partition(int32_t n_nodes, const int64_t *node_x_mm, const int
                             const int32_t *lanes, const double *node_weight, int32_t k,
                             double imbalance, uint64_t seed, int32_t *domain_of_node);
 
+/* Native exchange transport for domain mode (G1, H2/H7; PAPER.md:404-427,
+ * 897-900): NCCL point-to-point inside the library, so that ts_step(n) runs
+ * whole steps (lane change, exchange #1, move, exchange #2) for a domain with
+ * neighbours without a host round trip per exchange.  libnccl.so.2 is opened
+ * at run time (the copy already loaded by the process, else the system's).
+ * ts_nccl_unique_id: writes a 128-byte ncclUniqueId (one rank creates it, the
+ * caller distributes it).  ts_nccl_init: after ts_init, join the
+ * communicator of nranks = k ranks as rank = this handle's domain (one GPU
+ * per rank).  ts_exchange: one exchange of the packed strips now (e.g. the
+ * one after ts_init), enqueued on the handle's stream.  TS_EINTERNAL if NCCL
+ * is missing or fails; TS_EINVAL for ranks that are not the domains. */
+int ts_nccl_unique_id(void *id128);
+int ts_nccl_init(ts_sim *h, const void *id128, int32_t nranks, int32_t rank);
+int ts_exchange(ts_sim *h);
+
 /* Kernel-level timing of the last ts_step call (CUDA events on the
  * handle's stream): total ms, and ms inside the dominant (move) kernel. */
 int ts_last_timing(ts_sim *h, double *total_ms, double *move_ms,

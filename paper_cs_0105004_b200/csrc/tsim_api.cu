@@ -2,6 +2,8 @@
 // tiling and device layout, kernel orchestration, state read-back.
 // C-ABI declared in include/tsim.h.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <climits>
@@ -96,6 +98,7 @@ struct ts_sim {
   int64_t n_xs = 0;  // strips per exchange (sum over neighbours)
   Strip *d_send = nullptr, *d_recv = nullptr;
   int32_t *d_send_slot = nullptr, *d_recv_slot = nullptr;
+  ncclComm_t comm = nullptr;  // native exchange transport (ts_nccl_init)
   std::vector<int32_t> my_nodes;
   int32_t *d_node_ids = nullptr;
   std::vector<uint32_t> node_sig;  // per node: phase-0 signal word (R23), 0 = none
@@ -243,7 +246,101 @@ static void parallel_for(int64_t n, F f) {
   for (auto &t : th) t.join();
 }
 
+// ---------------------------------------------------------------- NCCL
+// The strip exchanges of domain mode (H2/H7) can run inside the library over
+// NCCL point-to-point (NVLink between the GPUs of one node), so ts_step(n)
+// runs whole steps with neighbours and no host round trip per exchange.
+// libnccl is opened at run time (the one torch already loaded, else the
+// system's): single-GPU use needs no NCCL.
+struct NcclApi {
+  bool tried = false, ok = false;
+  ncclResult_t (*getUniqueId)(ncclUniqueId *) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*groupStart)() = nullptr;
+  ncclResult_t (*groupEnd)() = nullptr;
+  ncclResult_t (*send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  const char *(*errorString)(ncclResult_t) = nullptr;
+};
+
+static NcclApi &nccl() {
+  static NcclApi a;
+  if (a.tried) return a;
+  a.tried = true;
+  void *lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+  if (!lib) lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!lib) lib = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!lib) return a;
+  a.getUniqueId = (decltype(a.getUniqueId))dlsym(lib, "ncclGetUniqueId");
+  a.commInitRank = (decltype(a.commInitRank))dlsym(lib, "ncclCommInitRank");
+  a.commDestroy = (decltype(a.commDestroy))dlsym(lib, "ncclCommDestroy");
+  a.groupStart = (decltype(a.groupStart))dlsym(lib, "ncclGroupStart");
+  a.groupEnd = (decltype(a.groupEnd))dlsym(lib, "ncclGroupEnd");
+  a.send = (decltype(a.send))dlsym(lib, "ncclSend");
+  a.recv = (decltype(a.recv))dlsym(lib, "ncclRecv");
+  a.errorString = (decltype(a.errorString))dlsym(lib, "ncclGetErrorString");
+  a.ok = a.getUniqueId && a.commInitRank && a.commDestroy && a.groupStart && a.groupEnd &&
+         a.send && a.recv && a.errorString;
+  return a;
+}
+
+#define NCK(h, x)                                                                       \
+  do {                                                                                   \
+    ncclResult_t r_ = (x);                                                               \
+    if (r_ != ncclSuccess)                                                               \
+      return fail(h, TS_EINTERNAL, "%s failed: %s", #x, nccl().errorString(r_));         \
+  } while (0)
+
+// one exchange: the packed strips to and from every neighbour domain, one
+// message each way per neighbour, on the handle's stream
+static int nccl_exchange(ts_sim *h) {
+  if (h->nbrs.empty()) return TS_OK;
+  NcclApi &a = nccl();
+  NCK(h, a.groupStart());
+  for (const ts_sim::Nbr &nb : h->nbrs) {
+    const size_t bytes = nb.send_slot.size() * sizeof(Strip);
+    NCK(h, a.send(h->d_send + nb.off, bytes, ncclUint8, nb.dom, h->comm, h->stream));
+    NCK(h, a.recv(h->d_recv + nb.off, bytes, ncclUint8, nb.dom, h->comm, h->stream));
+  }
+  NCK(h, a.groupEnd());
+  return TS_OK;
+}
+
 extern "C" {
+
+int ts_nccl_unique_id(void *id128) {
+  if (!id128) return TS_EINVAL;
+  NcclApi &a = nccl();
+  if (!a.ok) return TS_EINTERNAL;
+  ncclUniqueId id;
+  if (a.getUniqueId(&id) != ncclSuccess) return TS_EINTERNAL;
+  memcpy(id128, &id, sizeof(id));
+  return TS_OK;
+}
+
+int ts_nccl_init(ts_sim *h, const void *id128, int32_t nranks, int32_t rank) {
+  if (!h || !id128) return TS_EINVAL;
+  if (!h->inited) return fail(h, TS_EINVAL, "call ts_init first");
+  if (h->comm) return fail(h, TS_EINVAL, "communicator already set");
+  if (nranks != h->dom_k || rank != h->dom_me)
+    return fail(h, TS_EINVAL, "ranks must be the domains: nranks %d != k %d or rank %d != domain %d",
+                nranks, h->dom_k, rank, h->dom_me);
+  NcclApi &a = nccl();
+  if (!a.ok) return fail(h, TS_EINTERNAL, "libnccl.so.2 not found");
+  CK(h, cudaSetDevice(h->dev));
+  ncclUniqueId id;
+  memcpy(&id, id128, sizeof(id));
+  NCK(h, a.commInitRank(&h->comm, nranks, id, rank));
+  return TS_OK;
+}
+
+int ts_exchange(ts_sim *h) {
+  if (!h || !h->inited) return fail(h, TS_EINVAL, "call ts_init first");
+  if (!h->comm) return fail(h, TS_EINVAL, "no communicator (ts_nccl_init)");
+  CK(h, cudaSetDevice(h->dev));
+  return nccl_exchange(h);
+}
 
 int ts_create(const ts_config *cfg, ts_sim **out) {
   if (!out) return fail(nullptr, TS_EINVAL, "out is NULL");
@@ -281,6 +378,7 @@ void ts_destroy(ts_sim *h) {
   if (h->stream) cudaStreamSynchronize(h->stream);
   for (void *p : h->allocs) cudaFree(p);
   for (auto e : h->mv_ev) cudaEventDestroy(e);
+  if (h->comm) nccl().commDestroy(h->comm);
   for (auto g : h->graph_exec)
     if (g) cudaGraphExecDestroy(g);
   if (h->ev0) cudaEventDestroy(h->ev0);
@@ -1441,10 +1539,25 @@ static bool capture_graph(ts_sim *h) {
 static int enqueue_steps(ts_sim *h, int32_t n) {
   if (!h || !h->inited) return fail(h, TS_EINVAL, "call ts_init first");
   if (n < 0) return fail(h, TS_EINVAL, "negative step count");
-  if (h->n_xs > 0)
-    return fail(h, TS_EINVAL, "domain with neighbours: step with ts_step_phase and an exchange");
+  if (h->n_xs > 0 && !h->comm)
+    return fail(h, TS_EINVAL, "domain with neighbours: ts_nccl_init, or ts_step_phase and an exchange");
   if (n == 0) return TS_OK;
   CK(h, cudaSetDevice(h->dev));
+  if (h->n_xs > 0) {  // whole steps with the native exchange (G1): LC, #1, move, #2
+    if (zero_stats(h, h->t + 1, std::min(n + 1, kHist))) return TS_EINTERNAL;
+    CK(h, cudaEventRecord(h->ev0, h->stream));
+    for (int i = 0; i < n; i++) {
+      phase_lc(h);
+      if (int rc = nccl_exchange(h)) return rc;
+      phase_move(h, i < n - 1, nullptr, nullptr);
+      if (int rc = nccl_exchange(h)) return rc;
+      unpack_strips(h);
+    }
+    CK(h, cudaEventRecord(h->ev1, h->stream));
+    CK(h, cudaGetLastError());
+    h->last_move_launches = 0;
+    return TS_OK;
+  }
   // TS_FLAG_GRAPH: whole kGraphSteps blocks of steps replay one CUDA graph
   int reps = 0;
   if ((h->cfg.flags & TS_FLAG_GRAPH) && !h->graph_off && n >= kGraphSteps && pending_lc(h) == 3 &&

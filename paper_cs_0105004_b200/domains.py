@@ -206,10 +206,13 @@ class _CudaBuf:
 
 
 class DistDomain:
-    """The domain of this rank; exchanges over torch.distributed."""
+    """The domain of this rank.  Exchanges: native (the library's own NCCL
+    communicator; ts_step runs whole steps) when `native` and the group is
+    the whole world with ranks = domains, else torch.distributed
+    batched isend / irecv between the phases."""
 
     def __init__(self, scn, domain_of_node, device=0, t0=0, flags=_t.FLAG_FUSED, group=None,
-                 state=None, **kw):
+                 state=None, native=False, **kw):
         import torch
         import torch.distributed as dist
         self.group = group
@@ -234,15 +237,27 @@ class DistDomain:
                       for _, n, off in self.plan]
         self.stream = torch.cuda.ExternalStream(self.sim.stream(), device=cuda)
         self.exchange_ms = 0.0
+        self.native = False
+        if native and group is None:
+            uid = [_t.nccl_unique_id() if self.rank == 0 else None]
+            dist.broadcast_object_list(uid, src=0)
+            self.sim.nccl_init(uid[0], self.k, self.rank)
+            self.native = True
         self.exchange()
         self.sim.phase(2)
 
     def exchange(self):
+        if self.native:
+            self.sim.exchange()
+            return
         import torch
         with torch.cuda.stream(self.stream):
             exchange_p2p(self.sends, self.recvs, self.peers, self.group)
 
     def step(self, n=1):
+        if self.native:  # whole steps inside the library (both exchanges native)
+            self.sim.step(n)
+            return
         for i in range(n):
             self.sim.phase(0)
             self.exchange()

@@ -72,6 +72,9 @@ def load_library():
         "ts_set_signals": (ctypes.c_int, [P, I32, P, P, P, P]),
         "ts_domain_plan": (ctypes.c_int, [I32, I32, P, P, P, P, I32, P, I32, I32, P, P, P]),
         "ts_strip_bytes": (I32, []),
+        "ts_nccl_unique_id": (ctypes.c_int, [P]),
+        "ts_nccl_init": (ctypes.c_int, [P, P, I32, I32]),
+        "ts_exchange": (ctypes.c_int, [P]),
         "ts_resume": (ctypes.c_int, [P, I32]),
         "ts_step_phase": (ctypes.c_int, [P, I32, I32]),
         "ts_exchange_plan": (ctypes.c_int, [P, I32, P, P, P, P]),
@@ -155,6 +158,14 @@ def domain_plan(scn, k, domain_of_node, me):
     if rc:
         raise TsError(f"ts_domain_plan failed ({rc})")
     return nb[:n.value].tolist(), ns[:n.value].tolist()
+
+
+def nccl_unique_id():
+    """128-byte NCCL communicator id for ts_nccl_init (one rank creates it)"""
+    buf = ctypes.create_string_buffer(128)
+    if load_library().ts_nccl_unique_id(buf):
+        raise TsError("ts_nccl_unique_id failed (libnccl.so.2 not found?)")
+    return buf.raw
 
 
 def exchange_local(sims):
@@ -251,6 +262,15 @@ class Sim:
         self._check(self.lib.ts_exchange_plan(self.h, cap, nb.ctypes.data, ns.ctypes.data,
                                               off.ctypes.data, ctypes.byref(n)))
         return [(int(nb[i]), int(ns[i]), int(off[i])) for i in range(n.value)]
+
+    def nccl_init(self, unique_id, nranks, rank):
+        """join the library's own NCCL communicator (native exchanges)"""
+        buf = ctypes.create_string_buffer(bytes(unique_id), 128)
+        self._check(self.lib.ts_nccl_init(self.h, buf, int(nranks), int(rank)))
+
+    def exchange(self):
+        """one native exchange of the packed strips (after ts_nccl_init)"""
+        self._check(self.lib.ts_exchange(self.h))
 
     def exchange_buffers(self):
         """device pointers (send, recv) of the packed strip buffers"""

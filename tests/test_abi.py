@@ -52,3 +52,14 @@ def test_orb_partition_host():
         assert set(d.tolist()) == set(range(k))
         loads = np.bincount(d, weights=w, minlength=k)
         assert loads.max() <= w.sum() / k + 2 * w.max() + 1e-9
+
+
+def test_nccl_unique_id():
+    """the native exchange transport opens libnccl at run time: a
+    communicator id is 128 bytes and fresh on every call (no GPU needed)"""
+    import paper_cs_0105004_b200 as tsim
+    try:
+        a, b = tsim.nccl_unique_id(), tsim.nccl_unique_id()
+    except tsim.TsError:
+        pytest.skip("libnccl.so.2 not available")
+    assert len(a) == 128 == len(b) and a != b
