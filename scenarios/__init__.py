@@ -279,12 +279,14 @@ def _gen_lib():
 
 
 def big_grid(rows=256, cols=256, cells=100, lanes=4, density=0.2, n_veh=None,
-             seed=1, steps=3600, name="config4a_grid256"):
+             seed=1, steps=3600, name="config4a_grid256", dest_radius=None):
     """BASELINE.json configs[3]: rows x cols
     lattice of `cells`-cell links with `lanes` lanes; vehicles placed at t = 0
     uniformly without replacement at v = 0; destination node uniform; route
     = canonical x-then-y Manhattan path from the head node of the first link
-    (U-turns allowed)."""
+    (U-turns allowed).  dest_radius (tests only): destination uniform within
+    +-dest_radius rows / columns of the first link's head node instead, so
+    the full-size network carries short routes (small host memory)."""
     net = grid_network(rows, cols, cells * CELL_MM, lanes)
     rng = np.random.default_rng(seed)
     nl = net["link_from"].size
@@ -299,6 +301,12 @@ def big_grid(rows=256, cols=256, cells=100, lanes=4, density=0.2, n_veh=None,
     cell = (rem % cells).astype(np.int32)
     del flat, rem
     dest = rng.integers(0, rows * cols, size=n_veh).astype(np.int32)
+    if dest_radius is not None:
+        head = np.asarray(net["link_to"])[first].astype(np.int64)
+        hr, hc = head // cols, head % cols
+        dr = np.clip(hr + rng.integers(-dest_radius, dest_radius + 1, n_veh), 0, rows - 1)
+        dc = np.clip(hc + rng.integers(-dest_radius, dest_radius + 1, n_veh), 0, cols - 1)
+        dest = (dr * cols + dc).astype(np.int32)
     lib = _gen_lib()
     lens = np.empty(n_veh, dtype=np.int64)
     lib.manhattan_lengths(n_veh, first.ctypes.data, dest.ctypes.data, rows, cols, lens.ctypes.data)

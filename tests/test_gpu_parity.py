@@ -217,3 +217,15 @@ def test_graph_replay_ring():
     """the periodic ring (general tiles only, lane change not fusable)"""
     s = scenarios.ring(n_cells=3000, lanes=3, density=0.2, seed=5)
     run_parity(s, 150, GRAPH, full_every=1, hash_every=30)
+
+
+def test_config4a_full_size_prefix():
+    """BASELINE.json configs[3] at full size (256 x 256 nodes, 104,448,000
+    lane-cells, 20,889,600 vehicles at density 0.2) in the bench's launch
+    configuration: per-step hash and full state against the oracle for the
+    first steps.  Routes are short (destination within 4 rows / columns) so
+    the oracle's copy fits the host; cells, vehicles and kernels are the
+    bench's."""
+    s = scenarios.big_grid(seed=1, dest_radius=4, name="config4a_full_shortroutes")
+    assert s.n_vehicles == 20_889_600
+    run_parity(s, 3, tsim.FLAG_FUSED | tsim.FLAG_HASH, full_every=3, hash_every=3)
