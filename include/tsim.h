@@ -265,6 +265,12 @@ int ts_nccl_unique_id(void *id128);
 int ts_nccl_init(ts_sim *h, const void *id128, int32_t nranks, int32_t rank);
 int ts_exchange(ts_sim *h);
 
+/* Device time (ms, CUDA events on the handle's stream) of all step work --
+ * ts_step calls and ts_step_phase calls -- since the previous call; resets.
+ * The measured per-domain step time of the adaptive rebalancing
+ * (PAPER.md:730-735).  Synchronises the handle's stream. */
+int ts_busy_time(ts_sim *h, double *ms);
+
 /* Kernel-level timing of the last ts_step call (CUDA events on the
  * handle's stream): total ms, and ms inside the dominant (move) kernel. */
 int ts_last_timing(ts_sim *h, double *total_ms, double *move_ms,

@@ -184,6 +184,11 @@ struct ts_sim {
   int32_t graph_t0 = 0;
   std::vector<cudaEvent_t> mv_ev;
   double last_total_ms = 0, last_move_ms = 0;
+  // device time of all step work since the last ts_busy_time (the measured
+  // per-domain step time of the rebalancing feedback)
+  double busy_ms = 0;
+  std::vector<cudaEvent_t> ph_ev;  // event pairs around ts_step_phase calls
+  size_t ph_used = 0;
   int64_t last_move_launches = 0;
   bool timing = true;
 };
@@ -378,6 +383,7 @@ void ts_destroy(ts_sim *h) {
   if (h->stream) cudaStreamSynchronize(h->stream);
   for (void *p : h->allocs) cudaFree(p);
   for (auto e : h->mv_ev) cudaEventDestroy(e);
+  for (auto e : h->ph_ev) cudaEventDestroy(e);
   if (h->comm) nccl().commDestroy(h->comm);
   for (auto g : h->graph_exec)
     if (g) cudaGraphExecDestroy(g);
@@ -1621,6 +1627,7 @@ static int finish_steps(ts_sim *h, int32_t t_from, int32_t n) {
   float ms = 0;
   CK(h, cudaEventElapsedTime(&ms, h->ev0, h->ev1));
   h->last_total_ms = ms;
+  h->busy_ms += ms;
   double mv = 0;
   if (h->timing)
     for (int i = 0; i < h->last_move_launches; i++) {
@@ -1659,9 +1666,38 @@ int ts_sync(ts_sim *h) {
   return fold_stats(h);
 }
 
+static int fold_busy(ts_sim *h) {
+  if (h->ph_used == 0) return TS_OK;
+  CK(h, cudaStreamSynchronize(h->stream));
+  for (size_t i = 0; i + 1 < h->ph_used; i += 2) {
+    float m = 0;
+    CK(h, cudaEventElapsedTime(&m, h->ph_ev[i], h->ph_ev[i + 1]));
+    h->busy_ms += m;
+  }
+  h->ph_used = 0;
+  return TS_OK;
+}
+
+int ts_busy_time(ts_sim *h, double *ms) {
+  if (!h || !h->inited || !ms) return TS_EINVAL;
+  CK(h, cudaSetDevice(h->dev));
+  if (int rc = fold_busy(h)) return rc;
+  *ms = h->busy_ms;
+  h->busy_ms = 0;
+  return TS_OK;
+}
+
 int ts_step_phase(ts_sim *h, int32_t phase, int32_t more) {
   if (!h || !h->inited) return fail(h, TS_EINVAL, "call ts_init first");
   CK(h, cudaSetDevice(h->dev));
+  if (h->ph_used >= 8192)
+    if (int rc = fold_busy(h)) return rc;
+  while (h->ph_ev.size() < h->ph_used + 2) {
+    cudaEvent_t e;
+    CK(h, cudaEventCreate(&e));
+    h->ph_ev.push_back(e);
+  }
+  CK(h, cudaEventRecord(h->ph_ev[h->ph_used], h->stream));
   switch (phase) {
     case 0:
       if (zero_stats(h, h->t + 1, 1)) return TS_EINTERNAL;
@@ -1677,6 +1713,8 @@ int ts_step_phase(ts_sim *h, int32_t phase, int32_t more) {
     default:
       return fail(h, TS_EINVAL, "phase must be 0, 1 or 2");
   }
+  CK(h, cudaEventRecord(h->ph_ev[h->ph_used + 1], h->stream));
+  h->ph_used += 2;
   CK(h, cudaGetLastError());
   return TS_OK;
 }

@@ -63,6 +63,31 @@ def partition(scn, k, weights=None, method="orb"):
     return _t.orb_partition(scn.node_x, scn.node_y, k, weights)
 
 
+def link_times(link_work_per_domain, domain_ms):
+    """execution time per link ("we collect the execution
+    time of each link and intersection"): each domain's measured step time
+    apportioned to its links by their share of the domain's work (vehicle
+    updates; a split link's halves are counted by their owners)"""
+    t = np.zeros(len(link_work_per_domain[0]), np.float64)
+    for lw, ms in zip(link_work_per_domain, domain_ms):
+        lw = np.asarray(lw, np.float64)
+        tot = lw.sum()
+        if tot > 0:
+            t += ms * lw / tot
+    return t
+
+
+def rebalance_weights(scn, link_work_per_domain, domain_ms, floor=None):
+    """node weights for the next partition from the measured link times
+    (half of every attached link); links without work keep
+    a small floor (their static load share) so empty regions still count"""
+    lt = link_times(link_work_per_domain, domain_ms)
+    if floor is None:
+        static = link_cells(scn) * np.asarray(scn.link_lanes, np.float64)
+        floor = 1e-3 * static / static.sum() * max(lt.sum(), 1e-12)
+    return node_weights(scn, lt + floor)
+
+
 def split_stats(scn, dom):
     """N_spl (split links) and the domain neighbour graph"""
     d = np.asarray(dom)
@@ -166,6 +191,24 @@ class LocalDomains:
 
     def link_work(self):
         return sum(s.link_work() for s in self.sims)
+
+    def rebalance(self, method="orb"):
+        """adaptive repartition (BASELINE: "rebalanced from
+        measured per-domain step times"): per-domain device time and per-link
+        work since the last rebalance -> link times -> node weights -> a new
+        partition; the state migrates exactly.  Needs FLAG_LINK_WORK.
+        Returns (new domain_of_node, per-domain ms of the window)."""
+        ms = [s.busy_time() for s in self.sims]
+        lw = [s.link_work() for s in self.sims]
+        base = getattr(self, "_lw_base", None)
+        win = [w - b for w, b in zip(lw, base)] if base is not None and len(base) == len(lw) else lw
+        w = rebalance_weights(self.scn, win, ms)
+        dom = partition(self.scn, self.k, w, method=method)
+        self.repartition(dom)
+        self._lw_base = [s.link_work() for s in self.sims]
+        for s in self.sims:  # the migration's own work is not step time
+            s.busy_time()
+        return dom, ms
 
     def repartition(self, domain_of_node, k=None):
         """migrate to a new partition at the current time (exact)"""

@@ -75,6 +75,7 @@ def load_library():
         "ts_nccl_unique_id": (ctypes.c_int, [P]),
         "ts_nccl_init": (ctypes.c_int, [P, P, I32, I32]),
         "ts_exchange": (ctypes.c_int, [P]),
+        "ts_busy_time": (ctypes.c_int, [P, ctypes.POINTER(ctypes.c_double)]),
         "ts_resume": (ctypes.c_int, [P, I32]),
         "ts_step_phase": (ctypes.c_int, [P, I32, I32]),
         "ts_exchange_plan": (ctypes.c_int, [P, I32, P, P, P, P]),
@@ -355,6 +356,12 @@ class Sim:
         out = np.zeros(self.n_links, np.int64)
         self._check(self.lib.ts_get_link_work(self.h, out.ctypes.data))
         return out
+
+    def busy_time(self):
+        """device ms of all step work since the previous call (resets)"""
+        ms = ctypes.c_double()
+        self._check(self.lib.ts_busy_time(self.h, ctypes.byref(ms)))
+        return ms.value
 
     def last_timing(self):
         tot, mv, n = ctypes.c_double(), ctypes.c_double(), ctypes.c_int64()

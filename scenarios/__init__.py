@@ -195,18 +195,25 @@ def _routes_csr(routes):
 
 # ------------------------------------------------------------------- config 1
 def grid_trips(rows=4, cols=4, spacing_mm=500_000, lanes=2, n_veh=1000, seed=1,
-               steps=600, depart_max=0, name="config1_grid4x4"):
+               steps=600, depart_max=0, name="config1_grid4x4", od_cols=None):
     """BASELINE.json configs[0]: 4x4 grid, 48 links of 500 m (67 cells),
     2 lanes, unsignalled priority intersections, 1,000 vehicles with seeded
-    random shortest-path routes, all departing at t = 0 on lane 0."""
+    random shortest-path routes, all departing at t = 0 on lane 0.
+    od_cols=(c0, c1) (tests): origins and destinations only on links between
+    nodes of columns c0..c1 (a spatially concentrated load)."""
     net = grid_network(rows, cols, spacing_mm, lanes)
     rng = np.random.default_rng(seed)
     nl = net["link_from"].size
     succ = successors(net["link_from"], net["link_to"], rows * cols)
+    pool = np.arange(nl)
+    if od_cols is not None:
+        cf, ct = net["link_from"] % cols, net["link_to"] % cols
+        pool = np.nonzero((cf >= od_cols[0]) & (cf <= od_cols[1]) &
+                          (ct >= od_cols[0]) & (ct <= od_cols[1]))[0]
     routes = []
     for _ in range(n_veh):
         while True:
-            o, q = (int(v) for v in rng.integers(0, nl, size=2))
+            o, q = (int(pool[v]) for v in rng.integers(0, pool.size, size=2))
             if o == q:
                 continue
             r = dijkstra_route(succ, net["link_len_mm"], o, q)

@@ -146,3 +146,34 @@ def test_signalized_grid_domains(k):
     undivided oracle (signal state is a function of t and the node only)"""
     s = scenarios.with_signals(scenarios.config("1"), seed=5)
     run_domains(s, k, 200, chunk=50)
+
+
+def test_adaptive_rebalance_from_measured_times():
+    """PAPER.md:730-735 / BASELINE config 5: every 60 steps the partition is
+    recomputed from the measured per-domain device time apportioned to the
+    links by their work; trips concentrated in one half of the network make
+    the first partition unbalanced.  The run stays bit-exact with the
+    undivided oracle across the migrations, and the load (measured link
+    time) of the heaviest domain drops after the first rebalance."""
+    s = scenarios.grid_trips(rows=8, cols=8, n_veh=6000, depart_max=100, seed=12,
+                             name="grid8rebal", od_cols=(0, 3))
+    o = oracle.Oracle.from_scenario(s)
+    d = domains.LocalDomains(s, 4, flags=FUSED | tsim.FLAG_LINK_WORK)
+    e_before = e_after = None
+    for r in range(3):
+        t_from = o.t + 1
+        oh = o.run_hashes(60)
+        d.step(60)
+        gh = d.history(t_from, 60)["hash"]
+        assert list(gh) == list(oh), f"round {r}"
+        lw = [x.link_work() for x in d.sims]
+        dom_old = d.dom.copy()
+        new, ms = d.rebalance()
+        lt = domains.link_times(lw, ms)
+        load_old = np.bincount(dom_old[np.asarray(s.link_from)], weights=lt, minlength=4)
+        load_new = np.bincount(np.asarray(new)[np.asarray(s.link_from)], weights=lt, minlength=4)
+        if r == 0:
+            e_before = load_old.mean() / load_old.max()
+            e_after = load_new.mean() / load_new.max()
+    assert e_after > e_before
+    assert_same(o.vehicles(), d.vehicles(), "after rebalancing")

@@ -64,3 +64,24 @@ def test_partition_input_errors():
         tsim.multilevel_partition(s, s.n_nodes + 1)
     with pytest.raises(tsim.TsError):
         tsim.orb_partition(s.node_x, s.node_y, s.n_nodes + 1)
+
+
+def test_rebalance_weights_follow_measured_time():
+    """link times = each domain's measured time split by its links' work
+    (PAPER.md:730-733); a domain twice as slow per unit of work gets twice
+    the weight, so ORB moves its boundary towards it"""
+    from paper_cs_0105004_b200 import domains
+    scn = scenarios.config("1")
+    n = scn.n_links
+    dom = (np.asarray(scn.node_x) > np.median(scn.node_x)).astype(np.int32)
+    own = dom[np.asarray(scn.link_from)]  # work attributed to the from-node's domain
+    work = [np.where(own == d, 100, 0) for d in (0, 1)]
+    lt = domains.link_times(work, [2.0, 1.0])
+    assert lt.sum() == pytest.approx(3.0)
+    assert lt[own == 0].sum() == pytest.approx(2.0) and lt[own == 1].sum() == pytest.approx(1.0)
+    w = domains.rebalance_weights(scn, work, [2.0, 1.0])
+    assert w[dom == 0].sum() > 1.5 * w[dom == 1].sum()
+    new = domains.partition(scn, 2, w)
+    # the domain holding the slow (left) side now has fewer than half the nodes
+    slow = new[int(np.argmin(np.asarray(scn.node_x)))]
+    assert np.bincount(new, minlength=2)[slow] < scn.n_nodes // 2

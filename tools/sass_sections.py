@@ -21,7 +21,7 @@ for ln in dis:
         cur = (m.group(1).split('/')[-1], int(m.group(2)))
         if cur[0] == 'tsim_rows.cu':
             last = cur[1]
-    if re.search(r'/\*[0-9a-f]{4,}\*/', ln) and fn and 'k_rowsENS' in fn:
+    if re.search(r'/\*[0-9a-f]{4,}\*/', ln) and fn and 'k_rowsILi5E' in fn:
         cnt[last] += 1
 src = open(f'{src_dir}/tsim_rows.cu').read().split('\n')
 k0 = next(i for i, l in enumerate(src) if 'k_rows(const StepParams' in l) + 1
