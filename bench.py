@@ -291,6 +291,11 @@ def bench_multi(args):
     dist.barrier()
     ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=f"cuda:{local}")
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    # exchange time, reported separately: mean device time of one exchange
+    # (timed on every 8th step by the library), max over ranks
+    xms, xn = d.sim.last_exchange_timing() if d.native else (0.0, 0)
+    xchg = torch.tensor([xms / max(1, xn)], dtype=torch.float64, device=f"cuda:{local}")
+    dist.all_reduce(xchg, op=dist.ReduceOp.MAX)
     hist = d.sim.history(t_from, args.steps + 1)
     tot = d.sim.totals()
     vst = d.sim.vehicles()
@@ -322,6 +327,11 @@ def bench_multi(args):
                        "split_links": n_spl,
                        "domain_pairs": len(pairs)},
             "real_time_ratio": args.steps / (ms_total / 1e3),
+            "exchange": {"ms_per_exchange": float(xchg.item()) if d.native else None,
+                         "exchanges_per_step": 2,
+                         "share_of_step": 2 * float(xchg.item()) / (ms_total / args.steps)
+                         if d.native else None,
+                         "transport": "native NCCL" if d.native else "torch.distributed"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved / hbm_peak, "traffic": None,
                          "kernel": "whole step per GPU (incl. exchanges)",

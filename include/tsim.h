@@ -271,6 +271,12 @@ int ts_exchange(ts_sim *h);
  * (PAPER.md:730-735).  Synchronises the handle's stream. */
 int ts_busy_time(ts_sim *h, double *ms);
 
+/* Exchange timing of the last ts_step call of a domain with the native
+ * transport: total ms of the timed exchanges (both exchanges of every 8th
+ * step, CUDA events around the NCCL group on the handle's stream) and their
+ * count; n = 0 otherwise. */
+int ts_last_exchange_timing(ts_sim *h, double *ms, int64_t *n);
+
 /* Kernel-level timing of the last ts_step call (CUDA events on the
  * handle's stream): total ms, and ms inside the dominant (move) kernel. */
 int ts_last_timing(ts_sim *h, double *total_ms, double *move_ms,

@@ -183,7 +183,8 @@ struct ts_sim {
   bool graph_off = false, capturing = false;
   int32_t graph_t0 = 0;
   std::vector<cudaEvent_t> mv_ev;
-  double last_total_ms = 0, last_move_ms = 0;
+  double last_total_ms = 0, last_move_ms = 0, last_xchg_ms = 0;
+  int64_t last_xchg_n = 0;  // exchanges timed in the last native ts_step call
   // device time of all step work since the last ts_busy_time (the measured
   // per-domain step time of the rebalancing feedback)
   double busy_ms = 0;
@@ -1551,17 +1552,34 @@ static int enqueue_steps(ts_sim *h, int32_t n) {
   CK(h, cudaSetDevice(h->dev));
   if (h->n_xs > 0) {  // whole steps with the native exchange (G1): LC, #1, move, #2
     if (zero_stats(h, h->t + 1, std::min(n + 1, kHist))) return TS_EINTERNAL;
+    // both exchanges of every kTimingStride-th step are bracketed by events
+    // (exchange time reported separately from the step, BASELINE config 5)
+    const int nt = h->timing ? (n + kTimingStride - 1) / kTimingStride : 0;
+    while ((int)h->mv_ev.size() < 4 * nt) {
+      cudaEvent_t e;
+      CK(h, cudaEventCreate(&e));
+      h->mv_ev.push_back(e);
+    }
     CK(h, cudaEventRecord(h->ev0, h->stream));
+    int ne = 0;
     for (int i = 0; i < n; i++) {
+      const bool tm = h->timing && i % kTimingStride == 0;
       phase_lc(h);
+      if (tm) CK(h, cudaEventRecord(h->mv_ev[2 * ne], h->stream));
       if (int rc = nccl_exchange(h)) return rc;
+      if (tm) CK(h, cudaEventRecord(h->mv_ev[2 * ne + 1], h->stream));
+      ne += tm;
       phase_move(h, i < n - 1, nullptr, nullptr);
+      if (tm) CK(h, cudaEventRecord(h->mv_ev[2 * ne], h->stream));
       if (int rc = nccl_exchange(h)) return rc;
+      if (tm) CK(h, cudaEventRecord(h->mv_ev[2 * ne + 1], h->stream));
+      ne += tm;
       unpack_strips(h);
     }
     CK(h, cudaEventRecord(h->ev1, h->stream));
     CK(h, cudaGetLastError());
     h->last_move_launches = 0;
+    h->last_xchg_n = ne;
     return TS_OK;
   }
   // TS_FLAG_GRAPH: whole kGraphSteps blocks of steps replay one CUDA graph
@@ -1598,6 +1616,7 @@ static int enqueue_steps(ts_sim *h, int32_t n) {
   CK(h, cudaEventRecord(h->ev1, h->stream));
   CK(h, cudaGetLastError());
   h->last_move_launches = ns;
+  h->last_xchg_n = 0;
   return TS_OK;
 }
 
@@ -1636,6 +1655,13 @@ static int finish_steps(ts_sim *h, int32_t t_from, int32_t n) {
       mv += m;
     }
   h->last_move_ms = mv;
+  double xm = 0;
+  for (int64_t i = 0; i < h->last_xchg_n; i++) {
+    float m = 0;
+    CK(h, cudaEventElapsedTime(&m, h->mv_ev[2 * i], h->mv_ev[2 * i + 1]));
+    xm += m;
+  }
+  h->last_xchg_ms = xm;
   return fold_stats(h);
 }
 
@@ -2062,6 +2088,13 @@ int ts_get_link_work(ts_sim *h, int64_t *link_work) {
   if (!h || !h->inited) return fail(h, TS_EINVAL, "not initialised");
   CK(h, cudaStreamSynchronize(h->stream));
   CK(h, cudaMemcpy(link_work, h->d_work, sizeof(int64_t) * h->nl, cudaMemcpyDeviceToHost));
+  return TS_OK;
+}
+
+int ts_last_exchange_timing(ts_sim *h, double *ms, int64_t *n) {
+  if (!h) return TS_EINVAL;
+  if (ms) *ms = h->last_xchg_ms;
+  if (n) *n = h->last_xchg_n;
   return TS_OK;
 }
 

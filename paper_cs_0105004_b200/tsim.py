@@ -76,6 +76,8 @@ def load_library():
         "ts_nccl_init": (ctypes.c_int, [P, P, I32, I32]),
         "ts_exchange": (ctypes.c_int, [P]),
         "ts_busy_time": (ctypes.c_int, [P, ctypes.POINTER(ctypes.c_double)]),
+        "ts_last_exchange_timing": (ctypes.c_int, [P, ctypes.POINTER(ctypes.c_double),
+                                                   ctypes.POINTER(ctypes.c_int64)]),
         "ts_resume": (ctypes.c_int, [P, I32]),
         "ts_step_phase": (ctypes.c_int, [P, I32, I32]),
         "ts_exchange_plan": (ctypes.c_int, [P, I32, P, P, P, P]),
@@ -356,6 +358,12 @@ class Sim:
         out = np.zeros(self.n_links, np.int64)
         self._check(self.lib.ts_get_link_work(self.h, out.ctypes.data))
         return out
+
+    def last_exchange_timing(self):
+        """(total ms, count) of the timed native exchanges of the last ts_step"""
+        ms, n = ctypes.c_double(), ctypes.c_int64()
+        self._check(self.lib.ts_last_exchange_timing(self.h, ctypes.byref(ms), ctypes.byref(n)))
+        return ms.value, n.value
 
     def busy_time(self):
         """device ms of all step work since the previous call (resets)"""
