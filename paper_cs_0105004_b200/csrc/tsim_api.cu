@@ -78,7 +78,10 @@ struct ts_sim {
   // vehicles (host)
   int32_t nv = 0;
   std::vector<int64_t> roff;
-  std::vector<int32_t, UninitAlloc<int32_t>> route;
+  // plans as out-slot sequences (R7): rslot[roff[f] + j] = slot of route link
+  // j at its from-node (0xFF for j = 0); the link ids are not kept (a link
+  // at cursor c is the walk from first_link along the slots, link_at)
+  std::vector<uint8_t, UninitAlloc<uint8_t>> rslot;
   std::vector<int32_t> dep, entry;
   std::vector<int32_t> pl_vid, pl_lane, pl_cell, pl_v, pl_cur;
   std::vector<uint8_t> placed;
@@ -250,6 +253,14 @@ static void parallel_for(int64_t n, F f) {
   for (int i = 0; i < nt; i++)
     th.emplace_back([=, &f]() { f(n * i / nt, n * (i + 1) / nt, i); });
   for (auto &t : th) t.join();
+}
+
+// the link at cursor c of vehicle f: the walk along its out-slots
+static int link_at(const ts_sim *h, int f, int c) {
+  const int64_t a = h->roff[f];
+  int k = h->first_link[f];
+  for (int j = 1; j <= c; j++) k = h->out_list[h->out_off[h->to[k]] + h->rslot[a + j]];
+  return k;
 }
 
 // ---------------------------------------------------------------- NCCL
@@ -523,9 +534,16 @@ int ts_load_vehicles(ts_sim *h, int32_t n, const int64_t *route_off, const int32
   h->nv = n;
   h->roff.assign(route_off, route_off + n + 1);
   if (n == 0) h->roff.assign(1, 0);
-  h->route.resize(h->roff[n]);
-  parallel_for(h->roff[n], [&](int64_t lo, int64_t hi, int) {
-    std::copy(route_links + lo, route_links + hi, h->route.begin() + lo);
+  h->rslot.resize(h->roff[n]);
+  h->first_link.resize(n);
+  parallel_for(n, [&](int64_t lo, int64_t hi, int) {
+    for (int64_t f = lo; f < hi; f++) {
+      const int64_t a = h->roff[f];
+      h->first_link[f] = route_links[a];
+      h->rslot[a] = 0xFF;
+      for (int64_t j = a + 1; j < h->roff[f + 1]; j++)
+        h->rslot[j] = (uint8_t)h->out_pos[route_links[j]];
+    }
   });
   h->dep.assign(depart, depart + n);
   h->entry.assign(entry_cell, entry_cell + n);
@@ -546,7 +564,7 @@ int ts_place_vehicles_at(ts_sim *h, int32_t n, const int32_t *vid, const int32_t
     const int32_t c = cursor ? cursor[i] : 0;
     if (c < 0 || c >= h->roff[f + 1] - h->roff[f])
       return fail(h, TS_EINVAL, "placement %d: cursor outside the route", i);
-    const int32_t k = h->route[h->roff[f] + c];
+    const int32_t k = link_at(h, f, c);
     if (lane[i] < 0 || lane[i] >= h->lanes[k] || cell[i] < 0 || cell[i] >= h->ncell[k])
       return fail(h, TS_EINVAL, "placement %d: cell outside link", i);
     if (v[i] < 0 || v[i] > h->vmax[k]) return fail(h, TS_EINVAL, "placement %d: velocity", i);
@@ -943,10 +961,6 @@ static int tile_of(const ts_sim *h, int k, int x) {
   return -1;
 }
 
-static int first_slot(const ts_sim *h, int f) {
-  const int64_t a = h->roff[f];
-  return h->roff[f + 1] - a > 1 ? h->out_pos[h->route[a + 1]] : kSlotFinal;
-}
 
 static StepParams step_params(ts_sim *h, int t, int mode) {
   StepParams P{};
@@ -1105,9 +1119,9 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
   CK(h, cudaSetDevice(h->dev));
   if (h->dom_of_node.empty()) h->dom_of_node.assign(h->nn, 0);
   build_tiles(h);
-  h->first_link.resize(h->nv);
+
   h->entry_h = h->entry;
-  for (int f = 0; f < h->nv; f++) h->first_link[f] = h->route[h->roff[f]];
+
   // host staging of the initial placement: codes + compact vid lists (cells
   // of other domains are skipped)
   std::vector<uint8_t> code(h->total_cells, kEmpty);
@@ -1116,7 +1130,7 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
   h->n_placed = 0;
   for (size_t i = 0; i < h->pl_vid.size(); i++) {
     const int f = h->pl_vid[i], c = h->pl_cur[i];
-    const int k = h->route[h->roff[f] + c];
+    const int k = link_at(h, f, c);
     cur0[f] = c;
     const int ti = tile_of(h, k, h->pl_cell[i]);
     if (ti < 0) continue;  // another domain's cell
@@ -1124,7 +1138,7 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
     const int64_t pos = d.off + (int64_t)h->pl_lane[i] * row_pitch(d.w) + (h->pl_cell[i] - d.a);
     if (code[pos] != kEmpty) return fail(h, TS_EINVAL, "placement %zu: cell taken", i);
     const int64_t ro = h->roff[f];
-    const int slot = c + 1 < h->roff[f + 1] - ro ? h->out_pos[h->route[ro + c + 1]] : kSlotFinal;
+    const int slot = c + 1 < h->roff[f + 1] - ro ? (int)h->rslot[ro + c + 1] : kSlotFinal;
     code[pos] = (uint8_t)(h->pl_v[i] | (slot << 3));
     cellvid[pos] = f;
     h->n_placed++;
@@ -1284,18 +1298,36 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
   if ((rc = upload(h, &h->d_vmax, vmax8))) return rc;
   if ((rc = upload(h, &h->d_tt, h->tt))) return rc;
   if ((rc = upload(h, &h->d_out_pos, h->out_pos))) return rc;
-  {  // routes as out-slot sequences: rslot[j] = slot of R[j] at its from-node
-    std::vector<uint8_t, UninitAlloc<uint8_t>> rslot(h->route.size());
-    parallel_for(h->nv, [&](int64_t lo, int64_t hi, int) {
-      for (int64_t f = lo; f < hi; f++) {
-        rslot[h->roff[f]] = 0xFF;
-        for (int64_t j = h->roff[f] + 1; j < h->roff[f + 1]; j++)
-          rslot[j] = (uint8_t)h->out_pos[h->route[j]];
+  {  // routes as out-slot sequences (built at load), through pinned staging
+    const size_t nb = h->rslot.size();
+    if ((rc = dalloc(h, &h->d_rslot, std::max<size_t>(nb, 1)))) return rc;
+    const size_t chunk = (size_t)64 << 20;
+    uint8_t *pin[2] = {nullptr, nullptr};
+    cudaEvent_t done[2] = {nullptr, nullptr};
+    bool pinned = nb > chunk && cudaMallocHost(&pin[0], chunk) == cudaSuccess &&
+                  cudaMallocHost(&pin[1], chunk) == cudaSuccess &&
+                  cudaEventCreateWithFlags(&done[0], cudaEventDisableTiming) == cudaSuccess &&
+                  cudaEventCreateWithFlags(&done[1], cudaEventDisableTiming) == cudaSuccess;
+    if (pinned) {  // double-buffered: fill one buffer while the other copies
+      for (size_t o = 0, i = 0; o < nb; o += chunk, i++) {
+        const size_t m = std::min(chunk, nb - o);
+        uint8_t *b = pin[i & 1];
+        if (i >= 2) cudaEventSynchronize(done[i & 1]);
+        parallel_for((int64_t)m, [&](int64_t lo, int64_t hi, int) {
+          memcpy(b + lo, h->rslot.data() + o + lo, hi - lo);
+        });
+        CK(h, cudaMemcpyAsync(h->d_rslot + o, b, m, cudaMemcpyHostToDevice, h->stream));
+        CK(h, cudaEventRecord(done[i & 1], h->stream));
       }
-    });
-    if ((rc = dalloc(h, &h->d_rslot, rslot.size()))) return rc;
-    if (!rslot.empty())
-      CK(h, cudaMemcpy(h->d_rslot, rslot.data(), rslot.size(), cudaMemcpyHostToDevice));
+      CK(h, cudaStreamSynchronize(h->stream));
+    } else if (nb) {
+      CK(h, cudaMemcpy(h->d_rslot, h->rslot.data(), nb, cudaMemcpyHostToDevice));
+    }
+    for (int i = 0; i < 2; i++) {
+      if (pin[i]) cudaFreeHost(pin[i]);
+      if (done[i]) cudaEventDestroy(done[i]);
+    }
+    cudaGetLastError();
     std::vector<NodeOut> nodeout(h->out_list.size());
     for (size_t i = 0; i < h->out_list.size(); i++) {
       const int k = h->out_list[i];
@@ -1405,7 +1437,7 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
   CK(h, cudaMemcpy(st, h->d_stats + (size_t)(t0 & (kHist - 1)) * ST_N, sizeof st, cudaMemcpyDeviceToHost));
   h->injected = (int64_t)st[ST_INJ];
   // the host copies of the plans are no longer needed (all on the device)
-  std::vector<int32_t, UninitAlloc<int32_t>>().swap(h->route);
+  std::vector<uint8_t, UninitAlloc<uint8_t>>().swap(h->rslot);
   std::vector<int32_t>().swap(h->pl_vid);
   std::vector<int32_t>().swap(h->pl_cur);
   std::vector<int32_t>().swap(h->pl_lane);
