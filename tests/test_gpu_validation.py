@@ -101,3 +101,43 @@ def test_signal_half_green_half_saturation(p):
     half = passed_per_step(discharge_network(256, 30, 30, p), 960)
     assert sat > 0.25
     assert 0.45 <= half / sat <= 0.55, (half, sat)
+
+
+def _check_invariants(g, n_veh, vmax=5):
+    """conservation; active vehicles on distinct (link, lane, cell); 0 <= v
+    <= vmax; cursors inside their routes"""
+    v = g.vehicles()
+    st = v["status"]
+    act = st == tsim.ACTIVE
+    assert np.sum(act) + np.sum(st == tsim.PENDING) + np.sum(st == tsim.ARRIVED) == n_veh
+    key = (v["link"][act].astype(np.int64) * 8 + v["lane"][act]) * 4_000_000 + v["cell"][act]
+    assert np.unique(key).size == key.size, "two vehicles in one cell"
+    assert v["v"][act].min(initial=0) >= 0 and v["v"][act].max(initial=0) <= vmax
+    assert np.all(v["cursor"][act] >= 0)
+    return v
+
+
+def test_full_size_grid_invariants_long_run():
+    """config 4a at full size (20.9 M vehicles, short routes): 600 steps in
+    the bench's launch configuration, then the invariants hold and the
+    counters agree with the state"""
+    import scenarios as sc
+    s = sc.big_grid(seed=2, dest_radius=6, name="config4a_full_inv")
+    g = tsim.Sim.from_scenario(s, flags=tsim.FLAG_FUSED)
+    g.step(600)
+    v = _check_invariants(g, s.n_vehicles)
+    tot = g.totals()
+    assert tot["active"] == int(np.sum(v["status"] == tsim.ACTIVE))
+    assert tot["arrived"] == int(np.sum(v["status"] == tsim.ARRIVED))
+    assert tot["arrived"] > 0
+
+
+def test_full_size_ring_invariants_long_run():
+    """config 2 at full size for its 1,000 steps: no vehicle lost or
+    duplicated on the 3 x 1,000,000-cell ring"""
+    import scenarios as sc
+    s = sc.config("2")
+    g = tsim.Sim.from_scenario(s, flags=tsim.FLAG_FUSED | tsim.FLAG_GRAPH)
+    g.step(1000)
+    _check_invariants(g, s.n_vehicles)
+    assert g.totals()["active"] == s.n_vehicles
