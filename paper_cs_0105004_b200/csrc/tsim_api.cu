@@ -1384,7 +1384,7 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
   // leave ~55 KB of shared memory per block; group_cells overrides (tuning)
   h->rows_cap = h->cfg.group_cells > 0 ? (h->cfg.group_cells + 3) & ~3 : 1344;
   h->pdl = getenv("TSIM_NO_PDL") == nullptr;
-  h->rows_threads = 128;
+  h->rows_threads = TS_ROWS_TPB;
   h->rows_smem = (h->rows_threads / 32) * rows_stage_words(h->rows_cap) * 4;
   CK(h, set_rows_smem(h->rows_smem));
   {  // persistent grid: every resident warp loops over groups

@@ -94,6 +94,9 @@ __host__ __device__ inline int64_t tile_cells_padded(int w, int L) {
 // move).  A row's list starts at the prefix sum of the vehicle counts of
 // the rows before it (popcounts of their occupancy planes), so the block
 // is read and written with dense, coalesced warp accesses.
+#ifndef TS_ROWS_TPB
+#define TS_ROWS_TPB 128  // k_rows threads per block (one warp per group)
+#endif
 constexpr int kSlotShift = 27;
 constexpr uint32_t kVidMask = (1u << kSlotShift) - 1u;
 constexpr int kRowWords = 4;

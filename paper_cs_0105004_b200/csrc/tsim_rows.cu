@@ -226,7 +226,7 @@ static __device__ __noinline__ uint32_t zone_lc(uint32_t zc, int c0, int w, int 
 }
 
 #ifndef TS_ROWS_MINB
-#define TS_ROWS_MINB 4  // resident 128-thread blocks per SM (128 registers; 5 -> 96 regs measured 2.5% slower)
+#define TS_ROWS_MINB (512 / TS_ROWS_TPB)  // resident blocks per SM: 128 registers (96 measured 2.5% slower)
 #endif
 #ifndef TS_ROWS_ASYNC
 #define TS_ROWS_ASYNC 1  // vid blocks: cp.async in, bulk (TMA) store out
@@ -234,9 +234,9 @@ static __device__ __noinline__ uint32_t zone_lc(uint32_t zc, int c0, int w, int 
 // MODE = the uniform mode bits kModeMove | kModeLC | kModeHash of the launch
 // (specialised so the hot fused instantiation carries no dead paths)
 template <int MODE>
-__global__ void __launch_bounds__(128, TS_ROWS_MINB) k_rows(const StepParams P_, const RowsParams R) {
+__global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepParams P_, const RowsParams R) {
   const StepParams P = with_time(P_);
-  __shared__ unsigned long long red[4 * 8];
+  __shared__ unsigned long long red[(TS_ROWS_TPB / 32) * 8];
   extern __shared__ __align__(16) int32_t stage[];  // per warp: vid block in, vid block out
   const int lane = threadIdx.x & 31;
   int32_t *s_in = stage + (threadIdx.x >> 5) * rows_stage_words(R.cap);
