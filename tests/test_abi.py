@@ -63,3 +63,17 @@ def test_nccl_unique_id():
     except tsim.TsError:
         pytest.skip("libnccl.so.2 not available")
     assert len(a) == 128 == len(b) and a != b
+
+
+def test_null_handles_are_rejected():
+    """every entry point taking a handle returns TS_EINVAL (2) for NULL,
+    without touching a device (SPEC.md:617 exit codes)"""
+    lib = tsim.load_library()
+    c_d, c_i = ctypes.c_double(), ctypes.c_int64()
+    assert lib.ts_busy_time(None, ctypes.byref(c_d)) == 2
+    assert lib.ts_exchange(None) == 2
+    assert lib.ts_nccl_init(None, None, 1, 0) == 2
+    assert lib.ts_last_exchange_timing(None, ctypes.byref(c_d), ctypes.byref(c_i)) == 2
+    assert lib.ts_step(None, 1) == 2
+    assert lib.ts_init(None, 0) == 2
+    assert lib.ts_nccl_unique_id(None) == 2
