@@ -153,6 +153,35 @@ __device__ __forceinline__ void bulk_store(int32_t *gdst, const int32_t *src, in
                "r"(bytes) : "memory");
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
+// TMA bulk load of a vid block into shared memory, completion on an
+// mbarrier (one per warp): lane 0 arms the barrier with the byte count and
+// issues the copy; every lane waits on the barrier's phase
+__device__ __forceinline__ void mbar_init(uint64_t *bar) {
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(a) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_load(int32_t *sdst, const int32_t *gsrc, int n, uint64_t *bar) {
+  const uint32_t sa = (uint32_t)__cvta_generic_to_shared(sdst);
+  const uint32_t ba = (uint32_t)__cvta_generic_to_shared(bar);
+  const uint32_t bytes = (uint32_t)((n + 3) & ~3) * 4u;
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(ba), "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(sa),
+      "l"(gsrc), "r"(bytes), "r"(ba)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  const uint32_t ba = (uint32_t)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra W;\n}" ::"r"(ba),
+      "r"(parity)
+      : "memory");
+}
+
 // the bulk stores of this thread have finished reading shared memory
 __device__ __forceinline__ void bulk_wait_read() {
   asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
@@ -228,6 +257,9 @@ static __device__ __noinline__ uint32_t zone_lc(uint32_t zc, int c0, int w, int 
 #ifndef TS_ROWS_MINB
 #define TS_ROWS_MINB (512 / TS_ROWS_TPB)  // resident blocks per SM: 128 registers (96 measured 2.5% slower)
 #endif
+#ifndef TS_ROWS_TMA_IN
+#define TS_ROWS_TMA_IN 1  // vid block in by one TMA bulk copy (else cp.async pieces)
+#endif
 #ifndef TS_ROWS_ASYNC
 #define TS_ROWS_ASYNC 1  // vid blocks: cp.async in, bulk (TMA) store out
 #endif
@@ -237,6 +269,7 @@ template <int MODE>
 __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepParams P_, const RowsParams R) {
   const StepParams P = with_time(P_);
   __shared__ unsigned long long red[(TS_ROWS_TPB / 32) * 8];
+  __shared__ uint64_t vbar[TS_ROWS_TPB / 32];  // per warp: vid block arrival
   extern __shared__ __align__(16) int32_t stage[];  // per warp: vid block in, vid block out
   const int lane = threadIdx.x & 31;
   int32_t *s_in = stage + (threadIdx.x >> 5) * rows_stage_words(R.cap);
@@ -271,6 +304,10 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
+  uint64_t *bar = &vbar[threadIdx.x >> 5];
+  uint32_t bar_phase = 0;
+  if (TS_ROWS_TMA_IN && lane == 0) mbar_init(bar);
+  __syncwarp();
   int g_next = grab();
   if (TS_ROWS_PPF && g_next < R.ngroups) issue_planes(g_next);
   for (;;) {
@@ -300,9 +337,18 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
     // staged in shared memory when it fits, loaded together with the planes
     const int tot_in = R.gcnt_in[g];
     const bool staged = tot_in <= R.cap;
+    const bool tma_in = TS_ROWS_TMA_IN && staged && tot_in > 0;
     if (staged) {
-      if (TS_ROWS_ASYNC) warp_load_async(s_in, R.vid_in + voff, tot_in, lane);
-      else warp_load(s_in, R.vid_in + voff, tot_in, lane);
+      if (tma_in) {
+        if (lane == 0) {  // the previous group's generic reads of s_in come first
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          bulk_load(s_in, R.vid_in + voff, tot_in, bar);
+        }
+      } else if (TS_ROWS_ASYNC) {
+        warp_load_async(s_in, R.vid_in + voff, tot_in, lane);
+      } else {
+        warp_load(s_in, R.vid_in + voff, tot_in, lane);
+      }
     }
     const bool pl_next = TS_ROWS_PPF && g_next < R.ngroups;
     if (pl_next) issue_planes(g_next);  // committed after the vid block
@@ -337,8 +383,14 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
     const int in_off = warp_scan(nin, lane, &tot_chk);
     if (staged) {
       if (TS_ROWS_ASYNC) {
-        if (pl_next) asm volatile("cp.async.wait_group 1;" ::: "memory");  // planes may pend
-        else cp_async_wait();
+        if (tma_in) {
+          mbar_wait(bar, bar_phase);
+          bar_phase ^= 1u;
+        } else if (pl_next) {
+          asm volatile("cp.async.wait_group 1;" ::: "memory");  // planes may pend
+        } else {
+          cp_async_wait();
+        }
       }
       __syncwarp();
     }
