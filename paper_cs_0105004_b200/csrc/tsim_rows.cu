@@ -269,7 +269,8 @@ template <int MODE>
 __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepParams P_, const RowsParams R) {
   const StepParams P = with_time(P_);
   __shared__ unsigned long long red[(TS_ROWS_TPB / 32) * 8];
-  __shared__ uint64_t vbar[TS_ROWS_TPB / 32];  // per warp: vid block arrival
+  __shared__ uint64_t vbar[TS_ROWS_TPB / 32];   // per warp: vid block arrival
+  __shared__ uint64_t pvbar[TS_ROWS_TPB / 32];  // per warp: prefetched planes arrival
   extern __shared__ __align__(16) int32_t stage[];  // per warp: vid block in, vid block out
   const int lane = threadIdx.x & 31;
   int32_t *s_in = stage + (threadIdx.x >> 5) * rows_stage_words(R.cap);
@@ -296,18 +297,21 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
     return __shfl_sync(FULL, g, 0);
   };
   uint32_t *s_pl = reinterpret_cast<uint32_t *>(s_out + R.cap + kRowsAuxWords);  // PPF buffer
-  auto issue_planes = [&](int gg) {  // cp.async of the group's 3 KB of planes
-    const uint32_t *src = R.planes_in + group_plane_base(gg);
-    for (int c = lane; c < kStatePlanes * kRowWords * 8; c += 32) {
-      const uint32_t sa = (uint32_t)__cvta_generic_to_shared(s_pl + 4 * c);
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(src + 4 * c) : "memory");
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  };
-  uint64_t *bar = &vbar[threadIdx.x >> 5];
-  uint32_t bar_phase = 0;
-  if (TS_ROWS_TMA_IN && lane == 0) mbar_init(bar);
+  uint64_t *bar = &vbar[threadIdx.x >> 5], *pbar = &pvbar[threadIdx.x >> 5];
+  uint32_t bar_phase = 0, pbar_phase = 0;
+  if (lane == 0) {
+    if (TS_ROWS_TMA_IN) mbar_init(bar);
+    if (TS_ROWS_PPF) mbar_init(pbar);
+  }
   __syncwarp();
+  auto issue_planes = [&](int gg) {  // TMA bulk copy of the group's 3 KB of planes
+    if (lane == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      bulk_load(reinterpret_cast<int32_t *>(s_pl),
+                reinterpret_cast<const int32_t *>(R.planes_in + group_plane_base(gg)),
+                kStatePlanes * kRowWords * 32, pbar);
+    }
+  };
   int g_next = grab();
   if (TS_ROWS_PPF && g_next < R.ngroups) issue_planes(g_next);
   for (;;) {
@@ -317,8 +321,8 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
     if (TS_ROWS_ASYNC && lane == 0) bulk_wait_read();  // the previous group's output block
     uint32_t O[NW], V0[NW], V1[NW], V2[NW], A0[NW], A1[NW];
     if (TS_ROWS_PPF) {  // this group's planes, prefetched during the previous one
-      asm volatile("cp.async.wait_all;" ::: "memory");
-      __syncwarp();
+      mbar_wait(pbar, pbar_phase);
+      pbar_phase ^= 1u;
 #pragma unroll
       for (int i = 0; i < NW; i++) {
         O[i] = s_pl[(0 * NW + i) * 32 + lane];
@@ -386,8 +390,6 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
         if (tma_in) {
           mbar_wait(bar, bar_phase);
           bar_phase ^= 1u;
-        } else if (pl_next) {
-          asm volatile("cp.async.wait_group 1;" ::: "memory");  // planes may pend
         } else {
           cp_async_wait();
         }
