@@ -1071,7 +1071,9 @@ static void rows_launch(ts_sim *h, const StepParams &p, bool pdl = false) {
 }
 
 static int base_mode(const ts_sim *h) {
-  int m = kModeMove | kModeInject;
+  // injection only while this domain still has pending trips (the count
+  // only falls; a stale host count errs on the side of injecting)
+  int m = kModeMove | (h->n_pending0 - h->injected > 0 ? kModeInject : 0);
   if (h->cfg.flags & TS_FLAG_HASH) m |= kModeHash;
   if (h->cfg.flags & TS_FLAG_LINK_WORK) m |= kModeWork;
   return m;
