@@ -65,6 +65,10 @@ struct ts_sim {
   std::string err;
   int dev = 0;
   cudaStream_t stream = nullptr;
+  // second stream: the general-tile move kernel runs beside the row kernel
+  // (disjoint tiles, both after the node kernel); fork / join by events
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   size_t dev_bytes = 0;
   std::vector<void *> allocs;
   // network (host)
@@ -379,6 +383,9 @@ int ts_create(const ts_config *cfg, ts_sim **out) {
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaEventCreate(&h->ev0);
   if (e == cudaSuccess) e = cudaEventCreate(&h->ev1);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming);
   if (e != cudaSuccess) {
     delete h;
     return fail(nullptr, TS_EINTERNAL, "CUDA init failed: %s", cudaGetErrorString(e));
@@ -402,6 +409,9 @@ void ts_destroy(ts_sim *h) {
   if (h->ev0) cudaEventDestroy(h->ev0);
   if (h->ev1) cudaEventDestroy(h->ev1);
   if (h->stream) cudaStreamDestroy(h->stream);
+  if (h->side) cudaStreamDestroy(h->side);
+  if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+  if (h->ev_join) cudaEventDestroy(h->ev_join);
   delete h;
 }
 
@@ -1489,21 +1499,31 @@ static void phase_move(ts_sim *h, bool more, cudaEvent_t e0, cudaEvent_t e1) {
                      h->stream, h->pdl);
   else
     launch_node(node_params(h, t), h->stream);
+  // row tiles and general tiles are disjoint: with both present, the
+  // general kernel runs on the side stream next to the row kernel
+  const bool fork = h->ngroups > 0 && !h->gtiles.empty() && h->side;
+  if (!h->gtiles.empty()) {
+    const bool f = more && h->gfused;
+    const StepParams gp = step_params(h, t, mode | (f ? kModeLC : 0));
+    if (fork) {
+      cudaEventRecord(h->ev_fork, h->stream);
+      cudaStreamWaitEvent(h->side, h->ev_fork, 0);
+      launch_step(gp, h->blocks, h->threads, h->smem, h->side);
+      cudaEventRecord(h->ev_join, h->side);
+    }
+    h->gen_s1 = f;
+    if (!fork) launch_step(gp, h->blocks, h->threads, h->smem, h->stream);
+    h->gcur ^= 1;
+  }
   if (e0) cudaEventRecord(e0, h->stream);
   if (h->ngroups > 0) {
     const bool f = more && h->rfused;
-    rows_launch(h, step_params(h, t, mode | (f ? kModeLC : 0)), h->pdl && h->node_warp);
+    rows_launch(h, step_params(h, t, mode | (f ? kModeLC : 0)), h->pdl && h->node_warp && !fork);
     h->rcur ^= 1;
     h->rows_s1 = f;
   }
-  if (!h->gtiles.empty()) {
-    const bool f = more && h->gfused;
-    launch_step(step_params(h, t, mode | (f ? kModeLC : 0)), h->blocks, h->threads, h->smem,
-                h->stream);
-    h->gcur ^= 1;
-    h->gen_s1 = f;
-  }
   if (e1) cudaEventRecord(e1, h->stream);
+  if (fork) cudaStreamWaitEvent(h->stream, h->ev_join, 0);
   h->t = t + 1;
   if (h->n_xs > 0) pack_strips(h);
 }
