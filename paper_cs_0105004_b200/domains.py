@@ -115,6 +115,32 @@ def merge_vehicles(parts):
     return out
 
 
+def merge_vehicles_dist(part, group=None):
+    """merge_vehicles across the ranks of a torch.distributed group: every
+    rank passes its own domain's read and gets the merged state (per
+    vehicle the report of the rank with the highest status rank; two
+    max-reductions, so any backend works: NCCL on GPUs, gloo on CPUs)"""
+    import torch
+    import torch.distributed as dist
+    dev = (torch.device("cuda", torch.cuda.current_device())
+           if dist.get_backend(group) == "nccl" else torch.device("cpu"))
+    order = np.array([1, 3, 2, 0], np.int32)  # PENDING 0, ACTIVE 1, ARRIVED 2, ABSENT 3 -> rank
+    key = torch.as_tensor(order[np.asarray(part["status"], np.int64)], device=dev)
+    best = key.clone()
+    dist.all_reduce(best, op=dist.ReduceOp.MAX, group=group)
+    if bool((best == 0).any()):
+        raise _t.TsError(f"{int((best == 0).sum())} vehicles reported by no domain")
+    mine = key == best
+    out = {}
+    lo = torch.iinfo(torch.int32).min
+    for k, v in part.items():
+        x = torch.as_tensor(np.asarray(v, np.int32), device=dev)
+        x = torch.where(mine, x, torch.full_like(x, lo))
+        dist.all_reduce(x, op=dist.ReduceOp.MAX, group=group)
+        out[k] = x.cpu().numpy().astype(np.asarray(v).dtype)
+    return out
+
+
 def restore_into(sim, state, t):
     """place a vehicle state (merged read at time t) into a fresh handle
     (loaded without initial placement) and resume at t"""
@@ -259,6 +285,7 @@ class DistDomain:
         import torch
         import torch.distributed as dist
         self.group = group
+        self.scn, self.flags, self.kw = scn, flags, kw
         self.rank = dist.get_rank(group)
         self.k = dist.get_world_size(group)
         self.dev = device
@@ -311,3 +338,36 @@ class DistDomain:
     @property
     def t(self):
         return self.sim.t
+
+    def vehicles(self):
+        """the merged state of all ranks (every rank gets it)"""
+        return merge_vehicles_dist(self.sim.vehicles(), self.group)
+
+    def rebalance(self, method="orb"):
+        """adaptive repartition across the ranks: this
+        domain's device time since the last rebalance split over its links by
+        their work, summed over the ranks into link times -> node weights ->
+        the same new partition on every rank; the merged state S(t) is
+        restored into a new handle.  Needs FLAG_LINK_WORK."""
+        import torch
+        import torch.distributed as dist
+        ms = self.sim.busy_time()
+        lw = self.sim.link_work().astype(np.float64)
+        base = getattr(self, "_lw_base", None)
+        win = lw - base if base is not None else lw
+        lt_me = ms * win / win.sum() if win.sum() > 0 else np.zeros_like(win)
+        dev = (torch.device("cuda", self.dev) if dist.get_backend(self.group) == "nccl"
+               else torch.device("cpu"))
+        lt = torch.as_tensor(lt_me, dtype=torch.float64, device=dev)
+        dist.all_reduce(lt, op=dist.ReduceOp.SUM, group=self.group)
+        lt = lt.cpu().numpy()
+        static = link_cells(self.scn) * np.asarray(self.scn.link_lanes, np.float64)
+        w = node_weights(self.scn, lt + 1e-3 * static / static.sum() * max(lt.sum(), 1e-12))
+        dom = partition(self.scn, self.k, w, method=method)
+        t, state = self.t, self.vehicles()
+        self.sim.close()
+        self.__init__(self.scn, dom, device=self.dev, t0=t, flags=self.flags, group=self.group,
+                      state=state, native=self.native, **self.kw)
+        self._lw_base = self.sim.link_work().astype(np.float64)
+        self.sim.busy_time()
+        return dom

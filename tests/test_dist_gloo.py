@@ -109,3 +109,52 @@ def test_orb_weights_balance():
         np.add.at(load, dom[scn.link_from], 0.5 * lw)
         np.add.at(load, dom[scn.link_to], 0.5 * lw)
         assert load.max() / load.mean() < 1.25, (k, load)
+
+
+def _merge_worker(rank, world, port, q):
+    import torch.distributed as dist
+    from paper_cs_0105004_b200 import domains
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        parts = _synthetic_parts(world)
+        got = domains.merge_vehicles_dist(parts[rank])
+        want = domains.merge_vehicles(parts)
+        q.put((rank, all(np.array_equal(got[k], want[k]) for k in want)))
+    finally:
+        dist.destroy_process_group()
+
+
+def _synthetic_parts(world, n=5000, seed=3):
+    """per-domain reads of one state: every vehicle reported ACTIVE /
+    ARRIVED / PENDING by exactly one domain, ABSENT by the others"""
+    from paper_cs_0105004_b200 import domains
+    rng = np.random.default_rng(seed)
+    owner = rng.integers(0, world, n)
+    st = rng.choice([domains.ACTIVE, domains.ARRIVED, domains.PENDING], n)
+    parts = []
+    for d in range(world):
+        mine = owner == d
+        p = {"status": np.where(mine, st, domains.ABSENT).astype(np.int8)}
+        for k in ("link", "lane", "cell", "v", "cursor", "t_arrive"):
+            val = rng.integers(0, 1000, n).astype(np.int32)
+            p[k] = np.where(mine, (np.arange(n) * 7 + len(k)) % 997, val).astype(np.int32)
+        parts.append(p)
+    return parts
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_merge_vehicles_dist_matches_local(world):
+    """the cross-rank merge used by DistDomain.vehicles / rebalance equals
+    the in-process merge of the same per-domain reads"""
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_merge_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(ok for _, ok in res), res
