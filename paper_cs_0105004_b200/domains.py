@@ -309,10 +309,22 @@ class DistDomain:
         self.exchange_ms = 0.0
         self.native = False
         if native and group is None:
-            uid = [_t.nccl_unique_id() if self.rank == 0 else None]
-            dist.broadcast_object_list(uid, src=0)
-            self.sim.nccl_init(uid[0], self.k, self.rank)
-            self.native = True
+            # every rank must take the same transport: probe libnccl on all
+            # ranks first (a rank missing it would leave the others waiting in
+            # the communicator's collective init)
+            try:
+                _t.nccl_unique_id()
+                ok = 1
+            except _t.TsError:
+                ok = 0
+            dev = (torch.device(cuda) if dist.get_backend() == "nccl" else torch.device("cpu"))
+            flag = torch.tensor([ok], dtype=torch.int32, device=dev)
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+            if int(flag.item()) == 1:
+                uid = [_t.nccl_unique_id() if self.rank == 0 else None]
+                dist.broadcast_object_list(uid, src=0)
+                self.sim.nccl_init(uid[0], self.k, self.rank)
+                self.native = True
         self.exchange()
         self.sim.phase(2)
 
