@@ -123,6 +123,37 @@ int ts_domain_plan(int32_t n_nodes, int32_t n_links, const int32_t *from, const 
                    int64_t *nbr_strips, int32_t *n_out);
 int32_t ts_strip_bytes(void);
 
+/* SPEC text formats (SPEC.md "External Interfaces"; load_network
+ * SPEC.md:46-54).  Network file: line-oriented text, `#` comments, sections
+ * NODES (`id x y`, metres), LINKS (`id from to length lanes vmax`, metres,
+ * cells/s), TURNS (`node in_link out_link control [red_s green_s]`).  Ids
+ * are arbitrary integers, mapped to indices in file order; the priority
+ * class of a link is its lane count (reading R9); turn permissions are not
+ * restricted (all turns allowed); a `signal` TURNS record gives its node a
+ * fixed-time two-phase plan (reading R23): phase 0 green for green_s, the
+ * other phase for red_s (the node's first such record counts).
+ * ts_parse_network_text: pure host parser into caller arrays (NULL pointers
+ * = count only): node coordinates in mm, links (from / to as node indices,
+ * length in mm, lanes, vmax, class, file id), signals (node index, green,
+ * red).  TS_EINVAL with "line N: ..." in errbuf (char[256]) on a parse
+ * error, a dangling node reference or a non-positive length.
+ * ts_load_network_text: parse + ts_load_network (+ ts_set_signals).
+ * Plans file: `vehicle_id departure_s entry_cell link_1 ... link_n` per
+ * line, link ids of the network file; vids are the line order.
+ * ts_parse_plans_text: pure host parser (route_off[n_veh + 1], route links
+ * as indices); ts_load_plans_text: parse + ts_load_vehicles. */
+int ts_parse_network_text(const char *text, size_t len, int32_t *n_nodes, int32_t *n_links,
+                          int32_t *n_sig, int64_t *node_x_mm, int64_t *node_y_mm, int32_t *from,
+                          int32_t *to, int64_t *length_mm, int32_t *lanes, int32_t *vmax,
+                          int32_t *prio_class, int32_t *link_id, int32_t *sig_node,
+                          int32_t *sig_green, int32_t *sig_red, char *errbuf);
+int ts_load_network_text(ts_sim *h, const char *text, size_t len);
+int ts_parse_plans_text(const char *text, size_t len, int32_t n_links, const int32_t *link_id,
+                        int32_t *n_veh, int64_t *n_entries, int64_t *route_off,
+                        int32_t *route_links, int32_t *depart, int32_t *entry_cell,
+                        int32_t *vehicle_id, char *errbuf);
+int ts_load_plans_text(ts_sim *h, const char *text, size_t len);
+
 /* Fixed-time two-phase signals (reading R23) at the given
  * nodes: phase 0 = the incoming links of the node's maximal priority class,
  * green for the first green0 seconds of every (green0 + green1)-second

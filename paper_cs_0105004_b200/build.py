@@ -3,7 +3,8 @@ import os
 import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SRCS = ["csrc/tsim_kernels.cu", "csrc/tsim_rows.cu", "csrc/tsim_api.cu", "csrc/tsim_partition.cpp"]
+SRCS = ["csrc/tsim_kernels.cu", "csrc/tsim_rows.cu", "csrc/tsim_api.cu", "csrc/tsim_partition.cpp",
+        "csrc/tsim_text.cpp"]
 SO = os.path.join(HERE, "libtsim.so")
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v", "-ldl"]

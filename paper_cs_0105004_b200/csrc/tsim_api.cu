@@ -90,6 +90,7 @@ struct ts_sim {
   std::vector<int32_t> pl_vid, pl_lane, pl_cell, pl_v, pl_cur;
   std::vector<uint8_t> placed;
   std::vector<int32_t> arr0;     // arrival time of vehicles restored as arrived (-1 otherwise)
+  std::vector<int32_t> text_link_id;  // link ids of a network file (ts_load_network_text)
   std::vector<int32_t> first_link, entry_h;  // route[0] and entry cell (kept after init)
   // domain decomposition (§4; ts_set_domain): owned cells per link
   int32_t dom_k = 1, dom_me = 0;
@@ -610,6 +611,48 @@ int ts_set_arrived(ts_sim *h, int32_t n, const int32_t *vid, const int32_t *t_ar
 
 static uint32_t sig_word(int cycle, int shift, int len) {
   return (1u << 31) | (uint32_t)cycle | ((uint32_t)shift << 10) | ((uint32_t)len << 20);
+}
+
+int ts_load_network_text(ts_sim *h, const char *text, size_t len) {
+  if (!h || !text) return TS_EINVAL;
+  int32_t nn = 0, nl = 0, ns = 0;
+  char eb[256] = {0};
+  if (ts_parse_network_text(text, len, &nn, &nl, &ns, nullptr, nullptr, nullptr, nullptr, nullptr,
+                            nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, eb))
+    return fail(h, TS_EINVAL, "network text: %s", eb);
+  std::vector<int64_t> x(nn), y(nn), len_mm(nl);
+  std::vector<int32_t> fr(nl), to(nl), la(nl), vm(nl), cls(nl), ids(nl), sn(ns), sg(ns), sr(ns);
+  ts_parse_network_text(text, len, &nn, &nl, &ns, x.data(), y.data(), fr.data(), to.data(),
+                        len_mm.data(), la.data(), vm.data(), cls.data(), ids.data(), sn.data(),
+                        sg.data(), sr.data(), eb);
+  if (int rc = ts_load_network(h, nn, x.data(), y.data(), nl, fr.data(), to.data(), len_mm.data(),
+                               la.data(), vm.data(), cls.data(), -1))
+    return rc;
+  h->text_link_id = ids;
+  if (ns > 0) {
+    std::vector<int32_t> off(ns, 0);
+    return ts_set_signals(h, ns, sn.data(), sg.data(), sr.data(), off.data());
+  }
+  return TS_OK;
+}
+
+int ts_load_plans_text(ts_sim *h, const char *text, size_t len) {
+  if (!h || !text) return TS_EINVAL;
+  if (!h->have_net) return fail(h, TS_EINVAL, "load the network first");
+  std::vector<int32_t> ids = h->text_link_id;
+  if (ids.empty())  // network from arrays: link ids are the indices
+    for (int32_t k = 0; k < h->nl; k++) ids.push_back(k);
+  int32_t nv = 0;
+  int64_t ne = 0;
+  char eb[256] = {0};
+  if (ts_parse_plans_text(text, len, h->nl, ids.data(), &nv, &ne, nullptr, nullptr, nullptr,
+                          nullptr, nullptr, eb))
+    return fail(h, TS_EINVAL, "plans text: %s", eb);
+  std::vector<int64_t> off(nv + 1);
+  std::vector<int32_t> route(std::max<int64_t>(ne, 1)), dep(nv), entry(nv);
+  ts_parse_plans_text(text, len, h->nl, ids.data(), &nv, &ne, off.data(), route.data(), dep.data(),
+                      entry.data(), nullptr, eb);
+  return ts_load_vehicles(h, nv, off.data(), route.data(), dep.data(), entry.data());
 }
 
 int ts_set_signals(ts_sim *h, int32_t n, const int32_t *node, const int32_t *green0,

@@ -73,6 +73,11 @@ def load_library():
         "ts_domain_plan": (ctypes.c_int, [I32, I32, P, P, P, P, I32, P, I32, I32, P, P, P]),
         "ts_strip_bytes": (I32, []),
         "ts_nccl_unique_id": (ctypes.c_int, [P]),
+        "ts_parse_network_text": (ctypes.c_int, [P, ctypes.c_size_t, P, P, P, P, P, P, P, P, P, P,
+                                                 P, P, P, P, P, P]),
+        "ts_load_network_text": (ctypes.c_int, [P, P, ctypes.c_size_t]),
+        "ts_parse_plans_text": (ctypes.c_int, [P, ctypes.c_size_t, I32, P, P, P, P, P, P, P, P, P]),
+        "ts_load_plans_text": (ctypes.c_int, [P, P, ctypes.c_size_t]),
         "ts_nccl_init": (ctypes.c_int, [P, P, I32, I32]),
         "ts_exchange": (ctypes.c_int, [P]),
         "ts_busy_time": (ctypes.c_int, [P, ctypes.POINTER(ctypes.c_double)]),
@@ -163,6 +168,47 @@ def domain_plan(scn, k, domain_of_node, me):
     return nb[:n.value].tolist(), ns[:n.value].tolist()
 
 
+def parse_network_text(text):
+    """SPEC network file -> arrays (pure host; ts_parse_network_text)"""
+    lib = load_library()
+    b = text.encode() if isinstance(text, str) else bytes(text)
+    nn, nl, ns = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+    err = ctypes.create_string_buffer(256)
+    z = [None] * 12
+    if lib.ts_parse_network_text(b, len(b), ctypes.byref(nn), ctypes.byref(nl), ctypes.byref(ns),
+                                 *z, err):
+        raise TsError(err.value.decode())
+    out = dict(node_x_mm=np.zeros(nn.value, np.int64), node_y_mm=np.zeros(nn.value, np.int64),
+               link_from=np.zeros(nl.value, np.int32), link_to=np.zeros(nl.value, np.int32),
+               link_len_mm=np.zeros(nl.value, np.int64), link_lanes=np.zeros(nl.value, np.int32),
+               link_vmax=np.zeros(nl.value, np.int32), link_class=np.zeros(nl.value, np.int32),
+               link_id=np.zeros(nl.value, np.int32), sig_node=np.zeros(ns.value, np.int32),
+               sig_green=np.zeros(ns.value, np.int32), sig_red=np.zeros(ns.value, np.int32))
+    lib.ts_parse_network_text(b, len(b), ctypes.byref(nn), ctypes.byref(nl), ctypes.byref(ns),
+                              *(a.ctypes.data for a in out.values()), err)
+    return out
+
+
+def parse_plans_text(text, link_id):
+    """SPEC plans file -> (route_off, route, depart, entry, vehicle_id) with
+    route links as indices into link_id (pure host; ts_parse_plans_text)"""
+    lib = load_library()
+    b = text.encode() if isinstance(text, str) else bytes(text)
+    ids = _a(link_id, np.int32)
+    nv, ne = ctypes.c_int32(), ctypes.c_int64()
+    err = ctypes.create_string_buffer(256)
+    if lib.ts_parse_plans_text(b, len(b), ids.size, ids.ctypes.data, ctypes.byref(nv),
+                               ctypes.byref(ne), *([None] * 5), err):
+        raise TsError(err.value.decode())
+    off = np.zeros(nv.value + 1, np.int64)
+    route = np.zeros(max(1, ne.value), np.int32)
+    dep, ent, vid = (np.zeros(nv.value, np.int32) for _ in range(3))
+    lib.ts_parse_plans_text(b, len(b), ids.size, ids.ctypes.data, ctypes.byref(nv), ctypes.byref(ne),
+                            off.ctypes.data, route.ctypes.data, dep.ctypes.data, ent.ctypes.data,
+                            vid.ctypes.data, err)
+    return off, route[:ne.value], dep, ent, vid
+
+
 def nccl_unique_id():
     """128-byte NCCL communicator id for ts_nccl_init (one rank creates it)"""
     buf = ctypes.create_string_buffer(128)
@@ -237,6 +283,19 @@ class Sim:
         if place and scn.place_vid.size:
             pl = [i32(scn.place_vid), i32(scn.place_lane), i32(scn.place_cell), i32(scn.place_v)]
             self._check(self.lib.ts_place_vehicles(self.h, pl[0].size, *(a.ctypes.data for a in pl)))
+
+    def load_text(self, network_text, plans_text):
+        """load a SPEC network file and plans file (ts_load_network_text,
+        ts_load_plans_text)"""
+        for fn, t in (("ts_load_network_text", network_text), ("ts_load_plans_text", plans_text)):
+            b = t.encode() if isinstance(t, str) else bytes(t)
+            self._check(getattr(self.lib, fn)(self.h, b, len(b)))
+        self.n_veh = sum(1 for ln in (plans_text if isinstance(plans_text, str)
+                                      else plans_text.decode()).splitlines()
+                         if ln.split("#")[0].strip())
+        net = parse_network_text(network_text)
+        self.n_links = net["link_from"].size
+        self.lanes = net["link_lanes"]
 
     def place_at(self, vid, cursor, lane, cell, v):
         """place vehicles on link route[cursor] (restore / repartition)"""

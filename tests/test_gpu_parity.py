@@ -229,3 +229,28 @@ def test_config4a_full_size_prefix():
     s = scenarios.big_grid(seed=1, dest_radius=4, name="config4a_full_shortroutes")
     assert s.n_vehicles == 20_889_600
     run_parity(s, 3, tsim.FLAG_FUSED | tsim.FLAG_HASH, full_every=3, hash_every=3)
+
+
+def test_spec_text_files_load():
+    """network and plans in the SPEC text formats (ts_load_network_text /
+    ts_load_plans_text) give the same run as the array loaders"""
+    s = scenarios.config("1")
+    ids = np.arange(s.n_links) * 10 + 3  # arbitrary file ids
+    net = ["NODES"] + [f"{i + 100} {x / 1000} {y / 1000}" for i, (x, y) in
+                       enumerate(zip(s.node_x, s.node_y))]
+    net += ["LINKS"] + [f"{ids[k]} {a + 100} {b + 100} {ln / 1000} {la} {vm}" for k, (a, b, ln, la, vm)
+                        in enumerate(zip(s.link_from, s.link_to, s.link_len_mm, s.link_lanes,
+                                         s.link_vmax))]
+    plans = [f"{f} {s.depart[f]} {s.entry[f]} " +
+             " ".join(str(ids[k]) for k in s.route[s.route_off[f]:s.route_off[f + 1]])
+             for f in range(s.n_vehicles)]
+    # the text network's class is the lane count (R9): align the array run
+    s.link_class = np.asarray(s.link_lanes, np.int32).copy()
+    o = oracle.Oracle.from_scenario(s)
+    g = tsim.Sim(p_slow=s.p_slow, seed=s.seed, flags=FUSED)
+    g.load_text("\n".join(net) + "\n", "\n".join(plans) + "\n")
+    g.init(0)
+    assert g.state_hash() == o.state_hash()
+    oh = o.run_hashes(200)
+    g.step(200)
+    assert list(g.history(1, 200)["hash"]) == list(oh)
