@@ -269,6 +269,13 @@ int ts_orb_partition(int32_t n_nodes, const int64_t *node_x_mm,
                      const int64_t *node_y_mm, const double *node_weight,
                      int32_t k, int32_t *domain_of_node);
 
+/* ts_orb_partition of this handle's network (node weights: NULL = half of
+ * cells x lanes of every attached link) followed by
+ * ts_set_domain(h, k, partition, me); the partition is copied to
+ * domain_of_node_out[n_nodes] (nullable).  Before ts_init. */
+int ts_partition(ts_sim *h, int32_t k, const double *node_weight, int32_t me,
+                 int32_t *domain_of_node_out);
+
 /* Multilevel k-way partition of the node graph (the
  * METIS-style alternative to ORB): heavy-edge matching
  * coarsening (seeded), ORB of the coarsest graph, greedy boundary

@@ -2251,3 +2251,29 @@ int ts_orb_partition(int32_t n_nodes, const int64_t *node_x_mm, const int64_t *n
 }
 
 }  // extern "C"
+
+extern "C" {
+// ORB partition of the handle's own network with the paper's default node
+// weights (half of cells x lanes of every attached link)
+// or the given ones, and this handle set up as domain `me` (ts_set_domain).
+int ts_partition(ts_sim *h, int32_t k, const double *node_weight, int32_t me,
+                 int32_t *domain_of_node_out) {
+  if (!h) return TS_EINVAL;
+  if (!h->have_net) return fail(h, TS_EINVAL, "load the network first");
+  std::vector<double> w(h->nn, 1e-9);
+  if (node_weight) {
+    w.assign(node_weight, node_weight + h->nn);
+  } else {
+    for (int j = 0; j < h->nl; j++) {
+      const double lw = 0.5 * (double)h->ncell[j] * h->lanes[j];
+      w[h->from[j]] += lw;
+      w[h->to[j]] += lw;
+    }
+  }
+  std::vector<int32_t> dom(h->nn);
+  if (ts_orb_partition(h->nn, h->nx.data(), h->ny.data(), w.data(), k, dom.data()))
+    return fail(h, TS_EINVAL, "bad partition: k = %d for %d nodes", k, h->nn);
+  if (domain_of_node_out) std::copy(dom.begin(), dom.end(), domain_of_node_out);
+  return ts_set_domain(h, k, dom.data(), me);
+}
+}

@@ -78,6 +78,7 @@ def load_library():
         "ts_load_network_text": (ctypes.c_int, [P, P, ctypes.c_size_t]),
         "ts_parse_plans_text": (ctypes.c_int, [P, ctypes.c_size_t, I32, P, P, P, P, P, P, P, P, P]),
         "ts_load_plans_text": (ctypes.c_int, [P, P, ctypes.c_size_t]),
+        "ts_partition": (ctypes.c_int, [P, I32, P, I32, P]),
         "ts_nccl_init": (ctypes.c_int, [P, P, I32, I32]),
         "ts_exchange": (ctypes.c_int, [P]),
         "ts_busy_time": (ctypes.c_int, [P, ctypes.POINTER(ctypes.c_double)]),
@@ -275,6 +276,7 @@ class Sim:
         self._check(self.lib.ts_load_vehicles(self.h, scn.n_vehicles, *(_p(a) for a in veh)))
         self.n_veh = scn.n_vehicles
         self.n_links = scn.n_links
+        self._n_nodes = scn.n_nodes
         self.lanes = np.asarray(scn.link_lanes, dtype=np.int32)
         sig = getattr(scn, "sig_node", None)
         if sig is not None and len(sig):
@@ -324,6 +326,16 @@ class Sim:
         self._check(self.lib.ts_exchange_plan(self.h, cap, nb.ctypes.data, ns.ctypes.data,
                                               off.ctypes.data, ctypes.byref(n)))
         return [(int(nb[i]), int(ns[i]), int(off[i])) for i in range(n.value)]
+
+    def partition(self, k, me, node_weight=None, n_nodes=None):
+        """ORB of the loaded network + this handle as domain `me`
+        (ts_partition); returns the partition"""
+        n = int(n_nodes if n_nodes is not None else self._n_nodes)
+        out = np.zeros(n, np.int32)
+        w = None if node_weight is None else _a(node_weight, np.float64)
+        self._check(self.lib.ts_partition(self.h, int(k), None if w is None else w.ctypes.data,
+                                          int(me), out.ctypes.data))
+        return out
 
     def nccl_init(self, unique_id, nranks, rank):
         """join the library's own NCCL communicator (native exchanges)"""

@@ -177,3 +177,16 @@ def test_adaptive_rebalance_from_measured_times():
             e_after = load_new.mean() / load_new.max()
     assert e_after > e_before
     assert_same(o.vehicles(), d.vehicles(), "after rebalancing")
+
+
+def test_ts_partition_matches_orb():
+    """ts_partition: ORB of the handle's own network with the paper's node
+    weights, the same partition as domains.partition, and the handle runs
+    as that domain"""
+    s = scenarios.config("1")
+    g = tsim.Sim(p_slow=s.p_slow, seed=s.seed, flags=FUSED)
+    g.load(s)
+    dom = g.partition(4, 2)
+    assert np.array_equal(dom, domains.partition(s, 4))
+    g.init(0)
+    assert len(g.exchange_plan()) >= 1
