@@ -123,6 +123,11 @@ struct ts_sim {
   WarpLayout lay{};
   int threads = 256, blocks = 1, smem = 0;
   bool gfused = false, rfused = false, node_warp = false;
+  // the periodic link as a chain of row-tile segments joined by pass-through
+  // virtual nodes (row kernel instead of the warp-per-tile kernels)
+  bool ring_rows = false;
+  std::vector<NodeOut> ring_nodeout;
+  int32_t *d_ring_next = nullptr, *d_ring_prev = nullptr, *d_row_a = nullptr;
   // general tiles (halo / long / periodic links): byte codes at device
   // offsets of their own; uploaded as d_tiles
   std::vector<TileDesc> gtiles;
@@ -736,6 +741,8 @@ static void owned_range(int n, int dfrom, int dto, int me, int &lo, int &hi) {
 static void build_tiles(ts_sim *h) {
   const int tc = h->cfg.tile_cells > 0 ? h->cfg.tile_cells : 512;
   const bool dom = h->dom_k > 1;
+  h->ring_rows = h->periodic >= 0 && !dom && !(h->cfg.flags & TS_FLAG_GENERAL) &&
+                 h->lanes[h->periodic] <= 32 && getenv("TSIM_RING_GENERAL") == nullptr;
   h->tiles.clear();
   h->link_tile0.assign(h->nl + 1, 0);
   h->link_ntiles.assign(h->nl, 0);
@@ -758,11 +765,12 @@ static void build_tiles(ts_sim *h) {
     const bool split = lo > 0 || hi < n;
     // the ring is one very long link: smaller tiles give its warp-per-tile
     // kernels more warps (config 2: 512 -> 91 us, 256 -> 66 us per step)
-    const int tck = (per && h->cfg.tile_cells <= 0) ? 256 : tc;
+    const bool rseg = per && h->ring_rows;  // segments of <= kRowMaxCells cells
+    const int tck = rseg ? kRowMaxCells : (per && h->cfg.tile_cells <= 0) ? 256 : tc;
     int nt = (span + tck - 1) / tck;
     if (nt > 1 && span / nt < 10) nt = std::max(1, span / 10);
     h->link_ntiles[k] = nt;
-    const bool halo = per || nt > 1 || split;
+    const bool halo = !rseg && (per || nt > 1 || split);
     int a = lo;
     for (int i = 0; i < nt; i++) {
       const int w = span / nt + (i < span % nt ? 1 : 0);
@@ -777,7 +785,8 @@ static void build_tiles(ts_sim *h) {
       uint8_t f = 0;
       if (!per && a == 0) f |= kFirst;
       if (!per && a + w == n) f |= kLast;
-      if (per) f |= kPeriodic;
+      if (per && !rseg) f |= kPeriodic;
+      if (rseg) f |= kFirst | kLast | kRingSeg;
       if (halo) {
         f |= kHalo;
         if (per || a > 0) f |= kHasUp;
@@ -902,7 +911,9 @@ static void build_tiles(ts_sim *h) {
   for (const TileDesc &d : h->gtiles) nc_max = std::max(nc_max, (int)d.L * tile_stride(d.w, d.flags));
   h->lay = warp_layout(nc_max);
   h->gfused = (h->cfg.flags & TS_FLAG_FUSED) && h->nstrips == 0;
-  h->rfused = (h->cfg.flags & TS_FLAG_FUSED) != 0;
+  // ring segment rows take their lane change in a launch of its own (its
+  // neighbour segments must hold S(t))
+  h->rfused = (h->cfg.flags & TS_FLAG_FUSED) != 0 && !h->ring_rows;
 }
 
 // incoming lanes of every node in priority order (R9: major class first,
@@ -957,7 +968,58 @@ static bool build_node_lanes(ts_sim *h, std::vector<NodeLane> &lanes,
 // node-lane indices (tail records, node grants): the lane's position in the
 // node kernel's lane array, or the identity for the thread-per-node kernel;
 // lanes without a node of this domain share a dummy slot at the end
+// the periodic link's segments joined by pass-through virtual nodes: node s
+// takes the L lanes of segment s to the same lanes of segment s + 1 (mod S)
+// -- a straight continuation with a single approach, so the node kernel's
+// entry space and crossing are exactly the in-lane gap and move across the
+// cut (reading R2 / R10 on a ring, where no vehicle can pass two cuts)
+static int setup_ring_nodes(ts_sim *h) {
+  const int k = h->periodic, L = h->lanes[k];
+  std::vector<int> seg;  // tiles of the ring in cell order
+  for (size_t ti = 0; ti < h->tiles.size(); ti++)
+    if (h->tiles[ti].flags & kRingSeg) seg.push_back((int)ti);
+  const int S = (int)seg.size(), per_chunk = 32 / L;
+  std::vector<NodeLane> nlanes;
+  h->ring_nodeout.assign(S, NodeOut{});
+  std::vector<int32_t> nxt(h->rows.size(), -1), prv(h->rows.size(), -1), ra(h->rows.size(), 0);
+  for (int s = 0; s < S; s++) {
+    if (s % per_chunk == 0)
+      while (nlanes.size() % 32) nlanes.push_back(NodeLane{-1, 0, 0u, 0, 0, 1, 0});
+    const int first = (int)(nlanes.size() % 32);
+    const TileDesc &d = h->tiles[seg[s]];
+    const TileDesc &dn = h->tiles[seg[(s + 1) % S]], &dp = h->tiles[seg[(s + S - 1) % S]];
+    for (int l = 0; l < L; l++) {
+      const int row = h->tile_row[seg[s]] + l;
+      RowDesc &r = h->rows[row];
+      r.nli = (int32_t)nlanes.size();
+      r.lg = s * L + l;  // node-out-lane index: segment s is the target of node s - 1
+      nxt[row] = h->tile_row[seg[(s + 1) % S]] + l;
+      prv[row] = (h->tile_row[seg[(s + S - 1) % S]] + l) | ((int32_t)dp.w << 24);
+      ra[row] = d.a;
+      // pass-through (major | 2): out-slot 0 is the next segment, straight on
+      nlanes.push_back(NodeLane{k, s, 0u, (uint8_t)l, (uint8_t)(1 | 2), (uint8_t)h->vmax[k],
+                                (uint8_t)first});
+    }
+    h->ring_nodeout[s] = NodeOut{((s + 1) % S) * L, (int16_t)L, (int16_t)dn.w};
+  }
+  while (nlanes.size() % 32) nlanes.push_back(NodeLane{-1, 0, 0u, 0, 0, 1, 0});
+  h->node_warp = true;
+  h->nchunks = (int32_t)(nlanes.size() / 32);
+  h->n_nli = (int64_t)nlanes.size() + 1;
+  h->n_nlo = (int64_t)S * L + 1;
+  h->nli.assign(h->nlanes, 0);
+  h->nlo.assign(h->nlanes, 0);
+  h->d_lane_sig = nullptr;
+  int rc;
+  if ((rc = upload(h, &h->d_nlanes, nlanes))) return rc;
+  if ((rc = upload(h, &h->d_ring_next, nxt))) return rc;
+  if ((rc = upload(h, &h->d_ring_prev, prv))) return rc;
+  if ((rc = upload(h, &h->d_row_a, ra))) return rc;
+  return 0;
+}
+
 static int setup_node_lanes(ts_sim *h) {
+  if (h->ring_rows) return setup_ring_nodes(h);
   std::vector<NodeLane> nlanes;
   std::vector<uint32_t> lsig;
   h->node_warp = h->periodic < 0 && !(h->cfg.flags & (TS_FLAG_GENERAL | TS_FLAG_NODE_GENERAL)) &&
@@ -1100,6 +1162,9 @@ static NodeParams node_params(ts_sim *h, int t) {
 static RowsParams rows_params(ts_sim *h) {
   RowsParams r{};
   r.rows = h->d_rows;
+  r.ring_next = h->ring_rows ? h->d_ring_next : nullptr;
+  r.ring_prev = h->ring_rows ? h->d_ring_prev : nullptr;
+  r.row_a = h->ring_rows ? h->d_row_a : nullptr;
   r.gvoff = h->d_gvoff;
   r.planes_in = h->d_planes[h->rcur];
   r.planes_out = h->d_planes[h->rcur ^ 1];
@@ -1193,7 +1258,10 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
     const int64_t pos = d.off + (int64_t)h->pl_lane[i] * row_pitch(d.w) + (h->pl_cell[i] - d.a);
     if (code[pos] != kEmpty) return fail(h, TS_EINVAL, "placement %zu: cell taken", i);
     const int64_t ro = h->roff[f];
-    const int slot = c + 1 < h->roff[f + 1] - ro ? (int)h->rslot[ro + c + 1] : kSlotFinal;
+    // ring segment rows: every vehicle goes straight on through the virtual
+    // nodes (out-slot 0, all lanes allowed) instead of being on a final link
+    const int slot = h->ring_rows ? 0
+                     : c + 1 < h->roff[f + 1] - ro ? (int)h->rslot[ro + c + 1] : kSlotFinal;
     code[pos] = (uint8_t)(h->pl_v[i] | (slot << 3));
     cellvid[pos] = f;
     h->n_placed++;
@@ -1351,6 +1419,7 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
   if ((rc = upload(h, &h->d_halo_up, h->halo_up))) return rc;
   if ((rc = upload(h, &h->d_halo_dn, h->halo_dn))) return rc;
   if ((rc = upload(h, &h->d_vmax, vmax8))) return rc;
+  if (h->ring_rows) h->tt[h->periodic] = 0u;  // straight on through the virtual nodes
   if ((rc = upload(h, &h->d_tt, h->tt))) return rc;
   if ((rc = upload(h, &h->d_out_pos, h->out_pos))) return rc;
   {  // routes as out-slot sequences (built at load), through pinned staging
@@ -1389,7 +1458,7 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
       nodeout[i] = NodeOut{h->nlo[h->lgid[k]], (int16_t)h->lanes[k],
                            (int16_t)std::min(h->ncell[k], 32767)};
     }
-    if ((rc = upload(h, &h->d_nodeout, nodeout))) return rc;
+    if ((rc = upload(h, &h->d_nodeout, h->ring_rows ? h->ring_nodeout : nodeout))) return rc;
   }
   {
     std::vector<VehPos> vp(h->nv);
@@ -1523,7 +1592,7 @@ static void phase_lc(ts_sim *h) {
     h->gcur ^= 1;
   }
   if (h->ngroups > 0 && !h->rows_s1) {
-    rows_launch(h, step_params(h, t, kModeLC));
+    rows_launch(h, step_params(h, t, kModeLC | (h->ring_rows ? kModeHalo : 0)));
     h->rcur ^= 1;
   }
   h->gen_s1 = h->rows_s1 = true;

@@ -24,6 +24,7 @@ constexpr uint8_t kPeriodic = 4;  // tile of the periodic (ring) link
 constexpr uint8_t kHalo = 8;      // tile reads 5-cell halos from strips
 constexpr uint8_t kHasUp = 16;    // upstream halo present
 constexpr uint8_t kHasDn = 32;    // downstream halo present
+constexpr uint8_t kRingSeg = 128; // a segment of the periodic link run as a row tile
 
 // One tile = cells [a, a+w) of all lanes of one link.  Lane l of the tile
 // is a "row" of Wp = roundup(w, 4) cells: codes at code[off + l*Wp + i],
@@ -188,6 +189,7 @@ constexpr int kModeInject = 2;  // injection (H6)
 constexpr int kModeLC = 4;      // lane change on the output state (H1)
 constexpr int kModeHash = 8;    // accumulate state hash
 constexpr int kModeWork = 16;   // per-link work counters
+constexpr int kModeHalo = 32;   // ring segment rows: the lane change reads the neighbour segments
 
 struct StepParams {
   const TileDesc *tiles;
@@ -267,6 +269,10 @@ struct NodeParams {
 
 struct RowsParams {
   const RowDesc *rows;        // [ngroups * 32]
+  // ring segment rows (kModeHalo): per row slot the slot of the next
+  // segment's row in the same lane, and of the previous one | its width << 24;
+  // the segment's first cell (for the state hash); NULL otherwise
+  const int32_t *ring_next, *ring_prev, *row_a;
   const int32_t *gvoff;       // first entry of each group's vid block (multiple of 4)
   const uint32_t *planes_in;  // S1(t) (fused) or S(t)
   uint32_t *planes_out;

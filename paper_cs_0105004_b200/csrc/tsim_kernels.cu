@@ -495,19 +495,22 @@ __device__ __forceinline__ Cand node_candidate(const NodeParams &P, uint64_t rec
 // head: occupancy of the first cells of the target lane.  The route
 // position record (16 bytes per vehicle) is read only for a crossing.
 __device__ __forceinline__ int node_grant(const NodeParams &P, const Cand &c, int vk, uint8_t head,
-                                          uint32_t &crossings) {
+                                          uint32_t &crossings, bool pass = false) {
   const int E = min(ctz32((uint32_t)head | 0x20u), min(kGmax, c.n2));
   if (E == 0) return 0;
   const int v3 = nasch_v3(c.v, vk, min(kGmax, c.d + E), (uint32_t)P.t, (uint32_t)c.vid, P.k0,
                           P.k1, P.p32);
   if (v3 > c.d) {
-    const VehPos q = P.vpos[c.vid];
-    const int nslot = (q.p + 2 < q.e) ? (int)P.rslot[q.p + 2] : kSlotFinal;
-    P.vpos[c.vid].p = q.p + 1;
+    int nslot = 0;  // pass-through node of a ring: straight on, same route position
+    if (!pass) {
+      const VehPos q = P.vpos[c.vid];
+      nslot = (q.p + 2 < q.e) ? (int)P.rslot[q.p + 2] : kSlotFinal;
+      P.vpos[c.vid].p = q.p + 1;
+    }
     const int y2 = v3 - c.d - 1;
     P.entr[c.tgt] = (uint64_t)(uint32_t)c.vid | ((uint64_t)(v3 | (nslot << 3)) << 32) |
                     ((uint64_t)y2 << 40) | ((uint64_t)((P.t + 1) & 0x1FFFFF) << 43);
-    crossings++;
+    crossings += pass ? 0u : 1u;
   }
   return E;
 }
@@ -586,7 +589,7 @@ __global__ void __launch_bounds__(256) k_node_warp(const NodeParams P_, const No
 #pragma unroll
   for (int k = 0; k < kNodeILP; k++) {  // stage 4: grants
     int ext = 0;
-    if (win[k]) ext = node_grant(P, cd[k], e[k].vk, head[k], crossings);
+    if (win[k]) ext = node_grant(P, cd[k], e[k].vk, head[k], crossings, (e[k].major & 2) != 0);
     if (act[k]) P.ext[32 * (c0 + k) + lane] = (uint8_t)ext;
   }
   node_flush(P, crossings, red);

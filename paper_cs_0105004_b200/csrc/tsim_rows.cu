@@ -203,7 +203,7 @@ struct RowWords {
 static __device__ __noinline__ uint64_t hash_row(RowWords oo, RowWords v0, RowWords v1,
                                                  RowWords v2, RowWords inj, int ent_y,
                                                  uint32_t ent_e, const int32_t *vin,
-                                                 const int32_t *scratch, int link, int l) {
+                                                 const int32_t *scratch, int link, int l, int a) {
   uint64_t h = 0;
   int k = 0;
   for (int c = 0; c < kRowMaxCells; c++) {
@@ -215,7 +215,7 @@ static __device__ __noinline__ uint64_t hash_row(RowWords oo, RowWords v0, RowWo
     else e = (uint32_t)vin[k++];
     const int v = (int)((v0.w[i] >> x) & 1u) | (int)(((v1.w[i] >> x) & 1u) << 1) |
                   (int)(((v2.w[i] >> x) & 1u) << 2);
-    h += vmix((int)(e & kVidMask), link, l, c, v);
+    h += vmix((int)(e & kVidMask), link, l, a + c, v);
   }
   return h;
 }
@@ -279,6 +279,7 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
   constexpr bool do_move = (MODE & kModeMove) != 0;
   constexpr bool hash = (MODE & kModeHash) != 0;
   constexpr bool lc = (MODE & kModeLC) != 0;
+  constexpr bool halo = (MODE & kModeHalo) != 0;  // ring segment rows
   const int lct = do_move ? P.t + 1 : P.t;  // time of the lane-change sub-step
   const int dir = (lct & 1) ? -1 : +1;      // R4
   Acc acc = {};
@@ -640,6 +641,27 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
       uint32_t T0[NW];
 #pragma unroll
       for (int i = 0; i < NW; i++) T0[i] = shfl_w(OO[i], lane + dir);
+      // ring segment rows (kModeHalo): the lane change looks across the
+      // cuts -- the next segment's first cells ahead, the previous
+      // segment's last cells behind (S(t), the launch's input)
+      uint32_t hx = 0u, hp = 0u;
+      if (halo && w > 0) {
+        const int slot = g * 32 + lane;
+        const int ns = R.ring_next[slot], pq = R.ring_prev[slot];
+        hx = R.planes_in[group_plane_base(ns >> 5) + (ns & 31)];  // occupancy word 0
+        const int ps = pq & 0xFFFFFF, pw = (int)((uint32_t)pq >> 24), kq = pw >> 5, sq = pw & 31;
+        const uint32_t *pb = R.planes_in + group_plane_base(ps >> 5) + (ps & 31);
+        hp = kq == 0 ? pb[0] << (32 - sq)
+                     : (sq == 0 ? pb[(kq - 1) * 32] : __funnelshift_r(pb[(kq - 1) * 32], pb[kq * 32], sq));
+      }
+      const uint32_t thx = shfl_w(hx, lane + dir), thp = shfl_w(hp, lane + dir);
+      // cells 32 i .. 32 i + 31 of a row, those past its end from the next segment
+      auto ext_word = [&](const uint32_t (&X)[NW], uint32_t nx, int i) -> uint32_t {
+        const int o = 32 * i - w;
+        const uint32_t nxt = o >= 0 ? (o < 32 ? nx >> o : 0u) : (o > -32 ? nx << (-o) : 0u);
+        if (i >= NW) return nxt;
+        return (X[i] & VAL[i]) | (nxt & ~VAL[i]);
+      };
       uint32_t cand[NW];
       bool anyc = false;
 #pragma unroll
@@ -654,9 +676,13 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
           // word i: gaps ahead in the own and target lanes (stop at the row
           // end, R2); gap behind in the target lane (before the row start =
           // empty).  G_k / TG_k / BK_k = gap >= k.
-          const uint32_t o0 = OO[i] | ~VAL[i], o1 = i + 1 < NW ? (OO[i + 1] | ~VAL[i + 1]) : FULL;
-          const uint32_t t0 = T0[i] | ~VAL[i], t1 = i + 1 < NW ? (T0[i + 1] | ~VAL[i + 1]) : FULL;
-          const uint32_t tp = i > 0 ? T0[i - 1] : 0u;
+          const uint32_t o0 = halo ? ext_word(OO, hx, i) : OO[i] | ~VAL[i],
+                         o1 = halo ? ext_word(OO, hx, i + 1)
+                                   : (i + 1 < NW ? (OO[i + 1] | ~VAL[i + 1]) : FULL);
+          const uint32_t t0 = halo ? ext_word(T0, thx, i) : T0[i] | ~VAL[i],
+                         t1 = halo ? ext_word(T0, thx, i + 1)
+                                   : (i + 1 < NW ? (T0[i + 1] | ~VAL[i + 1]) : FULL);
+          const uint32_t tp = i > 0 ? T0[i - 1] : (halo ? thp : 0u);
           uint32_t G[6], TG[6], BK = FULL, BKv = FULL;
           G[0] = TG[0] = FULL;
 #pragma unroll
@@ -859,7 +885,8 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
           inj.w[i] = INJ[i];
         }
         acc.hash += hash_row(oo, v0, v1, v2, inj, ent_y, ent_e, vin,
-                             R.inj_scratch + ((size_t)g * 32 + lane) * kRowMaxCells, link, l);
+                             R.inj_scratch + ((size_t)g * 32 + lane) * kRowMaxCells, link, l,
+                             R.row_a ? R.row_a[g * 32 + lane] : 0);
       }
       (void)gmask;
     }
@@ -923,7 +950,7 @@ __global__ void __launch_bounds__(128) k_rows_hash(const RowsParams R, unsigned 
                       (int)(((pl[(2 * NW + i) * 32] >> x) & 1u) << 1) |
                       (int)(((pl[(3 * NW + i) * 32] >> x) & 1u) << 2);
         const uint32_t e = (uint32_t)vl[k++];
-        h += vmix((int)(e & kVidMask), rd.link, rd.l, 32 * i + x, v);
+        h += vmix((int)(e & kVidMask), rd.link, rd.l, (R.row_a ? R.row_a[gid] : 0) + 32 * i + x, v);
         cnt++;
       }
     }
@@ -941,11 +968,12 @@ __global__ void __launch_bounds__(128) k_rows_hash(const RowsParams R, unsigned 
 
 void launch_rows(const StepParams &p, const RowsParams &r, int blocks, int threads, int smem,
                  void *stream, bool pdl) {
-  switch (p.mode & (kModeMove | kModeLC | kModeHash)) {
+  switch (p.mode & (kModeMove | kModeLC | kModeHash | kModeHalo)) {
 #define TS_ROWS_CASE(m) \
   case m: launch_pdl(k_rows<m>, blocks, threads, smem, stream, pdl, p, r); break;
     TS_ROWS_CASE(0) TS_ROWS_CASE(1) TS_ROWS_CASE(4) TS_ROWS_CASE(5)
     TS_ROWS_CASE(8) TS_ROWS_CASE(9) TS_ROWS_CASE(12) TS_ROWS_CASE(13)
+    TS_ROWS_CASE(36) TS_ROWS_CASE(44)
 #undef TS_ROWS_CASE
   }
 }
@@ -970,7 +998,9 @@ cudaError_t set_rows_smem(int bytes) {  // only ever raised (see set_smem_attrs)
                         cudaFuncSetAttribute(k_rows<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
                         cudaFuncSetAttribute(k_rows<9>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
                         cudaFuncSetAttribute(k_rows<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
-                        cudaFuncSetAttribute(k_rows<13>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes)})
+                        cudaFuncSetAttribute(k_rows<13>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
+                        cudaFuncSetAttribute(k_rows<36>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
+                        cudaFuncSetAttribute(k_rows<44>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes)})
     if (x != cudaSuccess) e = x;
   return e;
 }
