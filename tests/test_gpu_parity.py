@@ -254,3 +254,37 @@ def test_spec_text_files_load():
     oh = o.run_hashes(200)
     g.step(200)
     assert list(g.history(1, 200)["hash"]) == list(oh)
+
+
+# ------------------------------------------------------------- edge cases
+@pytest.mark.parametrize("p", [0.0, 1.0])
+def test_degenerate_slowdown_probabilities(p):
+    """p = 0 (no draw ever brakes: the unique deterministic trajectory,
+    R22) and p = 1 (every mover brakes, P32 = 2^32 compares as 64-bit)"""
+    s = scenarios.big_grid(rows=8, cols=8, seed=6, name="grid8p")
+    s.p_slow = p
+    run_parity(s, 120, FUSED, full_every=40, hash_every=40)
+    r = scenarios.ring(n_cells=2000, lanes=3, density=0.3, seed=4)
+    r.p_slow = p
+    run_parity(r, 120, FUSED, full_every=40, hash_every=40)
+
+
+def test_empty_networks():
+    """no vehicles at all: every step runs (and exchanges), the state stays
+    empty, the hash is 0"""
+    s = scenarios.grid_trips(rows=4, cols=4, n_veh=0, name="grid_empty")
+    o, g = run_parity(s, 30, FUSED, full_every=10, hash_every=10)
+    assert g.state_hash() == 0 and g.totals()["active"] == 0
+    r = scenarios.ring(n_cells=500, lanes=2, n_veh=0, seed=1)
+    o, g = run_parity(r, 30, FUSED, full_every=10, hash_every=10)
+    assert g.state_hash() == 0
+
+
+def test_eight_lane_links_and_minimum_ring():
+    """the widest links (8 lanes, kMaxLanes) on a dense grid, and the
+    smallest ring (10 cells, one segment that is its own neighbour)"""
+    s = scenarios.big_grid(rows=6, cols=6, lanes=8, cells=40, density=0.25, seed=9,
+                           name="grid6x8lanes")
+    run_parity(s, 120, FUSED, full_every=30, hash_every=30)
+    r = scenarios.ring(n_cells=10, lanes=3, n_veh=9, seed=2)
+    run_parity(r, 200, FUSED, full_every=20, hash_every=20)
