@@ -18,6 +18,7 @@
 #include <chrono>
 #include <utility>
 #include <memory>
+#include <unordered_set>
 #include <vector>
 
 #include "../../include/tsim.h"
@@ -263,6 +264,17 @@ static void parallel_for(int64_t n, F f) {
   for (int i = 0; i < nt; i++)
     th.emplace_back([=, &f]() { f(n * i / nt, n * (i + 1) / nt, i); });
   for (auto &t : th) t.join();
+}
+
+// a host staging array of n copies of v, first-touched by the host cores
+// in parallel (value-initialising GB-sized vectors serially dominates init)
+template <typename T>
+using HostVec = std::vector<T, UninitAlloc<T>>;
+template <typename T>
+static HostVec<T> filled(size_t n, T v) {
+  HostVec<T> a(n);
+  parallel_for((int64_t)n, [&](int64_t lo, int64_t hi, int) { std::fill(a.data() + lo, a.data() + hi, v); });
+  return a;
 }
 
 // the link at cursor c of vehicle f: the walk along its out-slots
@@ -520,46 +532,49 @@ int ts_load_vehicles(ts_sim *h, int32_t n, const int64_t *route_off, const int32
   if (h->have_veh) return fail(h, TS_EINVAL, "vehicles already loaded");
   if (n < 0) return fail(h, TS_EINVAL, "negative vehicle count");
   if (n > 0 && route_off[0] != 0) return fail(h, TS_EINVAL, "route_off[0] != 0");
-  // validation in parallel over vehicles: error code of vehicle i (0 = ok);
-  // the first failing vehicle is reported
-  auto check = [&](int32_t i) -> int {
+  // validation in parallel over vehicles, fused with the conversion of the
+  // routes to out-slot sequences (one pass over the route links): error code
+  // of vehicle i (0 = ok); the first failing vehicle is reported.  Empty or
+  // decreasing route offsets are found first (they size the slot array).
+  auto check = [&](int32_t i, bool conv) -> int {
     const int64_t a = route_off[i], b = route_off[i + 1];
     if (b <= a) return 1;
     for (int64_t j = a; j < b; j++) {
       const int32_t k = route_links[j];
       if (k < 0 || k >= h->nl) return 2;
       if (j > a && h->to[route_links[j - 1]] != h->from[k]) return 3;
+      if (conv) h->rslot[j] = j > a ? (uint8_t)h->out_pos[k] : (uint8_t)0xFF;
     }
     if (entry_cell[i] < 0 || entry_cell[i] >= h->ncell[route_links[a]]) return 4;
     return 0;
   };
-  std::vector<int32_t> first_bad(64, INT32_MAX);
-  parallel_for(n, [&](int64_t lo, int64_t hi, int t) {
-    for (int64_t i = lo; i < hi; i++)
-      if (check((int32_t)i)) {
-        first_bad[t] = (int32_t)i;
-        return;
-      }
-  });
-  const int32_t bad = *std::min_element(first_bad.begin(), first_bad.end());
+  auto first_failing = [&](auto pred) {
+    std::vector<int32_t> first_bad(64, INT32_MAX);
+    parallel_for(n, [&](int64_t lo, int64_t hi, int t) {
+      for (int64_t i = lo; i < hi; i++)
+        if (pred((int32_t)i)) {
+          first_bad[t] = (int32_t)i;
+          return;
+        }
+    });
+    return *std::min_element(first_bad.begin(), first_bad.end());
+  };
+  static const char *msg[] = {"", "empty route", "bad link", "route links not consecutive",
+                              "entry cell outside link"};
+  const int32_t bad_off = first_failing([&](int32_t i) { return route_off[i + 1] <= route_off[i]; });
+  if (bad_off != INT32_MAX) return fail(h, TS_EINVAL, "vehicle %d: %s", bad_off, msg[1]);
+  h->rslot.resize(n > 0 ? route_off[n] : 0);
+  const int32_t bad = first_failing([&](int32_t i) { return check(i, true) != 0; });
   if (bad != INT32_MAX) {
-    static const char *msg[] = {"", "empty route", "bad link", "route links not consecutive",
-                                "entry cell outside link"};
-    return fail(h, TS_EINVAL, "vehicle %d: %s", bad, msg[check(bad)]);
+    decltype(h->rslot)().swap(h->rslot);
+    return fail(h, TS_EINVAL, "vehicle %d: %s", bad, msg[check(bad, false)]);
   }
   h->nv = n;
   h->roff.assign(route_off, route_off + n + 1);
   if (n == 0) h->roff.assign(1, 0);
-  h->rslot.resize(h->roff[n]);
   h->first_link.resize(n);
   parallel_for(n, [&](int64_t lo, int64_t hi, int) {
-    for (int64_t f = lo; f < hi; f++) {
-      const int64_t a = h->roff[f];
-      h->first_link[f] = route_links[a];
-      h->rslot[a] = 0xFF;
-      for (int64_t j = a + 1; j < h->roff[f + 1]; j++)
-        h->rslot[j] = (uint8_t)h->out_pos[route_links[j]];
-    }
+    for (int64_t f = lo; f < hi; f++) h->first_link[f] = route_links[route_off[f]];
   });
   h->dep.assign(depart, depart + n);
   h->entry.assign(entry_cell, entry_cell + n);
@@ -573,25 +588,60 @@ int ts_place_vehicles_at(ts_sim *h, int32_t n, const int32_t *vid, const int32_t
   if (!h) return TS_EINVAL;
   if (!h->have_veh) return fail(h, TS_EINVAL, "load vehicles first");
   if (h->inited) return fail(h, TS_EINVAL, "already initialised");
+  if (n < 0) return fail(h, TS_EINVAL, "negative placement count");
+  // error code of placement i against the loaded routes (0 = ok)
+  auto check = [&](int32_t i) -> int {
+    const int32_t f = vid[i];
+    if (f < 0 || f >= h->nv) return 1;
+    const int32_t c = cursor ? cursor[i] : 0;
+    if (c < 0 || c >= h->roff[f + 1] - h->roff[f]) return 3;
+    const int32_t k = link_at(h, f, c);
+    if (lane[i] < 0 || lane[i] >= h->lanes[k] || cell[i] < 0 || cell[i] >= h->ncell[k]) return 4;
+    if (v[i] < 0 || v[i] > h->vmax[k]) return 5;
+    return 0;
+  };
+  // parallel pass: validate, claim the vehicles (atomic flag), record the
+  // placement at its batch index; any failure undoes the claims and the
+  // serial pass below reports the first failing placement in input order
+  const size_t base = h->pl_vid.size();
+  for (auto *a : {&h->pl_vid, &h->pl_cur, &h->pl_lane, &h->pl_cell, &h->pl_v}) a->resize(base + n);
+  std::vector<uint8_t> won(n, 0);
+  std::vector<uint8_t> failed(64, 0);
+  parallel_for(n, [&](int64_t lo, int64_t hi, int th) {
+    for (int64_t i = lo; i < hi; i++) {
+      if (check((int32_t)i)) {
+        failed[th] = 1;
+        return;
+      }
+      const int32_t f = vid[i];
+      if (__atomic_exchange_n(&h->placed[f], (uint8_t)1, __ATOMIC_RELAXED)) {
+        failed[th] = 1;
+        return;
+      }
+      won[i] = 1;
+      h->pl_vid[base + i] = f;
+      h->pl_cur[base + i] = cursor ? cursor[i] : 0;
+      h->pl_lane[base + i] = lane[i];
+      h->pl_cell[base + i] = cell[i];
+      h->pl_v[base + i] = v[i];
+    }
+  });
+  if (std::find(failed.begin(), failed.end(), 1) == failed.end()) return TS_OK;
+  for (int32_t i = 0; i < n; i++)
+    if (won[i]) h->placed[vid[i]] = 0;
+  for (auto *a : {&h->pl_vid, &h->pl_cur, &h->pl_lane, &h->pl_cell, &h->pl_v}) a->resize(base);
+  static const char *msg[] = {"", "bad vid", "vehicle placed twice", "cursor outside the route",
+                              "cell outside link", "velocity"};
   for (int32_t i = 0; i < n; i++) {
     const int32_t f = vid[i];
-    if (f < 0 || f >= h->nv) return fail(h, TS_EINVAL, "placement %d: bad vid", i);
-    if (h->placed[f]) return fail(h, TS_EINVAL, "placement %d: vehicle placed twice", i);
-    const int32_t c = cursor ? cursor[i] : 0;
-    if (c < 0 || c >= h->roff[f + 1] - h->roff[f])
-      return fail(h, TS_EINVAL, "placement %d: cursor outside the route", i);
-    const int32_t k = link_at(h, f, c);
-    if (lane[i] < 0 || lane[i] >= h->lanes[k] || cell[i] < 0 || cell[i] >= h->ncell[k])
-      return fail(h, TS_EINVAL, "placement %d: cell outside link", i);
-    if (v[i] < 0 || v[i] > h->vmax[k]) return fail(h, TS_EINVAL, "placement %d: velocity", i);
-    h->placed[f] = 1;
-    h->pl_vid.push_back(f);
-    h->pl_cur.push_back(c);
-    h->pl_lane.push_back(lane[i]);
-    h->pl_cell.push_back(cell[i]);
-    h->pl_v.push_back(v[i]);
+    const int e = (f < 0 || f >= h->nv) ? 1 : h->placed[f] ? 2 : check(i);
+    if (e) {
+      for (int32_t j = 0; j < i; j++) h->placed[vid[j]] = 0;
+      return fail(h, TS_EINVAL, "placement %d: %s", i, msg[e]);
+    }
+    h->placed[vid[i]] = 1;
   }
-  return TS_OK;
+  return fail(h, TS_EINTERNAL, "placement: inconsistent parallel check");
 }
 
 int ts_place_vehicles(ts_sim *h, int32_t n, const int32_t *vid, const int32_t *lane,
@@ -1240,33 +1290,115 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
   if (h->dom_of_node.empty()) h->dom_of_node.assign(h->nn, 0);
   build_tiles(h);
 
+  // the routes (out-slot sequences built at load, GBs at the largest
+  // configs) go to the device on a host thread of their own through pinned
+  // double-buffered staging, overlapping the placement and plane build below
+  struct RouteUpload {
+    std::thread th;
+    cudaError_t err = cudaSuccess;
+    ~RouteUpload() {
+      if (th.joinable()) th.join();
+    }
+  } rup;
+  {
+    const size_t nb = h->rslot.size();
+    int rc;
+    if ((rc = dalloc(h, &h->d_rslot, std::max<size_t>(nb, 1)))) return rc;
+    rup.th = std::thread([h, nb, &rup]() {
+      cudaError_t &e = rup.err;
+      if ((e = cudaSetDevice(h->dev)) != cudaSuccess || nb == 0) return;
+      const size_t chunk = (size_t)64 << 20;
+      uint8_t *pin[2] = {nullptr, nullptr};
+      cudaEvent_t done[2] = {nullptr, nullptr};
+      cudaStream_t st = nullptr;
+      const bool pinned = nb > chunk && cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) == cudaSuccess &&
+                          cudaMallocHost(&pin[0], chunk) == cudaSuccess &&
+                          cudaMallocHost(&pin[1], chunk) == cudaSuccess &&
+                          cudaEventCreateWithFlags(&done[0], cudaEventDisableTiming) == cudaSuccess &&
+                          cudaEventCreateWithFlags(&done[1], cudaEventDisableTiming) == cudaSuccess;
+      if (pinned) {  // fill one buffer while the other copies
+        for (size_t o = 0, i = 0; o < nb && e == cudaSuccess; o += chunk, i++) {
+          const size_t m = std::min(chunk, nb - o);
+          uint8_t *b = pin[i & 1];
+          if (i >= 2) cudaEventSynchronize(done[i & 1]);
+          {  // a few copy threads: one host thread alone cannot keep up with the DMA
+            constexpr int kCp = 6;
+            std::thread cp[kCp];
+            for (int q = 0; q < kCp; q++)
+              cp[q] = std::thread([=]() {
+                std::memcpy(b + m * q / kCp, h->rslot.data() + o + m * q / kCp, m * (q + 1) / kCp - m * q / kCp);
+              });
+            for (auto &t : cp) t.join();
+          }
+          if ((e = cudaMemcpyAsync(h->d_rslot + o, b, m, cudaMemcpyHostToDevice, st)) == cudaSuccess)
+            e = cudaEventRecord(done[i & 1], st);
+        }
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+      } else {
+        e = cudaMemcpy(h->d_rslot, h->rslot.data(), nb, cudaMemcpyHostToDevice);
+      }
+      for (int i = 0; i < 2; i++) {
+        if (pin[i]) cudaFreeHost(pin[i]);
+        if (done[i]) cudaEventDestroy(done[i]);
+      }
+      if (st) cudaStreamDestroy(st);
+    });
+  }
+
   h->entry_h = h->entry;
 
   // host staging of the initial placement: codes + compact vid lists (cells
   // of other domains are skipped)
-  std::vector<uint8_t> code(h->total_cells, kEmpty);
-  std::vector<int32_t> cellvid(h->total_cells, -1);
+  HostVec<uint8_t> code = filled<uint8_t>(h->total_cells, kEmpty);
+  HostVec<int32_t> cellvid = filled<int32_t>(h->total_cells, -1);
   std::vector<int32_t> cur0(h->nv, 0);
   h->n_placed = 0;
-  for (size_t i = 0; i < h->pl_vid.size(); i++) {
-    const int f = h->pl_vid[i], c = h->pl_cur[i];
-    const int k = link_at(h, f, c);
-    cur0[f] = c;
-    const int ti = tile_of(h, k, h->pl_cell[i]);
-    if (ti < 0) continue;  // another domain's cell
-    const TileDesc &d = h->tiles[ti];
-    const int64_t pos = d.off + (int64_t)h->pl_lane[i] * row_pitch(d.w) + (h->pl_cell[i] - d.a);
-    if (code[pos] != kEmpty) return fail(h, TS_EINVAL, "placement %zu: cell taken", i);
-    const int64_t ro = h->roff[f];
-    // ring segment rows: every vehicle goes straight on through the virtual
-    // nodes (out-slot 0, all lanes allowed) instead of being on a final link
-    const int slot = h->ring_rows ? 0
-                     : c + 1 < h->roff[f + 1] - ro ? (int)h->rslot[ro + c + 1] : kSlotFinal;
-    code[pos] = (uint8_t)(h->pl_v[i] | (slot << 3));
-    cellvid[pos] = f;
-    h->n_placed++;
+  // placements in parallel: a cell claimed twice is found by the
+  // compare-and-swap on its vehicle slot (the first placement in input
+  // order is reported)
+  std::vector<int64_t> taken(64, INT64_MAX);
+  std::vector<int64_t> placed_cnt(64, 0);
+  parallel_for((int64_t)h->pl_vid.size(), [&](int64_t lo, int64_t hi, int th) {
+    for (int64_t i = lo; i < hi; i++) {
+      const int f = h->pl_vid[i], c = h->pl_cur[i];
+      const int k = link_at(h, f, c);
+      cur0[f] = c;
+      const int ti = tile_of(h, k, h->pl_cell[i]);
+      if (ti < 0) continue;  // another domain's cell
+      const TileDesc &d = h->tiles[ti];
+      const int64_t pos = d.off + (int64_t)h->pl_lane[i] * row_pitch(d.w) + (h->pl_cell[i] - d.a);
+      int32_t expect = -1;
+      if (!__atomic_compare_exchange_n(&cellvid[pos], &expect, (int32_t)f, false, __ATOMIC_RELAXED,
+                                       __ATOMIC_RELAXED)) {
+        taken[th] = std::min(taken[th], i);
+        continue;
+      }
+      const int64_t ro = h->roff[f];
+      // ring segment rows: every vehicle goes straight on through the virtual
+      // nodes (out-slot 0, all lanes allowed) instead of being on a final link
+      const int slot = h->ring_rows ? 0
+                       : c + 1 < h->roff[f + 1] - ro ? (int)h->rslot[ro + c + 1] : kSlotFinal;
+      code[pos] = (uint8_t)(h->pl_v[i] | (slot << 3));
+      placed_cnt[th]++;
+    }
+  });
+  {
+    const int64_t bad = *std::min_element(taken.begin(), taken.end());
+    if (bad != INT64_MAX) {  // the first placement (input order) on a taken cell
+      std::unordered_set<int64_t> seen;
+      for (size_t i = 0; i < h->pl_vid.size(); i++) {
+        const int k = link_at(h, h->pl_vid[i], h->pl_cur[i]);
+        const int ti = tile_of(h, k, h->pl_cell[i]);
+        if (ti < 0) continue;
+        const TileDesc &d = h->tiles[ti];
+        if (!seen.insert(d.off + (int64_t)h->pl_lane[i] * row_pitch(d.w) + (h->pl_cell[i] - d.a)).second)
+          return fail(h, TS_EINVAL, "placement %zu: cell taken", i);
+      }
+      return fail(h, TS_EINVAL, "placement %lld: cell taken", (long long)bad);
+    }
+    for (int64_t c : placed_cnt) h->n_placed += c;
   }
-  std::vector<int32_t> vids(h->total_cells, -1);
+  HostVec<int32_t> vids = filled<int32_t>(h->total_cells, -1);
   parallel_for((int64_t)h->tiles.size(), [&](int64_t lo, int64_t hi, int) {
     for (int64_t ti = lo; ti < hi; ti++) {  // per-row vid lists in cell order
       const TileDesc &d = h->tiles[ti];
@@ -1280,7 +1412,7 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
     }
   });
   trace("placement + row lists");
-  std::vector<int32_t>().swap(cellvid);
+  HostVec<int32_t>().swap(cellvid);
   // general tiles: the byte layout at their own device offsets
   std::vector<uint8_t> gcode(h->gcells, kEmpty);
   std::vector<int32_t> gvid(h->gcells, -1);
@@ -1297,8 +1429,8 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
   if (h->ngroups > 0 && h->nv > (int32_t)kVidMask)
     return fail(h, TS_EINVAL, "too many vehicles for the row kernel");
   if (h->rvid_entries > INT32_MAX) return fail(h, TS_EINVAL, "network too large for one device");
-  std::vector<uint32_t> planes(group_plane_base(h->ngroups), 0u);
-  std::vector<int32_t> rvid(h->rvid_entries, -1);
+  HostVec<uint32_t> planes = filled<uint32_t>(group_plane_base(h->ngroups), 0u);
+  HostVec<int32_t> rvid = filled<int32_t>(h->rvid_entries, -1);
   std::vector<int32_t> row_tile(h->rows.size(), -1);  // row slot -> tile
   for (size_t ti = 0; ti < h->tiles.size(); ti++)
     if (h->tile_row[ti] >= 0)
@@ -1338,8 +1470,8 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
     gcnt[g] = (int32_t)(k - k0);
   }
   });
-  std::vector<uint8_t>().swap(code);
-  std::vector<int32_t>().swap(vids);
+  HostVec<uint8_t>().swap(code);
+  HostVec<int32_t>().swap(vids);
   trace("planes + vid blocks");
   // pending lists per first link in (departure, vid) order (R13)
   std::vector<int32_t> pend_off(h->nl + 1, 0), pend_list;
@@ -1422,35 +1554,10 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
   if (h->ring_rows) h->tt[h->periodic] = 0u;  // straight on through the virtual nodes
   if ((rc = upload(h, &h->d_tt, h->tt))) return rc;
   if ((rc = upload(h, &h->d_out_pos, h->out_pos))) return rc;
-  {  // routes as out-slot sequences (built at load), through pinned staging
-    const size_t nb = h->rslot.size();
-    if ((rc = dalloc(h, &h->d_rslot, std::max<size_t>(nb, 1)))) return rc;
-    const size_t chunk = (size_t)64 << 20;
-    uint8_t *pin[2] = {nullptr, nullptr};
-    cudaEvent_t done[2] = {nullptr, nullptr};
-    bool pinned = nb > chunk && cudaMallocHost(&pin[0], chunk) == cudaSuccess &&
-                  cudaMallocHost(&pin[1], chunk) == cudaSuccess &&
-                  cudaEventCreateWithFlags(&done[0], cudaEventDisableTiming) == cudaSuccess &&
-                  cudaEventCreateWithFlags(&done[1], cudaEventDisableTiming) == cudaSuccess;
-    if (pinned) {  // double-buffered: fill one buffer while the other copies
-      for (size_t o = 0, i = 0; o < nb; o += chunk, i++) {
-        const size_t m = std::min(chunk, nb - o);
-        uint8_t *b = pin[i & 1];
-        if (i >= 2) cudaEventSynchronize(done[i & 1]);
-        parallel_for((int64_t)m, [&](int64_t lo, int64_t hi, int) {
-          memcpy(b + lo, h->rslot.data() + o + lo, hi - lo);
-        });
-        CK(h, cudaMemcpyAsync(h->d_rslot + o, b, m, cudaMemcpyHostToDevice, h->stream));
-        CK(h, cudaEventRecord(done[i & 1], h->stream));
-      }
-      CK(h, cudaStreamSynchronize(h->stream));
-    } else if (nb) {
-      CK(h, cudaMemcpy(h->d_rslot, h->rslot.data(), nb, cudaMemcpyHostToDevice));
-    }
-    for (int i = 0; i < 2; i++) {
-      if (pin[i]) cudaFreeHost(pin[i]);
-      if (done[i]) cudaEventDestroy(done[i]);
-    }
+  {  // routes as out-slot sequences: the upload started above
+    rup.th.join();
+    if (rup.err != cudaSuccess)
+      return fail(h, TS_EINTERNAL, "route upload: %s", cudaGetErrorString(rup.err));
     cudaGetLastError();
     std::vector<NodeOut> nodeout(h->out_list.size());
     for (size_t i = 0; i < h->out_list.size(); i++) {
@@ -1994,12 +2101,12 @@ int32_t ts_time(const ts_sim *h) { return h ? h->t : -1; }
 // State of tiles [t0, t1) in the byte-code layout (codes at off + l*Wp + x,
 // per-row vid lists) starting at element 0 = cell off(t0).  Row mode:
 // decoded from the bit-planes and the vid | slot << 27 list entries.
-static int download_tiles(ts_sim *h, int t0, int t1, std::vector<uint8_t> &code,
-                          std::vector<int32_t> &vids) {
+static int download_tiles(ts_sim *h, int t0, int t1, HostVec<uint8_t> &code,
+                          HostVec<int32_t> &vids) {
   const int64_t c0 = h->tiles[t0].off;
   const int64_t c1 = t1 < (int)h->tiles.size() ? h->tiles[t1].off : h->total_cells;
-  code.assign(c1 - c0, kEmpty);
-  vids.assign(c1 - c0, -1);
+  code = filled<uint8_t>(c1 - c0, kEmpty);
+  vids = filled<int32_t>(c1 - c0, -1);
   // general tiles of the range: one contiguous device range
   int g0 = -1, g1 = -1, s0 = -1, s1 = -1;
   for (int ti = t0; ti < t1; ti++) {
@@ -2080,16 +2187,19 @@ int ts_read_vehicles(ts_sim *h, int8_t *status, int32_t *link, int32_t *lane, in
   if (!h || !h->inited) return fail(h, TS_EINVAL, "not initialised");
   CK(h, cudaSetDevice(h->dev));
   CK(h, cudaStreamSynchronize(h->stream));
-  std::vector<uint8_t> code;
-  std::vector<int32_t> vids, inj(h->nv), arr(h->nv), cur(h->nv);
+  HostVec<uint8_t> code;
+  HostVec<int32_t> vids, inj(h->nv), arr(h->nv), cur(h->nv);
   std::vector<VehPos> vp(h->nv);
   if (int rc = download_tiles(h, 0, (int)h->tiles.size(), code, vids)) return rc;
   CK(h, cudaMemcpy(inj.data(), h->d_inj, inj.size() * 4, cudaMemcpyDeviceToHost));
   CK(h, cudaMemcpy(arr.data(), h->d_arr, arr.size() * 4, cudaMemcpyDeviceToHost));
   CK(h, cudaMemcpy(vp.data(), h->d_vpos, vp.size() * sizeof(VehPos), cudaMemcpyDeviceToHost));
-  for (int f = 0; f < h->nv; f++) cur[f] = (int32_t)(vp[f].p - h->roff[f]);
-  std::vector<int32_t> lk(h->nv, -1), ln(h->nv, -1), ce(h->nv, -1), vv(h->nv, -1);
-  std::vector<uint8_t> seen(h->nv, 0);
+  parallel_for(h->nv, [&](int64_t lo, int64_t hi, int) {
+    for (int64_t f = lo; f < hi; f++) cur[f] = (int32_t)(vp[f].p - h->roff[f]);
+  });
+  HostVec<int32_t> lk = filled<int32_t>(h->nv, -1), ln = filled<int32_t>(h->nv, -1),
+                   ce = filled<int32_t>(h->nv, -1), vv = filled<int32_t>(h->nv, -1);
+  HostVec<uint8_t> seen = filled<uint8_t>(h->nv, 0);
   std::vector<int64_t> bad(64, -1);  // per thread: a corrupt entry (vid << 32 | link)
   parallel_for((int64_t)h->tiles.size(), [&](int64_t lo, int64_t hi, int th) {
     for (int64_t ti = lo; ti < hi; ti++) {
@@ -2116,27 +2226,34 @@ int ts_read_vehicles(ts_sim *h, int8_t *status, int32_t *link, int32_t *lane, in
   for (int64_t b : bad)
     if (b != -1)
       return fail(h, TS_EINTERNAL, "corrupt state: vid %d at link %d", (int)(b >> 32), (int)(int32_t)b);
-  for (int f = 0; f < h->nv; f++) {
-    int8_t s = TS_ACTIVE;
-    if (seen[f]) s = TS_ACTIVE;
-    else if (arr[f] >= 0) s = TS_ARRIVED;
-    else if (inj[f] == INT_MAX) {
-      // pending: reported by the domain owning its entry cell
-      const int k = h->first_link[f];
-      s = (h->entry_h[f] >= h->own_lo[k] && h->entry_h[f] < h->own_hi[k]) ? TS_PENDING : TS_ABSENT;
-    } else {
-      s = TS_ABSENT;  // on a cell of another domain
+  std::vector<int32_t> lost(64, INT32_MAX);
+  parallel_for(h->nv, [&](int64_t lo, int64_t hi, int th) {
+    for (int f = (int)lo; f < (int)hi; f++) {
+      int8_t s = TS_ACTIVE;
+      if (seen[f]) s = TS_ACTIVE;
+      else if (arr[f] >= 0) s = TS_ARRIVED;
+      else if (inj[f] == INT_MAX) {
+        // pending: reported by the domain owning its entry cell
+        const int k = h->first_link[f];
+        s = (h->entry_h[f] >= h->own_lo[k] && h->entry_h[f] < h->own_hi[k]) ? TS_PENDING : TS_ABSENT;
+      } else {
+        s = TS_ABSENT;  // on a cell of another domain
+      }
+      if (s == TS_ABSENT && h->dom_k == 1) {
+        lost[th] = std::min(lost[th], f);
+        return;
+      }
+      if (status) status[f] = s;
+      if (link) link[f] = lk[f];
+      if (lane) lane[f] = ln[f];
+      if (cell) cell[f] = ce[f];
+      if (v) v[f] = vv[f];
+      if (cursor) cursor[f] = (s == TS_ACTIVE || s == TS_ARRIVED) ? cur[f] : -1;
+      if (t_arrive) t_arrive[f] = s == TS_ARRIVED ? arr[f] : -1;
     }
-    if (s == TS_ABSENT && h->dom_k == 1)
-      return fail(h, TS_EINTERNAL, "corrupt state: vehicle %d lost", f);
-    if (status) status[f] = s;
-    if (link) link[f] = lk[f];
-    if (lane) lane[f] = ln[f];
-    if (cell) cell[f] = ce[f];
-    if (v) v[f] = vv[f];
-    if (cursor) cursor[f] = (s == TS_ACTIVE || s == TS_ARRIVED) ? cur[f] : -1;
-    if (t_arrive) t_arrive[f] = s == TS_ARRIVED ? arr[f] : -1;
-  }
+  });
+  if (const int32_t f = *std::min_element(lost.begin(), lost.end()); f != INT32_MAX)
+    return fail(h, TS_EINTERNAL, "corrupt state: vehicle %d lost", f);
   return TS_OK;
 }
 
@@ -2149,8 +2266,8 @@ int ts_read_cells(ts_sim *h, int32_t link, int32_t *vid_out) {
   for (int i = h->link_tile0[link]; i < h->link_tile0[link + 1]; i++) {
     const TileDesc &d = h->tiles[i];
     const int Wp = row_pitch(d.w);
-    std::vector<uint8_t> code;
-    std::vector<int32_t> vids;
+    HostVec<uint8_t> code;
+    HostVec<int32_t> vids;
     if (int rc = download_tiles(h, i, i + 1, code, vids)) return rc;
     for (int l = 0; l < L; l++) {
       int r = l * Wp;
@@ -2173,8 +2290,8 @@ int ts_read_raw(ts_sim *h, int32_t link, uint8_t *code_out, int32_t *vid_out, in
   const TileDesc &d = h->tiles[ti];
   const int Wp = row_pitch(d.w);
   *pitch = Wp;
-  std::vector<uint8_t> code;
-  std::vector<int32_t> vids;
+  HostVec<uint8_t> code;
+  HostVec<int32_t> vids;
   if (int rc = download_tiles(h, ti, ti + 1, code, vids)) return rc;
   memcpy(code_out, code.data(), (size_t)d.L * Wp);
   memcpy(vid_out, vids.data(), (size_t)d.L * Wp * 4);
