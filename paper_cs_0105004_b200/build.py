@@ -32,7 +32,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if verbose:
         print(r.stderr)
     with open(os.path.join(HERE, "ptxas_info.txt"), "w") as f:
-        f.write(r.stderr)
+        # register / spill / shared-memory report per kernel (compile times
+        # dropped so the file changes only with the code)
+        f.write("".join(ln for ln in r.stderr.splitlines(True) if "Compile time" not in ln))
     return SO
 
 
