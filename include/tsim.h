@@ -79,7 +79,11 @@ int ts_load_network(ts_sim *h, int32_t n_nodes, const int64_t *node_x_mm,
 
 /* Vehicles vid = 0..n-1 (plans): route CSR route_off[n+1]
  * into route_links (consecutive links must share a node), departure second
- * and entry cell on route[0] (R13). */
+ * and entry cell on route[0] (R13).  Host arrays, read
+ * during the call only.  Validated in parallel on the host cores; a bad
+ * record returns TS_EINVAL naming the first failing vehicle in input order
+ * ("vehicle i: empty route | bad link | route links not consecutive |
+ * entry cell outside link") and loads nothing. */
 int ts_load_vehicles(ts_sim *h, int32_t n, const int64_t *route_off,
                      const int32_t *route_links, const int32_t *depart,
                      const int32_t *entry_cell);
@@ -93,7 +97,11 @@ int ts_place_vehicles(ts_sim *h, int32_t n, const int32_t *vid,
 /* Placement on any link of the route (checkpoint restore, repartitioning):
  * vehicle vid[i] stands on link route[cursor[i]] (cursor NULL = 0) at
  * (lane, cell) with velocity v.  Vehicles neither placed nor marked arrived
- * are pending. */
+ * are pending.  A batch is all or nothing: a bad record (bad vid, vehicle
+ * placed twice, cursor outside the route, cell outside link, velocity)
+ * returns TS_EINVAL naming the first failing index of the batch and places
+ * none of it.  Two placements on one cell are found by ts_init ("placement
+ * i: cell taken", i the later one in placement order). */
 int ts_place_vehicles_at(ts_sim *h, int32_t n, const int32_t *vid, const int32_t *cursor,
                          const int32_t *lane, const int32_t *cell, const int32_t *v);
 /* Vehicles that already arrived (restore): vid[i] left at t_arrive[i]. */
