@@ -536,16 +536,33 @@ int ts_load_vehicles(ts_sim *h, int32_t n, const int64_t *route_off, const int32
   // routes to out-slot sequences (one pass over the route links): error code
   // of vehicle i (0 = ok); the first failing vehicle is reported.  Empty or
   // decreasing route offsets are found first (they size the slot array).
-  auto check = [&](int32_t i, bool conv) -> int {
+  // per link (from, to, out-slot at its from node) in one 16-byte record:
+  // one gather per route entry; raw pointers in locals (the byte stores
+  // into the slot array would otherwise force reloads through h)
+  struct LinkRec {
+    int32_t from, to, slot, pad;
+  };
+  std::vector<LinkRec> lrec(h->nl);
+  for (int k = 0; k < h->nl; k++) lrec[k] = LinkRec{h->from[k], h->to[k], h->out_pos[k], 0};
+  const LinkRec *lr = lrec.data();
+  const uint32_t nl = (uint32_t)h->nl;
+  const int32_t *ncell = h->ncell.data();
+  auto check = [&, lr, nl, ncell](int32_t i, uint8_t *slot) -> int {
     const int64_t a = route_off[i], b = route_off[i + 1];
     if (b <= a) return 1;
-    for (int64_t j = a; j < b; j++) {
+    const int32_t k0 = route_links[a];
+    if ((uint32_t)k0 >= nl) return 2;
+    if (slot) slot[a] = 0xFF;
+    int32_t at = lr[k0].to;
+    for (int64_t j = a + 1; j < b; j++) {
       const int32_t k = route_links[j];
-      if (k < 0 || k >= h->nl) return 2;
-      if (j > a && h->to[route_links[j - 1]] != h->from[k]) return 3;
-      if (conv) h->rslot[j] = j > a ? (uint8_t)h->out_pos[k] : (uint8_t)0xFF;
+      if ((uint32_t)k >= nl) return 2;
+      const LinkRec r = lr[k];
+      if (r.from != at) return 3;
+      if (slot) slot[j] = (uint8_t)r.slot;
+      at = r.to;
     }
-    if (entry_cell[i] < 0 || entry_cell[i] >= h->ncell[route_links[a]]) return 4;
+    if (entry_cell[i] < 0 || entry_cell[i] >= ncell[k0]) return 4;
     return 0;
   };
   auto first_failing = [&](auto pred) {
@@ -564,10 +581,11 @@ int ts_load_vehicles(ts_sim *h, int32_t n, const int64_t *route_off, const int32
   const int32_t bad_off = first_failing([&](int32_t i) { return route_off[i + 1] <= route_off[i]; });
   if (bad_off != INT32_MAX) return fail(h, TS_EINVAL, "vehicle %d: %s", bad_off, msg[1]);
   h->rslot.resize(n > 0 ? route_off[n] : 0);
-  const int32_t bad = first_failing([&](int32_t i) { return check(i, true) != 0; });
+  uint8_t *const slot = h->rslot.data();
+  const int32_t bad = first_failing([&](int32_t i) { return check(i, slot) != 0; });
   if (bad != INT32_MAX) {
     decltype(h->rslot)().swap(h->rslot);
-    return fail(h, TS_EINVAL, "vehicle %d: %s", bad, msg[check(bad, false)]);
+    return fail(h, TS_EINVAL, "vehicle %d: %s", bad, msg[check(bad, nullptr)]);
   }
   h->nv = n;
   h->roff.assign(route_off, route_off + n + 1);
