@@ -3,7 +3,7 @@ import os
 import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SRCS = ["csrc/tsim_kernels.cu", "csrc/tsim_rows.cu", "csrc/tsim_api.cu", "csrc/tsim_partition.cpp",
+SRCS = ["csrc/tsim_kernels.cu", "csrc/tsim_rows.cu", "csrc/tsim_api.cu", "csrc/tsim_readers.cu", "csrc/tsim_partition.cpp",
         "csrc/tsim_text.cpp"]
 SO = os.path.join(HERE, "libtsim.so")
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
@@ -16,6 +16,7 @@ def stale() -> bool:
     t = os.path.getmtime(SO)
     deps = [os.path.join(HERE, s) for s in SRCS] + [
         os.path.join(HERE, "csrc", "tsim_internal.h"),
+        os.path.join(HERE, "csrc", "tsim_host.h"),
         os.path.join(HERE, "csrc", "tsim_device.cuh"),
         os.path.join(os.path.dirname(HERE), "include", "tsim.h")]
     return any(os.path.getmtime(d) > t for d in deps)

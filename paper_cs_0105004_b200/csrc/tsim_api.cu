@@ -1,214 +1,12 @@
 // tsim_api.cu -- host side of libtsim: input validation, network tables,
-// tiling and device layout, kernel orchestration, state read-back.
-// C-ABI declared in include/tsim.h.
-#include <cuda_runtime.h>
-#include <dlfcn.h>
-#include <nccl.h>
+// tiling and device layout, initial state, kernel orchestration, the
+// exchange transport (state read-back: tsim_readers.cu; handle state and
+// shared helpers: tsim_host.h).  C-ABI declared in include/tsim.h.
+#include "tsim_host.h"
 
-#include <algorithm>
-#include <climits>
-#include <cmath>
-#include <cstdarg>
-#include <cstdio>
-#include <cstdlib>
-#include <cstring>
-#include <numeric>
-#include <string>
-#include <thread>
-#include <chrono>
-#include <utility>
-#include <memory>
-#include <unordered_set>
-#include <vector>
+std::string g_create_err;
 
-#include "../../include/tsim.h"
-#include "tsim_internal.h"
-
-namespace tsim {
-cudaError_t set_smem_attrs(int bytes);
-cudaError_t set_rows_smem(int bytes);
-int occupancy_blocks(int threads, int smem);
-int occupancy_rows(int threads, int smem);
-}  // namespace tsim
-
-using namespace tsim;
-
-static std::string g_create_err;
-
-struct DevBuf {
-  void *p = nullptr;
-  size_t bytes = 0;
-};
-
-// vector allocator that leaves elements uninitialised (the multi-GB route
-// arrays are filled in parallel right after allocation)
-template <typename T>
-struct UninitAlloc : std::allocator<T> {
-  template <typename U>
-  struct rebind {
-    using other = UninitAlloc<U>;
-  };
-  UninitAlloc() = default;
-  template <typename U>
-  UninitAlloc(const UninitAlloc<U> &) {}
-  template <typename U>
-  void construct(U *p) noexcept {
-    ::new (static_cast<void *>(p)) U;
-  }
-  template <typename U, typename... A>
-  void construct(U *p, A &&...a) {
-    ::new (static_cast<void *>(p)) U(std::forward<A>(a)...);
-  }
-};
-
-struct ts_sim {
-  ts_config cfg{};
-  std::string err;
-  int dev = 0;
-  cudaStream_t stream = nullptr;
-  // second stream: the general-tile move kernel runs beside the row kernel
-  // (disjoint tiles, both after the node kernel); fork / join by events
-  cudaStream_t side = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  size_t dev_bytes = 0;
-  std::vector<void *> allocs;
-  // network (host)
-  bool have_net = false, have_veh = false, inited = false;
-  int32_t nn = 0, nl = 0, periodic = -1;
-  std::vector<int64_t> nx, ny, len;
-  std::vector<int32_t> from, to, lanes, vmax, cls, ncell, lgid;
-  std::vector<int32_t> in_off, in_list, out_off, out_list, out_pos;
-  std::vector<uint32_t> tt;
-  int64_t nlanes = 0, lane_cells = 0;
-  // vehicles (host)
-  int32_t nv = 0;
-  std::vector<int64_t> roff;
-  // plans as out-slot sequences (R7): rslot[roff[f] + j] = slot of route link
-  // j at its from-node (0xFF for j = 0); the link ids are not kept (a link
-  // at cursor c is the walk from first_link along the slots, link_at)
-  std::vector<uint8_t, UninitAlloc<uint8_t>> rslot;
-  std::vector<int32_t> dep, entry;
-  std::vector<int32_t> pl_vid, pl_lane, pl_cell, pl_v, pl_cur;
-  std::vector<uint8_t> placed;
-  std::vector<int32_t> arr0;     // arrival time of vehicles restored as arrived (-1 otherwise)
-  std::vector<int32_t> text_link_id;  // link ids of a network file (ts_load_network_text)
-  std::vector<int32_t> first_link, entry_h;  // route[0] and entry cell (kept after init)
-  // domain decomposition (§4; ts_set_domain): owned cells per link
-  int32_t dom_k = 1, dom_me = 0;
-  std::vector<int32_t> dom_of_node;
-  std::vector<int32_t> own_lo, own_hi;
-  std::vector<int32_t> mirror;  // per link: first mirror strip slot of the remote half, or -1
-  struct Nbr {
-    int32_t dom;
-    std::vector<int32_t> send_slot, recv_slot;  // strip slots, (link, lane) order
-    int64_t off;                                // first Strip of this neighbour in d_send/d_recv
-  };
-  std::vector<Nbr> nbrs;
-  int64_t n_xs = 0;  // strips per exchange (sum over neighbours)
-  Strip *d_send = nullptr, *d_recv = nullptr;
-  int32_t *d_send_slot = nullptr, *d_recv_slot = nullptr;
-  ncclComm_t comm = nullptr;  // native exchange transport (ts_nccl_init)
-  std::vector<int32_t> my_nodes;
-  int32_t *d_node_ids = nullptr;
-  std::vector<uint32_t> node_sig;  // per node: phase-0 signal word (R23), 0 = none
-  uint32_t *d_node_sig = nullptr, *d_lane_sig = nullptr;
-  bool rows_s1 = false, gen_s1 = false;  // row / general state holds S1(t) (lane change applied)
-  int64_t n_pending0 = 0;
-  int32_t folded_t = 0;  // stats folded into the host counters up to this time
-  // layout
-  std::vector<TileDesc> tiles;
-  std::vector<int32_t> link_tile0, link_ntiles;
-  int64_t total_cells = 0;
-  int32_t nstrips = 0;
-  std::vector<int32_t> halo_up, halo_dn;
-  WarpLayout lay{};
-  int threads = 256, blocks = 1, smem = 0;
-  bool gfused = false, rfused = false, node_warp = false;
-  // the periodic link as a chain of row-tile segments joined by pass-through
-  // virtual nodes (row kernel instead of the warp-per-tile kernels)
-  bool ring_rows = false;
-  std::vector<NodeOut> ring_nodeout;
-  int32_t *d_ring_next = nullptr, *d_ring_prev = nullptr, *d_row_a = nullptr;
-  // general tiles (halo / long / periodic links): byte codes at device
-  // offsets of their own; uploaded as d_tiles
-  std::vector<TileDesc> gtiles;
-  std::vector<int32_t> tile_g;  // tile -> index in gtiles, or -1
-  int64_t gcells = 0;
-  // row tiles (whole links of <= kRowMaxCells cells): k_rows
-  std::vector<int32_t> tile_row;  // tile -> global row slot of its lane 0, or -1
-  std::vector<RowDesc> rows;      // ngroups * 32 slots
-  int32_t ngroups = 0;
-  int64_t rvid_entries = 0;
-  uint32_t *d_planes[2] = {nullptr, nullptr};
-  int32_t *d_rvid[2] = {nullptr, nullptr};
-  int32_t *d_gcnt[2] = {nullptr, nullptr};  // vehicles per group
-  unsigned long long *d_gctr = nullptr;      // k_rows work counter
-  unsigned long long gctr_base = 0;
-  int32_t *d_inj_scratch = nullptr;
-  RowDesc *d_rows = nullptr;
-  int rows_threads = 128, rows_blocks = 1, rows_cap = 0, rows_smem = 0;
-  // programmatic dependent launch of the node and move kernels (TSIM_NO_PDL
-  // turns it off for comparisons)
-  bool pdl = true;
-  std::vector<int32_t> gvoff;                // first vid-block entry of each group
-  int32_t *d_gvoff = nullptr;
-  NodeLane *d_nlanes = nullptr;
-  int32_t nchunks = 0;
-  std::vector<int32_t> nli;   // node-lane index of every global lane id
-  int64_t n_nli = 0;          // size of the node-lane indexed arrays
-  int32_t *d_nli = nullptr;
-  std::vector<int32_t> nlo;   // node-out-lane index of every global lane id
-  int64_t n_nlo = 0;          // size of the node-out-lane indexed arrays
-  int32_t *d_nlo = nullptr;
-  uint64_t p32 = 0;
-  // device
-  TileDesc *d_tiles = nullptr;
-  uint8_t *d_code[2] = {nullptr, nullptr};
-  int32_t *d_vid[2] = {nullptr, nullptr};
-  Strip *d_strip[2] = {nullptr, nullptr};
-  int32_t *d_halo_up = nullptr, *d_halo_dn = nullptr;
-  uint8_t *d_vmax = nullptr;
-  uint32_t *d_tt = nullptr;
-  int32_t *d_out_pos = nullptr;
-  int64_t *d_roff = nullptr;
-  uint8_t *d_rslot = nullptr;
-  NodeOut *d_nodeout = nullptr;
-  VehPos *d_vpos = nullptr;
-  int32_t *d_dep = nullptr, *d_entry = nullptr;
-  int32_t *d_inj = nullptr, *d_arr = nullptr;
-  int32_t *d_pend_off = nullptr, *d_pend_list = nullptr, *d_pend_head = nullptr;
-  uint64_t *d_tail = nullptr, *d_entr = nullptr;
-  uint8_t *d_head = nullptr, *d_ext = nullptr;
-  unsigned long long *d_stats = nullptr, *d_work = nullptr, *d_hash = nullptr;
-  int32_t *d_in_off = nullptr, *d_in_list = nullptr, *d_out_off = nullptr, *d_out_list = nullptr;
-  int32_t *d_ncell = nullptr, *d_lanes = nullptr, *d_lgid = nullptr, *d_cls = nullptr;
-  int gcur = 0, rcur = 0;  // current buffer of the general / row state
-  int32_t t = 0;
-  int64_t veh_updates = 0, arrived = 0, injected = 0, n_placed = 0, n_arrived0 = 0;
-  // timing
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  // CUDA-graph replay of kGraphSteps steps (TS_FLAG_GRAPH): the kernels read
-  // the step time from the device clock d_clock; while capturing, step and
-  // node parameters carry t - graph_t0 and tdev = d_clock
-  int32_t *d_clock = nullptr;
-  // one graph per parity of the double buffers (rcur, gcur) at its start
-  cudaGraphExec_t graph_exec[4] = {nullptr, nullptr, nullptr, nullptr};
-  unsigned long long graph_gctr_end[4] = {0, 0, 0, 0};
-  bool graph_off = false, capturing = false;
-  int32_t graph_t0 = 0;
-  std::vector<cudaEvent_t> mv_ev;
-  double last_total_ms = 0, last_move_ms = 0, last_xchg_ms = 0;
-  int64_t last_xchg_n = 0;  // exchanges timed in the last native ts_step call
-  // device time of all step work since the last ts_busy_time (the measured
-  // per-domain step time of the rebalancing feedback)
-  double busy_ms = 0;
-  std::vector<cudaEvent_t> ph_ev;  // event pairs around ts_step_phase calls
-  size_t ph_used = 0;
-  int64_t last_move_launches = 0;
-  bool timing = true;
-};
-
-static int fail(ts_sim *h, int code, const char *fmt, ...) {
+int fail(ts_sim *h, int code, const char *fmt, ...) {
   char buf[1024];
   va_list ap;
   va_start(ap, fmt);
@@ -217,72 +15,6 @@ static int fail(ts_sim *h, int code, const char *fmt, ...) {
   if (h) h->err = buf;
   else g_create_err = buf;
   return code;
-}
-
-#define CK(h, call)                                                                     \
-  do {                                                                                  \
-    cudaError_t e_ = (call);                                                            \
-    if (e_ != cudaSuccess)                                                              \
-      return fail((h), TS_EINTERNAL, "%s failed: %s (%s:%d)", #call,                    \
-                  cudaGetErrorString(e_), __FILE__, __LINE__);                          \
-  } while (0)
-
-template <class T>
-static int dalloc(ts_sim *h, T **p, size_t n, int fill = -1) {
-  size_t bytes = std::max<size_t>(n, 1) * sizeof(T);
-  cudaError_t e = cudaMalloc((void **)p, bytes);
-  if (e != cudaSuccess)
-    return fail(h, TS_EINTERNAL, "cudaMalloc(%zu) failed: %s", bytes, cudaGetErrorString(e));
-  h->allocs.push_back(*p);
-  h->dev_bytes += bytes;
-  if (fill >= 0) {
-    e = cudaMemsetAsync(*p, fill, bytes, h->stream);
-    if (e != cudaSuccess) return fail(h, TS_EINTERNAL, "memset: %s", cudaGetErrorString(e));
-  }
-  return TS_OK;
-}
-
-template <class T>
-static int upload(ts_sim *h, T **p, const std::vector<T> &v) {
-  int rc = dalloc(h, p, v.size());
-  if (rc) return rc;
-  if (!v.empty())
-    CK(h, cudaMemcpyAsync(*p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, h->stream));
-  return TS_OK;
-}
-
-// parallel loop over [0, n) in contiguous chunks on the host cores (load
-// and init handle billions of route entries at the largest configs)
-template <typename F>
-static void parallel_for(int64_t n, F f) {
-  const int nt = (int)std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
-  if (n < (int64_t)1 << 16 || nt == 1) {
-    f((int64_t)0, n, 0);
-    return;
-  }
-  std::vector<std::thread> th;
-  for (int i = 0; i < nt; i++)
-    th.emplace_back([=, &f]() { f(n * i / nt, n * (i + 1) / nt, i); });
-  for (auto &t : th) t.join();
-}
-
-// a host staging array of n copies of v, first-touched by the host cores
-// in parallel (value-initialising GB-sized vectors serially dominates init)
-template <typename T>
-using HostVec = std::vector<T, UninitAlloc<T>>;
-template <typename T>
-static HostVec<T> filled(size_t n, T v) {
-  HostVec<T> a(n);
-  parallel_for((int64_t)n, [&](int64_t lo, int64_t hi, int) { std::fill(a.data() + lo, a.data() + hi, v); });
-  return a;
-}
-
-// the link at cursor c of vehicle f: the walk along its out-slots
-static int link_at(const ts_sim *h, int f, int c) {
-  const int64_t a = h->roff[f];
-  int k = h->first_link[f];
-  for (int j = 1; j <= c; j++) k = h->out_list[h->out_off[h->to[k]] + h->rslot[a + j]];
-  return k;
 }
 
 // ---------------------------------------------------------------- NCCL
@@ -1145,7 +877,7 @@ static int tile_of(const ts_sim *h, int k, int x) {
 }
 
 
-static StepParams step_params(ts_sim *h, int t, int mode) {
+StepParams step_params(ts_sim *h, int t, int mode) {
   StepParams P{};
   if (h->capturing) {
     P.tdev = h->d_clock;
@@ -1227,7 +959,7 @@ static NodeParams node_params(ts_sim *h, int t) {
   return N;
 }
 
-static RowsParams rows_params(ts_sim *h) {
+RowsParams rows_params(ts_sim *h) {
   RowsParams r{};
   r.rows = h->d_rows;
   r.ring_next = h->ring_rows ? h->d_ring_next : nullptr;
@@ -1913,7 +1645,7 @@ static int enqueue_steps(ts_sim *h, int32_t n) {
 
 // fold the per-step counters of steps whose result time is in
 // (folded_t, t] into the host totals
-static int fold_stats(ts_sim *h) {
+int fold_stats(ts_sim *h) {
   const int n = h->t - h->folded_t;
   if (n <= 0) return TS_OK;
   if (n < kHist) {
@@ -2115,369 +1847,4 @@ int ts_exchange_local(ts_sim **hs, int32_t k) {
 
 int32_t ts_time(const ts_sim *h) { return h ? h->t : -1; }
 
-// ------------------------------------------------------------------ readers
-// State of tiles [t0, t1) in the byte-code layout (codes at off + l*Wp + x,
-// per-row vid lists) starting at element 0 = cell off(t0).  Row mode:
-// decoded from the bit-planes and the vid | slot << 27 list entries.
-static int download_tiles(ts_sim *h, int t0, int t1, HostVec<uint8_t> &code,
-                          HostVec<int32_t> &vids) {
-  const int64_t c0 = h->tiles[t0].off;
-  const int64_t c1 = t1 < (int)h->tiles.size() ? h->tiles[t1].off : h->total_cells;
-  code = filled<uint8_t>(c1 - c0, kEmpty);
-  vids = filled<int32_t>(c1 - c0, -1);
-  // general tiles of the range: one contiguous device range
-  int g0 = -1, g1 = -1, s0 = -1, s1 = -1;
-  for (int ti = t0; ti < t1; ti++) {
-    if (h->tile_g[ti] >= 0) {
-      if (g0 < 0) g0 = h->tile_g[ti];
-      g1 = h->tile_g[ti] + 1;
-    }
-    if (h->tile_row[ti] >= 0) {
-      if (s0 < 0) s0 = h->tile_row[ti];
-      s1 = h->tile_row[ti] + h->tiles[ti].L;
-    }
-  }
-  if (g0 >= 0) {
-    const TileDesc &la = h->gtiles[g1 - 1];
-    const int64_t a = h->gtiles[g0].off, b = la.off + tile_cells_padded(la.w, la.L);
-    std::vector<uint8_t> gc(b - a);
-    std::vector<int32_t> gv(b - a);
-    CK(h, cudaMemcpy(gc.data(), h->d_code[h->gcur] + a, b - a, cudaMemcpyDeviceToHost));
-    CK(h, cudaMemcpy(gv.data(), h->d_vid[h->gcur] + a, (b - a) * 4, cudaMemcpyDeviceToHost));
-    for (int ti = t0; ti < t1; ti++) {
-      if (h->tile_g[ti] < 0) continue;
-      const TileDesc &d = h->tiles[ti];
-      const int64_t n = (int64_t)d.L * row_pitch(d.w), src = h->gtiles[h->tile_g[ti]].off - a;
-      std::copy(gc.begin() + src, gc.begin() + src + n, code.begin() + (d.off - c0));
-      std::copy(gv.begin() + src, gv.begin() + src + n, vids.begin() + (d.off - c0));
-    }
-  }
-  if (s0 >= 0) {
-    // row tiles: planes and vid blocks of the covering groups; a row's list
-    // starts at the prefix of the vehicle counts of the rows before it
-    const int gr0 = s0 >> 5, gr1 = ((s1 - 1) >> 5) + 1;
-    const int64_t va = h->gvoff[gr0];
-    const int64_t vb = gr1 < h->ngroups ? h->gvoff[gr1] : h->rvid_entries;
-    std::vector<uint32_t> pl(group_plane_base(gr1) - group_plane_base(gr0));
-    std::vector<int32_t> rv(vb - va);
-    CK(h, cudaMemcpy(pl.data(), h->d_planes[h->rcur] + group_plane_base(gr0), pl.size() * 4,
-                     cudaMemcpyDeviceToHost));
-    CK(h, cudaMemcpy(rv.data(), h->d_rvid[h->rcur] + va, rv.size() * 4, cudaMemcpyDeviceToHost));
-    std::vector<int64_t> roff((size_t)(gr1 - gr0) * 32);
-    for (int g = gr0; g < gr1; g++) {
-      int64_t k = h->gvoff[g] - va;
-      for (int sl = 0; sl < 32; sl++) {
-        roff[(size_t)(g - gr0) * 32 + sl] = k;
-        const uint32_t *P = pl.data() + (group_plane_base(g) - group_plane_base(gr0)) + sl;
-        for (int wd = 0; wd < kRowWords; wd++) k += __builtin_popcount(P[wd * 32]);
-      }
-    }
-    parallel_for(t1 - t0, [&](int64_t lo, int64_t hi, int) {
-    for (int ti = t0 + (int)lo; ti < t0 + (int)hi; ti++) {
-      if (h->tile_row[ti] < 0) continue;
-      const TileDesc &d = h->tiles[ti];
-      const int Wp = row_pitch(d.w);
-      for (int l = 0; l < d.L; l++) {
-        const int s = h->tile_row[ti] + l;
-        const uint32_t *P = pl.data() + (group_plane_base(s >> 5) - group_plane_base(gr0)) + (s & 31);
-        const int32_t *lst = rv.data() + roff[(size_t)(s - gr0 * 32)];
-        const int64_t rb = d.off - c0 + (int64_t)l * Wp;
-        int64_t r = rb, k = 0;
-        for (int x = 0; x < d.w; x++) {
-          const int wd = x >> 5, bt = x & 31;
-          if (!((P[wd * 32] >> bt) & 1u)) continue;
-          const int v = (int)((P[(kRowWords + wd) * 32] >> bt) & 1u) |
-                        (int)(((P[(2 * kRowWords + wd) * 32] >> bt) & 1u) << 1) |
-                        (int)(((P[(3 * kRowWords + wd) * 32] >> bt) & 1u) << 2);
-          const uint32_t e = (uint32_t)lst[k++];
-          code[rb + x] = (uint8_t)(v | ((e >> kSlotShift) << 3));
-          vids[r++] = (int32_t)(e & kVidMask);
-        }
-      }
-    }
-    });
-  }
-  return TS_OK;
-}
-
-int ts_read_vehicles(ts_sim *h, int8_t *status, int32_t *link, int32_t *lane, int32_t *cell,
-                     int32_t *v, int32_t *cursor, int32_t *t_arrive) {
-  if (!h || !h->inited) return fail(h, TS_EINVAL, "not initialised");
-  CK(h, cudaSetDevice(h->dev));
-  CK(h, cudaStreamSynchronize(h->stream));
-  HostVec<uint8_t> code;
-  HostVec<int32_t> vids, inj(h->nv), arr(h->nv), cur(h->nv);
-  std::vector<VehPos> vp(h->nv);
-  if (int rc = download_tiles(h, 0, (int)h->tiles.size(), code, vids)) return rc;
-  CK(h, cudaMemcpy(inj.data(), h->d_inj, inj.size() * 4, cudaMemcpyDeviceToHost));
-  CK(h, cudaMemcpy(arr.data(), h->d_arr, arr.size() * 4, cudaMemcpyDeviceToHost));
-  CK(h, cudaMemcpy(vp.data(), h->d_vpos, vp.size() * sizeof(VehPos), cudaMemcpyDeviceToHost));
-  parallel_for(h->nv, [&](int64_t lo, int64_t hi, int) {
-    for (int64_t f = lo; f < hi; f++) cur[f] = (int32_t)(vp[f].p - h->roff[f]);
-  });
-  HostVec<int32_t> lk = filled<int32_t>(h->nv, -1), ln = filled<int32_t>(h->nv, -1),
-                   ce = filled<int32_t>(h->nv, -1), vv = filled<int32_t>(h->nv, -1);
-  HostVec<uint8_t> seen = filled<uint8_t>(h->nv, 0);
-  std::vector<int64_t> bad(64, -1);  // per thread: a corrupt entry (vid << 32 | link)
-  parallel_for((int64_t)h->tiles.size(), [&](int64_t lo, int64_t hi, int th) {
-    for (int64_t ti = lo; ti < hi; ti++) {
-      const TileDesc &d = h->tiles[ti];
-      for (int l = 0; l < d.L; l++) {
-        const int64_t rb = d.off + (int64_t)l * row_pitch(d.w);
-        int64_t r = rb;
-        for (int x = 0; x < d.w; x++) {
-          uint8_t c = code[rb + x];
-          if (c & 0x80) continue;
-          int f = vids[r++];
-          if (f < 0 || f >= h->nv || __atomic_exchange_n(&seen[f], (uint8_t)1, __ATOMIC_RELAXED)) {
-            bad[th] = ((int64_t)f << 32) | (uint32_t)d.link;
-            return;
-          }
-          lk[f] = d.link;
-          ln[f] = l;
-          ce[f] = d.a + x;
-          vv[f] = c & 7;
-        }
-      }
-    }
-  });
-  for (int64_t b : bad)
-    if (b != -1)
-      return fail(h, TS_EINTERNAL, "corrupt state: vid %d at link %d", (int)(b >> 32), (int)(int32_t)b);
-  std::vector<int32_t> lost(64, INT32_MAX);
-  parallel_for(h->nv, [&](int64_t lo, int64_t hi, int th) {
-    for (int f = (int)lo; f < (int)hi; f++) {
-      int8_t s = TS_ACTIVE;
-      if (seen[f]) s = TS_ACTIVE;
-      else if (arr[f] >= 0) s = TS_ARRIVED;
-      else if (inj[f] == INT_MAX) {
-        // pending: reported by the domain owning its entry cell
-        const int k = h->first_link[f];
-        s = (h->entry_h[f] >= h->own_lo[k] && h->entry_h[f] < h->own_hi[k]) ? TS_PENDING : TS_ABSENT;
-      } else {
-        s = TS_ABSENT;  // on a cell of another domain
-      }
-      if (s == TS_ABSENT && h->dom_k == 1) {
-        lost[th] = std::min(lost[th], f);
-        return;
-      }
-      if (status) status[f] = s;
-      if (link) link[f] = lk[f];
-      if (lane) lane[f] = ln[f];
-      if (cell) cell[f] = ce[f];
-      if (v) v[f] = vv[f];
-      if (cursor) cursor[f] = (s == TS_ACTIVE || s == TS_ARRIVED) ? cur[f] : -1;
-      if (t_arrive) t_arrive[f] = s == TS_ARRIVED ? arr[f] : -1;
-    }
-  });
-  if (const int32_t f = *std::min_element(lost.begin(), lost.end()); f != INT32_MAX)
-    return fail(h, TS_EINTERNAL, "corrupt state: vehicle %d lost", f);
-  return TS_OK;
-}
-
-int ts_read_cells(ts_sim *h, int32_t link, int32_t *vid_out) {
-  if (!h || !h->inited) return fail(h, TS_EINVAL, "not initialised");
-  if (link < 0 || link >= h->nl) return fail(h, TS_EINVAL, "bad link");
-  CK(h, cudaSetDevice(h->dev));
-  CK(h, cudaStreamSynchronize(h->stream));
-  const int n = h->ncell[link], L = h->lanes[link];
-  for (int i = h->link_tile0[link]; i < h->link_tile0[link + 1]; i++) {
-    const TileDesc &d = h->tiles[i];
-    const int Wp = row_pitch(d.w);
-    HostVec<uint8_t> code;
-    HostVec<int32_t> vids;
-    if (int rc = download_tiles(h, i, i + 1, code, vids)) return rc;
-    for (int l = 0; l < L; l++) {
-      int r = l * Wp;
-      for (int x = 0; x < d.w; x++) {
-        uint8_t c = code[(size_t)l * Wp + x];
-        vid_out[(size_t)l * n + d.a + x] = (c & 0x80) ? -1 : vids[r++];
-      }
-    }
-  }
-  return TS_OK;
-}
-
-int ts_read_raw(ts_sim *h, int32_t link, uint8_t *code_out, int32_t *vid_out, int32_t *pitch) {
-  if (!h || !h->inited) return fail(h, TS_EINVAL, "not initialised");
-  if (link < 0 || link >= h->nl) return fail(h, TS_EINVAL, "bad link");
-  if (h->link_ntiles[link] != 1) return fail(h, TS_EINVAL, "link spans several tiles");
-  CK(h, cudaSetDevice(h->dev));
-  CK(h, cudaStreamSynchronize(h->stream));
-  const int ti = h->link_tile0[link];
-  const TileDesc &d = h->tiles[ti];
-  const int Wp = row_pitch(d.w);
-  *pitch = Wp;
-  HostVec<uint8_t> code;
-  HostVec<int32_t> vids;
-  if (int rc = download_tiles(h, ti, ti + 1, code, vids)) return rc;
-  memcpy(code_out, code.data(), (size_t)d.L * Wp);
-  memcpy(vid_out, vids.data(), (size_t)d.L * Wp * 4);
-  return TS_OK;
-}
-
-int ts_state_hash(ts_sim *h, uint64_t *out) {
-  if (!h || !h->inited) return fail(h, TS_EINVAL, "not initialised");
-  CK(h, cudaSetDevice(h->dev));
-  CK(h, cudaMemsetAsync(h->d_hash, 0, 16, h->stream));
-  StepParams P = step_params(h, h->t, 0);
-  if (h->ngroups > 0) launch_rows_hash(P, rows_params(h), h->stream, h->d_hash);
-  if (!h->gtiles.empty()) launch_hash(P, h->blocks, h->threads, h->smem, h->stream, h->d_hash);
-  CK(h, cudaGetLastError());
-  unsigned long long r[2];
-  CK(h, cudaMemcpyAsync(r, h->d_hash, 16, cudaMemcpyDeviceToHost, h->stream));
-  CK(h, cudaStreamSynchronize(h->stream));
-  *out = r[0];
-  return TS_OK;
-}
-
-int ts_read_history(ts_sim *h, int32_t t_from, int32_t n, uint64_t *hash, int64_t *active,
-                    int64_t *arrivals, int64_t *injections, int64_t *lane_changes,
-                    int64_t *crossings) {
-  if (!h || !h->inited) return fail(h, TS_EINVAL, "not initialised");
-  if (n < 0 || n > kHist || t_from + n - 1 > h->t || t_from < h->t - kHist + 1)
-    return fail(h, TS_EINVAL, "history range not available");
-  CK(h, cudaSetDevice(h->dev));
-  CK(h, cudaStreamSynchronize(h->stream));
-  std::vector<unsigned long long> st((size_t)kHist * ST_N);
-  CK(h, cudaMemcpy(st.data(), h->d_stats, st.size() * 8, cudaMemcpyDeviceToHost));
-  for (int i = 0; i < n; i++) {
-    const unsigned long long *s = &st[(size_t)((t_from + i) & (kHist - 1)) * ST_N];
-    if (hash) hash[i] = s[ST_HASH];
-    if (active) active[i] = (int64_t)s[ST_ACTIVE];
-    if (arrivals) arrivals[i] = (int64_t)s[ST_ARR];
-    if (injections) injections[i] = (int64_t)s[ST_INJ];
-    if (lane_changes) lane_changes[i] = (int64_t)s[ST_LC];
-    if (crossings) crossings[i] = (int64_t)s[ST_CROSS];
-  }
-  return TS_OK;
-}
-
-int ts_read_flow(ts_sim *h, int32_t t_from, int32_t n, int64_t *sumv) {
-  if (!h || !h->inited) return fail(h, TS_EINVAL, "not initialised");
-  if (n < 0 || n > kHist || t_from + n - 1 > h->t || t_from < h->t - kHist + 1)
-    return fail(h, TS_EINVAL, "history range not available");
-  CK(h, cudaSetDevice(h->dev));
-  CK(h, cudaStreamSynchronize(h->stream));
-  std::vector<unsigned long long> st((size_t)kHist * ST_N);
-  CK(h, cudaMemcpy(st.data(), h->d_stats, st.size() * 8, cudaMemcpyDeviceToHost));
-  for (int i = 0; i < n; i++)
-    sumv[i] = (int64_t)st[(size_t)((t_from + i) & (kHist - 1)) * ST_N + ST_SUMV];
-  return TS_OK;
-}
-
-int ts_get_totals(ts_sim *h, int64_t out[8]) {
-  if (!h || !h->inited) return fail(h, TS_EINVAL, "not initialised");
-  CK(h, cudaStreamSynchronize(h->stream));
-  if (int rc = fold_stats(h)) return rc;
-  unsigned long long st[ST_N];
-  CK(h, cudaMemcpy(st, h->d_stats + (size_t)(h->t & (kHist - 1)) * ST_N, sizeof st,
-                   cudaMemcpyDeviceToHost));
-  const int64_t active = (int64_t)st[ST_ACTIVE];
-  out[0] = active;
-  out[1] = h->n_pending0 - h->injected;
-  out[2] = h->n_arrived0 + h->arrived;
-  out[3] = h->veh_updates;
-  out[4] = h->lane_cells;
-  out[5] = (int64_t)h->tiles.size();
-  out[6] = (int64_t)h->dev_bytes;
-  out[7] = 2 * h->lane_cells + 8 * active;
-  return TS_OK;
-}
-
-int ts_get_link_work(ts_sim *h, int64_t *link_work) {
-  if (!h || !h->inited) return fail(h, TS_EINVAL, "not initialised");
-  CK(h, cudaStreamSynchronize(h->stream));
-  CK(h, cudaMemcpy(link_work, h->d_work, sizeof(int64_t) * h->nl, cudaMemcpyDeviceToHost));
-  return TS_OK;
-}
-
-int ts_last_exchange_timing(ts_sim *h, double *ms, int64_t *n) {
-  if (!h) return TS_EINVAL;
-  if (ms) *ms = h->last_xchg_ms;
-  if (n) *n = h->last_xchg_n;
-  return TS_OK;
-}
-
-int ts_last_timing(ts_sim *h, double *total_ms, double *move_ms, int64_t *move_launches) {
-  if (!h) return TS_EINVAL;
-  if (total_ms) *total_ms = h->last_total_ms;
-  if (move_ms) *move_ms = h->last_move_ms;
-  if (move_launches) *move_launches = h->last_move_launches;
-  return TS_OK;
-}
-
-// --------------------------------------------------------------- partition
-// Orthogonal recursive bisection: a vertical line halves
-// the load, then the larger piece is cut by a horizontal line, and so on
-// until k pieces; non-power-of-two k splits in proportion.
-static void orb_rec(std::vector<int32_t> &idx, size_t lo, size_t hi, const int64_t *x,
-                    const int64_t *y, const std::vector<double> &w, int k, int dom0, bool vertical,
-                    int32_t *out) {
-  if (k == 1) {
-    for (size_t i = lo; i < hi; i++) out[idx[i]] = dom0;
-    return;
-  }
-  const int64_t *c = vertical ? x : y;
-  std::stable_sort(idx.begin() + lo, idx.begin() + hi, [&](int a, int b) {
-    return c[a] < c[b] || (c[a] == c[b] && a < b);
-  });
-  const int kl = (k + 1) / 2, kr = k - kl;
-  double tot = 0;
-  for (size_t i = lo; i < hi; i++) tot += w[idx[i]];
-  const double target = tot * kl / k;
-  double acc = 0, best = 1e300;
-  size_t cut = lo + 1;
-  for (size_t i = lo; i + 1 < hi + 1 && i < hi; i++) {
-    acc += w[idx[i]];
-    const size_t c1 = i + 1;
-    if (c1 - lo < (size_t)kl || hi - c1 < (size_t)kr) continue;
-    const double dev = std::fabs(acc - target);
-    if (dev < best) {
-      best = dev;
-      cut = c1;
-    }
-  }
-  orb_rec(idx, lo, cut, x, y, w, kl, dom0, !vertical, out);
-  orb_rec(idx, cut, hi, x, y, w, kr, dom0 + kl, !vertical, out);
-}
-
-int ts_orb_partition(int32_t n_nodes, const int64_t *node_x_mm, const int64_t *node_y_mm,
-                     const double *node_weight, int32_t k, int32_t *domain_of_node) {
-  if (n_nodes < 1 || k < 1 || k > n_nodes) return TS_EINVAL;
-  std::vector<double> w(n_nodes, 1.0);
-  if (node_weight)
-    for (int i = 0; i < n_nodes; i++) w[i] = std::max(0.0, node_weight[i]);
-  std::vector<int32_t> idx(n_nodes);
-  std::iota(idx.begin(), idx.end(), 0);
-  orb_rec(idx, 0, n_nodes, node_x_mm, node_y_mm, w, k, 0, true, domain_of_node);
-  return TS_OK;
-}
-
 }  // extern "C"
-
-extern "C" {
-// ORB partition of the handle's own network with the paper's default node
-// weights (half of cells x lanes of every attached link)
-// or the given ones, and this handle set up as domain `me` (ts_set_domain).
-int ts_partition(ts_sim *h, int32_t k, const double *node_weight, int32_t me,
-                 int32_t *domain_of_node_out) {
-  if (!h) return TS_EINVAL;
-  if (!h->have_net) return fail(h, TS_EINVAL, "load the network first");
-  std::vector<double> w(h->nn, 1e-9);
-  if (node_weight) {
-    w.assign(node_weight, node_weight + h->nn);
-  } else {
-    for (int j = 0; j < h->nl; j++) {
-      const double lw = 0.5 * (double)h->ncell[j] * h->lanes[j];
-      w[h->from[j]] += lw;
-      w[h->to[j]] += lw;
-    }
-  }
-  std::vector<int32_t> dom(h->nn);
-  if (ts_orb_partition(h->nn, h->nx.data(), h->ny.data(), w.data(), k, dom.data()))
-    return fail(h, TS_EINVAL, "bad partition: k = %d for %d nodes", k, h->nn);
-  if (domain_of_node_out) std::copy(dom.begin(), dom.end(), domain_of_node_out);
-  return ts_set_domain(h, k, dom.data(), me);
-}
-}
