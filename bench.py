@@ -28,6 +28,8 @@ import numpy as np  # noqa: E402
 
 import scenarios  # noqa: E402
 
+NOMINAL_HBM_GBS = 8000.0  # north_star: "against the B200's ~8 TB/s"
+
 FALLBACK_HBM_GBS = 6650.0
 
 
@@ -235,7 +237,11 @@ def bench_tsim(args):
                      "traffic_source": traffic["source"], "kernel": "k_rows",
                      "alg_bytes_per_launch": alg_per_launch, "kernel_ms": mv_ms,
                      "kernel_share": mv_ms * args.steps / ms_total,
-                     "kernel_launches_timed": timing["move_launches"], "peak_source": peak_src},
+                     "kernel_launches_timed": timing["move_launches"], "peak_source": peak_src,
+                     # also against north_star's nominal ~8 TB/s, and
+                     # the whole step (node kernel included) against the measured peak
+                     "nominal_peak": NOMINAL_HBM_GBS, "frac_nominal": achieved / NOMINAL_HBM_GBS,
+                     "step_frac": alg_per_launch / (ms_total / args.steps * 1e-3) / 1e9 / hbm_peak},
         "e2e": {"value": upd_all / e2e_wall, "unit": "vehicle-updates/s",
                 "h2d_bytes_per_step": h2d / (args.steps + args.warmup),
                 "d2h_bytes_per_step": d2h / (args.steps + args.warmup),
