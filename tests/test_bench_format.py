@@ -25,3 +25,27 @@ def test_reference_arm_line():
     assert d["config"]["workload"] == "config1_grid4x4"
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] == 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 == d["e2e"]["d2h_bytes_per_step"]
+
+
+def test_committed_gpu_line():
+    """the newest committed GPU bench line (profiles/) carries every key of
+    the contract and a self-consistent roofline"""
+    import glob
+    import re
+    files = glob.glob(os.path.join(ROOT, "profiles", "r1_bench_v*.json"))
+    newest = max(files, key=lambda f: int(re.search(r"_v(\d+)\.json$", f).group(1)))
+    d = json.loads(open(newest).read().strip().splitlines()[-1])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+              "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config",
+              "roofline", "cpu_baseline", "e2e", "clocks", "gpu_launches"):
+        assert k in d, k
+    r = d["roofline"]
+    assert r["bound"] == "hbm" and r["unit"] == "GB/s"
+    assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
+    assert abs(r["achieved"] - r["alg_bytes_per_launch"] / (r["kernel_ms"] * 1e-3) / 1e9) < 1e-6 * r["achieved"]
+    assert 0 < r["frac"] < 1 and 0 < r["kernel_share"] <= 1
+    assert d["steps"] >= 1 and d["warmup"] >= 3 and d["gpu_launches"] > 0
+    assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["value"] < d["value"]
+    assert d["cpu_baseline"]["kind"] == "oracle"
+    assert not set(d["clocks"]["reasons"]) & {"hw_slowdown", "hw_thermal_slowdown",
+                                               "sw_thermal_slowdown"}
