@@ -1229,18 +1229,24 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
     const int k = h->first_link[f];
     return !h->placed[f] && h->entry[f] >= h->own_lo[k] && h->entry[f] < h->own_hi[k];
   };
+  // which vehicles are this domain's pending trips: flags in parallel, then
+  // a counting sort by first link (input order kept, stable-sorted below)
+  HostVec<uint8_t> pend_me(h->nv);
+  parallel_for(h->nv, [&](int64_t lo, int64_t hi, int) {
+    for (int64_t f = lo; f < hi; f++) pend_me[f] = mine((int)f) ? 1 : 0;
+  });
   h->n_pending0 = 0;
   for (int f = 0; f < h->nv; f++)
-    if (mine(f)) {
+    if (pend_me[f]) {
       pend_off[h->first_link[f] + 1]++;
       h->n_pending0++;
     }
   for (int k = 0; k < h->nl; k++) pend_off[k + 1] += pend_off[k];
   pend_list.assign(std::max(1, pend_off[h->nl]), 0);
-  {
+  if (h->n_pending0 > 0) {
     std::vector<int32_t> fill(h->nl, 0);
     for (int f = 0; f < h->nv; f++)
-      if (mine(f)) {
+      if (pend_me[f]) {
         int k = h->first_link[f];
         pend_list[pend_off[k] + fill[k]++] = f;
       }
@@ -1248,8 +1254,10 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
       std::stable_sort(pend_list.begin() + pend_off[k], pend_list.begin() + pend_off[k + 1],
                        [&](int a, int b) { return h->dep[a] < h->dep[b] || (h->dep[a] == h->dep[b] && a < b); });
   }
-  std::vector<int32_t> inj(h->nv), arr(h->nv, -1);
-  for (int f = 0; f < h->nv; f++) inj[f] = h->placed[f] ? INT_MIN : INT_MAX;
+  HostVec<int32_t> inj(h->nv), arr = filled<int32_t>(h->nv, -1);
+  parallel_for(h->nv, [&](int64_t lo, int64_t hi, int) {
+    for (int64_t f = lo; f < hi; f++) inj[f] = h->placed[f] ? INT_MIN : INT_MAX;
+  });
   h->n_arrived0 = 0;
   if (!h->arr0.empty()) {
     for (int f = 0; f < h->nv; f++) {

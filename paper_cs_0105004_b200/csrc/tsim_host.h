@@ -244,8 +244,8 @@ static int dalloc(ts_sim *h, T **p, size_t n, int fill = -1) {
   return TS_OK;
 }
 
-template <class T>
-static int upload(ts_sim *h, T **p, const std::vector<T> &v) {
+template <class T, class A>
+static int upload(ts_sim *h, T **p, const std::vector<T, A> &v) {
   int rc = dalloc(h, p, v.size());
   if (rc) return rc;
   if (!v.empty())
