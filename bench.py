@@ -220,7 +220,8 @@ def bench_tsim(args):
     alg_per_launch = alg / args.steps
     mv_ms = timing["move_ms"] / max(1, timing["move_launches"])
     achieved = alg_per_launch / (mv_ms / 1e3) / 1e9
-    upd_all = updates + int(np.sum(sim.history(1, min(args.warmup, 4096))["active"])) if args.warmup else updates
+    # the warm-up steps update the vehicles of S(0) .. S(W-1)
+    upd_all = updates + int(np.sum(sim.history(0, args.warmup)["active"]))
     out = {
         "metric": "vehicle-updates/s", "value": value, "unit": "vehicle-updates/s",
         "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,

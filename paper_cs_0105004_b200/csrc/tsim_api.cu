@@ -70,9 +70,13 @@ static int nccl_exchange(ts_sim *h) {
   NcclApi &a = nccl();
   NCK(h, a.groupStart());
   for (const ts_sim::Nbr &nb : h->nbrs) {
-    const size_t bytes = nb.send_slot.size() * sizeof(Strip);
-    NCK(h, a.send(h->d_send + nb.off, bytes, ncclUint8, nb.dom, h->comm, h->stream));
-    NCK(h, a.recv(h->d_recv + nb.off, bytes, ncclUint8, nb.dom, h->comm, h->stream));
+    // send and receive segments have the same size by construction (one
+    // strip per lane of every shared split link, both sides in link order;
+    // checked in build_tiles)
+    NCK(h, a.send(h->d_send + nb.off, nb.send_slot.size() * sizeof(Strip), ncclUint8, nb.dom,
+                  h->comm, h->stream));
+    NCK(h, a.recv(h->d_recv + nb.off, nb.recv_slot.size() * sizeof(Strip), ncclUint8, nb.dom,
+                  h->comm, h->stream));
   }
   NCK(h, a.groupEnd());
   return TS_OK;
@@ -136,6 +140,8 @@ int ts_create(const ts_config *cfg, ts_sim **out) {
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_packed, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_copied, cudaEventDisableTiming);
   if (e != cudaSuccess) {
     delete h;
     return fail(nullptr, TS_EINTERNAL, "CUDA init failed: %s", cudaGetErrorString(e));
@@ -162,6 +168,8 @@ void ts_destroy(ts_sim *h) {
   if (h->side) cudaStreamDestroy(h->side);
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
   if (h->ev_join) cudaEventDestroy(h->ev_join);
+  if (h->ev_packed) cudaEventDestroy(h->ev_packed);
+  if (h->ev_copied) cudaEventDestroy(h->ev_copied);
   delete h;
 }
 
@@ -538,7 +546,7 @@ static void owned_range(int n, int dfrom, int dto, int me, int &lo, int &hi) {
   }
 }
 
-static void build_tiles(ts_sim *h) {
+static bool build_tiles(ts_sim *h) {
   const int tc = h->cfg.tile_cells > 0 ? h->cfg.tile_cells : 512;
   const bool dom = h->dom_k > 1;
   h->ring_rows = h->periodic >= 0 && !dom && !(h->cfg.flags & TS_FLAG_GENERAL) &&
@@ -658,6 +666,7 @@ static void build_tiles(ts_sim *h) {
     for (ts_sim::Nbr &nb : h->nbrs) {
       nb.off = h->n_xs;
       h->n_xs += (int64_t)nb.send_slot.size();
+      if (nb.send_slot.size() != nb.recv_slot.size()) return false;  // one strip each way per lane
     }
   }
   // classify: whole non-periodic links of <= kRowMaxCells cells and <= 32
@@ -714,6 +723,7 @@ static void build_tiles(ts_sim *h) {
   // ring segment rows take their lane change in a launch of its own (its
   // neighbour segments must hold S(t))
   h->rfused = (h->cfg.flags & TS_FLAG_FUSED) != 0 && !h->ring_rows;
+  return true;
 }
 
 // incoming lanes of every node in priority order (R9: major class first,
@@ -1038,7 +1048,7 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
   if (t0 < 0) return fail(h, TS_EINVAL, "t0 must be >= 0");
   CK(h, cudaSetDevice(h->dev));
   if (h->dom_of_node.empty()) h->dom_of_node.assign(h->nn, 0);
-  build_tiles(h);
+  if (!build_tiles(h)) return fail(h, TS_EINTERNAL, "asymmetric exchange plan");
 
   // the routes (out-slot sequences built at load, GBs at the largest
   // configs) go to the device on a host thread of their own through pinned
@@ -1506,6 +1516,10 @@ static void phase_move(ts_sim *h, bool more, cudaEvent_t e0, cudaEvent_t e1) {
 }
 
 constexpr int kTimingStride = 8;
+// Steps are enqueued in blocks of at most kStepBlock: the per-step counters
+// live in a ring of kHist slots, which must be folded into the host totals
+// before a slot is reused (a longer run is finished block by block).
+constexpr int kStepBlock = kHist / 2;
 // steps per CUDA graph: odd, so that the row buffers return to their parity
 // (one lane-change-only launch + kGraphSteps move launches flip them)
 constexpr int kGraphSteps = 15;
@@ -1580,6 +1594,7 @@ static int enqueue_steps(ts_sim *h, int32_t n) {
   if (h->n_xs > 0 && !h->comm)
     return fail(h, TS_EINVAL, "domain with neighbours: ts_nccl_init, or ts_step_phase and an exchange");
   if (n == 0) return TS_OK;
+  if (n > kStepBlock) return fail(h, TS_EINTERNAL, "step block too long");
   CK(h, cudaSetDevice(h->dev));
   if (h->n_xs > 0) {  // whole steps with the native exchange (G1): LC, #1, move, #2
     if (zero_stats(h, h->t + 1, std::min(n + 1, kHist))) return TS_EINTERNAL;
@@ -1671,8 +1686,7 @@ int fold_stats(ts_sim *h) {
   return TS_OK;
 }
 
-static int finish_steps(ts_sim *h, int32_t t_from, int32_t n) {
-  (void)t_from;
+static int finish_steps(ts_sim *h) {
   CK(h, cudaStreamSynchronize(h->stream));
   float ms = 0;
   CK(h, cudaEventElapsedTime(&ms, h->ev0, h->ev1));
@@ -1696,28 +1710,83 @@ static int finish_steps(ts_sim *h, int32_t t_from, int32_t n) {
   return fold_stats(h);
 }
 
-int ts_step(ts_sim *h, int32_t n_steps) {
-  const int32_t t_from = h ? h->t : 0;
-  int rc = enqueue_steps(h, n_steps);
-  if (rc) return rc;
-  if (n_steps == 0) return TS_OK;
-  return finish_steps(h, t_from, n_steps);
+struct StepTotals {
+  double ms = 0, move_ms = 0, xchg_ms = 0;
+  int64_t move_launches = 0, xchg_n = 0;
+  void add(const ts_sim *h) {
+    ms += h->last_total_ms;
+    move_ms += h->last_move_ms;
+    xchg_ms += h->last_xchg_ms;
+    move_launches += h->last_move_launches;
+    xchg_n += h->last_xchg_n;
+  }
+  void store(ts_sim *h) const {
+    h->last_total_ms = ms;
+    h->last_move_ms = move_ms;
+    h->last_xchg_ms = xchg_ms;
+    h->last_move_launches = move_launches;
+    h->last_xchg_n = xchg_n;
+  }
+};
+
+// run all but the last block of n steps to completion (totals in *acc);
+// returns the size of the last block, or < 0 on error
+static int run_leading_blocks(ts_sim *h, int32_t n, StepTotals *acc) {
+  while (n > kStepBlock) {
+    if (int rc = enqueue_steps(h, kStepBlock)) return -rc;
+    if (int rc = finish_steps(h)) return -rc;
+    acc->add(h);
+    n -= kStepBlock;
+  }
+  return n;
 }
 
-static int32_t g_async_from = 0, g_async_n = 0;
+int ts_step(ts_sim *h, int32_t n_steps) {
+  if (!h) return TS_EINVAL;
+  if (n_steps < 0) return fail(h, TS_EINVAL, "negative step count");
+  StepTotals acc;
+  const int last = run_leading_blocks(h, n_steps, &acc);
+  if (last < 0) return -last;
+  if (int rc = enqueue_steps(h, last)) return rc;
+  if (n_steps == 0) return TS_OK;
+  if (last > 0) {
+    if (int rc = finish_steps(h)) return rc;
+    acc.add(h);
+  }
+  acc.store(h);
+  return TS_OK;
+}
 
+// asynchronous steps: per-handle state (several handles may interleave);
+// a run longer than kStepBlock finishes its leading blocks before returning
 int ts_step_async(ts_sim *h, int32_t n_steps) {
-  g_async_from = h ? h->t : 0;
-  g_async_n = n_steps;
-  return enqueue_steps(h, n_steps);
+  if (!h) return TS_EINVAL;
+  if (h->async_n > 0) return fail(h, TS_EINVAL, "ts_step_async: previous steps not synced");
+  if (n_steps < 0) return fail(h, TS_EINVAL, "negative step count");
+  StepTotals acc;
+  const int last = run_leading_blocks(h, n_steps, &acc);
+  if (last < 0) return -last;
+  h->async_ms = acc.ms;
+  h->async_move_ms = acc.move_ms;
+  h->async_move_launches = acc.move_launches;
+  h->async_from = h->t;
+  if (int rc = enqueue_steps(h, last)) return rc;
+  h->async_n = last;
+  return TS_OK;
 }
 
 int ts_sync(ts_sim *h) {
   if (!h) return TS_EINVAL;
-  if (g_async_n > 0) {
-    int rc = finish_steps(h, g_async_from, g_async_n);
-    g_async_n = 0;
-    return rc;
+  CK(h, cudaSetDevice(h->dev));
+  if (h->async_n > 0) {
+    h->async_n = 0;
+    if (int rc = finish_steps(h)) return rc;
+    h->last_total_ms += h->async_ms;
+    h->last_move_ms += h->async_move_ms;
+    h->last_move_launches += h->async_move_launches;
+    h->async_ms = h->async_move_ms = 0;
+    h->async_move_launches = 0;
+    return TS_OK;
   }
   CK(h, cudaStreamSynchronize(h->stream));
   return fold_stats(h);
@@ -1757,6 +1826,10 @@ int ts_step_phase(ts_sim *h, int32_t phase, int32_t more) {
   CK(h, cudaEventRecord(h->ph_ev[h->ph_used], h->stream));
   switch (phase) {
     case 0:
+      if (h->t + 1 - h->folded_t >= kStepBlock) {  // fold before the stats ring wraps
+        CK(h, cudaStreamSynchronize(h->stream));
+        if (int rc = fold_stats(h)) return rc;
+      }
       if (zero_stats(h, h->t + 1, 1)) return TS_EINTERNAL;
       phase_lc(h);
       break;
@@ -1811,13 +1884,13 @@ int ts_exchange_local(ts_sim **hs, int32_t k) {
     if (!hs[i] || !hs[i]->inited || hs[i]->dom_k != k) return TS_EINVAL;
     by_dom[hs[i]->dom_me] = hs[i];
   }
-  std::vector<cudaEvent_t> ev(k);
+  // ordering by each handle's reusable events: the receivers' copies wait
+  // for their senders' packs; the senders' next work waits for the copies
   for (int i = 0; i < k; i++) {
     ts_sim *a = by_dom[i];
     if (!a) return fail(hs[0], TS_EINVAL, "domain %d missing", i);
     CK(a, cudaSetDevice(a->dev));
-    CK(a, cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
-    CK(a, cudaEventRecord(ev[i], a->stream));
+    CK(a, cudaEventRecord(a->ev_packed, a->stream));
   }
   for (int i = 0; i < k; i++) {
     ts_sim *b = by_dom[i];  // receiver
@@ -1830,7 +1903,7 @@ int ts_exchange_local(ts_sim **hs, int32_t k) {
       if (!back || back->send_slot.size() != nb.recv_slot.size())
         return fail(b, TS_EINTERNAL, "exchange plans of domains %d and %d disagree", a->dom_me,
                     b->dom_me);
-      CK(b, cudaStreamWaitEvent(b->stream, ev[nb.dom], 0));
+      CK(b, cudaStreamWaitEvent(b->stream, a->ev_packed, 0));
       CK(b, cudaMemcpyPeerAsync(b->d_recv + nb.off, b->dev, a->d_send + back->off, a->dev,
                                 nb.recv_slot.size() * sizeof(Strip), b->stream));
     }
@@ -1838,18 +1911,14 @@ int ts_exchange_local(ts_sim **hs, int32_t k) {
   // a sender may not overwrite its send buffer before the receivers copied
   for (int i = 0; i < k; i++) {
     ts_sim *b = by_dom[i];
-    cudaEvent_t done;
     CK(b, cudaSetDevice(b->dev));
-    CK(b, cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
-    CK(b, cudaEventRecord(done, b->stream));
+    CK(b, cudaEventRecord(b->ev_copied, b->stream));
     for (const ts_sim::Nbr &nb : b->nbrs) {
       ts_sim *a = by_dom[nb.dom];
       CK(a, cudaSetDevice(a->dev));
-      CK(a, cudaStreamWaitEvent(a->stream, done, 0));
+      CK(a, cudaStreamWaitEvent(a->stream, b->ev_copied, 0));
     }
-    cudaEventDestroy(done);
   }
-  for (int i = 0; i < k; i++) cudaEventDestroy(ev[i]);
   return TS_OK;
 }
 

@@ -207,6 +207,12 @@ struct ts_sim {
   size_t ph_used = 0;
   int64_t last_move_launches = 0;
   bool timing = true;
+  // ts_step_async / ts_sync: the steps enqueued and not yet finished
+  int32_t async_from = 0, async_n = 0;
+  double async_ms = 0, async_move_ms = 0;  // timing of the leading blocks of a long async run
+  int64_t async_move_launches = 0;
+  // ts_exchange_local: reusable ordering events (after the pack, after the copies)
+  cudaEvent_t ev_packed = nullptr, ev_copied = nullptr;
 };
 
 // shared by the step (tsim_api.cu) and the readers (tsim_readers.cu);

@@ -225,7 +225,7 @@ int ts_read_history(ts_sim *h, int32_t t_from, int32_t n, uint64_t *hash, int64_
                     int64_t *arrivals, int64_t *injections, int64_t *lane_changes,
                     int64_t *crossings) {
   if (!h || !h->inited) return fail(h, TS_EINVAL, "not initialised");
-  if (n < 0 || n > kHist || t_from + n - 1 > h->t || t_from < h->t - kHist + 1)
+  if (n < 0 || n > kHist || t_from + n - 1 > h->t || t_from < h->t - kHist + 2)
     return fail(h, TS_EINVAL, "history range not available");
   CK(h, cudaSetDevice(h->dev));
   CK(h, cudaStreamSynchronize(h->stream));
@@ -245,7 +245,7 @@ int ts_read_history(ts_sim *h, int32_t t_from, int32_t n, uint64_t *hash, int64_
 
 int ts_read_flow(ts_sim *h, int32_t t_from, int32_t n, int64_t *sumv) {
   if (!h || !h->inited) return fail(h, TS_EINVAL, "not initialised");
-  if (n < 0 || n > kHist || t_from + n - 1 > h->t || t_from < h->t - kHist + 1)
+  if (n < 0 || n > kHist || t_from + n - 1 > h->t || t_from < h->t - kHist + 2)
     return fail(h, TS_EINVAL, "history range not available");
   CK(h, cudaSetDevice(h->dev));
   CK(h, cudaStreamSynchronize(h->stream));

@@ -102,10 +102,11 @@ def merge_vehicles(parts):
     """merge per-domain vehicle reads: per vehicle, the domain reporting it
     ACTIVE, else ARRIVED, else PENDING (include/tsim.h)"""
     out = {k: np.array(v, copy=True) for k, v in parts[0].items()}
-    rank = {ACTIVE: 3, ARRIVED: 2, PENDING: 1, ABSENT: 0}
-    best = np.vectorize(rank.get)(out["status"])
+    rank = np.zeros(4, np.int8)
+    rank[[ACTIVE, ARRIVED, PENDING, ABSENT]] = [3, 2, 1, 0]
+    best = rank[out["status"]]
     for p in parts[1:]:
-        r = np.vectorize(rank.get)(p["status"])
+        r = rank[p["status"]]
         take = r > best
         for k in out:
             out[k][take] = p[k][take]

@@ -117,6 +117,31 @@ def test_portland_small(flags):
     run_parity(s, 400, flags, full_every=0, hash_every=40)
 
 
+# ------------------------------------- the benchmarked path, without the hash
+BENCH = tsim.FLAG_FUSED  # exactly bench.py's flags (k_rows<5>, no hash instrument)
+
+
+@pytest.mark.parametrize("chunk", [7, 25, 50])
+@pytest.mark.parametrize("net", ["grid6", "grid24dense", "portland"])
+def test_bench_flags_full_state(net, chunk):
+    """bench.py's launch flags (FLAG_FUSED only: k_rows<5>, whose unchanged
+    rows take the prefix-copy vid path): the full vehicle state (status,
+    link, lane, cell, v, cursor, arrival) against the oracle after every
+    call of `chunk` steps, so two vids swapped inside a row would fail"""
+    if net == "grid6":
+        s = scenarios.grid_trips(rows=6, cols=6, n_veh=3000, depart_max=300, seed=8, name="grid6nh")
+        steps = 300
+    elif net == "grid24dense":
+        s = scenarios.big_grid(rows=24, cols=24, seed=3, name="grid24dense_nh")
+        steps = 100
+    else:
+        s = scenarios.portland(n_nodes=600, n_edges=800, n_veh=8000, side_km=8.0, n_zones=64,
+                               seed=2)
+        s.depart = (s.depart // 12).astype(np.int32)
+        steps = 300
+    run_parity(s, steps, BENCH, full_every=chunk, hash_every=chunk)
+
+
 def test_big_grid_dense():
     """config-4a recipe (density 0.2, 4 lanes, 100-cell links, Manhattan
     routes) on a 24x24 lattice: heavy lane changing and node traffic"""
