@@ -268,6 +268,42 @@ int ts_get_totals(ts_sim *h, int64_t out[8]);
  * set (PAPER.md:730-735 load statistics). link_work[n_links]. */
 int ts_get_link_work(ts_sim *h, int64_t *link_work);
 
+/* Load statistics (§7: "the execution time of each link
+ * and each intersection"), accumulated since ts_init when TS_FLAG_LINK_WORK
+ * is set (zeros otherwise): link_work[n_links] = vehicle updates on the
+ * link's cells owned by this handle; node_work[n_nodes] = per step, the
+ * incoming lanes of the node whose front vehicle is inside the interaction
+ * range plus the node's crossings (nodes of this domain only).  Either
+ * pointer may be NULL.  Synchronises the handle's stream. */
+int ts_get_load(ts_sim *h, int64_t *link_work, int64_t *node_work);
+
+/* Pure host, for the adaptive rebalancing: apportion one
+ * domain's measured device time domain_ms over a window (ts_busy_time) to
+ * its links and nodes in proportion to their work counts over the same
+ * window (differences of ts_get_load; one vehicle update and one node unit
+ * count alike).  ADDS into link_time[n_links] and node_time[n_nodes]
+ * (node_work / node_time may be NULL), so the k domains of a partition
+ * accumulate into one pair of arrays (across ranks: sum them).  A domain
+ * without work adds nothing.  TS_EINVAL on negative counts or time. */
+int ts_load_times(double domain_ms, int32_t n_links, const int64_t *link_work, int32_t n_nodes,
+                  const int64_t *node_work, double *link_time, double *node_time);
+
+/* Pure host: the next partition from measured times (
+ * SPEC.md:373-379).  Node weight = node_time (NULL = 0) + half of the time
+ * of every attached link, links without measured time keeping a floor of
+ * 1e-3 x total time x their share of cells x lanes; then a k-way
+ * partition, method 0 = ORB (ts_orb_partition), 1 = multilevel
+ * (ts_multilevel_partition with imbalance and seed).  Outputs the node
+ * weights (nullable, [n_nodes]) and domain_of_node_out[n_nodes].  The
+ * caller migrates the state (read, ts_place_vehicles_at / ts_set_arrived
+ * into handles of the new partition, ts_resume); results are unchanged,
+ * only speed.  TS_EINVAL: bad network, k, method or a negative time. */
+int ts_rebalance(int32_t n_nodes, const int64_t *node_x_mm, const int64_t *node_y_mm,
+                 int32_t n_links, const int32_t *from, const int32_t *to, const int32_t *lanes,
+                 const int64_t *length_mm, const double *link_time, const double *node_time,
+                 int32_t k, int32_t method, double imbalance, uint64_t seed,
+                 double *node_weight_out, int32_t *domain_of_node_out);
+
 /* Orthogonal recursive bisection of the nodes (SPEC.md
  * :210-218): node weights (the load of the attached half-links; NULL =
  * uniform), k domains, output domain_of_node[n_nodes].  Vertical cut first;

@@ -729,14 +729,16 @@ static bool build_tiles(ts_sim *h) {
 // incoming lanes of every node in priority order (R9: major class first,
 // then link id, then lane), packed into chunks of <= 32 lanes
 static bool build_node_lanes(ts_sim *h, std::vector<NodeLane> &lanes,
-                             std::vector<uint32_t> &sig) {
+                             std::vector<uint32_t> &sig, std::vector<int32_t> &nl_node) {
   lanes.clear();
   sig.clear();
+  nl_node.clear();
   int in_chunk = 0;
   auto close_chunk = [&]() {  // pad the chunk to 32 entries
     while (lanes.size() % 32) {
       lanes.push_back(NodeLane{-1, 0, 0u, 0, 0, 1, 0});
       sig.push_back(0u);
+      nl_node.push_back(-1);
     }
     in_chunk = 0;
   };
@@ -759,6 +761,7 @@ static bool build_node_lanes(ts_sim *h, std::vector<NodeLane> &lanes,
           lanes.push_back(NodeLane{h->lgid[j] + l, h->out_off[nd], h->tt[j], (uint8_t)l,
                                    (uint8_t)(pass == 0), (uint8_t)h->vmax[j],
                                    (uint8_t)node_first});
+          nl_node.push_back(nd);
           uint32_t sw = 0u;  // the lane's phase (R23): 0 = maximal class, 1 = the rest
           const uint32_t s0 = h->node_sig.empty() ? 0u : h->node_sig[nd];
           if (s0 >> 31) {
@@ -832,8 +835,9 @@ static int setup_node_lanes(ts_sim *h) {
   if (h->ring_rows) return setup_ring_nodes(h);
   std::vector<NodeLane> nlanes;
   std::vector<uint32_t> lsig;
+  std::vector<int32_t> nl_node;
   h->node_warp = h->periodic < 0 && !(h->cfg.flags & (TS_FLAG_GENERAL | TS_FLAG_NODE_GENERAL)) &&
-                 build_node_lanes(h, nlanes, lsig);
+                 build_node_lanes(h, nlanes, lsig, nl_node);
   h->nli.assign(h->nlanes, 0);
   if (h->node_warp) {
     h->nchunks = (int32_t)(nlanes.size() / 32);
@@ -843,6 +847,7 @@ static int setup_node_lanes(ts_sim *h) {
       if (nlanes[i].lane_gid >= 0) h->nli[nlanes[i].lane_gid] = (int32_t)i;
     int rc;
     if ((rc = upload(h, &h->d_nlanes, nlanes))) return rc;
+    if ((rc = upload(h, &h->d_nl_node, nl_node))) return rc;
     if (h->node_sig.empty()) h->d_lane_sig = nullptr;
     else if ((rc = upload(h, &h->d_lane_sig, lsig))) return rc;
   } else {
@@ -966,6 +971,7 @@ static NodeParams node_params(ts_sim *h, int t) {
   N.ext = h->d_ext;
   N.entr = h->d_entr;
   N.stats = h->d_stats;
+  N.node_work = (h->cfg.flags & TS_FLAG_LINK_WORK) && h->periodic < 0 ? h->d_node_work : nullptr;
   return N;
 }
 
@@ -1356,6 +1362,7 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
   if ((rc = dalloc(h, &h->d_ext, h->n_nli, 0))) return rc;
   if ((rc = dalloc(h, &h->d_stats, (size_t)kHist * ST_N, 0))) return rc;
   if ((rc = dalloc(h, &h->d_work, h->nl, 0))) return rc;
+  if ((rc = dalloc(h, &h->d_node_work, h->nn, 0))) return rc;
   if ((rc = dalloc(h, &h->d_hash, 2, 0))) return rc;
   if ((rc = upload(h, &h->d_in_off, h->in_off))) return rc;
   if ((rc = upload(h, &h->d_in_list, h->in_list))) return rc;
@@ -1482,8 +1489,9 @@ static void phase_move(ts_sim *h, bool more, cudaEvent_t e0, cudaEvent_t e1) {
   const int mode = base_mode(h);
   if (h->n_xs > 0) unpack_strips(h);
   if (h->node_warp)
-    launch_node_warp(node_params(h, t), NodeWarpParams{h->d_lane_sig, h->d_nlanes, h->nchunks},
-                     h->stream, h->pdl);
+    launch_node_warp(node_params(h, t),
+                     NodeWarpParams{h->d_lane_sig, h->d_nlanes, h->nchunks, h->d_nl_node}, h->stream,
+                     h->pdl);
   else
     launch_node(node_params(h, t), h->stream);
   // row tiles and general tiles are disjoint: with both present, the

@@ -181,6 +181,8 @@ struct ts_sim {
   uint64_t *d_tail = nullptr, *d_entr = nullptr;
   uint8_t *d_head = nullptr, *d_ext = nullptr;
   unsigned long long *d_stats = nullptr, *d_work = nullptr, *d_hash = nullptr;
+  unsigned long long *d_node_work = nullptr;  // per node (TS_FLAG_LINK_WORK)
+  int32_t *d_nl_node = nullptr;               // node id per node-lane index
   int32_t *d_in_off = nullptr, *d_in_list = nullptr, *d_out_off = nullptr, *d_out_list = nullptr;
   int32_t *d_ncell = nullptr, *d_lanes = nullptr, *d_lgid = nullptr, *d_cls = nullptr;
   int gcur = 0, rcur = 0;  // current buffer of the general / row state

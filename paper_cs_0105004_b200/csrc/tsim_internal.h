@@ -258,6 +258,10 @@ struct NodeParams {
   uint8_t *ext;              // by node-lane index (k_node: identity)
   uint64_t *entr;
   unsigned long long *stats;
+  // per-node work counters (load statistics), by node id;
+  // NULL unless TS_FLAG_LINK_WORK: incoming lanes whose front vehicle is in
+  // the interaction range, plus crossings
+  unsigned long long *node_work;
 };
 
 // tail record of a lane in S1 (read by k_node):
@@ -299,6 +303,7 @@ struct NodeWarpParams {
   const uint32_t *sig;  // per lane (same order as lanes); NULL = no signals
   const NodeLane *lanes;  // [32 * nchunks]
   int32_t nchunks;
+  const int32_t *nl_node;  // node id of every node-lane index (-1 for pads; node work only)
 };
 
 void launch_lc(const StepParams &p, int blocks, int threads, int smem, void *stream);

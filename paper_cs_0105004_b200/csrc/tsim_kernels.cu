@@ -589,8 +589,17 @@ __global__ void __launch_bounds__(256) k_node_warp(const NodeParams P_, const No
 #pragma unroll
   for (int k = 0; k < kNodeILP; k++) {  // stage 4: grants
     int ext = 0;
+    const uint32_t cr0 = crossings;
     if (win[k]) ext = node_grant(P, cd[k], e[k].vk, head[k], crossings, (e[k].major & 2) != 0);
     if (act[k]) P.ext[32 * (c0 + k) + lane] = (uint8_t)ext;
+    if (P.node_work) {  // load statistics: the node's lanes in range + its crossings
+      const bool a = act[k] && e[k].lane_gid >= 0;
+      const uint32_t nodemask = __match_any_sync(FULL, a ? (int)e[k].first : 64 + lane);
+      const uint32_t wk = (uint32_t)((rec[k] >> 43) & 1) + (crossings - cr0);
+      const uint32_t sum = __reduce_add_sync(nodemask, wk);
+      if (a && (__ffs(nodemask) - 1) == lane && sum)
+        atomicAdd(P.node_work + W.nl_node[32 * (c0 + k) + lane], (unsigned long long)sum);
+    }
   }
   node_flush(P, crossings, red);
 }
@@ -619,6 +628,13 @@ __global__ void __launch_bounds__(128) k_node(const NodeParams P_) {
           majorfree = false;
       }
     }
+    const uint32_t cr0 = crossings;
+    uint32_t in_range = 0;  // load statistics: lanes whose front vehicle is in range
+    if (P.node_work)
+      for (int i = a; i < b; i++) {
+        const int j = P.in_list[i], lg = P.link_lgid[j];
+        for (int l = 0; l < P.link_lanes[j]; l++) in_range += (uint32_t)((P.tail_rec[lg + l] >> 43) & 1);
+      }
     constexpr int kMaxClaim = 128;  // target lanes taken (<= out-links x lanes)
     int claimed[kMaxClaim];
     int nclaimed = 0;
@@ -651,6 +667,8 @@ __global__ void __launch_bounds__(128) k_node(const NodeParams P_) {
         }
       }
     }
+    if (P.node_work && in_range + (crossings - cr0))
+      P.node_work[node] += (unsigned long long)(in_range + (crossings - cr0));
   }
   node_flush(P, crossings, red);
 }

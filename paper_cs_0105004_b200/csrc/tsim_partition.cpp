@@ -264,3 +264,79 @@ extern "C" int ts_multilevel_partition(int32_t n_nodes, const int64_t *node_x_mm
   for (int i = 0; i < n_nodes; i++) domain_of_node[i] = part[i];
   return TS_OK;
 }
+
+// ------------------------------------------------- adaptive load balancing
+// PAPER.md:726-735 (§7): "we collect the execution time of each link and
+// each intersection (node)" during a run and feed it to the partitioner.
+// Here a domain's measured device time over a window (ts_busy_time) is
+// apportioned to its links and nodes in proportion to their work counts
+// over the same window (ts_get_load: vehicle updates per link, lanes in
+// range + crossings per node; one unit of either counts alike).
+extern "C" int ts_load_times(double domain_ms, int32_t n_links, const int64_t *link_work,
+                             int32_t n_nodes, const int64_t *node_work, double *link_time,
+                             double *node_time) {
+  if (n_links < 0 || n_nodes < 0 || !(domain_ms >= 0.0)) return TS_EINVAL;
+  if ((n_links && (!link_work || !link_time)) || (n_nodes && node_work && !node_time))
+    return TS_EINVAL;
+  double tot = 0.0;
+  for (int32_t j = 0; j < n_links; j++) {
+    if (link_work[j] < 0) return TS_EINVAL;
+    tot += (double)link_work[j];
+  }
+  if (node_work)
+    for (int32_t i = 0; i < n_nodes; i++) {
+      if (node_work[i] < 0) return TS_EINVAL;
+      tot += (double)node_work[i];
+    }
+  if (tot <= 0.0) return TS_OK;  // an idle domain: no time to apportion
+  const double per = domain_ms / tot;
+  for (int32_t j = 0; j < n_links; j++) link_time[j] += per * (double)link_work[j];
+  if (node_work)
+    for (int32_t i = 0; i < n_nodes; i++) node_time[i] += per * (double)node_work[i];
+  return TS_OK;
+}
+
+// Node weights for the next partition from the per-link and per-node times
+// (node weight = its own time + half of every attached
+// link's time; links without measured work keep a floor of 1e-3 of their
+// static share cells x lanes, so empty regions still count), then a new
+// k-way partition: method 0 = ORB, 1 = multilevel
+// (PAPER.md:585-636).
+extern "C" int ts_orb_partition(int32_t n_nodes, const int64_t *node_x_mm, const int64_t *node_y_mm,
+                                const double *node_weight, int32_t k, int32_t *domain_of_node);
+
+extern "C" int ts_rebalance(int32_t n_nodes, const int64_t *node_x_mm, const int64_t *node_y_mm,
+                            int32_t n_links, const int32_t *from, const int32_t *to,
+                            const int32_t *lanes, const int64_t *length_mm,
+                            const double *link_time, const double *node_time, int32_t k,
+                            int32_t method, double imbalance, uint64_t seed,
+                            double *node_weight_out, int32_t *domain_of_node_out) {
+  if (n_nodes < 1 || n_links < 0 || k < 1 || k > n_nodes || !node_x_mm || !node_y_mm ||
+      !link_time || !domain_of_node_out || (method != 0 && method != 1))
+    return TS_EINVAL;
+  double lsum = 0.0, ssum = 0.0;
+  std::vector<double> stat(n_links);
+  for (int32_t j = 0; j < n_links; j++) {
+    if (from[j] < 0 || from[j] >= n_nodes || to[j] < 0 || to[j] >= n_nodes || length_mm[j] <= 0 ||
+        !(link_time[j] >= 0.0))
+      return TS_EINVAL;
+    const int64_t cells = std::max<int64_t>(1, (length_mm[j] + 3750) / 7500);  // R1
+    stat[j] = (double)cells * lanes[j];
+    ssum += stat[j];
+    lsum += link_time[j];
+  }
+  const double fl = ssum > 0.0 ? 1e-3 * std::max(lsum, 1e-12) / ssum : 0.0;
+  std::vector<double> w(n_nodes, 1e-9);
+  if (node_time)
+    for (int32_t i = 0; i < n_nodes; i++) w[i] += std::max(0.0, node_time[i]);
+  for (int32_t j = 0; j < n_links; j++) {
+    const double lt = link_time[j] + fl * stat[j];
+    w[from[j]] += 0.5 * lt;
+    w[to[j]] += 0.5 * lt;
+  }
+  if (node_weight_out) std::copy(w.begin(), w.end(), node_weight_out);
+  if (method == 0)
+    return ts_orb_partition(n_nodes, node_x_mm, node_y_mm, w.data(), k, domain_of_node_out);
+  return ts_multilevel_partition(n_nodes, node_x_mm, node_y_mm, n_links, from, to, lanes, w.data(),
+                                 k, imbalance, seed, domain_of_node_out);
+}

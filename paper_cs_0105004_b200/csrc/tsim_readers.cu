@@ -282,6 +282,15 @@ int ts_get_link_work(ts_sim *h, int64_t *link_work) {
   return TS_OK;
 }
 
+int ts_get_load(ts_sim *h, int64_t *link_work, int64_t *node_work) {
+  if (!h || !h->inited) return fail(h, TS_EINVAL, "not initialised");
+  CK(h, cudaSetDevice(h->dev));
+  CK(h, cudaStreamSynchronize(h->stream));
+  if (link_work) CK(h, cudaMemcpy(link_work, h->d_work, sizeof(int64_t) * h->nl, cudaMemcpyDeviceToHost));
+  if (node_work) CK(h, cudaMemcpy(node_work, h->d_node_work, sizeof(int64_t) * h->nn, cudaMemcpyDeviceToHost));
+  return TS_OK;
+}
+
 int ts_last_exchange_timing(ts_sim *h, double *ms, int64_t *n) {
   if (!h) return TS_EINVAL;
   if (ms) *ms = h->last_xchg_ms;

@@ -67,25 +67,30 @@ def link_times(link_work_per_domain, domain_ms):
     """execution time per link ("we collect the execution
     time of each link and intersection"): each domain's measured step time
     apportioned to its links by their share of the domain's work (vehicle
-    updates; a split link's halves are counted by their owners)"""
-    t = np.zeros(len(link_work_per_domain[0]), np.float64)
+    updates; a split link's halves are counted by their owners) -- the
+    library's ts_load_times"""
+    lt = np.zeros(len(link_work_per_domain[0]), np.float64)
     for lw, ms in zip(link_work_per_domain, domain_ms):
-        lw = np.asarray(lw, np.float64)
-        tot = lw.sum()
-        if tot > 0:
-            t += ms * lw / tot
-    return t
+        _t.load_times(ms, lw, link_time=lt)
+    return lt
 
 
-def rebalance_weights(scn, link_work_per_domain, domain_ms, floor=None):
+def load_times(windows, domain_ms, n_nodes):
+    """link and node times of a window from every domain's (link work, node
+    work) and measured time (ts_load_times, accumulated over the domains)"""
+    lt = np.zeros(len(windows[0][0]), np.float64)
+    nt = np.zeros(n_nodes, np.float64)
+    for (lw, nw), ms in zip(windows, domain_ms):
+        _t.load_times(ms, lw, nw, link_time=lt, node_time=nt)
+    return lt, nt
+
+
+def rebalance_weights(scn, link_work_per_domain, domain_ms):
     """node weights for the next partition from the measured link times
-    (half of every attached link); links without work keep
-    a small floor (their static load share) so empty regions still count"""
+    (ts_rebalance: half of every attached link; links
+    without work keep a floor of their static load share)"""
     lt = link_times(link_work_per_domain, domain_ms)
-    if floor is None:
-        static = link_cells(scn) * np.asarray(scn.link_lanes, np.float64)
-        floor = 1e-3 * static / static.sum() * max(lt.sum(), 1e-12)
-    return node_weights(scn, lt + floor)
+    return _t.rebalance(scn, 1, lt)[1]
 
 
 def split_stats(scn, dom):
@@ -222,17 +227,20 @@ class LocalDomains:
     def rebalance(self, method="orb"):
         """adaptive repartition (BASELINE: "rebalanced from
         measured per-domain step times"): per-domain device time and per-link
-        work since the last rebalance -> link times -> node weights -> a new
-        partition; the state migrates exactly.  Needs FLAG_LINK_WORK.
-        Returns (new domain_of_node, per-domain ms of the window)."""
+        / per-node work since the last rebalance (ts_busy_time, ts_get_load)
+        -> link and node times (ts_load_times) -> node weights and a new
+        partition (ts_rebalance); the state migrates exactly.  Needs
+        FLAG_LINK_WORK.  Returns (new domain_of_node, per-domain ms of the
+        window)."""
         ms = [s.busy_time() for s in self.sims]
-        lw = [s.link_work() for s in self.sims]
-        base = getattr(self, "_lw_base", None)
-        win = [w - b for w, b in zip(lw, base)] if base is not None and len(base) == len(lw) else lw
-        w = rebalance_weights(self.scn, win, ms)
-        dom = partition(self.scn, self.k, w, method=method)
+        loads = [s.load_stats() for s in self.sims]
+        base = getattr(self, "_load_base", None)
+        win = ([(lw - bl, nw - bn) for (lw, nw), (bl, bn) in zip(loads, base)]
+               if base is not None and len(base) == len(loads) else loads)
+        lt, nt = load_times(win, ms, self.scn.n_nodes)
+        dom, _ = _t.rebalance(self.scn, self.k, lt, nt, method=method)
         self.repartition(dom)
-        self._lw_base = [s.link_work() for s in self.sims]
+        self._load_base = [s.load_stats() for s in self.sims]
         for s in self.sims:  # the migration's own work is not step time
             s.busy_time()
         return dom, ms
@@ -307,6 +315,12 @@ class DistDomain:
         self.recvs = [torch.as_tensor(_CudaBuf(rp + off * sb, n * sb), device=cuda)
                       for _, n, off in self.plan]
         self.stream = torch.cuda.ExternalStream(self.sim.stream(), device=cuda)
+        # a backend without device tensors (gloo) exchanges host copies of
+        # the packed strips
+        self.host_staging = dist.get_backend(group) != "nccl"
+        if self.host_staging:
+            self.hsends = [torch.empty(t.numel(), dtype=torch.uint8).pin_memory() for t in self.sends]
+            self.hrecvs = [torch.empty(t.numel(), dtype=torch.uint8).pin_memory() for t in self.recvs]
         self.exchange_ms = 0.0
         self.native = False
         if native and group is None:
@@ -334,6 +348,17 @@ class DistDomain:
             self.sim.exchange()
             return
         import torch
+        if self.host_staging:  # device -> host, exchange, host -> device
+            with torch.cuda.stream(self.stream):
+                for h, d in zip(self.hsends, self.sends):
+                    h.copy_(d, non_blocking=True)
+            self.stream.synchronize()
+            exchange_p2p(self.hsends, self.hrecvs, self.peers, self.group)
+            with torch.cuda.stream(self.stream):
+                for d, h in zip(self.recvs, self.hrecvs):
+                    d.copy_(h, non_blocking=True)
+            self.stream.synchronize()
+            return
         with torch.cuda.stream(self.stream):
             exchange_p2p(self.sends, self.recvs, self.peers, self.group)
 
@@ -365,22 +390,22 @@ class DistDomain:
         import torch
         import torch.distributed as dist
         ms = self.sim.busy_time()
-        lw = self.sim.link_work().astype(np.float64)
-        base = getattr(self, "_lw_base", None)
-        win = lw - base if base is not None else lw
-        lt_me = ms * win / win.sum() if win.sum() > 0 else np.zeros_like(win)
+        lw, nw = self.sim.load_stats()
+        base = getattr(self, "_load_base", None)
+        if base is not None:
+            lw, nw = lw - base[0], nw - base[1]
+        lt_me, nt_me = _t.load_times(ms, lw, nw)
         dev = (torch.device("cuda", self.dev) if dist.get_backend(self.group) == "nccl"
                else torch.device("cpu"))
-        lt = torch.as_tensor(lt_me, dtype=torch.float64, device=dev)
-        dist.all_reduce(lt, op=dist.ReduceOp.SUM, group=self.group)
-        lt = lt.cpu().numpy()
-        static = link_cells(self.scn) * np.asarray(self.scn.link_lanes, np.float64)
-        w = node_weights(self.scn, lt + 1e-3 * static / static.sum() * max(lt.sum(), 1e-12))
-        dom = partition(self.scn, self.k, w, method=method)
+        both = torch.as_tensor(np.concatenate([lt_me, nt_me]), dtype=torch.float64, device=dev)
+        dist.all_reduce(both, op=dist.ReduceOp.SUM, group=self.group)
+        both = both.cpu().numpy()
+        lt, nt = both[:lw.size], both[lw.size:]
+        dom, _ = _t.rebalance(self.scn, self.k, lt, nt, method=method)
         t, state = self.t, self.vehicles()
         self.sim.close()
         self.__init__(self.scn, dom, device=self.dev, t0=t, flags=self.flags, group=self.group,
                       state=state, native=self.native, **self.kw)
-        self._lw_base = self.sim.link_work().astype(np.float64)
+        self._load_base = self.sim.load_stats()
         self.sim.busy_time()
         return dom

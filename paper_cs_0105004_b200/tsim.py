@@ -63,6 +63,10 @@ def load_library():
         "ts_get_totals": (ctypes.c_int, [P, P]),
         "ts_read_flow": (ctypes.c_int, [P, I32, I32, P]),
         "ts_get_link_work": (ctypes.c_int, [P, P]),
+        "ts_get_load": (ctypes.c_int, [P, P, P]),
+        "ts_load_times": (ctypes.c_int, [ctypes.c_double, I32, P, I32, P, P, P]),
+        "ts_rebalance": (ctypes.c_int, [I32, P, P, I32, P, P, P, P, P, P, I32, I32,
+                                        ctypes.c_double, ctypes.c_uint64, P, P]),
         "ts_orb_partition": (ctypes.c_int, [I32, P, P, P, I32, P]),
         "ts_multilevel_partition": (ctypes.c_int, [I32, P, P, I32, P, P, P, P, I32,
                                                    ctypes.c_double, ctypes.c_uint64, P]),
@@ -143,6 +147,44 @@ def multilevel_partition(scn, k, weight=None, imbalance=0.05, seed=1):
     if rc:
         raise TsError(f"ts_multilevel_partition failed ({rc})")
     return out
+
+
+def load_times(domain_ms, link_work, node_work=None, link_time=None, node_time=None):
+    """one domain's measured time apportioned to its links and nodes by
+    their work (ts_load_times); adds into (and returns)
+    link_time / node_time"""
+    lib = load_library()
+    lw = _a(link_work, np.int64)
+    nw = None if node_work is None else _a(node_work, np.int64)
+    lt = np.zeros(lw.size, np.float64) if link_time is None else link_time
+    nt = (np.zeros(0 if nw is None else nw.size, np.float64) if node_time is None else node_time)
+    assert lt.dtype == np.float64 and lt.flags.c_contiguous and nt.dtype == np.float64
+    rc = lib.ts_load_times(float(domain_ms), lw.size, _p(lw), 0 if nw is None else nw.size, _p(nw),
+                           _p(lt), _p(nt) if nw is not None else None)
+    if rc:
+        raise TsError(f"ts_load_times failed ({rc})")
+    return lt, nt
+
+
+def rebalance(scn, k, link_time, node_time=None, method="orb", imbalance=0.05, seed=1):
+    """the next partition from measured link / node times (ts_rebalance,
+    PAPER.md:726-735) -> (domain_of_node, node weights)"""
+    lib = load_library()
+    i32 = lambda a: _a(a, np.int32)  # noqa: E731
+    x, y = _a(scn.node_x, np.int64), _a(scn.node_y, np.int64)
+    fr, to, la = i32(scn.link_from), i32(scn.link_to), i32(scn.link_lanes)
+    ln = _a(scn.link_len_mm, np.int64)
+    lt = _a(link_time, np.float64)
+    nt = None if node_time is None or len(node_time) == 0 else _a(node_time, np.float64)
+    w = np.zeros(x.size, np.float64)
+    dom = np.zeros(x.size, np.int32)
+    rc = lib.ts_rebalance(x.size, x.ctypes.data, y.ctypes.data, fr.size, fr.ctypes.data,
+                          to.ctypes.data, la.ctypes.data, ln.ctypes.data, lt.ctypes.data, _p(nt),
+                          int(k), {"orb": 0, "multilevel": 1}[method], float(imbalance), int(seed),
+                          w.ctypes.data, dom.ctypes.data)
+    if rc:
+        raise TsError(f"ts_rebalance failed ({rc})")
+    return dom, w
 
 
 def strip_bytes():
@@ -429,6 +471,14 @@ class Sim:
         out = np.zeros(self.n_links, np.int64)
         self._check(self.lib.ts_get_link_work(self.h, out.ctypes.data))
         return out
+
+    def load_stats(self):
+        """accumulated load statistics (ts_get_load): (vehicle updates per
+        link, node units per node)"""
+        lw = np.zeros(self.n_links, np.int64)
+        nw = np.zeros(self._n_nodes, np.int64)
+        self._check(self.lib.ts_get_load(self.h, lw.ctypes.data, nw.ctypes.data))
+        return lw, nw
 
     def last_exchange_timing(self):
         """(total ms, count) of the timed native exchanges of the last ts_step"""

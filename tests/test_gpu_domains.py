@@ -190,3 +190,31 @@ def test_ts_partition_matches_orb():
     assert np.array_equal(dom, domains.partition(s, 4))
     g.init(0)
     assert len(g.exchange_plan()) >= 1
+
+
+def test_load_statistics_links_and_nodes():
+    """ts_get_load ("the execution time of each link and
+    each intersection"): per-link vehicle updates sum to the vehicle updates
+    of the run; per-node work (lanes in range + crossings) covers every
+    crossing, is zero at nodes without incoming traffic, and the warp node
+    kernel and the thread-per-node kernel count identically; a k-domain
+    partition's loads add up to the undivided run's"""
+    s = scenarios.config("1")
+    flags = FUSED | tsim.FLAG_LINK_WORK
+    a = tsim.Sim.from_scenario(s, flags=flags)
+    b = tsim.Sim.from_scenario(s, flags=flags | 32)  # TS_FLAG_NODE_GENERAL: k_node
+    a.step(150)
+    b.step(150)
+    lw, nw = a.load_stats()
+    lw2, nw2 = b.load_stats()
+    assert np.array_equal(lw, lw2) and np.array_equal(nw, nw2)
+    h = a.history(0, 150)
+    assert lw.sum() == a.totals()["vehicle_updates"] == int(np.sum(h["active"]))
+    assert nw.sum() >= int(np.sum(a.history(1, 150)["crossings"])) > 0
+    indeg = np.bincount(np.asarray(s.link_to), minlength=s.n_nodes)
+    assert np.all(nw[indeg == 0] == 0)
+    d = domains.LocalDomains(s, 4, flags=flags)
+    d.step(150)
+    parts = [x.load_stats() for x in d.sims]
+    assert np.array_equal(sum(p[0] for p in parts), lw)
+    assert np.array_equal(sum(p[1] for p in parts), nw)

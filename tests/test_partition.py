@@ -85,3 +85,52 @@ def test_rebalance_weights_follow_measured_time():
     # the domain holding the slow (left) side now has fewer than half the nodes
     slow = new[int(np.argmin(np.asarray(scn.node_x)))]
     assert np.bincount(new, minlength=2)[slow] < scn.n_nodes // 2
+
+
+def test_load_times_apportions_domain_time():
+    """ts_load_times: a domain's time is split over its
+    links and nodes in proportion to their work; the parts sum to the
+    domain's time; domains accumulate into one pair of arrays; an idle
+    domain adds nothing; negative inputs are rejected"""
+    lw = np.array([0, 10, 30, 0, 60], np.int64)
+    nw = np.array([0, 50, 50], np.int64)
+    lt, nt = tsim.load_times(4.0, lw, nw)
+    assert lt.sum() + nt.sum() == pytest.approx(4.0)
+    assert lt == pytest.approx(4.0 * lw / 200.0) and nt == pytest.approx(4.0 * nw / 200.0)
+    tsim.load_times(2.0, np.array([1, 0, 0, 0, 1], np.int64), np.zeros(3, np.int64), lt, nt)
+    assert lt[0] == pytest.approx(1.0) and lt[4] == pytest.approx(1.2 + 1.0)
+    before = lt.copy()
+    tsim.load_times(7.0, np.zeros(5, np.int64), np.zeros(3, np.int64), lt, nt)
+    assert np.array_equal(before, lt)
+    with pytest.raises(tsim.TsError):
+        tsim.load_times(1.0, np.array([-1, 2], np.int64))
+    with pytest.raises(tsim.TsError):
+        tsim.load_times(-1.0, np.array([1, 2], np.int64))
+
+
+def test_rebalance_weights_closed_form():
+    """ts_rebalance: node weight = own time + half of every attached link's
+    time (+ the floor 1e-3 x total x static share of links), then ORB --
+    the same partition as ts_orb_partition of those weights; multilevel is a
+    valid k-way partition; bad inputs are rejected"""
+    scn = scenarios.config("1")
+    rng = np.random.default_rng(3)
+    lt = rng.uniform(0, 2, scn.n_links)
+    lt[rng.random(scn.n_links) < 0.3] = 0.0
+    nt = rng.uniform(0, 0.5, scn.n_nodes)
+    dom, w = tsim.rebalance(scn, 4, lt, nt)
+    cells = (np.asarray(scn.link_len_mm) + 3750) // 7500
+    stat = cells * np.asarray(scn.link_lanes, np.float64)
+    fl = 1e-3 * lt.sum() / stat.sum()
+    ref = 1e-9 + nt.copy()
+    for j in range(scn.n_links):
+        ref[scn.link_from[j]] += 0.5 * (lt[j] + fl * stat[j])
+        ref[scn.link_to[j]] += 0.5 * (lt[j] + fl * stat[j])
+    assert w == pytest.approx(ref, rel=1e-12)
+    assert np.array_equal(dom, tsim.orb_partition(scn.node_x, scn.node_y, 4, ref))
+    dm, _ = tsim.rebalance(scn, 4, lt, nt, method="multilevel")
+    assert set(dm.tolist()) == {0, 1, 2, 3}
+    with pytest.raises(tsim.TsError):
+        tsim.rebalance(scn, scn.n_nodes + 1, lt)
+    with pytest.raises(tsim.TsError):
+        tsim.rebalance(scn, 2, -lt - 1.0)
