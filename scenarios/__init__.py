@@ -544,3 +544,91 @@ def config(name: str, **kw) -> Scenario:
     if name == "5":
         return portland_tiled(**kw)
     raise KeyError(name)
+
+
+def stop_sign_merges(headways=(0, 12, 8, 6, 4, 3, 2, -1), copies=64, steps=2400, n_minor=1500,
+                     seed=1, name="fig4c_stop_sign_merge"):
+    """Fig. 4c (PAPER.md:517-518, "merge flows through a stop sign"; SPEC.md
+    merge_capacity): independent T-junctions, `copies` per priority-flow
+    level.  Each: a 2-lane major road A -> J -> B (class 1, 40 cells each)
+    and a 1-lane stop-controlled minor approach M -> J (class 0, 40 cells)
+    whose right turn merges onto J -> B.  The minor approach holds a
+    saturated queue (n_minor trips departing at t = 0 at its entry cell,
+    retrying injection every step).  Major flow level h > 0: one major trip
+    every h s (offset per copy) at the start of A -> J; h = 0: no major
+    traffic; h = -1: the major road is bumper-to-bumper -- every cell of
+    A -> J, J -> B and B -> C occupied at t = 0 by vehicles routed through
+    node C, whose signal is never green (reading R23), so nothing on it ever
+    moves.  Returns the scenario; the minor trips of copy c of level i are
+    vids [minor_base[i][c], + n_minor)."""
+    rng = np.random.default_rng(seed)
+    cell = 7500
+    nx, ny, frm, to, ln, la, cls = [], [], [], [], [], [], []
+    routes, dep, ent = [], [], []
+    pv, pl, pc, pvv = [], [], [], []
+    sig_nodes = []
+    minor_base = []
+    meta = []
+    for i, h in enumerate(headways):
+        mb = []
+        for c in range(copies):
+            x0, y0 = c * 200 * cell, i * 200 * cell
+            b = len(nx)
+            # A, J, B, M, C, D
+            for (x, y) in ((0, 0), (40, 0), (80, 0), (40, -40), (120, 0), (130, 0)):
+                nx.append(x0 + x * cell)
+                ny.append(y0 + y * cell)
+            A, J, B, Mn, C, D = range(b, b + 6)
+            k = len(frm)
+            for (u, v, n, L, cl) in ((A, J, 40, 2, 1), (J, B, 40, 2, 1), (Mn, J, 40, 1, 0),
+                                     (B, C, 40, 2, 1), (C, D, 10, 2, 1)):
+                frm.append(u)
+                to.append(v)
+                ln.append(n * cell)
+                la.append(L)
+                cls.append(cl)
+            kAJ, kJB, kMJ, kBC, kCD = range(k, k + 5)
+            mb.append(len(routes))
+            for _ in range(n_minor):  # the saturated stop-controlled queue
+                routes.append([kMJ, kJB])
+                dep.append(0)
+                ent.append(0)
+            if h > 0:
+                off = int(rng.integers(0, h))
+                for t in range(off, steps, h):
+                    routes.append([kAJ, kJB])
+                    dep.append(t)
+                    ent.append(0)
+            elif h < 0:  # jammed major road behind a never-green signal at C
+                sig_nodes.append(C)
+                for kk in (kAJ, kJB, kBC):
+                    for lane in range(2):
+                        for x in range(40):
+                            pv.append(len(routes))
+                            routes.append([kk, kCD] if kk == kBC else
+                                          ([kJB, kBC, kCD] if kk == kJB else [kAJ, kJB, kBC, kCD]))
+                            dep.append(0)
+                            ent.append(x)
+                            pl.append(lane)
+                            pc.append(x)
+                            pvv.append(0)
+        minor_base.append(mb)
+        meta.append(h)
+    off = np.zeros(len(routes) + 1, np.int64)
+    off[1:] = np.cumsum([len(r) for r in routes])
+    s = Scenario(name=name, node_x=_i64(nx), node_y=_i64(ny), link_from=_i32(frm), link_to=_i32(to),
+                 link_len_mm=_i64(ln), link_lanes=_i32(la), link_vmax=_i32([5] * len(frm)),
+                 link_class=_i32(cls), periodic_link=-1, route_off=off,
+                 route=_i32([k for r in routes for k in r]), depart=_i32(dep), entry=_i32(ent),
+                 place_vid=_i32(pv), place_lane=_i32(pl), place_cell=_i32(pc), place_v=_i32(pvv),
+                 steps=steps, recipe=f"{copies} T-junctions per major headway {list(headways)}")
+    if sig_nodes:
+        n = len(sig_nodes)
+        s.sig_node = _i32(sig_nodes)
+        s.sig_g0 = _i32([0] * n)   # phase 0 (the maximal class: the only approach) never green
+        s.sig_g1 = _i32([1] * n)
+        s.sig_off = _i32([0] * n)
+    s.minor_base = minor_base
+    s.n_minor = n_minor
+    s.headways = list(meta)
+    return s
