@@ -50,7 +50,7 @@ typedef struct {
   double p_slow;          /* random-slowdown probability, PAPER.md:334-335 (R3) */
   uint64_t seed;          /* Philox key = (seed & 0xffffffff, seed >> 32) (R3) */
   int32_t gap_accept_G;   /* unprotected-turn gap, cells (R9), <= 5 */
-  int32_t desperation_D;  /* lane-change desperation distance, cells (R6) */
+  int32_t desperation_D;  /* lane-change desperation distance, cells (R6), 1..4096 */
   uint32_t flags;         /* TS_FLAG_* */
   int32_t device;         /* CUDA device ordinal */
   int32_t tile_cells;     /* max cells per lane in one tile (0 = default) */

@@ -124,7 +124,8 @@ int ts_create(const ts_config *cfg, ts_sim **out) {
   if (!(cfg->p_slow >= 0.0 && cfg->p_slow <= 1.0)) return fail(nullptr, TS_EINVAL, "p_slow not in [0,1]");
   if (cfg->gap_accept_G < 0 || cfg->gap_accept_G > kGmax)
     return fail(nullptr, TS_EINVAL, "gap_accept_G must be in [0, 5]");
-  if (cfg->desperation_D < 1) return fail(nullptr, TS_EINVAL, "desperation_D must be >= 1");
+  if (cfg->desperation_D < 1 || cfg->desperation_D > 4096)
+    return fail(nullptr, TS_EINVAL, "desperation_D must be in [1, 4096]");
   int ndev = 0;
   cudaError_t e = cudaGetDeviceCount(&ndev);
   if (e != cudaSuccess || ndev == 0)
@@ -903,8 +904,13 @@ StepParams step_params(ts_sim *h, int t, int mode) {
   P.t = t;
   P.mode = mode;
   P.D = h->cfg.desperation_D;
+  P.Dmul = (uint32_t)((0x100000000ull + (uint64_t)P.D - 1) / (uint64_t)P.D);
   P.k0 = (uint32_t)(h->cfg.seed & 0xffffffffu);
   P.k1 = (uint32_t)(h->cfg.seed >> 32);
+  for (int r = 0; r < 10; r++) {  // Philox4x32-10 key schedule (curand's Weyl constants)
+    P.rk[2 * r] = P.k0 + (uint32_t)r * 0x9E3779B9u;
+    P.rk[2 * r + 1] = P.k1 + (uint32_t)r * 0xBB67AE85u;
+  }
   P.p32 = h->p32;
   P.lay = h->lay;
   P.code_in = h->d_code[h->gcur];

@@ -72,6 +72,25 @@ static __device__ __forceinline__ uint32_t philox_w0(uint32_t t, uint32_t vid, u
   return c0;
 }
 
+// The same with the key schedule precomputed per launch (rk[2 r] / rk[2 r
+// + 1] = round-r keys, kernel parameters): the round keys are operands from
+// the constant bank instead of per-draw additions in registers.
+static __device__ __forceinline__ uint32_t philox_w0_rk(uint32_t t, uint32_t vid,
+                                                        const uint32_t (&rk)[20]) {
+  uint32_t c0 = t, c1 = vid, c2 = 0u, c3 = 0u;
+#pragma unroll
+  for (int r = 0; r < 10; r++) {
+    const uint32_t lo0 = 0xD2511F53u * c0, hi0 = __umulhi(0xD2511F53u, c0);
+    const uint32_t lo1 = 0xCD9E8D57u * c2, hi1 = __umulhi(0xCD9E8D57u, c2);
+    const uint32_t n0 = hi1 ^ c1 ^ rk[2 * r], n2 = hi0 ^ c3 ^ rk[2 * r + 1];
+    c0 = n0;
+    c1 = lo1;
+    c2 = n2;
+    c3 = lo0;
+  }
+  return c0;
+}
+
 // NaSch velocity update (PAPER.md:330-335 rules (i)-(iii); R15):
 // accelerate, clamp to the gap, random slowdown (draw skipped when v2 = 0,
 // which cannot change the result).

@@ -124,6 +124,10 @@ static_assert(sizeof(RowDesc) == 16, "RowDesc must be 16 bytes");
 // during the draws, the masks and list offsets of the rows the lane change
 // touched during the list rebuild
 constexpr int kRowsAuxWords = 4 * 32 * kRowWords + 5 * 32 + 4 + 64;
+// splice path of the vid lists: per row up to kSpliceMax leavers and
+// arrivals (3 words each) in the aux area
+constexpr int kSpliceMax = 6;
+static_assert(32 * 3 * kSpliceMax <= kRowsAuxWords, "splice events exceed the aux area");
 #ifndef TS_ROWS_PPF
 #define TS_ROWS_PPF 0  // prefetch the next group's planes into shared memory
 #endif
@@ -198,7 +202,9 @@ struct StepParams {
   const int32_t *tdev;  // CUDA-graph replay: t = *tdev + t (NULL: t as is)
   int32_t mode;
   int32_t D;
+  uint32_t Dmul;  // ceil(2^32 / D): floor(x / D) = umulhi(x, Dmul) for x < 2^32 / D
   uint32_t k0, k1;
+  uint32_t rk[20];  // Philox round keys (k0 + r W0, k1 + r W1), r = 0..9
   uint64_t p32;
   WarpLayout lay;
   // state (in / out buffers)

@@ -182,6 +182,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
       : "memory");
 }
 
+// bitwise OR into a shared-memory word (no return value)
+__device__ __forceinline__ void red_or_shared(uint32_t saddr, uint32_t v) {
+  asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(saddr), "r"(v) : "memory");
+}
 // the bulk stores of this thread have finished reading shared memory
 __device__ __forceinline__ void bulk_wait_read() {
   asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
@@ -225,7 +229,7 @@ static __device__ __noinline__ uint64_t hash_row(RowWords oo, RowWords v0, RowWo
 // floor(V d/D)); evaluated per candidate (rare, kept out of line).  zc:
 // candidates of the word starting at cell c0; tg1..tg5: target-lane gap
 // ahead >= k; tp, t0: target-lane occupancy of the previous / this word.
-static __device__ __noinline__ uint32_t zone_lc(uint32_t zc, int c0, int w, int vk, int D,
+static __device__ __noinline__ uint32_t zone_lc(uint32_t zc, int c0, int w, int vk, uint32_t Dmul,
                                                 uint32_t v0, uint32_t v1, uint32_t v2,
                                                 uint32_t tg1, uint32_t tg2, uint32_t tg3,
                                                 uint32_t tg4, uint32_t tg5, uint32_t tp,
@@ -236,7 +240,9 @@ static __device__ __noinline__ uint32_t zone_lc(uint32_t zc, int c0, int w, int 
     zc &= zc - 1u;
     const int d = w - 1 - (c0 + x);
     const int v = (int)((v0 >> x) & 1u) | (int)(((v1 >> x) & 1u) << 1) | (int)(((v2 >> x) & 1u) << 2);
-    const int rf = (min(v + 1, vk) * d) / D, rb = (vk * d) / D;
+    // floor(x / D) = umulhi(x, ceil(2^32 / D)) for x < 2^32 / D (x <= 5 d < 5 D)
+    const int rf = (int)__umulhi((uint32_t)(min(v + 1, vk) * d), Dmul),
+              rb = (int)__umulhi((uint32_t)(vk * d), Dmul);
     // ahead >= rf: tg_rf at x; behind >= rb: target cells x-1..x-rb empty,
     // cells before the row start count as empty
     const uint32_t tg = rf <= 0 ? FULL : rf == 1 ? tg1 : rf == 2 ? tg2 : rf == 3 ? tg3
@@ -474,12 +480,28 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
         uint32_t *bw = reinterpret_cast<uint32_t *>(s_out + R.cap);
 #pragma unroll
         for (int i = 0; i < NW; i++) bw[lane * NW + i] = 0u;  // this row's brake bits
-        auto draw = [&](int n) {  // the draws of list entries [0, n)
-          for (int jj = lane; jj < n; jj += 32) {
-            const int me = mlist[jj];
-            const uint32_t e = (uint32_t)vbase[me >> 12];
-            if ((uint64_t)philox_w0((uint32_t)P.t, e & kVidMask, P.k0, P.k1) < P.p32)
-              atomicOr(bw + ((me >> 7) & 31) * NW + ((me >> 5) & 3), 1u << (me & 31));
+        // the draws of list entries [0, n): the vid from the staged block
+        // (shared memory) or the global one; brake bit by a shared-memory
+        // reduction at word (row slot * NW + word) = (entry >> 5) & 127
+        const uint32_t bw_s = (uint32_t)__cvta_generic_to_shared(bw);
+        // brake iff u < p32, i.e. u <= p32 - 1 (p32 in [1, 2^32]; p32 = 0 draws nothing)
+        const uint32_t p32m1 = (uint32_t)(P.p32 - 1);
+        auto draw = [&](int n) {
+          if (P.p32 == 0) return;
+          if (staged) {
+            for (int jj = lane; jj < n; jj += 32) {
+              const uint32_t me = (uint32_t)mlist[jj];
+              const uint32_t e = (uint32_t)s_in[me >> 12];
+              if (philox_w0_rk((uint32_t)P.t, e & kVidMask, P_.rk) <= p32m1)
+                red_or_shared(bw_s + (((me >> 5) & 127u) << 2), 1u << (me & 31u));
+            }
+          } else {
+            for (int jj = lane; jj < n; jj += 32) {
+              const uint32_t me = (uint32_t)mlist[jj];
+              const uint32_t e = (uint32_t)vbase[me >> 12];
+              if (philox_w0_rk((uint32_t)P.t, e & kVidMask, P_.rk) <= p32m1)
+                red_or_shared(bw_s + (((me >> 5) & 127u) << 2), 1u << (me & 31u));
+            }
           }
         };
         if (mtot <= R.cap) {  // one chunk (the common case): no bounds checks
@@ -716,7 +738,7 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
             lv |= turn & ~ZN & req & BKv;
             const uint32_t zc = turn & ZN;  // scaled thresholds (R6): per candidate
             if (zc)
-              lv |= zone_lc(zc, 32 * i, w, vk, P.D, OV0[i], OV1[i], OV2[i], TG[1], TG[2], TG[3],
+              lv |= zone_lc(zc, 32 * i, w, vk, P.Dmul, OV0[i], OV1[i], OV2[i], TG[1], TG[2], TG[3],
                             TG[4], TG[5], tp, T0[i]);
           }
           LV[i] = lv;
@@ -769,8 +791,9 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
     const bool moved_lc = any_row(LV) || any_row(AR);
     // the state hash (tests) is taken below for every row, so hashed runs
     // take exactly the vid-list paths of the unhashed (benchmarked) runs
-    const bool general = moved_lc || injected;
-    if (!general && nfin > 0) {
+    const bool changed = moved_lc || injected;
+    const bool ginj = __any_sync(FULL, injected);
+    if (!changed && nfin > 0) {
       // input vehicles minus an exit at the front (a prefix of the input
       // list), shifted by one when the entrant lands behind every vehicle
       const int sh = has_ent ? 1 : 0;
@@ -786,6 +809,67 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
       }
       for (; i < nfin; i++) vout[i] = vin[i - sh];
     }
+    // rows whose set changed by lane changes only (no injection in the
+    // warp): the own list with its leavers (LV) skipped and the arrivals
+    // (AR, from row l - dir) spliced in -- a few segment copies per row
+    bool spliced = false;
+    if (!ginj && __any_sync(FULL, changed)) {
+      uint32_t sOO[NW];  // the arrivals' source row (l - dir) before its lane change
+#pragma unroll
+      for (int i = 0; i < NW; i++) sOO[i] = shfl_w(OO[i], lane - dir);
+      const int s_in_off = __shfl_sync(FULL, in_off, lane - dir);
+      const int s_ent_y = __shfl_sync(FULL, ent_y, lane - dir);
+      const uint32_t s_ent_e = __shfl_sync(FULL, ent_e, lane - dir);
+      const bool fits = popc_row(LV) <= kSpliceMax && popc_row(AR) <= kSpliceMax;
+      if (__all_sync(FULL, fits)) {
+        spliced = true;
+        if (changed) {
+          const int32_t *vb = staged ? (const int32_t *)s_in : R.vid_in + voff;
+          int32_t *ev = s_out + R.cap + lane * (3 * kSpliceMax);  // aux area: this row's events
+          int32_t *Lr = ev, *Ao = ev + kSpliceMax, *Ae = ev + 2 * kSpliceMax;
+          int nl = 0, na = 0, po = 0, pf = 0, ps = 0;
+#pragma unroll
+          for (int i = 0; i < NW; i++) {
+            uint32_t m = LV[i];
+            while (m) {  // leavers: their rank in the own list (increasing)
+              const uint32_t below = (m & (0u - m)) - 1u;
+              m &= m - 1u;
+              Lr[nl++] = po + __popc(OO[i] & below);
+            }
+            uint32_t a = AR[i];
+            while (a) {  // arrivals: output rank and list entry
+              const uint32_t below = (a & (0u - a)) - 1u;
+              a &= a - 1u;
+              const int c = 32 * i + __popc(below);
+              Ao[na] = pf + __popc(FO[i] & below);
+              const int q = ps + __popc(sOO[i] & below);
+              Ae[na++] = c == s_ent_y ? (int32_t)s_ent_e
+                                      : vb[s_in_off + q - (s_ent_y >= 0 ? 1 : 0)];
+            }
+            po += __popc(OO[i]);
+            pf += __popc(FO[i]);
+            ps += __popc(sOO[i]);
+          }
+          // own list entry k: the entrant (lowest cell) first, then the input
+          // list (its exited front is past the end)
+          const int sh = has_ent ? 1 : 0;
+          int j = 0, k = 0, il = 0, ia = 0;
+          while (j < nfin) {
+            const int jl = il < nl ? j + (Lr[il] - k) : 0x7fffffff;
+            const int ja = ia < na ? Ao[ia] : 0x7fffffff;
+            const int stop = min(min(jl, ja), nfin);
+            for (; j < stop; j++, k++) vout[j] = (k < sh) ? (int32_t)ent_e : vin[k - sh];
+            if (j == jl && jl <= ja) {
+              k++;
+              il++;
+            } else if (j == ja) {
+              vout[j++] = Ae[ia++];
+            }
+          }
+        }
+      }
+    }
+    const bool general = changed && !spliced;
     if (const uint32_t gmask = __ballot_sync(FULL, general)) {
       // rows whose vehicle set changed inside (lane changes, injections):
       // every vehicle of S(t+1) before the lane change goes to its rank in
@@ -800,7 +884,6 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
       // per row: popcount prefixes of the OO / FO words (bytes 1..3: words 0,
       // 0-1, 0-2), so an item finds its word and its rank without loops
       uint32_t *pOO = reinterpret_cast<uint32_t *>(mItem + 36), *pFO = pOO + 32;
-      const bool ginj = __any_sync(FULL, injected);
       {
         uint32_t po = 0u, pf = 0u;
         int so = 0, sf = 0;

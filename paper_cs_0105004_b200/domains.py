@@ -318,9 +318,9 @@ class DistDomain:
         # a backend without device tensors (gloo) exchanges host copies of
         # the packed strips
         self.host_staging = dist.get_backend(group) != "nccl"
-        if self.host_staging:
-            self.hsends = [torch.empty(t.numel(), dtype=torch.uint8).pin_memory() for t in self.sends]
-            self.hrecvs = [torch.empty(t.numel(), dtype=torch.uint8).pin_memory() for t in self.recvs]
+        if self.host_staging:  # pageable: no host-allocator events on the library's stream
+            self.hsends = [torch.empty(t.numel(), dtype=torch.uint8) for t in self.sends]
+            self.hrecvs = [torch.empty(t.numel(), dtype=torch.uint8) for t in self.recvs]
         self.exchange_ms = 0.0
         self.native = False
         if native and group is None:
@@ -351,12 +351,11 @@ class DistDomain:
         if self.host_staging:  # device -> host, exchange, host -> device
             with torch.cuda.stream(self.stream):
                 for h, d in zip(self.hsends, self.sends):
-                    h.copy_(d, non_blocking=True)
-            self.stream.synchronize()
+                    h.copy_(d)
             exchange_p2p(self.hsends, self.hrecvs, self.peers, self.group)
             with torch.cuda.stream(self.stream):
                 for d, h in zip(self.recvs, self.hrecvs):
-                    d.copy_(h, non_blocking=True)
+                    d.copy_(h)
             self.stream.synchronize()
             return
         with torch.cuda.stream(self.stream):
@@ -376,6 +375,15 @@ class DistDomain:
     @property
     def t(self):
         return self.sim.t
+
+    def close(self):
+        """drop the torch views of the library's buffers and stream, then the
+        handle (its stream and memory go away with it)"""
+        import torch
+        torch.cuda.synchronize(self.dev)
+        self.sends = self.recvs = self.hsends = self.hrecvs = []
+        self.stream = None
+        self.sim.close()
 
     def vehicles(self):
         """the merged state of all ranks (every rank gets it)"""
@@ -403,7 +411,7 @@ class DistDomain:
         lt, nt = both[:lw.size], both[lw.size:]
         dom, _ = _t.rebalance(self.scn, self.k, lt, nt, method=method)
         t, state = self.t, self.vehicles()
-        self.sim.close()
+        self.close()
         self.__init__(self.scn, dom, device=self.dev, t0=t, flags=self.flags, group=self.group,
                       state=state, native=self.native, **self.kw)
         self._load_base = self.sim.load_stats()

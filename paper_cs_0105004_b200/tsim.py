@@ -99,6 +99,8 @@ def load_library():
                                           ctypes.POINTER(ctypes.c_int64)]),
     }
     for name, (res, args) in sig.items():
+        if not hasattr(lib, name):  # an older in-tree variant (tools/variants.py)
+            continue
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args

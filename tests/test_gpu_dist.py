@@ -75,6 +75,7 @@ def _worker(rank, world, port, name, steps, q):
                 new = d.rebalance()
                 assert d.t == (o.t if rank == 0 else d.t)
                 assert new.shape == dom.shape
+        d.close()
         q.put((rank, "ok", checked))
     except Exception as e:  # pragma: no cover - reported to the parent
         import traceback
@@ -91,9 +92,19 @@ def test_two_processes_one_gpu(name, steps):
     ps = [ctx.Process(target=_worker, args=(r, 2, port, name, steps, q)) for r in range(2)]
     for p in ps:
         p.start()
-    res = [q.get(timeout=600) for _ in ps]
+    res = []
+    import queue
+    import time
+    t0 = time.time()
+    while len(res) < len(ps) and time.time() - t0 < 600:
+        try:
+            res.append(q.get(timeout=5))
+        except queue.Empty:  # a rank that died without reporting fails the test now
+            dead = [p.exitcode for p in ps if p.exitcode not in (None, 0)]
+            assert not dead, f"rank exited with {dead}"
     for p in ps:
         p.join(timeout=60)
+    assert len(res) == len(ps), "ranks did not report"
     for rank, msg, checked in res:
         assert msg == "ok", (rank, msg)
     assert max(c for _, _, c in res) == 2 * steps
