@@ -730,16 +730,19 @@ static bool build_tiles(ts_sim *h) {
 // incoming lanes of every node in priority order (R9: major class first,
 // then link id, then lane), packed into chunks of <= 32 lanes
 static bool build_node_lanes(ts_sim *h, std::vector<NodeLane> &lanes,
-                             std::vector<uint32_t> &sig, std::vector<int32_t> &nl_node) {
+                             std::vector<uint32_t> &sig, std::vector<int32_t> &nl_node,
+                             std::vector<int32_t> &nl_row, const std::vector<int32_t> &lane_row) {
   lanes.clear();
   sig.clear();
   nl_node.clear();
+  nl_row.clear();
   int in_chunk = 0;
   auto close_chunk = [&]() {  // pad the chunk to 32 entries
     while (lanes.size() % 32) {
       lanes.push_back(NodeLane{-1, 0, 0u, 0, 0, 1, 0});
       sig.push_back(0u);
       nl_node.push_back(-1);
+      nl_row.push_back(-1);
     }
     in_chunk = 0;
   };
@@ -763,6 +766,7 @@ static bool build_node_lanes(ts_sim *h, std::vector<NodeLane> &lanes,
                                    (uint8_t)(pass == 0), (uint8_t)h->vmax[j],
                                    (uint8_t)node_first});
           nl_node.push_back(nd);
+          nl_row.push_back(lane_row[h->lgid[j] + l]);
           uint32_t sw = 0u;  // the lane's phase (R23): 0 = maximal class, 1 = the rest
           const uint32_t s0 = h->node_sig.empty() ? 0u : h->node_sig[nd];
           if (s0 >> 31) {
@@ -794,16 +798,23 @@ static int setup_ring_nodes(ts_sim *h) {
     if (h->tiles[ti].flags & kRingSeg) seg.push_back((int)ti);
   const int S = (int)seg.size(), per_chunk = 32 / L;
   std::vector<NodeLane> nlanes;
+  std::vector<int32_t> nl_row;  // row slot per node-lane index
+  auto pad = [&]() {
+    while (nlanes.size() % 32) {
+      nlanes.push_back(NodeLane{-1, 0, 0u, 0, 0, 1, 0});
+      nl_row.push_back(-1);
+    }
+  };
   h->ring_nodeout.assign(S, NodeOut{});
   std::vector<int32_t> nxt(h->rows.size(), -1), prv(h->rows.size(), -1), ra(h->rows.size(), 0);
   for (int s = 0; s < S; s++) {
-    if (s % per_chunk == 0)
-      while (nlanes.size() % 32) nlanes.push_back(NodeLane{-1, 0, 0u, 0, 0, 1, 0});
+    if (s % per_chunk == 0) pad();
     const int first = (int)(nlanes.size() % 32);
     const TileDesc &d = h->tiles[seg[s]];
     const TileDesc &dn = h->tiles[seg[(s + 1) % S]], &dp = h->tiles[seg[(s + S - 1) % S]];
     for (int l = 0; l < L; l++) {
       const int row = h->tile_row[seg[s]] + l;
+      nl_row.push_back(row);
       RowDesc &r = h->rows[row];
       r.nli = (int32_t)nlanes.size();
       r.lg = s * L + l;  // node-out-lane index: segment s is the target of node s - 1
@@ -814,9 +825,10 @@ static int setup_ring_nodes(ts_sim *h) {
       nlanes.push_back(NodeLane{k, s, 0u, (uint8_t)l, (uint8_t)(1 | 2), (uint8_t)h->vmax[k],
                                 (uint8_t)first});
     }
-    h->ring_nodeout[s] = NodeOut{((s + 1) % S) * L, (int16_t)L, (int16_t)dn.w};
+    h->ring_nodeout[s] = NodeOut{((s + 1) % S) * L, (int16_t)L, (int16_t)dn.w,
+                                 h->tile_row[seg[(s + 1) % S]]};
   }
-  while (nlanes.size() % 32) nlanes.push_back(NodeLane{-1, 0, 0u, 0, 0, 1, 0});
+  pad();
   h->node_warp = true;
   h->nchunks = (int32_t)(nlanes.size() / 32);
   h->n_nli = (int64_t)nlanes.size() + 1;
@@ -826,19 +838,36 @@ static int setup_ring_nodes(ts_sim *h) {
   h->d_lane_sig = nullptr;
   int rc;
   if ((rc = upload(h, &h->d_nlanes, nlanes))) return rc;
+  if ((rc = upload(h, &h->d_nl_row, nl_row))) return rc;
   if ((rc = upload(h, &h->d_ring_next, nxt))) return rc;
   if ((rc = upload(h, &h->d_ring_prev, prv))) return rc;
   if ((rc = upload(h, &h->d_row_a, ra))) return rc;
   return 0;
 }
 
+// row slot of every global lane id (-1: not a row-kernel lane); the node
+// kernels write the grants and entrant records of these lanes by row slot too
+static std::vector<int32_t> lane_rows(const ts_sim *h) {
+  std::vector<int32_t> lr(std::max<int64_t>(h->nlanes, 1), -1);
+  if (h->ring_rows) return lr;  // ring segments: by node lane (setup_ring_nodes)
+  for (size_t ti = 0; ti < h->tiles.size(); ti++)
+    if (h->tile_row[ti] >= 0)
+      for (int l = 0; l < h->tiles[ti].L; l++) lr[h->tiles[ti].lane_gid + l] = h->tile_row[ti] + l;
+  return lr;
+}
+
 static int setup_node_lanes(ts_sim *h) {
+  int rc;
+  const std::vector<int32_t> lane_row = lane_rows(h);
+  if ((rc = upload(h, &h->d_lane_row, lane_row))) return rc;
+  h->lane_row0.resize(h->nl);
+  for (int k = 0; k < h->nl; k++) h->lane_row0[k] = lane_row[h->lgid[k]];
   if (h->ring_rows) return setup_ring_nodes(h);
   std::vector<NodeLane> nlanes;
   std::vector<uint32_t> lsig;
-  std::vector<int32_t> nl_node;
+  std::vector<int32_t> nl_node, nl_row;
   h->node_warp = h->periodic < 0 && !(h->cfg.flags & (TS_FLAG_GENERAL | TS_FLAG_NODE_GENERAL)) &&
-                 build_node_lanes(h, nlanes, lsig, nl_node);
+                 build_node_lanes(h, nlanes, lsig, nl_node, nl_row, lane_row);
   h->nli.assign(h->nlanes, 0);
   if (h->node_warp) {
     h->nchunks = (int32_t)(nlanes.size() / 32);
@@ -846,9 +875,9 @@ static int setup_node_lanes(ts_sim *h) {
     for (int32_t &x : h->nli) x = (int32_t)(h->n_nli - 1);
     for (size_t i = 0; i < nlanes.size(); i++)
       if (nlanes[i].lane_gid >= 0) h->nli[nlanes[i].lane_gid] = (int32_t)i;
-    int rc;
     if ((rc = upload(h, &h->d_nlanes, nlanes))) return rc;
     if ((rc = upload(h, &h->d_nl_node, nl_node))) return rc;
+    if ((rc = upload(h, &h->d_nl_row, nl_row))) return rc;
     if (h->node_sig.empty()) h->d_lane_sig = nullptr;
     else if ((rc = upload(h, &h->d_lane_sig, lsig))) return rc;
   } else {
@@ -939,6 +968,8 @@ StepParams step_params(ts_sim *h, int t, int mode) {
   P.head_occ = h->d_head;
   P.ext = h->d_ext;
   P.entr = h->d_entr;
+  P.ext_row = h->d_ext_row;
+  P.entr_row = h->d_entr_row;
   P.stats = h->d_stats;
   P.link_work = h->d_work;
   return P;
@@ -976,6 +1007,9 @@ static NodeParams node_params(ts_sim *h, int t) {
   N.head_occ = h->d_head;
   N.ext = h->d_ext;
   N.entr = h->d_entr;
+  N.ext_row = h->d_ext_row;
+  N.entr_row = h->d_entr_row;
+  N.lane_row = h->d_lane_row;
   N.stats = h->d_stats;
   N.node_work = (h->cfg.flags & TS_FLAG_LINK_WORK) && h->periodic < 0 ? h->d_node_work : nullptr;
   return N;
@@ -1002,12 +1036,14 @@ RowsParams rows_params(ts_sim *h) {
   return r;
 }
 
-// k_rows launch; the work counter advances by the groups plus one failed
-// fetch per warp
+// k_rows launch; the work counter advances by the groups: every warp takes
+// its first group by its index, then one fetch per further group and one
+// failed fetch (warps without a first group fetch nothing)
 static void rows_launch(ts_sim *h, const StepParams &p, bool pdl = false) {
   launch_rows(p, rows_params(h), h->rows_blocks, h->rows_threads, h->rows_smem, h->stream, pdl);
-  h->gctr_base += (unsigned long long)h->ngroups + (unsigned long long)h->rows_blocks *
-                                                        (h->rows_threads / 32);
+  h->gctr_base += (unsigned long long)h->ngroups +
+                  (TS_ROWS_FIRST_STATIC ? 0ull
+                                        : (unsigned long long)h->rows_blocks * (h->rows_threads / 32));
 }
 
 static int base_mode(const ts_sim *h) {
@@ -1343,7 +1379,7 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
     for (size_t i = 0; i < h->out_list.size(); i++) {
       const int k = h->out_list[i];
       nodeout[i] = NodeOut{h->nlo[h->lgid[k]], (int16_t)h->lanes[k],
-                           (int16_t)std::min(h->ncell[k], 32767)};
+                           (int16_t)std::min(h->ncell[k], 32767), h->lane_row0[k]};
     }
     if ((rc = upload(h, &h->d_nodeout, h->ring_rows ? h->ring_nodeout : nodeout))) return rc;
   }
@@ -1366,6 +1402,8 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
   if ((rc = dalloc(h, &h->d_entr, h->n_nlo, 0))) return rc;
   if ((rc = dalloc(h, &h->d_head, h->n_nlo, 0))) return rc;
   if ((rc = dalloc(h, &h->d_ext, h->n_nli, 0))) return rc;
+  if ((rc = dalloc(h, &h->d_ext_row, (size_t)h->ngroups * 32 + 1, 0))) return rc;
+  if ((rc = dalloc(h, &h->d_entr_row, (size_t)h->ngroups * 32 + 1, 0))) return rc;
   if ((rc = dalloc(h, &h->d_stats, (size_t)kHist * ST_N, 0))) return rc;
   if ((rc = dalloc(h, &h->d_work, h->nl, 0))) return rc;
   if ((rc = dalloc(h, &h->d_node_work, h->nn, 0))) return rc;
@@ -1496,7 +1534,8 @@ static void phase_move(ts_sim *h, bool more, cudaEvent_t e0, cudaEvent_t e1) {
   if (h->n_xs > 0) unpack_strips(h);
   if (h->node_warp)
     launch_node_warp(node_params(h, t),
-                     NodeWarpParams{h->d_lane_sig, h->d_nlanes, h->nchunks, h->d_nl_node}, h->stream,
+                     NodeWarpParams{h->d_lane_sig, h->d_nlanes, h->nchunks, h->d_nl_node,
+                                    h->d_nl_row}, h->stream,
                      h->pdl);
   else
     launch_node(node_params(h, t), h->stream);

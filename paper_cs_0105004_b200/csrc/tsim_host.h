@@ -183,6 +183,11 @@ struct ts_sim {
   unsigned long long *d_stats = nullptr, *d_work = nullptr, *d_hash = nullptr;
   unsigned long long *d_node_work = nullptr;  // per node (TS_FLAG_LINK_WORK)
   int32_t *d_nl_node = nullptr;               // node id per node-lane index
+  int32_t *d_nl_row = nullptr;                // row slot per node-lane index (or -1)
+  int32_t *d_lane_row = nullptr;              // row slot per global lane id (or -1)
+  uint8_t *d_ext_row = nullptr;               // node grants by row slot
+  uint64_t *d_entr_row = nullptr;             // entrant records by row slot
+  std::vector<int32_t> lane_row0;             // per link: row slot of its lane 0 (or -1)
   int32_t *d_in_off = nullptr, *d_in_list = nullptr, *d_out_off = nullptr, *d_out_list = nullptr;
   int32_t *d_ncell = nullptr, *d_lanes = nullptr, *d_lgid = nullptr, *d_cls = nullptr;
   int gcur = 0, rcur = 0;  // current buffer of the general / row state

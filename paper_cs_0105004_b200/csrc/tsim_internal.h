@@ -124,14 +124,15 @@ static_assert(sizeof(RowDesc) == 16, "RowDesc must be 16 bytes");
 // during the draws, the masks and list offsets of the rows the lane change
 // touched during the list rebuild
 constexpr int kRowsAuxWords = 4 * 32 * kRowWords + 5 * 32 + 4 + 64;
-// splice path of the vid lists: per row up to kSpliceMax leavers and
-// arrivals (3 words each) in the aux area
-constexpr int kSpliceMax = 6;
-static_assert(32 * 3 * kSpliceMax <= kRowsAuxWords, "splice events exceed the aux area");
 #ifndef TS_ROWS_PPF
 #define TS_ROWS_PPF 0  // prefetch the next group's planes into shared memory
 #endif
 constexpr int kRowsPlaneWords = TS_ROWS_PPF ? kStatePlanes * kRowWords * 32 : 0;
+#ifndef TS_ROWS_FIRST_STATIC
+#define TS_ROWS_FIRST_STATIC 1  // k_rows: a warp's first group is its index (no atomic)
+#endif
+// per warp: vid block in, vid block out (cap entries each), the aux area,
+// the plane prefetch buffer (TS_ROWS_PPF)
 __host__ __device__ inline int rows_stage_words(int cap) {
   return 2 * cap + kRowsAuxWords + kRowsPlaneWords;  // cap % 4 == 0: 16-byte aligned
 }
@@ -157,6 +158,7 @@ struct NodeOut {
   int32_t lgid;  // node-out-lane index of its lane 0 (head occupancy, entrant record)
   int16_t L;     // lanes
   int16_t n;     // cells
+  int32_t row0;  // row slot of its lane 0 in the row kernel (lanes consecutive), or -1
 };
 
 __host__ __device__ inline WarpLayout warp_layout(int NCmax) {
@@ -237,6 +239,10 @@ struct StepParams {
   uint8_t *head_occ;   // per node-out-lane index, written with S1
   const uint8_t *ext;  // per node-lane index, from k_node
   const uint64_t *entr;  // per node-out-lane index
+  // the same two node outputs for the row-kernel lanes by ROW SLOT, so the
+  // row kernel loads them contiguously without its row descriptors first
+  const uint8_t *ext_row;
+  const uint64_t *entr_row;
   // outputs
   unsigned long long *stats;  // [kHist][ST_N]
   unsigned long long *link_work;
@@ -263,6 +269,9 @@ struct NodeParams {
   const uint8_t *head_occ;
   uint8_t *ext;              // by node-lane index (k_node: identity)
   uint64_t *entr;
+  uint8_t *ext_row;          // by row slot (row-kernel lanes): the grant again
+  uint64_t *entr_row;        // by row slot: the entrant record again
+  const int32_t *lane_row;   // row slot of every global lane id, or -1 (k_node)
   unsigned long long *stats;
   // per-node work counters (load statistics), by node id;
   // NULL unless TS_FLAG_LINK_WORK: incoming lanes whose front vehicle is in
@@ -310,6 +319,7 @@ struct NodeWarpParams {
   const NodeLane *lanes;  // [32 * nchunks]
   int32_t nchunks;
   const int32_t *nl_node;  // node id of every node-lane index (-1 for pads; node work only)
+  const int32_t *nl_row;   // row slot of every node-lane index, or -1
 };
 
 void launch_lc(const StepParams &p, int blocks, int threads, int smem, void *stream);

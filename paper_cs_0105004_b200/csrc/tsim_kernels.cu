@@ -468,13 +468,14 @@ __global__ void __launch_bounds__(256) k_hash(const StepParams P, unsigned long 
 struct Cand {
   bool cand;
   int tgt, n2, d, v, vid;
+  int tgt_row;  // row slot of the target lane (row kernel), or -1
 };
 
 // the front vehicle of an incoming lane: candidate to cross (d < min(v+1,
 // V)) unless it is on its final link; its target lane (R8)
 __device__ __forceinline__ Cand node_candidate(const NodeParams &P, uint64_t rec, int lane,
                                                int out_base, uint32_t tt, int vk) {
-  Cand c{false, -1, 0, 0, 0, 0};
+  Cand c{false, -1, 0, 0, 0, 0, -1};
   if (!((rec >> 43) & 1)) return c;
   const int code = (int)((rec >> 32) & 0xFF);
   c.d = (int)((rec >> 40) & 7);
@@ -485,6 +486,7 @@ __device__ __forceinline__ Cand node_candidate(const NodeParams &P, uint64_t rec
   const int tty = (tt >> (2 * slot)) & 3;
   const int l2 = tty == 0 ? min(lane, o.L - 1) : (tty == 2 ? 0 : o.L - 1);  // R8
   c.tgt = o.lgid + l2;
+  c.tgt_row = o.row0 >= 0 ? o.row0 + l2 : -1;
   c.n2 = o.n;
   c.vid = (int)(uint32_t)rec;
   c.cand = true;
@@ -508,8 +510,10 @@ __device__ __forceinline__ int node_grant(const NodeParams &P, const Cand &c, in
       P.vpos[c.vid].p = q.p + 1;
     }
     const int y2 = v3 - c.d - 1;
-    P.entr[c.tgt] = (uint64_t)(uint32_t)c.vid | ((uint64_t)(v3 | (nslot << 3)) << 32) |
-                    ((uint64_t)y2 << 40) | ((uint64_t)((P.t + 1) & 0x1FFFFF) << 43);
+    const uint64_t rec = (uint64_t)(uint32_t)c.vid | ((uint64_t)(v3 | (nslot << 3)) << 32) |
+                         ((uint64_t)y2 << 40) | ((uint64_t)((P.t + 1) & 0x1FFFFF) << 43);
+    P.entr[c.tgt] = rec;
+    if (c.tgt_row >= 0) P.entr_row[c.tgt_row] = rec;
     crossings += pass ? 0u : 1u;
   }
   return E;
@@ -573,7 +577,7 @@ __global__ void __launch_bounds__(256) k_node_warp(const NodeParams P_, const No
     const uint32_t nodemask = __match_any_sync(FULL, a ? (int)e[k].first : 64 + lane);
     const bool busy =
         (__ballot_sync(FULL, a && e[k].major && (((uint32_t)(rec[k] >> 44)) & gmask)) & nodemask) != 0u;
-    cd[k] = Cand{false, -1, 0, 0, 0, 0};
+    cd[k] = Cand{false, -1, 0, 0, 0, 0, -1};
     if (a) cd[k] = node_candidate(P, rec[k], e[k].lane, e[k].out_base, e[k].tt, e[k].vk);
     // signalized node (R23): red approaches have the virtual blocker, green
     // ones need no gap acceptance; otherwise priority + gap acceptance (R9)
@@ -591,7 +595,11 @@ __global__ void __launch_bounds__(256) k_node_warp(const NodeParams P_, const No
     int ext = 0;
     const uint32_t cr0 = crossings;
     if (win[k]) ext = node_grant(P, cd[k], e[k].vk, head[k], crossings, (e[k].major & 2) != 0);
-    if (act[k]) P.ext[32 * (c0 + k) + lane] = (uint8_t)ext;
+    if (act[k]) {
+      P.ext[32 * (c0 + k) + lane] = (uint8_t)ext;
+      const int row = W.nl_row[32 * (c0 + k) + lane];
+      if (row >= 0) P.ext_row[row] = (uint8_t)ext;
+    }
     if (P.node_work) {  // load statistics: the node's lanes in range + its crossings
       const bool a = act[k] && e[k].lane_gid >= 0;
       const uint32_t nodemask = __match_any_sync(FULL, a ? (int)e[k].first : 64 + lane);
@@ -623,6 +631,7 @@ __global__ void __launch_bounds__(128) k_node(const NodeParams P_) {
       const int lg = P.link_lgid[j];
       for (int l = 0; l < P.link_lanes[j]; l++) {
         P.ext[lg + l] = 0;
+        if (P.lane_row[lg + l] >= 0) P.ext_row[P.lane_row[lg + l]] = 0;
         if (!(sg0 >> 31) && P.link_cls[j] == maxcls &&
             ((uint32_t)(P.tail_rec[lg + l] >> 44) & gmask))
           majorfree = false;
@@ -664,6 +673,7 @@ __global__ void __launch_bounds__(128) k_node(const NodeParams P_) {
           if (nclaimed < kMaxClaim) claimed[nclaimed++] = bit;
           P.ext[lg + l] = (uint8_t)node_grant(P, cd, P.vmax_link[j], P.head_occ[cd.tgt],
                                               crossings);
+          if (P.lane_row[lg + l] >= 0) P.ext_row[P.lane_row[lg + l]] = P.ext[lg + l];
         }
       }
     }

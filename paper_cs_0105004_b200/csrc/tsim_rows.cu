@@ -260,6 +260,14 @@ static __device__ __noinline__ uint32_t zone_lc(uint32_t zc, int c0, int w, int 
   return lv;
 }
 
+#ifndef TS_ROWS_DRAW_RK
+#define TS_ROWS_DRAW_RK 1  // Philox round keys from the launch parameters
+#endif
+#if TS_ROWS_DRAW_RK
+#define PHILOX_DRAW(e) philox_w0_rk((uint32_t)P.t, (e) & kVidMask, P_.rk)
+#else
+#define PHILOX_DRAW(e) philox_w0((uint32_t)P.t, (e) & kVidMask, P.k0, P.k1)
+#endif
 #ifndef TS_ROWS_MINB
 #define TS_ROWS_MINB (512 / TS_ROWS_TPB)  // resident blocks per SM: 128 registers (96 measured 2.5% slower)
 #endif
@@ -297,10 +305,12 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
   // warp idles while another still has a queue of groups
   // The next group is fetched one iteration ahead; with TS_ROWS_PPF its
   // planes are copied into shared memory (cp.async) while this one runs.
-  (void)nwarps;
+  // every warp's first group is its warp index (no atomic at the start,
+  // where all warps would queue on the one counter); later groups come from
+  // the counter, offset by the warp count
   auto grab = [&]() {
     int g = 0;
-    if (lane == 0) g = (int)(atomicAdd(R.gctr, 1ull) - R.gbase);
+    if (lane == 0) g = (int)(atomicAdd(R.gctr, 1ull) - R.gbase) + (TS_ROWS_FIRST_STATIC ? nwarps : 0);
     return __shfl_sync(FULL, g, 0);
   };
   uint32_t *s_pl = reinterpret_cast<uint32_t *>(s_out + R.cap + kRowsAuxWords);  // PPF buffer
@@ -319,14 +329,37 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
                 kStatePlanes * kRowWords * 32, pbar);
     }
   };
+#if TS_ROWS_FIRST_STATIC
+  int g_next = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+#else
   int g_next = grab();
+#endif
   if (TS_ROWS_PPF && g_next < R.ngroups) issue_planes(g_next);
+  // the next group's vid-block offset and vehicle count, loaded one
+  // iteration ahead (the bulk copy of its block needs them first)
+  int voff_n = 0, tot_n = 0;
+  if (g_next < R.ngroups) {
+    voff_n = R.gvoff[g_next];
+    tot_n = R.gcnt_in[g_next];
+  }
   for (;;) {
     const int g = g_next;
     if (g >= R.ngroups) break;
     g_next = grab();
     if (TS_ROWS_ASYNC && lane == 0) bulk_wait_read();  // the previous group's output block
     uint32_t O[NW], V0[NW], V1[NW], V2[NW], A0[NW], A1[NW];
+    if (!TS_ROWS_PPF) {  // the planes first: they depend on nothing
+      const uint32_t *pin = R.planes_in + group_plane_base(g) + lane;
+#pragma unroll
+      for (int i = 0; i < NW; i++) {
+        O[i] = __ldcs(pin + (0 * NW + i) * 32);
+        V0[i] = __ldcs(pin + (1 * NW + i) * 32);
+        V1[i] = __ldcs(pin + (2 * NW + i) * 32);
+        V2[i] = __ldcs(pin + (3 * NW + i) * 32);
+        A0[i] = __ldcs(pin + (4 * NW + i) * 32);
+        A1[i] = __ldcs(pin + (5 * NW + i) * 32);
+      }
+    }
     if (TS_ROWS_PPF) {  // this group's planes, prefetched during the previous one
       mbar_wait(pbar, pbar_phase);
       pbar_phase ^= 1u;
@@ -343,10 +376,10 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
     __syncwarp();  // the previous group's staged blocks (and the plane buffer) are free
     const RowDesc rd = R.rows[(size_t)g * 32 + lane];
     const int w = rd.w, l = rd.l, L = rd.L, link = rd.link, lg = rd.lg, vk = rd.vk;
-    const int voff = R.gvoff[g];
+    const int voff = voff_n;
     // the group's vid block (its vehicle count was written with it) is
     // staged in shared memory when it fits, loaded together with the planes
-    const int tot_in = R.gcnt_in[g];
+    const int tot_in = tot_n;
     const bool staged = tot_in <= R.cap;
     const bool tma_in = TS_ROWS_TMA_IN && staged && tot_in > 0;
     if (staged) {
@@ -370,22 +403,13 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
       grid_dep_wait();
       dep_done = true;
     }
-    const int ext_lg = do_move0 ? (int)P.ext[rd.nli] : 0;
-    const uint64_t ent_rec = do_move0 ? P.entr[lg] : 0ull;
+    // node grant and entrant by row slot (no dependence on the descriptor)
+    const int ext_raw = do_move ? (int)P.ext_row[(size_t)g * 32 + lane] : 0;
+    const uint64_t ent_raw = do_move ? P.entr_row[(size_t)g * 32 + lane] : 0ull;
+    const int ext_lg = do_move0 ? ext_raw : 0;
+    const uint64_t ent_rec = do_move0 ? ent_raw : 0ull;
     const bool may_inject = (P.mode & kModeInject) && w > 0 && l == 0 &&
                             P.pend_off[link + 1] > P.pend_head[link];
-    if (!TS_ROWS_PPF) {
-      const uint32_t *pin = R.planes_in + group_plane_base(g) + lane;
-#pragma unroll
-      for (int i = 0; i < NW; i++) {
-        O[i] = __ldcs(pin + (0 * NW + i) * 32);
-        V0[i] = __ldcs(pin + (1 * NW + i) * 32);
-        V1[i] = __ldcs(pin + (2 * NW + i) * 32);
-        V2[i] = __ldcs(pin + (3 * NW + i) * 32);
-        A0[i] = __ldcs(pin + (4 * NW + i) * 32);
-        A1[i] = __ldcs(pin + (5 * NW + i) * 32);
-      }
-    }
     uint32_t VAL[NW];
 #pragma unroll
     for (int i = 0; i < NW; i++) VAL[i] = lowm(w - 32 * i);
@@ -492,14 +516,14 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
             for (int jj = lane; jj < n; jj += 32) {
               const uint32_t me = (uint32_t)mlist[jj];
               const uint32_t e = (uint32_t)s_in[me >> 12];
-              if (philox_w0_rk((uint32_t)P.t, e & kVidMask, P_.rk) <= p32m1)
+              if (PHILOX_DRAW(e) <= p32m1)
                 red_or_shared(bw_s + (((me >> 5) & 127u) << 2), 1u << (me & 31u));
             }
           } else {
             for (int jj = lane; jj < n; jj += 32) {
               const uint32_t me = (uint32_t)mlist[jj];
               const uint32_t e = (uint32_t)vbase[me >> 12];
-              if (philox_w0_rk((uint32_t)P.t, e & kVidMask, P_.rk) <= p32m1)
+              if (PHILOX_DRAW(e) <= p32m1)
                 red_or_shared(bw_s + (((me >> 5) & 127u) << 2), 1u << (me & 31u));
             }
           }
@@ -625,6 +649,10 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
         OA0[i] = A0[i];
         OA1[i] = A1[i];
       }
+    }
+    if (g_next < R.ngroups) {  // the next group's block offset and count (see above)
+      voff_n = R.gvoff[g_next];
+      tot_n = R.gcnt_in[g_next];
     }
     // ---- injection from parking (H6, R13): lane 0 of links with pending trips
     uint32_t INJ[NW];
@@ -809,67 +837,7 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
       }
       for (; i < nfin; i++) vout[i] = vin[i - sh];
     }
-    // rows whose set changed by lane changes only (no injection in the
-    // warp): the own list with its leavers (LV) skipped and the arrivals
-    // (AR, from row l - dir) spliced in -- a few segment copies per row
-    bool spliced = false;
-    if (!ginj && __any_sync(FULL, changed)) {
-      uint32_t sOO[NW];  // the arrivals' source row (l - dir) before its lane change
-#pragma unroll
-      for (int i = 0; i < NW; i++) sOO[i] = shfl_w(OO[i], lane - dir);
-      const int s_in_off = __shfl_sync(FULL, in_off, lane - dir);
-      const int s_ent_y = __shfl_sync(FULL, ent_y, lane - dir);
-      const uint32_t s_ent_e = __shfl_sync(FULL, ent_e, lane - dir);
-      const bool fits = popc_row(LV) <= kSpliceMax && popc_row(AR) <= kSpliceMax;
-      if (__all_sync(FULL, fits)) {
-        spliced = true;
-        if (changed) {
-          const int32_t *vb = staged ? (const int32_t *)s_in : R.vid_in + voff;
-          int32_t *ev = s_out + R.cap + lane * (3 * kSpliceMax);  // aux area: this row's events
-          int32_t *Lr = ev, *Ao = ev + kSpliceMax, *Ae = ev + 2 * kSpliceMax;
-          int nl = 0, na = 0, po = 0, pf = 0, ps = 0;
-#pragma unroll
-          for (int i = 0; i < NW; i++) {
-            uint32_t m = LV[i];
-            while (m) {  // leavers: their rank in the own list (increasing)
-              const uint32_t below = (m & (0u - m)) - 1u;
-              m &= m - 1u;
-              Lr[nl++] = po + __popc(OO[i] & below);
-            }
-            uint32_t a = AR[i];
-            while (a) {  // arrivals: output rank and list entry
-              const uint32_t below = (a & (0u - a)) - 1u;
-              a &= a - 1u;
-              const int c = 32 * i + __popc(below);
-              Ao[na] = pf + __popc(FO[i] & below);
-              const int q = ps + __popc(sOO[i] & below);
-              Ae[na++] = c == s_ent_y ? (int32_t)s_ent_e
-                                      : vb[s_in_off + q - (s_ent_y >= 0 ? 1 : 0)];
-            }
-            po += __popc(OO[i]);
-            pf += __popc(FO[i]);
-            ps += __popc(sOO[i]);
-          }
-          // own list entry k: the entrant (lowest cell) first, then the input
-          // list (its exited front is past the end)
-          const int sh = has_ent ? 1 : 0;
-          int j = 0, k = 0, il = 0, ia = 0;
-          while (j < nfin) {
-            const int jl = il < nl ? j + (Lr[il] - k) : 0x7fffffff;
-            const int ja = ia < na ? Ao[ia] : 0x7fffffff;
-            const int stop = min(min(jl, ja), nfin);
-            for (; j < stop; j++, k++) vout[j] = (k < sh) ? (int32_t)ent_e : vin[k - sh];
-            if (j == jl && jl <= ja) {
-              k++;
-              il++;
-            } else if (j == ja) {
-              vout[j++] = Ae[ia++];
-            }
-          }
-        }
-      }
-    }
-    const bool general = changed && !spliced;
+    const bool general = changed;
     if (const uint32_t gmask = __ballot_sync(FULL, general)) {
       // rows whose vehicle set changed inside (lane changes, injections):
       // every vehicle of S(t+1) before the lane change goes to its rank in
