@@ -275,8 +275,16 @@ def bench_multi(args):
     from paper_cs_0105004_b200 import domains
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # TSIM_BENCH_BACKEND=gloo: a functional check of this multi-rank path with
+    # fewer GPUs than ranks (ranks share devices, strips staged through host
+    # memory); its timings are not scaling numbers
+    backend = os.environ.get("TSIM_BENCH_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count()) if backend != "nccl" else local
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    else:
+        dist.init_process_group(backend)
     hbm_peak, peak_src = measured_peaks()
     scn = workload(args.config)
     dom = domains.partition(scn, world)
@@ -285,7 +293,8 @@ def bench_multi(args):
     # native exchanges (the library's own NCCL communicator, whole steps per
     # ts_step call); torch.distributed send/recv between the phases otherwise
     try:
-        d = domains.DistDomain(scn, dom, device=local, flags=tsim.FLAG_FUSED, native=True)
+        d = domains.DistDomain(scn, dom, device=local, flags=tsim.FLAG_FUSED,
+                               native=backend == "nccl")
     except tsim.TsError:
         d = domains.DistDomain(scn, dom, device=local, flags=tsim.FLAG_FUSED)
     d.step(args.warmup)
@@ -299,12 +308,13 @@ def bench_multi(args):
         e1.record(d.stream)
         torch.cuda.synchronize()
     dist.barrier()
-    ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=f"cuda:{local}")
+    red_dev = f"cuda:{local}" if backend == "nccl" else "cpu"
+    ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=red_dev)
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     # exchange time, reported separately: mean device time of one exchange
     # (timed on every 8th step by the library), max over ranks
     xms, xn = d.sim.last_exchange_timing() if d.native else (0.0, 0)
-    xchg = torch.tensor([xms / max(1, xn)], dtype=torch.float64, device=f"cuda:{local}")
+    xchg = torch.tensor([xms / max(1, xn)], dtype=torch.float64, device=red_dev)
     dist.all_reduce(xchg, op=dist.ReduceOp.MAX)
     hist = d.sim.history(t_from, args.steps + 1)
     tot = d.sim.totals()
@@ -312,7 +322,7 @@ def bench_multi(args):
     e2e_local = time.perf_counter() - w0
     loc = torch.tensor([float(np.sum(hist["active"][:args.steps])), float(tot["lane_cells"]),
                         float(np.sum(hist["crossings"][1:])), e2e_local], dtype=torch.float64,
-                       device=f"cuda:{local}")
+                       device=red_dev)
     s = loc.clone()
     dist.all_reduce(s, op=dist.ReduceOp.SUM)
     e2e = loc[3:4].clone()

@@ -216,6 +216,19 @@ void *ts_stream(const ts_sim *h);
  * events after the senders' packs and before the receivers' next work. */
 int ts_exchange_local(ts_sim **hs, int32_t k);
 
+/* n_steps whole steps of the k domains of one partition held by this
+ * process (the k handles in any order; any devices), with the in-process
+ * exchanges between them (lane change, exchange #1,
+ * intersections + move + injection, exchange #2, per step), enqueued by the
+ * library with no host round trip per phase.  With TS_FLAG_GRAPH on every
+ * handle (one device), blocks of 15 steps replay one CUDA graph that holds
+ * all k domains' streams and both exchanges of every step.  Synchronous.
+ * The handles must be at the same time t with no step in progress; not with
+ * a native communicator.  Each domain's busy time (ts_busy_time) covers its
+ * phases (not the exchange waits), except inside replayed graphs.  Not
+ * thread-safe (the captured graphs are kept per handle set). */
+int ts_local_step(ts_sim **hs, int32_t k, int32_t n_steps);
+
 /* current time t (state is S(t)) */
 int32_t ts_time(const ts_sim *h);
 

@@ -153,8 +153,11 @@ int ts_create(const ts_config *cfg, ts_sim **out) {
   return TS_OK;
 }
 
+static void drop_local_graphs(const ts_sim *h);
+
 void ts_destroy(ts_sim *h) {
   if (!h) return;
+  drop_local_graphs(h);
   cudaSetDevice(h->dev);
   if (h->stream) cudaStreamSynchronize(h->stream);
   for (void *p : h->allocs) cudaFree(p);
@@ -1930,18 +1933,16 @@ void *ts_stream(const ts_sim *h) { return h ? (void *)h->stream : nullptr; }
 // the same k-way partition, any devices): every send segment is copied into
 // the partner's receive segment, ordered after the sender's pack and before
 // the receiver's unpack by events
-int ts_exchange_local(ts_sim **hs, int32_t k) {
-  if (!hs || k < 1) return TS_EINVAL;
-  std::vector<ts_sim *> by_dom(k, nullptr);
-  for (int i = 0; i < k; i++) {
-    if (!hs[i] || !hs[i]->inited || hs[i]->dom_k != k) return TS_EINVAL;
-    by_dom[hs[i]->dom_me] = hs[i];
-  }
+// the exchange among the handles of one partition, by_dom[d] = domain d:
+// every send segment into its partner's receive segment (device copies,
+// peer copies across devices), ordered by the handles' reusable events
+static int exchange_local_enqueue(const std::vector<ts_sim *> &by_dom) {
+  const int k = (int)by_dom.size();
   // ordering by each handle's reusable events: the receivers' copies wait
   // for their senders' packs; the senders' next work waits for the copies
   for (int i = 0; i < k; i++) {
     ts_sim *a = by_dom[i];
-    if (!a) return fail(hs[0], TS_EINVAL, "domain %d missing", i);
+    if (!a) return TS_EINVAL;  // checked by by_domain
     CK(a, cudaSetDevice(a->dev));
     CK(a, cudaEventRecord(a->ev_packed, a->stream));
   }
@@ -1971,6 +1972,221 @@ int ts_exchange_local(ts_sim **hs, int32_t k) {
       CK(a, cudaSetDevice(a->dev));
       CK(a, cudaStreamWaitEvent(a->stream, b->ev_copied, 0));
     }
+  }
+  return TS_OK;
+}
+
+
+// the k handles of one partition indexed by domain (TS_EINVAL otherwise)
+static int by_domain(ts_sim **hs, int32_t k, std::vector<ts_sim *> &by_dom) {
+  if (!hs || k < 1) return TS_EINVAL;
+  by_dom.assign(k, nullptr);
+  for (int i = 0; i < k; i++) {
+    if (!hs[i] || !hs[i]->inited || hs[i]->dom_k != k || by_dom[hs[i]->dom_me])
+      return hs[i] ? fail(hs[i], TS_EINVAL, "not the %d initialised domains of one partition", k)
+                   : TS_EINVAL;
+    by_dom[hs[i]->dom_me] = hs[i];
+  }
+  return TS_OK;
+}
+
+int ts_exchange_local(ts_sim **hs, int32_t k) {
+  std::vector<ts_sim *> by_dom;
+  if (int rc = by_domain(hs, k, by_dom)) return rc;
+  return exchange_local_enqueue(by_dom);
+}
+
+// one whole step of all domains: lane change + pack #1,
+// exchange, unpack + intersections + move + injection + pack #2, exchange,
+// unpack; every phase of a domain bracketed by its busy-time events unless
+// capturing
+static int local_step_enqueue(const std::vector<ts_sim *> &ds, bool more) {
+  auto timed = [&](ts_sim *h, auto &&fn) -> int {
+    const bool ev = !h->capturing;
+    if (ev) {
+      if (h->ph_used >= 8192)
+        if (int rc = fold_busy(h)) return rc;
+      while (h->ph_ev.size() < h->ph_used + 2) {
+        cudaEvent_t e;
+        CK(h, cudaEventCreate(&e));
+        h->ph_ev.push_back(e);
+      }
+      CK(h, cudaEventRecord(h->ph_ev[h->ph_used], h->stream));
+    }
+    fn();
+    if (ev) {
+      CK(h, cudaEventRecord(h->ph_ev[h->ph_used + 1], h->stream));
+      h->ph_used += 2;
+    }
+    return TS_OK;
+  };
+  for (ts_sim *h : ds) {
+    CK(h, cudaSetDevice(h->dev));
+    if (int rc = timed(h, [&]() { phase_lc(h); })) return rc;
+  }
+  if (int rc = exchange_local_enqueue(ds)) return rc;
+  for (ts_sim *h : ds) {
+    CK(h, cudaSetDevice(h->dev));
+    if (int rc = timed(h, [&]() { phase_move(h, more, nullptr, nullptr); })) return rc;
+  }
+  if (int rc = exchange_local_enqueue(ds)) return rc;
+  for (ts_sim *h : ds) {
+    CK(h, cudaSetDevice(h->dev));
+    if (int rc = timed(h, [&]() {
+          if (h->n_xs > 0) unpack_strips(h);
+        }))
+      return rc;
+  }
+  return TS_OK;
+}
+
+// capture kGraphSteps steps of all domains into one CUDA graph (the
+// domains' streams forked from / joined into domain 0's stream); false if
+// the capture is not possible
+struct LocalGraph {
+  std::vector<ts_sim *> ds;
+  cudaGraphExec_t exec = nullptr;
+  int key = -1;
+  std::vector<unsigned long long> gctr_end;
+};
+static std::vector<LocalGraph> g_local_graphs;  // per partition (handle set) and parity
+
+// a destroyed handle's graphs go with it (their nodes use its buffers)
+static void drop_local_graphs(const ts_sim *h) {
+  for (size_t i = 0; i < g_local_graphs.size();) {
+    LocalGraph &g = g_local_graphs[i];
+    if (std::find(g.ds.begin(), g.ds.end(), h) != g.ds.end()) {
+      if (g.exec) cudaGraphExecDestroy(g.exec);
+      g_local_graphs.erase(g_local_graphs.begin() + i);
+    } else {
+      i++;
+    }
+  }
+}
+
+static bool capture_local(std::vector<ts_sim *> &ds, LocalGraph &lg) {
+  ts_sim *h0 = ds[0];
+  struct Saved {
+    int32_t t;
+    int rcur, gcur;
+    bool rs, gs;
+    unsigned long long gb;
+  };
+  std::vector<Saved> sv;
+  for (ts_sim *h : ds) {
+    if (!h->d_clock && dalloc(h, &h->d_clock, 1, 0)) return false;
+    sv.push_back(Saved{h->t, h->rcur, h->gcur, h->rows_s1, h->gen_s1, h->gctr_base});
+  }
+  cudaGraph_t graph = nullptr;
+  bool ok = cudaStreamBeginCapture(h0->stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+  if (ok) {
+    cudaEventRecord(h0->ev_packed, h0->stream);  // fork every domain's stream into the capture
+    for (ts_sim *h : ds) {
+      if (h != h0) cudaStreamWaitEvent(h->stream, h0->ev_packed, 0);
+      h->capturing = true;
+      h->graph_t0 = h->t;
+      h->gctr_base = 0;
+      cudaMemsetAsync(h->d_gctr, 0, sizeof(unsigned long long), h->stream);
+      launch_clock(h->d_clock, h->d_stats, kGraphSteps + 1, false, h->stream);
+    }
+    for (int i = 0; i < kGraphSteps && ok; i++) ok = local_step_enqueue(ds, i < kGraphSteps - 1) == TS_OK;
+    for (ts_sim *h : ds) {
+      launch_clock(h->d_clock, h->d_stats, kGraphSteps, true, h->stream);
+      if (h != h0) {  // join
+        cudaEventRecord(h->ev_copied, h->stream);
+        cudaStreamWaitEvent(h0->stream, h->ev_copied, 0);
+      }
+    }
+    const cudaError_t e = cudaStreamEndCapture(h0->stream, &graph);
+    ok = ok && e == cudaSuccess && graph;
+    if (!ok && getenv("TSIM_TRACE")) fprintf(stderr, "[tsim] local capture: %s\n", cudaGetErrorString(e));
+  }
+  for (size_t i = 0; i < ds.size(); i++) {
+    ts_sim *h = ds[i];
+    ok = ok && h->rcur == sv[i].rcur && h->gcur == sv[i].gcur && pending_lc(h) == 3;
+    lg.gctr_end.push_back(h->gctr_base);
+    h->capturing = false;
+    h->t = sv[i].t;
+    h->rcur = sv[i].rcur;
+    h->gcur = sv[i].gcur;
+    h->rows_s1 = sv[i].rs;
+    h->gen_s1 = sv[i].gs;
+    h->gctr_base = sv[i].gb;
+  }
+  if (ok) ok = cudaGraphInstantiate(&lg.exec, graph, 0) == cudaSuccess;
+  if (graph) cudaGraphDestroy(graph);
+  cudaGetLastError();
+  if (getenv("TSIM_TRACE"))
+    fprintf(stderr, "[tsim] local graph capture of %d steps, %zu domains: %s\n", kGraphSteps, ds.size(),
+            ok ? "ok" : "failed (steps launched one by one)");
+  return ok;
+}
+
+int ts_local_step(ts_sim **hs, int32_t k, int32_t n_steps) {
+  std::vector<ts_sim *> ds;
+  if (int rc = by_domain(hs, k, ds)) return rc;
+  if (n_steps < 0) return fail(ds[0], TS_EINVAL, "negative step count");
+  bool graph = true;
+  for (ts_sim *h : ds) {
+    if (h->comm) return fail(h, TS_EINVAL, "a domain with a native communicator");
+    if (pending_lc(h) != 3) return fail(h, TS_EINVAL, "domain in the middle of a step");
+    if (h->t != ds[0]->t) return fail(h, TS_EINVAL, "domains at different times");
+    graph = graph && (h->cfg.flags & TS_FLAG_GRAPH) && !h->graph_off && h->dev == ds[0]->dev;
+  }
+  while (n_steps > 0) {
+    const int32_t m = std::min<int32_t>(n_steps, kStepBlock);
+    for (ts_sim *h : ds) {
+      CK(h, cudaSetDevice(h->dev));
+      if (zero_stats(h, h->t + 1, std::min(m + 1, kHist))) return TS_EINTERNAL;
+    }
+    int done = 0;
+    if (graph && m >= kGraphSteps) {  // whole blocks replay one graph of all domains
+      int key = 0;
+      for (size_t i = 0; i < ds.size(); i++) key |= (graph_key(ds[i]) << (2 * (i % 16)));
+      LocalGraph *lg = nullptr;
+      for (LocalGraph &x : g_local_graphs)
+        if (x.ds == ds && x.key == key) lg = &x;
+      if (!lg) {
+        LocalGraph nl;
+        nl.ds = ds;
+        nl.key = key;
+        if (capture_local(ds, nl)) {
+          g_local_graphs.push_back(nl);
+          lg = &g_local_graphs.back();
+        } else {
+          for (ts_sim *h : ds) h->graph_off = true;
+          graph = false;
+        }
+      }
+      if (lg) {
+        const int reps = m / kGraphSteps;
+        ts_sim *h0 = ds[0];
+        CK(h0, cudaSetDevice(h0->dev));
+        for (ts_sim *h : ds) {  // clocks, after each domain's previous work
+          CK(h0, cudaEventRecord(h->ev_packed, h->stream));
+          CK(h0, cudaStreamWaitEvent(h0->stream, h->ev_packed, 0));
+          CK(h0, cudaMemcpyAsync(h->d_clock, &h->t, sizeof(int32_t), cudaMemcpyHostToDevice, h0->stream));
+        }
+        for (int r = 0; r < reps; r++) CK(h0, cudaGraphLaunch(lg->exec, h0->stream));
+        CK(h0, cudaEventRecord(h0->ev_copied, h0->stream));
+        for (size_t i = 0; i < ds.size(); i++) {
+          ts_sim *h = ds[i];
+          CK(h, cudaStreamWaitEvent(h->stream, h0->ev_copied, 0));  // later work after the graph
+          h->t += reps * kGraphSteps;
+          h->gctr_base = lg->gctr_end[i];
+        }
+        done = reps * kGraphSteps;
+        CK(h0, cudaStreamSynchronize(h0->stream));  // the host clock values were read
+      }
+    }
+    for (int i = done; i < m; i++)
+      if (int rc = local_step_enqueue(ds, i < m - 1)) return rc;
+    for (ts_sim *h : ds) {
+      CK(h, cudaSetDevice(h->dev));
+      CK(h, cudaStreamSynchronize(h->stream));
+      if (int rc = fold_stats(h)) return rc;
+    }
+    n_steps -= m;
   }
   return TS_OK;
 }

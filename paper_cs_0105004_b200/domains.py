@@ -190,6 +190,14 @@ class LocalDomains:
             _t.exchange_local(self.sims)
 
     def step(self, n=1):
+        """n whole steps of all domains inside the library (ts_local_step;
+        CUDA-graph replays with FLAG_GRAPH)"""
+        if n > 0:
+            _t.local_step(self.sims, n)
+
+    def step_phases(self, n=1):
+        """the same steps driven phase by phase from here (ts_step_phase +
+        ts_exchange_local)"""
         for i in range(n):
             for s in self.sims:
                 s.phase(0)

@@ -94,6 +94,7 @@ def load_library():
         "ts_exchange_buffers": (ctypes.c_int, [P, ctypes.POINTER(P), ctypes.POINTER(P)]),
         "ts_stream": (P, [P]),
         "ts_exchange_local": (ctypes.c_int, [ctypes.POINTER(P), I32]),
+        "ts_local_step": (ctypes.c_int, [ctypes.POINTER(P), I32, I32]),
         "ts_last_timing": (ctypes.c_int, [P, ctypes.POINTER(ctypes.c_double),
                                           ctypes.POINTER(ctypes.c_double),
                                           ctypes.POINTER(ctypes.c_int64)]),
@@ -267,6 +268,15 @@ def exchange_local(sims):
     lib = load_library()
     arr = (ctypes.c_void_p * len(sims))(*[s.h for s in sims])
     rc = lib.ts_exchange_local(arr, len(sims))
+    if rc:
+        raise TsError(lib.ts_last_error(sims[0].h).decode())
+
+
+def local_step(sims, n):
+    """n whole steps of the in-process domains of one partition (ts_local_step)"""
+    lib = load_library()
+    arr = (ctypes.c_void_p * len(sims))(*[s.h for s in sims])
+    rc = lib.ts_local_step(arr, len(sims), int(n))
     if rc:
         raise TsError(lib.ts_last_error(sims[0].h).decode())
 

@@ -218,3 +218,30 @@ def test_load_statistics_links_and_nodes():
     parts = [x.load_stats() for x in d.sims]
     assert np.array_equal(sum(p[0] for p in parts), lw)
     assert np.array_equal(sum(p[1] for p in parts), nw)
+
+
+@pytest.mark.parametrize("graph", [False, True])
+def test_local_step_in_library(graph):
+    """ts_local_step: whole steps of all k domains enqueued by the library
+    (both exchanges per step), and with FLAG_GRAPH replayed from one CUDA
+    graph holding every domain's stream and the exchanges: per-step hash
+    equal to the undivided oracle for 300 steps in chunks of 7, 15, 31, 45
+    steps (graph blocks + remainders); the phase-by-phase driver gives the
+    same state"""
+    s = scenarios.portland(n_nodes=600, n_edges=800, n_veh=8000, side_km=8.0, n_zones=64, seed=2)
+    s.depart = (s.depart // 12).astype(np.int32)
+    s = scenarios.with_signals(s, green0=20, green1=25, seed=4)
+    flags = FUSED | (tsim.FLAG_GRAPH if graph else 0)
+    o = oracle.Oracle.from_scenario(s)
+    d = domains.LocalDomains(s, 8, flags=flags)
+    p = domains.LocalDomains(s, 8, flags=FUSED)
+    for chunk in (7, 15, 31, 45, 7, 15, 31, 45, 104):
+        t_from = o.t + 1
+        oh = o.run_hashes(chunk)
+        d.step(chunk)
+        p.step_phases(chunk)
+        gh = d.history(t_from, chunk)["hash"]
+        bad = [t_from + i for i in range(chunk) if gh[i] != oh[i]]
+        assert not bad, f"per-step hash differs at t={bad[:5]}"
+        assert d.state_hash() == p.state_hash() == o.state_hash()
+    assert_same(o.vehicles(), d.vehicles(), "after 300 steps")
