@@ -260,9 +260,6 @@ static __device__ __noinline__ uint32_t zone_lc(uint32_t zc, int c0, int w, int 
   return lv;
 }
 
-#ifndef TS_ROWS_LC_SKIP
-#define TS_ROWS_LC_SKIP 1  // warps without lane changes skip the arrival shuffles
-#endif
 #ifndef TS_ROWS_DRAW_RK
 #define TS_ROWS_DRAW_RK 1  // Philox round keys from the launch parameters
 #endif
@@ -787,8 +784,6 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
     uint32_t FO[NW], FV0[NW], FV1[NW], FV2[NW];
     {
       uint32_t *pout = R.planes_out + group_plane_base(g) + lane;
-      // a warp without lane changes keeps its planes (no shuffles)
-      const bool wlc = lc && (!TS_ROWS_LC_SKIP || __any_sync(FULL, any_row(AR)));
 #pragma unroll
       for (int i = 0; i < NW; i++) {
         const uint32_t keep = ~LV[i], ar = AR[i];
@@ -797,7 +792,7 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
         FV0[i] = OV0[i];
         FV1[i] = OV1[i];
         FV2[i] = OV2[i];
-        if (wlc) {  // arrivals carry their velocity and class bits from lane l - dir
+        if (lc) {  // arrivals carry their velocity and class bits from lane l - dir
           FV0[i] = (FV0[i] & keep) | (shfl_w(OV0[i], lane - dir) & ar);
           FV1[i] = (FV1[i] & keep) | (shfl_w(OV1[i], lane - dir) & ar);
           FV2[i] = (FV2[i] & keep) | (shfl_w(OV2[i], lane - dir) & ar);
