@@ -342,8 +342,8 @@ def bench_multi(args):
             "config": {"workload": scn.name, "recipe": scn.recipe, "lane_cells": int(lane_cells),
                        "vehicles": scn.n_vehicles,
                        "l2": "inputs larger than L2 (state read+written per step > 126 MB)",
-                       "parallelism": f"{world} GPUs, ORB domains, split links, 2 NCCL strip "
-                                      f"exchanges per step ({'native' if d.native else 'torch'})",
+                       "parallelism": f"{world} ranks, ORB domains, split links, 2 strip exchanges "
+                                      f"per step ({'native NCCL' if d.native else 'torch.distributed ' + backend})",
                        "split_links": n_spl,
                        "domain_pairs": len(pairs)},
             "real_time_ratio": args.steps / (ms_total / 1e3),
@@ -351,7 +351,7 @@ def bench_multi(args):
                          "exchanges_per_step": 2,
                          "share_of_step": 2 * float(xchg.item()) / (ms_total / args.steps)
                          if d.native else None,
-                         "transport": "native NCCL" if d.native else "torch.distributed"},
+                         "transport": "native NCCL" if d.native else f"torch.distributed {backend}"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved / hbm_peak, "traffic": None,
                          "kernel": "whole step per GPU (incl. exchanges)",
