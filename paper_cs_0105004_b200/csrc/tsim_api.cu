@@ -155,9 +155,12 @@ int ts_create(const ts_config *cfg, ts_sim **out) {
 
 static void drop_local_graphs(const ts_sim *h);
 
+static void drop_direct_plans(const ts_sim *h);
+
 void ts_destroy(ts_sim *h) {
   if (!h) return;
   drop_local_graphs(h);
+  drop_direct_plans(h);
   cudaSetDevice(h->dev);
   if (h->stream) cudaStreamSynchronize(h->stream);
   for (void *p : h->allocs) cudaFree(p);
@@ -1504,10 +1507,12 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
 // --------------------------------------------------------------------- step
 // strips of the boundary tiles -> send buffer (after k_lc / k_step)
 static void pack_strips(ts_sim *h) {
+  if (h->direct) return;  // delivered straight from the strip buffers (ts_local_step)
   launch_strip_copy(h->d_strip[h->gcur], h->d_send_slot, h->d_send, nullptr, h->n_xs, h->stream);
 }
 // receive buffer -> mirror strips, read as halos by the next kernel
 static void unpack_strips(ts_sim *h) {
+  if (h->direct) return;
   launch_strip_copy(h->d_recv, nullptr, h->d_strip[h->gcur], h->d_recv_slot, h->n_xs, h->stream);
 }
 
@@ -1996,11 +2001,85 @@ int ts_exchange_local(ts_sim **hs, int32_t k) {
   return exchange_local_enqueue(by_dom);
 }
 
+// direct exchange plans of in-process partitions on one device: per
+// partition (handle set), every (sender, its strip slot) -> (receiver,
+// mirror slot), in the receivers' segment order
+struct DirectPlan {
+  std::vector<ts_sim *> ds;
+  int4 *d_plan = nullptr;
+  int64_t n = 0;
+};
+static std::vector<DirectPlan> g_direct_plans;
+
+static const DirectPlan *direct_plan(const std::vector<ts_sim *> &ds) {
+  for (const DirectPlan &p : g_direct_plans)
+    if (p.ds == ds) return &p;
+  if ((int)ds.size() > kDirectMax) return nullptr;
+  for (ts_sim *h : ds)
+    if (h->dev != ds[0]->dev) return nullptr;
+  std::vector<int4> plan;
+  for (size_t bi = 0; bi < ds.size(); bi++) {
+    ts_sim *b = ds[bi];
+    for (const ts_sim::Nbr &nb : b->nbrs) {
+      ts_sim *a = ds[nb.dom];
+      const ts_sim::Nbr *back = nullptr;
+      for (const ts_sim::Nbr &x : a->nbrs)
+        if (x.dom == b->dom_me) back = &x;
+      if (!back || back->send_slot.size() != nb.recv_slot.size()) return nullptr;
+      for (size_t j = 0; j < nb.recv_slot.size(); j++)
+        plan.push_back(int4{nb.dom, back->send_slot[j], (int)bi, nb.recv_slot[j]});
+    }
+  }
+  DirectPlan p;
+  p.ds = ds;
+  p.n = (int64_t)plan.size();
+  if (!plan.empty()) {
+    // owned by domain 0's handle (freed with it; the plan is dropped then)
+    if (upload(ds[0], &p.d_plan, plan)) return nullptr;
+  }
+  g_direct_plans.push_back(p);
+  return &g_direct_plans.back();
+}
+
+static void drop_direct_plans(const ts_sim *h) {
+  for (size_t i = 0; i < g_direct_plans.size();) {
+    if (std::find(g_direct_plans[i].ds.begin(), g_direct_plans[i].ds.end(), h) !=
+        g_direct_plans[i].ds.end())
+      g_direct_plans.erase(g_direct_plans.begin() + i);
+    else
+      i++;
+  }
+}
+
+// the exchange as one kernel on domain 0's stream, after every domain's
+// last work and before its next (the strips of the handles' current buffers)
+static int exchange_direct_enqueue(const std::vector<ts_sim *> &ds, const DirectPlan &pl) {
+  ts_sim *h0 = ds[0];
+  DirectParams P{};
+  for (size_t i = 0; i < ds.size(); i++) {
+    P.src[i] = ds[i]->d_strip[ds[i]->gcur];
+    P.dst[i] = ds[i]->d_strip[ds[i]->gcur];
+    if (ds[i] != h0) {
+      CK(h0, cudaEventRecord(ds[i]->ev_packed, ds[i]->stream));
+      CK(h0, cudaStreamWaitEvent(h0->stream, ds[i]->ev_packed, 0));
+    }
+  }
+  P.plan = pl.d_plan;
+  P.n = pl.n;
+  launch_strip_direct(P, h0->stream);
+  CK(h0, cudaEventRecord(h0->ev_copied, h0->stream));
+  for (ts_sim *h : ds)
+    if (h != h0) CK(h0, cudaStreamWaitEvent(h->stream, h0->ev_copied, 0));
+  return TS_OK;
+}
+
 // one whole step of all domains: lane change + pack #1,
 // exchange, unpack + intersections + move + injection + pack #2, exchange,
 // unpack; every phase of a domain bracketed by its busy-time events unless
 // capturing
-static int local_step_enqueue(const std::vector<ts_sim *> &ds, bool more) {
+static int local_step_enqueue(const std::vector<ts_sim *> &ds, bool more,
+                              const DirectPlan *dp = nullptr) {
+  auto exchange = [&]() { return dp ? exchange_direct_enqueue(ds, *dp) : exchange_local_enqueue(ds); };
   auto timed = [&](ts_sim *h, auto &&fn) -> int {
     const bool ev = !h->capturing;
     if (ev) {
@@ -2024,12 +2103,12 @@ static int local_step_enqueue(const std::vector<ts_sim *> &ds, bool more) {
     CK(h, cudaSetDevice(h->dev));
     if (int rc = timed(h, [&]() { phase_lc(h); })) return rc;
   }
-  if (int rc = exchange_local_enqueue(ds)) return rc;
+  if (int rc = exchange()) return rc;
   for (ts_sim *h : ds) {
     CK(h, cudaSetDevice(h->dev));
     if (int rc = timed(h, [&]() { phase_move(h, more, nullptr, nullptr); })) return rc;
   }
-  if (int rc = exchange_local_enqueue(ds)) return rc;
+  if (int rc = exchange()) return rc;
   for (ts_sim *h : ds) {
     CK(h, cudaSetDevice(h->dev));
     if (int rc = timed(h, [&]() {
@@ -2064,7 +2143,7 @@ static void drop_local_graphs(const ts_sim *h) {
   }
 }
 
-static bool capture_local(std::vector<ts_sim *> &ds, LocalGraph &lg) {
+static bool capture_local(std::vector<ts_sim *> &ds, LocalGraph &lg, const DirectPlan *dp) {
   ts_sim *h0 = ds[0];
   struct Saved {
     int32_t t;
@@ -2089,7 +2168,8 @@ static bool capture_local(std::vector<ts_sim *> &ds, LocalGraph &lg) {
       cudaMemsetAsync(h->d_gctr, 0, sizeof(unsigned long long), h->stream);
       launch_clock(h->d_clock, h->d_stats, kGraphSteps + 1, false, h->stream);
     }
-    for (int i = 0; i < kGraphSteps && ok; i++) ok = local_step_enqueue(ds, i < kGraphSteps - 1) == TS_OK;
+    for (int i = 0; i < kGraphSteps && ok; i++)
+      ok = local_step_enqueue(ds, i < kGraphSteps - 1, dp) == TS_OK;
     for (ts_sim *h : ds) {
       launch_clock(h->d_clock, h->d_stats, kGraphSteps, true, h->stream);
       if (h != h0) {  // join
@@ -2126,6 +2206,16 @@ int ts_local_step(ts_sim **hs, int32_t k, int32_t n_steps) {
   std::vector<ts_sim *> ds;
   if (int rc = by_domain(hs, k, ds)) return rc;
   if (n_steps < 0) return fail(ds[0], TS_EINVAL, "negative step count");
+  // one device: the strips go straight from the senders' to the receivers'
+  // strip buffers, one kernel per exchange (else device / peer copies)
+  const DirectPlan *dp = getenv("TSIM_LOCAL_COPIES") ? nullptr : direct_plan(ds);
+  struct DirectGuard {
+    std::vector<ts_sim *> &ds;
+    ~DirectGuard() {
+      for (ts_sim *h : ds) h->direct = false;
+    }
+  } guard{ds};
+  for (ts_sim *h : ds) h->direct = dp != nullptr;
   bool graph = true;
   for (ts_sim *h : ds) {
     if (h->comm) return fail(h, TS_EINVAL, "a domain with a native communicator");
@@ -2150,7 +2240,7 @@ int ts_local_step(ts_sim **hs, int32_t k, int32_t n_steps) {
         LocalGraph nl;
         nl.ds = ds;
         nl.key = key;
-        if (capture_local(ds, nl)) {
+        if (capture_local(ds, nl, dp)) {
           g_local_graphs.push_back(nl);
           lg = &g_local_graphs.back();
         } else {
@@ -2180,7 +2270,7 @@ int ts_local_step(ts_sim **hs, int32_t k, int32_t n_steps) {
       }
     }
     for (int i = done; i < m; i++)
-      if (int rc = local_step_enqueue(ds, i < m - 1)) return rc;
+      if (int rc = local_step_enqueue(ds, i < m - 1, dp)) return rc;
     for (ts_sim *h : ds) {
       CK(h, cudaSetDevice(h->dev));
       CK(h, cudaStreamSynchronize(h->stream));

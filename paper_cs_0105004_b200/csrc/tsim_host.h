@@ -218,6 +218,9 @@ struct ts_sim {
   int32_t async_from = 0, async_n = 0;
   double async_ms = 0, async_move_ms = 0;  // timing of the leading blocks of a long async run
   int64_t async_move_launches = 0;
+  // ts_local_step on one device: strips delivered by one direct kernel per
+  // exchange (no pack / copy / unpack of this handle while set)
+  bool direct = false;
   // ts_exchange_local: reusable ordering events (after the pack, after the copies)
   cudaEvent_t ev_packed = nullptr, ev_copied = nullptr;
 };

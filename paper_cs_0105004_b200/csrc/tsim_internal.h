@@ -333,6 +333,18 @@ void launch_step(const StepParams &p, int blocks, int threads, int smem, void *s
 void launch_node(const NodeParams &p, void *stream);
 void launch_strip_copy(const Strip *src, const int32_t *sslot, Strip *dst, const int32_t *dslot,
                        int64_t n, void *stream);
+// Direct strip delivery among the in-process domains of one device (one
+// kernel per exchange instead of pack + copies + unpack): entry j moves
+// strip sslot of handle sh to slot dslot of handle dh, between the handles'
+// current strip buffers
+constexpr int kDirectMax = 64;  // domains of one partition
+struct DirectParams {
+  const Strip *src[kDirectMax];
+  Strip *dst[kDirectMax];
+  const int4 *plan;  // (sh, sslot, dh, dslot) per strip
+  int64_t n;
+};
+void launch_strip_direct(const DirectParams &p, void *stream);
 void launch_hash(const StepParams &p, int blocks, int threads, int smem, void *stream,
                  unsigned long long *out);
 void launch_rows_hash(const StepParams &p, const RowsParams &r, void *stream,

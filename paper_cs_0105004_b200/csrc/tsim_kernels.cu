@@ -698,7 +698,24 @@ __global__ void __launch_bounds__(256) k_strip_copy(const Strip *src, const int3
   reinterpret_cast<uint32_t *>(dst + d)[w] = reinterpret_cast<const uint32_t *>(src + s)[w];
 }
 
+// direct delivery: one 4-byte word of one strip per thread
+__global__ void __launch_bounds__(256) k_strip_direct(const DirectParams P) {
+  constexpr int kW = sizeof(Strip) / 4;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= P.n * kW) return;
+  const int64_t j = i / kW;
+  const int w = (int)(i - j * kW);
+  const int4 e = P.plan[j];
+  reinterpret_cast<uint32_t *>(P.dst[e.z] + e.w)[w] =
+      reinterpret_cast<const uint32_t *>(P.src[e.x] + e.y)[w];
+}
+
 // ------------------------------------------------------------ launchers
+void launch_strip_direct(const DirectParams &p, void *stream) {
+  if (p.n <= 0) return;
+  const int64_t words = p.n * (int64_t)(sizeof(Strip) / 4);
+  k_strip_direct<<<(unsigned)((words + 255) / 256), 256, 0, (cudaStream_t)stream>>>(p);
+}
 void launch_strip_copy(const Strip *src, const int32_t *sslot, Strip *dst, const int32_t *dslot,
                        int64_t n, void *stream) {
   if (n <= 0) return;
