@@ -496,11 +496,8 @@ __device__ __forceinline__ Cand node_candidate(const NodeParams &P, uint64_t rec
 // the winner's grant: returns ext; writes the entrant record if it crosses.
 // head: occupancy of the first cells of the target lane.  The route
 // position record (16 bytes per vehicle) is read only for a crossing.
-// pre: the winner's route position and next out-slot when prefetched (qp >=
-// 0), else they are read here for a crossing
 __device__ __forceinline__ int node_grant(const NodeParams &P, const Cand &c, int vk, uint8_t head,
-                                          uint32_t &crossings, bool pass = false,
-                                          int64_t qp = -1, int pre_slot = 0) {
+                                          uint32_t &crossings, bool pass = false) {
   const int E = min(ctz32((uint32_t)head | 0x20u), min(kGmax, c.n2));
   if (E == 0) return 0;
   const int v3 = nasch_v3(c.v, vk, min(kGmax, c.d + E), (uint32_t)P.t, (uint32_t)c.vid, P.k0,
@@ -508,14 +505,9 @@ __device__ __forceinline__ int node_grant(const NodeParams &P, const Cand &c, in
   if (v3 > c.d) {
     int nslot = 0;  // pass-through node of a ring: straight on, same route position
     if (!pass) {
-      if (qp >= 0) {
-        nslot = pre_slot;
-        P.vpos[c.vid].p = qp + 1;
-      } else {
-        const VehPos q = P.vpos[c.vid];
-        nslot = (q.p + 2 < q.e) ? (int)P.rslot[q.p + 2] : kSlotFinal;
-        P.vpos[c.vid].p = q.p + 1;
-      }
+      const VehPos q = P.vpos[c.vid];
+      nslot = (q.p + 2 < q.e) ? (int)P.rslot[q.p + 2] : kSlotFinal;
+      P.vpos[c.vid].p = q.p + 1;
     }
     const int y2 = v3 - c.d - 1;
     const uint64_t rec = (uint64_t)(uint32_t)c.vid | ((uint64_t)(v3 | (nslot << 3)) << 32) |
@@ -550,9 +542,6 @@ __device__ __forceinline__ void node_flush(const NodeParams &P, uint32_t crossin
 #define TS_NODE_ILP 1  // measured on 4a: 1 -> 31.5 us, 2 -> 35, 4 -> 39.6, 8 -> 49.6
 #endif
 constexpr int kNodeILP = TS_NODE_ILP;
-#ifndef TS_NODE_PREFETCH
-#define TS_NODE_PREFETCH 1  // winners' route position and next out-slot fetched ahead of the grant
-#endif
 __global__ void __launch_bounds__(256) k_node_warp(const NodeParams P_, const NodeWarpParams W) {
   const NodeParams P = with_time(P_);
   __shared__ unsigned long long red[8];
@@ -598,25 +587,14 @@ __global__ void __launch_bounds__(256) k_node_warp(const NodeParams P_, const No
     win[k] = eligible && (__ffs(grp) - 1) == lane;
   }
   uint8_t head[kNodeILP];
-  int64_t qp[kNodeILP];
-  int nslot[kNodeILP];
 #pragma unroll
-  for (int k = 0; k < kNodeILP; k++) {  // stage 3: target heads; the winners' route
-    head[k] = win[k] ? P.head_occ[cd[k].tgt] : (uint8_t)0;  // positions and next out-slots,
-    qp[k] = -1;                                             // fetched before the grant knows
-    nslot[k] = 0;                                           // whether they cross
-    if (TS_NODE_PREFETCH && win[k] && !(e[k].major & 2)) {
-      const VehPos q = P.vpos[cd[k].vid];
-      qp[k] = q.p;
-      nslot[k] = (q.p + 2 < q.e) ? (int)P.rslot[q.p + 2] : kSlotFinal;
-    }
-  }
+  for (int k = 0; k < kNodeILP; k++)  // stage 3: target heads
+    head[k] = win[k] ? P.head_occ[cd[k].tgt] : (uint8_t)0;
 #pragma unroll
   for (int k = 0; k < kNodeILP; k++) {  // stage 4: grants
     int ext = 0;
     const uint32_t cr0 = crossings;
-    if (win[k])
-      ext = node_grant(P, cd[k], e[k].vk, head[k], crossings, (e[k].major & 2) != 0, qp[k], nslot[k]);
+    if (win[k]) ext = node_grant(P, cd[k], e[k].vk, head[k], crossings, (e[k].major & 2) != 0);
     if (act[k]) {
       P.ext[32 * (c0 + k) + lane] = (uint8_t)ext;
       const int row = W.nl_row[32 * (c0 + k) + lane];
