@@ -120,29 +120,6 @@ __device__ __forceinline__ int warp_scan(int v, int lane, int *total) {
   *total = __shfl_sync(FULL, s, 31);
   return s - v;
 }
-// coalesced warp copies of n entries between 16-byte aligned buffers
-__device__ __forceinline__ void warp_load(int32_t *dst, const int32_t *gsrc, int n, int lane) {
-  const int n4 = n >> 2;
-  for (int i = lane; i < n4; i += 32)
-    reinterpret_cast<int4 *>(dst)[i] = __ldcs(reinterpret_cast<const int4 *>(gsrc) + i);
-  for (int i = 4 * n4 + lane; i < n; i += 32) dst[i] = __ldcs(gsrc + i);
-}
-// asynchronous variant of warp_load (cp.async, no register round trip):
-// 16-byte copies of the first n & ~3 entries, the tail entry by entry;
-// completes at cp_async_wait()
-__device__ __forceinline__ void warp_load_async(int32_t *dst, const int32_t *gsrc, int n, int lane) {
-  const int n4 = n >> 2;
-  for (int i = lane; i < n4; i += 32) {
-    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst + 4 * i);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gsrc + 4 * i) : "memory");
-  }
-  for (int i = 4 * n4 + lane; i < n; i += 32) {
-    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst + i);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(gsrc + i) : "memory");
-  }
-  asm volatile("cp.async.commit_group;" ::: "memory");
-}
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 // one-lane bulk (TMA) store of n entries of shared memory to global memory;
 // both 16-byte aligned, the byte count rounded up to 16 (the destination
 // block has room: group capacities are multiples of 4 entries)
@@ -189,12 +166,6 @@ __device__ __forceinline__ void red_or_shared(uint32_t saddr, uint32_t v) {
 // the bulk stores of this thread have finished reading shared memory
 __device__ __forceinline__ void bulk_wait_read() {
   asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-}
-__device__ __forceinline__ void warp_store(int32_t *gdst, const int32_t *src, int n, int lane) {
-  const int n4 = n >> 2;
-  for (int i = lane; i < n4; i += 32)
-    __stcs(reinterpret_cast<int4 *>(gdst) + i, reinterpret_cast<const int4 *>(src)[i]);
-  for (int i = 4 * n4 + lane; i < n; i += 32) __stcs(gdst + i, src[i]);
 }
 }  // namespace
 
@@ -260,6 +231,9 @@ static __device__ __noinline__ uint32_t zone_lc(uint32_t zc, int c0, int w, int 
   return lv;
 }
 
+#ifndef TS_ROWS_INJ_TMPL
+#define TS_ROWS_INJ_TMPL 1  // injection as a template mode bit (else a runtime test)
+#endif
 #ifndef TS_ROWS_DRAW_RK
 #define TS_ROWS_DRAW_RK 1  // Philox round keys from the launch parameters
 #endif
@@ -268,14 +242,42 @@ static __device__ __noinline__ uint32_t zone_lc(uint32_t zc, int c0, int w, int 
 #else
 #define PHILOX_DRAW(e) philox_w0((uint32_t)P.t, (e) & kVidMask, P.k0, P.k1)
 #endif
+// The slowdown draws of a group whose vid block is not staged (more vehicles
+// than the staging capacity; rare): the mover list in chunks of the
+// capacity, vids from global memory; brake bits into bw[row * NW + word]
+static __device__ __noinline__ void draws_unstaged(RowWords U1, RowWords O, int lane, int in_off,
+                                                   int moff, int mtot, int cap, int32_t *mlist,
+                                                   uint32_t *bw, const int32_t *vbase, uint32_t t,
+                                                   uint32_t k0, uint32_t k1, uint64_t p32) {
+  for (int base = 0; base < mtot; base += cap) {
+    int j = moff - base, rb = in_off;
+#pragma unroll 1
+    for (int i = 0; i < kRowWords; i++) {
+      uint32_t m = U1.w[i];
+      const uint32_t o = O.w[i];
+      while (m) {
+        const int x = __ffs(m) - 1;
+        m &= m - 1u;
+        if (j >= 0 && j < cap)
+          mlist[j] = ((rb + __popc(o & ((1u << x) - 1u))) << 12) | (lane << 7) | (32 * i + x);
+        j++;
+      }
+      rb += __popc(o);
+    }
+    __syncwarp();
+    const int n = min(mtot - base, cap);
+    for (int jj = lane; jj < n; jj += 32) {
+      const uint32_t me = (uint32_t)mlist[jj];
+      const uint32_t e = (uint32_t)vbase[me >> 12];
+      if ((uint64_t)philox_w0(t, e & kVidMask, k0, k1) < p32)
+        atomicOr(bw + ((me >> 5) & 127u), 1u << (me & 31u));
+    }
+    __syncwarp();
+  }
+}
+
 #ifndef TS_ROWS_MINB
 #define TS_ROWS_MINB (512 / TS_ROWS_TPB)  // resident blocks per SM: 128 registers (96 measured 2.5% slower)
-#endif
-#ifndef TS_ROWS_TMA_IN
-#define TS_ROWS_TMA_IN 1  // vid block in by one TMA bulk copy (else cp.async pieces)
-#endif
-#ifndef TS_ROWS_ASYNC
-#define TS_ROWS_ASYNC 1  // vid blocks: cp.async in, bulk (TMA) store out
 #endif
 // MODE = the uniform mode bits kModeMove | kModeLC | kModeHash of the launch
 // (specialised so the hot fused instantiation carries no dead paths)
@@ -294,6 +296,7 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
   constexpr bool hash = (MODE & kModeHash) != 0;
   constexpr bool lc = (MODE & kModeLC) != 0;
   constexpr bool halo = (MODE & kModeHalo) != 0;  // ring segment rows
+  constexpr bool inject = (MODE & kModeInject) != 0;  // injection from parking (pending trips)
   const int lct = do_move ? P.t + 1 : P.t;  // time of the lane-change sub-step
   const int dir = (lct & 1) ? -1 : +1;      // R4
   Acc acc = {};
@@ -317,7 +320,7 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
   uint64_t *bar = &vbar[threadIdx.x >> 5], *pbar = &pvbar[threadIdx.x >> 5];
   uint32_t bar_phase = 0, pbar_phase = 0;
   if (lane == 0) {
-    if (TS_ROWS_TMA_IN) mbar_init(bar);
+    mbar_init(bar);
     if (TS_ROWS_PPF) mbar_init(pbar);
   }
   __syncwarp();
@@ -346,7 +349,7 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
     const int g = g_next;
     if (g >= R.ngroups) break;
     g_next = grab();
-    if (TS_ROWS_ASYNC && lane == 0) bulk_wait_read();  // the previous group's output block
+    if (lane == 0) bulk_wait_read();  // the previous group's output block
     uint32_t O[NW], V0[NW], V1[NW], V2[NW], A0[NW], A1[NW];
     if (!TS_ROWS_PPF) {  // the planes first: they depend on nothing
       const uint32_t *pin = R.planes_in + group_plane_base(g) + lane;
@@ -381,18 +384,10 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
     // staged in shared memory when it fits, loaded together with the planes
     const int tot_in = tot_n;
     const bool staged = tot_in <= R.cap;
-    const bool tma_in = TS_ROWS_TMA_IN && staged && tot_in > 0;
-    if (staged) {
-      if (tma_in) {
-        if (lane == 0) {  // the previous group's generic reads of s_in come first
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          bulk_load(s_in, R.vid_in + voff, tot_in, bar);
-        }
-      } else if (TS_ROWS_ASYNC) {
-        warp_load_async(s_in, R.vid_in + voff, tot_in, lane);
-      } else {
-        warp_load(s_in, R.vid_in + voff, tot_in, lane);
-      }
+    const bool tma_in = staged && tot_in > 0;
+    if (tma_in && lane == 0) {  // the previous group's generic reads of s_in come first
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      bulk_load(s_in, R.vid_in + voff, tot_in, bar);
     }
     const bool pl_next = TS_ROWS_PPF && g_next < R.ngroups;
     if (pl_next) issue_planes(g_next);  // committed after the vid block
@@ -408,7 +403,7 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
     const uint64_t ent_raw = do_move ? P.entr_row[(size_t)g * 32 + lane] : 0ull;
     const int ext_lg = do_move0 ? ext_raw : 0;
     const uint64_t ent_rec = do_move0 ? ent_raw : 0ull;
-    const bool may_inject = (P.mode & kModeInject) && w > 0 && l == 0 &&
+    const bool may_inject = (TS_ROWS_INJ_TMPL ? inject : (P.mode & kModeInject) != 0) && w > 0 && l == 0 &&
                             P.pend_off[link + 1] > P.pend_head[link];
     uint32_t VAL[NW];
 #pragma unroll
@@ -416,17 +411,11 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
     const int nin = popc_row(O);
     int tot_chk;
     const int in_off = warp_scan(nin, lane, &tot_chk);
-    if (staged) {
-      if (TS_ROWS_ASYNC) {
-        if (tma_in) {
-          mbar_wait(bar, bar_phase);
-          bar_phase ^= 1u;
-        } else {
-          cp_async_wait();
-        }
-      }
-      __syncwarp();
+    if (tma_in) {
+      mbar_wait(bar, bar_phase);
+      bar_phase ^= 1u;
     }
+    __syncwarp();
     const int32_t *vin = (staged ? (const int32_t *)s_in : R.vid_in + voff) + in_off;
     acc.work += nin;
     if ((P.mode & kModeWork) && P.link_work && nin)
@@ -497,38 +486,14 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
         int mtot;
         const int mc = popc_row(U1);
         const int moff = warp_scan(mc, lane, &mtot);
-        const int32_t *vbase = staged ? (const int32_t *)s_in : R.vid_in + voff;
-        // mover list entries: block offset << 12 | row slot << 7 | cell, in
-        // chunks of the staging capacity (one chunk unless the group is huge)
+        // mover list entries: block offset << 12 | row slot << 7 | cell
         int32_t *mlist = s_out;  // free until the output phase
         uint32_t *bw = reinterpret_cast<uint32_t *>(s_out + R.cap);
 #pragma unroll
         for (int i = 0; i < NW; i++) bw[lane * NW + i] = 0u;  // this row's brake bits
-        // the draws of list entries [0, n): the vid from the staged block
-        // (shared memory) or the global one; brake bit by a shared-memory
-        // reduction at word (row slot * NW + word) = (entry >> 5) & 127
-        const uint32_t bw_s = (uint32_t)__cvta_generic_to_shared(bw);
         // brake iff u < p32, i.e. u <= p32 - 1 (p32 in [1, 2^32]; p32 = 0 draws nothing)
         const uint32_t p32m1 = (uint32_t)(P.p32 - 1);
-        auto draw = [&](int n) {
-          if (P.p32 == 0) return;
-          if (staged) {
-            for (int jj = lane; jj < n; jj += 32) {
-              const uint32_t me = (uint32_t)mlist[jj];
-              const uint32_t e = (uint32_t)s_in[me >> 12];
-              if (PHILOX_DRAW(e) <= p32m1)
-                red_or_shared(bw_s + (((me >> 5) & 127u) << 2), 1u << (me & 31u));
-            }
-          } else {
-            for (int jj = lane; jj < n; jj += 32) {
-              const uint32_t me = (uint32_t)mlist[jj];
-              const uint32_t e = (uint32_t)vbase[me >> 12];
-              if (PHILOX_DRAW(e) <= p32m1)
-                red_or_shared(bw_s + (((me >> 5) & 127u) << 2), 1u << (me & 31u));
-            }
-          }
-        };
-        if (mtot <= R.cap) {  // one chunk (the common case): no bounds checks
+        if (staged) {  // mtot <= tot_in <= cap: the whole list fits
           int j = moff, rb = in_off;
 #pragma unroll
           for (int i = 0; i < NW; i++) {
@@ -543,29 +508,26 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
             rb += __popc(o);
           }
           __syncwarp();
-          draw(mtot);
-          __syncwarp();
-        } else {
-          for (int base = 0; base < mtot; base += R.cap) {
-            int j = moff - base, rb = in_off;
-#pragma unroll 1
-            for (int i = 0; i < NW; i++) {
-              uint32_t m = pick(U1, i);
-              const uint32_t o = pick(O, i);
-              while (m) {
-                const int x = __ffs(m) - 1;
-                m &= m - 1u;
-                if (j >= 0 && j < R.cap)
-                  mlist[j] = ((rb + __popc(o & ((1u << x) - 1u))) << 12) | (lane << 7) | (32 * i + x);
-                j++;
-              }
-              rb += __popc(o);
+          // the draws: the vid from the staged block; brake bit by a shared-
+          // memory reduction at word (row slot * NW + word) = (entry >> 5) & 127
+          const uint32_t bw_s = (uint32_t)__cvta_generic_to_shared(bw);
+          if (P.p32 != 0)
+            for (int jj = lane; jj < mtot; jj += 32) {
+              const uint32_t me = (uint32_t)mlist[jj];
+              const uint32_t e = (uint32_t)s_in[me >> 12];
+              if (PHILOX_DRAW(e) <= p32m1)
+                red_or_shared(bw_s + (((me >> 5) & 127u) << 2), 1u << (me & 31u));
             }
-            __syncwarp();
-            const int n = min(mtot - base, R.cap);
-            draw(n);
-            __syncwarp();
+          __syncwarp();
+        } else {  // a group larger than the staging (rare): out of line
+          RowWords u1w, ow;
+#pragma unroll
+          for (int i = 0; i < NW; i++) {
+            u1w.w[i] = U1[i];
+            ow.w[i] = O[i];
           }
+          draws_unstaged(u1w, ow, lane, in_off, moff, mtot, R.cap, mlist, bw, R.vid_in + voff,
+                         (uint32_t)P.t, P.k0, P.k1, P.p32);
         }
 #pragma unroll
         for (int i = 0; i < NW; i++) Bm[i] = bw[lane * NW + i];
@@ -820,7 +782,7 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
     // the state hash (tests) is taken below for every row, so hashed runs
     // take exactly the vid-list paths of the unhashed (benchmarked) runs
     const bool changed = moved_lc || injected;
-    const bool ginj = __any_sync(FULL, injected);
+    const bool ginj = inject && __any_sync(FULL, injected);
     if (!changed && nfin > 0) {
       // input vehicles minus an exit at the front (a prefix of the input
       // list), shifted by one when the entrant lands behind every vehicle
@@ -944,16 +906,10 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
                            R.row_a ? R.row_a[g * 32 + lane] : 0);
     }
     // the output block's shared-memory writes become visible to the bulk copy
-    if (TS_ROWS_ASYNC) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncwarp();
     const uint32_t efin = nfin > 0 ? (uint32_t)vout[nfin - 1] : 0u;  // final front vehicle
-    if (ostaged) {
-      if (TS_ROWS_ASYNC) {
-        if (lane == 0 && tot_out > 0) bulk_store(R.vid_out + voff, s_out, tot_out);
-      } else {
-        warp_store(R.vid_out + voff, s_out, tot_out, lane);
-      }
-    }
+    if (ostaged && lane == 0 && tot_out > 0) bulk_store(R.vid_out + voff, s_out, tot_out);
     if (lane == 0) R.gcnt_out[g] = tot_out;
     // ---- node records of the output S1 (read by k_node_warp, H3)
     if (lc && w > 0) {
@@ -973,7 +929,7 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
       P.head_occ[lg] = (uint8_t)(FO[0] & lowm(nb));
     }
   }
-  if (TS_ROWS_ASYNC && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   flush_acc(P, acc, P.t + 1, red);
   if (lc) flush_acc(P, acc_next, lct + 1, red);
 }
@@ -1019,14 +975,18 @@ __global__ void __launch_bounds__(128) k_rows_hash(const RowsParams R, unsigned 
   }
 }
 
+// the mode bits that select an instantiation (injection only while trips
+// are pending, so the hot instantiation of a fully placed network carries
+// no injection code)
+constexpr int kRowsModeMask = kModeMove | kModeLC | kModeHash | kModeHalo | (TS_ROWS_INJ_TMPL ? kModeInject : 0);
+#define TS_ROWS_CASES(X)                                                                       \
+  X(0) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) X(36) X(44)
 void launch_rows(const StepParams &p, const RowsParams &r, int blocks, int threads, int smem,
                  void *stream, bool pdl) {
-  switch (p.mode & (kModeMove | kModeLC | kModeHash | kModeHalo)) {
+  switch (p.mode & kRowsModeMask) {
 #define TS_ROWS_CASE(m) \
   case m: launch_pdl(k_rows<m>, blocks, threads, smem, stream, pdl, p, r); break;
-    TS_ROWS_CASE(0) TS_ROWS_CASE(1) TS_ROWS_CASE(4) TS_ROWS_CASE(5)
-    TS_ROWS_CASE(8) TS_ROWS_CASE(9) TS_ROWS_CASE(12) TS_ROWS_CASE(13)
-    TS_ROWS_CASE(36) TS_ROWS_CASE(44)
+    TS_ROWS_CASES(TS_ROWS_CASE)
 #undef TS_ROWS_CASE
   }
 }
@@ -1044,17 +1004,10 @@ cudaError_t set_rows_smem(int bytes) {  // only ever raised (see set_smem_attrs)
   if (bytes <= current[dev]) return cudaSuccess;
   current[dev] = bytes;
   cudaError_t e = cudaSuccess;
-  for (cudaError_t x : {cudaFuncSetAttribute(k_rows<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
-                        cudaFuncSetAttribute(k_rows<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
-                        cudaFuncSetAttribute(k_rows<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
-                        cudaFuncSetAttribute(k_rows<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
-                        cudaFuncSetAttribute(k_rows<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
-                        cudaFuncSetAttribute(k_rows<9>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
-                        cudaFuncSetAttribute(k_rows<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
-                        cudaFuncSetAttribute(k_rows<13>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
-                        cudaFuncSetAttribute(k_rows<36>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
-                        cudaFuncSetAttribute(k_rows<44>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes)})
-    if (x != cudaSuccess) e = x;
+#define TS_ROWS_ATTR(m) \
+  if (cudaError_t x = cudaFuncSetAttribute(k_rows<m>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes)) e = x;
+  TS_ROWS_CASES(TS_ROWS_ATTR)
+#undef TS_ROWS_ATTR
   return e;
 }
 int occupancy_rows(int threads, int smem) {
