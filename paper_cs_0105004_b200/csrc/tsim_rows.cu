@@ -276,6 +276,142 @@ static __device__ __noinline__ void draws_unstaged(RowWords U1, RowWords O, int 
   }
 }
 
+// Vid lists of the final state (the group's output block): rows whose
+// vehicle set only lost its front or gained a back entrant are (shifted)
+// prefix copies of their input list; rows whose set changed inside (lane
+// changes, injections) scatter every vehicle of S(t+1) before the lane
+// change to its rank in the final occupancy of its row (own, or l + dir),
+// 32 at a time across the warp from the rows' masks published in aux.
+// ibase / obase: the group's input / output block (shared memory when
+// staged, else global); inj_scratch: the group's injection scratch.
+template <int NWT>
+__device__ __forceinline__ void vid_lists(const int32_t *ibase, int32_t *obase, int32_t *aux,
+                                          const uint32_t (&OO)[NWT], const uint32_t (&FO)[NWT],
+                                          const uint32_t (&LV)[NWT], const uint32_t (&INJ)[NWT],
+                                          int nfin, int in_off, int out_off, bool has_ent, int ent_y,
+                                          uint32_t ent_e, bool changed, bool ginj, int dir,
+                                          int lane, const int32_t *inj_scratch) {
+  constexpr int NW = NWT;
+  const int32_t *vin = ibase + in_off;
+  int32_t *vout = obase + out_off;
+  if (!changed && nfin > 0) {
+    // input vehicles minus an exit at the front (a prefix of the input
+    // list), shifted by one when the entrant lands behind every vehicle
+    const int sh = has_ent ? 1 : 0;
+    if (has_ent) vout[0] = (int32_t)ent_e;
+    int i = sh;
+    for (; i + 4 <= nfin; i += 4) {
+      const int32_t a0 = vin[i - sh], a1 = vin[i + 1 - sh], a2 = vin[i + 2 - sh],
+                    a3 = vin[i + 3 - sh];
+      vout[i] = a0;
+      vout[i + 1] = a1;
+      vout[i + 2] = a2;
+      vout[i + 3] = a3;
+    }
+    for (; i < nfin; i++) vout[i] = vin[i - sh];
+  }
+  if (const uint32_t gmask = __ballot_sync(FULL, changed)) {
+    // rows whose vehicle set changed inside (lane changes, injections):
+    // every vehicle of S(t+1) before the lane change goes to its rank in
+    // the final occupancy of its row (own, or l + dir).  The vehicles of
+    // all such rows are processed 32 at a time across the warp from the
+    // rows' masks published in shared memory.
+    uint32_t *rOO = reinterpret_cast<uint32_t *>(aux), *rFO = rOO + 32 * NW,
+             *rLV = rFO + 32 * NW, *rIN = rLV + 32 * NW;
+    int32_t *mInOff = aux + 4 * 32 * NW, *mOutOff = mInOff + 32, *mEnt = mOutOff + 32,
+            *mEntE = mEnt + 32, *mItem = mEntE + 32;  // mItem: 33 entries
+    // per row: popcount prefixes of the OO / FO words (bytes 1..3: words 0,
+    // 0-1, 0-2), so an item finds its word and its rank without loops
+    uint32_t *pOO = reinterpret_cast<uint32_t *>(mItem + 36), *pFO = pOO + 32;
+    {
+      uint32_t po = 0u, pf = 0u;
+      int so = 0, sf = 0;
+#pragma unroll
+      for (int i = 0; i < NW; i++) {
+        rOO[lane * NW + i] = OO[i];
+        rFO[lane * NW + i] = FO[i];
+        rLV[lane * NW + i] = LV[i];
+        if (ginj) rIN[lane * NW + i] = INJ[i];
+        if (i > 0) {
+          po |= (uint32_t)so << (8 * i);
+          pf |= (uint32_t)sf << (8 * i);
+        }
+        so += __popc(OO[i]);
+        sf += __popc(FO[i]);
+      }
+      pOO[lane] = po;
+      pFO[lane] = pf;
+    }
+    mInOff[lane] = in_off;
+    mOutOff[lane] = out_off;
+    mEnt[lane] = ent_y;
+    mEntE[lane] = (int32_t)ent_e;
+    int itot;
+    const int ioff = warp_scan(changed ? popc_row(OO) : 0, lane, &itot);
+    mItem[lane] = ioff;
+    if (lane == 0) mItem[32] = itot;
+    __syncwarp();
+    for (int J = lane; J < itot; J += 32) {
+      // the row of item J: the last row whose first item is <= J
+      int r0 = 0;
+#pragma unroll
+      for (int st = 16; st; st >>= 1)
+        if (mItem[r0 + st] <= J) r0 += st;
+      const int rr = J - mItem[r0];  // rank of the vehicle in the row's OO
+      // the word holding set bit number rr, and the rank inside it
+      const uint32_t po = pOO[r0];
+      const int p1 = (int)((po >> 8) & 0xFF), p2 = (int)((po >> 16) & 0xFF), p3 = (int)(po >> 24);
+      const int wi = (rr >= p1) + (rr >= p2) + (rr >= p3);
+      uint32_t wsel = rOO[r0 * NW + wi];
+      int c = 32 * wi, k2 = rr - (int)((po >> (8 * wi)) & 0xFF);
+      {  // select bit k2 of wsel by popcount halving
+        uint32_t m = wsel;
+        int pos = 0, cnt = __popc(m & 0xFFFFu);
+        if (k2 >= cnt) { k2 -= cnt; pos = 16; m >>= 16; }
+        cnt = __popc(m & 0xFFu);
+        if (k2 >= cnt) { k2 -= cnt; pos += 8; m >>= 8; }
+        cnt = __popc(m & 0xFu);
+        if (k2 >= cnt) { k2 -= cnt; pos += 4; m >>= 4; }
+        cnt = __popc(m & 0x3u);
+        if (k2 >= cnt) { k2 -= cnt; pos += 2; m >>= 2; }
+        c += pos + (k2 >= (int)(m & 1u) ? 1 : 0);
+      }
+      const int ci = c >> 5;
+      const uint32_t bit = 1u << (c & 31), lowb = bit - 1u;
+      const uint32_t inj_w = ginj ? rIN[r0 * NW + ci] : 0u;
+      uint32_t e;
+      if (c == mEnt[r0]) {
+        e = (uint32_t)mEntE[r0];
+      } else if (inj_w & bit) {
+        e = (uint32_t)inj_scratch[(size_t)r0 * kRowMaxCells + c];
+      } else {
+        int ninj = 0;
+        if (ginj) {
+          ninj = __popc(inj_w & lowb);
+          for (int i = 0; i < ci; i++) ninj += __popc(rIN[r0 * NW + i]);
+        }
+        const int me = (mEnt[r0] >= 0 && mEnt[r0] < c) ? 1 : 0;
+        e = (uint32_t)ibase[mInOff[r0] + rr - me - ninj];
+      }
+      const int dst = (rLV[r0 * NW + ci] & bit) ? r0 + dir : r0;
+      const int rank = __popc(rFO[dst * NW + ci] & lowb) + (int)((pFO[dst] >> (8 * ci)) & 0xFF);
+      obase[mOutOff[dst] + rank] = (int32_t)e;
+    }
+  }
+}
+
+// the same out of line, for groups whose blocks are not staged (rare)
+static __device__ __noinline__ void vid_lists_global(const int32_t *ibase, int32_t *obase,
+                                                     int32_t *aux, RowWords OO, RowWords FO,
+                                                     RowWords LV, RowWords INJ, int nfin,
+                                                     int in_off, int out_off, bool has_ent,
+                                                     int ent_y, uint32_t ent_e, bool changed,
+                                                     bool ginj, int dir, int lane,
+                                                     const int32_t *inj_scratch) {
+  vid_lists(ibase, obase, aux, OO.w, FO.w, LV.w, INJ.w, nfin, in_off, out_off, has_ent, ent_y,
+            ent_e, changed, ginj, dir, lane, inj_scratch);
+}
+
 #ifndef TS_ROWS_MINB
 #define TS_ROWS_MINB (512 / TS_ROWS_TPB)  // resident blocks per SM: 128 registers (96 measured 2.5% slower)
 #endif
@@ -783,113 +919,22 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
     // take exactly the vid-list paths of the unhashed (benchmarked) runs
     const bool changed = moved_lc || injected;
     const bool ginj = inject && __any_sync(FULL, injected);
-    if (!changed && nfin > 0) {
-      // input vehicles minus an exit at the front (a prefix of the input
-      // list), shifted by one when the entrant lands behind every vehicle
-      const int sh = has_ent ? 1 : 0;
-      if (has_ent) vout[0] = (int32_t)ent_e;
-      int i = sh;
-      for (; i + 4 <= nfin; i += 4) {
-        const int32_t a0 = vin[i - sh], a1 = vin[i + 1 - sh], a2 = vin[i + 2 - sh],
-                      a3 = vin[i + 3 - sh];
-        vout[i] = a0;
-        vout[i + 1] = a1;
-        vout[i + 2] = a2;
-        vout[i + 3] = a3;
-      }
-      for (; i < nfin; i++) vout[i] = vin[i - sh];
-    }
-    const bool general = changed;
-    if (const uint32_t gmask = __ballot_sync(FULL, general)) {
-      // rows whose vehicle set changed inside (lane changes, injections):
-      // every vehicle of S(t+1) before the lane change goes to its rank in
-      // the final occupancy of its row (own, or l + dir).  The vehicles of
-      // all such rows are processed 32 at a time across the warp from the
-      // rows' masks published in shared memory.
-      int32_t *aux = s_out + R.cap;  // brake bits are dead by now
-      uint32_t *rOO = reinterpret_cast<uint32_t *>(aux), *rFO = rOO + 32 * NW,
-               *rLV = rFO + 32 * NW, *rIN = rLV + 32 * NW;
-      int32_t *mInOff = aux + 4 * 32 * NW, *mOutOff = mInOff + 32, *mEnt = mOutOff + 32,
-              *mEntE = mEnt + 32, *mItem = mEntE + 32;  // mItem: 33 entries
-      // per row: popcount prefixes of the OO / FO words (bytes 1..3: words 0,
-      // 0-1, 0-2), so an item finds its word and its rank without loops
-      uint32_t *pOO = reinterpret_cast<uint32_t *>(mItem + 36), *pFO = pOO + 32;
-      {
-        uint32_t po = 0u, pf = 0u;
-        int so = 0, sf = 0;
+    const int32_t *scr = R.inj_scratch + (size_t)g * 32 * kRowMaxCells;
+    if (staged && ostaged) {  // shared-memory blocks (the common case)
+      vid_lists(s_in, s_out, s_out + R.cap, OO, FO, LV, INJ, nfin, in_off, out_off, has_ent, ent_y,
+                ent_e, changed, ginj, dir, lane, scr);
+    } else {
+      RowWords oo, fo, lv, inj;
 #pragma unroll
-        for (int i = 0; i < NW; i++) {
-          rOO[lane * NW + i] = OO[i];
-          rFO[lane * NW + i] = FO[i];
-          rLV[lane * NW + i] = LV[i];
-          if (ginj) rIN[lane * NW + i] = INJ[i];
-          if (i > 0) {
-            po |= (uint32_t)so << (8 * i);
-            pf |= (uint32_t)sf << (8 * i);
-          }
-          so += __popc(OO[i]);
-          sf += __popc(FO[i]);
-        }
-        pOO[lane] = po;
-        pFO[lane] = pf;
+      for (int i = 0; i < NW; i++) {
+        oo.w[i] = OO[i];
+        fo.w[i] = FO[i];
+        lv.w[i] = LV[i];
+        inj.w[i] = INJ[i];
       }
-      mInOff[lane] = in_off;
-      mOutOff[lane] = out_off;
-      mEnt[lane] = ent_y;
-      mEntE[lane] = (int32_t)ent_e;
-      int itot;
-      const int ioff = warp_scan(general ? popc_row(OO) : 0, lane, &itot);
-      mItem[lane] = ioff;
-      if (lane == 0) mItem[32] = itot;
-      __syncwarp();
-      const int32_t *ibase = staged ? (const int32_t *)s_in : R.vid_in + voff;
-      for (int J = lane; J < itot; J += 32) {
-        // the row of item J: the last row whose first item is <= J
-        int r0 = 0;
-#pragma unroll
-        for (int st = 16; st; st >>= 1)
-          if (mItem[r0 + st] <= J) r0 += st;
-        const int rr = J - mItem[r0];  // rank of the vehicle in the row's OO
-        // the word holding set bit number rr, and the rank inside it
-        const uint32_t po = pOO[r0];
-        const int p1 = (int)((po >> 8) & 0xFF), p2 = (int)((po >> 16) & 0xFF), p3 = (int)(po >> 24);
-        const int wi = (rr >= p1) + (rr >= p2) + (rr >= p3);
-        uint32_t wsel = rOO[r0 * NW + wi];
-        int c = 32 * wi, k2 = rr - (int)((po >> (8 * wi)) & 0xFF);
-        {  // select bit k2 of wsel by popcount halving
-          uint32_t m = wsel;
-          int pos = 0, cnt = __popc(m & 0xFFFFu);
-          if (k2 >= cnt) { k2 -= cnt; pos = 16; m >>= 16; }
-          cnt = __popc(m & 0xFFu);
-          if (k2 >= cnt) { k2 -= cnt; pos += 8; m >>= 8; }
-          cnt = __popc(m & 0xFu);
-          if (k2 >= cnt) { k2 -= cnt; pos += 4; m >>= 4; }
-          cnt = __popc(m & 0x3u);
-          if (k2 >= cnt) { k2 -= cnt; pos += 2; m >>= 2; }
-          c += pos + (k2 >= (int)(m & 1u) ? 1 : 0);
-        }
-        const int ci = c >> 5;
-        const uint32_t bit = 1u << (c & 31), lowb = bit - 1u;
-        const uint32_t inj_w = ginj ? rIN[r0 * NW + ci] : 0u;
-        uint32_t e;
-        if (c == mEnt[r0]) {
-          e = (uint32_t)mEntE[r0];
-        } else if (inj_w & bit) {
-          e = (uint32_t)R.inj_scratch[((size_t)g * 32 + r0) * kRowMaxCells + c];
-        } else {
-          int ninj = 0;
-          if (ginj) {
-            ninj = __popc(inj_w & lowb);
-            for (int i = 0; i < ci; i++) ninj += __popc(rIN[r0 * NW + i]);
-          }
-          const int me = (mEnt[r0] >= 0 && mEnt[r0] < c) ? 1 : 0;
-          e = (uint32_t)ibase[mInOff[r0] + rr - me - ninj];
-        }
-        const int dst = (rLV[r0 * NW + ci] & bit) ? r0 + dir : r0;
-        const int rank = __popc(rFO[dst * NW + ci] & lowb) + (int)((pFO[dst] >> (8 * ci)) & 0xFF);
-        obase[mOutOff[dst] + rank] = (int32_t)e;
-      }
-      (void)gmask;
+      vid_lists_global(staged ? (const int32_t *)s_in : R.vid_in + voff, obase, s_out + R.cap, oo,
+                       fo, lv, inj, nfin, in_off, out_off, has_ent, ent_y, ent_e, changed, ginj,
+                       dir, lane, scr);
     }
     if (hash && (do_move || !lc) && w > 0) {  // hash of S(t+1) before its lane change (tests)
       RowWords oo, v0, v1, v2, inj;
