@@ -234,14 +234,6 @@ static __device__ __noinline__ uint32_t zone_lc(uint32_t zc, int c0, int w, int 
 #ifndef TS_ROWS_INJ_TMPL
 #define TS_ROWS_INJ_TMPL 1  // injection as a template mode bit (else a runtime test)
 #endif
-#ifndef TS_ROWS_DRAW_RK
-#define TS_ROWS_DRAW_RK 1  // Philox round keys from the launch parameters
-#endif
-#if TS_ROWS_DRAW_RK
-#define PHILOX_DRAW(e) philox_w0_rk((uint32_t)P.t, (e) & kVidMask, P_.rk)
-#else
-#define PHILOX_DRAW(e) philox_w0((uint32_t)P.t, (e) & kVidMask, P.k0, P.k1)
-#endif
 // The slowdown draws of a group whose vid block is not staged (more vehicles
 // than the staging capacity; rare): the mover list in chunks of the
 // capacity, vids from global memory; brake bits into bw[row * NW + word]
@@ -647,11 +639,16 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
           // the draws: the vid from the staged block; brake bit by a shared-
           // memory reduction at word (row slot * NW + word) = (entry >> 5) & 127
           const uint32_t bw_s = (uint32_t)__cvta_generic_to_shared(bw);
+          // the Philox round keys (launch parameters) in registers for the
+          // whole loop, not reloaded per draw
+          uint32_t rk[20];
+#pragma unroll
+          for (int r = 0; r < 20; r++) rk[r] = __shfl_sync(FULL, P_.rk[r], 0);
           if (P.p32 != 0)
             for (int jj = lane; jj < mtot; jj += 32) {
               const uint32_t me = (uint32_t)mlist[jj];
               const uint32_t e = (uint32_t)s_in[me >> 12];
-              if (PHILOX_DRAW(e) <= p32m1)
+              if (philox_w0_rk((uint32_t)P.t, e & kVidMask, rk) <= p32m1)
                 red_or_shared(bw_s + (((me >> 5) & 127u) << 2), 1u << (me & 31u));
             }
           __syncwarp();
