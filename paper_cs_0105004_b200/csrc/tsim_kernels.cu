@@ -542,6 +542,8 @@ __device__ __forceinline__ void node_flush(const NodeParams &P, uint32_t crossin
 #define TS_NODE_ILP 1  // measured on 4a: 1 -> 31.5 us, 2 -> 35, 4 -> 39.6, 8 -> 49.6
 #endif
 constexpr int kNodeILP = TS_NODE_ILP;
+// SIG: the domain has signalized nodes; WORK: load statistics requested
+template <bool SIG, bool WORK>
 __global__ void __launch_bounds__(256) k_node_warp(const NodeParams P_, const NodeWarpParams W) {
   const NodeParams P = with_time(P_);
   __shared__ unsigned long long red[8];
@@ -552,13 +554,15 @@ __global__ void __launch_bounds__(256) k_node_warp(const NodeParams P_, const No
   NodeLane e[kNodeILP];
   uint64_t rec[kNodeILP];
   uint32_t sg[kNodeILP];
+  int row[kNodeILP];
   bool act[kNodeILP];
 #pragma unroll
   for (int k = 0; k < kNodeILP; k++) {  // stage 1: static lane data (before the wait)
     const int c = min(c0 + k, W.nchunks - 1), i = 32 * c + lane;  // node-lane index
     act[k] = c0 + k < W.nchunks;
     e[k] = W.lanes[i];
-    sg[k] = W.sig ? W.sig[i] : 0u;
+    sg[k] = SIG ? W.sig[i] : 0u;
+    row[k] = W.nl_row[i];
   }
   // programmatic dependent launch: the records of S1 are the previous
   // kernel's output; once it is complete the next move kernel may start
@@ -582,7 +586,7 @@ __global__ void __launch_bounds__(256) k_node_warp(const NodeParams P_, const No
     // signalized node (R23): red approaches have the virtual blocker, green
     // ones need no gap acceptance; otherwise priority + gap acceptance (R9)
     const bool eligible =
-        cd[k].cand && ((sg[k] >> 31) ? sig_green(sg[k], P.t) : (e[k].major || !busy));
+        cd[k].cand && ((SIG && (sg[k] >> 31)) ? sig_green(sg[k], P.t) : (e[k].major || !busy));
     const uint32_t grp = __match_any_sync(FULL, eligible ? cd[k].tgt : -1 - lane);
     win[k] = eligible && (__ffs(grp) - 1) == lane;
   }
@@ -597,10 +601,9 @@ __global__ void __launch_bounds__(256) k_node_warp(const NodeParams P_, const No
     if (win[k]) ext = node_grant(P, cd[k], e[k].vk, head[k], crossings, (e[k].major & 2) != 0);
     if (act[k]) {
       P.ext[32 * (c0 + k) + lane] = (uint8_t)ext;
-      const int row = W.nl_row[32 * (c0 + k) + lane];
-      if (row >= 0) P.ext_row[row] = (uint8_t)ext;
+      if (row[k] >= 0) P.ext_row[row[k]] = (uint8_t)ext;
     }
-    if (P.node_work) {  // load statistics: the node's lanes in range + its crossings
+    if (WORK) {  // load statistics: the node's lanes in range + its crossings
       const bool a = act[k] && e[k].lane_gid >= 0;
       const uint32_t nodemask = __match_any_sync(FULL, a ? (int)e[k].first : 64 + lane);
       const uint32_t wk = (uint32_t)((rec[k] >> 43) & 1) + (crossings - cr0);
@@ -749,7 +752,13 @@ void launch_clock(int32_t *clock, unsigned long long *stats, int n, bool advance
 void launch_node_warp(const NodeParams &p, const NodeWarpParams &w, void *stream, bool pdl) {
   if (w.nchunks <= 0) return;
   const int blocks = (w.nchunks + 8 * kNodeILP - 1) / (8 * kNodeILP);
-  launch_pdl(k_node_warp, blocks, 256, 0, stream, pdl, p, w);
+  if (w.sig) {
+    if (p.node_work) launch_pdl(k_node_warp<true, true>, blocks, 256, 0, stream, pdl, p, w);
+    else launch_pdl(k_node_warp<true, false>, blocks, 256, 0, stream, pdl, p, w);
+  } else {
+    if (p.node_work) launch_pdl(k_node_warp<false, true>, blocks, 256, 0, stream, pdl, p, w);
+    else launch_pdl(k_node_warp<false, false>, blocks, 256, 0, stream, pdl, p, w);
+  }
 }
 void launch_hash(const StepParams &p, int blocks, int threads, int smem, void *stream,
                  unsigned long long *out) {
