@@ -392,6 +392,87 @@ __device__ __forceinline__ void vid_lists(const int32_t *ibase, int32_t *obase, 
   }
 }
 
+// The vid lists of a group whose blocks are staged, without injections,
+// when the lane-change rows have at most kCellTab vehicles: as vid_lists,
+// but every lane-change row first lists its vehicles' cells in a table
+// (entry row << 8 | cell, rows one after another), so an item finds its row
+// and cell with one load instead of a binary search and a bit select.
+constexpr int kCellTab = 576;  // uint16 entries in the aux area rOO / pOO / rIN leave free
+template <int NWT>
+__device__ __forceinline__ void vid_lists_tab(const int32_t *ibase, int32_t *obase, int32_t *aux,
+                                              const uint32_t (&OO)[NWT], const uint32_t (&FO)[NWT],
+                                              const uint32_t (&LV)[NWT], int nfin, int in_off,
+                                              int out_off, bool has_ent, int ent_y, uint32_t ent_e,
+                                              bool changed, int ioff, int itot, int dir, int lane) {
+  constexpr int NW = NWT;
+  const int32_t *vin = ibase + in_off;
+  int32_t *vout = obase + out_off;
+  if (!changed && nfin > 0) {  // (shifted) prefix copy, as in vid_lists
+    const int sh = has_ent ? 1 : 0;
+    if (has_ent) vout[0] = (int32_t)ent_e;
+    int i = sh;
+    for (; i + 4 <= nfin; i += 4) {
+      const int32_t a0 = vin[i - sh], a1 = vin[i + 1 - sh], a2 = vin[i + 2 - sh],
+                    a3 = vin[i + 3 - sh];
+      vout[i] = a0;
+      vout[i + 1] = a1;
+      vout[i + 2] = a2;
+      vout[i + 3] = a3;
+    }
+    for (; i < nfin; i++) vout[i] = vin[i - sh];
+  }
+  if (itot == 0) return;  // warp-uniform
+  // aux layout: cell table (kCellTab uint16 = 288 words), rFO, rLV, the
+  // per-row scalars, mItem, pFO
+  uint16_t *ctab = reinterpret_cast<uint16_t *>(aux);
+  uint32_t *rFO = reinterpret_cast<uint32_t *>(aux) + kCellTab / 2, *rLV = rFO + 32 * NW;
+  int32_t *mInOff = reinterpret_cast<int32_t *>(rLV + 32 * NW), *mOutOff = mInOff + 32,
+          *mEnt = mOutOff + 32, *mItem = mEnt + 32;
+  uint32_t *pFO = reinterpret_cast<uint32_t *>(mItem + 32);
+  {
+    uint32_t pf = 0u;
+    int sf = 0;
+#pragma unroll
+    for (int i = 0; i < NW; i++) {
+      rFO[lane * NW + i] = FO[i];
+      rLV[lane * NW + i] = LV[i];
+      if (i > 0) pf |= (uint32_t)sf << (8 * i);
+      sf += __popc(FO[i]);
+    }
+    pFO[lane] = pf;
+  }
+  mInOff[lane] = in_off - (ent_y >= 0 ? 1 : 0);  // OO rank -> input index (entrant first)
+  mOutOff[lane] = out_off;
+  mEnt[lane] = ent_y >= 0 ? (int32_t)ent_e : -1;
+  mItem[lane] = ioff;
+  if (changed) {  // this row's vehicles (cells of OO, in order) into the table
+    int k = ioff;
+#pragma unroll
+    for (int i = 0; i < NW; i++) {
+      uint32_t m = OO[i];
+      while (m) {
+        const int x = __ffs(m) - 1;
+        m &= m - 1u;
+        ctab[k++] = (uint16_t)((lane << 8) | (32 * i + x));
+      }
+    }
+  }
+  __syncwarp();
+  for (int J = lane; J < itot; J += 32) {
+    const uint32_t it = ctab[J];
+    const int r0 = (int)(it >> 8), c = (int)(it & 0xFFu);
+    const int rr = J - mItem[r0];  // rank of the vehicle in the row's OO
+    // the entrant is the row's lowest vehicle (rank 0), then the input list
+    const uint32_t e = (rr == 0 && mEnt[r0] != -1) ? (uint32_t)mEnt[r0]
+                                                   : (uint32_t)ibase[mInOff[r0] + rr];
+    const int ci = c >> 5;
+    const uint32_t bit = 1u << (c & 31), lowb = bit - 1u;
+    const int dst = (rLV[r0 * NW + ci] & bit) ? r0 + dir : r0;
+    const int rank = __popc(rFO[dst * NW + ci] & lowb) + (int)((pFO[dst] >> (8 * ci)) & 0xFF);
+    obase[mOutOff[dst] + rank] = (int32_t)e;
+  }
+}
+
 // the same out of line, for groups whose blocks are not staged (rare)
 static __device__ __noinline__ void vid_lists_global(const int32_t *ibase, int32_t *obase,
                                                      int32_t *aux, RowWords OO, RowWords FO,
@@ -917,9 +998,11 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
     const bool changed = moved_lc || injected;
     const bool ginj = inject && __any_sync(FULL, injected);
     const int32_t *scr = R.inj_scratch + (size_t)g * 32 * kRowMaxCells;
-    if (staged && ostaged) {  // shared-memory blocks (the common case)
-      vid_lists(s_in, s_out, s_out + R.cap, OO, FO, LV, INJ, nfin, in_off, out_off, has_ent, ent_y,
-                ent_e, changed, ginj, dir, lane, scr);
+    int itot;
+    const int ioff = warp_scan(changed ? popc_row(OO) : 0, lane, &itot);
+    if (staged && ostaged && !ginj && itot <= kCellTab) {  // shared-memory blocks (the common case)
+      vid_lists_tab(s_in, s_out, s_out + R.cap, OO, FO, LV, nfin, in_off, out_off, has_ent, ent_y,
+                    ent_e, changed, ioff, itot, dir, lane);
     } else {
       RowWords oo, fo, lv, inj;
 #pragma unroll
