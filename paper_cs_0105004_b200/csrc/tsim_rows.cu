@@ -729,8 +729,10 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
             for (int jj = lane; jj < mtot; jj += 32) {
               const uint32_t me = (uint32_t)mlist[jj];
               const uint32_t e = (uint32_t)s_in[me >> 12];
-              if (philox_w0_rk((uint32_t)P.t, e & kVidMask, rk) <= p32m1)
-                red_or_shared(bw_s + (((me >> 5) & 127u) << 2), 1u << (me & 31u));
+              // no branch: every lane ORs its brake bit, or 0 (measured faster
+              // than a divergent reduction of the ~20 % that brake)
+              const uint32_t brk = philox_w0_rk((uint32_t)P.t, e & kVidMask, rk) <= p32m1 ? 1u : 0u;
+              red_or_shared(bw_s + (((me >> 5) & 127u) << 2), brk << (me & 31u));
             }
           __syncwarp();
         } else {  // a group larger than the staging (rare): out of line

@@ -12,6 +12,7 @@ T = {}
 t = time.perf_counter()
 scn = scenarios.config(sys.argv[1] if len(sys.argv) > 1 else "4a")
 T["generate"] = time.perf_counter() - t
+tsim.Sim(p_slow=scn.p_slow, seed=scn.seed, flags=tsim.FLAG_FUSED).close()  # CUDA context (as bench.py)
 t = time.perf_counter()
 sim = tsim.Sim(p_slow=scn.p_slow, seed=scn.seed, flags=tsim.FLAG_FUSED)
 T["create"] = time.perf_counter() - t
