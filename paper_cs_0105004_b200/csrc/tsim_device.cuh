@@ -247,6 +247,32 @@ static __device__ __forceinline__ void acc_place(Acc &a, bool hash, int vid, int
   if (hash) a.hash += vmix(vid, link, l, x, v);
 }
 
+// warp reduction of the counters into the stats slot of time slot_t (no
+// block barrier: a warp that finishes early exits)
+static __device__ void flush_acc_warp(const StepParams &P, Acc &a, int slot_t) {
+  const int lane = threadIdx.x & 31;
+  uint64_t h = a.hash, sv = a.sumv;
+  uint32_t act = a.active, arr = a.arr, inj = a.inj, lc = a.lc;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    h += __shfl_down_sync(FULL, h, o);
+    sv += __shfl_down_sync(FULL, sv, o);
+    act += __shfl_down_sync(FULL, act, o);
+    arr += __shfl_down_sync(FULL, arr, o);
+    inj += __shfl_down_sync(FULL, inj, o);
+    lc += __shfl_down_sync(FULL, lc, o);
+  }
+  if (lane == 0) {
+    unsigned long long *st = P.stats + (size_t)(slot_t & (kHist - 1)) * ST_N;
+    if (h) atomicAdd(st + ST_HASH, (unsigned long long)h);
+    if (act) atomicAdd(st + ST_ACTIVE, (unsigned long long)act);
+    if (arr) atomicAdd(st + ST_ARR, (unsigned long long)arr);
+    if (inj) atomicAdd(st + ST_INJ, (unsigned long long)inj);
+    if (lc) atomicAdd(st + ST_LC, (unsigned long long)lc);
+    if (sv) atomicAdd(st + ST_SUMV, (unsigned long long)sv);
+  }
+}
+
 // block reduction of the counters into the stats slot of time slot_t
 static __device__ void flush_acc(const StepParams &P, Acc &a, int slot_t,
                                  unsigned long long *smem_red) {

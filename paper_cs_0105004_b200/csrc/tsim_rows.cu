@@ -485,6 +485,9 @@ static __device__ __noinline__ void vid_lists_global(const int32_t *ibase, int32
             ent_e, changed, ginj, dir, lane, inj_scratch);
 }
 
+#ifndef TS_ROWS_WARP_FLUSH
+#define TS_ROWS_WARP_FLUSH 1  // counters flushed per warp (no block barrier at the end)
+#endif
 #ifndef TS_ROWS_MINB
 #define TS_ROWS_MINB (512 / TS_ROWS_TPB)  // resident blocks per SM: 128 registers (96 measured 2.5% slower)
 #endif
@@ -1057,8 +1060,14 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
     }
   }
   if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+#if TS_ROWS_WARP_FLUSH
+  flush_acc_warp(P, acc, P.t + 1);
+  if (lc) flush_acc_warp(P, acc_next, lct + 1);
+  (void)red;
+#else
   flush_acc(P, acc, P.t + 1, red);
   if (lc) flush_acc(P, acc_next, lct + 1, red);
+#endif
 }
 
 // state hash of the row-mode state S(t) (one thread per lane-row)
