@@ -485,6 +485,9 @@ static __device__ __noinline__ void vid_lists_global(const int32_t *ibase, int32
             ent_e, changed, ginj, dir, lane, inj_scratch);
 }
 
+#ifndef TS_ROWS_DRAW2
+#define TS_ROWS_DRAW2 1  // two Philox chains per lane in the draw loop
+#endif
 #ifndef TS_ROWS_WARP_FLUSH
 #define TS_ROWS_WARP_FLUSH 1  // counters flushed per warp (no block barrier at the end)
 #endif
@@ -728,8 +731,22 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
           uint32_t rk[20];
 #pragma unroll
           for (int r = 0; r < 20; r++) rk[r] = __shfl_sync(FULL, P_.rk[r], 0);
-          if (P.p32 != 0)
+          if (P.p32 != 0) {
+#if TS_ROWS_DRAW2
+            // two independent Philox chains per lane and iteration
+            int jj = lane;
+            for (; jj + 32 < mtot; jj += 64) {
+              const uint32_t me0 = (uint32_t)mlist[jj], me1 = (uint32_t)mlist[jj + 32];
+              const uint32_t e0 = (uint32_t)s_in[me0 >> 12], e1 = (uint32_t)s_in[me1 >> 12];
+              const uint32_t b0 = philox_w0_rk((uint32_t)P.t, e0 & kVidMask, rk) <= p32m1 ? 1u : 0u;
+              const uint32_t b1 = philox_w0_rk((uint32_t)P.t, e1 & kVidMask, rk) <= p32m1 ? 1u : 0u;
+              red_or_shared(bw_s + (((me0 >> 5) & 127u) << 2), b0 << (me0 & 31u));
+              red_or_shared(bw_s + (((me1 >> 5) & 127u) << 2), b1 << (me1 & 31u));
+            }
+            for (; jj < mtot; jj += 32) {
+#else
             for (int jj = lane; jj < mtot; jj += 32) {
+#endif
               const uint32_t me = (uint32_t)mlist[jj];
               const uint32_t e = (uint32_t)s_in[me >> 12];
               // no branch: every lane ORs its brake bit, or 0 (measured faster
@@ -737,6 +754,7 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
               const uint32_t brk = philox_w0_rk((uint32_t)P.t, e & kVidMask, rk) <= p32m1 ? 1u : 0u;
               red_or_shared(bw_s + (((me >> 5) & 127u) << 2), brk << (me & 31u));
             }
+          }
           __syncwarp();
         } else {  // a group larger than the staging (rare): out of line
           RowWords u1w, ow;
