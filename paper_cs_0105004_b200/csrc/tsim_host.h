@@ -171,7 +171,8 @@ struct ts_sim {
   uint8_t *d_vmax = nullptr;
   uint32_t *d_tt = nullptr;
   int32_t *d_out_pos = nullptr;
-  int64_t *d_roff = nullptr;
+  int64_t *d_roff = nullptr;   // route offsets (device read-back of cursors; allocated on demand)
+  int32_t *d_rd = nullptr;     // read-back scratch (ts_read_vehicles on the device)
   uint8_t *d_rslot = nullptr;
   NodeOut *d_nodeout = nullptr;
   VehPos *d_vpos = nullptr;

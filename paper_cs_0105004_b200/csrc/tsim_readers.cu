@@ -3,6 +3,164 @@
 // work-weighted partition entry points.  C-ABI declared in include/tsim.h.
 #include "tsim_host.h"
 
+// ------------------------------------------------- device-side read-back
+// Per-vehicle state gathered on the device (single-domain handles): every
+// vehicle found in the row planes / vid blocks or the general tiles writes
+// its link, lane, cell, velocity by vid and counts itself in `seen` (a
+// count > 1 is a corrupt state); then one thread per vehicle derives
+// status, route cursor and arrival time.  Only the caller's arrays cross
+// PCIe.
+struct ReadOut {
+  int32_t *link, *lane, *cell, *v;
+  uint32_t *seen;
+};
+
+__global__ void __launch_bounds__(128) k_read_rows(const RowsParams R, ReadOut o) {
+  const int gid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int g = gid >> 5, lane = gid & 31;
+  const bool act = g < R.ngroups;
+  const uint32_t *pl = R.planes_in + group_plane_base(act ? g : 0) + lane;
+  int n = 0;
+  uint32_t O[kRowWords];
+  for (int i = 0; i < kRowWords; i++) {
+    O[i] = act ? pl[i * 32] : 0u;
+    n += __popc(O[i]);
+  }
+  int off = n;  // exclusive warp prefix of the row counts
+  for (int d = 1; d < 32; d <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, off, d);
+    if (lane >= d) off += y;
+  }
+  off -= n;
+  if (!act || n == 0) return;
+  const RowDesc rd = R.rows[gid];
+  const int a = R.row_a ? R.row_a[gid] : 0;
+  const int32_t *lst = R.vid_in + R.gvoff[g] + off;
+  int k = 0;
+  for (int i = 0; i < kRowWords; i++) {
+    uint32_t m = O[i];
+    while (m) {
+      const int x = __ffs(m) - 1;
+      m &= m - 1u;
+      const int v = (int)((pl[(kRowWords + i) * 32] >> x) & 1u) |
+                    (int)(((pl[(2 * kRowWords + i) * 32] >> x) & 1u) << 1) |
+                    (int)(((pl[(3 * kRowWords + i) * 32] >> x) & 1u) << 2);
+      const int f = (int)((uint32_t)lst[k++] & kVidMask);
+      atomicAdd(o.seen + f, 1u);
+      o.link[f] = rd.link;
+      o.lane[f] = rd.l;
+      o.cell[f] = a + 32 * i + x;
+      o.v[f] = v;
+    }
+  }
+}
+
+// general tiles: one thread per lane of a tile (byte codes, per-lane lists)
+__global__ void __launch_bounds__(128) k_read_tiles(const TileDesc *tiles, int ntiles,
+                                                    const uint8_t *code, const int32_t *vid,
+                                                    ReadOut o) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int ti = (int)(i >> 3), l = (int)(i & 7);
+  if (ti >= ntiles) return;
+  const TileDesc d = tiles[ti];
+  if (l >= d.L) return;
+  const int Wp = row_pitch(d.w);
+  const int64_t rb = d.off + (int64_t)l * Wp;
+  int64_t r = rb;
+  for (int x = 0; x < d.w; x++) {
+    const uint8_t c = code[rb + x];
+    if (c & 0x80) continue;
+    const int f = vid[r++];
+    atomicAdd(o.seen + f, 1u);
+    o.link[f] = d.link;
+    o.lane[f] = l;
+    o.cell[f] = d.a + x;
+    o.v[f] = c & 7;
+  }
+}
+
+// per vehicle: status / cursor / arrival (single domain); bad[0] = the
+// smallest vid seen twice, bad[1] = the smallest vid that is nowhere
+__global__ void __launch_bounds__(256) k_read_status(int32_t nv, ReadOut o, const int32_t *inj,
+                                                     const int32_t *arr, const VehPos *vpos,
+                                                     const int64_t *roff, int8_t *status,
+                                                     int32_t *cursor, int32_t *tarr,
+                                                     int32_t *bad) {
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= nv) return;
+  const uint32_t sn = o.seen[f];
+  int8_t st;
+  if (sn > 1) atomicMin(bad, f);
+  if (sn) st = TS_ACTIVE;
+  else if (arr[f] >= 0) st = TS_ARRIVED;
+  else if (inj[f] == INT_MAX) st = TS_PENDING;
+  else {
+    atomicMin(bad + 1, f);
+    st = TS_ABSENT;
+  }
+  status[f] = st;
+  cursor[f] = (st == TS_ACTIVE || st == TS_ARRIVED) ? (int32_t)(vpos[f].p - roff[f]) : -1;
+  tarr[f] = st == TS_ARRIVED ? arr[f] : -1;
+  if (!sn) {
+    o.link[f] = -1;
+    o.lane[f] = -1;
+    o.cell[f] = -1;
+    o.v[f] = -1;
+  }
+}
+
+static int read_vehicles_device(ts_sim *h, int8_t *status, int32_t *link, int32_t *lane,
+                                int32_t *cell, int32_t *v, int32_t *cursor, int32_t *t_arrive) {
+  const size_t nv = (size_t)std::max(h->nv, 1);
+  if (!h->d_roff) {
+    int rc;
+    if ((rc = upload(h, &h->d_roff, h->roff))) return rc;
+  }
+  if (!h->d_rd) {  // scratch: 7 int32 arrays + the status bytes + 2 error words
+    int rc;
+    if ((rc = dalloc(h, &h->d_rd, nv * 7 + nv / 4 + 4))) return rc;
+  }
+  ReadOut o{h->d_rd, h->d_rd + nv, h->d_rd + 2 * nv, h->d_rd + 3 * nv,
+            reinterpret_cast<uint32_t *>(h->d_rd + 4 * nv)};
+  int32_t *dcur = h->d_rd + 5 * nv, *darr = h->d_rd + 6 * nv;
+  int8_t *dst = reinterpret_cast<int8_t *>(h->d_rd + 7 * nv);
+  int32_t *dbad = h->d_rd + 7 * nv + nv / 4 + 1;
+  CK(h, cudaMemsetAsync(o.seen, 0, nv * 4, h->stream));
+  CK(h, cudaMemsetAsync(dbad, 0x7f, 8, h->stream));
+  if (h->ngroups > 0) {
+    RowsParams R = rows_params(h);
+    R.planes_in = h->d_planes[h->rcur];
+    R.vid_in = h->d_rvid[h->rcur];
+    const int n = h->ngroups * 32;
+    k_read_rows<<<(n + 127) / 128, 128, 0, h->stream>>>(R, o);
+  }
+  if (!h->gtiles.empty()) {
+    const int64_t n = (int64_t)h->gtiles.size() * 8;
+    k_read_tiles<<<(unsigned)((n + 127) / 128), 128, 0, h->stream>>>(
+        h->d_tiles, (int)h->gtiles.size(), h->d_code[h->gcur], h->d_vid[h->gcur], o);
+  }
+  if (h->nv > 0)
+    k_read_status<<<(h->nv + 255) / 256, 256, 0, h->stream>>>(h->nv, o, h->d_inj, h->d_arr,
+                                                              h->d_vpos, h->d_roff, dst, dcur,
+                                                              darr, dbad);
+  CK(h, cudaGetLastError());
+  int32_t bad[2];
+  CK(h, cudaMemcpyAsync(bad, dbad, 8, cudaMemcpyDeviceToHost, h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  if (bad[0] != 0x7f7f7f7f) return fail(h, TS_EINTERNAL, "corrupt state: vid %d held twice", bad[0]);
+  if (bad[1] != 0x7f7f7f7f) return fail(h, TS_EINTERNAL, "corrupt state: vehicle %d lost", bad[1]);
+  const size_t b4 = (size_t)h->nv * 4;
+  if (h->nv == 0) return TS_OK;
+  if (status) CK(h, cudaMemcpy(status, dst, (size_t)h->nv, cudaMemcpyDeviceToHost));
+  if (link) CK(h, cudaMemcpy(link, o.link, b4, cudaMemcpyDeviceToHost));
+  if (lane) CK(h, cudaMemcpy(lane, o.lane, b4, cudaMemcpyDeviceToHost));
+  if (cell) CK(h, cudaMemcpy(cell, o.cell, b4, cudaMemcpyDeviceToHost));
+  if (v) CK(h, cudaMemcpy(v, o.v, b4, cudaMemcpyDeviceToHost));
+  if (cursor) CK(h, cudaMemcpy(cursor, dcur, b4, cudaMemcpyDeviceToHost));
+  if (t_arrive) CK(h, cudaMemcpy(t_arrive, darr, b4, cudaMemcpyDeviceToHost));
+  return TS_OK;
+}
+
 extern "C" {
 
 // ------------------------------------------------------------------ readers
@@ -94,6 +252,10 @@ int ts_read_vehicles(ts_sim *h, int8_t *status, int32_t *link, int32_t *lane, in
                      int32_t *v, int32_t *cursor, int32_t *t_arrive) {
   if (!h || !h->inited) return fail(h, TS_EINVAL, "not initialised");
   CK(h, cudaSetDevice(h->dev));
+  // one domain: gathered on the device; domains (pending vehicles are
+  // reported by the owner of their entry cell): on the host
+  if (h->dom_k == 1 && !getenv("TSIM_HOST_READ"))
+    return read_vehicles_device(h, status, link, lane, cell, v, cursor, t_arrive);
   CK(h, cudaStreamSynchronize(h->stream));
   HostVec<uint8_t> code;
   HostVec<int32_t> vids, inj(h->nv), arr(h->nv), cur(h->nv);
