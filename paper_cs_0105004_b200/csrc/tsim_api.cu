@@ -325,8 +325,10 @@ int ts_load_vehicles(ts_sim *h, int32_t n, const int64_t *route_off, const int32
   };
   static const char *msg[] = {"", "empty route", "bad link", "route links not consecutive",
                               "entry cell outside link"};
+  InitTrace trace("load");
   const int32_t bad_off = first_failing([&](int32_t i) { return route_off[i + 1] <= route_off[i]; });
   if (bad_off != INT32_MAX) return fail(h, TS_EINVAL, "vehicle %d: %s", bad_off, msg[1]);
+  trace("offsets");
   h->rslot.resize(n > 0 ? route_off[n] : 0);
   uint8_t *const slot = h->rslot.data();
   const int32_t bad = first_failing([&](int32_t i) { return check(i, slot) != 0; });
@@ -334,17 +336,24 @@ int ts_load_vehicles(ts_sim *h, int32_t n, const int64_t *route_off, const int32
     decltype(h->rslot)().swap(h->rslot);
     return fail(h, TS_EINVAL, "vehicle %d: %s", bad, msg[check(bad, nullptr)]);
   }
+  trace("routes -> out-slots");
   h->nv = n;
-  h->roff.assign(route_off, route_off + n + 1);
-  if (n == 0) h->roff.assign(1, 0);
+  h->roff.resize(n + 1);
+  h->roff[0] = 0;
   h->first_link.resize(n);
+  h->dep.resize(n);
+  h->entry.resize(n);
   parallel_for(n, [&](int64_t lo, int64_t hi, int) {
-    for (int64_t f = lo; f < hi; f++) h->first_link[f] = route_links[route_off[f]];
+    for (int64_t f = lo; f < hi; f++) {
+      h->roff[f + 1] = route_off[f + 1];
+      h->first_link[f] = route_links[route_off[f]];
+      h->dep[f] = depart[f];
+      h->entry[f] = entry_cell[f];
+    }
   });
-  h->dep.assign(depart, depart + n);
-  h->entry.assign(entry_cell, entry_cell + n);
   h->placed.assign(n, 0);
   h->have_veh = true;
+  trace("vehicle arrays");
   return TS_OK;
 }
 
@@ -1076,97 +1085,15 @@ static int zero_stats(ts_sim *h, int32_t t_from, int32_t n) {
   return TS_OK;
 }
 
-static int init_impl(ts_sim *h, int32_t t0, bool inject0);
-static void pack_strips(ts_sim *h);
 
-int ts_init(ts_sim *h, int32_t t0) { return init_impl(h, t0, true); }
-int ts_resume(ts_sim *h, int32_t t) { return init_impl(h, t, false); }
-
-// TSIM_TRACE=1: wall-clock phases of ts_init on stderr (host-side tuning)
-struct InitTrace {
-  bool on = getenv("TSIM_TRACE") != nullptr;
-  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
-  void operator()(const char *what) {
-    if (!on) return;
-    const auto n = std::chrono::steady_clock::now();
-    fprintf(stderr, "[tsim init] %-28s %8.3f s\n", what, std::chrono::duration<double>(n - t).count());
-    t = n;
-  }
-};
-
-static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
-  InitTrace trace;
-  if (!h) return TS_EINVAL;
-  if (!h->have_veh) return fail(h, TS_EINVAL, "load vehicles first");
-  if (h->inited) return fail(h, TS_EINVAL, "already initialised");
-  if (t0 < 0) return fail(h, TS_EINVAL, "t0 must be >= 0");
-  CK(h, cudaSetDevice(h->dev));
-  if (h->dom_of_node.empty()) h->dom_of_node.assign(h->nn, 0);
-  if (!build_tiles(h)) return fail(h, TS_EINTERNAL, "asymmetric exchange plan");
-
-  // the routes (out-slot sequences built at load, GBs at the largest
-  // configs) go to the device on a host thread of their own through pinned
-  // double-buffered staging, overlapping the placement and plane build below
-  struct RouteUpload {
-    std::thread th;
-    cudaError_t err = cudaSuccess;
-    ~RouteUpload() {
-      if (th.joinable()) th.join();
-    }
-  } rup;
-  {
-    const size_t nb = h->rslot.size();
-    int rc;
-    if ((rc = dalloc(h, &h->d_rslot, std::max<size_t>(nb, 1)))) return rc;
-    rup.th = std::thread([h, nb, &rup]() {
-      cudaError_t &e = rup.err;
-      if ((e = cudaSetDevice(h->dev)) != cudaSuccess || nb == 0) return;
-      const size_t chunk = (size_t)64 << 20;
-      uint8_t *pin[2] = {nullptr, nullptr};
-      cudaEvent_t done[2] = {nullptr, nullptr};
-      cudaStream_t st = nullptr;
-      const bool pinned = nb > chunk && cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) == cudaSuccess &&
-                          cudaMallocHost(&pin[0], chunk) == cudaSuccess &&
-                          cudaMallocHost(&pin[1], chunk) == cudaSuccess &&
-                          cudaEventCreateWithFlags(&done[0], cudaEventDisableTiming) == cudaSuccess &&
-                          cudaEventCreateWithFlags(&done[1], cudaEventDisableTiming) == cudaSuccess;
-      if (pinned) {  // fill one buffer while the other copies
-        for (size_t o = 0, i = 0; o < nb && e == cudaSuccess; o += chunk, i++) {
-          const size_t m = std::min(chunk, nb - o);
-          uint8_t *b = pin[i & 1];
-          if (i >= 2) cudaEventSynchronize(done[i & 1]);
-          {  // a few copy threads: one host thread alone cannot keep up with the DMA
-            constexpr int kCp = 6;
-            std::thread cp[kCp];
-            for (int q = 0; q < kCp; q++)
-              cp[q] = std::thread([=]() {
-                std::memcpy(b + m * q / kCp, h->rslot.data() + o + m * q / kCp, m * (q + 1) / kCp - m * q / kCp);
-              });
-            for (auto &t : cp) t.join();
-          }
-          if ((e = cudaMemcpyAsync(h->d_rslot + o, b, m, cudaMemcpyHostToDevice, st)) == cudaSuccess)
-            e = cudaEventRecord(done[i & 1], st);
-        }
-        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-      } else {
-        e = cudaMemcpy(h->d_rslot, h->rslot.data(), nb, cudaMemcpyHostToDevice);
-      }
-      for (int i = 0; i < 2; i++) {
-        if (pin[i]) cudaFreeHost(pin[i]);
-        if (done[i]) cudaEventDestroy(done[i]);
-      }
-      if (st) cudaStreamDestroy(st);
-    });
-  }
-
-  h->entry_h = h->entry;
-
-  // host staging of the initial placement: codes + compact vid lists (cells
-  // of other domains are skipped)
+// host staging of the initial placement (TSIM_HOST_INIT=1, and the exact
+// report of a cell claimed twice): codes + compact vid lists per tile, then
+// the row planes and vid blocks, uploaded
+static int place_host(ts_sim *h, HostVec<int32_t> &cur0, std::vector<uint8_t> &gcode,
+                      std::vector<int32_t> &gvid) {
+  // cells of other domains are skipped
   HostVec<uint8_t> code = filled<uint8_t>(h->total_cells, kEmpty);
   HostVec<int32_t> cellvid = filled<int32_t>(h->total_cells, -1);
-  std::vector<int32_t> cur0(h->nv, 0);
-  h->n_placed = 0;
   // placements in parallel: a cell claimed twice is found by the
   // compare-and-swap on its vehicle slot (the first placement in input
   // order is reported)
@@ -1225,11 +1152,10 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
       }
     }
   });
-  trace("placement + row lists");
   HostVec<int32_t>().swap(cellvid);
   // general tiles: the byte layout at their own device offsets
-  std::vector<uint8_t> gcode(h->gcells, kEmpty);
-  std::vector<int32_t> gvid(h->gcells, -1);
+  gcode.assign(h->gcells, kEmpty);
+  gvid.assign(h->gcells, -1);
   for (size_t ti = 0; ti < h->tiles.size(); ti++) {
     if (h->tile_g[ti] < 0) continue;
     const TileDesc &d = h->tiles[ti], &gd = h->gtiles[h->tile_g[ti]];
@@ -1237,12 +1163,8 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
     std::copy(code.begin() + d.off, code.begin() + d.off + n, gcode.begin() + gd.off);
     std::copy(vids.begin() + d.off, vids.begin() + d.off + n, gvid.begin() + gd.off);
   }
-  trace("general tiles");
   // row tiles: bit-planes O, V0..V2, A0, A1 per row (group-interleaved);
   // list entries vid | slot << 27
-  if (h->ngroups > 0 && h->nv > (int32_t)kVidMask)
-    return fail(h, TS_EINVAL, "too many vehicles for the row kernel");
-  if (h->rvid_entries > INT32_MAX) return fail(h, TS_EINVAL, "network too large for one device");
   HostVec<uint32_t> planes = filled<uint32_t>(group_plane_base(h->ngroups), 0u);
   HostVec<int32_t> rvid = filled<int32_t>(h->rvid_entries, -1);
   std::vector<int32_t> row_tile(h->rows.size(), -1);  // row slot -> tile
@@ -1284,9 +1206,289 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
     gcnt[g] = (int32_t)(k - k0);
   }
   });
-  HostVec<uint8_t>().swap(code);
-  HostVec<int32_t>().swap(vids);
-  trace("planes + vid blocks");
+  if (h->ngroups > 0) {
+    CK(h, cudaMemcpyAsync(h->d_planes[0], planes.data(), planes.size() * 4, cudaMemcpyHostToDevice,
+                          h->stream));
+    CK(h, cudaMemcpyAsync(h->d_rvid[0], rvid.data(), rvid.size() * 4, cudaMemcpyHostToDevice,
+                          h->stream));
+    CK(h, cudaMemcpyAsync(h->d_gcnt[0], gcnt.data(), gcnt.size() * 4, cudaMemcpyHostToDevice,
+                          h->stream));
+    CK(h, cudaStreamSynchronize(h->stream));  // the staging arrays are freed on return
+  }
+  return TS_OK;
+}
+
+// ------------------------------------------------ device-side placement
+// The row-tile placements become one record each (row slot s and cell x as
+// s << 7 | x, the list entry vid | slot << 27, velocity | lane class << 3);
+// k_place_bits ORs each into the bit-planes (an occupancy bit already set
+// is a cell claimed twice: flagged, and the host path reports it),
+// k_place_rows turns each group's occupancy popcounts into row offsets
+// (warp scan) and the group count, k_place_lists writes each entry at its
+// rank within its row (popcount of the occupancy below its cell) -- the
+// layout the host path builds, without staging planes and lists in host
+// memory.
+constexpr int kPlaceHost = -1000;       // place_device: use the host path
+constexpr uint32_t kNoPlace = 0xFFFFFFFFu;
+
+__global__ void k_place_bits(const uint32_t *__restrict__ pos, const uint8_t *__restrict__ vc, int64_t n,
+                             uint32_t *planes, uint32_t *conflict) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n || pos[i] == kNoPlace) return;
+  const uint32_t s = pos[i] >> 7, x = pos[i] & 127u, q = vc[i];
+  uint32_t *pl = planes + group_plane_base(s >> 5) + (s & 31u) + (x >> 5) * 32;
+  const uint32_t bit = 1u << (x & 31u);
+  if (atomicOr(pl, bit) & bit) atomicExch(conflict, 1u);
+  for (int p = 1; p <= 5; p++)  // V0..V2 (q bits 0-2), A0, A1 (q bits 3-4)
+    if ((q >> (p - 1)) & 1u) atomicOr(pl + p * kRowWords * 32, bit);
+}
+
+__global__ void k_place_rows(const uint32_t *__restrict__ planes, const int32_t *__restrict__ gvoff, int ngroups,
+                             int32_t *rowoff, int32_t *gcnt) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int g = (int)(s >> 5), lane = threadIdx.x & 31;
+  if (g >= ngroups) return;  // whole warps (blockDim a multiple of 32)
+  const uint32_t *pl = planes + group_plane_base(g) + lane;
+  int c = 0;
+  for (int w = 0; w < kRowWords; w++) c += __popc(pl[w * 32]);
+  int inc = c;
+  for (int d = 1; d < 32; d <<= 1) {
+    const int o = __shfl_up_sync(0xFFFFFFFFu, inc, d);
+    if (lane >= d) inc += o;
+  }
+  rowoff[s] = gvoff[g] + inc - c;
+  if (lane == 31) gcnt[g] = inc;
+}
+
+__global__ void k_place_lists(const uint32_t *__restrict__ pos, const uint32_t *__restrict__ ent, int64_t n,
+                              const uint32_t *__restrict__ planes, const int32_t *__restrict__ rowoff,
+                              int32_t *rvid) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n || pos[i] == kNoPlace) return;
+  const uint32_t s = pos[i] >> 7, x = pos[i] & 127u;
+  const uint32_t *pl = planes + group_plane_base(s >> 5) + (s & 31u);
+  int r = __popc(pl[(x >> 5) * 32] & ((1u << (x & 31u)) - 1u));
+  for (uint32_t w = 0; w < (x >> 5); w++) r += __popc(pl[w * 32]);
+  rvid[rowoff[s] + r] = (int32_t)ent[i];
+}
+
+// the placement with the row tiles built on the device (general tiles on
+// the host, at their own offsets); kPlaceHost when the host path must run
+static int place_device(ts_sim *h, HostVec<int32_t> &cur0, std::vector<uint8_t> &gcode,
+                        std::vector<int32_t> &gvid) {
+  InitTrace trace;
+  const int64_t n = (int64_t)h->pl_vid.size();
+  if (h->rows.size() > ((size_t)1 << 25)) return kPlaceHost;  // s << 7 | x in 32 bits
+  HostVec<uint32_t> pos(std::max<int64_t>(n, 1)), ent(std::max<int64_t>(n, 1));
+  HostVec<uint8_t> vc(std::max<int64_t>(n, 1));
+  gcode.assign(h->gcells, kEmpty);
+  std::vector<int32_t> gcell(h->gcells, -1);
+  std::vector<int64_t> placed_cnt(64, 0);
+  std::vector<uint8_t> taken(64, 0);
+  parallel_for(n, [&](int64_t lo, int64_t hi, int th) {
+    for (int64_t i = lo; i < hi; i++) {
+      pos[i] = kNoPlace;
+      const int f = h->pl_vid[i], c = h->pl_cur[i];
+      const int k = link_at(h, f, c);
+      cur0[f] = c;
+      const int ti = tile_of(h, k, h->pl_cell[i]);
+      if (ti < 0) continue;  // another domain's cell
+      const TileDesc &d = h->tiles[ti];
+      const int64_t ro = h->roff[f];
+      // ring segment rows: straight on through the virtual nodes (out-slot 0)
+      const int slot = h->ring_rows ? 0
+                       : c + 1 < h->roff[f + 1] - ro ? (int)h->rslot[ro + c + 1] : kSlotFinal;
+      const int x = h->pl_cell[i] - d.a;
+      if (h->tile_row[ti] >= 0) {
+        // allowed-lane class (R7): 0 all, 1 curb (right turn), 2 median (left)
+        int cls = 0;
+        if (slot != kSlotFinal) {
+          const int tty = (h->tt[d.link] >> (2 * slot)) & 3;
+          cls = tty == 0 ? 0 : (tty == 2 ? 1 : 2);
+        }
+        pos[i] = ((uint32_t)(h->tile_row[ti] + h->pl_lane[i]) << 7) | (uint32_t)x;
+        ent[i] = (uint32_t)f | ((uint32_t)slot << kSlotShift);
+        vc[i] = (uint8_t)(h->pl_v[i] | (cls << 3));
+      } else {
+        const TileDesc &gd = h->gtiles[h->tile_g[ti]];
+        const int64_t p = gd.off + (int64_t)h->pl_lane[i] * row_pitch(d.w) + x;
+        int32_t expect = -1;
+        if (!__atomic_compare_exchange_n(&gcell[p], &expect, (int32_t)f, false, __ATOMIC_RELAXED,
+                                         __ATOMIC_RELAXED)) {
+          taken[th] = 1;
+          continue;
+        }
+        gcode[p] = (uint8_t)(h->pl_v[i] | (slot << 3));
+      }
+      placed_cnt[th]++;
+    }
+  });
+  for (uint8_t t : taken)
+    if (t) return kPlaceHost;
+  trace("  records");
+  // general tiles: per-row vid lists in cell order
+  gvid.assign(h->gcells, -1);
+  parallel_for((int64_t)h->gtiles.size(), [&](int64_t lo, int64_t hi, int) {
+    for (int64_t gi = lo; gi < hi; gi++) {
+      const TileDesc &d = h->gtiles[gi];
+      const int Wp = row_pitch(d.w);
+      for (int l = 0; l < d.L; l++) {
+        const int64_t rb = d.off + (int64_t)l * Wp;
+        int64_t r = rb;
+        for (int x = 0; x < d.w; x++)
+          if (gcode[rb + x] != kEmpty) gvid[r++] = gcell[rb + x];
+      }
+    }
+  });
+  // row tiles on the device (stream-ordered scratch)
+  const int64_t nrows = (int64_t)h->ngroups * 32;
+  uint32_t *d_pos = nullptr, *d_ent = nullptr, *d_flag = nullptr;
+  uint8_t *d_vc = nullptr;
+  int32_t *d_rowoff = nullptr;
+  const size_t nb = (size_t)std::max<int64_t>(n, 1);
+  CK(h, cudaMallocAsync(&d_pos, nb * 4, h->stream));
+  CK(h, cudaMallocAsync(&d_ent, nb * 4, h->stream));
+  CK(h, cudaMallocAsync(&d_vc, nb, h->stream));
+  CK(h, cudaMallocAsync(&d_rowoff, (size_t)nrows * 4, h->stream));
+  CK(h, cudaMallocAsync(&d_flag, 4, h->stream));
+  CK(h, cudaMemsetAsync(d_flag, 0, 4, h->stream));
+  CK(h, cudaMemcpyAsync(d_pos, pos.data(), nb * 4, cudaMemcpyHostToDevice, h->stream));
+  CK(h, cudaMemcpyAsync(d_ent, ent.data(), nb * 4, cudaMemcpyHostToDevice, h->stream));
+  CK(h, cudaMemcpyAsync(d_vc, vc.data(), nb, cudaMemcpyHostToDevice, h->stream));
+  trace("  general lists + uploads");
+  const int nblk = (int)((n + 255) / 256);
+  if (n > 0) k_place_bits<<<nblk, 256, 0, h->stream>>>(d_pos, d_vc, n, h->d_planes[0], d_flag);
+  k_place_rows<<<(int)((nrows + 255) / 256), 256, 0, h->stream>>>(h->d_planes[0], h->d_gvoff, h->ngroups,
+                                                                  d_rowoff, h->d_gcnt[0]);
+  if (n > 0)
+    k_place_lists<<<nblk, 256, 0, h->stream>>>(d_pos, d_ent, n, h->d_planes[0], d_rowoff, h->d_rvid[0]);
+  CK(h, cudaGetLastError());
+  uint32_t conflict = 0;
+  CK(h, cudaMemcpyAsync(&conflict, d_flag, 4, cudaMemcpyDeviceToHost, h->stream));
+  for (void *p : {(void *)d_pos, (void *)d_ent, (void *)d_vc, (void *)d_rowoff, (void *)d_flag})
+    CK(h, cudaFreeAsync(p, h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));  // the host records are freed on return
+  trace("  kernels");
+  if (conflict) {  // planes and lists are rebuilt by the host path
+    CK(h, cudaMemsetAsync(h->d_planes[0], 0, group_plane_base(h->ngroups) * 4, h->stream));
+    return kPlaceHost;
+  }
+  for (int64_t c : placed_cnt) h->n_placed += c;
+  return TS_OK;
+}
+
+static int init_impl(ts_sim *h, int32_t t0, bool inject0);
+static void pack_strips(ts_sim *h);
+
+int ts_init(ts_sim *h, int32_t t0) { return init_impl(h, t0, true); }
+int ts_resume(ts_sim *h, int32_t t) { return init_impl(h, t, false); }
+
+static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
+  InitTrace trace;
+  if (!h) return TS_EINVAL;
+  if (!h->have_veh) return fail(h, TS_EINVAL, "load vehicles first");
+  if (h->inited) return fail(h, TS_EINVAL, "already initialised");
+  if (t0 < 0) return fail(h, TS_EINVAL, "t0 must be >= 0");
+  CK(h, cudaSetDevice(h->dev));
+  if (h->dom_of_node.empty()) h->dom_of_node.assign(h->nn, 0);
+  if (!build_tiles(h)) return fail(h, TS_EINTERNAL, "asymmetric exchange plan");
+
+  // the routes (out-slot sequences built at load, GBs at the largest
+  // configs) go to the device on a host thread of their own through pinned
+  // double-buffered staging, overlapping the placement and plane build below
+  struct RouteUpload {
+    std::thread th;
+    cudaError_t err = cudaSuccess;
+    double secs = 0;
+    ~RouteUpload() {
+      if (th.joinable()) th.join();
+    }
+  } rup;
+  {
+    const size_t nb = h->rslot.size();
+    int rc;
+    if ((rc = dalloc(h, &h->d_rslot, std::max<size_t>(nb, 1)))) return rc;
+    rup.th = std::thread([h, nb, &rup]() {
+      cudaError_t &e = rup.err;
+      const auto t_start = std::chrono::steady_clock::now();
+      struct Done {
+        RouteUpload &r;
+        std::chrono::steady_clock::time_point t;
+        ~Done() { r.secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t).count(); }
+      } done_{rup, t_start};
+      if ((e = cudaSetDevice(h->dev)) != cudaSuccess || nb == 0) return;
+      const size_t chunk = (size_t)64 << 20;
+      uint8_t *pin[2] = {nullptr, nullptr};
+      cudaEvent_t done[2] = {nullptr, nullptr};
+      cudaStream_t st = nullptr;
+      const bool pinned = nb > chunk && cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) == cudaSuccess &&
+                          cudaMallocHost(&pin[0], chunk) == cudaSuccess &&
+                          cudaMallocHost(&pin[1], chunk) == cudaSuccess &&
+                          cudaEventCreateWithFlags(&done[0], cudaEventDisableTiming) == cudaSuccess &&
+                          cudaEventCreateWithFlags(&done[1], cudaEventDisableTiming) == cudaSuccess;
+      if (pinned) {  // fill one buffer while the other copies
+        for (size_t o = 0, i = 0; o < nb && e == cudaSuccess; o += chunk, i++) {
+          const size_t m = std::min(chunk, nb - o);
+          uint8_t *b = pin[i & 1];
+          if (i >= 2) cudaEventSynchronize(done[i & 1]);
+          {  // a few copy threads: one host thread alone cannot keep up with the DMA
+            constexpr int kCp = 6;
+            std::thread cp[kCp];
+            for (int q = 0; q < kCp; q++)
+              cp[q] = std::thread([=]() {
+                std::memcpy(b + m * q / kCp, h->rslot.data() + o + m * q / kCp, m * (q + 1) / kCp - m * q / kCp);
+              });
+            for (auto &t : cp) t.join();
+          }
+          if ((e = cudaMemcpyAsync(h->d_rslot + o, b, m, cudaMemcpyHostToDevice, st)) == cudaSuccess)
+            e = cudaEventRecord(done[i & 1], st);
+        }
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+      } else {
+        e = cudaMemcpy(h->d_rslot, h->rslot.data(), nb, cudaMemcpyHostToDevice);
+      }
+      for (int i = 0; i < 2; i++) {
+        if (pin[i]) cudaFreeHost(pin[i]);
+        if (done[i]) cudaEventDestroy(done[i]);
+      }
+      if (st) cudaStreamDestroy(st);
+    });
+  }
+
+  h->entry_h = h->entry;
+
+  if (h->ngroups > 0 && h->nv > (int32_t)kVidMask)
+    return fail(h, TS_EINVAL, "too many vehicles for the row kernel");
+  if (h->rvid_entries > INT32_MAX) return fail(h, TS_EINVAL, "network too large for one device");
+  int rc;
+  for (int b = 0; b < 2; b++) {  // device state (both buffers)
+    if ((rc = dalloc(h, &h->d_code[b], h->gtiles.empty() ? 16 : h->gcells, 0xFF))) return rc;
+    if ((rc = dalloc(h, &h->d_vid[b], h->gtiles.empty() ? 16 : h->gcells, 0xFF))) return rc;
+    if ((rc = dalloc(h, &h->d_strip[b], std::max(1, h->nstrips), 0xFF))) return rc;
+    if ((rc = dalloc(h, &h->d_planes[b], std::max<size_t>(16, group_plane_base(h->ngroups)), 0))) return rc;
+    if ((rc = dalloc(h, &h->d_rvid[b], h->rvid_entries, 0xFF))) return rc;
+    if ((rc = dalloc(h, &h->d_gcnt[b], std::max(1, h->ngroups), 0))) return rc;
+    if (b == 0 && (rc = dalloc(h, &h->d_gctr, 1, 0))) return rc;
+  }
+  if (h->ngroups > 0 && (rc = upload(h, &h->d_gvoff, h->gvoff))) return rc;
+  trace("tiles + device state");
+  // the initial placement: row tiles built on the device (TSIM_HOST_INIT=1:
+  // on the host, as are a doubly claimed cell's exact report and an
+  // oversized row table)
+  HostVec<int32_t> cur0 = filled<int32_t>(h->nv, 0);
+  std::vector<uint8_t> gcode;
+  std::vector<int32_t> gvid;
+  h->n_placed = 0;
+  rc = kPlaceHost;
+  if (h->ngroups > 0 && getenv("TSIM_HOST_INIT") == nullptr) {
+    rc = place_device(h, cur0, gcode, gvid);
+    if (rc != TS_OK && rc != kPlaceHost) return rc;
+  }
+  if (rc == kPlaceHost) {
+    h->n_placed = 0;
+    if ((rc = place_host(h, cur0, gcode, gvid))) return rc;
+  }
+  trace("placement");
   // pending lists per first link in (departure, vid) order (R13)
   std::vector<int32_t> pend_off(h->nl + 1, 0), pend_list;
   auto mine = [&](int f) {  // pending vehicle whose entry cell this domain owns
@@ -1333,33 +1535,14 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
   std::vector<uint8_t> vmax8(h->nl);
   for (int k = 0; k < h->nl; k++) vmax8[k] = (uint8_t)h->vmax[k];
   // device
-  int rc;
   if ((rc = setup_node_lanes(h))) return rc;
+  if (h->ngroups > 0 && (rc = upload(h, &h->d_rows, h->rows))) return rc;  // node lanes resolved
   if ((rc = upload(h, &h->d_nli, h->nli))) return rc;
   if ((rc = upload(h, &h->d_nlo, h->nlo))) return rc;
   if ((rc = upload(h, &h->d_tiles, h->gtiles))) return rc;
-  for (int b = 0; b < 2; b++) {
-    if ((rc = dalloc(h, &h->d_code[b], h->gtiles.empty() ? 16 : h->gcells, 0xFF))) return rc;
-    if ((rc = dalloc(h, &h->d_vid[b], h->gtiles.empty() ? 16 : h->gcells, 0xFF))) return rc;
-    if ((rc = dalloc(h, &h->d_strip[b], std::max(1, h->nstrips), 0xFF))) return rc;
-    if ((rc = dalloc(h, &h->d_planes[b], std::max<size_t>(16, planes.size()), 0))) return rc;
-    if ((rc = dalloc(h, &h->d_rvid[b], h->rvid_entries, 0xFF))) return rc;
-    if ((rc = dalloc(h, &h->d_gcnt[b], std::max(1, h->ngroups), 0))) return rc;
-    if (b == 0 && (rc = dalloc(h, &h->d_gctr, 1, 0))) return rc;
-  }
   if (!h->gtiles.empty()) {
     CK(h, cudaMemcpyAsync(h->d_code[0], gcode.data(), gcode.size(), cudaMemcpyHostToDevice, h->stream));
     CK(h, cudaMemcpyAsync(h->d_vid[0], gvid.data(), gvid.size() * 4, cudaMemcpyHostToDevice, h->stream));
-  }
-  if (h->ngroups > 0) {
-    if ((rc = upload(h, &h->d_rows, h->rows))) return rc;
-    if ((rc = upload(h, &h->d_gvoff, h->gvoff))) return rc;
-    CK(h, cudaMemcpyAsync(h->d_planes[0], planes.data(), planes.size() * 4, cudaMemcpyHostToDevice,
-                          h->stream));
-    CK(h, cudaMemcpyAsync(h->d_rvid[0], rvid.data(), rvid.size() * 4, cudaMemcpyHostToDevice,
-                          h->stream));
-    CK(h, cudaMemcpyAsync(h->d_gcnt[0], gcnt.data(), gcnt.size() * 4, cudaMemcpyHostToDevice,
-                          h->stream));
   }
   trace("pending + uploads");
   {  // injection scratch of the row kernel: needed only if a row link has pending trips
@@ -1378,6 +1561,8 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
   if ((rc = upload(h, &h->d_out_pos, h->out_pos))) return rc;
   {  // routes as out-slot sequences: the upload started above
     rup.th.join();
+    trace("route upload joined");
+    if (trace.on) fprintf(stderr, "[tsim init]   (route upload took %.3f s)\n", rup.secs);
     if (rup.err != cudaSuccess)
       return fail(h, TS_EINTERNAL, "route upload: %s", cudaGetErrorString(rup.err));
     cudaGetLastError();
@@ -1390,10 +1575,13 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
     if ((rc = upload(h, &h->d_nodeout, h->ring_rows ? h->ring_nodeout : nodeout))) return rc;
   }
   {
-    std::vector<VehPos> vp(h->nv);
-    for (int f = 0; f < h->nv; f++) vp[f] = VehPos{h->roff[f] + cur0[f], h->roff[f + 1]};
+    HostVec<VehPos> vp(h->nv);
+    parallel_for(h->nv, [&](int64_t lo, int64_t hi, int) {
+      for (int64_t f = lo; f < hi; f++) vp[f] = VehPos{h->roff[f] + cur0[f], h->roff[f + 1]};
+    });
     if ((rc = upload(h, &h->d_vpos, vp))) return rc;
   }
+  trace("node outs + vehicle positions");
   if ((rc = upload(h, &h->d_dep, h->dep))) return rc;
   if ((rc = upload(h, &h->d_entry, h->entry))) return rc;
   if ((rc = upload(h, &h->d_inj, inj))) return rc;
@@ -1492,6 +1680,7 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
   unsigned long long st[ST_N];
   CK(h, cudaMemcpy(st, h->d_stats + (size_t)(t0 & (kHist - 1)) * ST_N, sizeof st, cudaMemcpyDeviceToHost));
   h->injected = (int64_t)st[ST_INJ];
+  trace("initial kernels");
   // the host copies of the plans are no longer needed (all on the device)
   std::vector<uint8_t, UninitAlloc<uint8_t>>().swap(h->rslot);
   std::vector<int32_t>().swap(h->pl_vid);
@@ -1500,7 +1689,7 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
   std::vector<int32_t>().swap(h->pl_cell);
   std::vector<int32_t>().swap(h->pl_v);
   h->inited = true;
-  trace("initial kernels");
+  trace("host plans freed");
   return TS_OK;
 }
 

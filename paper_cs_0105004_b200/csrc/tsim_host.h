@@ -4,6 +4,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <sys/mman.h>
 #include <nccl.h>
 
 #include <algorithm>
@@ -52,6 +53,27 @@ struct UninitAlloc : std::allocator<T> {
   UninitAlloc() = default;
   template <typename U>
   UninitAlloc(const UninitAlloc<U> &) {}
+  // GB-sized arrays on transparent huge pages: first touch and release
+  // (page faults / unmapping of 4 KB pages) dominate their cost otherwise
+  // (measured: on for the GB-sized route slots, off below 1 GB where
+  // concurrent 2 MB first-touch faults were slower than 4 KB ones)
+  static constexpr size_t kHuge = (size_t)64 << 20, kHugeAlign = (size_t)2 << 20, kHugeMin = (size_t)1 << 30;
+  T *allocate(size_t n) {
+    const size_t b = n * sizeof(T);
+    if (b < kHuge) return std::allocator<T>::allocate(n);
+    const size_t r = (b + kHugeAlign - 1) & ~(kHugeAlign - 1);
+    void *p = aligned_alloc(kHugeAlign, r);
+    if (!p) throw std::bad_alloc();
+    static const size_t thp = getenv("TSIM_THP_MIN") ? (size_t)atoll(getenv("TSIM_THP_MIN")) : kHugeMin;
+    if (b >= thp) madvise(p, r, MADV_HUGEPAGE);
+    return static_cast<T *>(p);
+  }
+  void deallocate(T *p, size_t n) {
+    if (n * sizeof(T) < kHuge)
+      std::allocator<T>::deallocate(p, n);
+    else
+      free(p);
+  }
   template <typename U>
   void construct(U *p) noexcept {
     ::new (static_cast<void *>(p)) U;
@@ -83,17 +105,17 @@ struct ts_sim {
   int64_t nlanes = 0, lane_cells = 0;
   // vehicles (host)
   int32_t nv = 0;
-  std::vector<int64_t> roff;
+  std::vector<int64_t, UninitAlloc<int64_t>> roff;
   // plans as out-slot sequences (R7): rslot[roff[f] + j] = slot of route link
   // j at its from-node (0xFF for j = 0); the link ids are not kept (a link
   // at cursor c is the walk from first_link along the slots, link_at)
   std::vector<uint8_t, UninitAlloc<uint8_t>> rslot;
-  std::vector<int32_t> dep, entry;
+  std::vector<int32_t, UninitAlloc<int32_t>> dep, entry;
   std::vector<int32_t> pl_vid, pl_lane, pl_cell, pl_v, pl_cur;
   std::vector<uint8_t> placed;
   std::vector<int32_t> arr0;     // arrival time of vehicles restored as arrived (-1 otherwise)
   std::vector<int32_t> text_link_id;  // link ids of a network file (ts_load_network_text)
-  std::vector<int32_t> first_link, entry_h;  // route[0] and entry cell (kept after init)
+  std::vector<int32_t, UninitAlloc<int32_t>> first_link, entry_h;  // route[0] and entry cell (kept after init)
   // domain decomposition (§4; ts_set_domain): owned cells per link
   int32_t dom_k = 1, dom_me = 0;
   std::vector<int32_t> dom_of_node;
@@ -270,11 +292,32 @@ static int upload(ts_sim *h, T **p, const std::vector<T, A> &v) {
   return TS_OK;
 }
 
+// TSIM_TRACE=1: wall-clock phases of ts_init on stderr (host-side tuning)
+struct InitTrace {
+  const char *what = "init";
+  bool on = getenv("TSIM_TRACE") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  InitTrace() = default;
+  explicit InitTrace(const char *w) : what(w) {}
+  void operator()(const char *phase) {
+    if (!on) return;
+    const auto n = std::chrono::steady_clock::now();
+    fprintf(stderr, "[tsim %s] %-28s %8.3f s\n", what, phase, std::chrono::duration<double>(n - t).count());
+    t = n;
+  }
+};
+
 // parallel loop over [0, n) in contiguous chunks on the host cores (load
 // and init handle billions of route entries at the largest configs)
 template <typename F>
 static void parallel_for(int64_t n, F f) {
-  const int nt = (int)std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+  // host threads: min(cores, 32) (TSIM_THREADS overrides, at most 64: the
+  // per-thread result arrays of the callers hold 64 entries)
+  static const int nt = []() {
+    const char *e = getenv("TSIM_THREADS");
+    const int cap = e ? std::max(1, std::min(64, atoi(e))) : 32;
+    return (int)std::max(1u, std::min((unsigned)cap, std::thread::hardware_concurrency()));
+  }();
   if (n < (int64_t)1 << 16 || nt == 1) {
     f((int64_t)0, n, 0);
     return;

@@ -60,3 +60,40 @@ def test_interleaved_async_handles():
     assert a.t == 5030
     t = a.totals()
     assert t["active"] + t["pending"] + t["arrived"] == s.n_vehicles
+
+
+@pytest.mark.parametrize("which", ["grid", "portland", "ring", "split"])
+def test_device_init_equals_host_init(which, monkeypatch):
+    """The row-tile placement built on the device (default) gives the same
+    state as the host build (TSIM_HOST_INIT=1): identical vehicle state at
+    t0 and after 30 steps, with general tiles (links > 128 cells), ring
+    rows and a split domain (at t0) in the mix"""
+    if which in ("grid", "split"):
+        s = scenarios.grid_trips(rows=4, cols=4, n_veh=3000, depart_max=20, seed=5, name="g")
+    elif which == "portland":
+        s = scenarios.portland(n_nodes=600, n_edges=800, n_veh=6000, side_km=8.0, n_zones=16, seed=4)
+    else:
+        s = scenarios.ring(n_cells=20_000, lanes=3, density=0.2, seed=2, steps=30)
+
+    def run(host):
+        if host:
+            monkeypatch.setenv("TSIM_HOST_INIT", "1")
+        else:
+            monkeypatch.delenv("TSIM_HOST_INIT", raising=False)
+        sim = tsim.Sim(p_slow=s.p_slow, seed=s.seed, flags=tsim.FLAG_FUSED | tsim.FLAG_HASH)
+        sim.load(s)
+        if which == "split":
+            sim.partition(2, 0)
+        sim.init(0)
+        out = [sim.vehicles(), sim.totals()["active"]]
+        if which != "split":  # (a lone domain with neighbours does not step)
+            sim.step(30)
+        out += [sim.vehicles(), sim.state_hash()]
+        sim.close()
+        return out
+
+    a, b = run(False), run(True)
+    for x, y in ((a[0], b[0]), (a[2], b[2])):
+        for k in x:
+            assert np.array_equal(x[k], y[k]), k
+    assert a[1] == b[1] and a[3] == b[3]
