@@ -1,3 +1,6 @@
+# round-end evidence on the GPU box: full GPU suite, smoke, the driver's bench command
+# (twice), the default bench, the reference arm, the ncu launch list of the
+# driver's window and full captures of k_rows / k_node_warp inside it
 python -m pytest tests -m gpu -q -x --durations=8 > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/pytest_gpu.log
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"; tail -1 gpurun_out/smoke.log
 python bench.py --steps 20 --warmup 5 > gpurun_out/bench_driver.log 2>&1; echo "bench rc=$?"
