@@ -485,6 +485,9 @@ static __device__ __noinline__ void vid_lists_global(const int32_t *ibase, int32
             ent_e, changed, ginj, dir, lane, inj_scratch);
 }
 
+#ifndef TS_ROWS_MLIST1
+#define TS_ROWS_MLIST1 0  // mover list: one loop over all words of the row
+#endif
 #ifndef TS_ROWS_DRAW2
 #define TS_ROWS_DRAW2 1  // two Philox chains per lane in the draw loop
 #endif
@@ -710,6 +713,28 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
         const uint32_t p32m1 = (uint32_t)(P.p32 - 1);
         if (staged) {  // mtot <= tot_in <= cap: the whole list fits
           int j = moff, rb = in_off;
+#if TS_ROWS_MLIST1
+          // one loop over the row's movers across its words (the warp
+          // iterates max-over-rows of the row's movers, not the sum over
+          // words of the per-word maxima)
+          {
+            int i = 0;
+            uint32_t m = U1[0], o = O[0];
+            int b = (rb << 12) | (lane << 7);
+            for (;;) {
+              while (m == 0u && i < NW - 1) {
+                b += (__popc(o) << 12) + 32;
+                i++;
+                m = i == 1 ? U1[1] : i == 2 ? U1[2] : U1[NW - 1];
+                o = i == 1 ? O[1] : i == 2 ? O[2] : O[NW - 1];
+              }
+              if (m == 0u) break;
+              const uint32_t lsb = m & (0u - m), below = lsb - 1u;
+              m ^= lsb;
+              mlist[j++] = b + (__popc(o & below) << 12) + __popc(below);
+            }
+          }
+#else
 #pragma unroll
           for (int i = 0; i < NW; i++) {
             uint32_t m = U1[i];
@@ -722,6 +747,7 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
             }
             rb += __popc(o);
           }
+#endif
           __syncwarp();
           // the draws: the vid from the staged block; brake bit by a shared-
           // memory reduction at word (row slot * NW + word) = (entry >> 5) & 127
