@@ -39,9 +39,13 @@ static NcclApi &nccl() {
   static NcclApi a;
   if (a.tried) return a;
   a.tried = true;
-  void *lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
-  if (!lib) lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
-  if (!lib) lib = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  // TSIM_NCCL_LIB: another library with the same entry points (the tests'
+  // in-process stand-in, tests/fake_nccl.cpp: several ranks on one GPU)
+  const char *alt = getenv("TSIM_NCCL_LIB");
+  void *lib = alt ? dlopen(alt, RTLD_NOW | RTLD_LOCAL) : nullptr;
+  if (!lib && !alt) lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+  if (!lib && !alt) lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!lib && !alt) lib = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
   if (!lib) return a;
   a.getUniqueId = (decltype(a.getUniqueId))dlsym(lib, "ncclGetUniqueId");
   a.commInitRank = (decltype(a.commInitRank))dlsym(lib, "ncclCommInitRank");
