@@ -160,7 +160,7 @@ def bench_reference(args):
         "impl": "reference", "metric": "vehicle-updates/s", "value": r["value"],
         "unit": "vehicle-updates/s", "n_gpus": args.gpus, "steps": r["steps"],
         "warmup": args.warmup, "ms_per_step": 1000 * r["seconds"] / max(1, r["steps"]),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int32",
         "data": "synthetic",
         "config": {"workload": WORKLOAD_NAMES.get(args.config, f"config{args.config}"),
                    "sample": r["desc"], "l2": "sample runs on the host (CPU oracle)",
@@ -187,10 +187,7 @@ def bench_tsim(args):
     flags = tsim.FLAG_FUSED | (tsim.FLAG_HASH if args.hash else 0)
     # e2e: wall clock around the public API from host arrays to the final
     # state on the host (H2D of network + vehicles, W+K steps, D2H of state)
-    h2d = sum(a.nbytes for a in (scn.node_x, scn.node_y, scn.link_from, scn.link_to,
-                                 scn.link_len_mm, scn.link_lanes, scn.link_vmax, scn.link_class,
-                                 scn.route_off, scn.route, scn.depart, scn.entry, scn.place_vid,
-                                 scn.place_lane, scn.place_cell, scn.place_v))
+    h2d = scenario_bytes(scn)
     # the CUDA context of the process is created before the timed region (a
     # throwaway handle): process start-up, not part of the job
     tsim.Sim(p_slow=scn.p_slow, seed=scn.seed, flags=flags).close()
@@ -225,12 +222,12 @@ def bench_tsim(args):
     out = {
         "metric": "vehicle-updates/s", "value": value, "unit": "vehicle-updates/s",
         "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms_total / args.steps, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": ms_total / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "u8",
         "data": "synthetic (seeded generator, DESIGN.md §5)",
         "config": {"workload": scn.name, "recipe": scn.recipe, "lane_cells": lane_cells,
                    "vehicles": scn.n_vehicles, "tiles": tot["tiles"],
-                   "l2": "inputs larger than L2 (state read+written per step > 126 MB)",
+                   "l2": l2_note(lane_cells),
                    "parallelism": "1 GPU, 1 domain", "flags": "fused" + ("+hash" if args.hash else "")},
         "real_time_ratio": rtr,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
@@ -262,6 +259,22 @@ def bench_tsim(args):
     print(json.dumps(out), flush=True)
 
 
+def l2_note(lane_cells):
+    """between timed steps the state is re-read from HBM only if it is larger
+    than the 126 MB L2 (no flush is done)"""
+    if 2 * lane_cells > 126e6:
+        return "inputs larger than L2 (state read+written per step > 126 MB)"
+    return "state fits in L2 (no flush between steps: a small-config number, not a roofline one)"
+
+
+def scenario_bytes(scn):
+    """host bytes the public API copies to the device for one scenario"""
+    return sum(a.nbytes for a in (scn.node_x, scn.node_y, scn.link_from, scn.link_to,
+                                  scn.link_len_mm, scn.link_lanes, scn.link_vmax, scn.link_class,
+                                  scn.route_off, scn.route, scn.depart, scn.entry, scn.place_vid,
+                                  scn.place_lane, scn.place_cell, scn.place_v))
+
+
 def bench_multi(args):
     """N > 1: one process per GPU, one domain of an ORB partition per rank
     (§4), two strip exchanges per step with the neighbour domains
@@ -289,6 +302,7 @@ def bench_multi(args):
     scn = workload(args.config)
     dom = domains.partition(scn, world)
     n_spl, pairs = domains.split_stats(scn, dom)
+    h2d = scenario_bytes(scn)  # every rank loads the whole network and plan set
     w0 = time.perf_counter()
     # native exchanges (the library's own NCCL communicator, whole steps per
     # ts_step call); torch.distributed send/recv between the phases otherwise
@@ -320,15 +334,17 @@ def bench_multi(args):
     tot = d.sim.totals()
     vst = d.sim.vehicles()
     e2e_local = time.perf_counter() - w0
+    # the warm-up steps update the vehicles of S(0) .. S(W-1) (counted for e2e)
+    upd_w = float(np.sum(d.sim.history(0, args.warmup)["active"]))
     loc = torch.tensor([float(np.sum(hist["active"][:args.steps])), float(tot["lane_cells"]),
-                        float(np.sum(hist["crossings"][1:])), e2e_local], dtype=torch.float64,
-                       device=red_dev)
+                        float(np.sum(hist["crossings"][1:])), e2e_local, upd_w],
+                       dtype=torch.float64, device=red_dev)
     s = loc.clone()
     dist.all_reduce(s, op=dist.ReduceOp.SUM)
     e2e = loc[3:4].clone()
     dist.all_reduce(e2e, op=dist.ReduceOp.MAX)
     ms_total = float(ms.item())
-    updates, lane_cells, cross = float(s[0]), float(s[1]), float(s[2])
+    updates, lane_cells, cross, upd_all = float(s[0]), float(s[1]), float(s[2]), float(s[0] + s[4])
     if rank == 0:
         value = updates / (ms_total / 1e3)
         alg = (2 * lane_cells * args.steps + 8 * updates + 12 * cross) / world
@@ -341,7 +357,7 @@ def bench_multi(args):
             "data": "synthetic (seeded generator, DESIGN.md §5)",
             "config": {"workload": scn.name, "recipe": scn.recipe, "lane_cells": int(lane_cells),
                        "vehicles": scn.n_vehicles,
-                       "l2": "inputs larger than L2 (state read+written per step > 126 MB)",
+                       "l2": l2_note(lane_cells),
                        "parallelism": f"{world} ranks, ORB domains, split links, 2 strip exchanges "
                                       f"per step ({'native NCCL' if d.native else 'torch.distributed ' + backend})",
                        "split_links": n_spl,
@@ -356,8 +372,8 @@ def bench_multi(args):
                          "frac": achieved / hbm_peak, "traffic": None,
                          "kernel": "whole step per GPU (incl. exchanges)",
                          "alg_bytes_per_launch": alg / args.steps, "peak_source": peak_src},
-            "e2e": {"value": (updates) / float(e2e.item()), "unit": "vehicle-updates/s",
-                    "h2d_bytes_per_step": None, "d2h_bytes_per_step": sum(
+            "e2e": {"value": upd_all / float(e2e.item()), "unit": "vehicle-updates/s",
+                    "h2d_bytes_per_step": h2d / (args.steps + args.warmup), "d2h_bytes_per_step": sum(
                         a.nbytes for a in vst.values()) / (args.steps + args.warmup),
                     "wall_s": float(e2e.item()),
                     "scope": "per rank: load+init+W+K steps+state readback, max over ranks"},
