@@ -344,7 +344,9 @@ def bench_multi(args):
     e2e = loc[3:4].clone()
     dist.all_reduce(e2e, op=dist.ReduceOp.MAX)
     ms_total = float(ms.item())
-    updates, lane_cells, cross, upd_all = float(s[0]), float(s[1]), float(s[2]), float(s[0] + s[4])
+    # every rank reports the whole network's lane-cells (ts_get_totals): once
+    updates, lane_cells, cross, upd_all = (float(s[0]), float(s[1]) / world, float(s[2]),
+                                           float(s[0] + s[4]))
     if rank == 0:
         value = updates / (ms_total / 1e3)
         alg = (2 * lane_cells * args.steps + 8 * updates + 12 * cross) / world
