@@ -43,7 +43,10 @@ def measured_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons during the timed region"""
+    """SM clocks + throttle reasons during the timed region: NVML every
+    millisecond (the driver's 20-step window is ~5 ms long), else nvidia-smi.
+    The wait for the sampler thread at exit is recorded (`exit_s`) so that
+    wall-clock timings can leave the harness out."""
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
@@ -53,28 +56,57 @@ class ClockSampler:
         self.rows = []
         self.stop = threading.Event()
         self.th = None
+        self.exit_s = 0.0
+        self.source = "nvidia-smi"
+        self.nvml = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = (pynvml, pynvml.nvmlDeviceGetHandleByIndex(gpu))
+            self.source = "nvml"
+        except Exception:
+            self.nvml = None
+
+    def _sample_nvml(self):
+        nv, h = self.nvml
+        r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+        act = lambda bit: "Active" if r & bit else "Not Active"  # noqa: E731
+        return [str(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)),
+                str(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)), hex(r),
+                act(nv.nvmlClocksEventReasonHwSlowdown), act(nv.nvmlClocksEventReasonHwThermalSlowdown),
+                act(nv.nvmlClocksEventReasonSwThermalSlowdown), act(nv.nvmlClocksEventReasonSwPowerCap)]
 
     def _run(self):
         while not self.stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True,
-                                     text=True, timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([c.strip() for c in out.split(",")])
+                if self.nvml:
+                    self.rows.append(self._sample_nvml())
+                else:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits"], capture_output=True,
+                                         text=True, timeout=5).stdout.strip()
+                    if out:
+                        self.rows.append([c.strip() for c in out.split(",")])
             except Exception:
                 pass
-            self.stop.wait(0.05)
+            self.stop.wait(0.001 if self.nvml else 0.05)
 
     def __enter__(self):
+        if self.nvml:  # one sample before the region starts
+            try:
+                self.rows.append(self._sample_nvml())
+            except Exception:
+                pass
         self.th = threading.Thread(target=self._run, daemon=True)
         self.th.start()
         return self
 
     def __exit__(self, *a):
+        t = time.perf_counter()
         self.stop.set()
         if self.th:
             self.th.join(timeout=10)
+        self.exit_s = time.perf_counter() - t
 
     def summary(self):
         if not self.rows:
@@ -89,7 +121,7 @@ class ClockSampler:
                     reasons.add(n)
         return {"sm_mhz": float(np.median(sm)) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
-                "samples": len(self.rows)}
+                "samples": len(self.rows), "source": self.source}
 
 
 def ncu_traffic():
@@ -191,19 +223,20 @@ def bench_tsim(args):
     # the CUDA context of the process is created before the timed region (a
     # throwaway handle): process start-up, not part of the job
     tsim.Sim(p_slow=scn.p_slow, seed=scn.seed, flags=flags).close()
+    clk = ClockSampler(int(os.environ.get("LOCAL_RANK", "0")))  # (set up outside the timed region)
     w0 = time.perf_counter()
     sim = tsim.Sim(p_slow=scn.p_slow, seed=scn.seed, flags=flags)
     sim.load(scn)
     sim.init(0)
     sim.step(args.warmup)
     tot = sim.totals()
-    with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
+    with clk:
         t_from = sim.t
         sim.step(args.steps)
     timing = sim.last_timing()
     hist = sim.history(t_from, args.steps + 1)
     vst = sim.vehicles()
-    e2e_wall = time.perf_counter() - w0
+    e2e_wall = time.perf_counter() - w0 - clk.exit_s  # (the clock sampler is harness)
     d2h = sum(a.nbytes for a in vst.values())
     ms_total = timing["total_ms"]
     updates = int(np.sum(hist["active"][:args.steps]))
@@ -303,6 +336,7 @@ def bench_multi(args):
     dom = domains.partition(scn, world)
     n_spl, pairs = domains.split_stats(scn, dom)
     h2d = scenario_bytes(scn)  # every rank loads the whole network and plan set
+    clk = ClockSampler(local)  # (NVML set up outside the timed region)
     w0 = time.perf_counter()
     # native exchanges (the library's own NCCL communicator, whole steps per
     # ts_step call); torch.distributed send/recv between the phases otherwise
@@ -315,7 +349,7 @@ def bench_multi(args):
     torch.cuda.synchronize()
     dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
+    with clk:
         t_from = d.t
         e0.record(d.stream)
         d.step(args.steps)
@@ -333,7 +367,7 @@ def bench_multi(args):
     hist = d.sim.history(t_from, args.steps + 1)
     tot = d.sim.totals()
     vst = d.sim.vehicles()
-    e2e_local = time.perf_counter() - w0
+    e2e_local = time.perf_counter() - w0 - clk.exit_s
     # the warm-up steps update the vehicles of S(0) .. S(W-1) (counted for e2e)
     upd_w = float(np.sum(d.sim.history(0, args.warmup)["active"]))
     loc = torch.tensor([float(np.sum(hist["active"][:args.steps])), float(tot["lane_cells"]),
