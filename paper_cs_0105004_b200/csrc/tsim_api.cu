@@ -367,6 +367,7 @@ int ts_place_vehicles_at(ts_sim *h, int32_t n, const int32_t *vid, const int32_t
   if (!h->have_veh) return fail(h, TS_EINVAL, "load vehicles first");
   if (h->inited) return fail(h, TS_EINVAL, "already initialised");
   if (n < 0) return fail(h, TS_EINVAL, "negative placement count");
+  InitTrace trace("load");
   // error code of placement i against the loaded routes (0 = ok)
   auto check = [&](int32_t i) -> int {
     const int32_t f = vid[i];
@@ -404,7 +405,10 @@ int ts_place_vehicles_at(ts_sim *h, int32_t n, const int32_t *vid, const int32_t
       h->pl_v[base + i] = v[i];
     }
   });
-  if (std::find(failed.begin(), failed.end(), 1) == failed.end()) return TS_OK;
+  if (std::find(failed.begin(), failed.end(), 1) == failed.end()) {
+    trace("placements");
+    return TS_OK;
+  }
   for (int32_t i = 0; i < n; i++)
     if (won[i]) h->placed[vid[i]] = 0;
   for (auto *a : {&h->pl_vid, &h->pl_cur, &h->pl_lane, &h->pl_cell, &h->pl_v}) a->resize(base);
@@ -1687,11 +1691,11 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
   trace("initial kernels");
   // the host copies of the plans are no longer needed (all on the device)
   std::vector<uint8_t, UninitAlloc<uint8_t>>().swap(h->rslot);
-  std::vector<int32_t>().swap(h->pl_vid);
-  std::vector<int32_t>().swap(h->pl_cur);
-  std::vector<int32_t>().swap(h->pl_lane);
-  std::vector<int32_t>().swap(h->pl_cell);
-  std::vector<int32_t>().swap(h->pl_v);
+  decltype(h->pl_vid)().swap(h->pl_vid);
+  decltype(h->pl_cur)().swap(h->pl_cur);
+  decltype(h->pl_lane)().swap(h->pl_lane);
+  decltype(h->pl_cell)().swap(h->pl_cell);
+  decltype(h->pl_v)().swap(h->pl_v);
   h->inited = true;
   trace("host plans freed");
   return TS_OK;

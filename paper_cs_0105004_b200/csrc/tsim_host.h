@@ -111,7 +111,7 @@ struct ts_sim {
   // at cursor c is the walk from first_link along the slots, link_at)
   std::vector<uint8_t, UninitAlloc<uint8_t>> rslot;
   std::vector<int32_t, UninitAlloc<int32_t>> dep, entry;
-  std::vector<int32_t> pl_vid, pl_lane, pl_cell, pl_v, pl_cur;
+  std::vector<int32_t, UninitAlloc<int32_t>> pl_vid, pl_lane, pl_cell, pl_v, pl_cur;
   std::vector<uint8_t> placed;
   std::vector<int32_t> arr0;     // arrival time of vehicles restored as arrived (-1 otherwise)
   std::vector<int32_t> text_link_id;  // link ids of a network file (ts_load_network_text)
