@@ -320,8 +320,8 @@ int ts_load_vehicles(ts_sim *h, int32_t n, const int64_t *route_off, const int32
     std::vector<int32_t> first_bad(64, INT32_MAX);
     parallel_for(n, [&](int64_t lo, int64_t hi, int t) {
       for (int64_t i = lo; i < hi; i++)
-        if (pred((int32_t)i)) {
-          first_bad[t] = (int32_t)i;
+        if (pred((int32_t)i)) {  // (this thread's chunks come in increasing order)
+          first_bad[t] = std::min(first_bad[t], (int32_t)i);
           return;
         }
     });
@@ -1400,6 +1400,7 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
   CK(h, cudaSetDevice(h->dev));
   if (h->dom_of_node.empty()) h->dom_of_node.assign(h->nn, 0);
   if (!build_tiles(h)) return fail(h, TS_EINTERNAL, "asymmetric exchange plan");
+  trace("tiles");
 
   // the routes (out-slot sequences built at load, GBs at the largest
   // configs) go to the device on a host thread of their own through pinned
@@ -1408,7 +1409,12 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
     std::thread th;
     cudaError_t err = cudaSuccess;
     double secs = 0;
+    // the DMA starts once the placement's own uploads are done (they would
+    // otherwise queue behind GBs of route data); the host copies into the
+    // pinned buffers start at once
+    std::atomic<bool> go{getenv("TSIM_ROUTE_UNGATED") != nullptr};
     ~RouteUpload() {
+      go = true;
       if (th.joinable()) th.join();
     }
   } rup;
@@ -1448,11 +1454,13 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
               });
             for (auto &t : cp) t.join();
           }
+          while (!rup.go.load()) std::this_thread::sleep_for(std::chrono::microseconds(200));
           if ((e = cudaMemcpyAsync(h->d_rslot + o, b, m, cudaMemcpyHostToDevice, st)) == cudaSuccess)
             e = cudaEventRecord(done[i & 1], st);
         }
         if (e == cudaSuccess) e = cudaStreamSynchronize(st);
       } else {
+        while (!rup.go.load()) std::this_thread::sleep_for(std::chrono::microseconds(200));
         e = cudaMemcpy(h->d_rslot, h->rslot.data(), nb, cudaMemcpyHostToDevice);
       }
       for (int i = 0; i < 2; i++) {
@@ -1465,6 +1473,7 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
 
   h->entry_h = h->entry;
 
+  trace("route upload started");
   if (h->ngroups > 0 && h->nv > (int32_t)kVidMask)
     return fail(h, TS_EINVAL, "too many vehicles for the row kernel");
   if (h->rvid_entries > INT32_MAX) return fail(h, TS_EINVAL, "network too large for one device");
@@ -1479,7 +1488,7 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
     if (b == 0 && (rc = dalloc(h, &h->d_gctr, 1, 0))) return rc;
   }
   if (h->ngroups > 0 && (rc = upload(h, &h->d_gvoff, h->gvoff))) return rc;
-  trace("tiles + device state");
+  trace("device state");
   // the initial placement: row tiles built on the device (TSIM_HOST_INIT=1:
   // on the host, as are a doubly claimed cell's exact report and an
   // oversized row table)
@@ -1496,6 +1505,7 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
     h->n_placed = 0;
     if ((rc = place_host(h, cur0, gcode, gvid))) return rc;
   }
+  rup.go = true;  // the route DMA may start
   trace("placement");
   // pending lists per first link in (departure, vid) order (R13)
   std::vector<int32_t> pend_off(h->nl + 1, 0), pend_list;

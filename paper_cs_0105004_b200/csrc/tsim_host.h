@@ -8,6 +8,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <atomic>
 #include <climits>
 #include <cmath>
 #include <cstdarg>
@@ -308,7 +309,11 @@ struct InitTrace {
 };
 
 // parallel loop over [0, n) in contiguous chunks on the host cores (load
-// and init handle billions of route entries at the largest configs)
+// and init handle billions of route entries at the largest configs).  The
+// chunks (16 per thread) are handed out dynamically: a thread delayed by
+// the library's own copy threads or another process does not hold up the
+// loop.  f(lo, hi, t) is called once per chunk, chunks of one thread t in
+// increasing order.
 template <typename F>
 static void parallel_for(int64_t n, F f) {
   // host threads: min(cores, 32) (TSIM_THREADS overrides, at most 64: the
@@ -322,9 +327,21 @@ static void parallel_for(int64_t n, F f) {
     f((int64_t)0, n, 0);
     return;
   }
+  if (getenv("TSIM_STATIC_CHUNKS")) {  // one contiguous range per thread (A/B timing)
+    std::vector<std::thread> th;
+    for (int i = 0; i < nt; i++)
+      th.emplace_back([=, &f]() { f(n * i / nt, n * (i + 1) / nt, i); });
+    for (auto &t : th) t.join();
+    return;
+  }
+  const int64_t chunks = std::min<int64_t>(n, (int64_t)nt * 16);
+  std::atomic<int64_t> next{0};
   std::vector<std::thread> th;
   for (int i = 0; i < nt; i++)
-    th.emplace_back([=, &f]() { f(n * i / nt, n * (i + 1) / nt, i); });
+    th.emplace_back([=, &f, &next]() {
+      for (int64_t c; (c = next.fetch_add(1, std::memory_order_relaxed)) < chunks;)
+        f(n * c / chunks, n * (c + 1) / chunks, i);
+    });
   for (auto &t : th) t.join();
 }
 
