@@ -538,6 +538,9 @@ __device__ __forceinline__ void node_flush(const NodeParams &P, uint32_t crossin
 // stage by stage (records, out-slot table, target heads, grant), so their
 // dependent loads overlap instead of running as one latency chain per
 // chunk.
+#ifndef TS_NODE_HEAD_EARLY
+#define TS_NODE_HEAD_EARLY 1  // measured: window -0.3 %, steady -0.5 % per step
+#endif
 #ifndef TS_NODE_ILP
 #define TS_NODE_ILP 1  // measured on 4a: 1 -> 31.5 us, 2 -> 35, 4 -> 39.6, 8 -> 49.6
 #endif
@@ -574,6 +577,7 @@ __global__ void __launch_bounds__(256) k_node_warp(const NodeParams P_, const No
     rec[k] = P.tail_rec[32 * min(c0 + k, W.nchunks - 1) + lane];
   Cand cd[kNodeILP];
   bool win[kNodeILP];
+  uint8_t head[kNodeILP];
 #pragma unroll
   for (int k = 0; k < kNodeILP; k++) {  // stage 2: candidates and winners
     const bool a = act[k] && e[k].lane_gid >= 0;
@@ -583,6 +587,11 @@ __global__ void __launch_bounds__(256) k_node_warp(const NodeParams P_, const No
         (__ballot_sync(FULL, a && e[k].major && (((uint32_t)(rec[k] >> 44)) & gmask)) & nodemask) != 0u;
     cd[k] = Cand{false, -1, 0, 0, 0, 0, -1};
     if (a) cd[k] = node_candidate(P, rec[k], e[k].lane, e[k].out_base, e[k].tt, e[k].vk);
+#if TS_NODE_HEAD_EARLY
+    // every candidate's target head, loaded before the winner is known (one
+    // dependent load less on the chain; losers' loads are wasted)
+    head[k] = cd[k].cand ? P.head_occ[cd[k].tgt] : (uint8_t)0;
+#endif
     // signalized node (R23): red approaches have the virtual blocker, green
     // ones need no gap acceptance; otherwise priority + gap acceptance (R9)
     const bool eligible =
@@ -590,10 +599,11 @@ __global__ void __launch_bounds__(256) k_node_warp(const NodeParams P_, const No
     const uint32_t grp = __match_any_sync(FULL, eligible ? cd[k].tgt : -1 - lane);
     win[k] = eligible && (__ffs(grp) - 1) == lane;
   }
-  uint8_t head[kNodeILP];
+#if !TS_NODE_HEAD_EARLY
 #pragma unroll
   for (int k = 0; k < kNodeILP; k++)  // stage 3: target heads
     head[k] = win[k] ? P.head_occ[cd[k].tgt] : (uint8_t)0;
+#endif
 #pragma unroll
   for (int k = 0; k < kNodeILP; k++) {  // stage 4: grants
     int ext = 0;
