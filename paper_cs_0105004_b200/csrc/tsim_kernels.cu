@@ -465,6 +465,9 @@ __global__ void __launch_bounds__(256) k_hash(const StepParams P, unsigned long 
 // order; the winner is granted the entry space E and, if its velocity takes
 // it past the stop line, is written as the entrant of the target lane.
 // ====================================================================
+#ifndef TS_NODE_VPOS_EARLY
+#define TS_NODE_VPOS_EARLY 0
+#endif
 struct Cand {
   bool cand;
   int tgt, n2, d, v, vid;
@@ -498,6 +501,12 @@ __device__ __forceinline__ Cand node_candidate(const NodeParams &P, uint64_t rec
 // position record (16 bytes per vehicle) is read only for a crossing.
 __device__ __forceinline__ int node_grant(const NodeParams &P, const Cand &c, int vk, uint8_t head,
                                           uint32_t &crossings, bool pass = false) {
+#if TS_NODE_VPOS_EARLY
+  // the route position, loaded before the draw decides whether it crosses
+  // (its DRAM latency overlaps the Philox rounds)
+  VehPos q0{};
+  if (!pass) q0 = P.vpos[c.vid];
+#endif
   const int E = min(ctz32((uint32_t)head | 0x20u), min(kGmax, c.n2));
   if (E == 0) return 0;
   const int v3 = nasch_v3(c.v, vk, min(kGmax, c.d + E), (uint32_t)P.t, (uint32_t)c.vid, P.k0,
@@ -505,7 +514,11 @@ __device__ __forceinline__ int node_grant(const NodeParams &P, const Cand &c, in
   if (v3 > c.d) {
     int nslot = 0;  // pass-through node of a ring: straight on, same route position
     if (!pass) {
+#if TS_NODE_VPOS_EARLY
+      const VehPos q = q0;
+#else
       const VehPos q = P.vpos[c.vid];
+#endif
       nslot = (q.p + 2 < q.e) ? (int)P.rslot[q.p + 2] : kSlotFinal;
       P.vpos[c.vid].p = q.p + 1;
     }
