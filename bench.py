@@ -224,10 +224,13 @@ def bench_tsim(args):
     # throwaway handle): process start-up, not part of the job
     tsim.Sim(p_slow=scn.p_slow, seed=scn.seed, flags=flags).close()
     clk = ClockSampler(int(os.environ.get("LOCAL_RANK", "0")))  # (set up outside the timed region)
+    ph = {}  # wall-clock phases of the e2e region
     w0 = time.perf_counter()
     sim = tsim.Sim(p_slow=scn.p_slow, seed=scn.seed, flags=flags)
     sim.load(scn)
+    ph["load"] = time.perf_counter() - w0
     sim.init(0)
+    ph["init"] = time.perf_counter() - w0 - ph["load"]
     sim.step(args.warmup)
     tot = sim.totals()
     with clk:
@@ -235,8 +238,11 @@ def bench_tsim(args):
         sim.step(args.steps)
     timing = sim.last_timing()
     hist = sim.history(t_from, args.steps + 1)
+    t_rd = time.perf_counter()
     vst = sim.vehicles()
+    ph["readback"] = time.perf_counter() - t_rd
     e2e_wall = time.perf_counter() - w0 - clk.exit_s  # (the clock sampler is harness)
+    ph["steps_and_stats"] = e2e_wall - ph["load"] - ph["init"] - ph["readback"]
     d2h = sum(a.nbytes for a in vst.values())
     ms_total = timing["total_ms"]
     updates = int(np.sum(hist["active"][:args.steps]))
@@ -276,7 +282,8 @@ def bench_tsim(args):
         "e2e": {"value": upd_all / e2e_wall, "unit": "vehicle-updates/s",
                 "h2d_bytes_per_step": h2d / (args.steps + args.warmup),
                 "d2h_bytes_per_step": d2h / (args.steps + args.warmup),
-                "wall_s": e2e_wall, "scope": "load+init+W+K steps+state readback (CUDA context created before)"},
+                "wall_s": e2e_wall, "phases_s": {k: round(v, 4) for k, v in ph.items()},
+                "scope": "load+init+W+K steps+state readback (CUDA context created before)"},
         "clocks": clk.summary(),
         "gpu_launches": 1 + 2 * args.steps,
         "gen_s": t_gen,
