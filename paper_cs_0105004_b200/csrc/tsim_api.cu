@@ -181,6 +181,10 @@ void ts_destroy(ts_sim *h) {
   if (h->ev_join) cudaEventDestroy(h->ev_join);
   if (h->ev_packed) cudaEventDestroy(h->ev_packed);
   if (h->ev_copied) cudaEventDestroy(h->ev_copied);
+  for (int i = 0; i < 2; i++) {
+    if (h->pin_rd[i]) cudaFreeHost(h->pin_rd[i]);
+    if (h->ev_rd[i]) cudaEventDestroy(h->ev_rd[i]);
+  }
   delete h;
 }
 

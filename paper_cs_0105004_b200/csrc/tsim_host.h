@@ -196,6 +196,10 @@ struct ts_sim {
   int32_t *d_out_pos = nullptr;
   int64_t *d_roff = nullptr;   // route offsets (device read-back of cursors; allocated on demand)
   int32_t *d_rd = nullptr;     // read-back scratch (ts_read_vehicles on the device)
+  // pinned double buffer of the read-back (device -> pinned by DMA, pinned ->
+  // caller's arrays by the host cores), allocated at the first large read
+  uint8_t *pin_rd[2] = {nullptr, nullptr};
+  cudaEvent_t ev_rd[2] = {nullptr, nullptr};
   uint8_t *d_rslot = nullptr;
   NodeOut *d_nodeout = nullptr;
   VehPos *d_vpos = nullptr;

@@ -109,6 +109,68 @@ __global__ void __launch_bounds__(256) k_read_status(int32_t nv, ReadOut o, cons
   }
 }
 
+// device -> host copies of several arrays through the handle's pinned
+// double buffer: the DMA of one chunk overlaps the host cores' copy of the
+// previous one into the caller's (pageable) memory, whose first-touch page
+// faults are then taken by all cores instead of the driver's one staging
+// thread.  Small totals (or TSIM_PAGEABLE_READ) use plain cudaMemcpy.
+struct D2H {
+  void *dst;
+  const void *src;
+  size_t n;
+};
+static int d2h_staged(ts_sim *h, const std::vector<D2H> &segs) {
+  constexpr size_t kChunk = (size_t)32 << 20;
+  size_t total = 0;
+  for (const D2H &d : segs) total += d.dst ? d.n : 0;
+  const bool staged = total >= 2 * kChunk && getenv("TSIM_PAGEABLE_READ") == nullptr;
+  if (staged && !h->pin_rd[0]) {
+    for (int i = 0; i < 2; i++) {
+      if (cudaMallocHost(&h->pin_rd[i], kChunk) != cudaSuccess ||
+          cudaEventCreateWithFlags(&h->ev_rd[i], cudaEventDisableTiming) != cudaSuccess) {
+        cudaGetLastError();
+        for (int j = 0; j < 2; j++) {
+          if (h->pin_rd[j]) cudaFreeHost(h->pin_rd[j]);
+          if (h->ev_rd[j]) cudaEventDestroy(h->ev_rd[j]);
+          h->pin_rd[j] = nullptr;
+          h->ev_rd[j] = nullptr;
+        }
+        break;
+      }
+    }
+  }
+  if (!staged || !h->pin_rd[0]) {
+    for (const D2H &d : segs)
+      if (d.dst && d.n) CK(h, cudaMemcpy(d.dst, d.src, d.n, cudaMemcpyDeviceToHost));
+    return TS_OK;
+  }
+  struct Chunk {
+    uint8_t *dst;
+    const uint8_t *src;
+    size_t n;
+  };
+  std::vector<Chunk> ch;
+  for (const D2H &d : segs)
+    if (d.dst)
+      for (size_t o = 0; o < d.n; o += kChunk)
+        ch.push_back(Chunk{static_cast<uint8_t *>(d.dst) + o, static_cast<const uint8_t *>(d.src) + o,
+                           std::min(kChunk, d.n - o)});
+  auto issue = [&](size_t c) -> cudaError_t {
+    cudaError_t e = cudaMemcpyAsync(h->pin_rd[c & 1], ch[c].src, ch[c].n, cudaMemcpyDeviceToHost, h->stream);
+    return e == cudaSuccess ? cudaEventRecord(h->ev_rd[c & 1], h->stream) : e;
+  };
+  CK(h, issue(0));
+  for (size_t c = 0; c < ch.size(); c++) {
+    if (c + 1 < ch.size()) CK(h, issue(c + 1));  // its buffer was emptied in the last iteration
+    CK(h, cudaEventSynchronize(h->ev_rd[c & 1]));
+    const uint8_t *b = h->pin_rd[c & 1];
+    uint8_t *dst = ch[c].dst;
+    parallel_for((int64_t)ch[c].n,
+                 [&](int64_t lo, int64_t hi, int) { std::memcpy(dst + lo, b + lo, (size_t)(hi - lo)); });
+  }
+  return TS_OK;
+}
+
 static int read_vehicles_device(ts_sim *h, int8_t *status, int32_t *link, int32_t *lane,
                                 int32_t *cell, int32_t *v, int32_t *cursor, int32_t *t_arrive) {
   const size_t nv = (size_t)std::max(h->nv, 1);
@@ -151,14 +213,8 @@ static int read_vehicles_device(ts_sim *h, int8_t *status, int32_t *link, int32_
   if (bad[1] != 0x7f7f7f7f) return fail(h, TS_EINTERNAL, "corrupt state: vehicle %d lost", bad[1]);
   const size_t b4 = (size_t)h->nv * 4;
   if (h->nv == 0) return TS_OK;
-  if (status) CK(h, cudaMemcpy(status, dst, (size_t)h->nv, cudaMemcpyDeviceToHost));
-  if (link) CK(h, cudaMemcpy(link, o.link, b4, cudaMemcpyDeviceToHost));
-  if (lane) CK(h, cudaMemcpy(lane, o.lane, b4, cudaMemcpyDeviceToHost));
-  if (cell) CK(h, cudaMemcpy(cell, o.cell, b4, cudaMemcpyDeviceToHost));
-  if (v) CK(h, cudaMemcpy(v, o.v, b4, cudaMemcpyDeviceToHost));
-  if (cursor) CK(h, cudaMemcpy(cursor, dcur, b4, cudaMemcpyDeviceToHost));
-  if (t_arrive) CK(h, cudaMemcpy(t_arrive, darr, b4, cudaMemcpyDeviceToHost));
-  return TS_OK;
+  return d2h_staged(h, {{status, dst, (size_t)h->nv}, {link, o.link, b4}, {lane, o.lane, b4},
+                        {cell, o.cell, b4}, {v, o.v, b4}, {cursor, dcur, b4}, {t_arrive, darr, b4}});
 }
 
 extern "C" {
