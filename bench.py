@@ -220,9 +220,11 @@ def bench_tsim(args):
     # e2e: wall clock around the public API from host arrays to the final
     # state on the host (H2D of network + vehicles, W+K steps, D2H of state)
     h2d = scenario_bytes(scn)
-    # the CUDA context of the process is created before the timed region (a
-    # throwaway handle): process start-up, not part of the job
-    tsim.Sim(p_slow=scn.p_slow, seed=scn.seed, flags=flags).close()
+    # process start-up happens before the timed region: the CUDA context,
+    # the lazily loaded kernel modules and the driver's staging buffers,
+    # warmed by a throwaway 8x8-node grid of the same recipe run through the
+    # same calls (nothing of it is reused: it has its own handle and data)
+    warm_up(tsim, scn, flags)
     clk = ClockSampler(int(os.environ.get("LOCAL_RANK", "0")))  # (set up outside the timed region)
     ph = {}  # wall-clock phases of the e2e region
     w0 = time.perf_counter()
@@ -299,6 +301,20 @@ def bench_tsim(args):
     print(json.dumps(out), flush=True)
 
 
+def warm_up(tsim, scn, flags, device=0):
+    """process start-up outside the timed region: CUDA context, lazily
+    loaded kernel modules, the driver's staging buffers -- a throwaway 8x8
+    grid of the 4a recipe through load / init / step / read"""
+    warm = scenarios.big_grid(rows=8, cols=8, seed=scn.seed + 1, name="warm-up")
+    ws = tsim.Sim(p_slow=warm.p_slow, seed=warm.seed, flags=flags, device=device)
+    ws.load(warm)
+    ws.init(0)
+    ws.step(3)
+    ws.step(2)
+    ws.vehicles()
+    ws.close()
+
+
 def l2_note(lane_cells):
     """between timed steps the state is re-read from HBM only if it is larger
     than the 126 MB L2 (no flush is done)"""
@@ -343,6 +359,7 @@ def bench_multi(args):
     dom = domains.partition(scn, world)
     n_spl, pairs = domains.split_stats(scn, dom)
     h2d = scenario_bytes(scn)  # every rank loads the whole network and plan set
+    warm_up(tsim, scn, tsim.FLAG_FUSED, device=local)
     clk = ClockSampler(local)  # (NVML set up outside the timed region)
     w0 = time.perf_counter()
     # native exchanges (the library's own NCCL communicator, whole steps per
