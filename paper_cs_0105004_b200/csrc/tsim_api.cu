@@ -1467,9 +1467,15 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
         while (!rup.go.load()) std::this_thread::sleep_for(std::chrono::microseconds(200));
         e = cudaMemcpy(h->d_rslot, h->rslot.data(), nb, cudaMemcpyHostToDevice);
       }
-      for (int i = 0; i < 2; i++) {
-        if (pin[i]) cudaFreeHost(pin[i]);
+      for (int i = 0; i < 2; i++)
         if (done[i]) cudaEventDestroy(done[i]);
+      if (pin[0] && pin[1] && !h->pin_rd[0]) {  // kept as the read-back staging
+        h->pin_rd[0] = pin[0];
+        h->pin_rd[1] = pin[1];
+        h->pin_rd_bytes = chunk;
+      } else {
+        for (int i = 0; i < 2; i++)
+          if (pin[i]) cudaFreeHost(pin[i]);
       }
       if (st) cudaStreamDestroy(st);
     });

@@ -198,7 +198,8 @@ struct ts_sim {
   int32_t *d_rd = nullptr;     // read-back scratch (ts_read_vehicles on the device)
   // pinned double buffer of the read-back (device -> pinned by DMA, pinned ->
   // caller's arrays by the host cores), allocated at the first large read
-  uint8_t *pin_rd[2] = {nullptr, nullptr};
+  uint8_t *pin_rd[2] = {nullptr, nullptr};  // (the route upload's staging, kept after init)
+  size_t pin_rd_bytes = 0;
   cudaEvent_t ev_rd[2] = {nullptr, nullptr};
   uint8_t *d_rslot = nullptr;
   NodeOut *d_nodeout = nullptr;

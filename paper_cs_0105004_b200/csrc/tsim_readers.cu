@@ -120,26 +120,28 @@ struct D2H {
   size_t n;
 };
 static int d2h_staged(ts_sim *h, const std::vector<D2H> &segs) {
-  constexpr size_t kChunk = (size_t)32 << 20;
   size_t total = 0;
   for (const D2H &d : segs) total += d.dst ? d.n : 0;
-  const bool staged = total >= 2 * kChunk && getenv("TSIM_PAGEABLE_READ") == nullptr;
-  if (staged && !h->pin_rd[0]) {
-    for (int i = 0; i < 2; i++) {
-      if (cudaMallocHost(&h->pin_rd[i], kChunk) != cudaSuccess ||
-          cudaEventCreateWithFlags(&h->ev_rd[i], cudaEventDisableTiming) != cudaSuccess) {
+  const bool staged = total >= ((size_t)64 << 20) && getenv("TSIM_PAGEABLE_READ") == nullptr;
+  if (staged && !h->pin_rd[0]) {  // (no route staging kept: a network without routes to upload)
+    h->pin_rd_bytes = (size_t)32 << 20;
+    for (int i = 0; i < 2 && h->pin_rd_bytes; i++)
+      if (cudaMallocHost(&h->pin_rd[i], h->pin_rd_bytes) != cudaSuccess) {
         cudaGetLastError();
         for (int j = 0; j < 2; j++) {
           if (h->pin_rd[j]) cudaFreeHost(h->pin_rd[j]);
-          if (h->ev_rd[j]) cudaEventDestroy(h->ev_rd[j]);
           h->pin_rd[j] = nullptr;
-          h->ev_rd[j] = nullptr;
         }
-        break;
+        h->pin_rd_bytes = 0;
       }
-    }
   }
-  if (!staged || !h->pin_rd[0]) {
+  if (staged && h->pin_rd[0] && !h->ev_rd[0])
+    for (int i = 0; i < 2; i++)
+      if (cudaEventCreateWithFlags(&h->ev_rd[i], cudaEventDisableTiming) != cudaSuccess) {
+        cudaGetLastError();
+        h->ev_rd[i] = nullptr;
+      }
+  if (!staged || !h->pin_rd[0] || !h->ev_rd[0] || !h->ev_rd[1]) {
     for (const D2H &d : segs)
       if (d.dst && d.n) CK(h, cudaMemcpy(d.dst, d.src, d.n, cudaMemcpyDeviceToHost));
     return TS_OK;
@@ -152,9 +154,9 @@ static int d2h_staged(ts_sim *h, const std::vector<D2H> &segs) {
   std::vector<Chunk> ch;
   for (const D2H &d : segs)
     if (d.dst)
-      for (size_t o = 0; o < d.n; o += kChunk)
+      for (size_t o = 0; o < d.n; o += h->pin_rd_bytes)
         ch.push_back(Chunk{static_cast<uint8_t *>(d.dst) + o, static_cast<const uint8_t *>(d.src) + o,
-                           std::min(kChunk, d.n - o)});
+                           std::min(h->pin_rd_bytes, d.n - o)});
   auto issue = [&](size_t c) -> cudaError_t {
     cudaError_t e = cudaMemcpyAsync(h->pin_rd[c & 1], ch[c].src, ch[c].n, cudaMemcpyDeviceToHost, h->stream);
     return e == cudaSuccess ? cudaEventRecord(h->ev_rd[c & 1], h->stream) : e;
