@@ -176,7 +176,11 @@ int ts_set_signals(ts_sim *h, int32_t n, const int32_t *node, const int32_t *gre
 /* Build the device layout, upload, and run the initial injection of
  * vehicles with departure <= t0 (clock starts at t0).  In domain mode with
  * partners the boundary strips of S(t0) are packed at the end: exchange
- * them (below), then call ts_step_phase(h, 2, 0). */
+ * them (below), then call ts_step_phase(h, 2, 0).  The initial placement of
+ * the row tiles is built on the device (TSIM_HOST_INIT=1: on the host); a
+ * cell claimed twice is TS_EINVAL naming the first such placement in input
+ * order.  The handle keeps the route upload's pinned staging (2 x 64 MB of
+ * page-locked host memory) for ts_read_vehicles until ts_destroy. */
 int ts_init(ts_sim *h, int32_t t0);
 /* As ts_init without the initial injection: the placed / arrived /
  * pending vehicles ARE the state S(t) (restore at time t). */
@@ -238,6 +242,10 @@ int32_t ts_time(const ts_sim *h);
  * another domain's cells read TS_ABSENT; a pending vehicle is reported by
  * the domain owning its entry cell; merge by taking, per vehicle, the
  * domain that reports it ACTIVE, else ARRIVED, else PENDING. */
+/* (single-domain handles: gathered by vid on the device; copies of >= 64
+ * MB go through the handle's pinned double buffer, TSIM_PAGEABLE_READ=1:
+ * plain cudaMemcpy.  TS_EINTERNAL "corrupt state" if a vid is held twice or
+ * an unfinished vehicle is missing.) */
 int ts_read_vehicles(ts_sim *h, int8_t *status, int32_t *link, int32_t *lane,
                      int32_t *cell, int32_t *v, int32_t *cursor,
                      int32_t *t_arrive);
