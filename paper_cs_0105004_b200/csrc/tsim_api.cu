@@ -1284,6 +1284,20 @@ __global__ void k_place_lists(const uint32_t *__restrict__ pos, const uint32_t *
   rvid[rowoff[s] + r] = (int32_t)ent[i];
 }
 
+// per-vehicle words of a fresh start (no restored arrivals) built on the
+// device from the route offsets (uploaded once, also used by the read-back),
+// the initial cursors and the placed flags: route position, injection word
+// (placed: INT_MIN, pending: INT_MAX), arrival time -1
+__global__ void k_init_vehicles(int nv, const int64_t *__restrict__ roff, const int32_t *__restrict__ cur0,
+                                const uint8_t *__restrict__ placed, VehPos *vpos, int32_t *inj,
+                                int32_t *arr) {
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= nv) return;
+  vpos[f] = VehPos{roff[f] + cur0[f], roff[f + 1]};
+  inj[f] = placed[f] ? INT_MIN : INT_MAX;
+  arr[f] = -1;
+}
+
 // the placement with the row tiles built on the device (general tiles on
 // the host, at their own offsets); kPlaceHost when the host path must run
 static int place_device(ts_sim *h, HostVec<int32_t> &cur0, std::vector<uint8_t> &gcode,
@@ -1548,10 +1562,16 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
       std::stable_sort(pend_list.begin() + pend_off[k], pend_list.begin() + pend_off[k + 1],
                        [&](int a, int b) { return h->dep[a] < h->dep[b] || (h->dep[a] == h->dep[b] && a < b); });
   }
-  HostVec<int32_t> inj(h->nv), arr = filled<int32_t>(h->nv, -1);
-  parallel_for(h->nv, [&](int64_t lo, int64_t hi, int) {
-    for (int64_t f = lo; f < hi; f++) inj[f] = h->placed[f] ? INT_MIN : INT_MAX;
-  });
+  // a fresh start builds the per-vehicle words on the device (below)
+  const bool dev_veh = h->arr0.empty() && h->nv > 0 && getenv("TSIM_HOST_INIT") == nullptr;
+  HostVec<int32_t> inj, arr;
+  if (!dev_veh) {
+    inj.resize(h->nv);
+    arr = filled<int32_t>(h->nv, -1);
+    parallel_for(h->nv, [&](int64_t lo, int64_t hi, int) {
+      for (int64_t f = lo; f < hi; f++) inj[f] = h->placed[f] ? INT_MIN : INT_MAX;
+    });
+  }
   h->n_arrived0 = 0;
   if (!h->arr0.empty()) {
     for (int f = 0; f < h->nv; f++) {
@@ -1602,18 +1622,34 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
     }
     if ((rc = upload(h, &h->d_nodeout, h->ring_rows ? h->ring_nodeout : nodeout))) return rc;
   }
-  {
+  if (dev_veh) {  // 12 bytes per vehicle cross PCIe instead of 24
+    if (!h->d_roff && (rc = upload(h, &h->d_roff, h->roff))) return rc;
+    if ((rc = dalloc(h, &h->d_vpos, h->nv))) return rc;
+    if ((rc = dalloc(h, &h->d_inj, h->nv))) return rc;
+    if ((rc = dalloc(h, &h->d_arr, h->nv))) return rc;
+    int32_t *d_cur = nullptr;
+    uint8_t *d_placed = nullptr;
+    CK(h, cudaMallocAsync(&d_cur, (size_t)h->nv * 4, h->stream));
+    CK(h, cudaMallocAsync(&d_placed, (size_t)h->nv, h->stream));
+    CK(h, cudaMemcpyAsync(d_cur, cur0.data(), (size_t)h->nv * 4, cudaMemcpyHostToDevice, h->stream));
+    CK(h, cudaMemcpyAsync(d_placed, h->placed.data(), (size_t)h->nv, cudaMemcpyHostToDevice, h->stream));
+    k_init_vehicles<<<(h->nv + 255) / 256, 256, 0, h->stream>>>(h->nv, h->d_roff, d_cur, d_placed,
+                                                                h->d_vpos, h->d_inj, h->d_arr);
+    CK(h, cudaGetLastError());
+    CK(h, cudaFreeAsync(d_cur, h->stream));
+    CK(h, cudaFreeAsync(d_placed, h->stream));
+  } else {
     HostVec<VehPos> vp(h->nv);
     parallel_for(h->nv, [&](int64_t lo, int64_t hi, int) {
       for (int64_t f = lo; f < hi; f++) vp[f] = VehPos{h->roff[f] + cur0[f], h->roff[f + 1]};
     });
     if ((rc = upload(h, &h->d_vpos, vp))) return rc;
+    if ((rc = upload(h, &h->d_inj, inj))) return rc;
+    if ((rc = upload(h, &h->d_arr, arr))) return rc;
   }
   trace("node outs + vehicle positions");
   if ((rc = upload(h, &h->d_dep, h->dep))) return rc;
   if ((rc = upload(h, &h->d_entry, h->entry))) return rc;
-  if ((rc = upload(h, &h->d_inj, inj))) return rc;
-  if ((rc = upload(h, &h->d_arr, arr))) return rc;
   if ((rc = upload(h, &h->d_pend_off, pend_off))) return rc;
   if ((rc = upload(h, &h->d_pend_list, pend_list))) return rc;
   {  // absolute head index into pend_list per link
