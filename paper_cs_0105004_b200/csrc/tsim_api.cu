@@ -339,7 +339,34 @@ int ts_load_vehicles(ts_sim *h, int32_t n, const int64_t *route_off, const int32
   trace("offsets");
   h->rslot.resize(n > 0 ? route_off[n] : 0);
   uint8_t *const slot = h->rslot.data();
-  const int32_t bad = first_failing([&](int32_t i) { return check(i, slot) != 0; });
+  // the conversion pass: 8-byte records (from, to | slot << 24) and no
+  // branch per route entry (errors accumulate per vehicle; the first
+  // failing vehicle is then classified by check); networks with >= 2^24
+  // nodes take check itself
+  const bool packed = h->nn < (1 << 24) && getenv("TSIM_LOAD_CHECKED") == nullptr;
+  std::vector<uint64_t> prec(packed ? h->nl : 0);
+  for (int k = 0; k < (packed ? h->nl : 0); k++)
+    prec[k] = (uint64_t)(uint32_t)h->from[k] | ((uint64_t)((uint32_t)h->to[k] | ((uint32_t)h->out_pos[k] << 24)) << 32);
+  const uint64_t *pr = prec.data();
+  auto convert = [&, pr, nl, ncell](int32_t i) -> bool {  // true: vehicle i fails
+    const int64_t a = route_off[i], b = route_off[i + 1];
+    const uint32_t k0 = (uint32_t)route_links[a];
+    if (k0 >= nl) return true;
+    slot[a] = 0xFF;
+    uint32_t at = (uint32_t)(pr[k0] >> 32) & 0xFFFFFFu, bad = 0u;
+    for (int64_t j = a + 1; j < b; j++) {
+      const uint32_t k = (uint32_t)route_links[j];
+      bad |= k >= nl ? 1u : 0u;
+      const uint64_t r = pr[k < nl ? k : 0u];
+      bad |= (uint32_t)r != at ? 1u : 0u;
+      const uint32_t hi = (uint32_t)(r >> 32);
+      slot[j] = (uint8_t)(hi >> 24);
+      at = hi & 0xFFFFFFu;
+    }
+    return bad != 0u || entry_cell[i] < 0 || entry_cell[i] >= ncell[k0];
+  };
+  const int32_t bad = packed ? first_failing(convert)
+                             : first_failing([&](int32_t i) { return check(i, slot) != 0; });
   if (bad != INT32_MAX) {
     decltype(h->rslot)().swap(h->rslot);
     return fail(h, TS_EINVAL, "vehicle %d: %s", bad, msg[check(bad, nullptr)]);
