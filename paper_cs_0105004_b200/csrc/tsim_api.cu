@@ -1453,7 +1453,7 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
   struct RouteUpload {
     std::thread th;
     cudaError_t err = cudaSuccess;
-    double secs = 0;
+    double secs = 0, setup_secs = 0;
     // the DMA starts once the placement's own uploads are done (they would
     // otherwise queue behind GBs of route data); the host copies into the
     // pinned buffers start at once
@@ -1485,6 +1485,7 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
                           cudaMallocHost(&pin[1], chunk) == cudaSuccess &&
                           cudaEventCreateWithFlags(&done[0], cudaEventDisableTiming) == cudaSuccess &&
                           cudaEventCreateWithFlags(&done[1], cudaEventDisableTiming) == cudaSuccess;
+      rup.setup_secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
       if (pinned) {  // fill one buffer while the other copies
         for (size_t o = 0, i = 0; o < nb && e == cudaSuccess; o += chunk, i++) {
           const size_t m = std::min(chunk, nb - o);
@@ -1589,6 +1590,7 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
       std::stable_sort(pend_list.begin() + pend_off[k], pend_list.begin() + pend_off[k + 1],
                        [&](int a, int b) { return h->dep[a] < h->dep[b] || (h->dep[a] == h->dep[b] && a < b); });
   }
+  trace("pending lists");
   // a fresh start builds the per-vehicle words on the device (below)
   const bool dev_veh = h->arr0.empty() && h->nv > 0 && getenv("TSIM_HOST_INIT") == nullptr;
   HostVec<int32_t> inj, arr;
@@ -1611,6 +1613,7 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
   for (int k = 0; k < h->nl; k++) vmax8[k] = (uint8_t)h->vmax[k];
   // device
   if ((rc = setup_node_lanes(h))) return rc;
+  trace("node lanes");
   if (h->ngroups > 0 && (rc = upload(h, &h->d_rows, h->rows))) return rc;  // node lanes resolved
   if ((rc = upload(h, &h->d_nli, h->nli))) return rc;
   if ((rc = upload(h, &h->d_nlo, h->nlo))) return rc;
@@ -1619,7 +1622,7 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
     CK(h, cudaMemcpyAsync(h->d_code[0], gcode.data(), gcode.size(), cudaMemcpyHostToDevice, h->stream));
     CK(h, cudaMemcpyAsync(h->d_vid[0], gvid.data(), gvid.size() * 4, cudaMemcpyHostToDevice, h->stream));
   }
-  trace("pending + uploads");
+  trace("uploads");
   {  // injection scratch of the row kernel: needed only if a row link has pending trips
     bool need = false;
     for (size_t ti = 0; ti < h->tiles.size() && !need; ti++)
@@ -1637,7 +1640,9 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
   {  // routes as out-slot sequences: the upload started above
     rup.th.join();
     trace("route upload joined");
-    if (trace.on) fprintf(stderr, "[tsim init]   (route upload took %.3f s)\n", rup.secs);
+    if (trace.on)
+      fprintf(stderr, "[tsim init]   (route upload took %.3f s, its pinned staging set up in %.3f s)\n",
+              rup.secs, rup.setup_secs);
     if (rup.err != cudaSuccess)
       return fail(h, TS_EINTERNAL, "route upload: %s", cudaGetErrorString(rup.err));
     cudaGetLastError();
