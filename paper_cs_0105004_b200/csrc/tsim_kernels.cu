@@ -465,9 +465,6 @@ __global__ void __launch_bounds__(256) k_hash(const StepParams P, unsigned long 
 // order; the winner is granted the entry space E and, if its velocity takes
 // it past the stop line, is written as the entrant of the target lane.
 // ====================================================================
-#ifndef TS_NODE_VPOS_EARLY
-#define TS_NODE_VPOS_EARLY 0
-#endif
 struct Cand {
   bool cand;
   int tgt, n2, d, v, vid;
@@ -501,12 +498,6 @@ __device__ __forceinline__ Cand node_candidate(const NodeParams &P, uint64_t rec
 // position record (16 bytes per vehicle) is read only for a crossing.
 __device__ __forceinline__ int node_grant(const NodeParams &P, const Cand &c, int vk, uint8_t head,
                                           uint32_t &crossings, bool pass = false) {
-#if TS_NODE_VPOS_EARLY
-  // the route position, loaded before the draw decides whether it crosses
-  // (its DRAM latency overlaps the Philox rounds)
-  VehPos q0{};
-  if (!pass) q0 = P.vpos[c.vid];
-#endif
   const int E = min(ctz32((uint32_t)head | 0x20u), min(kGmax, c.n2));
   if (E == 0) return 0;
   const int v3 = nasch_v3(c.v, vk, min(kGmax, c.d + E), (uint32_t)P.t, (uint32_t)c.vid, P.k0,
@@ -514,11 +505,7 @@ __device__ __forceinline__ int node_grant(const NodeParams &P, const Cand &c, in
   if (v3 > c.d) {
     int nslot = 0;  // pass-through node of a ring: straight on, same route position
     if (!pass) {
-#if TS_NODE_VPOS_EARLY
-      const VehPos q = q0;
-#else
       const VehPos q = P.vpos[c.vid];
-#endif
       nslot = (q.p + 2 < q.e) ? (int)P.rslot[q.p + 2] : kSlotFinal;
       P.vpos[c.vid].p = q.p + 1;
     }
@@ -548,12 +535,9 @@ __device__ __forceinline__ void node_flush(const NodeParams &P, uint32_t crossin
 // one thread per incoming lane; the lanes of a node are consecutive threads
 // in priority order, so the winner of a target lane is the lowest eligible
 // thread with that target.  Every warp resolves kNodeILP chunks at once
-// stage by stage (records, out-slot table, target heads, grant), so their
+// stage by stage (records, out-slot table and target heads, grant), so their
 // dependent loads overlap instead of running as one latency chain per
 // chunk.
-#ifndef TS_NODE_HEAD_EARLY
-#define TS_NODE_HEAD_EARLY 1  // measured: window -0.3 %, steady -0.5 % per step
-#endif
 #ifndef TS_NODE_ILP
 #define TS_NODE_ILP 1  // measured on 4a: 1 -> 31.5 us, 2 -> 35, 4 -> 39.6, 8 -> 49.6
 #endif
@@ -600,11 +584,10 @@ __global__ void __launch_bounds__(256) k_node_warp(const NodeParams P_, const No
         (__ballot_sync(FULL, a && e[k].major && (((uint32_t)(rec[k] >> 44)) & gmask)) & nodemask) != 0u;
     cd[k] = Cand{false, -1, 0, 0, 0, 0, -1};
     if (a) cd[k] = node_candidate(P, rec[k], e[k].lane, e[k].out_base, e[k].tt, e[k].vk);
-#if TS_NODE_HEAD_EARLY
     // every candidate's target head, loaded before the winner is known (one
-    // dependent load less on the chain; losers' loads are wasted)
+    // dependent load less on the chain; losers' loads are wasted; measured
+    // -0.3 % window / -0.5 % steady per step)
     head[k] = cd[k].cand ? P.head_occ[cd[k].tgt] : (uint8_t)0;
-#endif
     // signalized node (R23): red approaches have the virtual blocker, green
     // ones need no gap acceptance; otherwise priority + gap acceptance (R9)
     const bool eligible =
@@ -612,11 +595,6 @@ __global__ void __launch_bounds__(256) k_node_warp(const NodeParams P_, const No
     const uint32_t grp = __match_any_sync(FULL, eligible ? cd[k].tgt : -1 - lane);
     win[k] = eligible && (__ffs(grp) - 1) == lane;
   }
-#if !TS_NODE_HEAD_EARLY
-#pragma unroll
-  for (int k = 0; k < kNodeILP; k++)  // stage 3: target heads
-    head[k] = win[k] ? P.head_occ[cd[k].tgt] : (uint8_t)0;
-#endif
 #pragma unroll
   for (int k = 0; k < kNodeILP; k++) {  // stage 4: grants
     int ext = 0;

@@ -485,15 +485,6 @@ static __device__ __noinline__ void vid_lists_global(const int32_t *ibase, int32
             ent_e, changed, ginj, dir, lane, inj_scratch);
 }
 
-#ifndef TS_ROWS_LATE_BWAIT
-#define TS_ROWS_LATE_BWAIT 0  // wait for the previous output block's bulk store where s_out is reused
-#endif
-#ifndef TS_ROWS_LATE_GRAB
-#define TS_ROWS_LATE_GRAB 0  // next-group ticket broadcast just before its first use
-#endif
-#ifndef TS_ROWS_MLIST1
-#define TS_ROWS_MLIST1 0  // mover list: one loop over all words of the row
-#endif
 #ifndef TS_ROWS_DRAW2
 #define TS_ROWS_DRAW2 1  // two Philox chains per lane in the draw loop
 #endif
@@ -535,12 +526,11 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
   // every warp's first group is its warp index (no atomic at the start,
   // where all warps would queue on the one counter); later groups come from
   // the counter, offset by the warp count
-  auto grab_raw = [&]() {  // lane 0's ticket; broadcast where it is first needed
+  auto grab = [&]() {
     int g = 0;
     if (lane == 0) g = (int)(atomicAdd(R.gctr, 1ull) - R.gbase) + (TS_ROWS_FIRST_STATIC ? nwarps : 0);
-    return g;
+    return __shfl_sync(FULL, g, 0);
   };
-  auto grab = [&]() { return __shfl_sync(FULL, grab_raw(), 0); };
   uint32_t *s_pl = reinterpret_cast<uint32_t *>(s_out + R.cap + kRowsAuxWords);  // PPF buffer
   uint64_t *bar = &vbar[threadIdx.x >> 5], *pbar = &pvbar[threadIdx.x >> 5];
   uint32_t bar_phase = 0, pbar_phase = 0;
@@ -573,12 +563,8 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
   for (;;) {
     const int g = g_next;
     if (g >= R.ngroups) break;
-#if TS_ROWS_LATE_GRAB && !TS_ROWS_PPF
-    const int g_raw = grab_raw();  // the atomic's latency hides behind this group's move
-#else
     g_next = grab();
-#endif
-    if (!TS_ROWS_LATE_BWAIT && lane == 0) bulk_wait_read();  // the previous group's output block
+    if (lane == 0) bulk_wait_read();  // the previous group's output block
     uint32_t O[NW], V0[NW], V1[NW], V2[NW], A0[NW], A1[NW];
     if (!TS_ROWS_PPF) {  // the planes first: they depend on nothing
       const uint32_t *pin = R.planes_in + group_plane_base(g) + lane;
@@ -716,10 +702,6 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
         const int mc = popc_row(U1);
         const int moff = warp_scan(mc, lane, &mtot);
         // mover list entries: block offset << 12 | row slot << 7 | cell
-        if (TS_ROWS_LATE_BWAIT) {  // the previous group's output block has been read out
-          if (lane == 0) bulk_wait_read();
-          __syncwarp();
-        }
         int32_t *mlist = s_out;  // free until the output phase
         uint32_t *bw = reinterpret_cast<uint32_t *>(s_out + R.cap);
 #pragma unroll
@@ -728,28 +710,6 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
         const uint32_t p32m1 = (uint32_t)(P.p32 - 1);
         if (staged) {  // mtot <= tot_in <= cap: the whole list fits
           int j = moff, rb = in_off;
-#if TS_ROWS_MLIST1
-          // one loop over the row's movers across its words (the warp
-          // iterates max-over-rows of the row's movers, not the sum over
-          // words of the per-word maxima)
-          {
-            int i = 0;
-            uint32_t m = U1[0], o = O[0];
-            int b = (rb << 12) | (lane << 7);
-            for (;;) {
-              while (m == 0u && i < NW - 1) {
-                b += (__popc(o) << 12) + 32;
-                i++;
-                m = i == 1 ? U1[1] : i == 2 ? U1[2] : U1[NW - 1];
-                o = i == 1 ? O[1] : i == 2 ? O[2] : O[NW - 1];
-              }
-              if (m == 0u) break;
-              const uint32_t lsb = m & (0u - m), below = lsb - 1u;
-              m ^= lsb;
-              mlist[j++] = b + (__popc(o & below) << 12) + __popc(below);
-            }
-          }
-#else
 #pragma unroll
           for (int i = 0; i < NW; i++) {
             uint32_t m = U1[i];
@@ -762,7 +722,6 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
             }
             rb += __popc(o);
           }
-#endif
           __syncwarp();
           // the draws: the vid from the staged block; brake bit by a shared-
           // memory reduction at word (row slot * NW + word) = (entry >> 5) & 127
@@ -890,9 +849,6 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
         OA1[i] = A1[i];
       }
     }
-#if TS_ROWS_LATE_GRAB && !TS_ROWS_PPF
-    g_next = __shfl_sync(FULL, g_raw, 0);
-#endif
     if (g_next < R.ngroups) {  // the next group's block offset and count (see above)
       voff_n = R.gvoff[g_next];
       tot_n = R.gcnt_in[g_next];
@@ -1057,10 +1013,6 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
     int tot_out;
     const int out_off = warp_scan(nfin, lane, &tot_out);
     const bool ostaged = tot_out <= R.cap;
-    if (TS_ROWS_LATE_BWAIT) {  // (no-op when the draws waited already)
-      if (lane == 0) bulk_wait_read();
-      __syncwarp();
-    }
     int32_t *obase = ostaged ? s_out : R.vid_out + voff;
     int32_t *vout = obase + out_off;
     const bool moved_lc = any_row(LV) || any_row(AR);
