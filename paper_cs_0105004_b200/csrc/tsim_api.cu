@@ -2286,13 +2286,22 @@ int ts_exchange_local(ts_sim **hs, int32_t k) {
   return exchange_local_enqueue(by_dom);
 }
 
-// direct exchange plans of in-process partitions on one device: per
-// partition (handle set), every (sender, its strip slot) -> (receiver,
-// mirror slot), in the receivers' segment order
+// direct exchange plans of in-process partitions: per partition (handle
+// set), every (sender, its strip slot) -> (receiver, mirror slot), grouped
+// by the receiver's device.  One kernel per receiving device pulls its
+// receivers' strips straight from the senders' strip buffers -- over
+// NVLink through peer pointers (UVA) when a sender is on another device --
+// ordered after every domain's last work and before its next by events.
+// TSIM_DIRECT_SPLIT=1 groups by receiving handle instead (one kernel per
+// domain: the multi-device structure exercised on one device, tests).
 struct DirectPlan {
+  struct Sub {
+    ts_sim *rep;  // a receiving handle on the group's device: stream, events, plan memory
+    int4 *d_plan = nullptr;
+    int64_t n = 0;
+  };
   std::vector<ts_sim *> ds;
-  int4 *d_plan = nullptr;
-  int64_t n = 0;
+  std::vector<Sub> subs;
 };
 static std::vector<DirectPlan> g_direct_plans;
 
@@ -2300,11 +2309,30 @@ static const DirectPlan *direct_plan(const std::vector<ts_sim *> &ds) {
   for (const DirectPlan &p : g_direct_plans)
     if (p.ds == ds) return &p;
   if ((int)ds.size() > kDirectMax) return nullptr;
-  for (ts_sim *h : ds)
-    if (h->dev != ds[0]->dev) return nullptr;
-  std::vector<int4> plan;
+  const bool split = getenv("TSIM_DIRECT_SPLIT") != nullptr;
+  // peer access from every receiving device to every sending device
+  for (ts_sim *b : ds)
+    for (const ts_sim::Nbr &nb : b->nbrs) {
+      ts_sim *a = ds[nb.dom];
+      if (a->dev == b->dev) continue;
+      int can = 0;
+      if (cudaDeviceCanAccessPeer(&can, b->dev, a->dev) != cudaSuccess || !can) return nullptr;
+      if (cudaSetDevice(b->dev) != cudaSuccess) return nullptr;
+      const cudaError_t e = cudaDeviceEnablePeerAccess(a->dev, 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) return nullptr;
+      cudaGetLastError();
+    }
+  DirectPlan p;
+  p.ds = ds;
+  std::vector<std::vector<int4>> plans;
   for (size_t bi = 0; bi < ds.size(); bi++) {
     ts_sim *b = ds[bi];
+    size_t g = 0;  // the receiver's group
+    while (g < p.subs.size() && (split ? p.subs[g].rep != b : p.subs[g].rep->dev != b->dev)) g++;
+    if (g == p.subs.size()) {
+      p.subs.push_back(DirectPlan::Sub{b});
+      plans.emplace_back();
+    }
     for (const ts_sim::Nbr &nb : b->nbrs) {
       ts_sim *a = ds[nb.dom];
       const ts_sim::Nbr *back = nullptr;
@@ -2312,15 +2340,16 @@ static const DirectPlan *direct_plan(const std::vector<ts_sim *> &ds) {
         if (x.dom == b->dom_me) back = &x;
       if (!back || back->send_slot.size() != nb.recv_slot.size()) return nullptr;
       for (size_t j = 0; j < nb.recv_slot.size(); j++)
-        plan.push_back(int4{nb.dom, back->send_slot[j], (int)bi, nb.recv_slot[j]});
+        plans[g].push_back(int4{nb.dom, back->send_slot[j], (int)bi, nb.recv_slot[j]});
     }
   }
-  DirectPlan p;
-  p.ds = ds;
-  p.n = (int64_t)plan.size();
-  if (!plan.empty()) {
-    // owned by domain 0's handle (freed with it; the plan is dropped then)
-    if (upload(ds[0], &p.d_plan, plan)) return nullptr;
+  for (size_t g = 0; g < p.subs.size(); g++) {
+    DirectPlan::Sub &sb = p.subs[g];
+    sb.n = (int64_t)plans[g].size();
+    // owned by the group's handle (freed with it; the plan is dropped then)
+    if (!plans[g].empty() &&
+        (cudaSetDevice(sb.rep->dev) != cudaSuccess || upload(sb.rep, &sb.d_plan, plans[g])))
+      return nullptr;
   }
   g_direct_plans.push_back(p);
   return &g_direct_plans.back();
@@ -2336,25 +2365,31 @@ static void drop_direct_plans(const ts_sim *h) {
   }
 }
 
-// the exchange as one kernel on domain 0's stream, after every domain's
+// the exchange as one kernel per receiving device, after every domain's
 // last work and before its next (the strips of the handles' current buffers)
 static int exchange_direct_enqueue(const std::vector<ts_sim *> &ds, const DirectPlan &pl) {
-  ts_sim *h0 = ds[0];
   DirectParams P{};
   for (size_t i = 0; i < ds.size(); i++) {
     P.src[i] = ds[i]->d_strip[ds[i]->gcur];
     P.dst[i] = ds[i]->d_strip[ds[i]->gcur];
-    if (ds[i] != h0) {
-      CK(h0, cudaEventRecord(ds[i]->ev_packed, ds[i]->stream));
-      CK(h0, cudaStreamWaitEvent(h0->stream, ds[i]->ev_packed, 0));
-    }
+    CK(ds[i], cudaSetDevice(ds[i]->dev));
+    CK(ds[i], cudaEventRecord(ds[i]->ev_packed, ds[i]->stream));
   }
-  P.plan = pl.d_plan;
-  P.n = pl.n;
-  launch_strip_direct(P, h0->stream);
-  CK(h0, cudaEventRecord(h0->ev_copied, h0->stream));
-  for (ts_sim *h : ds)
-    if (h != h0) CK(h0, cudaStreamWaitEvent(h->stream, h0->ev_copied, 0));
+  for (const DirectPlan::Sub &sb : pl.subs) {
+    ts_sim *r = sb.rep;
+    CK(r, cudaSetDevice(r->dev));
+    for (ts_sim *h : ds)
+      if (h != r) CK(r, cudaStreamWaitEvent(r->stream, h->ev_packed, 0));
+    P.plan = sb.d_plan;
+    P.n = sb.n;
+    launch_strip_direct(P, r->stream);
+    CK(r, cudaEventRecord(r->ev_copied, r->stream));
+  }
+  for (ts_sim *h : ds) {
+    CK(h, cudaSetDevice(h->dev));
+    for (const DirectPlan::Sub &sb : pl.subs)
+      if (sb.rep != h) CK(h, cudaStreamWaitEvent(h->stream, sb.rep->ev_copied, 0));
+  }
   return TS_OK;
 }
 
@@ -2491,8 +2526,10 @@ int ts_local_step(ts_sim **hs, int32_t k, int32_t n_steps) {
   std::vector<ts_sim *> ds;
   if (int rc = by_domain(hs, k, ds)) return rc;
   if (n_steps < 0) return fail(ds[0], TS_EINVAL, "negative step count");
-  // one device: the strips go straight from the senders' to the receivers'
-  // strip buffers, one kernel per exchange (else device / peer copies)
+  // the strips go straight from the senders' to the receivers' strip
+  // buffers, one kernel per receiving device and exchange (peer pointers
+  // across devices; TSIM_LOCAL_COPIES=1 or no peer access: device / peer
+  // copies)
   const DirectPlan *dp = getenv("TSIM_LOCAL_COPIES") ? nullptr : direct_plan(ds);
   struct DirectGuard {
     std::vector<ts_sim *> &ds;

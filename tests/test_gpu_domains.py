@@ -220,14 +220,21 @@ def test_load_statistics_links_and_nodes():
     assert np.array_equal(sum(p[1] for p in parts), nw)
 
 
-@pytest.mark.parametrize("graph", [False, True])
-def test_local_step_in_library(graph):
+@pytest.mark.parametrize("graph,split", [(False, False), (True, False), (False, True), (True, True)])
+def test_local_step_in_library(graph, split, monkeypatch):
     """ts_local_step: whole steps of all k domains enqueued by the library
     (both exchanges per step), and with FLAG_GRAPH replayed from one CUDA
     graph holding every domain's stream and the exchanges: per-step hash
     equal to the undivided oracle for 300 steps in chunks of 7, 15, 31, 45
     steps (graph blocks + remainders); the phase-by-phase driver gives the
-    same state"""
+    same state.  split: the direct strip delivery as one kernel per
+    receiving domain (TSIM_DIRECT_SPLIT, the structure of the multi-device
+    peer-pointer transport: one kernel per receiving device) instead of one
+    per exchange"""
+    if split:
+        monkeypatch.setenv("TSIM_DIRECT_SPLIT", "1")
+    else:
+        monkeypatch.delenv("TSIM_DIRECT_SPLIT", raising=False)
     s = scenarios.portland(n_nodes=600, n_edges=800, n_veh=8000, side_km=8.0, n_zones=64, seed=2)
     s.depart = (s.depart // 12).astype(np.int32)
     s = scenarios.with_signals(s, green0=20, green1=25, seed=4)
