@@ -26,9 +26,10 @@ def assert_same_state(o, g, msg=""):
                                f"oracle {vo[key][bad[:5]]} gpu {vg[key][bad[:5]]}")
 
 
-def run_parity(scn, steps, flags, full_every=1, t0=0, tile_cells=0, hash_every=1):
+def run_parity(scn, steps, flags, full_every=1, t0=0, tile_cells=0, hash_every=1, group_cells=0):
     o = oracle.Oracle.from_scenario(scn, t0=t0)
-    g = tsim.Sim.from_scenario(scn, t0=t0, flags=flags, tile_cells=tile_cells)
+    g = tsim.Sim.from_scenario(scn, t0=t0, flags=flags, tile_cells=tile_cells,
+                               group_cells=group_cells)
     assert g.state_hash() == o.state_hash()
     assert_same_state(o, g, "init")
     done = 0
@@ -140,6 +141,29 @@ def test_bench_flags_full_state(net, chunk):
         s.depart = (s.depart // 12).astype(np.int32)
         steps = 300
     run_parity(s, steps, BENCH, full_every=chunk, hash_every=chunk)
+
+
+@pytest.mark.parametrize("net,group_cells", [("grid6", 64), ("grid24dense", 64), ("grid24dense", 512),
+                                             ("portland", 96)])
+def test_unstaged_groups(net, group_cells):
+    """the row kernel's paths for a 32-row group whose vehicles exceed its
+    shared-memory staging (vid blocks read and written in HBM, draws and
+    vid lists out of line): a small staging capacity (group_cells) sends
+    most or some groups there; injections, lane changes and node traffic
+    included; bench flags and hashed fused flags, full state checked"""
+    if net == "grid6":
+        s = scenarios.grid_trips(rows=6, cols=6, n_veh=3000, depart_max=300, seed=8, name="grid6u")
+        steps = 200
+    elif net == "grid24dense":
+        s = scenarios.big_grid(rows=24, cols=24, seed=3, name="grid24dense_u")
+        steps = 60
+    else:
+        s = scenarios.portland(n_nodes=600, n_edges=800, n_veh=8000, side_km=8.0, n_zones=64,
+                               seed=2)
+        s.depart = (s.depart // 12).astype(np.int32)
+        steps = 200
+    run_parity(s, steps, BENCH, full_every=20, hash_every=20, group_cells=group_cells)
+    run_parity(s, steps // 2, FUSED, full_every=10, hash_every=10, group_cells=group_cells)
 
 
 def test_big_grid_dense():
