@@ -329,6 +329,17 @@ def test_empty_networks():
     assert g.state_hash() == 0
 
 
+@pytest.mark.parametrize("cells", [128, 129])
+def test_row_width_limit(cells):
+    """links of exactly 128 cells (row tiles with all four 32-cell words
+    full: the last cell is bit 31 of word 3) and of 129 (one cell too many
+    for a row: general tiles), dense, 4 lanes, bench and hashed flags"""
+    s = scenarios.big_grid(rows=8, cols=8, lanes=4, cells=cells, density=0.25, seed=11,
+                           name=f"grid8w{cells}")
+    run_parity(s, 120, BENCH, full_every=20, hash_every=20)
+    run_parity(s, 60, FUSED, full_every=20, hash_every=20)
+
+
 def test_eight_lane_links_and_minimum_ring():
     """the widest links (8 lanes, kMaxLanes) on a dense grid, and the
     smallest ring (10 cells, one segment that is its own neighbour)"""
