@@ -1689,11 +1689,13 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
     if ((rc = upload(h, &h->d_pend_head, head))) return rc;
   }
   if ((rc = dalloc(h, &h->d_tail, h->n_nli, 0))) return rc;
-  if ((rc = dalloc(h, &h->d_entr, h->n_nlo, 0))) return rc;
+  // entrant records start (and are reset to) all ones: vid 0xFFFFFFFF is
+  // no vehicle, so a record never matches before it is written
+  if ((rc = dalloc(h, &h->d_entr, h->n_nlo, 0xFF))) return rc;
   if ((rc = dalloc(h, &h->d_head, h->n_nlo, 0))) return rc;
   if ((rc = dalloc(h, &h->d_ext, h->n_nli, 0))) return rc;
   if ((rc = dalloc(h, &h->d_ext_row, (size_t)h->ngroups * 32 + 1, 0))) return rc;
-  if ((rc = dalloc(h, &h->d_entr_row, (size_t)h->ngroups * 32 + 1, 0))) return rc;
+  if ((rc = dalloc(h, &h->d_entr_row, (size_t)h->ngroups * 32 + 1, 0xFF))) return rc;
   if ((rc = dalloc(h, &h->d_stats, (size_t)kHist * ST_N, 0))) return rc;
   if ((rc = dalloc(h, &h->d_work, h->nl, 0))) return rc;
   if ((rc = dalloc(h, &h->d_node_work, h->nn, 0))) return rc;

@@ -99,6 +99,9 @@ __host__ __device__ inline int64_t tile_cells_padded(int w, int L) {
 #define TS_ROWS_TPB 128  // k_rows threads per block (one warp per group)
 #endif
 constexpr int kSlotShift = 27;
+// entrant record (node kernel -> move kernels): vid | code << 32 | y << 40 |
+// ((t + 1) mod 2^21) << 43; all ones = none (reset when consumed)
+constexpr uint32_t kNoEntrant = 0xFFFFFFFFu;
 constexpr uint32_t kVidMask = (1u << kSlotShift) - 1u;
 constexpr int kRowWords = 4;
 constexpr int kRowMaxCells = 32 * kRowWords;
@@ -238,11 +241,11 @@ struct StepParams {
   uint64_t *tail_rec;  // per node-lane index, written with S1
   uint8_t *head_occ;   // per node-out-lane index, written with S1
   const uint8_t *ext;  // per node-lane index, from k_node
-  const uint64_t *entr;  // per node-out-lane index
+  uint64_t *entr;  // per node-out-lane index (cleared when consumed)
   // the same two node outputs for the row-kernel lanes by ROW SLOT, so the
   // row kernel loads them contiguously without its row descriptors first
   const uint8_t *ext_row;
-  const uint64_t *entr_row;
+  uint64_t *entr_row;  // (cleared when consumed)
   // outputs
   unsigned long long *stats;  // [kHist][ST_N]
   unsigned long long *link_work;

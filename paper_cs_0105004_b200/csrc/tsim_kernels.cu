@@ -378,8 +378,10 @@ __global__ void __launch_bounds__(256) k_step(const StepParams P_) {
       }
       // entrants granted by the node kernel (H3/H5): at most one per lane
       if ((T.d.flags & kFirst) && lane < T.L) {
-        uint64_t rec = P.entr[P.nlo[T.d.lane_gid + lane]];
-        if ((uint32_t)(rec >> 43) == ((uint32_t)(P.t + 1) & 0x1FFFFFu)) {
+        const int el = P.nlo[T.d.lane_gid + lane];
+        uint64_t rec = P.entr[el];
+        if ((uint32_t)(rec >> 43) == ((uint32_t)(P.t + 1) & 0x1FFFFFu) && (uint32_t)rec != kNoEntrant) {
+          P.entr[el] = ~0ull;  // consumed (reset): the 21-bit time tag would match again 2^21 steps on
           int vid = (int)(uint32_t)rec;
           uint8_t code = (uint8_t)(rec >> 32);
           int y = (int)((rec >> 40) & 7);

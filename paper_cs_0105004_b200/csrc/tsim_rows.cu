@@ -824,7 +824,7 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
       // ---- entrant granted by the node kernel (H3/H5), behind every vehicle
       if (w > 0) {
         const uint64_t rec = ent_rec;
-        if ((uint32_t)(rec >> 43) == ((uint32_t)(P.t + 1) & 0x1FFFFFu)) {
+        if ((uint32_t)(rec >> 43) == ((uint32_t)(P.t + 1) & 0x1FFFFFu) && (uint32_t)rec != kNoEntrant) {
           const int code = (int)((rec >> 32) & 0xFF);
           ent_y = (int)((rec >> 40) & 7);
           set_row(OO, ent_y);
@@ -836,6 +836,8 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
           if (cls & 2) set_row(OA1, ent_y);
           ent_e = (uint32_t)rec | ((uint32_t)(code >> 3) << kSlotShift);
           has_ent = true;
+          // consumed (reset): the 21-bit time tag would match again 2^21 steps on
+          P.entr_row[(size_t)g * 32 + lane] = ~0ull;
         }
       }
     } else {  // no move: initial injection / lane change only

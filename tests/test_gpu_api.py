@@ -97,3 +97,21 @@ def test_device_init_equals_host_init(which, monkeypatch):
         for k in x:
             assert np.array_equal(x[k], y[k]), k
     assert a[1] == b[1] and a[3] == b[3]
+
+
+def test_entrant_record_time_wrap():
+    """The node kernel's entrant record carries the crossing time in 21 bits
+    ((t + 1) mod 2^21).  A target lane whose last entrant crossed at step T
+    and that sees none afterwards must not get it again at T + 2^21: config 1
+    (every vehicle arrived after ~600 steps) is run past 2^21 + 800 steps
+    with graph replay and must stay empty with every vehicle arrived"""
+    s = scenarios.config("1")
+    sim = tsim.Sim.from_scenario(s, flags=tsim.FLAG_FUSED | tsim.FLAG_GRAPH)
+    sim.step(800)
+    tot = sim.totals()
+    assert tot["arrived"] == s.n_vehicles and tot["active"] == 0
+    sim.step((1 << 21) + 800)
+    tot = sim.totals()
+    assert tot["active"] == 0 and tot["arrived"] == s.n_vehicles, tot
+    st = sim.vehicles()
+    assert (st["status"] == tsim.ARRIVED).all()
