@@ -99,14 +99,17 @@ def test_device_init_equals_host_init(which, monkeypatch):
     assert a[1] == b[1] and a[3] == b[3]
 
 
-def test_entrant_record_time_wrap():
+@pytest.mark.parametrize("general", [False, True])
+def test_entrant_record_time_wrap(general):
     """The node kernel's entrant record carries the crossing time in 21 bits
     ((t + 1) mod 2^21).  A target lane whose last entrant crossed at step T
-    and that sees none afterwards must not get it again at T + 2^21: config 1
-    (every vehicle arrived after ~600 steps) is run past 2^21 + 800 steps
-    with graph replay and must stay empty with every vehicle arrived"""
+    and that sees none afterwards must not get it again at T + 2^21 (nor a
+    never-written record at t + 1 = 2^21): config 1 (every vehicle arrived
+    after ~600 steps) is run past 2^21 + 800 steps with graph replay, row
+    kernel or general tiles, and must stay empty with every vehicle arrived"""
     s = scenarios.config("1")
-    sim = tsim.Sim.from_scenario(s, flags=tsim.FLAG_FUSED | tsim.FLAG_GRAPH)
+    flags = tsim.FLAG_FUSED | tsim.FLAG_GRAPH | (tsim.FLAG_GENERAL if general else 0)
+    sim = tsim.Sim.from_scenario(s, flags=flags)
     sim.step(800)
     tot = sim.totals()
     assert tot["arrived"] == s.n_vehicles and tot["active"] == 0
