@@ -127,17 +127,12 @@ static_assert(sizeof(RowDesc) == 16, "RowDesc must be 16 bytes");
 // during the draws, the masks and list offsets of the rows the lane change
 // touched during the list rebuild
 constexpr int kRowsAuxWords = 4 * 32 * kRowWords + 5 * 32 + 4 + 64;
-#ifndef TS_ROWS_PPF
-#define TS_ROWS_PPF 0  // prefetch the next group's planes into shared memory
-#endif
-constexpr int kRowsPlaneWords = TS_ROWS_PPF ? kStatePlanes * kRowWords * 32 : 0;
 #ifndef TS_ROWS_FIRST_STATIC
 #define TS_ROWS_FIRST_STATIC 1  // k_rows: a warp's first group is its index (no atomic)
 #endif
-// per warp: vid block in, vid block out (cap entries each), the aux area,
-// the plane prefetch buffer (TS_ROWS_PPF)
+// per warp: vid block in, vid block out (cap entries each), the aux area
 __host__ __device__ inline int rows_stage_words(int cap) {
-  return 2 * cap + kRowsAuxWords + kRowsPlaneWords;  // cap % 4 == 0: 16-byte aligned
+  return 2 * cap + kRowsAuxWords;  // cap % 4 == 0: 16-byte aligned
 }
 
 // Warp-cooperative node kernel: the incoming lanes of every node, in the

@@ -473,6 +473,14 @@ struct Cand {
   int tgt_row;  // row slot of the target lane (row kernel), or -1
 };
 
+// the lane's front vehicle (last kGmax cells) is on its final link: the row
+// kernel reads the grant by row slot as the front's gap beyond the stop
+// line, which for a final link is the open end (R12), kGmax -- so the row
+// kernel needs no vid-list entry to take the front's gap
+__device__ __forceinline__ bool front_final(uint64_t rec) {
+  return ((rec >> 43) & 1) && (int)((rec >> 35) & 0x1F) == kSlotFinal;
+}
+
 // the front vehicle of an incoming lane: candidate to cross (d < min(v+1,
 // V)) unless it is on its final link; its target lane (R8)
 __device__ __forceinline__ Cand node_candidate(const NodeParams &P, uint64_t rec, int lane,
@@ -604,7 +612,7 @@ __global__ void __launch_bounds__(256) k_node_warp(const NodeParams P_, const No
     if (win[k]) ext = node_grant(P, cd[k], e[k].vk, head[k], crossings, (e[k].major & 2) != 0);
     if (act[k]) {
       P.ext[32 * (c0 + k) + lane] = (uint8_t)ext;
-      if (row[k] >= 0) P.ext_row[row[k]] = (uint8_t)ext;
+      if (row[k] >= 0) P.ext_row[row[k]] = (uint8_t)(front_final(rec[k]) ? kGmax : ext);
     }
     if (WORK) {  // load statistics: the node's lanes in range + its crossings
       const bool a = act[k] && e[k].lane_gid >= 0;
@@ -637,7 +645,8 @@ __global__ void __launch_bounds__(128) k_node(const NodeParams P_) {
       const int lg = P.link_lgid[j];
       for (int l = 0; l < P.link_lanes[j]; l++) {
         P.ext[lg + l] = 0;
-        if (P.lane_row[lg + l] >= 0) P.ext_row[P.lane_row[lg + l]] = 0;
+        if (P.lane_row[lg + l] >= 0)
+          P.ext_row[P.lane_row[lg + l]] = (uint8_t)(front_final(P.tail_rec[lg + l]) ? kGmax : 0);
         if (!(sg0 >> 31) && P.link_cls[j] == maxcls &&
             ((uint32_t)(P.tail_rec[lg + l] >> 44) & gmask))
           majorfree = false;

@@ -501,7 +501,6 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
   const StepParams P = with_time(P_);
   __shared__ unsigned long long red[(TS_ROWS_TPB / 32) * 8];
   __shared__ uint64_t vbar[TS_ROWS_TPB / 32];   // per warp: vid block arrival
-  __shared__ uint64_t pvbar[TS_ROWS_TPB / 32];  // per warp: prefetched planes arrival
   extern __shared__ __align__(16) int32_t stage[];  // per warp: vid block in, vid block out
   const int lane = threadIdx.x & 31;
   int32_t *s_in = stage + (threadIdx.x >> 5) * rows_stage_words(R.cap);
@@ -520,39 +519,26 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
   grid_dep_launch();      // the next node kernel may start its prologue
 
   // groups are handed out dynamically (one atomic per warp and group): no
-  // warp idles while another still has a queue of groups
-  // The next group is fetched one iteration ahead; with TS_ROWS_PPF its
-  // planes are copied into shared memory (cp.async) while this one runs.
-  // every warp's first group is its warp index (no atomic at the start,
+  // warp idles while another still has a queue of groups (a static
+  // round-robin assignment measured 6-11 % slower: the groups' work varies).
+  // Every warp's first group is its warp index (no atomic at the start,
   // where all warps would queue on the one counter); later groups come from
-  // the counter, offset by the warp count
+  // the counter, offset by the warp count; the next group is fetched one
+  // iteration ahead
   auto grab = [&]() {
     int g = 0;
     if (lane == 0) g = (int)(atomicAdd(R.gctr, 1ull) - R.gbase) + (TS_ROWS_FIRST_STATIC ? nwarps : 0);
     return __shfl_sync(FULL, g, 0);
   };
-  uint32_t *s_pl = reinterpret_cast<uint32_t *>(s_out + R.cap + kRowsAuxWords);  // PPF buffer
-  uint64_t *bar = &vbar[threadIdx.x >> 5], *pbar = &pvbar[threadIdx.x >> 5];
-  uint32_t bar_phase = 0, pbar_phase = 0;
-  if (lane == 0) {
-    mbar_init(bar);
-    if (TS_ROWS_PPF) mbar_init(pbar);
-  }
+  uint64_t *bar = &vbar[threadIdx.x >> 5];
+  uint32_t bar_phase = 0;
+  if (lane == 0) mbar_init(bar);
   __syncwarp();
-  auto issue_planes = [&](int gg) {  // TMA bulk copy of the group's 3 KB of planes
-    if (lane == 0) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      bulk_load(reinterpret_cast<int32_t *>(s_pl),
-                reinterpret_cast<const int32_t *>(R.planes_in + group_plane_base(gg)),
-                kStatePlanes * kRowWords * 32, pbar);
-    }
-  };
 #if TS_ROWS_FIRST_STATIC
   int g_next = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
 #else
   int g_next = grab();
 #endif
-  if (TS_ROWS_PPF && g_next < R.ngroups) issue_planes(g_next);
   // the next group's vid-block offset and vehicle count, loaded one
   // iteration ahead (the bulk copy of its block needs them first)
   int voff_n = 0, tot_n = 0;
@@ -560,38 +546,36 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
     voff_n = R.gvoff[g_next];
     tot_n = R.gcnt_in[g_next];
   }
+  // the next group's planes are loaded into registers once this group's
+  // input planes are dead (after the hop), so they are in flight while this
+  // group changes lanes and builds its vid lists (measured: k_rows -2.8 %
+  // in the driver's window, -4.3 % at steady state; a shared-memory prefetch
+  // buffer measured 3-4 % slower: it cost occupancy)
+  uint32_t nP[kStatePlanes][NW];
+  auto load_planes = [&](int gg) {
+    const uint32_t *pin = R.planes_in + group_plane_base(gg) + lane;
+#pragma unroll
+    for (int q = 0; q < kStatePlanes; q++)
+#pragma unroll
+      for (int i = 0; i < NW; i++) nP[q][i] = __ldcs(pin + (q * NW + i) * 32);
+  };
+  if (g_next < R.ngroups) load_planes(g_next);
   for (;;) {
     const int g = g_next;
     if (g >= R.ngroups) break;
     g_next = grab();
     if (lane == 0) bulk_wait_read();  // the previous group's output block
     uint32_t O[NW], V0[NW], V1[NW], V2[NW], A0[NW], A1[NW];
-    if (!TS_ROWS_PPF) {  // the planes first: they depend on nothing
-      const uint32_t *pin = R.planes_in + group_plane_base(g) + lane;
 #pragma unroll
-      for (int i = 0; i < NW; i++) {
-        O[i] = __ldcs(pin + (0 * NW + i) * 32);
-        V0[i] = __ldcs(pin + (1 * NW + i) * 32);
-        V1[i] = __ldcs(pin + (2 * NW + i) * 32);
-        V2[i] = __ldcs(pin + (3 * NW + i) * 32);
-        A0[i] = __ldcs(pin + (4 * NW + i) * 32);
-        A1[i] = __ldcs(pin + (5 * NW + i) * 32);
-      }
+    for (int i = 0; i < NW; i++) {
+      O[i] = nP[0][i];
+      V0[i] = nP[1][i];
+      V1[i] = nP[2][i];
+      V2[i] = nP[3][i];
+      A0[i] = nP[4][i];
+      A1[i] = nP[5][i];
     }
-    if (TS_ROWS_PPF) {  // this group's planes, prefetched during the previous one
-      mbar_wait(pbar, pbar_phase);
-      pbar_phase ^= 1u;
-#pragma unroll
-      for (int i = 0; i < NW; i++) {
-        O[i] = s_pl[(0 * NW + i) * 32 + lane];
-        V0[i] = s_pl[(1 * NW + i) * 32 + lane];
-        V1[i] = s_pl[(2 * NW + i) * 32 + lane];
-        V2[i] = s_pl[(3 * NW + i) * 32 + lane];
-        A0[i] = s_pl[(4 * NW + i) * 32 + lane];
-        A1[i] = s_pl[(5 * NW + i) * 32 + lane];
-      }
-    }
-    __syncwarp();  // the previous group's staged blocks (and the plane buffer) are free
+    __syncwarp();  // the previous group's staged blocks are free
     const RowDesc rd = R.rows[(size_t)g * 32 + lane];
     const int w = rd.w, l = rd.l, L = rd.L, link = rd.link, lg = rd.lg, vk = rd.vk;
     const int voff = voff_n;
@@ -604,8 +588,6 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       bulk_load(s_in, R.vid_in + voff, tot_in, bar);
     }
-    const bool pl_next = TS_ROWS_PPF && g_next < R.ngroups;
-    if (pl_next) issue_planes(g_next);  // committed after the vid block
     // per-row gathers of this step, issued early: node grant, entrant,
     // pending trips
     const bool do_move0 = do_move && w > 0;
@@ -626,11 +608,17 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
     const int nin = popc_row(O);
     int tot_chk;
     const int in_off = warp_scan(nin, lane, &tot_chk);
-    if (tma_in) {
-      mbar_wait(bar, bar_phase);
-      bar_phase ^= 1u;
-    }
-    __syncwarp();
+    auto vid_wait = [&]() {
+      if (tma_in) {
+        mbar_wait(bar, bar_phase);
+        bar_phase ^= 1u;
+      }
+      __syncwarp();
+    };
+    // a move launch waits for the block only before its draws (the front's
+    // gap comes from the grant, not from its list entry): the bulk copy
+    // overlaps the thermometer code and the mover list (-0.8 % / -1 %)
+    if (!do_move) vid_wait();
     const int32_t *vin = (staged ? (const int32_t *)s_in : R.vid_in + voff) + in_off;
     acc.work += nin;
     if ((P.mode & kModeWork) && P.link_work && nin)
@@ -647,7 +635,6 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
       const int xf = top_row(O);
       const int nb = min(w, kGmax);
       const bool front_zone = xf >= w - nb && xf >= 0;
-      if (front_zone) efront = (uint32_t)vin[nin - 1];
       // ---- thermometer codes U_k = (v2 >= k), word by word; cells past the
       //      row end count as occupied.  The row front near the stop line
       //      takes its gap from the node grant (H3) or the open end of its
@@ -658,8 +645,8 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
       int fd = 99, fv2 = 0;
       if (front_zone) {
         const int d = w - 1 - xf;
-        const int slot = (int)(efront >> kSlotShift);
-        const int gp = slot == kSlotFinal ? kGmax : min(kGmax, d + ext_lg);
+        // (the node kernel grants kGmax to a front on its final link, R12)
+        const int gp = min(kGmax, d + ext_lg);
         if (gp > d) {
           const int v = bit_row(V0, xf) | (bit_row(V1, xf) << 1) | (bit_row(V2, xf) << 2);
           fd = d;
@@ -722,7 +709,7 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
             }
             rb += __popc(o);
           }
-          __syncwarp();
+          vid_wait();  // the vid block has arrived (includes the warp barrier)
           // the draws: the vid from the staged block; brake bit by a shared-
           // memory reduction at word (row slot * NW + word) = (entry >> 5) & 127
           const uint32_t bw_s = (uint32_t)__cvta_generic_to_shared(bw);
@@ -757,6 +744,7 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
           }
           __syncwarp();
         } else {  // a group larger than the staging (rare): out of line
+          vid_wait();
           RowWords u1w, ow;
 #pragma unroll
           for (int i = 0; i < NW; i++) {
@@ -770,6 +758,7 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
         for (int i = 0; i < NW; i++) Bm[i] = bw[lane * NW + i];
         __syncwarp();
       }
+      if (front_zone) efront = (uint32_t)vin[nin - 1];  // for an exit (below)
       // ---- hop, word by word: D_k = vehicles moving exactly k (v3 = k);
       //      those passing the row end leave it (LR); O' = OR_k D_k << k with
       //      the velocity and class bits carried along
@@ -851,6 +840,7 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
         OA1[i] = A1[i];
       }
     }
+    if (g_next < R.ngroups) load_planes(g_next);  // this group's input planes are dead
     if (g_next < R.ngroups) {  // the next group's block offset and count (see above)
       voff_n = R.gvoff[g_next];
       tot_n = R.gcnt_in[g_next];
