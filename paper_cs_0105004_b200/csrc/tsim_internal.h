@@ -120,6 +120,8 @@ struct RowDesc {
   uint8_t vk;    // vmax of the link
 };
 static_assert(sizeof(RowDesc) == 16, "RowDesc must be 16 bytes");
+// k_rows reads w, l, L, vk as one little-endian word (bytes 12..15)
+static_assert(offsetof(RowDesc, w) == 12 && offsetof(RowDesc, vk) == 15, "RowDesc packed word");
 
 // shared memory of one k_rows warp (4-byte words): the group's vid block in
 // and out (cap entries each; the out area first serves as the list of the

@@ -560,6 +560,11 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
       for (int i = 0; i < NW; i++) nP[q][i] = __ldcs(pin + (q * NW + i) * 32);
   };
   if (g_next < R.ngroups) load_planes(g_next);
+  // the packed descriptor word (w, l, L, vk) of the next group is loaded
+  // with its planes (-1.7 % / -2.2 %; its node grants and entrants loaded
+  // there too measured +1.2 %)
+  uint32_t n_dw = 0u;
+  if (g_next < R.ngroups) n_dw = reinterpret_cast<const uint32_t *>(R.rows + (size_t)g_next * 32 + lane)[3];
   for (;;) {
     const int g = g_next;
     if (g >= R.ngroups) break;
@@ -577,7 +582,9 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
     }
     __syncwarp();  // the previous group's staged blocks are free
     const RowDesc rd = R.rows[(size_t)g * 32 + lane];
-    const int w = rd.w, l = rd.l, L = rd.L, link = rd.link, lg = rd.lg, vk = rd.vk;
+    const uint32_t dw = n_dw;  // RowDesc bytes 12..15: w, l, L, vk
+    const int w = (int)(dw & 0xFF), l = (int)((dw >> 8) & 0xFF), L = (int)((dw >> 16) & 0xFF),
+              link = rd.link, lg = rd.lg, vk = (int)(dw >> 24);
     const int voff = voff_n;
     // the group's vid block (its vehicle count was written with it) is
     // staged in shared memory when it fits, loaded together with the planes
@@ -840,7 +847,10 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
         OA1[i] = A1[i];
       }
     }
-    if (g_next < R.ngroups) load_planes(g_next);  // this group's input planes are dead
+    if (g_next < R.ngroups) {
+      load_planes(g_next);  // this group's input planes are dead
+      n_dw = reinterpret_cast<const uint32_t *>(R.rows + (size_t)g_next * 32 + lane)[3];
+    }
     if (g_next < R.ngroups) {  // the next group's block offset and count (see above)
       voff_n = R.gvoff[g_next];
       tot_n = R.gcnt_in[g_next];
