@@ -522,8 +522,11 @@ __device__ __forceinline__ int node_grant(const NodeParams &P, const Cand &c, in
     const int y2 = v3 - c.d - 1;
     const uint64_t rec = (uint64_t)(uint32_t)c.vid | ((uint64_t)(v3 | (nslot << 3)) << 32) |
                          ((uint64_t)y2 << 40) | ((uint64_t)((P.t + 1) & 0x1FFFFF) << 43);
-    P.entr[c.tgt] = rec;
+    // a row-kernel lane reads its entrant by row slot, a general tile by
+    // node-out-lane index: one record each (a scattered 8-byte store costs
+    // a partial-sector read-modify-write in DRAM)
     if (c.tgt_row >= 0) P.entr_row[c.tgt_row] = rec;
+    else P.entr[c.tgt] = rec;
     crossings += pass ? 0u : 1u;
   }
   return E;
