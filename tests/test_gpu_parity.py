@@ -108,8 +108,14 @@ def test_grid_segmented_links():
     run_parity(s, 400, UNFUSED, full_every=20, tile_cells=64)
 
 
-@pytest.mark.parametrize("flags", [FUSED, GENERAL])
+@pytest.mark.parametrize("flags", [FUSED, GENERAL, "node_general"])
 def test_portland_small(flags):
+    """Portland-shaped network (row and general tiles, trips departing and
+    arriving); "node_general": every node resolved by the thread-per-node
+    kernel k_node (its grants by row slot, including the open end R12 of a
+    front on its final link)"""
+    if flags == "node_general":
+        flags = NODE_GENERAL
     s = scenarios.portland(n_nodes=600, n_edges=800, n_veh=8000, side_km=8.0, n_zones=64,
                            seed=2)
     # departures compressed into the first 300 s
