@@ -1654,17 +1654,21 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
     }
     if ((rc = upload(h, &h->d_nodeout, h->ring_rows ? h->ring_nodeout : nodeout))) return rc;
   }
+  trace("  node outs");
   if (dev_veh) {  // 12 bytes per vehicle cross PCIe instead of 24
     if (!h->d_roff && (rc = upload(h, &h->d_roff, h->roff))) return rc;
+    trace("  route offsets up");
     if ((rc = dalloc(h, &h->d_vpos, h->nv))) return rc;
     if ((rc = dalloc(h, &h->d_inj, h->nv))) return rc;
     if ((rc = dalloc(h, &h->d_arr, h->nv))) return rc;
+    trace("  vehicle arrays allocated");
     int32_t *d_cur = nullptr;
     uint8_t *d_placed = nullptr;
     CK(h, cudaMallocAsync(&d_cur, (size_t)h->nv * 4, h->stream));
     CK(h, cudaMallocAsync(&d_placed, (size_t)h->nv, h->stream));
     CK(h, cudaMemcpyAsync(d_cur, cur0.data(), (size_t)h->nv * 4, cudaMemcpyHostToDevice, h->stream));
     CK(h, cudaMemcpyAsync(d_placed, h->placed.data(), (size_t)h->nv, cudaMemcpyHostToDevice, h->stream));
+    trace("  cursors up");
     k_init_vehicles<<<(h->nv + 255) / 256, 256, 0, h->stream>>>(h->nv, h->d_roff, d_cur, d_placed,
                                                                 h->d_vpos, h->d_inj, h->d_arr);
     CK(h, cudaGetLastError());
