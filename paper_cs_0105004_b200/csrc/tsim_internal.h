@@ -240,7 +240,10 @@ struct StepParams {
   const uint8_t *ext;  // per node-lane index, from k_node
   uint64_t *entr;  // per node-out-lane index (cleared when consumed)
   // the same two node outputs for the row-kernel lanes by ROW SLOT, so the
-  // row kernel loads them contiguously without its row descriptors first
+  // row kernel loads them contiguously without its row descriptors first;
+  // ext_row is kGmax for a lane whose front vehicle is on its final link
+  // (the open end, R12), and a crossing's entrant record of a row-kernel
+  // lane is written here only (entr holds those of general-tile lanes)
   const uint8_t *ext_row;
   uint64_t *entr_row;  // (cleared when consumed)
   // outputs
@@ -269,8 +272,8 @@ struct NodeParams {
   const uint8_t *head_occ;
   uint8_t *ext;              // by node-lane index (k_node: identity)
   uint64_t *entr;
-  uint8_t *ext_row;          // by row slot (row-kernel lanes): the grant again
-  uint64_t *entr_row;        // by row slot: the entrant record again
+  uint8_t *ext_row;          // by row slot (row-kernel lanes): the grant again (kGmax: final link)
+  uint64_t *entr_row;        // by row slot: the entrant record of a row-kernel lane
   const int32_t *lane_row;   // row slot of every global lane id, or -1 (k_node)
   unsigned long long *stats;
   // per-node work counters (load statistics), by node id;
