@@ -132,9 +132,25 @@ def ncu_traffic():
         with open(p) as f:
             t = json.load(f)
         return {"bytes": t["traffic_bytes_per_launch"],
+                "inst": t.get("warp_instructions_per_launch"),
                 "source": f"ncu --set full, {t['report']}: {t['note']}"}
     except (OSError, KeyError, ValueError):
-        return {"bytes": None, "source": None}
+        return {"bytes": None, "inst": None, "source": None}
+
+
+def issue_roof(inst, kernel_ms, sm_mhz):
+    """the kernel's secondary roof, instruction issue: the
+    warp instructions of one launch (committed ncu capture) over the live
+    CUDA-event duration, against 148 SMs x 4 schedulers x 1 warp
+    instruction per cycle at the sampled SM clock"""
+    if not inst or not kernel_ms:
+        return None
+    mhz = sm_mhz or 1965.0
+    peak = 148 * 4 * mhz * 1e6
+    achieved = inst / (kernel_ms / 1e3)
+    return {"achieved": achieved, "peak": peak, "unit": "warp-instructions/s",
+            "frac": achieved / peak, "warp_instructions_per_launch": inst,
+            "note": "instruction count from the ncu capture (traffic_source), time and clock live"}
 
 
 def workload(name):
@@ -290,6 +306,7 @@ def bench_tsim(args):
         "gpu_launches": 1 + 2 * args.steps,
         "gen_s": t_gen,
     }
+    out["roofline"]["issue"] = issue_roof(traffic.get("inst"), mv_ms, out["clocks"].get("sm_mhz"))
     sim.close()
     if args.cpu_baseline and rank == 0:
         import multiprocessing

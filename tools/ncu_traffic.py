@@ -1,5 +1,6 @@
-"""DRAM traffic of the dominant kernel from an ncu --set full report ->
-profiles/traffic_k_rows.json (read by bench.py for roofline.traffic):
+"""DRAM traffic (and warp instructions) of the dominant kernel from an ncu
+--set full report -> profiles/traffic_k_rows.json (read by bench.py for
+roofline.traffic and roofline.issue):
   python tools/ncu_traffic.py REPORT [KERNEL_SUBSTR] [NOTE]"""
 import csv
 import json
@@ -30,6 +31,8 @@ for r in rows[2:]:
     res = {'kernel': r[h.index('Kernel Name')], 'dram_read_bytes': rd, 'dram_write_bytes': wr,
            'traffic_bytes_per_launch': rd + wr,
            'duration_s_under_ncu': val(r, 'gpu__time_duration.sum'),
+           'warp_instructions_per_launch': val(r, 'smsp__inst_executed.sum'),
+           'issue_active_pct_under_ncu': val(r, 'smsp__issue_active.avg.pct_of_peak_sustained_active'),
            'report': os.path.basename(rep), 'note': note}
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     with open(os.path.join(root, 'profiles', 'traffic_k_rows.json'), 'w') as f:
