@@ -306,7 +306,10 @@ def bench_tsim(args):
         "gpu_launches": 1 + 2 * args.steps,
         "gen_s": t_gen,
     }
-    out["roofline"]["issue"] = issue_roof(traffic.get("inst"), mv_ms, out["clocks"].get("sm_mhz"))
+    # (the captured launch is from the driver's window: its instruction count
+    # holds for that run only -- the steady state executes ~30 % fewer)
+    out["roofline"]["issue"] = (issue_roof(traffic.get("inst"), mv_ms, out["clocks"].get("sm_mhz"))
+                                if (args.steps, args.warmup, args.config) == (20, 5, "4a") else None)
     sim.close()
     if args.cpu_baseline and rank == 0:
         import multiprocessing
