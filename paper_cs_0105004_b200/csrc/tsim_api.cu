@@ -69,8 +69,9 @@ static NcclApi &nccl() {
 
 // one exchange: the packed strips to and from every neighbour domain, one
 // message each way per neighbour, on the handle's stream
-static int nccl_exchange(ts_sim *h) {
+static int nccl_exchange(ts_sim *h, cudaStream_t st = nullptr) {
   if (h->nbrs.empty()) return TS_OK;
+  if (!st) st = h->stream;
   NcclApi &a = nccl();
   NCK(h, a.groupStart());
   for (const ts_sim::Nbr &nb : h->nbrs) {
@@ -78,9 +79,9 @@ static int nccl_exchange(ts_sim *h) {
     // strip per lane of every shared split link, both sides in link order;
     // checked in build_tiles)
     NCK(h, a.send(h->d_send + nb.off, nb.send_slot.size() * sizeof(Strip), ncclUint8, nb.dom,
-                  h->comm, h->stream));
+                  h->comm, st));
     NCK(h, a.recv(h->d_recv + nb.off, nb.recv_slot.size() * sizeof(Strip), ncclUint8, nb.dom,
-                  h->comm, h->stream));
+                  h->comm, st));
   }
   NCK(h, a.groupEnd());
   return TS_OK;
@@ -145,6 +146,7 @@ int ts_create(const ts_config *cfg, ts_sim **out) {
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_lc, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_packed, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_copied, cudaEventDisableTiming);
   if (e != cudaSuccess) {
@@ -179,6 +181,7 @@ void ts_destroy(ts_sim *h) {
   if (h->side) cudaStreamDestroy(h->side);
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
   if (h->ev_join) cudaEventDestroy(h->ev_join);
+  if (h->ev_lc) cudaEventDestroy(h->ev_lc);
   if (h->ev_packed) cudaEventDestroy(h->ev_packed);
   if (h->ev_copied) cudaEventDestroy(h->ev_copied);
   for (int i = 0; i < 2; i++) {
@@ -1730,6 +1733,7 @@ static int init_impl(ts_sim *h, int32_t t0, bool inject0) {
   // leave ~55 KB of shared memory per block; group_cells overrides (tuning)
   h->rows_cap = h->cfg.group_cells > 0 ? (h->cfg.group_cells + 3) & ~3 : 1344;
   h->pdl = getenv("TSIM_NO_PDL") == nullptr;
+  h->no_xoverlap = getenv("TSIM_NO_XOVERLAP") != nullptr;
   h->rows_threads = TS_ROWS_TPB;
   h->rows_smem = (h->rows_threads / 32) * rows_stage_words(h->rows_cap) * 4;
   CK(h, set_rows_smem(h->rows_smem));
@@ -1802,9 +1806,9 @@ static void pack_strips(ts_sim *h) {
   launch_strip_copy(h->d_strip[h->gcur], h->d_send_slot, h->d_send, nullptr, h->n_xs, h->stream);
 }
 // receive buffer -> mirror strips, read as halos by the next kernel
-static void unpack_strips(ts_sim *h) {
+static void unpack_strips(ts_sim *h, cudaStream_t st = nullptr) {
   if (h->direct) return;
-  launch_strip_copy(h->d_recv, nullptr, h->d_strip[h->gcur], h->d_recv_slot, h->n_xs, h->stream);
+  launch_strip_copy(h->d_recv, nullptr, h->d_strip[h->gcur], h->d_recv_slot, h->n_xs, st ? st : h->stream);
 }
 
 // Phase 0 of step t: lane change on S(t) (H1) of the
@@ -1827,10 +1831,14 @@ static void phase_lc(ts_sim *h) {
 // Phase 1: intersections (H3), velocity update + move (H4/H5), injection
 // (H6); with `more`, the lane change of step t+1 is fused into the move
 // kernels whose tiles need no exchange for it.  Pack exchange #2 (H7).
-static void phase_move(ts_sim *h, bool more, cudaEvent_t e0, cudaEvent_t e1) {
+// xside: exchange #1 and its unpack were enqueued on the side stream (native
+// multi-rank step): only the general tiles read the mirror strips, so the
+// node kernel and the row kernel run on the main stream meanwhile and the
+// general-tile kernel follows the unpack on the side stream
+static void phase_move(ts_sim *h, bool more, cudaEvent_t e0, cudaEvent_t e1, bool xside = false) {
   const int t = h->t;
   const int mode = base_mode(h);
-  if (h->n_xs > 0) unpack_strips(h);
+  if (h->n_xs > 0 && !xside) unpack_strips(h);
   if (h->node_warp)
     launch_node_warp(node_params(h, t),
                      NodeWarpParams{h->d_lane_sig, h->d_nlanes, h->nchunks, h->d_nl_node,
@@ -1960,14 +1968,23 @@ static int enqueue_steps(ts_sim *h, int32_t n) {
     }
     CK(h, cudaEventRecord(h->ev0, h->stream));
     int ne = 0;
+    // exchange #1 overlaps the node and row kernels when the domain has
+    // both kinds of tiles (the row tiles never read the strips)
+    const bool xov = h->side && h->ngroups > 0 && !h->gtiles.empty() && !h->no_xoverlap;
     for (int i = 0; i < n; i++) {
       const bool tm = h->timing && i % kTimingStride == 0;
       phase_lc(h);
-      if (tm) CK(h, cudaEventRecord(h->mv_ev[2 * ne], h->stream));
-      if (int rc = nccl_exchange(h)) return rc;
-      if (tm) CK(h, cudaEventRecord(h->mv_ev[2 * ne + 1], h->stream));
+      const cudaStream_t xs = xov ? h->side : h->stream;
+      if (xov) {
+        CK(h, cudaEventRecord(h->ev_lc, h->stream));
+        CK(h, cudaStreamWaitEvent(h->side, h->ev_lc, 0));
+      }
+      if (tm) CK(h, cudaEventRecord(h->mv_ev[2 * ne], xs));
+      if (int rc = nccl_exchange(h, xs)) return rc;
+      if (tm) CK(h, cudaEventRecord(h->mv_ev[2 * ne + 1], xs));
       ne += tm;
-      phase_move(h, i < n - 1, nullptr, nullptr);
+      if (xov) unpack_strips(h, h->side);
+      phase_move(h, i < n - 1, nullptr, nullptr, xov);
       if (tm) CK(h, cudaEventRecord(h->mv_ev[2 * ne], h->stream));
       if (int rc = nccl_exchange(h)) return rc;
       if (tm) CK(h, cudaEventRecord(h->mv_ev[2 * ne + 1], h->stream));

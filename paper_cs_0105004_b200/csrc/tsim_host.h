@@ -94,6 +94,7 @@ struct ts_sim {
   // (disjoint tiles, both after the node kernel); fork / join by events
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_lc = nullptr;  // native multi-rank step: exchange #1 may start (side stream)
   size_t dev_bytes = 0;
   std::vector<void *> allocs;
   // network (host)
@@ -250,6 +251,7 @@ struct ts_sim {
   // ts_local_step on one device: strips delivered by one direct kernel per
   // exchange (no pack / copy / unpack of this handle while set)
   bool direct = false;
+  bool no_xoverlap = false;  // TSIM_NO_XOVERLAP: exchange #1 in stream order (A/B, tests)
   // ts_exchange_local: reusable ordering events (after the pack, after the copies)
   cudaEvent_t ev_packed = nullptr, ev_copied = nullptr;
 };

@@ -100,8 +100,16 @@ def fake_nccl(tmp_path_factory):
      'steps=300)', 3, 300, 100),
     ('scenarios.config("1")', 2, 5000, 5000),  # one call longer than the statistics ring
 ])
-def test_native_step_with_partners(fake_nccl, scn, k, steps, chunk):
+@pytest.mark.parametrize("overlap", [True, False])
+def test_native_step_with_partners(fake_nccl, scn, k, steps, chunk, overlap):
+    """overlap: exchange #1 on the side stream beside the node and row
+    kernels (the default for domains with row and general tiles); False:
+    TSIM_NO_XOVERLAP, every phase in stream order"""
+    if not overlap and steps > 1000:
+        pytest.skip("the long run once")
     env = dict(os.environ, TSIM_NCCL_LIB=fake_nccl)
+    if not overlap:
+        env["TSIM_NO_XOVERLAP"] = "1"
     code = CHILD.format(root=ROOT, scn=scn, k=k, steps=steps, chunk=chunk)
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
                        timeout=900)
