@@ -392,18 +392,22 @@ __device__ __forceinline__ void vid_lists(const int32_t *ibase, int32_t *obase, 
   }
 }
 
-// The vid lists of a group whose blocks are staged, without injections,
-// when the lane-change rows have at most kCellTab vehicles: as vid_lists,
-// but every lane-change row first lists its vehicles' cells in a table
-// (entry row << 8 | cell, rows one after another), so an item finds its row
-// and cell with one load instead of a binary search and a bit select.
-constexpr int kCellTab = 576;  // uint16 entries in the aux area rOO / pOO / rIN leave free
+// The vid lists of a staged group without injections (the common case),
+// lane-change rows by (row, word) items: every lane-change row publishes its masks, prefix
+// counts and offsets; then the warp takes the items (row, word) 32 at a
+// time and each lane writes the vehicles of its word of S(t+1) (before the
+// lane change) to their ranks in the final occupancy -- of their own row,
+// or of l + dir for a leaver.  The per-row data is loaded once per item,
+// not per vehicle, and the words of one round carry similar numbers of
+// vehicles (unlike whole rows).  (It replaced a per-vehicle cell table +
+// warp scatter: k_rows -3.3 % in the driver's window, -1.1 % at steady
+// state.)
 template <int NWT>
-__device__ __forceinline__ void vid_lists_tab(const int32_t *ibase, int32_t *obase, int32_t *aux,
-                                              const uint32_t (&OO)[NWT], const uint32_t (&FO)[NWT],
-                                              const uint32_t (&LV)[NWT], int nfin, int in_off,
-                                              int out_off, bool has_ent, int ent_y, uint32_t ent_e,
-                                              bool changed, int ioff, int itot, int dir, int lane) {
+__device__ __forceinline__ void vid_lists_rw(const int32_t *ibase, int32_t *obase, int32_t *aux,
+                                             const uint32_t (&OO)[NWT], const uint32_t (&FO)[NWT],
+                                             const uint32_t (&LV)[NWT], int nfin, int in_off,
+                                             int out_off, bool has_ent, int ent_y, uint32_t ent_e,
+                                             bool changed, int dir, int lane) {
   constexpr int NW = NWT;
   const int32_t *vin = ibase + in_off;
   int32_t *vout = obase + out_off;
@@ -421,55 +425,65 @@ __device__ __forceinline__ void vid_lists_tab(const int32_t *ibase, int32_t *oba
     }
     for (; i < nfin; i++) vout[i] = vin[i - sh];
   }
-  if (itot == 0) return;  // warp-uniform
-  // aux layout: cell table (kCellTab uint16 = 288 words), rFO, rLV, the
-  // per-row scalars, mItem, pFO
-  uint16_t *ctab = reinterpret_cast<uint16_t *>(aux);
-  uint32_t *rFO = reinterpret_cast<uint32_t *>(aux) + kCellTab / 2, *rLV = rFO + 32 * NW;
-  int32_t *mInOff = reinterpret_cast<int32_t *>(rLV + 32 * NW), *mOutOff = mInOff + 32,
-          *mEnt = mOutOff + 32, *mItem = mEnt + 32;
-  uint32_t *pFO = reinterpret_cast<uint32_t *>(mItem + 32);
+  const uint32_t cm = __ballot_sync(FULL, changed);
+  if (cm == 0u) return;  // warp-uniform
+  // aux: rOO, rFO, rLV (32 x NW each), then per row: pOO, pFO (byte i =
+  // count of words before i), mIn (input index of its rank-0 vehicle: the
+  // entrant, if any, counts as rank 0 and is not in the input), mOut, mEnt,
+  // and the list of the lane-change rows
+  uint32_t *rOO = reinterpret_cast<uint32_t *>(aux), *rFO = rOO + 32 * NW, *rLV = rFO + 32 * NW;
+  uint32_t *pOO = rLV + 32 * NW, *pFO = pOO + 32;
+  int32_t *mIn = reinterpret_cast<int32_t *>(pFO + 32), *mOut = mIn + 32, *mEnt = mOut + 32,
+          *rlist = mEnt + 32;
   {
-    uint32_t pf = 0u;
-    int sf = 0;
+    uint32_t po = 0u, pf = 0u;
+    int so = 0, sf = 0;
 #pragma unroll
     for (int i = 0; i < NW; i++) {
       rFO[lane * NW + i] = FO[i];
-      rLV[lane * NW + i] = LV[i];
-      if (i > 0) pf |= (uint32_t)sf << (8 * i);
+      if (changed) {
+        rOO[lane * NW + i] = OO[i];
+        rLV[lane * NW + i] = LV[i];
+      }
+      if (i > 0) {
+        po |= (uint32_t)so << (8 * i);
+        pf |= (uint32_t)sf << (8 * i);
+      }
+      so += __popc(OO[i]);
       sf += __popc(FO[i]);
     }
+    pOO[lane] = po;
     pFO[lane] = pf;
   }
-  mInOff[lane] = in_off - (ent_y >= 0 ? 1 : 0);  // OO rank -> input index (entrant first)
-  mOutOff[lane] = out_off;
+  mIn[lane] = in_off - (ent_y >= 0 ? 1 : 0);
+  mOut[lane] = out_off;
   mEnt[lane] = ent_y >= 0 ? (int32_t)ent_e : -1;
-  mItem[lane] = ioff;
-  if (changed) {  // this row's vehicles (cells of OO, in order) into the table
-    int k = ioff;
-#pragma unroll
-    for (int i = 0; i < NW; i++) {
-      uint32_t m = OO[i];
-      while (m) {
-        const int x = __ffs(m) - 1;
-        m &= m - 1u;
-        ctab[k++] = (uint16_t)((lane << 8) | (32 * i + x));
-      }
-    }
-  }
+  if (changed) rlist[__popc(cm & ((1u << lane) - 1u))] = lane;
   __syncwarp();
-  for (int J = lane; J < itot; J += 32) {
-    const uint32_t it = ctab[J];
-    const int r0 = (int)(it >> 8), c = (int)(it & 0xFFu);
-    const int rr = J - mItem[r0];  // rank of the vehicle in the row's OO
-    // the entrant is the row's lowest vehicle (rank 0), then the input list
-    const uint32_t e = (rr == 0 && mEnt[r0] != -1) ? (uint32_t)mEnt[r0]
-                                                   : (uint32_t)ibase[mInOff[r0] + rr];
-    const int ci = c >> 5;
-    const uint32_t bit = 1u << (c & 31), lowb = bit - 1u;
-    const int dst = (rLV[r0 * NW + ci] & bit) ? r0 + dir : r0;
-    const int rank = __popc(rFO[dst * NW + ci] & lowb) + (int)((pFO[dst] >> (8 * ci)) & 0xFF);
-    obase[mOutOff[dst] + rank] = (int32_t)e;
+  const int nitems = __popc(cm) * NW;
+  for (int J = lane; J < nitems; J += 32) {
+    const int r = rlist[J / NW], i = J % NW;
+    uint32_t m = rOO[r * NW + i];
+    if (!m) continue;
+    const uint32_t lvw = rLV[r * NW + i], fo = rFO[r * NW + i];
+    int k = (int)((pOO[r] >> (8 * i)) & 0xFFu);  // rank in the row's OO of the word's first vehicle
+    const int in0 = mIn[r], ent = mEnt[r];
+    const int of = mOut[r] + (int)((pFO[r] >> (8 * i)) & 0xFFu);
+    int ot = 0;
+    uint32_t fot = 0u;
+    if (lvw) {  // the target row of its leavers
+      const int r2 = r + dir;
+      fot = rFO[r2 * NW + i];
+      ot = mOut[r2] + (int)((pFO[r2] >> (8 * i)) & 0xFFu);
+    }
+    do {
+      const uint32_t bit = m & (0u - m), lowb = bit - 1u;
+      m ^= bit;
+      const uint32_t e = (k == 0 && ent != -1) ? (uint32_t)ent : (uint32_t)ibase[in0 + k];
+      k++;
+      const int dst = (lvw & bit) ? ot + __popc(fot & lowb) : of + __popc(fo & lowb);
+      obase[dst] = (int32_t)e;
+    } while (m);
   }
 }
 
@@ -1024,11 +1038,9 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
     const bool changed = moved_lc || injected;
     const bool ginj = inject && __any_sync(FULL, injected);
     const int32_t *scr = R.inj_scratch + (size_t)g * 32 * kRowMaxCells;
-    int itot;
-    const int ioff = warp_scan(changed ? popc_row(OO) : 0, lane, &itot);
-    if (staged && ostaged && !ginj && itot <= kCellTab) {  // shared-memory blocks (the common case)
-      vid_lists_tab(s_in, s_out, s_out + R.cap, OO, FO, LV, nfin, in_off, out_off, has_ent, ent_y,
-                    ent_e, changed, ioff, itot, dir, lane);
+    if (staged && ostaged && !ginj) {  // shared-memory blocks (the common case)
+      vid_lists_rw(s_in, s_out, s_out + R.cap, OO, FO, LV, nfin, in_off, out_off, has_ent, ent_y,
+                   ent_e, changed, dir, lane);
     } else {
       RowWords oo, fo, lv, inj;
 #pragma unroll
