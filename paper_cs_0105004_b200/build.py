@@ -39,5 +39,27 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return SO
 
 
+CHECKED_SO = os.path.join(os.path.dirname(HERE), "build", "checked", "libtsim.so")
+
+
+def build_checked(force: bool = False) -> str:
+    """The same sources with -DTS_CHECKED (invariant counters in the row
+    kernel, ts_debug_checks): a debug library for tests, never benchmarked."""
+    deps = [os.path.join(HERE, s) for s in SRCS] + [SO]
+    if (not force and os.path.exists(CHECKED_SO) and
+            all(os.path.getmtime(d) <= os.path.getmtime(CHECKED_SO) for d in deps if os.path.exists(d))):
+        return CHECKED_SO
+    os.makedirs(os.path.dirname(CHECKED_SO), exist_ok=True)
+    nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+    cmd = [nvcc] + NVCC_FLAGS + ["-DTS_CHECKED"] + \
+        [os.path.join(HERE, s) for s in SRCS] + ["-o", CHECKED_SO]
+    cmd = [c for i, c in enumerate(cmd) if not (c == "-Xptxas" and cmd[i + 1:i + 2] == ["-v"])
+           and not (c == "-v" and cmd[i - 1] == "-Xptxas")]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError("nvcc (checked) failed:\n" + r.stdout + r.stderr)
+    return CHECKED_SO
+
+
 if __name__ == "__main__":
     print(build(force=True, verbose=True))

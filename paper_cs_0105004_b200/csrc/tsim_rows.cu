@@ -32,6 +32,33 @@
 // rows whose vehicle set only lost its front or gained a back entrant are
 // plain (shifted) vector copies.
 #include "tsim_device.cuh"
+#include "../../include/tsim.h"
+
+// ---- checked build (-DTS_CHECKED; tests and tools only, never the bench):
+// invariants of the row kernel's state, counted per device instead of
+// asserted, read back by ts_debug_checks (include/tsim.h).  Bits:
+//   1  the group's vid-block count differs from its occupancy planes
+//   2  an input vehicle in a cell past its row end
+//   4  a lane-change arrival onto a cell its own row keeps (a cell
+//      written twice: "occupied by exactly one car")
+//   8  a final vehicle past its row end, 16 a final velocity above the
+//      link's vmax, 32 a group's output block larger
+//      than its cells, 64 a vid-list entry scattered to a cell of the
+//      final occupancy that is empty (a mis-ranked list), 128 the
+//      self-test (every group of every launch while armed)
+#ifdef TS_CHECKED
+__device__ unsigned int g_ts_chk[4] = {0u, 0xFFFFFFFFu, 0u, 0u};
+#define TS_CHK(cond, bit, grp)                          \
+  do {                                                  \
+    if (!(cond)) {                                      \
+      atomicOr(&g_ts_chk[0], (unsigned)(bit));          \
+      atomicMin(&g_ts_chk[1], (unsigned)(grp));         \
+      atomicAdd(&g_ts_chk[2], 1u);                      \
+    }                                                   \
+  } while (0)
+#else
+#define TS_CHK(cond, bit, grp) ((void)0)
+#endif
 
 namespace tsim {
 
@@ -387,6 +414,7 @@ __device__ __forceinline__ void vid_lists(const int32_t *ibase, int32_t *obase, 
       }
       const int dst = (rLV[r0 * NW + ci] & bit) ? r0 + dir : r0;
       const int rank = __popc(rFO[dst * NW + ci] & lowb) + (int)((pFO[dst] >> (8 * ci)) & 0xFF);
+      TS_CHK(rFO[dst * NW + ci] & bit, 64, 0xFFFFFFF0u);
       obase[mOutOff[dst] + rank] = (int32_t)e;
     }
   }
@@ -482,6 +510,7 @@ __device__ __forceinline__ void vid_lists_rw(const int32_t *ibase, int32_t *obas
       const uint32_t e = (k == 0 && ent != -1) ? (uint32_t)ent : (uint32_t)ibase[in0 + k];
       k++;
       const int dst = (lvw & bit) ? ot + __popc(fot & lowb) : of + __popc(fo & lowb);
+      TS_CHK(((lvw & bit) ? fot : fo) & bit, 64, 0xFFFFFFF0u);
       obase[dst] = (int32_t)e;
     } while (m);
   }
@@ -629,6 +658,11 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
     const int nin = popc_row(O);
     int tot_chk;
     const int in_off = warp_scan(nin, lane, &tot_chk);
+    TS_CHK(tot_chk == tot_in, 1, g);
+    TS_CHK(g_ts_chk[3] == 0u, 128, g);  // self-test armed by ts_debug_checks(out, 2)
+#ifdef TS_CHECKED
+    for (int i = 0; i < NW; i++) TS_CHK((O[i] & ~VAL[i]) == 0u, 2, g);
+#endif
     auto vid_wait = [&]() {
       if (tma_in) {
         mbar_wait(bar, bar_phase);
@@ -1021,6 +1055,16 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
         __stcs(pout + (3 * NW + i) * 32, FV2[i]);
         __stcs(pout + (4 * NW + i) * 32, fa0);
         __stcs(pout + (5 * NW + i) * 32, fa1);
+#ifdef TS_CHECKED
+        TS_CHK(((OO[i] & keep) & ar) == 0u, 4, g);
+        TS_CHK((FO[i] & ~VAL[i]) == 0u, 8, g);
+        for (uint32_t m = FO[i]; m; m &= m - 1u) {
+          const int x = __ffs(m) - 1;
+          const int v = (int)((FV0[i] >> x) & 1u) | (int)(((FV1[i] >> x) & 1u) << 1) |
+                        (int)(((FV2[i] >> x) & 1u) << 2);
+          TS_CHK(v <= vk, 16, g);
+        }
+#endif
       }
     }
 
@@ -1030,6 +1074,13 @@ __global__ void __launch_bounds__(TS_ROWS_TPB, TS_ROWS_MINB) k_rows(const StepPa
     int tot_out;
     const int out_off = warp_scan(nfin, lane, &tot_out);
     const bool ostaged = tot_out <= R.cap;
+#ifdef TS_CHECKED
+    {
+      int wsum;
+      (void)warp_scan(w, lane, &wsum);
+      TS_CHK(tot_out <= wsum, 32, g);
+    }
+#endif
     int32_t *obase = ostaged ? s_out : R.vid_out + voff;
     int32_t *vout = obase + out_off;
     const bool moved_lc = any_row(LV) || any_row(AR);
@@ -1186,3 +1237,28 @@ int occupancy_rows(int threads, int smem) {
 }
 
 }  // namespace tsim
+
+// Read (and optionally reset) the checked build's invariant counters of the
+// current device (include/tsim.h).
+extern "C" int ts_debug_checks(uint32_t *out, int32_t reset) {
+  if (!out) return TS_EINVAL;
+#ifdef TS_CHECKED
+  unsigned int v[4];
+  if (cudaMemcpyFromSymbol(v, g_ts_chk, sizeof v) != cudaSuccess) return TS_EINTERNAL;
+  out[0] = 1u;
+  out[1] = v[0];
+  out[2] = v[1];
+  out[3] = v[2];
+  if (reset) {  // 2: zero and arm the self-test, 1: zero and disarm
+    const unsigned int z[4] = {0u, 0xFFFFFFFFu, 0u, reset == 2 ? 1u : 0u};
+    if (cudaMemcpyToSymbol(g_ts_chk, z, sizeof z) != cudaSuccess) return TS_EINTERNAL;
+  }
+#else
+  (void)reset;
+  out[0] = 0u;
+  out[1] = 0u;
+  out[2] = 0xFFFFFFFFu;
+  out[3] = 0u;
+#endif
+  return TS_OK;
+}

@@ -59,6 +59,7 @@ def load_library():
         "ts_link_cells": (I32, [P, I32]),
         "ts_read_raw": (ctypes.c_int, [P, I32, P, P, P]),
         "ts_state_hash": (ctypes.c_int, [P, ctypes.POINTER(ctypes.c_uint64)]),
+        "ts_debug_checks": (ctypes.c_int, [P, I32]),
         "ts_read_history": (ctypes.c_int, [P, I32, I32, P, P, P, P, P, P]),
         "ts_get_totals": (ctypes.c_int, [P, P]),
         "ts_read_flow": (ctypes.c_int, [P, I32, I32, P]),
@@ -253,6 +254,16 @@ def parse_plans_text(text, link_id):
                             off.ctypes.data, route.ctypes.data, dep.ctypes.data, ent.ctypes.data,
                             vid.ctypes.data, err)
     return off, route[:ne.value], dep, ent, vid
+
+
+def debug_checks(reset=True, arm_selftest=False):
+    """ts_debug_checks: (checked_build, violated_bits, first_group, count)."""
+    lib = load_library()
+    out = (ctypes.c_uint32 * 4)()
+    mode = 2 if arm_selftest else (1 if reset else 0)
+    if lib.ts_debug_checks(ctypes.cast(out, ctypes.c_void_p), mode) != 0:
+        raise TsError("ts_debug_checks failed")
+    return tuple(int(x) for x in out)
 
 
 def nccl_unique_id():

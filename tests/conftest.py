@@ -20,3 +20,20 @@ def cuda_available():
         return torch.cuda.is_available()
     except Exception:
         return False
+
+
+@pytest.fixture(autouse=True)
+def _checked_build_invariants():
+    """Under TSIM_EXPECT_CHECKED=1 (tests/test_gpu_checked.py runs GPU tests
+    against the -DTS_CHECKED library): after every test, the row kernel's
+    invariant counters must be clean (ts_debug_checks, include/tsim.h)."""
+    if os.environ.get("TSIM_EXPECT_CHECKED") != "1":
+        yield
+        return
+    import paper_cs_0105004_b200 as tsim
+    tsim.debug_checks(reset=True)
+    yield
+    checked, bits, first_group, count = tsim.debug_checks(reset=True)
+    assert checked == 1, "TSIM_EXPECT_CHECKED=1 but the loaded library is not a checked build"
+    assert count == 0, (f"row-kernel invariants violated: bits {bits:#x}, "
+                        f"first group {first_group}, {count} violations")

@@ -77,3 +77,12 @@ def test_null_handles_are_rejected():
     assert lib.ts_step(None, 1) == 2
     assert lib.ts_init(None, 0) == 2
     assert lib.ts_nccl_unique_id(None) == 2
+
+
+def test_debug_checks_on_the_product_library():
+    """ts_debug_checks on the benchmarked (unchecked) library: no CUDA call,
+    reports 'not a checked build' with clean counters (include/tsim.h)."""
+    import paper_cs_0105004_b200 as tsim
+    if os.environ.get("TSIM_LIB"):
+        pytest.skip("TSIM_LIB selects another build")
+    assert tsim.debug_checks(reset=False) == (0, 0, 0xFFFFFFFF, 0)
