@@ -266,12 +266,15 @@ int ts_read_raw(ts_sim *h, int32_t link, uint8_t *code_out, int32_t *vid_out,
 /* Debug build check (race / bounds detection without a sanitizer): a
  * library compiled with -DTS_CHECKED (paper_cs_0105004_b200/build.py
  * build_checked, never the benchmarked library) counts, per device, every
- * violation of the row kernel's state invariants -- one vehicle per cell
- * (PAPER.md:324), v <= vmax, vid lists consistent with
- * the occupancy planes and ranked onto occupied cells, nothing past a row
- * end.  out[0] = 1 for a checked build (0 otherwise: out[1..3] = 0,
+ * violation of the row and node kernels' state invariants -- one vehicle
+ * per cell, v <= vmax, vid lists
+ * consistent with the occupancy planes and ranked onto occupied cells,
+ * nothing past a row end, a node crosser landing before the first occupied
+ * cell of its target lane and only with a next link on its route.
+ * out[0] = 1 for a checked build (0 otherwise: out[1..3] = 0,
  * 0xFFFFFFFF, 0), out[1] = OR of the violated invariants' bits
- * (csrc/tsim_rows.cu), out[2] = the smallest row group that violated one,
+ * (csrc/tsim_rows.cu, csrc/tsim_kernels.cu), out[2] = the smallest row
+ * group that violated a row-kernel one (0xFFFFFFFF if none),
  * out[3] = the number of violations.  reset != 0 zeroes the counters after
  * reading; reset = 2 also arms a self-test (every row group of every later
  * launch counts bit 128 until the next reset = 1) so a test can prove the

@@ -19,6 +19,25 @@
 //   k_node       one thread per node (fallback for > 32 incoming lanes)
 #include "tsim_device.cuh"
 
+// checked build (-DTS_CHECKED): invariants of a node crossing (H3/H5),
+// counted per device and read by ts_debug_checks (csrc/tsim_rows.cu).
+// Bits: 256 a crosser landing on or past the first occupied cell of its
+// target lane, 512 a crossing velocity above the link's
+// vmax, 1024 a crossing by a vehicle with no next link
+// on its route
+#ifdef TS_CHECKED
+__device__ unsigned int g_ts_chk_node[2] = {0u, 0u};  // bits, count
+#define TS_CHK_NODE(cond, bit)                        \
+  do {                                                \
+    if (!(cond)) {                                    \
+      atomicOr(&g_ts_chk_node[0], (unsigned)(bit));   \
+      atomicAdd(&g_ts_chk_node[1], 1u);               \
+    }                                                 \
+  } while (0)
+#else
+#define TS_CHK_NODE(cond, bit) ((void)0)
+#endif
+
 namespace tsim {
 
 // ====================================================================
@@ -513,9 +532,12 @@ __device__ __forceinline__ int node_grant(const NodeParams &P, const Cand &c, in
   const int v3 = nasch_v3(c.v, vk, min(kGmax, c.d + E), (uint32_t)P.t, (uint32_t)c.vid, P.k0,
                           P.k1, P.p32);
   if (v3 > c.d) {
+    TS_CHK_NODE(v3 - c.d - 1 < E, 256);
+    TS_CHK_NODE(v3 <= vk, 512);
     int nslot = 0;  // pass-through node of a ring: straight on, same route position
     if (!pass) {
       const VehPos q = P.vpos[c.vid];
+      TS_CHK_NODE(q.p + 1 < q.e, 1024);
       nslot = (q.p + 2 < q.e) ? (int)P.rslot[q.p + 2] : kSlotFinal;
       P.vpos[c.vid].p = q.p + 1;
     }
@@ -800,6 +822,22 @@ int occupancy_blocks(int threads, int smem) {
   int nb = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_step, threads, smem);
   return nb;
+}
+
+// the node checks' counters (bits, count) of the current device; reset
+// zeroes them.  0, or -1 on a CUDA error; zeros in an unchecked build
+int node_checks(unsigned int *v, int reset) {
+#ifdef TS_CHECKED
+  if (cudaMemcpyFromSymbol(v, g_ts_chk_node, 2 * sizeof(unsigned int)) != cudaSuccess) return -1;
+  if (reset) {
+    const unsigned int z[2] = {0u, 0u};
+    if (cudaMemcpyToSymbol(g_ts_chk_node, z, sizeof z) != cudaSuccess) return -1;
+  }
+#else
+  (void)reset;
+  v[0] = v[1] = 0u;
+#endif
+  return 0;
 }
 
 }  // namespace tsim

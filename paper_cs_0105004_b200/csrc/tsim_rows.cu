@@ -1238,17 +1238,22 @@ int occupancy_rows(int threads, int smem) {
 
 }  // namespace tsim
 
+namespace tsim {
+int node_checks(unsigned int *v, int reset);  // csrc/tsim_kernels.cu
+}
+
 // Read (and optionally reset) the checked build's invariant counters of the
-// current device (include/tsim.h).
+// current device (include/tsim.h): the row kernel's and the node kernels'.
 extern "C" int ts_debug_checks(uint32_t *out, int32_t reset) {
   if (!out) return TS_EINVAL;
 #ifdef TS_CHECKED
-  unsigned int v[4];
+  unsigned int v[4], vn[2];
   if (cudaMemcpyFromSymbol(v, g_ts_chk, sizeof v) != cudaSuccess) return TS_EINTERNAL;
+  if (tsim::node_checks(vn, reset != 0) != 0) return TS_EINTERNAL;
   out[0] = 1u;
-  out[1] = v[0];
+  out[1] = v[0] | vn[0];
   out[2] = v[1];
-  out[3] = v[2];
+  out[3] = v[2] + vn[1];
   if (reset) {  // 2: zero and arm the self-test, 1: zero and disarm
     const unsigned int z[4] = {0u, 0xFFFFFFFFu, 0u, reset == 2 ? 1u : 0u};
     if (cudaMemcpyToSymbol(g_ts_chk, z, sizeof z) != cudaSuccess) return TS_EINTERNAL;
