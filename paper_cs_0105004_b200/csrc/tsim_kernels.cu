@@ -19,12 +19,13 @@
 //   k_node       one thread per node (fallback for > 32 incoming lanes)
 #include "tsim_device.cuh"
 
-// checked build (-DTS_CHECKED): invariants of a node crossing (H3/H5),
-// counted per device and read by ts_debug_checks (csrc/tsim_rows.cu).
-// Bits: 256 a crosser landing on or past the first occupied cell of its
-// target lane, 512 a crossing velocity above the link's
-// vmax, 1024 a crossing by a vehicle with no next link
-// on its route
+// checked build (-DTS_CHECKED): invariants of a node crossing (H3/H5) and
+// of the general tiles' output state, counted per device and read by
+// ts_debug_checks (csrc/tsim_rows.cu).  Bits: 256 a crosser landing on or
+// past the first occupied cell of its target lane, 512 a
+// crossing velocity above the link's vmax, 1024 a
+// crossing by a vehicle with no next link on its route, 2048 an occupied
+// tile cell without a vehicle id, 4096 a tile vehicle above its link's vmax
 #ifdef TS_CHECKED
 __device__ unsigned int g_ts_chk_node[2] = {0u, 0u};  // bits, count
 #define TS_CHK_NODE(cond, bit)                        \
@@ -229,6 +230,8 @@ __device__ void write_back(const StepParams &P, TileCtx &T, bool node_recs, int 
   const int n = enumerate(T, T.bout, T.vpos, lane);
   for (int r = lane; r < n; r += 32) {
     const int q = T.vpos[r];
+    TS_CHK_NODE(T.vout[q] >= 0, 2048);
+    TS_CHK_NODE((int)(T.cout[q] & 7u) <= (int)P.vmax_link[T.d.link], 4096);
     P.vid_out[vid_index(T, q, r)] = T.vout[q];
   }
   if (T.d.strip >= 0) {

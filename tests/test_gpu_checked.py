@@ -3,7 +3,10 @@ available on the GPU pool): GPU parity and full-size invariant tests run
 again against the -DTS_CHECKED build of the same sources, whose row kernel
 counts every violation of its state invariants (one vehicle per cell,
 PAPER.md:324; v <= vmax; vid lists consistent with the
-occupancy planes and ranked onto occupied cells; nothing past a row end).
+occupancy planes and ranked onto occupied cells; nothing past a row end)
+and whose node and general-tile kernels count theirs (a crosser lands
+before the first occupied cell of its target lane; tile vehicles carry an
+id and v <= vmax).
 After every test the counters must be zero (tests/conftest.py), and the
 results must still equal the oracle's."""
 import os
@@ -25,6 +28,8 @@ CASES = [
     "tests/test_gpu_parity.py::test_portland_small",
     "tests/test_gpu_parity.py::test_signalized_grid",
     "tests/test_gpu_domains.py::test_dense_grid_lane_changes",
+    "tests/test_gpu_parity.py::test_config1_full",  # incl. every tile on the general kernels
+    "tests/test_gpu_domains.py::test_config1_orb",  # split links: general tiles + strips
     "tests/test_gpu_configs.py::test_config4a_bench_routes_driver_window",
     "tests/test_gpu_configs.py::test_config4b_prefix",
     "tests/test_gpu_validation.py::test_full_size_grid_invariants_long_run",
